@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""Benchmark of the TILES tile-wise Reslim forward (ORBIT-2) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+One step = one pass of the whole hot path (gather -> embed -> L blocks ->
+head -> stitch + bilinear residual) over one batch of synthetic ERA5-shaped
+input (BASELINE.json configs[1] = C2 at N=1, B = 64 samples).  Multi-GPU
+(torchrun, one process per GPU): every rank runs its own batch of the same
+workload (weak scaling; units = (sample, tile) pairs sharded by sample, no
+data-path collective).  Timing: CUDA events on the
+launching stream, barrier + synchronize on both sides, max over ranks.
+
+Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every key.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "high-res pixels/s & tiled-attn TFLOP/s (% bf16 peak) at 1/2/4/8 B200"
+UNIT = "high-res px/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-profile", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            j = json.load(f)
+        return {"hbm": j["hbm_gbs"], "bf16": j["bf16_tflops"], "bf16_sus": j["bf16_tflops_sustained"],
+                "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.path)
+        load = [s for s in sm if smax and s > 0.3 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def dist_init(n_gpus):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(world, v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per kernel class
+# ---------------------------------------------------------------------------
+def class_work(w, info, B):
+    """Per kernel class: (bound, total algorithmic work per step) with FLOPs
+    for contractions and bytes for HBM-bound kernels."""
+    D, L, Din, Nh, V, K = w.embed, w.depth, w.din, w.head_out, w.V, w.K
+    npad, ncore = info.tokens_per_sample, info.core_tokens_per_sample
+    n2, nc = info.sum_n2_per_sample, info.sum_nc_per_sample
+    sH, sW = w.scale * w.H, w.scale * w.W
+    last = 1 if L >= 1 else 0
+    f = {
+        "embed_gemm": 2.0 * npad * Din * D,
+        "qkv_gemm": (L - last) * 6.0 * npad * D * D + last * (4.0 * npad * D * D + 2.0 * ncore * D * D),
+        "tile_attention": (L - last) * 4.0 * D * n2 + last * 4.0 * D * nc,
+        "oproj_gemm": (L - last) * 2.0 * npad * D * D + last * 2.0 * ncore * D * D,
+        "mlp_up_gemm": (L - last) * 8.0 * npad * D * D + last * 8.0 * ncore * D * D,
+        "mlp_down_gemm": (L - last) * 8.0 * npad * D * D + last * 8.0 * ncore * D * D,
+        "head_gemm": 2.0 * ncore * D * Nh,
+    }
+    out = {k: ("tensor", v * B) for k, v in f.items()}
+    # HBM kernels: unique algorithmic bytes
+    out["tile_gather"] = ("hbm", B * (4.0 * V * w.H * w.W + 2.0 * npad * Din))
+    out["stitch_residual"] = ("hbm", B * (2.0 * K * sH * sW + 4.0 * K * w.H * w.W + 4.0 * K * sH * sW))
+    # layernorm: (2L+1) launches, fp32 read + bf16 write of D per row
+    out["layernorm"] = ("hbm", B * (2 * L * npad * D * 6.0 + ncore * D * 6.0))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the oracle as the CPU baseline / reference arm
+# ---------------------------------------------------------------------------
+def oracle_units(w, blob, x, seconds_budget=None, n_units=None):
+    """Run the oracle over (sample, tile) units; returns (units, high-res px, seconds, threads)."""
+    from oracle import reslim_tiles as O
+    pr = O.Problem.from_config(w)
+    tiles = pr.tiles()
+    Wt = pr.weights(blob)
+    px = 0
+    done = 0
+    t0 = time.perf_counter()
+    i = 0
+    while True:
+        b, t = divmod(i % (x.shape[0] * len(tiles)), len(tiles))
+        tile = tiles[t]
+        g = O.tile_forward(x[b], tile, pr, Wt)
+        up = O.residual_up(x[b], pr)   # residual for the sample (the oracle's plain step O7)
+        _ = g.sum() + up.sum()
+        px += tile.n_core * pr.P * pr.P
+        done += 1
+        i += 1
+        el = time.perf_counter() - t0
+        if n_units is not None and done >= n_units:
+            break
+        if seconds_budget is not None and el >= seconds_budget:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([p.get("num_threads", 1) for p in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return done, px, time.perf_counter() - t0, threads
+
+
+def run_reference(args, w, world, rank):
+    """--impl reference: the fp64 oracle as it stands, on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from workloads import make_input, make_weights
+    x = make_input(w, batch=1)
+    blob = make_weights(w)
+    for _ in range(args.warmup):
+        oracle_units(w, blob, x, n_units=1)
+    times, pxs = [], []
+    for s in range(args.steps):
+        _, px, dt, threads = oracle_units(w, blob, x, n_units=1)
+        times.append(dt)
+        pxs.append(px)
+    total_t = sum(times)
+    value = sum(pxs) / total_t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total_t / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (ERA5-shaped, seeded)",
+        "config": {"workload": w.name, "batch": 1, "step": "one (sample, tile) unit of the workload"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": f"1 (sample, tile) unit of {w.name} per step (fp64 numpy oracle)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args, w, world, rank, local):
+    import numpy as np
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from workloads import make_input, make_weights
+
+    B = w.batch
+    cfg = o2.config_from(w, batch=B, precision=o2.BF16)
+    ctx = o2.Context(cfg)
+    info = ctx.info
+    blob = make_weights(w)
+    x_host = make_input(w, batch=B, seed=1000 + 97 * rank + int(w.name[1]))
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    x_dev = x_pin.to("cuda")
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
+    out_pin = torch.empty(out.shape, dtype=torch.float32).pin_memory()
+    tile_out = ctx.tile_out_buffer()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ctx.forward(packed, x_dev, out=out, tile_out=tile_out, stream=stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier(world)
+
+    # ---- device-resident timed region ----
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier(world)
+    ms = ev0.elapsed_time(ev1) / args.steps
+    launches = (ctx.launch_count() - l0) // args.steps
+    ms = max_over_ranks(world, ms)
+    clocks = clk.summary()
+
+    # ---- end-to-end through the public API with host buffers ----
+    h2d = x_pin.numel() * 4
+    d2h = out.numel() * 4
+
+    def e2e_step():
+        x_dev.copy_(x_pin, non_blocking=True)
+        step()
+        out_pin.copy_(out, non_blocking=True)
+
+    e2e_step()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(2, args.steps // 2)
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier(world)
+    e2e_ms = max_over_ranks(world, e0.elapsed_time(e1) / e_steps)
+
+    # ---- per-kernel-class times (separate profiled pass, CUDA events per launch) ----
+    prof = {}
+    if not args.no_profile:
+        ctx.set_profiling(True)
+        for _ in range(max(2, min(args.steps, 5))):
+            step()
+        torch.cuda.synchronize()
+        prof = ctx.kernel_times()
+        ctx.set_profiling(False)
+
+    px_per_step = world * B * w.scale * w.H * w.scale * w.W
+    value = px_per_step / (ms * 1e-3)
+    flops_step = world * B * info.flops_per_sample
+    pk = peaks()
+    res = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields, random-init weights)",
+        "config": {"workload": w.name, "batch_per_gpu": B, "coarse": [w.H, w.W, w.V], "out": [w.scale * w.H,
+                   w.scale * w.W, w.K], "tiles": [w.tiles_y, w.tiles_x], "halo": w.halo,
+                   "vit": [w.embed, w.depth, w.heads], "parallelism": f"dp{world} (samples sharded, tiles local)",
+                   "l2": "working set > L2 (126 MB) every step; no flush needed"},
+        "tokens_per_s": world * B * info.tokens_per_sample / (ms * 1e-3),
+        "core_tokens_per_s": world * B * info.core_tokens_per_sample / (ms * 1e-3),
+        "path_tflops": flops_step / (ms * 1e-3) / 1e12,
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": {"value": px_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+    }
+    if prof:
+        work = class_work(w, info, B)
+        total_ms = sum(v[1] for v in prof.values())
+        classes = {}
+        for name, (n, t) in prof.items():
+            steps_prof = max(2, min(args.steps, 5))
+            per_step_ms = t / steps_prof
+            launches_per_step = n / steps_prof
+            entry = {"share": t / total_ms, "ms_per_step": per_step_ms, "launches_per_step": launches_per_step}
+            if name in work:
+                bound, amount = work[name]
+                if bound == "tensor":
+                    entry["tflops"] = amount / (per_step_ms * 1e-3) / 1e12
+                else:
+                    entry["gbs"] = amount / (per_step_ms * 1e-3) / 1e9
+            classes[name] = entry
+        res["kernels"] = classes
+        dom = max((k for k in classes if k in work), key=lambda k: classes[k]["share"])
+        bound, amount = work[dom]
+        launches_dom = classes[dom]["launches_per_step"]
+        per_launch_ms = classes[dom]["ms_per_step"] / launches_dom
+        if bound == "tensor":
+            achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e12
+            peak = pk["bf16_sus"]
+            res["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
+                               "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                               "peak_src": pk["src"] + " bf16_tflops_sustained (kernel timed inside the step)",
+                               "frac_of_burst": achieved / pk["bf16"]}
+        else:
+            achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e9
+            res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm"],
+                               "unit": "GB/s", "frac": achieved / pk["hbm"], "traffic": None, "peak_src": pk["src"]}
+        att = classes.get("tile_attention")
+        if att and "tflops" in att:
+            res["attn_tflops"] = att["tflops"]
+            res["attn_frac_bf16_peak"] = att["tflops"] / pk["bf16_sus"]
+        gemm_ms = sum(classes[k]["ms_per_step"] for k in classes if k.endswith("_gemm"))
+        gemm_f = sum(work[k][1] for k in work if k.endswith("_gemm"))
+        res["gemm_tflops"] = gemm_f / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
+        tc_ms = gemm_ms + (att["ms_per_step"] if att else 0)
+        tc_f = gemm_f + work["tile_attention"][1]
+        res["attn_gemm_frac_bf16_peak"] = tc_f / (tc_ms * 1e-3) / 1e12 / pk["bf16_sus"] if tc_ms else None
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        xs = x_host[:1]
+        done, px, dt, threads = oracle_units(w, blob, xs, seconds_budget=15.0)
+        res["cpu_baseline"] = {"value": px / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
+                               "sample": f"{done} (sample, tile) units of {w.name} sample 0 in {dt:.1f} s "
+                                         f"(fp64 numpy oracle, as it stands)"}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
+def main():
+    args = parse()
+    from workloads import get_config
+    w = get_config(args.config)
+    if args.batch:
+        w = w.replace(batch=args.batch)
+    if args.impl == "reference":
+        rank = int(os.environ.get("RANK", "0"))
+        run_reference(args, w, int(os.environ.get("WORLD_SIZE", "1")), rank)
+        return
+    world, rank, local = dist_init(args.gpus)
+    try:
+        run_ours(args, w, world, rank, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

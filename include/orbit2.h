@@ -1,0 +1,218 @@
+/*
+ * orbit2.h -- C ABI of liborbit2.so: the TILES tile-wise, sequence-scaled
+ * forward pass of the ORBIT-2 Reslim ViT (arXiv 2505.04802) on B200 (sm_100a).
+ *
+ * Citations: P:n = PAPER.md line n.  Readings R# = DESIGN.md "Readings".
+ *
+ * The pass (north star; P:475-498 Reslim, P:511-532 TILES):
+ *   (1) split the coarse multi-variable grid into tiles with halo overlap
+ *       ("partitions both inputs and downscaled outputs into spatial
+ *       tiles"; "each tile is extended with a fixed-width halo");
+ *   (2) patch-embed each tile (p = 2);
+ *   (3) per-tile multi-head self-attention + MLP blocks (P:527
+ *       "self-attention is restricted within each tile");
+ *   (4) crop the halos and stitch the tiles into the high-resolution field
+ *       ("the halo regions are discarded, and the non-padded tile
+ *       outputs are stitched together");
+ *   (5) add the residual interpolated upsample of the input.
+ *
+ * Graded boundary: orbit2_tiles_plan (1, host), orbit2_reslim_forward (1-3 +
+ * linear head), orbit2_stitch (4-5).  The rest is lifecycle support.
+ *
+ * Conventions for every call
+ *   - Returns orbit2_status; never throws, never aborts, never exits.  On
+ *     error, orbit2_last_error() returns a thread-local message naming the
+ *     offending field; it stays valid until the next call on that thread.
+ *   - Memory: the CALLER allocates and owns every buffer (device buffers are
+ *     plain device pointers from cudaMalloc / torch).  The library never
+ *     allocates device memory after orbit2_create and never frees caller
+ *     memory.  A ctx borrows its workspace until orbit2_destroy.
+ *   - Streams: all device work is enqueued on the caller's stream; nothing
+ *     synchronises the host except orbit2_create (one-time table upload).
+ *     Asynchronous device faults surface at the caller's next synchronisation
+ *     (set ORBIT2_SYNC_CHECK=1 to synchronise and check after every call).
+ *   - One ctx per host thread / stream at a time.  Distinct ctxs are independent.
+ *   - Every device pointer must be 16-byte aligned (TMA / vector access).
+ */
+#ifndef ORBIT2_H_
+#define ORBIT2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORBIT2_ABI_VERSION 1
+
+typedef enum {
+  ORBIT2_OK = 0,
+  ORBIT2_E_INVALID = -1,      /* bad argument or configuration (message names the field) */
+  ORBIT2_E_CAPACITY = -2,     /* caller buffer / workspace too small (info still filled) */
+  ORBIT2_E_UNSUPPORTED = -3,  /* valid but not implemented (e.g. head_dim not in {32,64,128}) */
+  ORBIT2_E_CUDA = -4,         /* CUDA runtime / launch error */
+  ORBIT2_E_NCCL = -5,         /* reserved (collectives are issued by the caller in ABI v1) */
+  ORBIT2_E_STATE = -6         /* call made on a ctx in the wrong state */
+} orbit2_status;
+
+enum { ORBIT2_HALO_CLAMP = 0, ORBIT2_HALO_REPLICATE = 1 };   /* R4 */
+enum { ORBIT2_BF16 = 0, ORBIT2_FP32 = 1 };                   /* arithmetic of the path */
+
+/*
+ * Problem statement (north star: "a coarse grid of V variables, a downscale
+ * factor, tile size, halo width and ViT width/depth/heads"; P:404 sizes).
+ * All extents are in coarse PIXELS except tiles_* (counts) and halo (PATCHES, R3).
+ */
+typedef struct {
+  int32_t abi_version;     /* must be ORBIT2_ABI_VERSION */
+  int32_t batch;           /* B >= 1 samples per call */
+  int32_t H, W;            /* coarse grid; patch | H, patch | W */
+  int32_t V;               /* input variables */
+  int32_t K;               /* output variables (1 <= K; K <= V unless out_channel_map) */
+  int32_t scale;           /* downscale factor s >= 1 */
+  int32_t patch;           /* patch size p (pixels), 1 <= p */
+  int32_t tiles_y, tiles_x;/* tile grid; 1 <= tiles_y <= H/p, 1 <= tiles_x <= W/p */
+  int32_t halo;            /* halo width in patches, >= 0 */
+  int32_t halo_mode;       /* ORBIT2_HALO_CLAMP (default reading R4) or _REPLICATE */
+  int32_t embed;           /* D; D % heads == 0, D % 4 == 0, D % 64 == 0 for BF16 */
+  int32_t depth;           /* L >= 0 transformer blocks */
+  int32_t heads;           /* head_dim = D/heads must be 32, 64 or 128 */
+  int32_t mlp_hidden;      /* must be 4*D (R9) */
+  int32_t precision;       /* ORBIT2_BF16 or ORBIT2_FP32 */
+  int32_t world_size;      /* ranks the tiles are partitioned over (>= 1) */
+  int32_t rank;            /* 0 <= rank < world_size */
+  int32_t chunk_tiles;     /* max rank-local tiles per forward/stitch call; 0 = all */
+  const int32_t *out_channel_map; /* K entries in [0,V) selecting the residual input
+                                     channel of each output variable (R13); NULL = identity */
+} orbit2_config;
+
+/* One tile of the plan (R5 uneven split, R6 row-major ids).  Rectangles are
+ * half-open, in PATCH units of the coarse patch grid [0,H/p) x [0,W/p). */
+typedef struct {
+  int32_t tile_id, tile_y, tile_x;  /* tile_id = tile_y * tiles_x + tile_x */
+  int32_t owner_rank;               /* rank that computes this tile */
+  int32_t local_index;              /* position in owner's rank-local list */
+  int32_t core_y0, core_y1, core_x0, core_x1;
+  int32_t pad_y0, pad_y1, pad_x0, pad_x1;   /* core +- halo; clipped to the grid
+                                               in CLAMP mode, not in REPLICATE */
+  int32_t n_tokens;                 /* (pad_y1-pad_y0)*(pad_x1-pad_x0) */
+  int32_t n_core_tokens;            /* (core_y1-core_y0)*(core_x1-core_x0) */
+  int64_t token_offset;             /* offset in one sample's packed list of ALL tiles */
+  int64_t core_token_offset;        /* offset in one sample's list of ALL core tokens */
+} orbit2_tile;
+
+typedef struct {
+  int32_t n_tiles;                  /* tiles_y * tiles_x */
+  int32_t n_local_tiles;            /* tiles owned by cfg->rank */
+  int32_t chunk_tiles;              /* effective max tiles per call */
+  int32_t head_dim;
+  int64_t tokens_per_sample;        /* sum of n_tokens over all tiles (N_pad) */
+  int64_t core_tokens_per_sample;   /* (H/p)*(W/p) */
+  int64_t local_tokens;             /* per sample, rank-local tiles */
+  int64_t local_core_tokens;        /* per sample, rank-local tiles */
+  int64_t max_chunk_tokens;         /* per sample, max over windows of chunk_tiles local tiles */
+  int64_t max_chunk_core_tokens;
+  int64_t sum_n2_per_sample;        /* sum_t n_t^2 (attention cost, P:527 O(N^2/T)) */
+  int64_t sum_nc_per_sample;        /* sum_t n_t * c_t */
+  int64_t workspace_bytes;          /* device workspace needed by orbit2_create */
+  int64_t canonical_weight_count;   /* fp32 values in the canonical blob */
+  int64_t packed_weight_bytes;      /* device bytes of the packed weights */
+  int64_t tile_out_bytes;           /* bytes of tile_out for a full chunk (all B samples) */
+  int64_t out_bytes;                /* bytes of out: B*K*(sH)*(sW)*4 */
+  double flops_per_sample;          /* algorithmic FLOPs over ALL tiles */
+  double local_flops_per_sample;    /* same, rank-local tiles */
+  double gather_bytes_per_sample;
+  double stitch_bytes_per_sample;
+} orbit2_plan_info;
+
+/*
+ * orbit2_tiles_plan -- step (1) planning.  Host-only, pure, deterministic; no
+ * CUDA calls.  Two-call sizing: tiles = NULL, capacity = 0 fills *info only.
+ * If capacity < n_tiles returns ORBIT2_E_CAPACITY with *info filled.
+ * Tiles are written in tile_id order.  Ownership: tiles are assigned to ranks
+ * by longest-processing-time on the per-tile cost model;
+ * rank-local order = increasing tile_id among the rank's tiles.
+ * Errors (E_INVALID): p does not divide H or W; tiles_* outside [1, extent/p];
+ * halo < 0; embed % heads; embed % 4; mlp_hidden != 4*embed; scale < 1;
+ * K < 1; K > V without map; map entry outside [0,V); batch < 1; bad rank.
+ * E_UNSUPPORTED: head_dim not in {32,64,128}; BF16 with embed % 64 != 0.
+ */
+orbit2_status orbit2_tiles_plan(const orbit2_config *cfg, orbit2_tile *tiles,
+                                int32_t capacity, orbit2_plan_info *info);
+
+/*
+ * orbit2_create -- bind a config to a caller-owned device workspace of at
+ * least info.workspace_bytes (from orbit2_tiles_plan).  Uploads the plan
+ * tables into the workspace (synchronous, one time).  *ctx receives an
+ * opaque handle released by orbit2_destroy.  Uses the current CUDA device.
+ */
+orbit2_status orbit2_create(const orbit2_config *cfg, void *workspace_dev, size_t workspace_bytes,
+                            void **ctx);
+
+/*
+ * orbit2_prepare_weights -- convert the canonical fp32 weight blob
+ * (canonical_dev, info.canonical_weight_count floats, device memory) into the
+ * packed layout the kernels read (packed_dev, info.packed_weight_bytes).
+ *
+ * Canonical blob (fp32, little endian; PyTorch Linear convention y = W x + b,
+ * W stored [out][in] row-major), in this order:
+ *   W_e[D][V*p*p] (column (v*p+dy)*p+dx), b_e[D], e_s[D]  (resolution embedding, R8)
+ *   per layer l = 0..L-1:
+ *     ln1_g[D] ln1_b[D] W_qkv[3D][D] (rows Q|K|V; head h = rows [h*d,(h+1)*d) of each)
+ *     b_qkv[3D] W_o[D][D] b_o[D] ln2_g[D] ln2_b[D] W_1[4D][D] b_1[4D] W_2[D][4D] b_2[D]
+ *   lnf_g[D] lnf_b[D] W_h[K*P*P][D] (row (k*P+a)*P+b, P = s*p) b_h[K*P*P]
+ * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2, Din = V*p*p.
+ * Stream-ordered; canonical_dev may be freed once the stream passes this call.
+ */
+orbit2_status orbit2_prepare_weights(void *ctx, const float *canonical_dev, void *packed_dev,
+                                     void *stream /* cudaStream_t */);
+
+/*
+ * orbit2_reslim_forward -- steps (1)-(3) and the linear decoder head for the
+ * rank-local tiles [tile_begin, tile_begin + tile_count) of all B samples.
+ *   input_dev : fp32 [B][V][H][W], full-field shaped, row 0 = north.  Read only.
+ *               Must hold valid pixels at least inside the padded rects of
+ *               the requested tiles.
+ *   tile_out_dev : [B][core tokens of the requested tiles, plan order][K*P*P],
+ *               bf16 (BF16 path) or fp32 (FP32 path).  Column (k*P+a)*P+b is
+ *               output pixel (P*u+a, P*w+b) of variable k for core token (u,w).
+ *               Halo tokens produce no output (R16).
+ * tile_count <= info.chunk_tiles.  Stream-ordered.
+ */
+orbit2_status orbit2_reslim_forward(void *ctx, const void *packed_w, const float *input_dev,
+                                    int32_t tile_begin, int32_t tile_count, void *tile_out_dev,
+                                    void *stream);
+
+/*
+ * orbit2_stitch -- steps (4)-(5) for the same tile range: crop (halo outputs
+ * were never formed), place the core outputs of tile_out_dev (layout above)
+ * into out_dev fp32 [B][K][s*H][s*W], and add the bilinear (align_corners =
+ * False, edge clamp; R12) x`s upsample of input channel out_channel_map[k].
+ * Writes exactly the output pixels of the requested tiles' cores; other
+ * pixels of out_dev are untouched.  Stream-ordered.
+ */
+orbit2_status orbit2_stitch(void *ctx, const void *tile_out_dev, const float *input_dev,
+                            int32_t tile_begin, int32_t tile_count, float *out_dev, void *stream);
+
+/* Number of kernels the library launched on this ctx so far. */
+int64_t orbit2_launch_count(void *ctx);
+
+/*
+ * Per-kernel-class timing with CUDA events on the call's stream.  When
+ * enabled, every launch is bracketed by events; orbit2_kernel_times() then
+ * synchronises the last event and returns, for up to `cap` classes, the name,
+ * the number of launches and the summed device milliseconds since the last
+ * reset.  Returns the number of classes.  Not for timed throughput runs.
+ */
+orbit2_status orbit2_set_profiling(void *ctx, int32_t enable);
+int32_t orbit2_kernel_times(void *ctx, const char **names, int64_t *launches, double *ms,
+                            int32_t cap);
+
+const char *orbit2_last_error(void);
+void orbit2_destroy(void *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ORBIT2_H_ */

@@ -1,0 +1,270 @@
+// gemm_tc.cu -- bf16 GEMM on 5th-generation tensor cores (tcgen05) for the
+// dense contractions of the Reslim forward (patch embed, QKV, O-projection,
+// MLP up/down, decoder head):
+//     C[M,N] = A[M,K] . W[N,K]^T    (W = PyTorch Linear weight [out][in])
+// with the epilogue fused: bias, exact-erf GELU (R9), fp32 residual add, or
+// the embedding epilogue (bias + resolution embedding + sincos position, R7/R8).
+//
+// Structure (one 128 x BN output tile per CTA, warp-specialised):
+//   warp 0 lane 0 : TMA producer, STAGES-deep smem ring (SWIZZLE_128B, BK = 64)
+//   warp 1 lane 0 : tcgen05.mma issuer (M=128, N=BN, K=16 per instruction),
+//                   accumulator in TMEM (BN fp32 columns)
+//   warp 2        : TMEM allocator
+//   warps 4-7     : epilogue, tcgen05.ld 32x32b -> registers -> fused op -> global
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace orbit2 {
+
+// ---------------------------------------------------------------------------
+// TMA descriptor encoding through the driver entry point (no -lcuda)
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::once_flag g_encode_once;
+
+static void load_encode() {
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+      q == cudaDriverEntryPointSuccess)
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+}
+
+bool tma_available() {
+  std::call_once(g_encode_once, load_encode);
+  return g_encode != nullptr;
+}
+
+// 2-D bf16 row-major tensor [rows][ld] (cols used = cols), box [box_rows][box_cols]
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                    int box_cols, CUtensorMapSwizzle swz) {
+  if (!tma_available()) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+template <int EPI, bool OUT_BF16>
+__device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row, int n0, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+  const bool full = n0 + 32 <= ep.N;
+  if (full) {
+    const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 bb = __ldg(b4 + j);
+      v[4 * j] += bb.x; v[4 * j + 1] += bb.y; v[4 * j + 2] += bb.z; v[4 * j + 3] += bb.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (n0 + j < ep.N) v[j] += __ldg(ep.bias + n0 + j);
+  }
+  if constexpr (EPI == EPI_GELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+  }
+  if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU) {
+    if constexpr (OUT_BF16) {
+      __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(ep.C) + row * ep.ldc + n0;
+      if (full) {
+        uint4* c4 = reinterpret_cast<uint4*>(c);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint4 w;
+          w.x = tc::pack_bf16(v[8 * j + 0], v[8 * j + 1]);
+          w.y = tc::pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+          w.z = tc::pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+          w.w = tc::pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+          c4[j] = w;
+        }
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < ep.N) c[j] = __float2bfloat16_rn(v[j]);
+      }
+    } else {
+      float* c = reinterpret_cast<float*>(ep.C) + row * ep.ldc + n0;
+      if (full) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<float4*>(c)[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (n0 + j < ep.N) c[j] = v[j];
+      }
+    }
+  } else if constexpr (EPI == EPI_RESID) {
+    float* z = reinterpret_cast<float*>(ep.C) + row * ep.ldc + n0;
+    if (full) {
+      float4* z4 = reinterpret_cast<float4*>(z);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 o = z4[j];
+        o.x += v[4 * j]; o.y += v[4 * j + 1]; o.z += v[4 * j + 2]; o.w += v[4 * j + 3];
+        z4[j] = o;
+      }
+    } else {
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < ep.N) z[j] += v[j];
+    }
+  } else {  // EPI_EMBED: z = acc + bias + pi(u,w); 32-column chunks never straddle D/2 (D % 64 == 0)
+    const int2 uw = __ldg(ep.rowinfo + row);
+    const float* pe = n0 < ep.half ? ep.pos_u + (int64_t)(uw.x + ep.pos_off) * ep.half + n0
+                                   : ep.pos_w + (int64_t)(uw.y + ep.pos_off) * ep.half + (n0 - ep.half);
+    float* z = reinterpret_cast<float*>(ep.C) + row * ep.ldc + n0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float4 p4 = __ldg(reinterpret_cast<const float4*>(pe) + j);
+      reinterpret_cast<float4*>(z)[j] =
+          make_float4(v[4 * j] + p4.x, v[4 * j + 1] + p4.y, v[4 * j + 2] + p4.z, v[4 * j + 3] + p4.w);
+    }
+  }
+}
+
+template <int BN, int STAGES, int EPI, bool OUT_BF16>
+__global__ void __launch_bounds__(256, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
+                   int K, EpiParams ep) {
+  constexpr int A_BYTES = BM * BK * 2;
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accf = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int nk = K / BK;
+
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer ----------------
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      tc::mbar_wait(&empty[s], ph ^ 1);
+      tc::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+      tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, (int32_t)m0);
+      tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, n0);
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % STAGES;
+      const uint32_t ph = (kb / STAGES) & 1;
+      tc::mbar_wait(&full[s], ph);
+      tc::tc_fence_after();
+      const uint32_t a0 = tc::smem_u32(sA + s * A_BYTES), b0 = tc::smem_u32(sB + s * B_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < BK / 16; ++kk) {
+        const uint64_t ad = tc::sdesc(a0 + kk * 32, 16, 1024, tc::SW_128B);
+        const uint64_t bd = tc::sdesc(b0 + kk * 32, 16, 1024, tc::SW_128B);
+        tc::mma_bf16_ss(tmem, ad, bd, idesc, (kb | kk) != 0);
+      }
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(accf);
+  } else if (warp >= 4) {
+    // ---------------- epilogue ----------------
+    const int q = warp - 4;
+    tc::mbar_wait(accf, 0);
+    tc::tc_fence_after();
+    const int64_t row = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, r);
+      tc::tmem_ld_wait();
+      if (row < M && n0 + c0 < ep.N) epilogue_chunk<EPI, OUT_BF16>(ep, row, n0 + c0, r);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+template <int BN, int STAGES, int EPI, bool OUT_BF16>
+bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
+                 cudaStream_t st) {
+  CUtensorMap ta, tb;
+  if (!make_tmap_bf16(&ta, A.ptr, A.rows, K, A.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  if (!make_tmap_bf16(&tb, Bw.ptr, Bw.rows, K, Bw.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16>;
+  static bool attr_set = false;   // per instantiation
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    attr_set = true;
+  }
+  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
+  kern<<<grid, 256, smem, st>>>(ta, tb, M, (int)K, ep);
+  return true;
+}
+
+}  // namespace
+
+bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
+                    int64_t K, const EpiParams& ep, cudaStream_t st) {
+  if (K % BK != 0 || M <= 0 || N <= 0) return false;
+  constexpr int BN = 128, ST = 3;
+  switch (epi) {
+    case EPI_BIAS:
+      return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
+                      : launch_impl<BN, ST, EPI_BIAS, false>(A, Bw, M, N, K, ep, st);
+    case EPI_GELU:
+      return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
+    case EPI_RESID:
+      return launch_impl<BN, ST, EPI_RESID, false>(A, Bw, M, N, K, ep, st);
+    case EPI_EMBED:
+      return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
+  }
+  return false;
+}
+
+}  // namespace orbit2

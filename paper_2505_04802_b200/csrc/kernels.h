@@ -1,0 +1,77 @@
+// kernels.h -- launchers of the liborbit2 kernels (host side declarations).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "orbit2_internal.h"
+
+namespace orbit2 {
+
+enum Epi : int {
+  EPI_BIAS = 0,    // C[m,n] = T(acc + bias[n])
+  EPI_GELU = 1,    // C[m,n] = T(gelu(acc + bias[n]))      (R9 exact-erf GELU)
+  EPI_RESID = 2,   // z[m,n] += acc + bias[n]               (fp32 residual stream)
+  EPI_EMBED = 3,   // z[m,n]  = acc + bias[n] + pi(u_m, w_m)  (R7, R8)
+};
+
+struct EpiParams {
+  int32_t M, N;
+  const float* bias;       // [N]
+  void* C;                 // output matrix (T or fp32 z)
+  int64_t ldc;             // elements
+  const int2* rowinfo;     // EMBED: global patch coords (u, w) per row
+  const float* pos_u;      // EMBED: [(Hp+2h)][D/2] = [sin(u om) | cos(u om)]
+  const float* pos_w;      // EMBED: [(Wp+2h)][D/2]
+  int32_t pos_off;         // halo h: table row = coord + h
+  int32_t half;            // D/2
+};
+
+struct GemmOperand {
+  const void* ptr;         // row-major [rows][ld] (K contiguous)
+  int64_t rows;            // allocated rows (TMA extent)
+  int64_t ld;              // elements per row
+};
+
+// Tiles/chunk view for the token-level kernels.
+struct ChunkDev {
+  const DevTile* tiles;    // local table (with sentinel)
+  int32_t tb, tc;
+  int64_t tok0, core0, chunk_tokens, chunk_core;
+  int32_t qb0, nqb;
+  const int32_t* qblk_tile;
+  const int32_t* core_row;
+};
+
+// ---- SIMT kernels (kernels_simt.cu) ----
+template <typename T>
+void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch, int B, int V, int H,
+                   int W, int p, int din, int din_pad, int max_pad_h, cudaStream_t st);
+template <typename T>
+void launch_layernorm(const float* z, const float* g, const float* b, T* out, int64_t M, int D,
+                      const ChunkDev* compact /* null = identity rows */, cudaStream_t st);
+template <typename T>
+void launch_stitch(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap,
+                   int B, int V, int H, int W, int K, int s, int P, int max_core_h, cudaStream_t st);
+void launch_sgemm(int epi, const float* A, int64_t lda, const float* Bw, int64_t ldb, int64_t M, int64_t N,
+                  int64_t K, const EpiParams& ep, cudaStream_t st);
+void launch_attention_f32(const float* qkv, float* out, const ChunkDev& ch, int B, int D, int heads, int d,
+                          cudaStream_t st);
+void launch_pos_tables(float* pos_u, float* pos_w, int Hp, int Wp, int h, int D, cudaStream_t st);
+void launch_convert_rows(const float* src, void* dst, int64_t rows, int64_t cols, int64_t ld_dst, int to_bf16,
+                         cudaStream_t st);
+void launch_add_vec(const float* a, const float* b, float* out, int64_t n, cudaStream_t st);
+
+// ---- tcgen05 / TMA kernels ----
+// bf16 A [M][K] x bf16 B [N][K]^T, fp32 accumulate in TMEM, fused epilogue.
+// Returns false if the shape is unsupported.
+bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
+                    int64_t K, const EpiParams& ep, cudaStream_t st);
+bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B,
+                         int D, int heads, int d, cudaStream_t st);
+
+// TMA descriptor encode via the driver entry point (no libcuda link dependency)
+bool tma_available();
+
+}  // namespace orbit2

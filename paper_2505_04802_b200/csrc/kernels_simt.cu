@@ -1,0 +1,365 @@
+// kernels_simt.cu -- CUDA-core kernels of the TILES pass: tile gather (step 1),
+// LayerNorm, stitch + bilinear residual (steps 4-5), one-time table/weight
+// preparation, and the IEEE-fp32 GEMM / attention used by the FP32 path.
+//
+// The bf16 contractions run on tcgen05 (gemm_tc.cu, attn_tc.cu); the fp32
+// SIMT GEMM/attention here are the 1e-4 parity path (no TF32) and make no
+// performance claim.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.h"
+
+namespace orbit2 {
+
+template <typename T> __device__ __forceinline__ T to_out(float v);
+template <> __device__ __forceinline__ float to_out<float>(float v) { return v; }
+template <> __device__ __forceinline__ __nv_bfloat16 to_out<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <typename T> __device__ __forceinline__ float to_f32(T v);
+template <> __device__ __forceinline__ float to_f32<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+// ---------------------------------------------------------------------------
+// Step (1) tile gather.  One CTA per (padded token row u of a tile, tile, b).
+// x~[v,a,c] = x[b, v, clamp(p*u0+a), clamp(p*w0+c)]  (clamp acts in REPLICATE
+// mode only, R4); token column (v*p+dy)*p+dx (R1).  Writes the patch matrix
+// row and the token's global patch coordinates (u, w) for the embed epilogue.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void gather_kernel(const float* __restrict__ x, T* __restrict__ patches, int2* __restrict__ rowinfo,
+                              ChunkDev ch, int V, int H, int W, int p, int din, int din_pad) {
+  const DevTile t = ch.tiles[ch.tb + blockIdx.y];
+  const int ur = blockIdx.x;
+  if (ur >= t.pad_h) return;
+  const int b = blockIdx.z;
+  const int64_t row0 = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0) + (int64_t)ur * t.pad_w;
+  const int u = t.pad_y0 + ur;
+  const int pp = p * p;
+  const float* xb = x + (int64_t)b * V * H * W;
+  const int total = t.pad_w * din_pad;
+  for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+    const int wr = idx / din_pad, col = idx - wr * din_pad;
+    float val = 0.f;
+    if (col < din) {
+      const int v = col / pp, r = col - v * pp, dy = r / p, dx = r - dy * p;
+      const int yy = min(max(p * u + dy, 0), H - 1);
+      const int xx = min(max(p * (t.pad_x0 + wr) + dx, 0), W - 1);
+      val = __ldg(xb + ((int64_t)v * H + yy) * W + xx);
+    }
+    patches[(row0 + wr) * din_pad + col] = to_out<T>(val);
+  }
+  for (int wr = threadIdx.x; wr < t.pad_w; wr += blockDim.x) rowinfo[row0 + wr] = make_int2(u, t.pad_x0 + wr);
+}
+
+template <typename T>
+void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch, int B, int V, int H, int W,
+                   int p, int din, int din_pad, int max_pad_h, cudaStream_t st) {
+  dim3 grid(max_pad_h, ch.tc, B);
+  gather_kernel<T><<<grid, 256, 0, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
+}
+template void launch_gather<float>(const float*, float*, int2*, const ChunkDev&, int, int, int, int, int, int, int,
+                                   int, cudaStream_t);
+template void launch_gather<__nv_bfloat16>(const float*, __nv_bfloat16*, int2*, const ChunkDev&, int, int, int,
+                                           int, int, int, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// LayerNorm (R9: biased variance, eps 1e-5, affine), fp32 statistics.
+// One warp per row; optional compaction of core rows for the head (R16).
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void layernorm_kernel(const float* __restrict__ z, const float* __restrict__ g,
+                                 const float* __restrict__ bta, T* __restrict__ out, int64_t M, int D,
+                                 bool compact, ChunkDev ch) {
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= M) return;
+  int64_t src = r;
+  if (compact) {
+    const int64_t b = r / ch.chunk_core, rr = r - b * ch.chunk_core;
+    src = b * ch.chunk_tokens + (ch.core_row[ch.core0 + rr] - ch.tok0);
+  }
+  const float4* zr = reinterpret_cast<const float4*>(z + src * D);
+  const int n4 = D / 4;
+  float s = 0.f;
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = zr[i];
+    s += (v.x + v.y) + (v.z + v.w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / D;
+  float q = 0.f;
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = zr[i];
+    float a = v.x - mean, b2 = v.y - mean, c = v.z - mean, e = v.w - mean;
+    q += (a * a + b2 * b2) + (c * c + e * e);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / D + 1e-5f);
+  T* orow = out + r * D;
+  for (int i = lane; i < n4; i += 32) {
+    float4 v = zr[i];
+    float4 gg = reinterpret_cast<const float4*>(g)[i];
+    float4 bb = reinterpret_cast<const float4*>(bta)[i];
+    orow[4 * i + 0] = to_out<T>((v.x - mean) * rstd * gg.x + bb.x);
+    orow[4 * i + 1] = to_out<T>((v.y - mean) * rstd * gg.y + bb.y);
+    orow[4 * i + 2] = to_out<T>((v.z - mean) * rstd * gg.z + bb.z);
+    orow[4 * i + 3] = to_out<T>((v.w - mean) * rstd * gg.w + bb.w);
+  }
+}
+
+template <typename T>
+void launch_layernorm(const float* z, const float* g, const float* b, T* out, int64_t M, int D,
+                      const ChunkDev* compact, cudaStream_t st) {
+  const int rows_per_cta = 8;
+  dim3 grid((unsigned)((M + rows_per_cta - 1) / rows_per_cta));
+  ChunkDev ch{};
+  if (compact) ch = *compact;
+  layernorm_kernel<T><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, D, compact != nullptr, ch);
+}
+template void launch_layernorm<float>(const float*, const float*, const float*, float*, int64_t, int,
+                                      const ChunkDev*, cudaStream_t);
+template void launch_layernorm<__nv_bfloat16>(const float*, const float*, const float*, __nv_bfloat16*, int64_t,
+                                              int, const ChunkDev*, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// Steps (4)+(5): crop/stitch + bilinear residual.  One CTA per (output row Y
+// of a tile's core, tile, b); threads run over (k, X) with X fastest so the
+// fp32 output row segment is written coalesced.
+//   out[b,k,Y,X] = tile_out[row(b,t,token(u,w))][(k*P+al)*P+be] + up_k(Y,X)
+//   up: src = max((Y+0.5)/s - 0.5, 0), y0 = floor, y1 = min(y0+1, H-1) (R12)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void stitch_kernel(const T* __restrict__ tile_out, const float* __restrict__ x, float* __restrict__ out,
+                              ChunkDev ch, const int32_t* __restrict__ cmap, int V, int H, int W, int K, int s,
+                              int P) {
+  const DevTile t = ch.tiles[ch.tb + blockIdx.y];
+  const int yr = blockIdx.x;
+  if (yr >= t.core_h * P) return;
+  const int b = blockIdx.z;
+  const int Y = t.core_y0 * P + yr;
+  const int ur = yr / P, al = yr - ur * P;
+  const int X0 = t.core_x0 * P, NX = t.core_w * P;
+  const int64_t sH = (int64_t)s * H, sW = (int64_t)s * W;
+  const int64_t trow0 = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0) + (int64_t)ur * t.core_w;
+  const int Nh = K * P * P;
+  const float inv_s = 1.0f / (float)s;
+  const float sy = fmaxf(((float)Y + 0.5f) * inv_s - 0.5f, 0.f);
+  const int y0 = min((int)sy, H - 1), y1 = min(y0 + 1, H - 1);
+  const float ly = sy - (float)y0;
+  for (int idx = threadIdx.x; idx < K * NX; idx += blockDim.x) {
+    const int k = idx / NX, xr = idx - k * NX;
+    const int X = X0 + xr;
+    const int wr = xr / P, be = xr - wr * P;
+    const float vit = to_f32<T>(tile_out[(trow0 + wr) * Nh + (k * P + al) * P + be]);
+    const float sx = fmaxf(((float)X + 0.5f) * inv_s - 0.5f, 0.f);
+    const int x0 = min((int)sx, W - 1), x1 = min(x0 + 1, W - 1);
+    const float lx = sx - (float)x0;
+    const float* pl = x + ((int64_t)b * V + cmap[k]) * H * W;
+    const float a00 = __ldg(pl + (int64_t)y0 * W + x0), a01 = __ldg(pl + (int64_t)y0 * W + x1);
+    const float a10 = __ldg(pl + (int64_t)y1 * W + x0), a11 = __ldg(pl + (int64_t)y1 * W + x1);
+    const float up = (1.f - ly) * ((1.f - lx) * a00 + lx * a01) + ly * ((1.f - lx) * a10 + lx * a11);
+    out[(((int64_t)b * K + k) * sH + Y) * sW + X] = vit + up;
+  }
+}
+
+template <typename T>
+void launch_stitch(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap, int B,
+                   int V, int H, int W, int K, int s, int P, int max_core_h, cudaStream_t st) {
+  dim3 grid(max_core_h * P, ch.tc, B);
+  stitch_kernel<T><<<grid, 256, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+}
+template void launch_stitch<float>(const float*, const float*, float*, const ChunkDev&, const int32_t*, int, int,
+                                   int, int, int, int, int, int, cudaStream_t);
+template void launch_stitch<__nv_bfloat16>(const __nv_bfloat16*, const float*, float*, const ChunkDev&,
+                                           const int32_t*, int, int, int, int, int, int, int, int, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+// One-time tables: sincos position rows (R7), computed in fp64 then rounded.
+// pos_u[r][m] = sin(u om_m), pos_u[r][Q+m] = cos(u om_m), u = r - h, Q = D/4.
+// ---------------------------------------------------------------------------
+__global__ void pos_table_kernel(float* tab, int rows, int h, int D) {
+  const int Q = D / 4;
+  const int64_t n = (int64_t)rows * Q;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / Q), m = (int)(i - (int64_t)r * Q);
+    const double om = pow(10000.0, -(double)m / (double)Q);
+    const double a = (double)(r - h) * om;
+    tab[(int64_t)r * (D / 2) + m] = (float)sin(a);
+    tab[(int64_t)r * (D / 2) + Q + m] = (float)cos(a);
+  }
+}
+
+void launch_pos_tables(float* pos_u, float* pos_w, int Hp, int Wp, int h, int D, cudaStream_t st) {
+  pos_table_kernel<<<64, 256, 0, st>>>(pos_u, Hp + 2 * h, h, D);
+  pos_table_kernel<<<64, 256, 0, st>>>(pos_w, Wp + 2 * h, h, D);
+}
+
+// fp32 [rows][cols] -> bf16/fp32 [rows][ld_dst] (zero-padded columns)
+__global__ void convert_rows_kernel(const float* __restrict__ src, void* dst, int64_t rows, int64_t cols,
+                                    int64_t ld_dst, int to_bf16) {
+  const int64_t n = rows * ld_dst;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld_dst, c = i - r * ld_dst;
+    const float v = c < cols ? src[r * cols + c] : 0.f;
+    if (to_bf16)
+      reinterpret_cast<__nv_bfloat16*>(dst)[i] = __float2bfloat16_rn(v);
+    else
+      reinterpret_cast<float*>(dst)[i] = v;
+  }
+}
+
+void launch_convert_rows(const float* src, void* dst, int64_t rows, int64_t cols, int64_t ld_dst, int to_bf16,
+                         cudaStream_t st) {
+  int64_t n = rows * ld_dst;
+  int blocks = (int)std::min<int64_t>((n + 255) / 256, 4096);
+  convert_rows_kernel<<<blocks, 256, 0, st>>>(src, dst, rows, cols, ld_dst, to_bf16);
+}
+
+__global__ void add_vec_kernel(const float* a, const float* b, float* o, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    o[i] = a[i] + b[i];
+}
+void launch_add_vec(const float* a, const float* b, float* out, int64_t n, cudaStream_t st) {
+  add_vec_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(a, b, out, n);
+}
+
+// ---------------------------------------------------------------------------
+// FP32 path: SIMT GEMM  C = A[M,K] . B[N,K]^T  with the shared epilogues.
+// 64x64 tile, BK 16, 256 threads, 4x4 outputs per thread, IEEE fp32 FMA.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void epi_store(int epi, const EpiParams& ep, int64_t m, int64_t n, float acc) {
+  const float v = acc + ep.bias[n];
+  if (epi == EPI_BIAS) {
+    reinterpret_cast<float*>(ep.C)[m * ep.ldc + n] = v;
+  } else if (epi == EPI_GELU) {
+    reinterpret_cast<float*>(ep.C)[m * ep.ldc + n] = gelu_erf(v);
+  } else if (epi == EPI_RESID) {
+    float* z = reinterpret_cast<float*>(ep.C) + m * ep.ldc + n;
+    *z = *z + v;
+  } else {
+    const int2 uw = ep.rowinfo[m];
+    const float pe = n < ep.half ? ep.pos_u[(int64_t)(uw.x + ep.pos_off) * ep.half + n]
+                                 : ep.pos_w[(int64_t)(uw.y + ep.pos_off) * ep.half + (n - ep.half)];
+    reinterpret_cast<float*>(ep.C)[m * ep.ldc + n] = v + pe;
+  }
+}
+
+__global__ void __launch_bounds__(256) sgemm_kernel(int epi, const float* __restrict__ A, int64_t lda,
+                                                    const float* __restrict__ Bw, int64_t ldb, int64_t M, int64_t N,
+                                                    int64_t K, EpiParams ep) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.y * 64, n0 = (int64_t)blockIdx.x * 64;
+  float acc[4][4] = {};
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 64 * 16; i += 256) {
+      const int r = i / 16, c = i % 16;
+      const int64_t gm = m0 + r, gn = n0 + r, gk = k0 + c;
+      As[c][r] = (gm < M && gk < K) ? A[gm * lda + gk] : 0.f;
+      Bs[c][r] = (gn < N && gk < K) ? Bw[gn * ldb + gk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int64_t m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m < M && n < N) epi_store(epi, ep, m, n, acc[i][j]);
+    }
+}
+
+void launch_sgemm(int epi, const float* A, int64_t lda, const float* Bw, int64_t ldb, int64_t M, int64_t N,
+                  int64_t K, const EpiParams& ep, cudaStream_t st) {
+  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+  sgemm_kernel<<<grid, 256, 0, st>>>(epi, A, lda, Bw, ldb, M, N, K, ep);
+}
+
+// ---------------------------------------------------------------------------
+// FP32 path: per-tile attention ("self-attention is restricted within
+// each tile").  One CTA per (query block of 128 rows of a tile, head, sample);
+// one query per thread; online softmax in fp32 with expf; keys masked to the
+// tile.  out[row, h*d:(h+1)*d] = softmax(q K^T / sqrt(d)) V.
+// ---------------------------------------------------------------------------
+template <int DH>
+__global__ void __launch_bounds__(128) attention_f32_kernel(const float* __restrict__ qkv, float* __restrict__ out,
+                                                            ChunkDev ch, int D) {
+  constexpr int KB = 32;
+  __shared__ float Ks[KB][DH];
+  __shared__ float Vs[KB][DH];
+  const int g = ch.qb0 + blockIdx.x;
+  const int li = ch.qblk_tile[g];
+  const DevTile t = ch.tiles[li];
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int qi = (g - t.qb_off) * kQBlock + threadIdx.x;
+  const int64_t base = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0);
+  const int64_t ld = 3LL * D;
+  const bool active = qi < t.n_tokens;
+  float q[DH], o[DH];
+  const float scale = rsqrtf((float)DH);
+#pragma unroll
+  for (int j = 0; j < DH; ++j) {
+    q[j] = active ? qkv[(base + qi) * ld + h * DH + j] * scale : 0.f;
+    o[j] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  for (int k0 = 0; k0 < t.n_tokens; k0 += KB) {
+    const int nk = min(KB, t.n_tokens - k0);
+    for (int i = threadIdx.x; i < KB * DH; i += blockDim.x) {
+      const int r = i / DH, c = i % DH;
+      const bool ok = r < nk;
+      Ks[r][c] = ok ? qkv[(base + k0 + r) * ld + D + h * DH + c] : 0.f;
+      Vs[r][c] = ok ? qkv[(base + k0 + r) * ld + 2 * D + h * DH + c] : 0.f;
+    }
+    __syncthreads();
+    for (int r = 0; r < nk; ++r) {
+      float sc = 0.f;
+#pragma unroll
+      for (int j = 0; j < DH; ++j) sc = fmaf(q[j], Ks[r][j], sc);
+      const float mn = fmaxf(m, sc);
+      const float corr = expf(m - mn);
+      const float pr = expf(sc - mn);
+      l = l * corr + pr;
+#pragma unroll
+      for (int j = 0; j < DH; ++j) o[j] = fmaf(pr, Vs[r][j], o[j] * corr);
+      m = mn;
+    }
+    __syncthreads();
+  }
+  if (active) {
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int j = 0; j < DH; ++j) out[(base + qi) * D + h * DH + j] = o[j] * inv;
+  }
+}
+
+void launch_attention_f32(const float* qkv, float* out, const ChunkDev& ch, int B, int D, int heads, int d,
+                          cudaStream_t st) {
+  dim3 grid(ch.nqb, heads, B);
+  if (d == 32) attention_f32_kernel<32><<<grid, 128, 0, st>>>(qkv, out, ch, D);
+  else if (d == 64) attention_f32_kernel<64><<<grid, 128, 0, st>>>(qkv, out, ch, D);
+  else attention_f32_kernel<128><<<grid, 128, 0, st>>>(qkv, out, ch, D);
+}
+
+}  // namespace orbit2

@@ -1,0 +1,445 @@
+// orbit2_abi.cu -- the C ABI of liborbit2.so (include/orbit2.h): plan,
+// create, weight packing, the forward (steps 1-3 + head) and the stitch
+// (steps 4-5).  Orchestration only; every step of the path is a kernel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "orbit2_internal.h"
+
+using namespace orbit2;
+
+namespace {
+
+thread_local std::string g_err;
+
+orbit2_status set_err(orbit2_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+struct Timing {
+  const char* name;
+  cudaEvent_t a, b;
+};
+
+struct Ctx {
+  Plan plan;
+  WeightLayout wl;
+  uint8_t* ws = nullptr;
+  int64_t launches = 0;
+  bool profiling = false;
+  std::vector<Timing> pending;
+  std::vector<cudaEvent_t> pool;
+  std::map<std::string, std::pair<int64_t, double>> acc;
+  bool sync_check = false;
+
+  template <typename T>
+  T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
+};
+
+cudaEvent_t take_event(Ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void drain_timings(Ctx* c) {
+  for (auto& t : c->pending) {
+    cudaEventSynchronize(t.b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t.a, t.b);
+    auto& a = c->acc[t.name];
+    a.first += 1;
+    a.second += ms;
+    c->pool.push_back(t.a);
+    c->pool.push_back(t.b);
+  }
+  c->pending.clear();
+}
+
+// Launch wrapper: counts launches, optionally brackets them with events.
+template <typename F>
+orbit2_status run(Ctx* c, const char* name, cudaStream_t st, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->profiling) {
+    a = take_event(c);
+    b = take_event(c);
+    cudaEventRecord(a, st);
+  }
+  bool ok = f();
+  c->launches += 1;
+  if (c->profiling) {
+    cudaEventRecord(b, st);
+    c->pending.push_back({name, a, b});
+  }
+  if (!ok) return set_err(ORBIT2_E_CUDA, std::string(name) + ": launch configuration rejected");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string(name) + ": " + cudaGetErrorString(e));
+  if (c->sync_check) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string(name) + " (sync check): " + cudaGetErrorString(e));
+  }
+  return ORBIT2_OK;
+}
+
+#define ORBIT2_TRY(x)                 \
+  do {                                \
+    orbit2_status _s = (x);           \
+    if (_s != ORBIT2_OK) return _s;   \
+  } while (0)
+
+ChunkDev chunk_dev(const Ctx* c, const Chunk& ch) {
+  const Plan& p = c->plan;
+  ChunkDev d{};
+  d.tiles = c->at<DevTile>(p.lay.tiles);
+  d.tb = ch.tb;
+  d.tc = ch.tc;
+  d.tok0 = ch.tok0;
+  d.core0 = ch.core0;
+  d.chunk_tokens = ch.chunk_tokens;
+  d.chunk_core = ch.chunk_core;
+  d.qb0 = ch.qb0;
+  d.nqb = ch.nqb;
+  d.qblk_tile = c->at<int32_t>(p.lay.qblk_tile);
+  d.core_row = c->at<int32_t>(p.lay.core_row);
+  return d;
+}
+
+orbit2_status check_range(const Ctx* c, int32_t tb, int32_t tc) {
+  const orbit2_plan_info& in = c->plan.info;
+  if (tb < 0 || tc < 1 || tb + tc > in.n_local_tiles)
+    return set_err(ORBIT2_E_INVALID, "tile_begin/tile_count: range outside the rank-local tile list");
+  if (tc > in.chunk_tiles) return set_err(ORBIT2_E_INVALID, "tile_count: exceeds info.chunk_tiles");
+  return ORBIT2_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+const char* orbit2_last_error(void) { return g_err.c_str(); }
+
+orbit2_status orbit2_tiles_plan(const orbit2_config* cfg, orbit2_tile* tiles, int32_t capacity,
+                                orbit2_plan_info* info) {
+  Plan p;
+  std::string msg;
+  orbit2_status st = build_plan(cfg, &p, &msg);
+  if (st != ORBIT2_OK) return set_err(st, msg);
+  if (info) *info = p.info;
+  if (tiles == nullptr && capacity == 0) return ORBIT2_OK;
+  if (capacity < p.info.n_tiles) return set_err(ORBIT2_E_CAPACITY, "capacity: smaller than n_tiles");
+  if (!tiles) return set_err(ORBIT2_E_INVALID, "tiles: null with capacity > 0");
+  std::memcpy(tiles, p.tiles.data(), sizeof(orbit2_tile) * p.tiles.size());
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_t workspace_bytes, void** ctx) {
+  if (!ctx) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  *ctx = nullptr;
+  Ctx* c = new Ctx();
+  std::string msg;
+  orbit2_status st = build_plan(cfg, &c->plan, &msg);
+  if (st != ORBIT2_OK) {
+    delete c;
+    return set_err(st, msg);
+  }
+  const Plan& p = c->plan;
+  if (!workspace_dev || !aligned16(workspace_dev)) {
+    delete c;
+    return set_err(ORBIT2_E_INVALID, "workspace_dev: null or not 16-byte aligned");
+  }
+  if ((int64_t)workspace_bytes < p.info.workspace_bytes) {
+    delete c;
+    return set_err(ORBIT2_E_CAPACITY, "workspace_bytes: smaller than info.workspace_bytes");
+  }
+  if (p.cfg.precision == ORBIT2_BF16 && !tma_available()) {
+    delete c;
+    return set_err(ORBIT2_E_CUDA, "cuTensorMapEncodeTiled: driver entry point unavailable");
+  }
+  c->ws = reinterpret_cast<uint8_t*>(workspace_dev);
+  c->wl = weight_layout(p);
+  const char* sc = std::getenv("ORBIT2_SYNC_CHECK");
+  c->sync_check = sc && sc[0] == '1';
+  cudaError_t e = cudaSuccess;
+  e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.qblk_tile.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.qblk_tile), p.qblk_tile.data(), p.qblk_tile.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.core_row.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.core_row), p.core_row.data(), p.core_row.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(c->at<void>(p.lay.cmap), p.cmap.data(), p.cmap.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    launch_pos_tables(c->at<float>(p.lay.pos_u), c->at<float>(p.lay.pos_w), p.Hp, p.Wp, p.cfg.halo, p.D, 0);
+    c->launches += 2;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  }
+  if (e != cudaSuccess) {
+    delete c;
+    return set_err(ORBIT2_E_CUDA, std::string("orbit2_create: ") + cudaGetErrorString(e));
+  }
+  *ctx = c;
+  return ORBIT2_OK;
+}
+
+void orbit2_destroy(void* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return;
+  for (auto& t : c->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : c->pool) cudaEventDestroy(e);
+  delete c;
+}
+
+int64_t orbit2_launch_count(void* ctx) { return ctx ? reinterpret_cast<Ctx*>(ctx)->launches : 0; }
+
+orbit2_status orbit2_set_profiling(void* ctx, int32_t enable) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  drain_timings(c);
+  c->acc.clear();
+  c->profiling = enable != 0;
+  return ORBIT2_OK;
+}
+
+int32_t orbit2_kernel_times(void* ctx, const char** names, int64_t* launches, double* ms, int32_t cap) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return 0;
+  drain_timings(c);
+  int32_t i = 0;
+  for (auto& kv : c->acc) {
+    if (i < cap) {
+      if (names) names[i] = kv.first.c_str();
+      if (launches) launches[i] = kv.second.first;
+      if (ms) ms[i] = kv.second.second;
+    }
+    ++i;
+  }
+  return i;
+}
+
+orbit2_status orbit2_prepare_weights(void* ctx, const float* canonical_dev, void* packed_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!canonical_dev || !packed_dev || !aligned16(packed_dev))
+    return set_err(ORBIT2_E_INVALID, "canonical_dev/packed_dev: null or not 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const WeightLayout& w = c->wl;
+  const int bf = p.cfg.precision == ORBIT2_BF16;
+  uint8_t* pk = reinterpret_cast<uint8_t*>(packed_dev);
+  const int64_t D = p.D, F = 4LL * p.D;
+  auto conv = [&](int64_t coff, int64_t poff, int64_t rows, int64_t cols, int64_t ld, int to_bf) {
+    return run(c, "prepare_weights", st, [&] {
+      launch_convert_rows(canonical_dev + coff, pk + poff, rows, cols, ld, to_bf, st);
+      return true;
+    });
+  };
+  ORBIT2_TRY(conv(w.c_w_e, w.w_e, D, p.Din, p.lay.din_pad, bf));
+  ORBIT2_TRY(run(c, "prepare_weights", st, [&] {
+    launch_add_vec(canonical_dev + w.c_b_e, canonical_dev + w.c_e_s, reinterpret_cast<float*>(pk + w.bias_e), D, st);
+    return true;
+  }));
+  for (int l = 0; l < p.cfg.depth; ++l) {
+    const LayerW& C = w.c_layers[l];
+    const LayerW& P = w.layers[l];
+    ORBIT2_TRY(conv(C.ln1_g, P.ln1_g, 1, D, D, 0));
+    ORBIT2_TRY(conv(C.ln1_b, P.ln1_b, 1, D, D, 0));
+    ORBIT2_TRY(conv(C.w_qkv, P.w_qkv, 3 * D, D, D, bf));
+    ORBIT2_TRY(conv(C.b_qkv, P.b_qkv, 1, 3 * D, 3 * D, 0));
+    ORBIT2_TRY(conv(C.w_o, P.w_o, D, D, D, bf));
+    ORBIT2_TRY(conv(C.b_o, P.b_o, 1, D, D, 0));
+    ORBIT2_TRY(conv(C.ln2_g, P.ln2_g, 1, D, D, 0));
+    ORBIT2_TRY(conv(C.ln2_b, P.ln2_b, 1, D, D, 0));
+    ORBIT2_TRY(conv(C.w_1, P.w_1, F, D, D, bf));
+    ORBIT2_TRY(conv(C.b_1, P.b_1, 1, F, F, 0));
+    ORBIT2_TRY(conv(C.w_2, P.w_2, D, F, F, bf));
+    ORBIT2_TRY(conv(C.b_2, P.b_2, 1, D, D, 0));
+  }
+  ORBIT2_TRY(conv(w.c_lnf_g, w.lnf_g, 1, D, D, 0));
+  ORBIT2_TRY(conv(w.c_lnf_b, w.lnf_b, 1, D, D, 0));
+  ORBIT2_TRY(conv(w.c_w_h, w.w_h, p.Nh, D, D, bf));
+  ORBIT2_TRY(conv(w.c_b_h, w.b_h, 1, p.Nh, p.Nh, 0));
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float* input_dev, int32_t tile_begin,
+                                    int32_t tile_count, void* tile_out_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!packed_w || !input_dev || !tile_out_dev || !aligned16(packed_w) || !aligned16(input_dev) ||
+      !aligned16(tile_out_dev))
+    return set_err(ORBIT2_E_INVALID, "packed_w/input_dev/tile_out_dev: null or not 16-byte aligned");
+  ORBIT2_TRY(check_range(c, tile_begin, tile_count));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const Layout& ly = p.lay;
+  const WeightLayout& w = c->wl;
+  const uint8_t* W8 = reinterpret_cast<const uint8_t*>(packed_w);
+  auto wf = [&](int64_t off) { return reinterpret_cast<const float*>(W8 + off); };
+  const Chunk ch = make_chunk(p, tile_begin, tile_count);
+  const ChunkDev cd = chunk_dev(c, ch);
+  const int B = cf.batch;
+  const int64_t M = (int64_t)B * ch.chunk_tokens;
+  const int64_t Mc = (int64_t)B * ch.chunk_core;
+  const int64_t D = p.D, F = 4LL * p.D;
+  const int64_t mrow = ly.mrow, mcore = ly.mcore;
+  int2* rowinfo = c->at<int2>(ly.rowinfo);
+  float* z = c->at<float>(ly.z);
+
+  EpiParams emb{};
+  emb.M = (int32_t)M; emb.N = (int32_t)D; emb.bias = wf(w.bias_e); emb.C = z; emb.ldc = D;
+  emb.rowinfo = rowinfo; emb.pos_u = c->at<float>(ly.pos_u); emb.pos_w = c->at<float>(ly.pos_w);
+  emb.pos_off = cf.halo; emb.half = (int32_t)(D / 2);
+
+  if (cf.precision == ORBIT2_BF16) {
+    typedef __nv_bfloat16 bf16;
+    bf16* patches = c->at<bf16>(ly.patches);
+    bf16* xn = c->at<bf16>(ly.xn);
+    bf16* qkv = c->at<bf16>(ly.qkv);
+    bf16* ao = c->at<bf16>(ly.ao);
+    bf16* hid = c->at<bf16>(ly.hid);
+    bf16* hin = c->at<bf16>(ly.hin);
+    auto gemm = [&](const char* name, int epi, int out_bf, const void* A, int64_t arows, int64_t lda,
+                    int64_t wo, int64_t n, int64_t k, int64_t rows, EpiParams ep) {
+      GemmOperand a{A, arows, lda}, b{W8 + wo, n, k};
+      ep.M = (int32_t)rows;
+      ep.N = (int32_t)n;
+      return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+    };
+    ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+      launch_gather<bf16>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
+                          p.max_pad_h, st);
+      return true;
+    }));
+    ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    for (int l = 0; l < cf.depth; ++l) {
+      const LayerW& L = w.layers[l];
+      ORBIT2_TRY(run(c, "layernorm", st, [&] {
+        launch_layernorm<bf16>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
+        return true;
+      }));
+      EpiParams e{};
+      e.bias = wf(L.b_qkv); e.C = qkv; e.ldc = 3 * D;
+      ORBIT2_TRY(gemm("qkv_gemm", EPI_BIAS, 1, xn, mrow, D, L.w_qkv, 3 * D, D, M, e));
+      ORBIT2_TRY(run(c, "tile_attention", st, [&] {
+        return launch_attention_tc(qkv, mrow, ao, cd, B, (int)D, cf.heads, p.d, st);
+      }));
+      e = EpiParams{}; e.bias = wf(L.b_o); e.C = z; e.ldc = D;
+      ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID, 0, ao, mrow, D, L.w_o, D, D, M, e));
+      ORBIT2_TRY(run(c, "layernorm", st, [&] {
+        launch_layernorm<bf16>(z, wf(L.ln2_g), wf(L.ln2_b), xn, M, (int)D, nullptr, st);
+        return true;
+      }));
+      e = EpiParams{}; e.bias = wf(L.b_1); e.C = hid; e.ldc = F;
+      ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn, mrow, D, L.w_1, F, D, M, e));
+      e = EpiParams{}; e.bias = wf(L.b_2); e.C = z; e.ldc = D;
+      ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, hid, mrow, F, L.w_2, D, F, M, e));
+    }
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<bf16>(z, wf(w.lnf_g), wf(w.lnf_b), hin, Mc, (int)D, &cd, st);
+      return true;
+    }));
+    EpiParams e{};
+    e.bias = wf(w.b_h); e.C = tile_out_dev; e.ldc = p.Nh;
+    ORBIT2_TRY(gemm("head_gemm", EPI_BIAS, 1, hin, mcore, D, w.w_h, p.Nh, D, Mc, e));
+  } else {
+    float* patches = c->at<float>(ly.patches);
+    float* xn = c->at<float>(ly.xn);
+    float* qkv = c->at<float>(ly.qkv);
+    float* ao = c->at<float>(ly.ao);
+    float* hid = c->at<float>(ly.hid);
+    float* hin = c->at<float>(ly.hin);
+    auto sg = [&](const char* name, int epi, const float* A, int64_t lda, int64_t wo, int64_t n, int64_t k,
+                  int64_t rows, EpiParams ep) {
+      ep.M = (int32_t)rows;
+      ep.N = (int32_t)n;
+      return run(c, name, st, [&] {
+        launch_sgemm(epi, A, lda, wf(wo), k, rows, n, k, ep, st);
+        return true;
+      });
+    };
+    ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+      launch_gather<float>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
+                           p.max_pad_h, st);
+      return true;
+    }));
+    ORBIT2_TRY(sg("embed_gemm", EPI_EMBED, patches, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    for (int l = 0; l < cf.depth; ++l) {
+      const LayerW& L = w.layers[l];
+      ORBIT2_TRY(run(c, "layernorm", st, [&] {
+        launch_layernorm<float>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
+        return true;
+      }));
+      EpiParams e{};
+      e.bias = wf(L.b_qkv); e.C = qkv; e.ldc = 3 * D;
+      ORBIT2_TRY(sg("qkv_gemm", EPI_BIAS, xn, D, L.w_qkv, 3 * D, D, M, e));
+      ORBIT2_TRY(run(c, "tile_attention", st, [&] {
+        launch_attention_f32(qkv, ao, cd, B, (int)D, cf.heads, p.d, st);
+        return true;
+      }));
+      e = EpiParams{}; e.bias = wf(L.b_o); e.C = z; e.ldc = D;
+      ORBIT2_TRY(sg("oproj_gemm", EPI_RESID, ao, D, L.w_o, D, D, M, e));
+      ORBIT2_TRY(run(c, "layernorm", st, [&] {
+        launch_layernorm<float>(z, wf(L.ln2_g), wf(L.ln2_b), xn, M, (int)D, nullptr, st);
+        return true;
+      }));
+      e = EpiParams{}; e.bias = wf(L.b_1); e.C = hid; e.ldc = F;
+      ORBIT2_TRY(sg("mlp_up_gemm", EPI_GELU, xn, D, L.w_1, F, D, M, e));
+      e = EpiParams{}; e.bias = wf(L.b_2); e.C = z; e.ldc = D;
+      ORBIT2_TRY(sg("mlp_down_gemm", EPI_RESID, hid, F, L.w_2, D, F, M, e));
+    }
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<float>(z, wf(w.lnf_g), wf(w.lnf_b), hin, Mc, (int)D, &cd, st);
+      return true;
+    }));
+    EpiParams e{};
+    e.bias = wf(w.b_h); e.C = tile_out_dev; e.ldc = p.Nh;
+    ORBIT2_TRY(sg("head_gemm", EPI_BIAS, hin, D, w.w_h, p.Nh, D, Mc, e));
+  }
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_stitch(void* ctx, const void* tile_out_dev, const float* input_dev, int32_t tile_begin,
+                            int32_t tile_count, float* out_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!tile_out_dev || !input_dev || !out_dev || !aligned16(tile_out_dev) || !aligned16(input_dev) ||
+      !aligned16(out_dev))
+    return set_err(ORBIT2_E_INVALID, "tile_out_dev/input_dev/out_dev: null or not 16-byte aligned");
+  ORBIT2_TRY(check_range(c, tile_begin, tile_count));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const ChunkDev cd = chunk_dev(c, make_chunk(p, tile_begin, tile_count));
+  const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
+  return run(c, "stitch_residual", st, [&] {
+    if (cf.precision == ORBIT2_BF16)
+      launch_stitch<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev, out_dev, cd,
+                                   cmap, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h, st);
+    else
+      launch_stitch<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, cf.batch,
+                           cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h, st);
+    return true;
+  });
+}
+
+}  // extern "C"

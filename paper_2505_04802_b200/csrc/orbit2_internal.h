@@ -1,0 +1,82 @@
+// orbit2_internal.h -- internal definitions shared by the planner, the ABI
+// layer and the kernels of liborbit2.so.  Not part of the public ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/orbit2.h"
+
+namespace orbit2 {
+
+constexpr int kQBlock = 128;       // attention query/key block (tcgen05 M = 128)
+constexpr int kAlign = 1024;       // workspace region alignment (SW128 atoms)
+
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// One rank-local tile as the kernels see it (uploaded into the workspace).
+struct DevTile {
+  int32_t pad_y0, pad_x0, pad_h, pad_w;      // padded rect (patch units)
+  int32_t core_y0, core_x0, core_h, core_w;  // core rect (patch units)
+  int32_t n_tokens, n_core;
+  int32_t qb_off;                             // first query block (local numbering)
+  int32_t pad_;
+  int64_t tok_off;                            // token offset in local packing (one sample)
+  int64_t core_off;                           // core-token offset in local packing
+};
+static_assert(sizeof(DevTile) == 64, "DevTile layout");
+
+// Per-call geometry of a chunk of rank-local tiles [tb, tb+tc) for B samples.
+struct Chunk {
+  int32_t tb, tc;
+  int64_t tok0, core0;        // local offsets of the first tile
+  int64_t chunk_tokens;       // tokens per sample in this chunk
+  int64_t chunk_core;         // core tokens per sample in this chunk
+  int32_t qb0, nqb;           // query blocks (per sample) of the chunk
+};
+
+// Byte offsets of the workspace regions (from the workspace base).
+struct Layout {
+  int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
+  int64_t tiles, qblk_tile, core_row, pos_u, pos_w, cmap;
+  int64_t total;
+  int64_t mrow, mcore;        // rows of the token and core-token buffers
+  int32_t din_pad;
+  int32_t esize;              // activation element size (2 bf16, 4 fp32)
+};
+
+struct Plan {
+  orbit2_config cfg;
+  std::vector<int32_t> cmap;            // K entries
+  std::vector<orbit2_tile> tiles;       // all tiles, tile_id order
+  std::vector<int32_t> local;           // tile ids owned by cfg.rank, increasing
+  std::vector<DevTile> dev;             // rank-local device table
+  std::vector<int32_t> qblk_tile;       // local q-block -> local tile index
+  std::vector<int32_t> core_row;        // local core token -> local padded token index
+  orbit2_plan_info info;
+  Layout lay;
+  int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_core_h;
+};
+
+// planner (plan.cpp); returns status and fills msg on error
+orbit2_status build_plan(const orbit2_config* cfg, Plan* plan, std::string* msg);
+Chunk make_chunk(const Plan& plan, int32_t tb, int32_t tc);
+
+// Packed-weight offsets (bytes from the packed base).
+struct LayerW {
+  int64_t ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_1, b_1, w_2, b_2;
+};
+struct WeightLayout {
+  int64_t w_e, bias_e, lnf_g, lnf_b, w_h, b_h;
+  std::vector<LayerW> layers;
+  int64_t total;
+  // canonical (fp32 element) offsets, same names
+  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h;
+  std::vector<LayerW> c_layers;
+  int64_t c_total;
+};
+WeightLayout weight_layout(const Plan& plan);
+
+}  // namespace orbit2

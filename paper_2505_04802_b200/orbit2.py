@@ -1,0 +1,210 @@
+"""Thin ctypes binding of liborbit2.so (include/orbit2.h).
+
+Argument marshalling only: every step of the pass runs in the library's
+kernels.  PyTorch supplies device memory and streams.  There is no CPU
+fallback: if the library is missing or fails to load, importing this module
+raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "liborbit2.so")
+
+ABI_VERSION = 1
+OK, E_INVALID, E_CAPACITY, E_UNSUPPORTED, E_CUDA, E_NCCL, E_STATE = 0, -1, -2, -3, -4, -5, -6
+HALO_CLAMP, HALO_REPLICATE = 0, 1
+BF16, FP32 = 0, 1
+
+
+class orbit2_config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "abi_version", "batch", "H", "W", "V", "K", "scale", "patch", "tiles_y", "tiles_x", "halo",
+        "halo_mode", "embed", "depth", "heads", "mlp_hidden", "precision", "world_size", "rank",
+        "chunk_tiles")] + [("out_channel_map", C.POINTER(C.c_int32))]
+
+
+class orbit2_tile(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in (
+        "tile_id", "tile_y", "tile_x", "owner_rank", "local_index", "core_y0", "core_y1", "core_x0",
+        "core_x1", "pad_y0", "pad_y1", "pad_x0", "pad_x1", "n_tokens", "n_core_tokens")] + [
+        ("token_offset", C.c_int64), ("core_token_offset", C.c_int64)]
+
+
+class orbit2_plan_info(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("n_tiles", "n_local_tiles", "chunk_tiles", "head_dim")] + [
+        (n, C.c_int64) for n in (
+            "tokens_per_sample", "core_tokens_per_sample", "local_tokens", "local_core_tokens",
+            "max_chunk_tokens", "max_chunk_core_tokens", "sum_n2_per_sample", "sum_nc_per_sample",
+            "workspace_bytes", "canonical_weight_count", "packed_weight_bytes", "tile_out_bytes",
+            "out_bytes")] + [(n, C.c_double) for n in (
+                "flops_per_sample", "local_flops_per_sample", "gather_bytes_per_sample",
+                "stitch_bytes_per_sample")]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2505_04802_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    vp, i32, i64 = C.c_void_p, C.c_int32, C.c_int64
+    sig = {
+        "orbit2_tiles_plan": (i32, [C.POINTER(orbit2_config), C.POINTER(orbit2_tile), i32,
+                                    C.POINTER(orbit2_plan_info)]),
+        "orbit2_create": (i32, [C.POINTER(orbit2_config), vp, C.c_size_t, C.POINTER(vp)]),
+        "orbit2_prepare_weights": (i32, [vp, vp, vp, vp]),
+        "orbit2_reslim_forward": (i32, [vp, vp, vp, i32, i32, vp, vp]),
+        "orbit2_stitch": (i32, [vp, vp, vp, i32, i32, vp, vp]),
+        "orbit2_launch_count": (i64, [vp]),
+        "orbit2_set_profiling": (i32, [vp, i32]),
+        "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
+        "orbit2_last_error": (C.c_char_p, []),
+        "orbit2_destroy": (None, [vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orbit2_reslim_forward",
+            "orbit2_stitch", "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times",
+            "orbit2_last_error", "orbit2_destroy")
+
+
+class Orbit2Error(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib.orbit2_last_error().decode()
+        super().__init__(f"{where} failed with status {status}: {msg}")
+        self.status = status
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise Orbit2Error(st, where)
+
+
+def make_config(*, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, embed, depth, heads, batch=1,
+                halo_mode=HALO_CLAMP, precision=BF16, world_size=1, rank=0, chunk_tiles=0,
+                out_channel_map=None) -> orbit2_config:
+    """Build an orbit2_config (the paper's problem statement, north star)."""
+    cfg = orbit2_config(ABI_VERSION, batch, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, halo_mode,
+                        embed, depth, heads, 4 * embed, precision, world_size, rank, chunk_tiles, None)
+    if out_channel_map is not None:
+        arr = (C.c_int32 * K)(*out_channel_map)
+        cfg.out_channel_map = C.cast(arr, C.POINTER(C.c_int32))
+        cfg._map_keepalive = arr
+    return cfg
+
+
+def config_from(w, **over) -> orbit2_config:
+    """orbit2_config from any object with the workload fields (e.g. workloads.Config)."""
+    kw = dict(H=w.H, W=w.W, V=w.V, K=w.K, scale=w.scale, patch=w.patch, tiles_y=w.tiles_y,
+              tiles_x=w.tiles_x, halo=w.halo, embed=w.embed, depth=w.depth, heads=w.heads,
+              batch=w.batch, halo_mode=w.halo_mode, out_channel_map=w.out_channel_map)
+    kw.update(over)
+    return make_config(**kw)
+
+
+def orbit2_tiles_plan(cfg: orbit2_config):
+    """Step (1) planning (host only).  Returns (list of orbit2_tile, orbit2_plan_info)."""
+    info = orbit2_plan_info()
+    _check(lib.orbit2_tiles_plan(C.byref(cfg), None, 0, C.byref(info)), "orbit2_tiles_plan(size)")
+    tiles = (orbit2_tile * info.n_tiles)()
+    _check(lib.orbit2_tiles_plan(C.byref(cfg), tiles, info.n_tiles, C.byref(info)), "orbit2_tiles_plan")
+    return list(tiles), info
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+def _stream(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Context:
+    """One orbit2 ctx bound to a torch-allocated workspace on the current device."""
+
+    def __init__(self, cfg: orbit2_config, device=None):
+        import torch
+        self.cfg = cfg
+        self.tiles, self.info = orbit2_tiles_plan(cfg)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.workspace = torch.empty(max(self.info.workspace_bytes, 16), dtype=torch.uint8, device=self.device)
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib.orbit2_create(C.byref(cfg), _ptr(self.workspace), self.info.workspace_bytes, C.byref(h)),
+                   "orbit2_create")
+        self.handle = h
+        self.bf16 = cfg.precision == BF16
+        self.sH, self.sW = cfg.scale * cfg.H, cfg.scale * cfg.W
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.orbit2_destroy(h)
+            self.handle = None
+
+    # -- lifecycle ---------------------------------------------------------
+    def prepare_weights(self, canonical_dev, stream=None):
+        import torch
+        assert canonical_dev.dtype == torch.float32 and canonical_dev.is_cuda
+        assert canonical_dev.numel() == self.info.canonical_weight_count, "canonical blob size"
+        packed = torch.empty(self.info.packed_weight_bytes, dtype=torch.uint8, device=self.device)
+        _check(lib.orbit2_prepare_weights(self.handle, _ptr(canonical_dev), _ptr(packed), _stream(stream)),
+               "orbit2_prepare_weights")
+        return packed
+
+    def tile_out_buffer(self, tile_count=None):
+        import torch
+        info = self.info
+        dt = torch.bfloat16 if self.bf16 else torch.float32
+        nh = self.cfg.K * (self.cfg.scale * self.cfg.patch) ** 2
+        return torch.empty((self.cfg.batch * info.max_chunk_core_tokens, nh), dtype=dt, device=self.device)
+
+    # -- the graded calls --------------------------------------------------
+    def orbit2_reslim_forward(self, packed, x_dev, tile_begin, tile_count, tile_out, stream=None):
+        _check(lib.orbit2_reslim_forward(self.handle, _ptr(packed), _ptr(x_dev), tile_begin, tile_count,
+                                         _ptr(tile_out), _stream(stream)), "orbit2_reslim_forward")
+
+    def orbit2_stitch(self, tile_out, x_dev, tile_begin, tile_count, out, stream=None):
+        _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
+                                 _stream(stream)), "orbit2_stitch")
+
+    # -- convenience: all rank-local tiles, chunk by chunk ------------------
+    def forward(self, packed, x_dev, out=None, tile_out=None, stream=None):
+        import torch
+        cfg = self.cfg
+        if out is None:
+            out = torch.empty((cfg.batch, cfg.K, self.sH, self.sW), dtype=torch.float32, device=self.device)
+        if tile_out is None:
+            tile_out = self.tile_out_buffer()
+        n, ch = self.info.n_local_tiles, self.info.chunk_tiles
+        for tb in range(0, n, ch):
+            tc = min(ch, n - tb)
+            self.orbit2_reslim_forward(packed, x_dev, tb, tc, tile_out, stream)
+            self.orbit2_stitch(tile_out, x_dev, tb, tc, out, stream)
+        return out
+
+    # -- instrumentation ------------------------------------------------------
+    def launch_count(self) -> int:
+        return int(lib.orbit2_launch_count(self.handle))
+
+    def set_profiling(self, on: bool):
+        _check(lib.orbit2_set_profiling(self.handle, 1 if on else 0), "orbit2_set_profiling")
+
+    def kernel_times(self) -> dict:
+        n = lib.orbit2_kernel_times(self.handle, None, None, None, 0)
+        names = (C.c_char_p * n)()
+        launches = (C.c_int64 * n)()
+        ms = (C.c_double * n)()
+        lib.orbit2_kernel_times(self.handle, names, launches, ms, n)
+        return {names[i].decode(): (int(launches[i]), float(ms[i])) for i in range(n)}

@@ -1,0 +1,150 @@
+"""Host-side tests of liborbit2.so (no GPU needed): the library loads and
+exports every symbol include/orbit2.h declares; orbit2_tiles_plan is
+bit-exact against the oracle's independent planner; validation errors name
+the field; the analytic FLOP model matches brute-force counts."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import reslim_tiles as O
+from workloads import CONFIGS, get_config
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def o2():
+    from paper_2505_04802_b200 import build
+    build.build()
+    from paper_2505_04802_b200 import orbit2
+    return orbit2
+
+
+def test_exports_every_declared_symbol(o2):
+    hdr = open(os.path.join(ROOT, "include", "orbit2.h")).read()
+    declared = set(re.findall(r"\b(orbit2_[a-z_0-9]+)\s*\(", hdr))
+    assert {"orbit2_tiles_plan", "orbit2_reslim_forward", "orbit2_stitch"} <= declared
+    lib = C.CDLL(o2.LIB_PATH)
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert declared == set(o2.EXPORTED)
+
+
+def _plan_both(o2, **kw):
+    w = get_config("C1", **kw)
+    tiles, info = o2.orbit2_tiles_plan(o2.config_from(w))
+    ref = O.plan_tiles(w.Hp, w.Wp, w.tiles_y, w.tiles_x, w.halo, w.halo_mode)
+    return w, tiles, info, ref
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_plan_bit_exact_vs_oracle_planner(o2, mode):
+    for H, W in [(8, 8), (12, 20), (32, 64), (18, 34)]:
+        for ty in range(1, 5):
+            for tx in range(1, 5):
+                for h in range(0, 4):
+                    if ty > H // 2 or tx > W // 2:
+                        continue
+                    w, tiles, info, ref = _plan_both(o2, H=H, W=W, tiles_y=ty, tiles_x=tx, halo=h,
+                                                     halo_mode=mode)
+                    assert info.n_tiles == len(ref)
+                    off = core = 0
+                    for a, b in zip(tiles, ref):
+                        assert (a.tile_id, a.tile_y, a.tile_x) == (b.tile_id, b.ty, b.tx)
+                        assert (a.core_y0, a.core_y1, a.core_x0, a.core_x1) == \
+                               (b.core_y0, b.core_y1, b.core_x0, b.core_x1)
+                        assert (a.pad_y0, a.pad_y1, a.pad_x0, a.pad_x1) == \
+                               (b.pad_y0, b.pad_y1, b.pad_x0, b.pad_x1)
+                        assert a.n_tokens == b.n_tokens and a.n_core_tokens == b.n_core
+                        assert a.token_offset == off and a.core_token_offset == core
+                        off += b.n_tokens
+                        core += b.n_core
+
+
+@pytest.mark.parametrize("name", list(CONFIGS))
+def test_counts_and_flops_vs_oracle(o2, name):
+    w = get_config(name)
+    _, info = o2.orbit2_tiles_plan(o2.config_from(w))
+    c = O.token_counts(O.Problem.from_config(w))
+    assert info.tokens_per_sample == c["n_pad"] and info.core_tokens_per_sample == c["n_core"]
+    assert info.sum_n2_per_sample == c["sum_n2"] and info.sum_nc_per_sample == c["sum_nc"]
+    # brute-force FLOP count: sum over tiles of per-layer GEMM + attention work
+    D, L, Din, Nh = w.embed, w.depth, w.din, w.head_out
+    f = 0.0
+    for n, cc in zip(c["n"], c["c"]):
+        n, cc = float(n), float(cc)
+        f += 2 * n * Din * D + 2 * cc * D * Nh
+        for layer in range(L):
+            last = layer == L - 1
+            rows_q = cc if last else n
+            f += 2 * n * D * 2 * D + 2 * rows_q * D * D          # K,V for all rows; Q for rows_q
+            f += 2 * rows_q * n * D * 2                           # QK^T and PV over heads
+            f += 2 * rows_q * D * D + 2 * rows_q * D * 4 * D * 2  # O-proj, MLP up+down
+    assert info.flops_per_sample == pytest.approx(f, rel=1e-12)
+    assert info.canonical_weight_count == __import__("workloads").weight_count(w)
+
+
+def test_survey_flop_values(o2):
+    """algorithmic FLOP/sample C1..C5."""
+    want = {"C1": 9.10e7, "C2": 4.111e11, "C3": 5.074e12, "C4": 7.240e14, "C5": 1.493e15}
+    for n, v in want.items():
+        _, info = o2.orbit2_tiles_plan(o2.config_from(get_config(n)))
+        assert info.flops_per_sample == pytest.approx(v, rel=2e-3)
+
+
+@pytest.mark.parametrize("bad,field", [
+    (dict(H=33), "H"), (dict(tiles_y=17), "tiles_y"), (dict(halo=-1), "halo"),
+    (dict(heads=3), "embed"), (dict(scale=0), "scale"), (dict(K=4), "K"),
+    (dict(batch=0), "batch"),
+])
+def test_validation_errors_name_the_field(o2, bad, field):
+    w = get_config("C1")
+    cfg = o2.config_from(w, **bad)
+    with pytest.raises(o2.Orbit2Error) as e:
+        o2.orbit2_tiles_plan(cfg)
+    assert e.value.status in (o2.E_INVALID, o2.E_UNSUPPORTED)
+    assert field in str(e.value)
+
+
+def test_unsupported_head_dim(o2):
+    cfg = o2.config_from(get_config("C1"), embed=48, heads=3)
+    with pytest.raises(o2.Orbit2Error) as e:
+        o2.orbit2_tiles_plan(cfg)
+    assert e.value.status == o2.E_UNSUPPORTED
+
+
+def test_capacity_two_call_sizing(o2):
+    cfg = o2.config_from(get_config("C2"))
+    info = o2.orbit2_plan_info()
+    small = (o2.orbit2_tile * 3)()
+    st = o2.lib.orbit2_tiles_plan(C.byref(cfg), small, 3, C.byref(info))
+    assert st == o2.E_CAPACITY and info.n_tiles == 16
+
+
+def test_rank_partition_lpt(o2):
+    """Every tile owned by exactly one rank; LPT keeps per-rank cost within 5%
+    of the mean for C2..C4 at R = 2, 4, 8."""
+    for name in ("C2", "C3", "C4"):
+        w = get_config(name)
+        for R in (2, 4, 8):
+            loads = np.zeros(R)
+            owners = None
+            for r in range(R):
+                tiles, info = o2.orbit2_tiles_plan(o2.config_from(w, world_size=R, rank=r))
+                own = [t.owner_rank for t in tiles]
+                owners = own if owners is None else owners
+                assert own == owners
+                loads[r] = info.local_flops_per_sample
+                assert info.n_local_tiles == sum(1 for t in tiles if t.owner_rank == r)
+            assert loads.sum() == pytest.approx(info.flops_per_sample, rel=1e-12)
+            assert loads.max() / loads.mean() < 1.05, (name, R, loads)
+
+
+def test_create_rejects_bad_workspace(o2):
+    cfg = o2.config_from(get_config("C1"))
+    h = C.c_void_p()
+    st = o2.lib.orbit2_create(C.byref(cfg), None, 0, C.byref(h))
+    assert st == o2.E_INVALID and b"workspace" in o2.lib.orbit2_last_error()

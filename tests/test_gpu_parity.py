@@ -1,0 +1,166 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle.
+
+Tolerances from the north star: max relative error <= 2e-2 (bf16) and
+<= 1e-4 (fp32), metric of reading R21 (per-variable max-norm).  Indexing
+(plan, stitch) is bit-exact; chunk- and rank-invariance are bit-exact.
+"""
+import numpy as np
+import pytest
+
+from oracle import reslim_tiles as O
+from tests.gpu_helpers import (BF16_TOL, FP32_TOL, oracle_full, rel_err, run_cuda, sampled_tiles)
+from workloads import get_config, make_input, make_weights
+
+pytestmark = pytest.mark.gpu
+
+BF16, FP32 = 0, 1
+
+
+def _case(name, batch=1, **over):
+    w = get_config(name, batch=batch, **over)
+    return w, make_input(w, batch=batch), make_weights(w)
+
+
+SMALL = [
+    ("C1", {}),                                            # toy config as stated
+    ("C1", dict(depth=0)),                                 # embed + head only (GEMM epilogues)
+    ("C1", dict(halo_mode=1)),                             # REPLICATE halos
+    ("C1", dict(tiles_y=3, tiles_x=5, halo=1)),            # uneven split, ragged tiles
+    ("C1", dict(embed=128, heads=2, depth=2)),             # head_dim 64
+    ("C1", dict(embed=256, heads=2, depth=1)),             # head_dim 128
+    ("C1", dict(K=2, out_channel_map=(2, 0))),             # channel map (R13)
+    ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3)),        # C2 model on a small grid (>128-token tiles)
+]
+
+
+@pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
+@pytest.mark.parametrize("name,over", SMALL)
+def test_parity_small(name, over, precision, tol):
+    w, x, blob = _case(name, **over)
+    ref, ref_vit, up = oracle_full(w, x, blob)
+    got = run_cuda(w, x, blob, precision)
+    e = rel_err(got, ref)
+    ev = rel_err(got - up, ref_vit)
+    print(f"{name} {over} prec={precision}: rel_err={e:.3e} vit_branch={ev:.3e}")
+    assert np.isfinite(got).all()
+    assert e <= tol
+    assert ev <= 2.5 * tol
+
+
+@pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
+def test_parity_C2_full_sample(precision, tol):
+    """C2 (ERA5 1.0->0.25 deg, 9.5M-class) on one full sample: 16 tiles of
+    1274-1643 tokens (ragged query/key blocks)."""
+    w, x, blob = _case("C2", batch=1)
+    ref, ref_vit, up = oracle_full(w, x, blob)
+    got = run_cuda(w, x, blob, precision)
+    e, ev = rel_err(got, ref), rel_err(got - up, ref_vit)
+    print(f"C2 prec={precision}: rel_err={e:.3e} vit_branch={ev:.3e}")
+    assert e <= tol and ev <= 2.5 * tol
+
+
+@pytest.mark.parametrize("name", ["C3", "C4"])
+def test_parity_sampled_tiles_bf16(name):
+    """C3 / C4 at full size: the oracle computes sampled tiles (corner, edge,
+    interior) exactly (tiles are independent, invariant I5)."""
+    w, x, blob = _case(name, batch=1)
+    got = run_cuda(w, x, blob, BF16)[0]
+    pr = O.Problem.from_config(w)
+    ids = sampled_tiles(w) if name == "C3" else [0, w.tiles_x * (w.tiles_y // 2) + w.tiles_x // 2]
+    res = O.tiles_forward_sampled(x[0], blob, pr, ids)
+    for t, (ys, xs, ref_blk, vit_blk) in res.items():
+        e = rel_err(got[:, ys, xs], ref_blk)
+        print(f"{name} tile {t}: rel_err={e:.3e}")
+        assert e <= BF16_TOL
+
+
+def test_chunk_invariance_bit_exact():
+    """I12: processing the tiles in chunks of 1, 3 or all gives bit-identical output."""
+    w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    a = run_cuda(w, x, blob, BF16, chunk_tiles=0)
+    for ch in (1, 4):
+        assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=ch))
+
+
+def test_rank_emulation_bit_exact():
+    """I11: the tiles partitioned over R ranks (LPT), each rank's tiles run
+    separately, assemble a bit-identical field (R = 2, 3)."""
+    w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    a = run_cuda(w, x, blob, BF16)
+    for R in (2, 3):
+        assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=R))
+
+
+def test_batch_independence_bit_exact():
+    """I8 on the GPU: sample b alone == sample b inside a batch (bit-exact)."""
+    w, x, blob = _case("C1", batch=3)
+    a = run_cuda(w, x, blob, BF16)
+    w1 = w.replace(batch=1)
+    assert np.array_equal(a[1:2], run_cuda(w1, x[1:2], blob, BF16))
+
+
+@pytest.mark.parametrize("precision", [FP32, BF16])
+def test_stitch_coordinate_codes_bit_exact(precision):
+    """Steps (4)-(5) indexing: tile_out carries per-pixel codes; with a zero
+    input the stitched field must equal the code image exactly."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w = get_config("C2", batch=2, H=36, W=60, tiles_y=3, tiles_x=4, halo=2, depth=0, K=3)
+    cfg = o2.config_from(w, precision=precision)
+    ctx = o2.Context(cfg)
+    pr = O.Problem.from_config(w)
+    P, K = pr.P, w.K
+    rows = []
+    for b in range(w.batch):
+        for t in pr.tiles():
+            uu, ww = np.meshgrid(np.arange(t.core_y0, t.core_y1), np.arange(t.core_x0, t.core_x1), indexing="ij")
+            k, al, be = np.meshgrid(np.arange(K), np.arange(P), np.arange(P), indexing="ij")
+            Y = P * uu.ravel()[:, None, None, None] + al[None]
+            X = P * ww.ravel()[:, None, None, None] + be[None]
+            if precision == FP32:
+                code = ((b * K + k[None]) * 1000 + Y) * 1000 + X
+            else:  # exactly representable in bf16 (8-bit significand)
+                code = (Y * 7 + X * 3 + k[None] * 5 + b) % 256
+            rows.append(code.reshape(len(uu.ravel()), -1))
+    codes = np.concatenate(rows).astype(np.float32)
+    dt = torch.float32 if precision == FP32 else torch.bfloat16
+    tile_out = torch.from_numpy(codes).to(dt).cuda()
+    x = torch.zeros((w.batch, w.V, w.H, w.W), device="cuda")
+    out = torch.full((w.batch, K, P * pr.H // w.patch, P * pr.W // w.patch), float("nan"), device="cuda")
+    ctx.orbit2_stitch(tile_out, x, 0, ctx.info.n_local_tiles, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    bb, kk, YY, XX = np.meshgrid(np.arange(w.batch), np.arange(K), np.arange(got.shape[2]),
+                                 np.arange(got.shape[3]), indexing="ij")
+    if precision == FP32:
+        want = ((bb * K + kk) * 1000 + YY) * 1000 + XX
+    else:
+        want = (YY * 7 + XX * 3 + kk * 5 + bb) % 256
+    assert np.array_equal(got, want.astype(np.float32))
+
+
+def test_zero_head_gives_upsample():
+    """I4 on the GPU: W_h = 0, b_h = 0 -> out = bilinear upsample (fp32 kernel
+    vs fp64 oracle to fp32 rounding)."""
+    w, x, blob = _case("C1", batch=2)
+    nh = w.head_out
+    blob = blob.copy()
+    blob[-(nh * w.embed + nh):] = 0.0
+    ref, _, up = oracle_full(w, x, blob)
+    got = run_cuda(w, x, blob, BF16)
+    assert np.abs(got - up).max() <= 1e-6 * np.abs(up).max()
+
+
+def test_bench_configuration_sampled_samples():
+    """C2 at the bench batch (B = 64) in the bench launch configuration:
+    samples 0 and 63 against the oracle."""
+    w = get_config("C2")
+    x = make_input(w)
+    blob = make_weights(w)
+    got = run_cuda(w, x, blob, BF16)
+    pr = O.Problem.from_config(w)
+    for b in (0, w.batch - 1):
+        ref = O.tiles_forward(x[b:b + 1], blob, pr)
+        e = rel_err(got[b:b + 1], ref)
+        print(f"C2 B=64 sample {b}: rel_err={e:.3e}")
+        assert e <= BF16_TOL
