@@ -330,6 +330,12 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
                           p.max_pad_h, st);
       return true;
     }));
+    // Key/value blocks of the last tile may read up to 127 rows past M: keep
+    // them finite (their probabilities are 0, but 0 * NaN would poison P.V).
+    if (mrow > M) {
+      cudaError_t e = cudaMemsetAsync(qkv + M * 3 * D, 0, (size_t)(mrow - M) * 3 * D * sizeof(bf16), st);
+      if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+    }
     ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
