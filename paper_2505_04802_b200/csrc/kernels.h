@@ -40,7 +40,9 @@ struct ChunkDev {
   int32_t tb, tc;
   int64_t tok0, core0, chunk_tokens, chunk_core;
   int32_t qb0, nqb;
+  int32_t qp0, nqp;
   const int32_t* qblk_tile;
+  const int32_t* qpair_tile;
   const int32_t* core_row;
 };
 

@@ -113,7 +113,10 @@ ChunkDev chunk_dev(const Ctx* c, const Chunk& ch) {
   d.chunk_core = ch.chunk_core;
   d.qb0 = ch.qb0;
   d.nqb = ch.nqb;
+  d.qp0 = ch.qp0;
+  d.nqp = ch.nqp;
   d.qblk_tile = c->at<int32_t>(p.lay.qblk_tile);
+  d.qpair_tile = c->at<int32_t>(p.lay.qpair_tile);
   d.core_row = c->at<int32_t>(p.lay.core_row);
   return d;
 }
@@ -179,6 +182,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qblk_tile), p.qblk_tile.data(), p.qblk_tile.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.qpair_tile.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.qpair_tile), p.qpair_tile.data(), p.qpair_tile.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.core_row.empty())
     e = cudaMemcpy(c->at<void>(p.lay.core_row), p.core_row.data(), p.core_row.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)

@@ -22,7 +22,7 @@ struct DevTile {
   int32_t core_y0, core_x0, core_h, core_w;  // core rect (patch units)
   int32_t n_tokens, n_core;
   int32_t qb_off;                             // first query block (local numbering)
-  int32_t pad_;
+  int32_t qp_off;                             // first query-block PAIR (local numbering)
   int64_t tok_off;                            // token offset in local packing (one sample)
   int64_t core_off;                           // core-token offset in local packing
 };
@@ -35,12 +35,13 @@ struct Chunk {
   int64_t chunk_tokens;       // tokens per sample in this chunk
   int64_t chunk_core;         // core tokens per sample in this chunk
   int32_t qb0, nqb;           // query blocks (per sample) of the chunk
+  int32_t qp0, nqp;           // query-block pairs (per sample) of the chunk
 };
 
 // Byte offsets of the workspace regions (from the workspace base).
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
-  int64_t tiles, qblk_tile, core_row, pos_u, pos_w, cmap;
+  int64_t tiles, qblk_tile, qpair_tile, core_row, pos_u, pos_w, cmap;
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;
@@ -54,6 +55,7 @@ struct Plan {
   std::vector<int32_t> local;           // tile ids owned by cfg.rank, increasing
   std::vector<DevTile> dev;             // rank-local device table
   std::vector<int32_t> qblk_tile;       // local q-block -> local tile index
+  std::vector<int32_t> qpair_tile;      // local q-block pair -> local tile index
   std::vector<int32_t> core_row;        // local core token -> local padded token index
   orbit2_plan_info info;
   Layout lay;

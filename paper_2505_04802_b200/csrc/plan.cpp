@@ -149,7 +149,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
 
   // ---- rank-local device tables ----
   int64_t ltok = 0, lcore = 0;
-  int32_t qb = 0;
+  int32_t qb = 0, qp = 0;
   p.max_pad_h = 0;
   p.max_core_h = 0;
   for (int32_t li = 0; li < (int32_t)p.local.size(); ++li) {
@@ -161,9 +161,12 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     dt.core_h = t.core_y1 - t.core_y0; dt.core_w = t.core_x1 - t.core_x0;
     dt.n_tokens = t.n_tokens; dt.n_core = t.n_core_tokens;
     dt.qb_off = qb;
+    dt.qp_off = qp;
     dt.tok_off = ltok; dt.core_off = lcore;
     int32_t nqb = (t.n_tokens + kQBlock - 1) / kQBlock;
     for (int32_t q = 0; q < nqb; ++q) p.qblk_tile.push_back(li);
+    const int32_t nqp = (nqb + 1) / 2;
+    for (int32_t q = 0; q < nqp; ++q) p.qpair_tile.push_back(li);
     for (int32_t u = 0; u < dt.core_h; ++u)
       for (int32_t w = 0; w < dt.core_w; ++w)
         p.core_row.push_back((int32_t)(ltok + (int64_t)(u + dt.core_y0 - dt.pad_y0) * dt.pad_w +
@@ -171,6 +174,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     p.max_pad_h = std::max(p.max_pad_h, dt.pad_h);
     p.max_core_h = std::max(p.max_core_h, dt.core_h);
     qb += nqb;
+    qp += nqp;
     ltok += t.n_tokens;
     lcore += t.n_core_tokens;
     p.dev.push_back(dt);
@@ -178,7 +182,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   // sentinel entry (offsets one past the end) simplifies chunk arithmetic
   {
     DevTile end{};
-    end.qb_off = qb; end.tok_off = ltok; end.core_off = lcore;
+    end.qb_off = qb; end.qp_off = qp; end.tok_off = ltok; end.core_off = lcore;
     p.dev.push_back(end);
   }
 
@@ -250,6 +254,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.hin = take(ly.mcore * (int64_t)p.D * E);
   ly.tiles = take((int64_t)p.dev.size() * sizeof(DevTile));
   ly.qblk_tile = take((int64_t)p.qblk_tile.size() * 4);
+  ly.qpair_tile = take((int64_t)p.qpair_tile.size() * 4);
   ly.core_row = take((int64_t)p.core_row.size() * 4);
   ly.pos_u = take((int64_t)(p.Hp + 2 * h) * (p.D / 2) * 4);
   ly.pos_w = take((int64_t)(p.Wp + 2 * h) * (p.D / 2) * 4);
@@ -273,6 +278,8 @@ Chunk make_chunk(const Plan& p, int32_t tb, int32_t tc) {
   ch.chunk_core = p.dev[tb + tc].core_off - ch.core0;
   ch.qb0 = p.dev[tb].qb_off;
   ch.nqb = p.dev[tb + tc].qb_off - ch.qb0;
+  ch.qp0 = p.dev[tb].qp_off;
+  ch.nqp = p.dev[tb + tc].qp_off - ch.qp0;
   return ch;
 }
 
