@@ -49,12 +49,13 @@ struct AttnCfg {
   static constexpr int ATOM = 128 * RB;               // bytes per atom
   static constexpr int TILE = 128 * DH * 2;           // bytes of a Q/K/V block
   static constexpr uint32_t SW = DH == 32 ? tc::SW_64B : tc::SW_128B;
-  static constexpr int KVST = DH == 128 ? 1 : 2;      // keeps DH=128 within 227 KB
+  static constexpr int KVST = DH == 128 ? 1 : 3;   // K/V ring depth (3 measured = 4 > 2)
   static constexpr int P_BYTES = 128 * 128 * 2;
   static constexpr int THREADS = 128 + 128 * NQ;
   static constexpr int TCOLS = 128 + DH;              // TMEM columns per Q tile: S | O
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
-  static constexpr int SMEM = NQ * TILE + 2 * KVST * TILE + NQ * P_BYTES + 1024 + 512;
+  static constexpr int PBUF = DH == 32 ? 2 : 1;       // P buffers per Q tile (smem: DH=64 192 KB)
+  static constexpr int SMEM = NQ * TILE + 2 * KVST * TILE + NQ * PBUF * P_BYTES + 1024 + 512;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -72,16 +73,16 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sQ = smem;                               // [NQ][TILE]
   uint8_t* sK = sQ + NQ * C::TILE;                  // [KVST][TILE]
   uint8_t* sV = sK + C::KVST * C::TILE;             // [KVST][TILE]
-  uint8_t* sP = sV + C::KVST * C::TILE;             // [NQ][P_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NQ * C::P_BYTES);
+  uint8_t* sP = sV + C::KVST * C::TILE;             // [NQ][PBUF][P_BYTES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NQ * C::PBUF * C::P_BYTES);
   uint64_t* q_full = bar;                           // 1
   uint64_t* kv_full = q_full + 1;                   // [KVST]
   uint64_t* kv_empty = kv_full + C::KVST;           // [KVST]
   uint64_t* s_full = kv_empty + C::KVST;            // [NQ]  S_j in TMEM
   uint64_t* s_free = s_full + NQ;                   // [NQ]  softmax has S_j in registers
   uint64_t* p_full = s_free + NQ;                   // [NQ]  P_j in smem (+ O rescaled)
-  uint64_t* o_done = p_full + NQ;                   // [NQ]  PV_j accumulated into O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + NQ);
+  uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done reading P buffer (and O updated)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p_free + NQ * C::PBUF);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = ch.qp0 + blockIdx.x;
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       tc::mbar_init(&s_full[s], 1);
       tc::mbar_init(&s_free[s], 128);
       tc::mbar_init(&p_full[s], 128);
-      tc::mbar_init(&o_done[s], 1);
+      for (int u = 0; u < C::PBUF; ++u) tc::mbar_init(&p_free[s * C::PBUF + u], 1);
     }
     tc::fence_barrier_init();
   }
@@ -160,12 +161,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {   // 128 keys, K = 16 per MMA
-          const uint64_t pd =
-              tc::sdesc(p_addr + qt * C::P_BYTES + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, tc::SW_128B);
+          const uint64_t pd = tc::sdesc(p_addr + (qt * C::PBUF + j % C::PBUF) * C::P_BYTES + (kk >> 2) * 16384 +
+                                            (kk & 3) * 32, 16, 1024, tc::SW_128B);
           const uint64_t vd = tc::sdesc(v_addr + st * C::TILE + kk * 16 * C::RB, C::ATOM, 8 * C::RB, C::SW);
           tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd, vd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::mma_commit(&o_done[qt]);
+        tc::mma_commit(&p_free[qt * C::PBUF + j % C::PBUF]);
       };
       tc::mbar_wait(q_full, 0);
       tc::mbar_wait(&kv_full[0], 0);
@@ -193,7 +194,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     const uint32_t o_addr = s_addr + 128;
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     float m_ref = -INFINITY, l_run = 0.f;
-    uint8_t* prow = sP + qt * C::P_BYTES + i * 128;
+    uint64_t* my_p_free = p_free + qt * C::PBUF;
     const int sw = i & 7;
 
     for (int j = 0; j < nkb; ++j) {
@@ -222,16 +223,17 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         m2 = fmaxf(m2, sv[c + 2]); m3 = fmaxf(m3, sv[c + 3]);
       }
       const float m_blk = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl;
-      if (j > 0) {                                 // PV_{j-1} done: P buffer free, O complete
-        tc::mbar_wait(&o_done[qt], (j - 1) & 1);
-        tc::tc_fence_after();
-      }
+      // PV_{j-PBUF} has released this P buffer (PV_{j-1} too when PBUF == 1)
+      if (j >= C::PBUF) tc::mbar_wait(&my_p_free[j % C::PBUF], ((j / C::PBUF) - 1) & 1);
       // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
       // (rows whose max did not move get alpha = 1).
       const bool rescaled = j > 0 && __any_sync(0xffffffffu, m_blk > m_ref + kRescaleLog2);
       if (j == 0 || rescaled) {
         const float m_new = fmaxf(m_blk, m_ref);
         if (rescaled) {
+          // O must hold PV_{j-1} before it is rescaled
+          tc::mbar_wait(&my_p_free[(j - 1) % C::PBUF], ((j - 1) / C::PBUF) & 1);
+          tc::tc_fence_after();
           const float alpha = ex2(m_ref - m_new);
           l_run *= alpha;
 #pragma unroll
@@ -247,6 +249,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         m_ref = m_new;
       }
       // probabilities -> bf16 P_j (SW128 K-major), row sum in fp32
+      uint8_t* prow = sP + (qt * C::PBUF + j % C::PBUF) * C::P_BYTES + i * 128;
       float rs0 = 0.f, rs1 = 0.f;
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 16) {
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       tc::mbar_arrive(&p_full[qt]);
     }
     // epilogue: O / l for this row of the head's output
-    tc::mbar_wait(&o_done[qt], (nkb - 1) & 1);
+    tc::mbar_wait(&my_p_free[(nkb - 1) % C::PBUF], ((nkb - 1) / C::PBUF) & 1);
     tc::tc_fence_after();
     const int qrow = q0 + qt * 128 + i;
     const float inv = 1.f / l_run;

@@ -5,17 +5,19 @@
 // with the epilogue fused: bias, exact-erf GELU (R9), fp32 residual add, or
 // the embedding epilogue (bias + resolution embedding + sincos position, R7/R8).
 //
-// Structure (one 128 x BN output tile per CTA, warp-specialised):
+// Structure (persistent, one CTA per SM, warp-specialised):
 //   warp 0 lane 0 : TMA producer, STAGES-deep smem ring (SWIZZLE_128B, BK = 64)
 //   warp 1 lane 0 : tcgen05.mma issuer (M=128, N=BN, K=16 per instruction),
-//                   accumulator in TMEM (BN fp32 columns)
+//                   accumulator in TMEM, double-buffered (2 x BN fp32 columns)
 //   warp 2        : TMEM allocator
-//   warps 4-7     : epilogue, tcgen05.ld 32x32b -> registers -> fused op -> global
+//   warps 4-11    : epilogue (2 warpgroups, one per column half), tcgen05.ld
+//                   32x32b -> registers -> fused op -> global
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "kernels.h"
@@ -143,25 +145,31 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 }
 
 template <int BN, int STAGES, int EPI, bool OUT_BF16>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
                    int K, EpiParams ep) {
+  // Persistent: CTA c owns output tiles c, c + gridDim.x, ... (m-major, n
+  // fastest so consecutive CTAs share the A block through L2).  The TMA ring
+  // runs continuously across tiles; the fp32 accumulator is double-buffered
+  // in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of
+  // tile i+1.
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
-  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  constexpr uint32_t TMEM_COLS = 2 * BN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* accf = empty + STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+  uint64_t* tfull = empty + STAGES;    // [2] accumulator ready
+  uint64_t* tempty = tfull + 2;        // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
   const int nk = K / BK;
+  const int num_n = (ep.N + BN - 1) / BN;
+  const int64_t num_tiles = ((M + BM - 1) / BM) * num_n;
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
@@ -170,7 +178,10 @@ __global__ void __launch_bounds__(256, 1)
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(accf, 1);
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(&tfull[s], 1);
+      tc::mbar_init(&tempty[s], 256);
+    }
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -179,46 +190,71 @@ __global__ void __launch_bounds__(256, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer ----------------
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      tc::mbar_wait(&empty[s], ph ^ 1);
-      tc::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-      tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, (int32_t)m0);
-      tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, n0);
-    }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t ph = (kb / STAGES) & 1;
-      tc::mbar_wait(&full[s], ph);
-      tc::tc_fence_after();
-      const uint32_t a0 = tc::smem_u32(sA + s * A_BYTES), b0 = tc::smem_u32(sB + s * B_BYTES);
-#pragma unroll
-      for (int kk = 0; kk < BK / 16; ++kk) {
-        const uint64_t ad = tc::sdesc(a0 + kk * 32, 16, 1024, tc::SW_128B);
-        const uint64_t bd = tc::sdesc(b0 + kk * 32, 16, 1024, tc::SW_128B);
-        tc::mma_bf16_ss(tmem, ad, bd, idesc, (kb | kk) != 0);
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      uint32_t it = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int32_t m0 = (int32_t)((tile / num_n) * BM), n0 = (int32_t)((tile % num_n) * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          tc::mbar_wait(&empty[s], ph ^ 1);
+          tc::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, m0);
+          tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, n0);
+        }
       }
-      tc::mma_commit(&empty[s]);
     }
-    tc::mma_commit(accf);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+      uint32_t it = 0, lt = 0;
+      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+        const uint32_t buf = lt & 1;
+        tc::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
+        tc::tc_fence_after();
+        const uint32_t acc = tmem + buf * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
+          tc::mbar_wait(&full[s], ph);
+          tc::tc_fence_after();
+          const uint32_t a0 = tc::smem_u32(sA + s * A_BYTES), b0 = tc::smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t ad = tc::sdesc(a0 + kk * 32, 16, 1024, tc::SW_128B);
+            const uint64_t bd = tc::sdesc(b0 + kk * 32, 16, 1024, tc::SW_128B);
+            tc::mma_bf16_ss(acc, ad, bd, idesc, (kb | kk) != 0);
+          }
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&tfull[buf]);
+      }
+    }
   } else if (warp >= 4) {
-    // ---------------- epilogue ----------------
-    const int q = warp - 4;
-    tc::mbar_wait(accf, 0);
-    tc::tc_fence_after();
-    const int64_t row = m0 + q * 32 + lane;
+    // ---------------- epilogue: 2 warpgroups, each half of the columns ----------------
+    const int q = warp & 3;                  // TMEM lane quarter of this warp
+    const int half = (warp - 4) >> 2;        // column half
+    uint32_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+      const uint32_t buf = lt & 1;
+      const int64_t m0 = (tile / num_n) * BM;
+      const int n0 = (int)((tile % num_n) * BN);
+      tc::mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc::tc_fence_after();
+      const int64_t row = m0 + q * 32 + lane;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + c0, r);
-      tc::tmem_ld_wait();
-      if (row < M && n0 + c0 < ep.N) epilogue_chunk<EPI, OUT_BF16>(ep, row, n0 + c0, r);
+      for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(taddr + c0, r);
+        tc::tmem_ld_wait();
+        if (c0 + 32 >= (half + 1) * (BN / 2)) {   // my half read: hand the buffer back
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[buf]);
+        }
+        if (row < M && n0 + c0 < ep.N) epilogue_chunk<EPI, OUT_BF16>(ep, row, n0 + c0, r);
+      }
     }
   }
   tc::tc_fence_before();
@@ -227,6 +263,17 @@ __global__ void __launch_bounds__(256, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int BN, int STAGES, int EPI, bool OUT_BF16>
@@ -242,8 +289,9 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
     attr_set = true;
   }
-  dim3 grid((unsigned)((M + BM - 1) / BM), (unsigned)((N + BN - 1) / BN));
-  kern<<<grid, 256, smem, st>>>(ta, tb, M, (int)K, ep);
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  kern<<<grid, 384, smem, st>>>(ta, tb, M, (int)K, ep);
   return true;
 }
 
@@ -252,17 +300,28 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
 bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
                     int64_t K, const EpiParams& ep, cudaStream_t st) {
   if (K % BK != 0 || M <= 0 || N <= 0) return false;
-  constexpr int BN = 128, ST = 3;
-  switch (epi) {
-    case EPI_BIAS:
-      return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
-                      : launch_impl<BN, ST, EPI_BIAS, false>(A, Bw, M, N, K, ep, st);
-    case EPI_GELU:
-      return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
-    case EPI_RESID:
-      return launch_impl<BN, ST, EPI_RESID, false>(A, Bw, M, N, K, ep, st);
-    case EPI_EMBED:
-      return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
+  // BN = 256 halves the shared-memory operand traffic per FLOP; 128 when N is
+  // not a multiple of 256 (e.g. the decoder head, K*P*P = 192).
+  if (N % 256 == 0) {
+    constexpr int BN = 256, ST = 4;
+    switch (epi) {
+      case EPI_BIAS:
+        return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
+                        : launch_impl<BN, ST, EPI_BIAS, false>(A, Bw, M, N, K, ep, st);
+      case EPI_GELU: return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
+      case EPI_RESID: return launch_impl<BN, ST, EPI_RESID, false>(A, Bw, M, N, K, ep, st);
+      case EPI_EMBED: return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
+    }
+  } else {
+    constexpr int BN = 128, ST = 6;
+    switch (epi) {
+      case EPI_BIAS:
+        return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
+                        : launch_impl<BN, ST, EPI_BIAS, false>(A, Bw, M, N, K, ep, st);
+      case EPI_GELU: return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
+      case EPI_RESID: return launch_impl<BN, ST, EPI_RESID, false>(A, Bw, M, N, K, ep, st);
+      case EPI_EMBED: return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
+    }
   }
   return false;
 }
