@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--set", action="append", default=[], metavar="FIELD=INT",
+                    help="override a workload field (experiments only, e.g. --set tiles_y=2)")
     return ap.parse_args()
 
 
@@ -392,6 +394,9 @@ def main():
     w = get_config(args.config)
     if args.batch:
         w = w.replace(batch=args.batch)
+    for kv in args.set:
+        k, v = kv.split("=")
+        w = w.replace(**{k: int(v)})
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, w, int(os.environ.get("WORLD_SIZE", "1")), rank)

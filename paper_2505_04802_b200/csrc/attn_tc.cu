@@ -8,7 +8,8 @@
 //
 // One CTA handles NQ = 2 query blocks of the same (tile, head, sample) and
 // shares every K/V block between them (FA4-style ping-pong of two Q tiles):
-//   warp 0 lane 0 : TMA producer (Q tiles once; K_j, V_j into a 2-stage ring)
+//   warp 0 lane 0 : TMA producer (Q tiles once; K_j and V_j into separate 2-slot
+//                   rings, issued in consumption order K_{j+1} before V_j)
 //   warp 1 lane 0 : tcgen05.mma issuer, per Q tile t:
 //                     S_j = Q_t K_j^T -> TMEM buffer (t, j&1)   [128 x 128 fp32]
 //                     O_j = P_j V_j   -> same TMEM buffer        [128 x d   fp32]
@@ -49,13 +50,14 @@ struct AttnCfg {
   static constexpr int ATOM = 128 * RB;               // bytes per atom
   static constexpr int TILE = 128 * DH * 2;           // bytes of a Q/K/V block
   static constexpr uint32_t SW = DH == 32 ? tc::SW_64B : tc::SW_128B;
-  static constexpr int KVST = DH == 128 ? 1 : 3;   // K/V ring depth (3 measured = 4 > 2)
+  static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
+  static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
   static constexpr int THREADS = 128 + 128 * NQ;
   static constexpr int TCOLS = 128 + DH;              // TMEM columns per Q tile: S | O
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
-  static constexpr int PBUF = DH == 32 ? 2 : 1;       // P buffers per Q tile (smem: DH=64 192 KB)
-  static constexpr int SMEM = NQ * TILE + 2 * KVST * TILE + NQ * PBUF * P_BYTES + 1024 + 512;
+  static constexpr int PBUF = DH == 128 ? 1 : 2;      // P buffers per Q tile (DH=64: 224 KB smem)
+  static constexpr int SMEM = NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_BYTES + 1024 + 512;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -71,14 +73,16 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;                               // [NQ][TILE]
-  uint8_t* sK = sQ + NQ * C::TILE;                  // [KVST][TILE]
-  uint8_t* sV = sK + C::KVST * C::TILE;             // [KVST][TILE]
-  uint8_t* sP = sV + C::KVST * C::TILE;             // [NQ][PBUF][P_BYTES]
+  uint8_t* sK = sQ + NQ * C::TILE;                  // [KST][TILE]
+  uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
+  uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NQ * C::PBUF * C::P_BYTES);
   uint64_t* q_full = bar;                           // 1
-  uint64_t* kv_full = q_full + 1;                   // [KVST]
-  uint64_t* kv_empty = kv_full + C::KVST;           // [KVST]
-  uint64_t* s_full = kv_empty + C::KVST;            // [NQ]  S_j in TMEM
+  uint64_t* k_full = q_full + 1;                    // [KST]
+  uint64_t* k_empty = k_full + C::KST;              // [KST]
+  uint64_t* v_full = k_empty + C::KST;              // [VST]
+  uint64_t* v_empty = v_full + C::VST;              // [VST]
+  uint64_t* s_full = v_empty + C::VST;              // [NQ]  S_j in TMEM
   uint64_t* s_free = s_full + NQ;                   // [NQ]  softmax has S_j in registers
   uint64_t* p_full = s_free + NQ;                   // [NQ]  P_j in smem (+ O rescaled)
   uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done reading P buffer (and O updated)
@@ -98,9 +102,13 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tm);
     tc::mbar_init(q_full, 1);
-    for (int s = 0; s < C::KVST; ++s) {
-      tc::mbar_init(&kv_full[s], 1);
-      tc::mbar_init(&kv_empty[s], 1);
+    for (int s = 0; s < C::KST; ++s) {
+      tc::mbar_init(&k_full[s], 1);
+      tc::mbar_init(&k_empty[s], 1);
+    }
+    for (int s = 0; s < C::VST; ++s) {
+      tc::mbar_init(&v_full[s], 1);
+      tc::mbar_init(&v_empty[s], 1);
     }
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
@@ -124,15 +132,26 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       for (int qt = 0; qt < nq; ++qt)
         for (int a = 0; a < C::NA; ++a)
           tc::tma_load_2d(&tm, sQ + qt * C::TILE + a * C::ATOM, q_full, h * DH + a * C::AC, y0 + q0 + qt * 128);
-      for (int j = 0; j < nkb; ++j) {
-        const int st = j % C::KVST;
-        tc::mbar_wait(&kv_empty[st], ((j / C::KVST) & 1) ^ 1);
-        tc::mbar_arrive_expect_tx(&kv_full[st], 2 * C::TILE);
-        for (int a = 0; a < C::NA; ++a) {
-          tc::tma_load_2d(&tm, sK + st * C::TILE + a * C::ATOM, &kv_full[st], D + h * DH + a * C::AC, y0 + j * 128);
-          tc::tma_load_2d(&tm, sV + st * C::TILE + a * C::ATOM, &kv_full[st], 2 * D + h * DH + a * C::AC,
+      // issue order = consumption order: K_0, then per j: K_{j+1}, V_j
+      auto load_k = [&](int j) {
+        const int st = j % C::KST;
+        tc::mbar_wait(&k_empty[st], ((j / C::KST) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&k_full[st], C::TILE);
+        for (int a = 0; a < C::NA; ++a)
+          tc::tma_load_2d(&tm, sK + st * C::TILE + a * C::ATOM, &k_full[st], D + h * DH + a * C::AC, y0 + j * 128);
+      };
+      auto load_v = [&](int j) {
+        const int st = j % C::VST;
+        tc::mbar_wait(&v_empty[st], ((j / C::VST) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&v_full[st], C::TILE);
+        for (int a = 0; a < C::NA; ++a)
+          tc::tma_load_2d(&tm, sV + st * C::TILE + a * C::ATOM, &v_full[st], 2 * D + h * DH + a * C::AC,
                           y0 + j * 128);
-        }
+      };
+      load_k(0);
+      for (int j = 0; j < nkb; ++j) {
+        if (j + 1 < nkb) load_k(j + 1);
+        load_v(j);
       }
     }
   } else if (warp == 1) {
@@ -143,7 +162,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const uint32_t p_addr = tc::smem_u32(sP);
       auto issue_s = [&](int j, int qt) {
-        const int st = j % C::KVST;
+        const int st = j % C::KST;
         if (j >= 1) tc::mbar_wait(&s_free[qt], (j - 1) & 1);   // softmax holds S_{j-1} in registers
         tc::tc_fence_after();
 #pragma unroll
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         tc::mma_commit(&s_full[qt]);
       };
       auto issue_pv = [&](int j, int qt) {
-        const int st = j % C::KVST;
+        const int st = j % C::VST;
         tc::mbar_wait(&p_full[qt], j & 1);
         tc::tc_fence_after();
 #pragma unroll
@@ -169,20 +188,18 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         tc::mma_commit(&p_free[qt * C::PBUF + j % C::PBUF]);
       };
       tc::mbar_wait(q_full, 0);
-      tc::mbar_wait(&kv_full[0], 0);
+      tc::mbar_wait(&k_full[0], 0);
       for (int qt = 0; qt < nq; ++qt) issue_s(0, qt);
+      tc::mma_commit(&k_empty[0]);
       for (int j = 0; j < nkb; ++j) {
-        const int st = j % C::KVST;
-        if (C::KVST > 1 && j + 1 < nkb) {   // S_{j+1} overlaps the softmax of block j
-          tc::mbar_wait(&kv_full[(j + 1) % C::KVST], ((j + 1) / C::KVST) & 1);
+        if (j + 1 < nkb) {   // S_{j+1} overlaps the softmax of block j
+          tc::mbar_wait(&k_full[(j + 1) % C::KST], ((j + 1) / C::KST) & 1);
           for (int qt = 0; qt < nq; ++qt) issue_s(j + 1, qt);
+          tc::mma_commit(&k_empty[(j + 1) % C::KST]);
         }
+        tc::mbar_wait(&v_full[j % C::VST], (j / C::VST) & 1);
         for (int qt = 0; qt < nq; ++qt) issue_pv(j, qt);
-        tc::mma_commit(&kv_empty[st]);
-        if (C::KVST == 1 && j + 1 < nkb) {  // single stage: K_{j+1} lands after PV_j
-          tc::mbar_wait(&kv_full[0], (j + 1) & 1);
-          for (int qt = 0; qt < nq; ++qt) issue_s(j + 1, qt);
-        }
+        tc::mma_commit(&v_empty[j % C::VST]);
       }
     }
   } else if (warp >= 4 && (warp - 4) / 4 < nq) {

@@ -63,8 +63,6 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
-
 template <int EPI, bool OUT_BF16>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row, int n0, const uint32_t (&r)[32]) {
   float v[32];
@@ -85,7 +83,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
   }
   if constexpr (EPI == EPI_GELU) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = gelu_erf(v[j]);
+    for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
   }
   if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU) {
     if constexpr (OUT_BF16) {

@@ -73,6 +73,10 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
 bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B,
                          int D, int heads, int d, cudaStream_t st);
 
+// Fused MLP for D = 256: z += W2 GELU(W1 x + b1) + b2 (hidden stays on chip).
+bool launch_mlp_fused(const void* xn, int64_t rows_alloc, const void* w1, const float* b1, const void* w2,
+                      const float* b2, float* z, int64_t M, int D, cudaStream_t st);
+
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();
 

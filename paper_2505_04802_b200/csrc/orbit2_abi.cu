@@ -40,6 +40,7 @@ struct Ctx {
   std::vector<cudaEvent_t> pool;
   std::map<std::string, std::pair<int64_t, double>> acc;
   bool sync_check = false;
+  bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -178,6 +179,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->wl = weight_layout(p);
   const char* sc = std::getenv("ORBIT2_SYNC_CHECK");
   c->sync_check = sc && sc[0] == '1';
+  const char* um = std::getenv("ORBIT2_UNFUSED_MLP");
+  c->unfused_mlp = um && um[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
@@ -360,10 +363,16 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
         launch_layernorm<bf16>(z, wf(L.ln2_g), wf(L.ln2_b), xn, M, (int)D, nullptr, st);
         return true;
       }));
-      e = EpiParams{}; e.bias = wf(L.b_1); e.C = hid; e.ldc = F;
-      ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn, mrow, D, L.w_1, F, D, M, e));
-      e = EpiParams{}; e.bias = wf(L.b_2); e.C = z; e.ldc = D;
-      ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, hid, mrow, F, L.w_2, D, F, M, e));
+      if (D == 256 && !c->unfused_mlp) {   // hidden tile stays on chip
+        ORBIT2_TRY(run(c, "mlp_fused", st, [&] {
+          return launch_mlp_fused(xn, mrow, W8 + L.w_1, wf(L.b_1), W8 + L.w_2, wf(L.b_2), z, M, (int)D, st);
+        }));
+      } else {
+        e = EpiParams{}; e.bias = wf(L.b_1); e.C = hid; e.ldc = F;
+        ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn, mrow, D, L.w_1, F, D, M, e));
+        e = EpiParams{}; e.bias = wf(L.b_2); e.C = z; e.ldc = D;
+        ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, hid, mrow, F, L.w_2, D, F, M, e));
+      }
     }
     ORBIT2_TRY(run(c, "layernorm", st, [&] {
       launch_layernorm<bf16>(z, wf(w.lnf_g), wf(w.lnf_b), hin, Mc, (int)D, &cd, st);
