@@ -83,7 +83,7 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
   }
   if constexpr (EPI == EPI_GELU) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
+    for (int j = 0; j < 32; ++j) v[j] = 0.5f * v[j] * (1.0f + erff(v[j] * 0.70710678118654752f));
   }
   if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU) {
     if constexpr (OUT_BF16) {

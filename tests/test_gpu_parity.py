@@ -74,6 +74,18 @@ def test_parity_sampled_tiles_bf16(name):
         assert e <= BF16_TOL
 
 
+def test_persistent_multi_item_batch():
+    """Persistent kernels with several work items per CTA (B = 8: > 148
+    attention items): first and last sample against the oracle."""
+    w, x, blob = _case("C2", batch=8, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    got = run_cuda(w, x, blob, BF16)
+    pr = O.Problem.from_config(w)
+    for b in (0, 7):
+        e = rel_err(got[b:b + 1], O.tiles_forward(x[b:b + 1], blob, pr))
+        print(f"multi-item sample {b}: rel_err={e:.3e}")
+        assert e <= BF16_TOL
+
+
 def test_chunk_invariance_bit_exact():
     """I12: processing the tiles in chunks of 1, 3 or all gives bit-identical output."""
     w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
