@@ -142,12 +142,15 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
   }
 }
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16>
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS>
 __global__ void __launch_bounds__(384, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int64_t M,
-                   int K, EpiParams ep) {
-  // Persistent: CTA c owns output tiles c, c + gridDim.x, ... (m-major, n
-  // fastest so consecutive CTAs share the A block through L2).  The TMA ring
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmC, int64_t M, int64_t Ncols, int K, EpiParams ep) {
+  // Persistent: CTA c owns output tiles c, c + gridDim.x, ...  Normal mode:
+  // m-major, n fastest (consecutive CTAs share the activation block through
+  // L2).  TRANS mode computes C^T = W X^T (A = weight rows, B = tokens) so the
+  // epilogue's fp32 residual update is coalesced; tiles are token-major.
+  // bf16 outputs leave through shared memory and TMA stores (full lines).  The TMA ring
   // runs continuously across tiles; the fp32 accumulator is double-buffered
   // in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of
   // tile i+1.
@@ -158,20 +161,28 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + 8 * 2 * 2048);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;    // [2] accumulator ready
   uint64_t* tempty = tfull + 2;        // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
   const int nk = K / BK;
-  const int num_n = (ep.N + BN - 1) / BN;
-  const int64_t num_tiles = ((M + BM - 1) / BM) * num_n;
+  const int64_t num_n = (Ncols + BN - 1) / BN;
+  const int64_t num_m = (M + BM - 1) / BM;
+  const int64_t num_tiles = num_m * num_n;
+  auto tile_mn = [&](int64_t tile, int64_t& m0, int64_t& n0) {
+    if (TRANS) { m0 = (tile % num_m) * BM; n0 = (tile / num_m) * BN; }
+    else       { m0 = (tile / num_n) * BM; n0 = (tile % num_n) * BN; }
+  };
+  uint8_t* stg = sB + STAGES * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16)
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
+    if (TMA_OUT) tc::prefetch_tmap(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -193,13 +204,14 @@ __global__ void __launch_bounds__(384, 1)
       // ---------------- TMA producer ----------------
       uint32_t it = 0;
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int32_t m0 = (int32_t)((tile / num_n) * BM), n0 = (int32_t)((tile % num_n) * BN);
+        int64_t m0, n0;
+        tile_mn(tile, m0, n0);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           tc::mbar_wait(&empty[s], ph ^ 1);
           tc::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-          tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, m0);
-          tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, n0);
+          tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, (int32_t)m0);
+          tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, (int32_t)n0);
         }
       }
     }
@@ -233,11 +245,12 @@ __global__ void __launch_bounds__(384, 1)
     // ---------------- epilogue: 2 warpgroups, each half of the columns ----------------
     const int q = warp & 3;                  // TMEM lane quarter of this warp
     const int half = (warp - 4) >> 2;        // column half
-    uint32_t lt = 0;
+    uint8_t* my_stg = stg + (warp - 4) * 2 * 2048;
+    uint32_t lt = 0, nst = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
       const uint32_t buf = lt & 1;
-      const int64_t m0 = (tile / num_n) * BM;
-      const int n0 = (int)((tile % num_n) * BN);
+      int64_t m0, n0;
+      tile_mn(tile, m0, n0);
       tc::mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc::tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
@@ -251,9 +264,69 @@ __global__ void __launch_bounds__(384, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&tempty[buf]);
         }
-        if (row < M && n0 + c0 < ep.N) epilogue_chunk<EPI, OUT_BF16>(ep, row, n0 + c0, r);
+        if constexpr (TRANS) {
+          // rows = output features, columns = tokens: z[t][f] += acc + bias[f]
+          if (row < M) {
+            const float bf = __ldg(ep.bias + row);
+            float* zc = reinterpret_cast<float*>(ep.C) + (n0 + c0) * ep.ldc + row;
+            const int64_t t0 = n0 + c0;
+            if (t0 + 32 <= ep.M) {
+              float zv[32];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) zv[j] = zc[(int64_t)j * ep.ldc];
+#pragma unroll
+              for (int j = 0; j < 32; ++j) zc[(int64_t)j * ep.ldc] = zv[j] + (__uint_as_float(r[j]) + bf);
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (t0 + j < ep.M) zc[(int64_t)j * ep.ldc] += __uint_as_float(r[j]) + bf;
+            }
+          }
+        } else if constexpr (TMA_OUT) {
+          if (n0 + c0 < ep.N) {
+            float v[32];
+            if (n0 + c0 + 32 <= ep.N) {
+              const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c0);
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 bb = __ldg(b4 + j);
+                v[4 * j] = __uint_as_float(r[4 * j]) + bb.x;
+                v[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bb.y;
+                v[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bb.z;
+                v[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bb.w;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                v[j] = __uint_as_float(r[j]) + (n0 + c0 + j < ep.N ? __ldg(ep.bias + n0 + c0 + j) : 0.f);
+            }
+            if constexpr (EPI == EPI_GELU) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
+            }
+            uint8_t* sb = my_stg + (nst & 1) * 2048;
+            if (lane == 0) tc::bulk_wait_read<1>();   // this buffer's previous store has read it
+            __syncwarp();
+            uint8_t* srow = sb + lane * 64;
+            const int sw = (lane >> 1) & 3;           // SWIZZLE_64B pattern of the TMA box
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              *reinterpret_cast<uint4*>(srow + ((u ^ sw) << 4)) =
+                  make_uint4(tc::pack_bf16(v[8 * u], v[8 * u + 1]), tc::pack_bf16(v[8 * u + 2], v[8 * u + 3]),
+                             tc::pack_bf16(v[8 * u + 4], v[8 * u + 5]), tc::pack_bf16(v[8 * u + 6], v[8 * u + 7]));
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+              tc::tma_store_2d(&tmC, sb, (int32_t)(n0 + c0), (int32_t)(m0 + q * 32));
+              tc::bulk_commit();
+            }
+            ++nst;
+          }
+        } else {
+          if (row < M && n0 + c0 < ep.N) epilogue_chunk<EPI, OUT_BF16>(ep, row, (int)(n0 + c0), r);
+        }
       }
     }
+    if (TMA_OUT && lane == 0) tc::bulk_wait_all();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -274,22 +347,33 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16>
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false>
 bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                  cudaStream_t st) {
-  CUtensorMap ta, tb;
-  if (!make_tmap_bf16(&ta, A.ptr, A.rows, K, A.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
-  if (!make_tmap_bf16(&tb, Bw.ptr, Bw.rows, K, Bw.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
-  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16>;
+  // normal: kernel rows = activations A (M), cols = weights Bw (N)
+  // TRANS : kernel rows = weights Bw (N features), cols = activations A (M tokens)
+  const GemmOperand& ka = TRANS ? Bw : A;
+  const GemmOperand& kb = TRANS ? A : Bw;
+  const int64_t Mk = TRANS ? N : M, Nk = TRANS ? M : N;
+  CUtensorMap ta, tb, tcm;
+  if (!make_tmap_bf16(&ta, ka.ptr, ka.rows, K, ka.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
+  if (TMA_OUT) {
+    if (!make_tmap_bf16(&tcm, ep.C, M, N, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
+  } else {
+    tcm = ta;   // unused
+  }
+  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 8 * 2 * 2048 + 1024 + 256;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
     attr_set = true;
   }
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int64_t tiles = ((Mk + BM - 1) / BM) * ((Nk + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  kern<<<grid, 384, smem, st>>>(ta, tb, M, (int)K, ep);
+  kern<<<grid, 384, smem, st>>>(ta, tb, tcm, Mk, Nk, (int)K, ep);
   return true;
 }
 
@@ -298,10 +382,12 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
 bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
                     int64_t K, const EpiParams& ep, cudaStream_t st) {
   if (K % BK != 0 || M <= 0 || N <= 0) return false;
+  // Residual update: transposed tiles (features on TMEM lanes) for coalesced z.
+  if (epi == EPI_RESID && N % BM == 0) return launch_impl<256, 3, EPI_RESID, false, true>(A, Bw, M, N, K, ep, st);
   // BN = 256 halves the shared-memory operand traffic per FLOP; 128 when N is
   // not a multiple of 256 (e.g. the decoder head, K*P*P = 192).
   if (N % 256 == 0) {
-    constexpr int BN = 256, ST = 4;
+    constexpr int BN = 256, ST = 3;
     switch (epi) {
       case EPI_BIAS:
         return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
@@ -311,7 +397,7 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
       case EPI_EMBED: return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
     }
   } else {
-    constexpr int BN = 128, ST = 6;
+    constexpr int BN = 128, ST = 5;
     switch (epi) {
       case EPI_BIAS:
         return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)

@@ -113,6 +113,62 @@ __global__ void layernorm_kernel(const float* __restrict__ z, const float* __res
   }
 }
 
+// Register-resident variant for D = 128 * NV4: the row is read from HBM once
+// (NV4 float4 per lane, coalesced), statistics from registers, one write.
+__device__ __forceinline__ void store4(float* o, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(o) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void store4(__nv_bfloat16* o, float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(o) = u;
+}
+
+template <typename T, int NV4>
+__global__ void layernorm_reg_kernel(const float* __restrict__ z, const float* __restrict__ g,
+                                     const float* __restrict__ bta, T* __restrict__ out, int64_t M, bool compact,
+                                     ChunkDev ch) {
+  constexpr int D = 128 * NV4;
+  const int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x & 31;
+  if (r >= M) return;
+  int64_t src = r;
+  if (compact) {
+    const int64_t b = r / ch.chunk_core, rr = r - b * ch.chunk_core;
+    src = b * ch.chunk_tokens + (ch.core_row[ch.core0 + rr] - ch.tok0);
+  }
+  const float4* zr = reinterpret_cast<const float4*>(z + src * D);
+  float4 v[NV4];
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) v[k] = __ldcs(zr + lane + 32 * k);
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s * (1.0f / D);
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const float a = v[k].x - mean, b2 = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
+    q += (a * a + b2 * b2) + (c * c + e * e);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q * (1.0f / D) + 1e-5f);
+  T* orow = out + r * D;
+#pragma unroll
+  for (int k = 0; k < NV4; ++k) {
+    const int c4 = lane + 32 * k;
+    const float4 gg = __ldg(reinterpret_cast<const float4*>(g) + c4);
+    const float4 bb = __ldg(reinterpret_cast<const float4*>(bta) + c4);
+    store4(orow + 4 * c4, (v[k].x - mean) * rstd * gg.x + bb.x, (v[k].y - mean) * rstd * gg.y + bb.y,
+           (v[k].z - mean) * rstd * gg.z + bb.z, (v[k].w - mean) * rstd * gg.w + bb.w);
+  }
+}
+
 template <typename T>
 void launch_layernorm(const float* z, const float* g, const float* b, T* out, int64_t M, int D,
                       const ChunkDev* compact, cudaStream_t st) {
@@ -120,7 +176,14 @@ void launch_layernorm(const float* z, const float* g, const float* b, T* out, in
   dim3 grid((unsigned)((M + rows_per_cta - 1) / rows_per_cta));
   ChunkDev ch{};
   if (compact) ch = *compact;
-  layernorm_kernel<T><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, D, compact != nullptr, ch);
+  const bool cp = compact != nullptr;
+  switch (D) {
+    case 256: layernorm_reg_kernel<T, 2><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, cp, ch); return;
+    case 512: layernorm_reg_kernel<T, 4><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, cp, ch); return;
+    case 1024: layernorm_reg_kernel<T, 8><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, cp, ch); return;
+    case 2048: layernorm_reg_kernel<T, 16><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, cp, ch); return;
+    default: layernorm_kernel<T><<<grid, 32 * rows_per_cta, 0, st>>>(z, g, b, out, M, D, cp, ch);
+  }
 }
 template void launch_layernorm<float>(const float*, const float*, const float*, float*, int64_t, int,
                                       const ChunkDev*, cudaStream_t);
