@@ -11,7 +11,7 @@
 // Q tiles):
 //   warp 0 lane 0 : TMA producer (Q tiles once; K_j and V_j into separate 2-slot
 //                   rings, issued in consumption order K_{j+1} before V_j)
-//   warp 1 lane 0 : tcgen05.mma issuer, per Q tile t:
+//   warps 1, 3    : tcgen05.mma issuers, one per Q tile t:
 //                     S_j = Q_t K_j^T -> TMEM buffer (t, j&1)   [128 x 128 fp32]
 //                     O_j = P_j V_j   -> same TMEM buffer        [128 x d   fp32]
 //   warp 2        : TMEM allocator (NQ * 256 columns)
@@ -35,13 +35,37 @@ namespace orbit2 {
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                     int box_cols, CUtensorMapSwizzle swz);
 
+long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timeline
+
 namespace {
 
+// volatile: keeps the exponentials after the ping-pong named barrier (a plain
+// asm is hoisted above it by the compiler, which re-collides the two tiles'
+// exp phases on the MUFU)
 __device__ __forceinline__ float ex2(float x) {
   float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x on the FMA pipe (FA4's trick to offload the MUFU): x = j + f with j the
+// nearest integer (1.5*2^23 magic add), 2^f on [-1/2, 1/2] by a degree-3 fit
+// (max relative error 1.0e-4, below bf16's half-ulp 2e-3 that P is rounded to),
+// 2^j by adding j to the exponent field.  x is clamped at -125 (2^-125 ~ 0).
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -125.0f);
+  const float t = x + 12582912.0f;
+  const float f = x - (t - 12582912.0f);
+  const float p = fmaf(fmaf(fmaf(0.05500886f, f, 0.24221101f), f, 0.69328296f), f, 1.0f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+
+// debug timeline: tl[(role * 64 + block) * 8 + event] for CTA 0, first 64 blocks
+#define TL_STAMP(role, blk, ev)                                                          \
+  do {                                                                                   \
+    if (tl != nullptr && blockIdx.x == 0 && (blk) < 64) tl[((role) * 64 + (blk)) * 8 + (ev)] = clock64(); \
+  } while (0)
 
 template <int DH, int NQ>
 struct AttnCfg {
@@ -67,6 +91,7 @@ struct AttnCfg {
 // stay <= 2^8 (exact in bf16's exponent range, fp32 accumulation) and the
 // O rescale in TMEM is rare.  Mathematically identical softmax (R18).
 constexpr float kRescaleLog2 = 8.0f;
+constexpr bool kPolyExp = false;   // FMA-pipe exp2 for 4/16 elements (off: measured slower)
 
 struct Item {
   int64_t base;     // first row of the tile's tokens in the packed workspace
@@ -98,10 +123,12 @@ __device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int64_t
 template <int DH, int NQ>
 __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
-                   int heads, int64_t n_items) {
+                   int heads, int64_t n_items, long long* __restrict__ tl) {
+  // tl: optional debug timeline (clock64 stamps of CTA 0), null in production
   using C = AttnCfg<DH, NQ>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // align inside the __shared__ array (keeps the shared address space: STS, not generic ST)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                               // [QBUF][NQ][TILE]
   uint8_t* sK = sQ + C::QBUF * NQ * C::TILE;        // [KST][TILE]
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
@@ -119,6 +146,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done (P buffer free, O updated)
   uint64_t* o_free = p_free + NQ * C::PBUF;         // [NQ]  epilogue has read O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + NQ);
+  float* zero_slot = reinterpret_cast<float*>(tmem_slot + 1);   // holds 0.0f (see ping-pong)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -126,16 +154,17 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     tc::prefetch_tmap(&tm);
     for (int s = 0; s < C::QBUF; ++s) {
       tc::mbar_init(&q_full[s], 1);
-      tc::mbar_init(&q_empty[s], 1);
+      tc::mbar_init(&q_empty[s], NQ);   // one arrival per MMA-issuer warp
     }
     for (int s = 0; s < C::KST; ++s) {
       tc::mbar_init(&k_full[s], 1);
-      tc::mbar_init(&k_empty[s], 1);
+      tc::mbar_init(&k_empty[s], NQ);
     }
     for (int s = 0; s < C::VST; ++s) {
       tc::mbar_init(&v_full[s], 1);
-      tc::mbar_init(&v_empty[s], 1);
+      tc::mbar_init(&v_empty[s], NQ);
     }
+    *zero_slot = 0.0f;
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
       tc::mbar_init(&s_free[s], 128);
@@ -168,6 +197,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         auto load_k = [&](int j) {
           const uint32_t st = gk % C::KST;
           tc::mbar_wait(&k_empty[st], ((gk / C::KST) & 1) ^ 1);
+          TL_STAMP(4, gk, 0);
           tc::mbar_arrive_expect_tx(&k_full[st], C::TILE);
           for (int a = 0; a < C::NA; ++a)
             tc::tma_load_2d(&tm, sK + st * C::TILE + a * C::ATOM, &k_full[st], D + it.h * DH + a * C::AC,
@@ -177,6 +207,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         auto load_v = [&](int j) {
           const uint32_t st = gv % C::VST;
           tc::mbar_wait(&v_empty[st], ((gv / C::VST) & 1) ^ 1);
+          TL_STAMP(4, gv, 1);
           tc::mbar_arrive_expect_tx(&v_full[st], C::TILE);
           for (int a = 0; a < C::NA; ++a)
             tc::tma_load_2d(&tm, sV + st * C::TILE + a * C::ATOM, &v_full[st], 2 * D + it.h * DH + a * C::AC,
@@ -191,65 +222,89 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+  } else if (warp == 1 || warp == 3) {
+    {   // whole warp runs the loop (uniform descriptors); one elected lane issues
+      // ---------------- MMA issuers: warp 1 -> Q tile 0, warp 3 -> Q tile 1 ----------------
+      // Each Q tile has its own issuing thread so the two softmax warpgroups
+      // are not forced into lockstep (their exp phases then alternate on the
+      // MUFU instead of colliding).  Shared Q/K/V slots are released by one
+      // arrival per issuer; an issuer whose tile is idle for a work item still
+      // walks the ring phases (wait full, arrive empty) to stay aligned.
+      const int qt = warp == 1 ? 0 : 1;
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
       constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);    // P K-major, V MN-major
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const uint32_t p_addr = tc::smem_u32(sP);
-      uint32_t li = 0, gk = 0, gv = 0;
-      uint32_t ns[NQ], np[NQ], ni[NQ];   // per Q tile: S issued, PV issued, items finished
-#pragma unroll
-      for (int qt = 0; qt < NQ; ++qt) ns[qt] = np[qt] = ni[qt] = 0;
+      uint32_t li = 0, gk = 0, gv = 0, ns = 0, np = 0, ni = 0;
       for (int64_t id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
         const Item it = item_info<NQ>(ch, heads, id);
+        const bool active = qt < it.nq;
         const uint32_t qb = li % C::QBUF;
         tc::mbar_wait(&q_full[qb], (li / C::QBUF) & 1);
-        auto issue_s_all = [&](bool last) {   // S = Q K_j^T for every active Q tile
+        auto issue_s = [&](bool last) {   // S = Q K_j^T for this Q tile
           const uint32_t st = gk % C::KST;
           tc::mbar_wait(&k_full[st], (gk / C::KST) & 1);
-          for (int qt = 0; qt < it.nq; ++qt) {
-            if (ns[qt] >= 1) tc::mbar_wait(&s_free[qt], (ns[qt] - 1) & 1);
+          if (lane == 0) TL_STAMP(2 + qt, ns, 0);
+          if (active) {
+            if (ns >= 1) tc::mbar_wait(&s_free[qt], (ns - 1) & 1);
+            if (lane == 0) TL_STAMP(2 + qt, ns, 1);
             tc::tc_fence_after();
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < DH / 16; ++kk) {
-              const int a = (kk * 16) / C::AC, off = ((kk * 16) % C::AC) * 2;
-              const uint64_t qd =
-                  tc::sdesc(q_addr + (qb * NQ + qt) * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
-              const uint64_t kd = tc::sdesc(k_addr + st * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
-              tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd, kd, id_s, kk > 0);
+              for (int kk = 0; kk < DH / 16; ++kk) {
+                const int a = (kk * 16) / C::AC, off = ((kk * 16) % C::AC) * 2;
+                const uint64_t qd =
+                    tc::sdesc(q_addr + (qb * NQ + qt) * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
+                const uint64_t kd = tc::sdesc(k_addr + st * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
+                tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd, kd, id_s, kk > 0);
+              }
+              tc::mma_commit(&s_full[qt]);
+              tc::mma_commit(&k_empty[st]);
+              if (last) tc::mma_commit(&q_empty[qb]);   // Q buffer free once the item's S MMAs finish
             }
-            tc::mma_commit(&s_full[qt]);
-            ++ns[qt];
+            __syncwarp();
+            ++ns;
+          } else {
+            if (lane == 0) {
+              tc::mbar_arrive(&k_empty[st]);
+              if (last) tc::mbar_arrive(&q_empty[qb]);
+            }
+            __syncwarp();
           }
-          tc::mma_commit(&k_empty[st]);
-          if (last) tc::mma_commit(&q_empty[qb]);   // Q buffer free once the item's S MMAs finish
           ++gk;
         };
-        issue_s_all(it.nkb == 1);
+        issue_s(it.nkb == 1);
         for (int j = 0; j < it.nkb; ++j) {
-          if (j + 1 < it.nkb) issue_s_all(j + 2 == it.nkb);   // S_{j+1} overlaps softmax of block j
+          if (j + 1 < it.nkb) issue_s(j + 2 == it.nkb);   // S_{j+1} overlaps softmax of block j
           const uint32_t st = gv % C::VST;
           tc::mbar_wait(&v_full[st], (gv / C::VST) & 1);
-          for (int qt = 0; qt < it.nq; ++qt) {
-            if (j == 0 && ni[qt] >= 1) tc::mbar_wait(&o_free[qt], (ni[qt] - 1) & 1);
-            tc::mbar_wait(&p_full[qt], np[qt] & 1);
+          if (lane == 0) TL_STAMP(2 + qt, np, 2);
+          if (active) {
+            if (j == 0 && ni >= 1) tc::mbar_wait(&o_free[qt], (ni - 1) & 1);
+            tc::mbar_wait(&p_full[qt], np & 1);
+            if (lane == 0) TL_STAMP(2 + qt, np, 3);
             tc::tc_fence_after();
+            if (tc::elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {   // 128 keys, K = 16 per MMA
-              const uint64_t pd = tc::sdesc(p_addr + (qt * C::PBUF + np[qt] % C::PBUF) * C::P_BYTES +
-                                                (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, tc::SW_128B);
-              const uint64_t vd = tc::sdesc(v_addr + st * C::TILE + kk * 16 * C::RB, C::ATOM, 8 * C::RB, C::SW);
-              tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd, vd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+              for (int kk = 0; kk < 8; ++kk) {   // 128 keys, K = 16 per MMA
+                const uint64_t pd = tc::sdesc(p_addr + (qt * C::PBUF + np % C::PBUF) * C::P_BYTES +
+                                                  (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, tc::SW_128B);
+                const uint64_t vd = tc::sdesc(v_addr + st * C::TILE + kk * 16 * C::RB, C::ATOM, 8 * C::RB, C::SW);
+                tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd, vd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+              }
+              tc::mma_commit(&p_free[qt * C::PBUF + np % C::PBUF]);
+              tc::mma_commit(&v_empty[st]);
+              if (lane == 0) TL_STAMP(2 + qt, np, 4);
             }
-            tc::mma_commit(&p_free[qt * C::PBUF + np[qt] % C::PBUF]);
-            ++np[qt];
+            __syncwarp();
+            ++np;
+          } else {
+            if (lane == 0) tc::mbar_arrive(&v_empty[st]);
+            __syncwarp();
           }
-          tc::mma_commit(&v_empty[st]);
           ++gv;
         }
-        for (int qt = 0; qt < it.nq; ++qt) ++ni[qt];
+        if (active) ++ni;
       }
     }
   } else if (warp >= 4) {
@@ -267,8 +322,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       const Item it = item_info<NQ>(ch, heads, id);
       if (qt >= it.nq) continue;
       float m_ref = -INFINITY, l_run = 0.f;
+      const bool tlr = (warp & 3) == 0 && lane == 0;
       for (int j = 0; j < it.nkb; ++j, ++cs) {
+        if (tlr) TL_STAMP(qt, cs, 0);
         tc::mbar_wait(&s_full[qt], cs & 1);
+        if (tlr) TL_STAMP(qt, cs, 1);
         tc::tc_fence_after();
         float sv[128];
         {
@@ -280,6 +338,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&s_free[qt]);               // TMEM S columns may take the next S
+        if (tlr) TL_STAMP(qt, cs, 2);
         const int kvalid = it.n - j * 128;
         if (kvalid < 128) {
 #pragma unroll
@@ -294,7 +353,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         }
         const float m_blk = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl;
         // PV of block cs-PBUF released this P buffer
+        if (tlr) TL_STAMP(qt, cs, 3);
         if (cs >= (uint32_t)C::PBUF) tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
+        if (tlr) TL_STAMP(qt, cs, 4);
         // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
         // (rows whose max did not move get alpha = 1).
         const bool rescaled = j > 0 && __any_sync(0xffffffffu, m_blk > m_ref + kRescaleLog2);
@@ -317,6 +378,20 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           }
           m_ref = m_new;
         }
+        // Exp phases of the two Q tiles alternate on the MUFU (A_j, B_j, A_{j+1}, ...):
+        // named barrier 1 = "tile 0 may start", 2 = "tile 1 may start".  While one
+        // tile exponentiates, the other loads S and reduces its row maxima.
+        const bool pingpong = it.nq == 2;
+        if (pingpong) {
+          if (qt == 0 && j > 0) asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (qt == 1) asm volatile("bar.sync 2, 256;" ::: "memory");
+        }
+        // Data dependency on a shared-memory load issued after the barrier: the
+        // scheduler otherwise hoists the MUFU work above BAR.SYNC (it only
+        // orders memory operations), re-colliding the two tiles' exp phases.
+        float zero_dep;
+        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(zero_dep) : "r"(tc::smem_u32(zero_slot)) : "memory");
+        const float m_use = m_ref + zero_dep;
         // probabilities -> bf16 P (SW128 K-major), row sum in fp32
         uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_BYTES + i * 128;
         float rs0 = 0.f, rs1 = 0.f;
@@ -325,8 +400,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           uint32_t pk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
-            const float p0 = ex2(fmaf(sv[c0 + e], sl, -m_ref));
-            const float p1 = ex2(fmaf(sv[c0 + e + 1], sl, -m_ref));
+            const float x0 = fmaf(sv[c0 + e], sl, -m_use), x1 = fmaf(sv[c0 + e + 1], sl, -m_use);
+            // all on the MUFU: moving 25% to ex2_poly (FMA pipe) measured slower here,
+            // the exp phase of one warp is issue/latency-bound, not MUFU-bound
+            const float p0 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x0) : ex2(x0);
+            const float p1 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x1) : ex2(x1);
             rs0 += p0;
             rs1 += p1;
             pk[e / 2] = tc::pack_bf16(p0, p1);
@@ -337,10 +415,16 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
         l_run += rs0 + rs1;
+        if (pingpong) {
+          if (qt == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
+          if (qt == 1 && j + 1 < it.nkb) asm volatile("bar.arrive 1, 256;" ::: "memory");
+        }
+        if (tlr) TL_STAMP(qt, cs, 5);
         if (rescaled) tc::tmem_st_wait();
         tc::fence_proxy_async_smem();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
+        if (tlr) TL_STAMP(qt, cs, 6);
       }
       // epilogue: O / l for this row of the head's output, then hand O back
       tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
@@ -399,7 +483,7 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (n_items == 0) return true;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM
   attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
-                                                             heads, n_items);
+                                                             heads, n_items, g_attn_timeline);
   return true;
 }
 

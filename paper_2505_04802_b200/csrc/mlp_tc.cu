@@ -46,8 +46,9 @@ __global__ void __launch_bounds__(384, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW1,
                   const __grid_constant__ CUtensorMap tmW2, const float* __restrict__ b1,
                   const float* __restrict__ b2, float* __restrict__ z, int64_t M) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // align inside the __shared__ array (keeps the shared address space: STS, not generic ST)
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;
   uint8_t* sH = sX + X_BYTES;          // [2][H_BYTES]
   uint8_t* sW = sH + 2 * H_BYTES;      // [RS][SLOT]
@@ -196,7 +197,6 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
     uint32_t tl = 0;
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl) {
-      const int64_t row = tile * BM + r;
       for (int h = 0; h < NCH; ++h) {
         const uint32_t gc = tl * NCH + h, buf = gc & 1, use = gc >> 1;
         tc::mbar_wait(&s_full[buf], use & 1);

@@ -40,7 +40,7 @@ struct Ctx {
   std::vector<cudaEvent_t> pool;
   std::map<std::string, std::pair<int64_t, double>> acc;
   bool sync_check = false;
-  bool unfused_mlp = true;    // ORBIT2_FUSED_MLP=1 selects mlp_fused (D = 256), slower today
+  bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -134,9 +134,15 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
+namespace orbit2 { extern long long* g_attn_timeline; }
+
 extern "C" {
 
 const char* orbit2_last_error(void) { return g_err.c_str(); }
+
+/* Debug only (not in orbit2.h): device buffer of 5*64*8 int64 that the next
+ * attention launches fill with clock64 stamps of CTA 0; NULL disables. */
+void orbit2_debug_attn_timeline(long long* dev_buf) { orbit2::g_attn_timeline = dev_buf; }
 
 orbit2_status orbit2_tiles_plan(const orbit2_config* cfg, orbit2_tile* tiles, int32_t capacity,
                                 orbit2_plan_info* info) {
@@ -179,8 +185,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->wl = weight_layout(p);
   const char* sc = std::getenv("ORBIT2_SYNC_CHECK");
   c->sync_check = sc && sc[0] == '1';
-  const char* fm = std::getenv("ORBIT2_FUSED_MLP");
-  c->unfused_mlp = !(fm && fm[0] == '1');
+  const char* um = std::getenv("ORBIT2_UNFUSED_MLP");
+  c->unfused_mlp = um && um[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
