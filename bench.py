@@ -176,6 +176,28 @@ def class_work(w, info, B):
     return out
 
 
+def attn_bytes(w, info, B):
+    """Algorithmic HBM bytes of one attention launch: read Q,K,V (bf16) once,
+    write the head outputs (bf16) once, over all padded tokens."""
+    return B * info.tokens_per_sample * (3 + 1) * w.embed * 2.0
+
+
+def latest_traffic():
+    """Per-launch DRAM traffic measured by the latest committed ncu capture."""
+    import glob
+    out = {}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic_*.json"))):
+        try:
+            with open(path) as f:
+                for k, v in json.load(f).items():
+                    v = dict(v)
+                    v["source"] = os.path.relpath(path, ROOT)
+                    out[k] = v
+        except Exception:
+            pass
+    return out
+
+
 # ---------------------------------------------------------------------------
 # the oracle as the CPU baseline / reference arm
 # ---------------------------------------------------------------------------
@@ -356,17 +378,26 @@ def run_ours(args, w, world, rank, local):
         bound, amount = work[dom]
         launches_dom = classes[dom]["launches_per_step"]
         per_launch_ms = classes[dom]["ms_per_step"] / launches_dom
+        traffic, traffic_note = None, None
+        tr = latest_traffic().get(dom)
+        if tr:
+            traffic = tr["dram_bytes_per_launch"] * B / tr["batch"]
+            traffic_note = (f"ncu --set full dram read+write of one {dom} launch at batch {tr['batch']} "
+                            f"({tr['source']}), scaled linearly to batch {B}")
         if bound == "tensor":
             achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e12
             peak = pk["bf16_sus"]
             res["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
-                               "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                               "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                               "traffic_note": traffic_note,
+                               "algorithmic_bytes_per_launch": attn_bytes(w, info, B) if dom == "tile_attention" else None,
                                "peak_src": pk["src"] + " bf16_tflops_sustained (kernel timed inside the step)",
                                "frac_of_burst": achieved / pk["bf16"]}
         else:
             achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e9
             res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm"],
-                               "unit": "GB/s", "frac": achieved / pk["hbm"], "traffic": None, "peak_src": pk["src"]}
+                               "unit": "GB/s", "frac": achieved / pk["hbm"], "traffic": traffic,
+                               "traffic_note": traffic_note, "peak_src": pk["src"]}
         att = classes.get("tile_attention")
         if att and "tflops" in att:
             res["attn_tflops"] = att["tflops"]
