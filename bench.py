@@ -38,6 +38,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
+    ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
@@ -176,6 +177,22 @@ def class_work(w, info, B):
     return out
 
 
+def auto_chunk(o2, w, B):
+    """Largest number of tiles per forward/stitch call whose workspace and
+    tile_out, plus the resident input and output fields, fit in 85% of free HBM."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    _, info = o2.orbit2_tiles_plan(o2.config_from(w, batch=B))
+    fixed = info.out_bytes + B * w.V * w.H * w.W * 4 + 4 * o2.orbit2_tiles_plan(o2.config_from(w))[1].canonical_weight_count * 2
+    n = info.n_local_tiles
+    for div in range(1, n + 1):
+        ch = -(-n // div)
+        _, ci = o2.orbit2_tiles_plan(o2.config_from(w, batch=B, chunk_tiles=ch))
+        if fixed + ci.workspace_bytes + ci.tile_out_bytes < 0.85 * free:
+            return 0 if ch >= n else ch
+    raise RuntimeError("workload does not fit one GPU even one tile at a time")
+
+
 def attn_bytes(w, info, B):
     """Algorithmic HBM bytes of one attention launch: read Q,K,V (bf16) once,
     write the head outputs (bf16) once, over all padded tokens."""
@@ -215,8 +232,10 @@ def oracle_units(w, blob, x, seconds_budget=None, n_units=None):
         b, t = divmod(i % (x.shape[0] * len(tiles)), len(tiles))
         tile = tiles[t]
         g = O.tile_forward(x[b], tile, pr, Wt)
-        up = O.residual_up(x[b], pr)   # residual for the sample (the oracle's plain step O7)
-        _ = g.sum() + up.sum()
+        ys = slice(tile.core_y0 * pr.P, tile.core_y1 * pr.P)      # the oracle's step O7 on this tile's
+        xs = slice(tile.core_x0 * pr.P, tile.core_x1 * pr.P)      # output block (stitch is a placement)
+        up = [O.upsample_bilinear_region(x[b][m], pr.scale, ys, xs) for m in pr.cmap()]
+        _ = g.sum() + sum(u.sum() for u in up)
         px += tile.n_core * pr.P * pr.P
         done += 1
         i += 1
@@ -272,7 +291,8 @@ def run_ours(args, w, world, rank, local):
     from workloads import make_input, make_weights
 
     B = w.batch
-    cfg = o2.config_from(w, batch=B, precision=o2.BF16)
+    chunk = args.chunk if args.chunk >= 0 else auto_chunk(o2, w, B)
+    cfg = o2.config_from(w, batch=B, precision=o2.BF16, chunk_tiles=chunk)
     ctx = o2.Context(cfg)
     info = ctx.info
     blob = make_weights(w)
@@ -348,7 +368,8 @@ def run_ours(args, w, world, rank, local):
         "config": {"workload": w.name, "batch_per_gpu": B, "coarse": [w.H, w.W, w.V], "out": [w.scale * w.H,
                    w.scale * w.W, w.K], "tiles": [w.tiles_y, w.tiles_x], "halo": w.halo,
                    "vit": [w.embed, w.depth, w.heads], "parallelism": f"dp{world} (samples sharded, tiles local)",
-                   "l2": "working set > L2 (126 MB) every step; no flush needed"},
+                   "l2": "working set > L2 (126 MB) every step; no flush needed",
+                   "chunk_tiles": info.chunk_tiles},
         "tokens_per_s": world * B * info.tokens_per_sample / (ms * 1e-3),
         "core_tokens_per_s": world * B * info.core_tokens_per_sample / (ms * 1e-3),
         "path_tflops": flops_step / (ms * 1e-3) / 1e12,
@@ -380,7 +401,7 @@ def run_ours(args, w, world, rank, local):
         per_launch_ms = classes[dom]["ms_per_step"] / launches_dom
         traffic, traffic_note = None, None
         tr = latest_traffic().get(dom)
-        if tr:
+        if tr and tr.get("workload") == w.name:
             traffic = tr["dram_bytes_per_launch"] * B / tr["batch"]
             traffic_note = (f"ncu --set full dram read+write of one {dom} launch at batch {tr['batch']} "
                             f"({tr['source']}), scaled linearly to batch {B}")

@@ -240,6 +240,23 @@ def _bilinear_axis(n_in: int, s: int):
     return y0, y1, lam
 
 
+def upsample_bilinear_region(plane: np.ndarray, s: int, ys: slice, xs: slice) -> np.ndarray:
+    """The same O7 formula evaluated only at output rows ys and columns xs
+    (for sampled-tile parity at sizes where the full field does not fit)."""
+    H, W = plane.shape
+    y0, y1, ly = (a[ys] for a in _bilinear_axis(H, s))
+    x0, x1, lx = (a[xs] for a in _bilinear_axis(W, s))
+    ly = ly[:, None]
+    lx = lx[None, :]
+    pr = plane[np.union1d(y0, y1)].astype(np.float64)   # only the rows needed
+    rmap = {r: i for i, r in enumerate(np.union1d(y0, y1))}
+    iy0 = np.array([rmap[r] for r in y0])
+    iy1 = np.array([rmap[r] for r in y1])
+    r0 = (1 - lx) * pr[iy0][:, x0] + lx * pr[iy0][:, x1]
+    r1 = (1 - lx) * pr[iy1][:, x0] + lx * pr[iy1][:, x1]
+    return (1 - ly) * r0 + ly * r1
+
+
 def upsample_bilinear(plane: np.ndarray, s: int) -> np.ndarray:
     """[H,W] -> [sH,sW]:
     up = (1-ly)((1-lx)x[y0,x0] + lx x[y0,x1]) + ly((1-lx)x[y1,x0] + lx x[y1,x1])."""
@@ -370,18 +387,16 @@ def tiles_forward_sampled(x_b: np.ndarray, blob: np.ndarray, pr: Problem, tile_i
     Wt = pr.weights(blob)
     tiles = pr.tiles()
     res = {}
-    up = None
     for t in tile_ids:
         tile = tiles[t]
         g = tile_forward(x_b, tile, pr, Wt)
         ch, cw = tile.core_y1 - tile.core_y0, tile.core_x1 - tile.core_x0
         vit = g.reshape(ch, cw, pr.K, pr.P, pr.P).transpose(2, 0, 3, 1, 4).reshape(
             pr.K, ch * pr.P, cw * pr.P)
-        if up is None:
-            up = residual_up(x_b, pr)
         ys = slice(tile.core_y0 * pr.P, tile.core_y1 * pr.P)
         xs = slice(tile.core_x0 * pr.P, tile.core_x1 * pr.P)
-        res[t] = (ys, xs, vit + up[:, ys, xs], vit)
+        up = np.stack([upsample_bilinear_region(x_b[m], pr.scale, ys, xs) for m in pr.cmap()])
+        res[t] = (ys, xs, vit + up, vit)
     return res
 
 

@@ -74,6 +74,32 @@ def test_parity_sampled_tiles_bf16(name):
         assert e <= BF16_TOL
 
 
+def test_parity_C5_chunked_sampled_tiles():
+    """C5 hyper-resolution (5400 x 10800 x 23 -> 21600 x 43200 x 18, 1296 tiles
+    of ~13k tokens) on one GPU, processed in chunks of 162 tiles (workspace
+    13.5 GB); an interior and a corner tile against the oracle.  Only the
+    sampled output blocks are copied back (the full field is 67 GB)."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w = get_config("C5", batch=1)
+    x = make_input(w, batch=1)
+    blob = make_weights(w)
+    ctx = o2.Context(o2.config_from(w, precision=BF16, chunk_tiles=162))
+    xd = torch.from_numpy(x).cuda()
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    out = torch.empty((1, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
+    ctx.forward(packed, xd, out=out)
+    torch.cuda.synchronize()
+    pr = O.Problem.from_config(w)
+    ids = [w.tiles_x * (w.tiles_y // 2) + w.tiles_x // 2, 0]
+    res = O.tiles_forward_sampled(x[0], blob, pr, ids)
+    for t, (ys, xs, ref_blk, vit_blk) in res.items():
+        got = out[0, :, ys, xs].cpu().numpy()
+        e = rel_err(got, ref_blk)
+        print(f"C5 tile {t}: rel_err={e:.3e}")
+        assert e <= BF16_TOL
+
+
 def test_persistent_multi_item_batch():
     """Persistent kernels with several work items per CTA (B = 8: > 148
     attention items): first and last sample against the oracle."""

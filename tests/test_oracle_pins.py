@@ -233,6 +233,16 @@ def test_bilinear_matches_interpolate(s):
     assert np.array_equal(O.upsample_bilinear(c, s), np.full((5 * s, 6 * s), 2.5))
 
 
+def test_bilinear_region_equals_full_slice():
+    """The region evaluation of O7 (used for sampled C4/C5 parity) is the full
+    upsample restricted to the region, bit for bit."""
+    x = np.random.default_rng(6).standard_normal((9, 13))
+    for s in (2, 4, 8):
+        full = O.upsample_bilinear(x, s)
+        for ys, xs in [(slice(0, 5), slice(3, 17)), (slice(7, 9 * s), slice(0, 13 * s)), (slice(11, 12), slice(5, 6))]:
+            assert np.array_equal(O.upsample_bilinear_region(x, s, ys, xs), full[ys, xs])
+
+
 # ---------------------------------------------------------------- O6 stitch
 def test_stitch_coordinate_codes():
     """every core token's head output lands at its own output pixels.
