@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_04802_b200 import orbit2 as o2  # noqa: E402
 from workloads import get_config, make_input, make_weights  # noqa: E402
 
-w = get_config("C2", batch=16)
+w = get_config(sys.argv[1] if len(sys.argv) > 1 else "C2", batch=int(sys.argv[2]) if len(sys.argv) > 2 else 16)
 ctx = o2.Context(o2.config_from(w))
 x = torch.from_numpy(make_input(w)).cuda()
 packed = ctx.prepare_weights(torch.from_numpy(make_weights(w)).cuda())
@@ -30,7 +30,7 @@ ev = {0: "loop,s_full_done,s_loaded,max_done,pfree_done,exp_done,p_arrive",
       4: "k_empty_done,v_empty_done"}
 for role in range(5):
     print(f"== {names[role]}: {ev.get(role if role in (0, 2, 4) else role - 1, '')}")
-    for b in range(24):
+    for b in range(40):
         row = t[role, b]
         if (row > 0).any():
             print(f"  blk {b:2d}: " + " ".join(f"{(v - t0):8d}" if v > 0 else "       -" for v in row[:7]))
