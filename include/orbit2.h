@@ -195,6 +195,51 @@ orbit2_status orbit2_reslim_forward(void *ctx, const void *packed_w, const float
 orbit2_status orbit2_stitch(void *ctx, const void *tile_out_dev, const float *input_dev,
                             int32_t tile_begin, int32_t tile_count, float *out_dev, void *stream);
 
+/*
+ * ---- TILES sequence parallelism across ranks ("assigning each tile to a
+ * separate GPU"; "stitched together") ----
+ * With world_size = R > 1 each rank computes its LPT-assigned tiles.  Data
+ * movement between ranks is expressed as lists of coarse-pixel rectangles
+ * (all B samples, all V channels) that the library packs into / unpacks from a
+ * contiguous fp32 buffer; the caller moves the buffers (e.g. NCCL send/recv
+ * over NVLink).  Message layout: rectangle by rectangle, each [B][V][rows][cols].
+ *
+ *   ORBIT2_XFER_HALO : halo exchange.  send = pixels of `peer`'s padded tile
+ *                      rectangles that lie in this rank's owned cores; recv =
+ *                      pixels of this rank's padded rectangles owned by `peer`.
+ *   ORBIT2_XFER_CORES: input gather to a root.  send = this rank's owned core
+ *                      pixels (peer = root); recv (at root) = `peer`'s owned cores.
+ * Owned cores: the core rectangles (pixels) of the rank's tiles; they partition
+ * the grid.  In CLAMP mode padded rectangles are clipped to the grid; in
+ * REPLICATE mode the clamped (edge) pixels are what the gather reads.
+ */
+typedef struct { int32_t y0, y1, x0, x1; } orbit2_rect;   /* coarse pixels, half-open */
+enum { ORBIT2_XFER_HALO = 0, ORBIT2_XFER_CORES = 1 };
+enum { ORBIT2_SEND = 0, ORBIT2_RECV = 1 };
+
+/* Host-only, pure: the rectangles and the element count (B*V*sum of areas) of
+ * one transfer of cfg->rank with `peer` (peer != rank).  rects may be NULL with
+ * cap = 0 (sizing); n_rects receives the count either way; E_CAPACITY if cap
+ * is too small. */
+orbit2_status orbit2_xfer_plan(const orbit2_config *cfg, int32_t kind, int32_t peer, int32_t direction,
+                               orbit2_rect *rects, int32_t cap, int32_t *n_rects, int64_t *n_elems);
+
+/* Pack this rank's SEND rectangles for (kind, peer) from input_dev [B][V][H][W]
+ * into buf_dev, or scatter a received buffer into input_dev (RECV rectangles).
+ * Stream-ordered; buf_dev holds n_elems floats. */
+orbit2_status orbit2_xfer_pack(void *ctx, int32_t kind, int32_t peer, const float *input_dev, float *buf_dev,
+                               void *stream);
+orbit2_status orbit2_xfer_unpack(void *ctx, int32_t kind, int32_t peer, const float *buf_dev, float *input_dev,
+                                 void *stream);
+
+/* Output gather: stitch (steps 4-5, as orbit2_stitch) ALL tiles of rank `peer`
+ * from tile_out_dev laid out as that rank's [B][its core tokens, plan order]
+ * [K*P*P] (i.e. the tile_out of one orbit2_reslim_forward over all of peer's
+ * tiles), reading the residual from input_dev (valid over peer's cores + 1
+ * coarse pixel) into out_dev.  peer may equal cfg->rank. */
+orbit2_status orbit2_stitch_peer(void *ctx, int32_t peer, const void *tile_out_dev, const float *input_dev,
+                                 float *out_dev, void *stream);
+
 /* Number of kernels the library launched on this ctx so far. */
 int64_t orbit2_launch_count(void *ctx);
 

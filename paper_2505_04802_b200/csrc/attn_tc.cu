@@ -358,7 +358,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         if (tlr) TL_STAMP(qt, cs, 4);
         // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
         // (rows whose max did not move get alpha = 1).
-        const bool rescaled = j > 0 && __any_sync(0xffffffffu, m_blk > m_ref + kRescaleLog2);
+        // Only rows inside the tile vote: rows past its end hold the next tile's (or
+        // stale) tokens, which must not change the valid rows' rounding (keeps the
+        // result independent of packing, chunking and rank assignment).
+        const bool row_valid = it.q0 + qt * 128 + i < it.n;
+        const bool rescaled = j > 0 && __any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2);
         if (j == 0 || rescaled) {
           const float m_new = fmaxf(m_blk, m_ref);
           if (rescaled) {   // O must hold PV_{j-1} (block cs-1) before it is rescaled

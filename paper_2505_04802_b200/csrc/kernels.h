@@ -60,6 +60,8 @@ void launch_sgemm(int epi, const float* A, int64_t lda, const float* Bw, int64_t
                   int64_t K, const EpiParams& ep, cudaStream_t st);
 void launch_attention_f32(const float* qkv, float* out, const ChunkDev& ch, int B, int D, int heads, int d,
                           cudaStream_t st);
+void launch_xfer(const DevRect* rects, int count, int B, int V, int H, int W, const float* src, float* dst, int pack,
+                 cudaStream_t st);
 void launch_pos_tables(float* pos_u, float* pos_w, int Hp, int Wp, int h, int D, cudaStream_t st);
 void launch_convert_rows(const float* src, void* dst, int64_t rows, int64_t cols, int64_t ld_dst, int to_bf16,
                          cudaStream_t st);

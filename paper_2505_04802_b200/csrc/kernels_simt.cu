@@ -243,6 +243,32 @@ template void launch_stitch<__nv_bfloat16>(const __nv_bfloat16*, const float*, f
                                            const int32_t*, int, int, int, int, int, int, int, int, cudaStream_t);
 
 // ---------------------------------------------------------------------------
+// Rank-to-rank transfers (halo exchange / input gather): pack the rectangles of
+// a [B][V][H][W] field into a contiguous message (rect by rect, [B][V][rows][cols])
+// or scatter a message back.  One CTA per (rectangle, b*V + v); coalesced rows.
+// ---------------------------------------------------------------------------
+__global__ void xfer_kernel(const DevRect* __restrict__ rects, int H, int W, const float* __restrict__ src,
+                            float* __restrict__ dst, int pack) {
+  const DevRect r = rects[blockIdx.x];
+  const int bv = blockIdx.y;
+  const int rows = r.y1 - r.y0, cols = r.x1 - r.x0;
+  const int64_t msg = r.off + (int64_t)bv * rows * cols;
+  const int64_t fld = ((int64_t)bv * H + r.y0) * W + r.x0;
+  for (int idx = threadIdx.x; idx < rows * cols; idx += blockDim.x) {
+    const int y = idx / cols, x = idx - y * cols;
+    if (pack) dst[msg + idx] = __ldg(src + fld + (int64_t)y * W + x);
+    else dst[fld + (int64_t)y * W + x] = __ldg(src + msg + idx);
+  }
+}
+
+void launch_xfer(const DevRect* rects, int count, int B, int V, int H, int W, const float* src, float* dst, int pack,
+                 cudaStream_t st) {
+  if (count == 0) return;
+  dim3 grid(count, B * V);
+  xfer_kernel<<<grid, 256, 0, st>>>(rects, H, W, src, dst, pack);
+}
+
+// ---------------------------------------------------------------------------
 // One-time tables: sincos position rows (R7), computed in fp64 then rounded.
 // pos_u[r][m] = sin(u om_m), pos_u[r][Q+m] = cos(u om_m), u = r - h, Q = D/4.
 // ---------------------------------------------------------------------------

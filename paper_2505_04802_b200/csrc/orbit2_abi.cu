@@ -198,6 +198,14 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   if (e == cudaSuccess)
     e = cudaMemcpy(c->at<void>(p.lay.cmap), p.cmap.data(), p.cmap.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) {
+    std::vector<DevTile> all;
+    for (auto& v : p.dev_by_rank) all.insert(all.end(), v.begin(), v.end());
+    if (!all.empty())
+      e = cudaMemcpy(c->at<void>(p.lay.peer_tiles), all.data(), all.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess && !p.rects.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.rects), p.rects.data(), p.rects.size() * sizeof(DevRect), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
     launch_pos_tables(c->at<float>(p.lay.pos_u), c->at<float>(p.lay.pos_w), p.Hp, p.Wp, p.cfg.halo, p.D, 0);
     c->launches += 2;
     e = cudaGetLastError();
@@ -442,6 +450,86 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
     ORBIT2_TRY(sg("head_gemm", EPI_BIAS, hin, D, w.w_h, p.Nh, D, Mc, e));
   }
   return ORBIT2_OK;
+}
+
+orbit2_status orbit2_xfer_plan(const orbit2_config* cfg, int32_t kind, int32_t peer, int32_t direction,
+                               orbit2_rect* rects, int32_t cap, int32_t* n_rects, int64_t* n_elems) {
+  Plan p;
+  std::string msg;
+  orbit2_status st = build_plan(cfg, &p, &msg);
+  if (st != ORBIT2_OK) return set_err(st, msg);
+  if (kind != ORBIT2_XFER_HALO && kind != ORBIT2_XFER_CORES) return set_err(ORBIT2_E_INVALID, "kind: unknown transfer");
+  if (direction != ORBIT2_SEND && direction != ORBIT2_RECV) return set_err(ORBIT2_E_INVALID, "direction: unknown");
+  if (peer < 0 || peer >= cfg->world_size || peer == cfg->rank)
+    return set_err(ORBIT2_E_INVALID, "peer: must be another rank in [0, world_size)");
+  std::vector<orbit2_rect> rs;
+  xfer_rects(p, kind, cfg->rank, peer, direction, &rs);
+  int64_t e = 0;
+  for (const orbit2_rect& r : rs) e += (int64_t)cfg->batch * cfg->V * (r.y1 - r.y0) * (r.x1 - r.x0);
+  if (n_rects) *n_rects = (int32_t)rs.size();
+  if (n_elems) *n_elems = e;
+  if (rects == nullptr && cap == 0) return ORBIT2_OK;
+  if (cap < (int32_t)rs.size()) return set_err(ORBIT2_E_CAPACITY, "cap: smaller than the rectangle count");
+  if (!rects) return set_err(ORBIT2_E_INVALID, "rects: null with cap > 0");
+  std::memcpy(rects, rs.data(), rs.size() * sizeof(orbit2_rect));
+  return ORBIT2_OK;
+}
+
+static orbit2_status xfer(void* ctx, int32_t kind, int32_t peer, const float* src, float* dst, int pack, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  const Plan& p = c->plan;
+  if (kind != ORBIT2_XFER_HALO && kind != ORBIT2_XFER_CORES) return set_err(ORBIT2_E_INVALID, "kind: unknown transfer");
+  if (peer < 0 || peer >= p.cfg.world_size || peer == p.cfg.rank)
+    return set_err(ORBIT2_E_INVALID, "peer: must be another rank in [0, world_size)");
+  if (!src || !dst) return set_err(ORBIT2_E_INVALID, "input_dev/buf_dev: null");
+  const XferList& xl = p.xfer[((size_t)kind * p.cfg.world_size + peer) * 2 + (pack ? ORBIT2_SEND : ORBIT2_RECV)];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return run(c, pack ? "xfer_pack" : "xfer_unpack", st, [&] {
+    launch_xfer(c->at<DevRect>(p.lay.rects) + xl.start, xl.count, p.cfg.batch, p.cfg.V, p.cfg.H, p.cfg.W, src, dst,
+                pack, st);
+    return true;
+  });
+}
+
+orbit2_status orbit2_xfer_pack(void* ctx, int32_t kind, int32_t peer, const float* input_dev, float* buf_dev,
+                               void* stream) {
+  return xfer(ctx, kind, peer, input_dev, buf_dev, 1, stream);
+}
+
+orbit2_status orbit2_xfer_unpack(void* ctx, int32_t kind, int32_t peer, const float* buf_dev, float* input_dev,
+                                 void* stream) {
+  return xfer(ctx, kind, peer, buf_dev, input_dev, 0, stream);
+}
+
+orbit2_status orbit2_stitch_peer(void* ctx, int32_t peer, const void* tile_out_dev, const float* input_dev,
+                                 float* out_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  if (peer < 0 || peer >= cf.world_size) return set_err(ORBIT2_E_INVALID, "peer: outside [0, world_size)");
+  if (!tile_out_dev || !input_dev || !out_dev || !aligned16(tile_out_dev) || !aligned16(input_dev) ||
+      !aligned16(out_dev))
+    return set_err(ORBIT2_E_INVALID, "tile_out_dev/input_dev/out_dev: null or not 16-byte aligned");
+  const int32_t n = (int32_t)p.dev_by_rank[peer].size() - 1;
+  if (n == 0) return ORBIT2_OK;
+  ChunkDev cd{};
+  cd.tiles = c->at<DevTile>(p.lay.peer_tiles) + p.peer_tab_off[peer];
+  cd.tb = 0;
+  cd.tc = n;
+  cd.chunk_core = p.local_core_by_rank[peer];
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
+  return run(c, "stitch_residual", st, [&] {
+    if (cf.precision == ORBIT2_BF16)
+      launch_stitch<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev, out_dev, cd, cmap,
+                                   cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h, st);
+    else
+      launch_stitch<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, cf.batch, cf.V,
+                           cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h, st);
+    return true;
+  });
 }
 
 orbit2_status orbit2_stitch(void* ctx, const void* tile_out_dev, const float* input_dev, int32_t tile_begin,

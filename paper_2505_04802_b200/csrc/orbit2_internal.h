@@ -41,11 +41,24 @@ struct Chunk {
 // Byte offsets of the workspace regions (from the workspace base).
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
-  int64_t tiles, qblk_tile, qpair_tile, core_row, pos_u, pos_w, cmap;
+  int64_t tiles, qblk_tile, qpair_tile, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;
   int32_t esize;              // activation element size (2 bf16, 4 fp32)
+};
+
+// A rectangle of coarse pixels with its element offset in a transfer message.
+struct DevRect {
+  int32_t y0, y1, x0, x1;
+  int64_t off;      // first element (floats) of this rect in the message: [B][V][rows][cols]
+  int64_t pad_;
+};
+static_assert(sizeof(DevRect) == 32, "DevRect layout");
+
+struct XferList {   // one (kind, peer, direction) list inside the workspace rect table
+  int32_t start, count;
+  int64_t elems;
 };
 
 struct Plan {
@@ -60,7 +73,16 @@ struct Plan {
   orbit2_plan_info info;
   Layout lay;
   int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_core_h;
+  // multi-rank: every rank's device tile table (for orbit2_stitch_peer) and
+  // this rank's transfer rectangle lists
+  std::vector<std::vector<DevTile>> dev_by_rank;   // with sentinel
+  std::vector<int64_t> peer_tab_off;               // element offset of rank r's table in peer_tiles
+  std::vector<int64_t> local_core_by_rank;
+  std::vector<DevRect> rects;                      // all lists back to back
+  std::vector<XferList> xfer;                      // index ((kind * R) + peer) * 2 + direction
 };
+// rectangles of one transfer (host side, pure)
+void xfer_rects(const Plan& p, int kind, int rank, int peer, int direction, std::vector<orbit2_rect>* out);
 
 // planner (plan.cpp); returns status and fills msg on error
 orbit2_status build_plan(const orbit2_config* cfg, Plan* plan, std::string* msg);

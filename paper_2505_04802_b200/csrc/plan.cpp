@@ -186,6 +186,53 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     p.dev.push_back(end);
   }
 
+  // ---- every rank's tile table (output gather / stitch_peer) ----
+  p.dev_by_rank.assign(c.world_size, {});
+  p.local_core_by_rank.assign(c.world_size, 0);
+  {
+    std::vector<int64_t> rtok(c.world_size, 0), rcore(c.world_size, 0);
+    for (int t = 0; t < T; ++t) {
+      const orbit2_tile& tt = p.tiles[t];
+      const int r = tt.owner_rank;
+      DevTile dt{};
+      dt.pad_y0 = tt.pad_y0; dt.pad_x0 = tt.pad_x0;
+      dt.pad_h = tt.pad_y1 - tt.pad_y0; dt.pad_w = tt.pad_x1 - tt.pad_x0;
+      dt.core_y0 = tt.core_y0; dt.core_x0 = tt.core_x0;
+      dt.core_h = tt.core_y1 - tt.core_y0; dt.core_w = tt.core_x1 - tt.core_x0;
+      dt.n_tokens = tt.n_tokens; dt.n_core = tt.n_core_tokens;
+      dt.tok_off = rtok[r]; dt.core_off = rcore[r];
+      rtok[r] += tt.n_tokens;
+      rcore[r] += tt.n_core_tokens;
+      p.dev_by_rank[r].push_back(dt);
+      p.max_core_h = std::max(p.max_core_h, dt.core_h);
+    }
+    int64_t off = 0;
+    for (int r = 0; r < c.world_size; ++r) {
+      DevTile end{};
+      end.tok_off = rtok[r]; end.core_off = rcore[r];
+      p.dev_by_rank[r].push_back(end);
+      p.local_core_by_rank[r] = rcore[r];
+      p.peer_tab_off.push_back(off);
+      off += (int64_t)p.dev_by_rank[r].size();
+    }
+  }
+  // ---- this rank's transfer rectangle lists ----
+  for (int kind = 0; kind < 2; ++kind)
+    for (int peer = 0; peer < c.world_size; ++peer)
+      for (int dir = 0; dir < 2; ++dir) {
+        std::vector<orbit2_rect> rs;
+        if (peer != c.rank) xfer_rects(p, kind, c.rank, peer, dir, &rs);
+        XferList xl{(int32_t)p.rects.size(), (int32_t)rs.size(), 0};
+        int64_t e = 0;
+        for (const orbit2_rect& r : rs) {
+          DevRect d{r.y0, r.y1, r.x0, r.x1, e, 0};
+          p.rects.push_back(d);
+          e += (int64_t)c.batch * c.V * (r.y1 - r.y0) * (r.x1 - r.x0);
+        }
+        xl.elems = e;
+        p.xfer.push_back(xl);
+      }
+
   // ---- info ----
   orbit2_plan_info& in = p.info;
   in = orbit2_plan_info{};
@@ -259,6 +306,12 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.pos_u = take((int64_t)(p.Hp + 2 * h) * (p.D / 2) * 4);
   ly.pos_w = take((int64_t)(p.Wp + 2 * h) * (p.D / 2) * 4);
   ly.cmap = take((int64_t)c.K * 4);
+  {
+    int64_t n = 0;
+    for (auto& v : p.dev_by_rank) n += (int64_t)v.size();
+    ly.peer_tiles = take(n * (int64_t)sizeof(DevTile));
+  }
+  ly.rects = take((int64_t)p.rects.size() * (int64_t)sizeof(DevRect));
   ly.total = off;
   in.workspace_bytes = ly.total;
   in.tile_out_bytes = (int64_t)c.batch * in.max_chunk_core_tokens * p.Nh * E;
@@ -266,6 +319,48 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   WeightLayout wl = weight_layout(p);
   in.packed_weight_bytes = wl.total;
   return ORBIT2_OK;
+}
+
+// Transfer rectangles in coarse pixels (see include/orbit2.h, orbit2_xfer_plan).
+namespace {
+orbit2_rect core_px(const orbit2_tile& t, int p) {
+  return {t.core_y0 * p, t.core_y1 * p, t.core_x0 * p, t.core_x1 * p};
+}
+orbit2_rect pad_px(const orbit2_tile& t, int p, int H, int W) {   // clamped to the grid (R4)
+  return {std::max(0, t.pad_y0 * p), std::min(H, t.pad_y1 * p), std::max(0, t.pad_x0 * p),
+          std::min(W, t.pad_x1 * p)};
+}
+bool intersect(const orbit2_rect& a, const orbit2_rect& b, orbit2_rect* o) {
+  o->y0 = std::max(a.y0, b.y0); o->y1 = std::min(a.y1, b.y1);
+  o->x0 = std::max(a.x0, b.x0); o->x1 = std::min(a.x1, b.x1);
+  return o->y0 < o->y1 && o->x0 < o->x1;
+}
+}  // namespace
+
+void xfer_rects(const Plan& p, int kind, int rank, int peer, int direction, std::vector<orbit2_rect>* out) {
+  out->clear();
+  const int pp = p.cfg.patch, H = p.cfg.H, W = p.cfg.W;
+  // direction RECV of (rank <- peer) equals direction SEND of (peer -> rank)
+  const int dst = direction == ORBIT2_RECV ? rank : peer;
+  const int src = direction == ORBIT2_RECV ? peer : rank;
+  if (kind == ORBIT2_XFER_CORES) {   // src's owned cores
+    for (const orbit2_tile& t : p.tiles)
+      if (t.owner_rank == src) out->push_back(core_px(t, pp));
+    return;
+  }
+  for (const orbit2_tile& t : p.tiles) {          // dst's padded rects
+    if (t.owner_rank != dst) continue;
+    const orbit2_rect need = pad_px(t, pp, H, W);
+    for (const orbit2_tile& u : p.tiles) {        // src's cores
+      if (u.owner_rank != src) continue;
+      orbit2_rect o;
+      if (!intersect(need, core_px(u, pp), &o)) continue;
+      bool dup = false;
+      for (const orbit2_rect& r : *out)
+        if (r.y0 == o.y0 && r.y1 == o.y1 && r.x0 == o.x0 && r.x1 == o.x1) dup = true;
+      if (!dup) out->push_back(o);
+    }
+  }
 }
 
 Chunk make_chunk(const Plan& p, int32_t tb, int32_t tc) {

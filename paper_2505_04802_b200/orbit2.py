@@ -17,6 +17,8 @@ ABI_VERSION = 1
 OK, E_INVALID, E_CAPACITY, E_UNSUPPORTED, E_CUDA, E_NCCL, E_STATE = 0, -1, -2, -3, -4, -5, -6
 HALO_CLAMP, HALO_REPLICATE = 0, 1
 BF16, FP32 = 0, 1
+XFER_HALO, XFER_CORES = 0, 1
+SEND, RECV = 0, 1
 
 
 class orbit2_config(C.Structure):
@@ -44,6 +46,10 @@ class orbit2_plan_info(C.Structure):
                 "stitch_bytes_per_sample")]
 
 
+class orbit2_rect(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("y0", "y1", "x0", "x1")]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2505_04802_b200.build` "
@@ -57,6 +63,11 @@ def _load():
         "orbit2_prepare_weights": (i32, [vp, vp, vp, vp]),
         "orbit2_reslim_forward": (i32, [vp, vp, vp, i32, i32, vp, vp]),
         "orbit2_stitch": (i32, [vp, vp, vp, i32, i32, vp, vp]),
+        "orbit2_xfer_plan": (i32, [C.POINTER(orbit2_config), i32, i32, i32, C.POINTER(orbit2_rect), i32,
+                                   C.POINTER(i32), C.POINTER(i64)]),
+        "orbit2_xfer_pack": (i32, [vp, i32, i32, vp, vp, vp]),
+        "orbit2_xfer_unpack": (i32, [vp, i32, i32, vp, vp, vp]),
+        "orbit2_stitch_peer": (i32, [vp, i32, vp, vp, vp, vp]),
         "orbit2_launch_count": (i64, [vp]),
         "orbit2_set_profiling": (i32, [vp, i32]),
         "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
@@ -72,8 +83,9 @@ def _load():
 
 lib = _load()
 EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orbit2_reslim_forward",
-            "orbit2_stitch", "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times",
-            "orbit2_last_error", "orbit2_destroy")
+            "orbit2_stitch", "orbit2_xfer_plan", "orbit2_xfer_pack", "orbit2_xfer_unpack", "orbit2_stitch_peer",
+            "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
+            "orbit2_destroy")
 
 
 class Orbit2Error(RuntimeError):
@@ -110,6 +122,17 @@ def config_from(w, **over) -> orbit2_config:
     return make_config(**kw)
 
 
+def config_from_cfg(cfg: orbit2_config, **over) -> orbit2_config:
+    """Copy of an orbit2_config with fields replaced (e.g. rank=peer)."""
+    new = orbit2_config()
+    C.pointer(new)[0] = cfg
+    for k, v in over.items():
+        setattr(new, k, v)
+    if hasattr(cfg, "_map_keepalive"):
+        new._map_keepalive = cfg._map_keepalive
+    return new
+
+
 def orbit2_tiles_plan(cfg: orbit2_config):
     """Step (1) planning (host only).  Returns (list of orbit2_tile, orbit2_plan_info)."""
     info = orbit2_plan_info()
@@ -117,6 +140,18 @@ def orbit2_tiles_plan(cfg: orbit2_config):
     tiles = (orbit2_tile * info.n_tiles)()
     _check(lib.orbit2_tiles_plan(C.byref(cfg), tiles, info.n_tiles, C.byref(info)), "orbit2_tiles_plan")
     return list(tiles), info
+
+
+def orbit2_xfer_plan(cfg: orbit2_config, kind: int, peer: int, direction: int):
+    """Rectangles (coarse pixels) and element count of one rank-to-rank transfer (host only)."""
+    n = C.c_int32()
+    e = C.c_int64()
+    _check(lib.orbit2_xfer_plan(C.byref(cfg), kind, peer, direction, None, 0, C.byref(n), C.byref(e)),
+           "orbit2_xfer_plan(size)")
+    rects = (orbit2_rect * max(n.value, 1))()
+    _check(lib.orbit2_xfer_plan(C.byref(cfg), kind, peer, direction, rects, n.value, C.byref(n), C.byref(e)),
+           "orbit2_xfer_plan")
+    return [(r.y0, r.y1, r.x0, r.x1) for r in rects[:n.value]], int(e.value)
 
 
 def _ptr(t) -> int:
@@ -149,7 +184,7 @@ class Context:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:
             lib.orbit2_destroy(h)
             self.handle = None
 
@@ -178,6 +213,53 @@ class Context:
     def orbit2_stitch(self, tile_out, x_dev, tile_begin, tile_count, out, stream=None):
         _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
                                  _stream(stream)), "orbit2_stitch")
+
+    # -- multi-rank (TILES sequence parallelism) ------------------------------
+    def orbit2_xfer_pack(self, kind, peer, x_dev, buf, stream=None):
+        _check(lib.orbit2_xfer_pack(self.handle, kind, peer, _ptr(x_dev), _ptr(buf), _stream(stream)),
+               "orbit2_xfer_pack")
+
+    def orbit2_xfer_unpack(self, kind, peer, buf, x_dev, stream=None):
+        _check(lib.orbit2_xfer_unpack(self.handle, kind, peer, _ptr(buf), _ptr(x_dev), _stream(stream)),
+               "orbit2_xfer_unpack")
+
+    def orbit2_stitch_peer(self, peer, tile_out, x_dev, out, stream=None):
+        _check(lib.orbit2_stitch_peer(self.handle, peer, _ptr(tile_out), _ptr(x_dev), _ptr(out), _stream(stream)),
+               "orbit2_stitch_peer")
+
+    def rank_tile_out(self):
+        """tile_out covering ALL of this rank's tiles: [B][local core tokens][K*P*P]."""
+        import torch
+        nh = self.cfg.K * (self.cfg.scale * self.cfg.patch) ** 2
+        dt = torch.bfloat16 if self.bf16 else torch.float32
+        return torch.empty((self.cfg.batch * max(self.info.local_core_tokens, 1), nh), dtype=dt, device=self.device)
+
+    def forward_rank(self, packed, x_dev, tile_out, stream=None):
+        """Steps (1)-(3) + head over all of this rank's tiles into a rank-wide
+        tile_out (chunked calls write consecutive slices: needs B == 1 when
+        chunk_tiles < n_local_tiles)."""
+        n, ch = self.info.n_local_tiles, self.info.chunk_tiles
+        if ch < n and self.cfg.batch != 1:
+            raise ValueError("rank-wide tile_out with chunked calls needs batch == 1")
+        nh = tile_out.shape[1]
+        for tb in range(0, n, ch):
+            tc = min(ch, n - tb)
+            off = self.tiles_core_offset(tb)
+            self.orbit2_reslim_forward(packed, x_dev, tb, tc, tile_out[off:], stream)
+        return tile_out
+
+    def tiles_core_offset(self, tb):
+        """Core-token offset (one sample) of rank-local tile tb."""
+        if not hasattr(self, "_core_off"):
+            r = self.cfg.rank
+            mine = [t for t in self.tiles if t.owner_rank == r]
+            offs, acc = [], 0
+            for t in mine:
+                offs.append(acc)
+                acc += t.n_core_tokens
+            offs.append(acc)
+            self._core_off = offs
+        return self._core_off[tb]
 
     # -- convenience: all rank-local tiles, chunk by chunk ------------------
     def forward(self, packed, x_dev, out=None, tile_out=None, stream=None):

@@ -120,6 +120,17 @@ def test_chunk_invariance_bit_exact():
         assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=ch))
 
 
+def test_packing_invariance_full_grid_bit_exact():
+    """I11/I12 at the full C2 grid (many persistent work items, last query
+    blocks overhanging into the next tile): chunks of 1 tile and a 3-rank split
+    give the same bits as one call (regression: rows past a tile's end must
+    not vote in the attention's conditional rescale)."""
+    w, x, blob = _case("C2", batch=4, depth=2)
+    a = run_cuda(w, x, blob, BF16)
+    assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=1))
+    assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=3))
+
+
 def test_rank_emulation_bit_exact():
     """I11: the tiles partitioned over R ranks (LPT), each rank's tiles run
     separately, assemble a bit-identical field (R = 2, 3)."""
