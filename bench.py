@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
     ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="dp", choices=["dp", "sp"],
+                    help="dp: every rank its own batch (weak scaling); sp: the tiles of one batch spread "
+                         "over the ranks with NCCL halo exchange + output gather (strong scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--set", action="append", default=[], metavar="FIELD=INT",
@@ -440,6 +443,74 @@ def run_ours(args, w, world, rank, local):
         print(json.dumps(res), flush=True)
 
 
+def run_sp(args, w, world, rank, local):
+    """TILES sequence parallelism: one batch, its tiles LPT-spread over the ranks.
+    Timed step = halo exchange (NCCL) + forward of the rank's tiles + output
+    gather (NCCL) + stitch of every tile on rank 0; inputs start as each
+    rank's owned core pixels (resident in HBM)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2505_04802_b200 import orbit2 as o2, sequence_parallel as sp
+    from workloads import make_input, make_weights
+    B = w.batch
+    cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world, rank=rank)
+    ctx = o2.Context(cfg)
+    info = ctx.info
+    full = torch.from_numpy(make_input(w, batch=B)).cuda()
+    packed = ctx.prepare_weights(torch.from_numpy(make_weights(w)).cuda())
+    x0 = torch.zeros_like(full)
+    if world > 1:
+        cores, _ = o2.orbit2_xfer_plan(cfg, o2.XFER_CORES, (rank + 1) % world, o2.SEND)
+        for y0, y1, xa, xb in cores:
+            x0[:, :, y0:y1, xa:xb] = full[:, :, y0:y1, xa:xb]
+    else:
+        x0.copy_(full)
+    del full
+    out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), device="cuda") if rank == 0 else None
+    x = x0.clone()
+    dd = dist if world > 1 else None
+
+    def step():
+        x.copy_(x0)   # reset to owned pixels (the halo exchange refills the rest)
+        if world > 1:
+            sp.forward_sequence_parallel(ctx, packed, x, out, dd)
+        else:
+            ctx.forward(packed, x, out=out)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier(world)
+    times = []
+    l0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            barrier(world)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            step()
+            e1.record()
+            barrier(world)
+            times.append(max_over_ranks(world, e0.elapsed_time(e1)))
+    launches = (ctx.launch_count() - l0) // args.steps
+    ms = statistics.median(times)
+    px = B * w.scale * w.H * w.scale * w.W
+    if rank == 0:
+        pk = peaks()
+        res = {
+            "metric": METRIC, "value": px / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields, random-init weights)",
+            "config": {"workload": w.name, "batch": B, "parallelism": f"tiles-sp{world} (LPT tiles, NCCL halo "
+                       "exchange + tile_out gather, stitch on rank 0)", "step_copy": "x reset from owned pixels (HBM copy)"},
+            "path_tflops": B * info.flops_per_sample / (ms * 1e-3) / 1e12,
+            "gpu_launches_rank0": int(launches),
+            "clocks": clk.summary(),
+            "e2e": None,
+            "note": "strong-scaling mode (one batch over N GPUs); median of per-step max-over-ranks event times",
+        }
+        print(json.dumps(res), flush=True)
+
+
 def main():
     args = parse()
     from workloads import get_config
@@ -455,7 +526,10 @@ def main():
         return
     world, rank, local = dist_init(args.gpus)
     try:
-        run_ours(args, w, world, rank, local)
+        if args.mode == "sp":
+            run_sp(args, w, world, rank, local)
+        else:
+            run_ours(args, w, world, rank, local)
     finally:
         if world > 1:
             import torch.distributed as dist
