@@ -52,6 +52,18 @@ __device__ __forceinline__ float ex2(float x) {
 // nearest integer (1.5*2^23 magic add), 2^f on [-1/2, 1/2] by a degree-3 fit
 // (max relative error 1.0e-4, below bf16's half-ulp 2e-3 that P is rounded to),
 // 2^j by adding j to the exponent field.  x is clamped at -125 (2^-125 ~ 0).
+// (a, b) <- (a, b) * s + t with one packed FFMA2 (sm_100a fma.rn.f32x2)
+__device__ __forceinline__ void ffma2(float& a, float& b, float s, float t) {
+  asm("{\n\t.reg .b64 x, sc, tt;\n\t"
+      "mov.b64 x, {%0, %1};\n\t"
+      "mov.b64 sc, {%2, %2};\n\t"
+      "mov.b64 tt, {%3, %3};\n\t"
+      "fma.rn.f32x2 x, x, sc, tt;\n\t"
+      "mov.b64 {%0, %1}, x;\n\t}"
+      : "+f"(a), "+f"(b)
+      : "f"(s), "f"(t));
+}
+
 __device__ __forceinline__ float ex2_poly(float x) {
   x = fmaxf(x, -125.0f);
   const float t = x + 12582912.0f;
@@ -76,14 +88,23 @@ struct AttnCfg {
   static constexpr int TILE = 128 * DH * 2;           // bytes of a Q/K/V block
   static constexpr uint32_t SW = DH == 32 ? tc::SW_64B : tc::SW_128B;
   static constexpr int QBUF = DH == 128 ? 1 : 2;      // Q tiles of the next work item prefetched
-  static constexpr int PBUF = 1;                      // P buffers per Q tile (2 deadlocked with QBUF=1; no gain seen)
+  static constexpr int PBUF = 1;                      // P buffers per Q tile
   static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
   static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
   static constexpr int THREADS = 128 + 128 * NQ;
-  static constexpr int TCOLS = 128 + DH;              // TMEM columns per Q tile: S | O
+  // P lives in TMEM (64 columns of bf16 pairs) and feeds the PV MMA as the A
+  // operand when TMEM allows: no shared-memory traffic for P (the SS form
+  // re-reads the 128 x 16 A tile from smem on every K step, which made the
+  // kernel shared-memory-bandwidth bound).
+  static constexpr bool P_TMEM = NQ * (128 + DH + 64) <= 512;
+  static constexpr bool TC_SUM = false;               // (P x ones row sums: superseded by P_TMEM)
+  static constexpr int SUMC = TC_SUM ? 16 : 0;
+  static constexpr int TCOLS = 128 + DH + SUMC + (P_TMEM ? 64 : 0);   // S | O | (sum) | (P)
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
-  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_BYTES + 1024 + 512;
+  static constexpr int ONES_BYTES = 4096;             // bf16 ones, 16 rows x 128 keys (K-major SW128)
+  static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
+  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -133,7 +154,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sK = sQ + C::QBUF * NQ * C::TILE;        // [KST][TILE]
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
   uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + NQ * C::PBUF * C::P_BYTES);
+  uint8_t* sOnes = sP + NQ * C::PBUF * C::P_SMEM;    // [ONES_BYTES]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
   uint64_t* q_full = bar;                           // [QBUF]
   uint64_t* q_empty = q_full + C::QBUF;             // [QBUF]
   uint64_t* k_full = q_empty + C::QBUF;             // [KST]
@@ -175,6 +197,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (C::TC_SUM) {   // all-ones B operand for the row sums (layout-free: every element equal)
+    for (int o = threadIdx.x * 16; o < C::ONES_BYTES; o += blockDim.x * 16)
+      *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    tc::fence_proxy_async_smem();
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -250,13 +277,13 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             if (lane == 0) TL_STAMP(2 + qt, ns, 1);
             tc::tc_fence_after();
             if (tc::elect_one()) {
+              // descriptors built once; k-steps advance the start-address field (addr >> 4)
+              const uint64_t qd0 = tc::sdesc(q_addr + (qb * NQ + qt) * C::TILE, 16, 8 * C::RB, C::SW);
+              const uint64_t kd0 = tc::sdesc(k_addr + st * C::TILE, 16, 8 * C::RB, C::SW);
 #pragma unroll
               for (int kk = 0; kk < DH / 16; ++kk) {
-                const int a = (kk * 16) / C::AC, off = ((kk * 16) % C::AC) * 2;
-                const uint64_t qd =
-                    tc::sdesc(q_addr + (qb * NQ + qt) * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
-                const uint64_t kd = tc::sdesc(k_addr + st * C::TILE + a * C::ATOM + off, 16, 8 * C::RB, C::SW);
-                tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd, kd, id_s, kk > 0);
+                const uint32_t adv = (uint32_t)(((kk * 16) / C::AC) * C::ATOM + ((kk * 16) % C::AC) * 2) >> 4;
+                tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd0 + adv, kd0 + adv, id_s, kk > 0);
               }
               tc::mma_commit(&s_full[qt]);
               tc::mma_commit(&k_empty[st]);
@@ -285,12 +312,25 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             if (lane == 0) TL_STAMP(2 + qt, np, 3);
             tc::tc_fence_after();
             if (tc::elect_one()) {
+              const uint64_t pd0 =
+                  tc::sdesc(p_addr + (qt * C::PBUF + np % C::PBUF) * C::P_SMEM, 16, 1024, tc::SW_128B);
+              const uint32_t ptm = tmem + qt * C::TCOLS + 128 + DH + C::SUMC;   // P columns (P_TMEM)
+              const uint64_t vd0 = tc::sdesc(v_addr + st * C::TILE, C::ATOM, 8 * C::RB, C::SW);
+              constexpr uint32_t id_l = tc::idesc_bf16(128, 16, 0, 0);
+              const uint64_t ld0 = tc::sdesc(tc::smem_u32(sOnes), 16, 1024, tc::SW_128B);
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {   // 128 keys, K = 16 per MMA
-                const uint64_t pd = tc::sdesc(p_addr + (qt * C::PBUF + np % C::PBUF) * C::P_BYTES +
-                                                  (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, tc::SW_128B);
-                const uint64_t vd = tc::sdesc(v_addr + st * C::TILE + kk * 16 * C::RB, C::ATOM, 8 * C::RB, C::SW);
-                tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd, vd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+                const uint32_t padv = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                const uint32_t vadv = (uint32_t)(kk * 16 * C::RB) >> 4;
+                const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+                if (C::P_TMEM)
+                  tc::mma_bf16_ts(tmem + qt * C::TCOLS + 128, ptm + kk * 8, vd0 + vadv, id_o, acc);
+                else
+                  tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd0 + padv, vd0 + vadv, id_o, acc);
+                if (C::TC_SUM) {   // row sums: SUM[128 x 16] (+)= P x ones
+                  const uint32_t ladv = (uint32_t)((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
+                  tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128 + DH, pd0 + padv, ld0 + ladv, id_l, acc);
+                }
               }
               tc::mma_commit(&p_free[qt * C::PBUF + np % C::PBUF]);
               tc::mma_commit(&v_empty[st]);
@@ -371,7 +411,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             const float alpha = ex2(m_ref - m_new);
             l_run *= alpha;
 #pragma unroll
-            for (int c0 = 0; c0 < DH; c0 += 16) {
+            for (int c0 = 0; c0 < DH + C::SUMC; c0 += 16) {   // O and the tensor-core row sums
               uint32_t r[16];
               tc::tmem_ld16(o_addr + c0, r);
               tc::tmem_ld_wait();
@@ -396,27 +436,47 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         float zero_dep;
         asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(zero_dep) : "r"(tc::smem_u32(zero_slot)) : "memory");
         const float m_use = m_ref + zero_dep;
-        // probabilities -> bf16 P (SW128 K-major), row sum in fp32
-        uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_BYTES + i * 128;
+        // probabilities -> bf16 P, row sum in fp32.  P goes to TMEM (A operand of the
+        // TS-form PV MMA) or, when TMEM is short, to smem (SW128 K-major).
         float rs0 = 0.f, rs1 = 0.f;
+        if constexpr (C::P_TMEM) {
+          const uint32_t p_tm = s_addr + 128 + DH + C::SUMC;
 #pragma unroll
-        for (int c0 = 0; c0 < 128; c0 += 16) {
-          uint32_t pk[8];
+          for (int c0 = 0; c0 < 128; c0 += 64) {
+            uint32_t pk[32];
 #pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            const float x0 = fmaf(sv[c0 + e], sl, -m_use), x1 = fmaf(sv[c0 + e + 1], sl, -m_use);
-            // all on the MUFU: moving 25% to ex2_poly (FMA pipe) measured slower here,
-            // the exp phase of one warp is issue/latency-bound, not MUFU-bound
-            const float p0 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x0) : ex2(x0);
-            const float p1 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x1) : ex2(x1);
-            rs0 += p0;
-            rs1 += p1;
-            pk[e / 2] = tc::pack_bf16(p0, p1);
+            for (int e = 0; e < 64; e += 2) {
+              float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
+              ffma2(x0, x1, sl, -m_use);                   // FFMA2: both (s*c - m) in one instruction
+              const float p0 = ex2(x0), p1 = ex2(x1);
+              rs0 += p0;
+              rs1 += p1;
+              pk[e / 2] = tc::pack_bf16(p0, p1);           // column = keys (2c, 2c+1), lower key in low half
+            }
+            tc::tmem_st32(p_tm + c0 / 2, pk);
           }
-          uint8_t* atom = prow + (c0 >> 6) * 16384;
-          const int cb = (c0 & 63) >> 3;
-          *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        } else {
+          uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_SMEM + i * 128;
+#pragma unroll
+          for (int c0 = 0; c0 < 128; c0 += 16) {
+            uint32_t pk[8];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
+              ffma2(x0, x1, sl, -m_use);
+              const float p0 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x0) : ex2(x0);
+              const float p1 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x1) : ex2(x1);
+              if (!C::TC_SUM) {
+                rs0 += p0;
+                rs1 += p1;
+              }
+              pk[e / 2] = tc::pack_bf16(p0, p1);
+            }
+            uint8_t* atom = prow + (c0 >> 6) * 16384;
+            const int cb = (c0 & 63) >> 3;
+            *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
         }
         l_run += rs0 + rs1;
         if (pingpong) {
@@ -424,8 +484,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           if (qt == 1 && j + 1 < it.nkb) asm volatile("bar.arrive 1, 256;" ::: "memory");
         }
         if (tlr) TL_STAMP(qt, cs, 5);
-        if (rescaled) tc::tmem_st_wait();
-        tc::fence_proxy_async_smem();
+        if (rescaled || C::P_TMEM) tc::tmem_st_wait();
+        if (!C::P_TMEM) tc::fence_proxy_async_smem();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
         if (tlr) TL_STAMP(qt, cs, 6);
@@ -434,6 +494,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
       tc::tc_fence_after();
       const int qrow = it.q0 + qt * 128 + i;
+      if (C::TC_SUM) {   // row sum of the bf16 probabilities, accumulated by the tensor core
+        uint32_t r[16];
+        tc::tmem_ld16(o_addr + DH, r);
+        tc::tmem_ld_wait();
+        l_run = __uint_as_float(r[0]);
+      }
       const float inv = 1.f / l_run;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 16) {
