@@ -436,6 +436,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         float zero_dep;
         asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(zero_dep) : "r"(tc::smem_u32(zero_slot)) : "memory");
         const float m_use = m_ref + zero_dep;
+        if (tlr) TL_STAMP(qt, cs, 7);
         // probabilities -> bf16 P, row sum in fp32.  P goes to TMEM (A operand of the
         // TS-form PV MMA) or, when TMEM is short, to smem (SW128 K-major).
         float rs0 = 0.f, rs1 = 0.f;

@@ -205,20 +205,23 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn_major, 
 }
 
 // GELU(x) = x * 0.5 * (1 + erf(x / sqrt(2)))  (R9).  erf from Abramowitz &
-// Stegun 7.1.26 (|error| <= 1.5e-7, one rcp + one ex2 on the MUFU pipe), i.e.
-// the exact-erf GELU to fp32 rounding, without erff's branches.
+// Stegun 7.1.28: erf(u) = 1 - (1 + a1 u + ... + a6 u^6)^-16, |error| <= 3e-7
+// (1.7e-6 in fp32 arithmetic; the GELU output is rounded to bf16, 2e-3), one
+// reciprocal on the MUFU plus FMA-pipe work, no branches.
 __device__ __forceinline__ float gelu_erf_fast(float x) {
   const float u = fabsf(x) * 0.70710678118654752f;
+  float p = fmaf(0.0000430638f, u, 0.0002765672f);
+  p = fmaf(p, u, 0.0001520143f);
+  p = fmaf(p, u, 0.0092705272f);
+  p = fmaf(p, u, 0.0422820123f);
+  p = fmaf(p, u, 0.0705230784f);
   float t;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, u, 1.0f)));
-  float p = fmaf(1.061405429f, t, -1.453152027f);
-  p = fmaf(p, t, 1.421413741f);
-  p = fmaf(p, t, -0.284496736f);
-  p = fmaf(p, t, 0.254829592f);
-  p *= t;
-  float e;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-u * u * 1.4426950408889634f));
-  const float erf_abs = fmaf(-p, e, 1.0f);
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(p, u, 1.0f)));
+  t = t * t;
+  t = t * t;
+  t = t * t;
+  t = t * t;
+  const float erf_abs = 1.0f - t;
   return 0.5f * x * (1.0f + copysignf(erf_abs, x));
 }
 

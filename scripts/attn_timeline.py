@@ -25,7 +25,7 @@ f(None)
 t = buf.cpu().numpy().reshape(5, 64, 8).astype(np.int64)
 t0 = t[t > 0].min()
 names = {0: "softmax tile0", 1: "softmax tile1", 2: "mma tile0", 3: "mma tile1", 4: "producer"}
-ev = {0: "loop,s_full_done,s_loaded,max_done,pfree_done,exp_done,p_arrive",
+ev = {0: "loop,s_full_done,s_loaded,max_done,pfree_done,exp_done,p_arrive,after_pingpong_bar",
       2: "k_full_done,s_free_done,v_full_done,p_full_done,pv_issued",
       4: "k_empty_done,v_empty_done"}
 for role in range(5):
@@ -33,4 +33,4 @@ for role in range(5):
     for b in range(40):
         row = t[role, b]
         if (row > 0).any():
-            print(f"  blk {b:2d}: " + " ".join(f"{(v - t0):8d}" if v > 0 else "       -" for v in row[:7]))
+            print(f"  blk {b:2d}: " + " ".join(f"{(v - t0):8d}" if v > 0 else "       -" for v in row[:8]))
