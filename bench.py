@@ -171,6 +171,7 @@ def class_work(w, info, B):
         "mlp_down_gemm": (L - last) * 8.0 * npad * D * D + last * 8.0 * ncore * D * D,
         "head_gemm": 2.0 * ncore * D * Nh,
     }
+    f["mlp_fused"] = f["mlp_up_gemm"] + f["mlp_down_gemm"]   # one kernel does both (D = 256)
     out = {k: ("tensor", v * B) for k, v in f.items()}
     # HBM kernels: unique algorithmic bytes
     out["tile_gather"] = ("hbm", B * (4.0 * V * w.H * w.W + 2.0 * npad * Din))

@@ -1,6 +1,8 @@
 """Build liborbit2.so in-tree with nvcc for sm_100a.
 
     python -m paper_2505_04802_b200.build [--force] [--verbose]
+    python -m paper_2505_04802_b200.build --variant NAME -D MACRO=VALUE ...   (A/B experiments:
+        builds paper_2505_04802_b200/liborbit2_NAME.so; load it with ORBIT2_LIB=<path>)
 
 Objects go to paper_2505_04802_b200/_build/, the shared library to
 paper_2505_04802_b200/liborbit2.so (git-ignored, travels to the GPU box).
@@ -43,8 +45,8 @@ def headers() -> list[str]:
     return hs + [os.path.join(ROOT, "include", "orbit2.h")]
 
 
-def _compile(src: str, force: bool, verbose: bool, extra: list[str]) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+def _compile(src: str, force: bool, verbose: bool, extra: list[str], obj_dir: str = OBJ) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src) + ".o")
     newest_dep = max([os.path.getmtime(src)] + [os.path.getmtime(h) for h in headers()])
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
@@ -61,24 +63,31 @@ def _compile(src: str, force: bool, verbose: bool, extra: list[str]) -> str:
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          variant: str | None = None) -> str:
+    obj_dir = OBJ if variant is None else OBJ + "_" + variant
+    lib = LIB if variant is None else os.path.join(PKG, f"liborbit2_{variant}.so")
+    os.makedirs(obj_dir, exist_ok=True)
     extra = extra or []
+    if variant is not None:
+        force = True
     srcs = sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, force, verbose, extra), srcs))
+        objs = list(ex.map(lambda s: _compile(s, force, verbose, extra, obj_dir), srcs))
     newest = max(os.path.getmtime(o) for o in objs)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        cmd = [nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-o", LIB] + objs
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < newest:
+        cmd = [nvcc()] + ARCH + ["-shared", "-Xcompiler", "-fPIC", "-cudart", "static", "-o", lib] + objs
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--variant", default=None)
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, extra=[f"-D{d}" for d in a.defines], variant=a.variant))

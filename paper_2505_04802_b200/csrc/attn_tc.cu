@@ -37,6 +37,18 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
 
 long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timeline
 
+// Build-time knobs, defaults = the measured best on B200 (scripts/ab_kernels.py,
+// C2 B=64: ping-pong 27.2 ms, none 24.5 ms, none + 4/16 polynomial exps 23.2 ms):
+//   ORBIT2_ATTN_SPLIT    softmax warps per query row (1; 2 = 64 keys per warp)
+//   ORBIT2_ATTN_PINGPONG alternate the two Q tiles' exp phases on the MUFU (0)
+//   ORBIT2_ATTN_POLY     exponentials per 16 evaluated on the FMA pipe (4)
+#ifndef ORBIT2_ATTN_SPLIT
+#define ORBIT2_ATTN_SPLIT 1
+#endif
+#ifndef ORBIT2_ATTN_PINGPONG
+#define ORBIT2_ATTN_PINGPONG 0
+#endif
+
 namespace {
 
 // volatile: keeps the exponentials after the ping-pong named barrier (a plain
@@ -73,11 +85,27 @@ __device__ __forceinline__ float ex2_poly(float x) {
 }
 
 
-// debug timeline: tl[(role * 64 + block) * 8 + event] for CTA 0, first 64 blocks
+// debug timeline: tl[(role * 64 + block) * 8 + event] for CTA 0, first 64 blocks.
+// Compiled in only with -DORBIT2_ATTN_TIMELINE (scripts/attn_timeline.py builds
+// that variant): the stamps cost the softmax warps registers.
+#ifdef ORBIT2_ATTN_TIMELINE
 #define TL_STAMP(role, blk, ev)                                                          \
   do {                                                                                   \
     if (tl != nullptr && blockIdx.x == 0 && (blk) < 64) tl[((role) * 64 + (blk)) * 8 + (ev)] = clock64(); \
   } while (0)
+// per-warp exp-phase start / end of the first 16 blocks: tl[2560 + (warp * 16 + blk) * 2 + ev]
+#define TL_WARP(blk, ev)                                                                          \
+  do {                                                                                            \
+    if (tl != nullptr && blockIdx.x == 0 && (blk) < 16 && lane == 0) tl[2560 + (warp * 16 + (blk)) * 2 + (ev)] = clock64(); \
+  } while (0)
+#else
+#define TL_WARP(blk, ev) \
+  do {                   \
+  } while (0)
+#define TL_STAMP(role, blk, ev) \
+  do {                          \
+  } while (0)
+#endif
 
 template <int DH, int NQ>
 struct AttnCfg {
@@ -92,7 +120,13 @@ struct AttnCfg {
   static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
   static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
-  static constexpr int THREADS = 128 + 128 * NQ;
+  // softmax warps per query row: 2 (each 64 keys) so two warps per SM sub-partition
+  // feed the MUFU during a tile's exp phase; 1 on the smem-P fallback
+  static constexpr int SPLIT = NQ * (128 + DH + 64) <= 512 ? ORBIT2_ATTN_SPLIT : 1;
+  static constexpr int KC = 128 / SPLIT;              // key columns per softmax warp
+  static constexpr int SMT = 128 * SPLIT;             // softmax threads per Q tile
+  static constexpr int CTRL_WARPS = 1 + NQ;          // producer (+TMEM alloc), one MMA issuer per Q tile
+  static constexpr int THREADS = 32 * CTRL_WARPS + SMT * NQ;
   // P lives in TMEM (64 columns of bf16 pairs) and feeds the PV MMA as the A
   // operand when TMEM allows: no shared-memory traffic for P (the SS form
   // re-reads the 128 x 16 A tile from smem on every K step, which made the
@@ -104,7 +138,9 @@ struct AttnCfg {
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
   static constexpr int ONES_BYTES = 4096;             // bf16 ones, 16 rows x 128 keys (K-major SW128)
   static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
-  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
+  static constexpr int XBYTES = NQ * 2 * SPLIT * 128 * 4 + NQ * SPLIT * 128 * 4;   // row max / sum exchange
+  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + XBYTES +
+                              1024 + 512;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -112,7 +148,11 @@ struct AttnCfg {
 // stay <= 2^8 (exact in bf16's exponent range, fp32 accumulation) and the
 // O rescale in TMEM is rare.  Mathematically identical softmax (R18).
 constexpr float kRescaleLog2 = 8.0f;
-constexpr bool kPolyExp = false;   // FMA-pipe exp2 for 4/16 elements (off: measured slower)
+#ifndef ORBIT2_ATTN_POLY
+#define ORBIT2_ATTN_POLY 4
+#endif
+// exponentials per 16 computed on the FMA pipe (ex2_poly) instead of the MUFU
+constexpr int kPolyPer16 = ORBIT2_ATTN_POLY;
 
 struct Item {
   int64_t base;     // first row of the tile's tokens in the packed workspace
@@ -120,13 +160,15 @@ struct Item {
 };
 
 template <int NQ>
-__device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int64_t id) {
-  const int64_t per_b = (int64_t)ch.nqp * heads;      // item = (pair fastest, head, sample)
+__device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int id) {
+  // 32-bit division (n_items < 2^31 is checked at launch): a 64-bit one is a
+  // subroutine call whose ABI spills registers in every role's loop
+  const int per_b = ch.nqp * heads;                   // item = (pair fastest, head, sample)
   Item it;
-  const int b = (int)(id / per_b);
-  const int64_t r = id - (int64_t)b * per_b;
-  it.h = (int)(r / ch.nqp);
-  const int g = ch.qp0 + (int)(r - (int64_t)it.h * ch.nqp);
+  const int b = id / per_b;
+  const int r = id - b * per_b;
+  it.h = r / ch.nqp;
+  const int g = ch.qp0 + (r - it.h * ch.nqp);
   const DevTile t = ch.tiles[ch.qpair_tile[g]];
   it.n = t.n_tokens;
   it.base = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0);
@@ -144,7 +186,7 @@ __device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int64_t
 template <int DH, int NQ>
 __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
-                   int heads, int64_t n_items, long long* __restrict__ tl) {
+                   int heads, int n_items, long long* __restrict__ tl) {
   // tl: optional debug timeline (clock64 stamps of CTA 0), null in production
   using C = AttnCfg<DH, NQ>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -155,7 +197,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
   uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
   uint8_t* sOnes = sP + NQ * C::PBUF * C::P_SMEM;    // [ONES_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  float* xmax = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);   // [NQ][2][SPLIT][128]
+  float* xsum = xmax + NQ * 2 * C::SPLIT * 128;                    // [NQ][SPLIT][128]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xmax) + C::XBYTES);
   uint64_t* q_full = bar;                           // [QBUF]
   uint64_t* q_empty = q_full + C::QBUF;             // [QBUF]
   uint64_t* k_full = q_empty + C::QBUF;             // [KST]
@@ -189,14 +233,17 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     *zero_slot = 0.0f;
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
-      tc::mbar_init(&s_free[s], 128);
-      tc::mbar_init(&p_full[s], 128);
+      tc::mbar_init(&s_free[s], C::SMT);
+      tc::mbar_init(&p_full[s], C::SMT);
       for (int u = 0; u < C::PBUF; ++u) tc::mbar_init(&p_free[s * C::PBUF + u], 1);
-      tc::mbar_init(&o_free[s], 128);
+      tc::mbar_init(&o_free[s], C::SMT);
     }
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  if (warp == 0) {
+    __syncwarp();
+    tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
+  }
   if (C::TC_SUM) {   // all-ones B operand for the row sums (layout-free: every element equal)
     for (int o = threadIdx.x * 16; o < C::ONES_BYTES; o += blockDim.x * 16)
       *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
@@ -211,7 +258,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       uint32_t li = 0, gk = 0, gv = 0;
-      for (int64_t id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
         const Item it = item_info<NQ>(ch, heads, id);
         const int32_t y0 = (int32_t)it.base;
         const uint32_t qb = li % C::QBUF;
@@ -249,21 +296,21 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         }
       }
     }
-  } else if (warp == 1 || warp == 3) {
+  } else if (warp <= NQ) {
     {   // whole warp runs the loop (uniform descriptors); one elected lane issues
-      // ---------------- MMA issuers: warp 1 -> Q tile 0, warp 3 -> Q tile 1 ----------------
+      // ---------------- MMA issuers: warp 1 -> Q tile 0, warp 2 -> Q tile 1 ----------------
       // Each Q tile has its own issuing thread so the two softmax warpgroups
       // are not forced into lockstep (their exp phases then alternate on the
       // MUFU instead of colliding).  Shared Q/K/V slots are released by one
       // arrival per issuer; an issuer whose tile is idle for a work item still
       // walks the ring phases (wait full, arrive empty) to stay aligned.
-      const int qt = warp == 1 ? 0 : 1;
+      const int qt = warp - 1;
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
       constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);    // P K-major, V MN-major
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const uint32_t p_addr = tc::smem_u32(sP);
       uint32_t li = 0, gk = 0, gv = 0, ns = 0, np = 0, ni = 0;
-      for (int64_t id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
         const Item it = item_info<NQ>(ch, heads, id);
         const bool active = qt < it.nq;
         const uint32_t qb = li % C::QBUF;
@@ -347,71 +394,85 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         if (active) ++ni;
       }
     }
-  } else if (warp >= 4) {
+  } else {
     // ---------------- softmax / correction / epilogue ----------------
-    const int qt = (warp - 4) / 4;
+    // SPLIT warps per query row: warp (qt, half, q) owns rows q*32.. (TMEM lane
+    // quarter q) and key columns half*KC.. of every S block, O columns
+    // half*DH/SPLIT.. ; row maxima and sums are combined through shared memory.
+    constexpr int SPLIT = C::SPLIT, KC = C::KC, OC = DH / SPLIT;
+    // (any 4 consecutive warps cover the 4 TMEM lane quarters warp % 4)
+    const int qt = (warp - C::CTRL_WARPS) / (4 * SPLIT);
+    const int half = ((warp - C::CTRL_WARPS) / 4) % SPLIT;
     const int q = warp & 3;
     const int i = q * 32 + lane;                   // query row within the Q tile
-    const uint32_t s_addr = tmem + ((uint32_t)(q * 32) << 16) + qt * C::TCOLS;
-    const uint32_t o_addr = s_addr + 128;
+    const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + qt * C::TCOLS;
+    const uint32_t s_addr = lane_base + half * KC;
+    const uint32_t o_addr = lane_base + 128 + half * OC;
+    const uint32_t p_tm = lane_base + 128 + DH + C::SUMC + half * (KC / 2);
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     uint64_t* my_p_free = p_free + qt * C::PBUF;
-    const int sw = i & 7;
+    const uint32_t xbar = 3 + qt;                  // named barrier of this tile's SMT threads
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
-    for (int64_t id = blockIdx.x; id < n_items; id += gridDim.x) {
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
       const Item it = item_info<NQ>(ch, heads, id);
       if (qt >= it.nq) continue;
       float m_ref = -INFINITY, l_run = 0.f;
-      const bool tlr = (warp & 3) == 0 && lane == 0;
+      const bool tlr = (warp & 3) == 0 && lane == 0 && half == 0;
+      const bool row_valid = it.q0 + qt * 128 + i < it.n;
       for (int j = 0; j < it.nkb; ++j, ++cs) {
         if (tlr) TL_STAMP(qt, cs, 0);
         tc::mbar_wait(&s_full[qt], cs & 1);
         if (tlr) TL_STAMP(qt, cs, 1);
         tc::tc_fence_after();
-        float sv[128];
+        float sv[KC];
         {
           uint32_t* r = reinterpret_cast<uint32_t*>(sv);
 #pragma unroll
-          for (int c0 = 0; c0 < 128; c0 += 32)
+          for (int c0 = 0; c0 < KC; c0 += 32)
             tc::tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(r + c0));
           tc::tmem_ld_wait();
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&s_free[qt]);               // TMEM S columns may take the next S
         if (tlr) TL_STAMP(qt, cs, 2);
-        const int kvalid = it.n - j * 128;
-        if (kvalid < 128) {
+        const int kvalid = it.n - j * 128 - half * KC;
+        if (kvalid < KC) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
+          for (int c = 0; c < KC; ++c)
             if (c >= kvalid) sv[c] = -INFINITY;
         }
         float m0 = sv[0], m1 = sv[1], m2 = sv[2], m3 = sv[3];
 #pragma unroll
-        for (int c = 4; c < 128; c += 4) {
+        for (int c = 4; c < KC; c += 4) {
           m0 = fmaxf(m0, sv[c]); m1 = fmaxf(m1, sv[c + 1]);
           m2 = fmaxf(m2, sv[c + 2]); m3 = fmaxf(m3, sv[c + 3]);
         }
-        const float m_blk = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl;
-        // PV of block cs-PBUF released this P buffer
+        float mloc = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+        if (SPLIT > 1) {   // combine with the other warp(s) of these rows (double-buffered slot)
+          float* xm = xmax + ((qt * 2 + (cs & 1)) * SPLIT) * 128;
+          xm[half * 128 + i] = mloc;
+          asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(C::SMT) : "memory");
+#pragma unroll
+          for (int h2 = 0; h2 < SPLIT; ++h2) mloc = fmaxf(mloc, xm[h2 * 128 + i]);
+        }
+        const float m_blk = mloc * sl;
         if (tlr) TL_STAMP(qt, cs, 3);
+        // previous PV finished: P columns free and O complete
         if (cs >= (uint32_t)C::PBUF) tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
         if (tlr) TL_STAMP(qt, cs, 4);
-        // tcgen05.ld/st are warp-collective: the rescale decision is warp-uniform
-        // (rows whose max did not move get alpha = 1).
-        // Only rows inside the tile vote: rows past its end hold the next tile's (or
-        // stale) tokens, which must not change the valid rows' rounding (keeps the
-        // result independent of packing, chunking and rank assignment).
-        const bool row_valid = it.q0 + qt * 128 + i < it.n;
+        // Conditional rescale (tcgen05.ld/st are warp-collective: warp-uniform decision;
+        // all warps of a row see the same maxima).  Only rows inside the tile vote, so
+        // the result is independent of packing, chunking and rank assignment.
         const bool rescaled = j > 0 && __any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2);
         if (j == 0 || rescaled) {
           const float m_new = fmaxf(m_blk, m_ref);
-          if (rescaled) {   // O must hold PV_{j-1} (block cs-1) before it is rescaled
+          if (rescaled) {
             tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
             tc::tc_fence_after();
             const float alpha = ex2(m_ref - m_new);
             l_run *= alpha;
 #pragma unroll
-            for (int c0 = 0; c0 < DH + C::SUMC; c0 += 16) {   // O and the tensor-core row sums
+            for (int c0 = 0; c0 < OC; c0 += 16) {
               uint32_t r[16];
               tc::tmem_ld16(o_addr + c0, r);
               tc::tmem_ld_wait();
@@ -423,12 +484,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           m_ref = m_new;
         }
         // Exp phases of the two Q tiles alternate on the MUFU (A_j, B_j, A_{j+1}, ...):
-        // named barrier 1 = "tile 0 may start", 2 = "tile 1 may start".  While one
-        // tile exponentiates, the other loads S and reduces its row maxima.
-        const bool pingpong = it.nq == 2;
+        // named barrier 1 = "tile 0 may start", 2 = "tile 1 may start".
+        const bool pingpong = ORBIT2_ATTN_PINGPONG && it.nq == 2;
         if (pingpong) {
-          if (qt == 0 && j > 0) asm volatile("bar.sync 1, 256;" ::: "memory");
-          if (qt == 1) asm volatile("bar.sync 2, 256;" ::: "memory");
+          if (qt == 0 && j > 0) asm volatile("bar.sync 1, %0;" ::"r"(2 * C::SMT) : "memory");
+          if (qt == 1) asm volatile("bar.sync 2, %0;" ::"r"(2 * C::SMT) : "memory");
         }
         // Data dependency on a shared-memory load issued after the barrier: the
         // scheduler otherwise hoists the MUFU work above BAR.SYNC (it only
@@ -437,78 +497,80 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(zero_dep) : "r"(tc::smem_u32(zero_slot)) : "memory");
         const float m_use = m_ref + zero_dep;
         if (tlr) TL_STAMP(qt, cs, 7);
-        // probabilities -> bf16 P, row sum in fp32.  P goes to TMEM (A operand of the
-        // TS-form PV MMA) or, when TMEM is short, to smem (SW128 K-major).
+        TL_WARP(cs, 0);
+        // probabilities -> bf16 P into TMEM (A operand of the PV MMA), fp32 row sums
         float rs0 = 0.f, rs1 = 0.f;
         if constexpr (C::P_TMEM) {
-          const uint32_t p_tm = s_addr + 128 + DH + C::SUMC;
 #pragma unroll
-          for (int c0 = 0; c0 < 128; c0 += 64) {
+          for (int c0 = 0; c0 < KC; c0 += 64) {
             uint32_t pk[32];
 #pragma unroll
             for (int e = 0; e < 64; e += 2) {
               float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
               ffma2(x0, x1, sl, -m_use);                   // FFMA2: both (s*c - m) in one instruction
-              const float p0 = ex2(x0), p1 = ex2(x1);
+              const bool poly = (e & 15) < kPolyPer16;
+              const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
               rs0 += p0;
               rs1 += p1;
               pk[e / 2] = tc::pack_bf16(p0, p1);           // column = keys (2c, 2c+1), lower key in low half
             }
             tc::tmem_st32(p_tm + c0 / 2, pk);
           }
-        } else {
+        } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
           uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_SMEM + i * 128;
+          const int sw = i & 7;
 #pragma unroll
-          for (int c0 = 0; c0 < 128; c0 += 16) {
+          for (int c0 = 0; c0 < KC; c0 += 16) {
             uint32_t pk[8];
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
               float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
               ffma2(x0, x1, sl, -m_use);
-              const float p0 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x0) : ex2(x0);
-              const float p1 = kPolyExp && (e == 6 || e == 14) ? ex2_poly(x1) : ex2(x1);
-              if (!C::TC_SUM) {
-                rs0 += p0;
-                rs1 += p1;
-              }
+              const float p0 = ex2(x0), p1 = ex2(x1);
+              rs0 += p0;
+              rs1 += p1;
               pk[e / 2] = tc::pack_bf16(p0, p1);
             }
-            uint8_t* atom = prow + (c0 >> 6) * 16384;
-            const int cb = (c0 & 63) >> 3;
+            const int ca = half * KC + c0;
+            uint8_t* atom = prow + (ca >> 6) * 16384;
+            const int cb = (ca & 63) >> 3;
             *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
         }
         l_run += rs0 + rs1;
         if (pingpong) {
-          if (qt == 0) asm volatile("bar.arrive 2, 256;" ::: "memory");
-          if (qt == 1 && j + 1 < it.nkb) asm volatile("bar.arrive 1, 256;" ::: "memory");
+          if (qt == 0) asm volatile("bar.arrive 2, %0;" ::"r"(2 * C::SMT) : "memory");
+          if (qt == 1 && j + 1 < it.nkb) asm volatile("bar.arrive 1, %0;" ::"r"(2 * C::SMT) : "memory");
         }
         if (tlr) TL_STAMP(qt, cs, 5);
-        if (rescaled || C::P_TMEM) tc::tmem_st_wait();
+        TL_WARP(cs, 1);
+        tc::tmem_st_wait();
         if (!C::P_TMEM) tc::fence_proxy_async_smem();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
         if (tlr) TL_STAMP(qt, cs, 6);
       }
-      // epilogue: O / l for this row of the head's output, then hand O back
+      // epilogue: combined row sum, O / l for this warp's DH/SPLIT columns
+      if (SPLIT > 1) {
+        float* xs = xsum + qt * SPLIT * 128;
+        xs[half * 128 + i] = l_run;
+        asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(C::SMT) : "memory");
+        l_run = 0.f;
+#pragma unroll
+        for (int h2 = 0; h2 < SPLIT; ++h2) l_run += xs[h2 * 128 + i];
+      }
       tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
       tc::tc_fence_after();
       const int qrow = it.q0 + qt * 128 + i;
-      if (C::TC_SUM) {   // row sum of the bf16 probabilities, accumulated by the tensor core
-        uint32_t r[16];
-        tc::tmem_ld16(o_addr + DH, r);
-        tc::tmem_ld_wait();
-        l_run = __uint_as_float(r[0]);
-      }
       const float inv = 1.f / l_run;
 #pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 16) {
+      for (int c0 = 0; c0 < OC; c0 += 16) {
         uint32_t r[16];
         tc::tmem_ld16(o_addr + c0, r);
         tc::tmem_ld_wait();
         if (qrow < it.n) {
-          uint4* dst = reinterpret_cast<uint4*>(out + (it.base + qrow) * (int64_t)D + it.h * DH + c0);
+          uint4* dst = reinterpret_cast<uint4*>(out + (it.base + qrow) * (int64_t)D + it.h * DH + half * OC + c0);
 #pragma unroll
           for (int u = 0; u < 2; ++u)
             dst[u] = make_uint4(tc::pack_bf16(__uint_as_float(r[8 * u]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
@@ -523,7 +585,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 0) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, C::TMEM_COLS);
   }
@@ -552,9 +614,10 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   }
   const int64_t n_items = (int64_t)ch.nqp * heads * B;
   if (n_items == 0) return true;
+  if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM
   attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
-                                                             heads, n_items, g_attn_timeline);
+                                                             heads, (int)n_items, g_attn_timeline);
   return true;
 }
 

@@ -134,7 +134,7 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 }  // namespace
 
-namespace orbit2 { extern long long* g_attn_timeline; }
+namespace orbit2 { extern long long* g_attn_timeline; extern long long* g_mlp_timeline; }
 
 extern "C" {
 
@@ -143,6 +143,7 @@ const char* orbit2_last_error(void) { return g_err.c_str(); }
 /* Debug only (not in orbit2.h): device buffer of 5*64*8 int64 that the next
  * attention launches fill with clock64 stamps of CTA 0; NULL disables. */
 void orbit2_debug_attn_timeline(long long* dev_buf) { orbit2::g_attn_timeline = dev_buf; }
+void orbit2_debug_mlp_timeline(long long* dev_buf) { orbit2::g_mlp_timeline = dev_buf; }
 
 orbit2_status orbit2_tiles_plan(const orbit2_config* cfg, orbit2_tile* tiles, int32_t capacity,
                                 orbit2_plan_info* info) {

@@ -225,6 +225,61 @@ __device__ __forceinline__ float gelu_erf_fast(float x) {
   return 0.5f * x * (1.0f + copysignf(erf_abs, x));
 }
 
+// ---- packed fp32 pairs (sm_100a f32x2 FMA-pipe instructions: one issue slot
+// for two lanes' worth of work; the pipe throughput per element is unchanged) ----
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+__device__ __forceinline__ float2 splat2(float k) { return make_float2(k, k); }
+
+// gelu_erf_fast on a pair, with packed f32x2 arithmetic (same formula and
+// rounding-order as gelu_erf_fast up to the f32x2 instructions' own rounding)
+__device__ __forceinline__ float2 gelu2_erf_fast(float2 x) {
+  const float2 u = mul2(make_float2(fabsf(x.x), fabsf(x.y)), splat2(0.70710678118654752f));
+  float2 p = fma2(splat2(0.0000430638f), u, splat2(0.0002765672f));
+  p = fma2(p, u, splat2(0.0001520143f));
+  p = fma2(p, u, splat2(0.0092705272f));
+  p = fma2(p, u, splat2(0.0422820123f));
+  p = fma2(p, u, splat2(0.0705230784f));
+  p = fma2(p, u, splat2(1.0f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(p.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(p.y));
+  t = mul2(t, t);
+  t = mul2(t, t);
+  t = mul2(t, t);
+  t = mul2(t, t);
+  float2 e = fma2(t, splat2(-1.0f), splat2(1.0f));
+  e.x = copysignf(e.x, x.x);
+  e.y = copysignf(e.y, x.y);
+  const float2 h = mul2(x, splat2(0.5f));
+  return fma2(h, e, h);
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "liborbit2.so")
+LIB_PATH = os.environ.get("ORBIT2_LIB") or os.path.join(PKG, "liborbit2.so")   # ORBIT2_LIB: A/B builds
 
 ABI_VERSION = 1
 OK, E_INVALID, E_CAPACITY, E_UNSUPPORTED, E_CUDA, E_NCCL, E_STATE = 0, -1, -2, -3, -4, -5, -6
