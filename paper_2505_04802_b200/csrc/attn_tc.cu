@@ -37,23 +37,21 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
 
 long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timeline
 
-// Build-time knobs, defaults = the measured best on B200 (scripts/ab_kernels.py,
-// C2 B=64: ping-pong 27.2 ms, none 24.5 ms, none + 4/16 polynomial exps 23.2 ms):
-//   ORBIT2_ATTN_SPLIT    softmax warps per query row (1; 2 = 64 keys per warp)
-//   ORBIT2_ATTN_PINGPONG alternate the two Q tiles' exp phases on the MUFU (0)
-//   ORBIT2_ATTN_POLY     exponentials per 16 evaluated on the FMA pipe (4)
-#ifndef ORBIT2_ATTN_SPLIT
-#define ORBIT2_ATTN_SPLIT 1
-#endif
-#ifndef ORBIT2_ATTN_PINGPONG
-#define ORBIT2_ATTN_PINGPONG 0
+// Design choices measured on B200 (scripts/ab_kernels.py, C2 B = 64, attention ms):
+//   ping-pong of the two Q tiles' exp phases (FA4 style)        27.2
+//   two softmax warps per row (64 keys each), with ping-pong   25.9
+//   both tiles' softmax concurrently, one warp per row          24.5   <- kept
+//   + 4 of 16 exponentials on the FMA pipe (ex2_poly)           23.2   <- kept
+// (ping-pong leaves one warp per SM sub-partition in an exp phase, which
+// reaches ~70% of the MUFU rate; two concurrent warps reach ~90%).
+// ORBIT2_ATTN_SKIPMAX: row max only on the first block and when the block's
+// exponential sum leaves the safe range (see the softmax loop).
+#ifndef ORBIT2_ATTN_SKIPMAX
+#define ORBIT2_ATTN_SKIPMAX 0   // measured slower (C2: 26.0 vs 23.8 ms)
 #endif
 
 namespace {
 
-// volatile: keeps the exponentials after the ping-pong named barrier (a plain
-// asm is hoisted above it by the compiler, which re-collides the two tiles'
-// exp phases on the MUFU)
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -77,7 +75,7 @@ __device__ __forceinline__ void ffma2(float& a, float& b, float s, float t) {
 }
 
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.0f);
+  x = fminf(fmaxf(x, -125.0f), 127.0f);   // 2^127 for larger x: the skip-max range check sees it
   const float t = x + 12582912.0f;
   const float f = x - (t - 12582912.0f);
   const float p = fmaf(fmaf(fmaf(0.05500886f, f, 0.24221101f), f, 0.69328296f), f, 1.0f);
@@ -93,15 +91,7 @@ __device__ __forceinline__ float ex2_poly(float x) {
   do {                                                                                   \
     if (tl != nullptr && blockIdx.x == 0 && (blk) < 64) tl[((role) * 64 + (blk)) * 8 + (ev)] = clock64(); \
   } while (0)
-// per-warp exp-phase start / end of the first 16 blocks: tl[2560 + (warp * 16 + blk) * 2 + ev]
-#define TL_WARP(blk, ev)                                                                          \
-  do {                                                                                            \
-    if (tl != nullptr && blockIdx.x == 0 && (blk) < 16 && lane == 0) tl[2560 + (warp * 16 + (blk)) * 2 + (ev)] = clock64(); \
-  } while (0)
 #else
-#define TL_WARP(blk, ev) \
-  do {                   \
-  } while (0)
 #define TL_STAMP(role, blk, ev) \
   do {                          \
   } while (0)
@@ -120,13 +110,8 @@ struct AttnCfg {
   static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
   static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
-  // softmax warps per query row: 2 (each 64 keys) so two warps per SM sub-partition
-  // feed the MUFU during a tile's exp phase; 1 on the smem-P fallback
-  static constexpr int SPLIT = NQ * (128 + DH + 64) <= 512 ? ORBIT2_ATTN_SPLIT : 1;
-  static constexpr int KC = 128 / SPLIT;              // key columns per softmax warp
-  static constexpr int SMT = 128 * SPLIT;             // softmax threads per Q tile
   static constexpr int CTRL_WARPS = 1 + NQ;          // producer (+TMEM alloc), one MMA issuer per Q tile
-  static constexpr int THREADS = 32 * CTRL_WARPS + SMT * NQ;
+  static constexpr int THREADS = 32 * CTRL_WARPS + 128 * NQ;   // + one softmax thread per query row
   // P lives in TMEM (64 columns of bf16 pairs) and feeds the PV MMA as the A
   // operand when TMEM allows: no shared-memory traffic for P (the SS form
   // re-reads the 128 x 16 A tile from smem on every K step, which made the
@@ -138,9 +123,7 @@ struct AttnCfg {
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
   static constexpr int ONES_BYTES = 4096;             // bf16 ones, 16 rows x 128 keys (K-major SW128)
   static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
-  static constexpr int XBYTES = NQ * 2 * SPLIT * 128 * 4 + NQ * SPLIT * 128 * 4;   // row max / sum exchange
-  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + XBYTES +
-                              1024 + 512;
+  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -148,6 +131,8 @@ struct AttnCfg {
 // stay <= 2^8 (exact in bf16's exponent range, fp32 accumulation) and the
 // O rescale in TMEM is rare.  Mathematically identical softmax (R18).
 constexpr float kRescaleLog2 = 8.0f;
+constexpr bool kSkipMax = ORBIT2_ATTN_SKIPMAX != 0;
+constexpr float kSumMax = 18446744073709551616.0f;   // 2^64: skip-max range bound of a block's row sum
 #ifndef ORBIT2_ATTN_POLY
 #define ORBIT2_ATTN_POLY 4
 #endif
@@ -197,9 +182,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
   uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
   uint8_t* sOnes = sP + NQ * C::PBUF * C::P_SMEM;    // [ONES_BYTES]
-  float* xmax = reinterpret_cast<float*>(sOnes + C::ONES_BYTES);   // [NQ][2][SPLIT][128]
-  float* xsum = xmax + NQ * 2 * C::SPLIT * 128;                    // [NQ][SPLIT][128]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(xmax) + C::XBYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
   uint64_t* q_full = bar;                           // [QBUF]
   uint64_t* q_empty = q_full + C::QBUF;             // [QBUF]
   uint64_t* k_full = q_empty + C::QBUF;             // [KST]
@@ -212,7 +195,6 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done (P buffer free, O updated)
   uint64_t* o_free = p_free + NQ * C::PBUF;         // [NQ]  epilogue has read O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + NQ);
-  float* zero_slot = reinterpret_cast<float*>(tmem_slot + 1);   // holds 0.0f (see ping-pong)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -230,13 +212,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       tc::mbar_init(&v_full[s], 1);
       tc::mbar_init(&v_empty[s], NQ);
     }
-    *zero_slot = 0.0f;
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
-      tc::mbar_init(&s_free[s], C::SMT);
-      tc::mbar_init(&p_full[s], C::SMT);
+      tc::mbar_init(&s_free[s], 128);
+      tc::mbar_init(&p_full[s], 128);
       for (int u = 0; u < C::PBUF; ++u) tc::mbar_init(&p_free[s * C::PBUF + u], 1);
-      tc::mbar_init(&o_free[s], C::SMT);
+      tc::mbar_init(&o_free[s], 128);
     }
     tc::fence_barrier_init();
   }
@@ -396,181 +377,167 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     }
   } else {
     // ---------------- softmax / correction / epilogue ----------------
-    // SPLIT warps per query row: warp (qt, half, q) owns rows q*32.. (TMEM lane
-    // quarter q) and key columns half*KC.. of every S block, O columns
-    // half*DH/SPLIT.. ; row maxima and sums are combined through shared memory.
-    constexpr int SPLIT = C::SPLIT, KC = C::KC, OC = DH / SPLIT;
-    // (any 4 consecutive warps cover the 4 TMEM lane quarters warp % 4)
-    const int qt = (warp - C::CTRL_WARPS) / (4 * SPLIT);
-    const int half = ((warp - C::CTRL_WARPS) / 4) % SPLIT;
+    // Thread = query row i of Q tile qt (TMEM lane i: warp w reads lane quarter
+    // w % 4; any 4 consecutive warps cover the quarters).  Both tiles' softmax
+    // warps run concurrently (two warps per SM sub-partition feed the MUFU).
+    const int qt = (warp - C::CTRL_WARPS) / 4;
     const int q = warp & 3;
     const int i = q * 32 + lane;                   // query row within the Q tile
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + qt * C::TCOLS;
-    const uint32_t s_addr = lane_base + half * KC;
-    const uint32_t o_addr = lane_base + 128 + half * OC;
-    const uint32_t p_tm = lane_base + 128 + DH + C::SUMC + half * (KC / 2);
+    const uint32_t s_addr = lane_base;
+    const uint32_t o_addr = lane_base + 128;
+    const uint32_t p_tm = lane_base + 128 + DH + C::SUMC;
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     uint64_t* my_p_free = p_free + qt * C::PBUF;
-    const uint32_t xbar = 3 + qt;                  // named barrier of this tile's SMT threads
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
     for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
       const Item it = item_info<NQ>(ch, heads, id);
       if (qt >= it.nq) continue;
       float m_ref = -INFINITY, l_run = 0.f;
-      const bool tlr = (warp & 3) == 0 && lane == 0 && half == 0;
+      const bool tlr = q == 0 && lane == 0;
+      // Only rows inside the tile take part in the (warp-uniform) range votes, so
+      // results do not depend on packing, chunking or the rank assignment.
       const bool row_valid = it.q0 + qt * 128 + i < it.n;
       for (int j = 0; j < it.nkb; ++j, ++cs) {
         if (tlr) TL_STAMP(qt, cs, 0);
         tc::mbar_wait(&s_full[qt], cs & 1);
         if (tlr) TL_STAMP(qt, cs, 1);
         tc::tc_fence_after();
-        float sv[KC];
+        float sv[128];
         {
           uint32_t* r = reinterpret_cast<uint32_t*>(sv);
 #pragma unroll
-          for (int c0 = 0; c0 < KC; c0 += 32)
+          for (int c0 = 0; c0 < 128; c0 += 32)
             tc::tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(r + c0));
           tc::tmem_ld_wait();
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&s_free[qt]);               // TMEM S columns may take the next S
         if (tlr) TL_STAMP(qt, cs, 2);
-        const int kvalid = it.n - j * 128 - half * KC;
-        if (kvalid < KC) {
+        const int kvalid = it.n - j * 128;
+        if (kvalid < 128) {
 #pragma unroll
-          for (int c = 0; c < KC; ++c)
+          for (int c = 0; c < 128; ++c)
             if (c >= kvalid) sv[c] = -INFINITY;
         }
-        float m0 = sv[0], m1 = sv[1], m2 = sv[2], m3 = sv[3];
+        auto row_max = [&]() {
+          float m0 = sv[0], m1 = sv[1], m2 = sv[2], m3 = sv[3];
 #pragma unroll
-        for (int c = 4; c < KC; c += 4) {
-          m0 = fmaxf(m0, sv[c]); m1 = fmaxf(m1, sv[c + 1]);
-          m2 = fmaxf(m2, sv[c + 2]); m3 = fmaxf(m3, sv[c + 3]);
-        }
-        float mloc = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
-        if (SPLIT > 1) {   // combine with the other warp(s) of these rows (double-buffered slot)
-          float* xm = xmax + ((qt * 2 + (cs & 1)) * SPLIT) * 128;
-          xm[half * 128 + i] = mloc;
-          asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(C::SMT) : "memory");
+          for (int c = 4; c < 128; c += 4) {
+            m0 = fmaxf(m0, sv[c]); m1 = fmaxf(m1, sv[c + 1]);
+            m2 = fmaxf(m2, sv[c + 2]); m3 = fmaxf(m3, sv[c + 3]);
+          }
+          return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl;
+        };
+        // O rescale by 2^(m_ref - m_new) (tcgen05.ld/st are warp-collective: callers
+        // take the decision warp-uniformly); needs the previous PV complete.
+        auto rescale = [&](float m_new) {
+          const float alpha = ex2(m_ref - m_new);
+          l_run *= alpha;
 #pragma unroll
-          for (int h2 = 0; h2 < SPLIT; ++h2) mloc = fmaxf(mloc, xm[h2 * 128 + i]);
-        }
-        const float m_blk = mloc * sl;
-        if (tlr) TL_STAMP(qt, cs, 3);
-        // previous PV finished: P columns free and O complete
-        if (cs >= (uint32_t)C::PBUF) tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
-        if (tlr) TL_STAMP(qt, cs, 4);
-        // Conditional rescale (tcgen05.ld/st are warp-collective: warp-uniform decision;
-        // all warps of a row see the same maxima).  Only rows inside the tile vote, so
-        // the result is independent of packing, chunking and rank assignment.
-        const bool rescaled = j > 0 && __any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2);
-        if (j == 0 || rescaled) {
-          const float m_new = fmaxf(m_blk, m_ref);
-          if (rescaled) {
-            tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
-            tc::tc_fence_after();
-            const float alpha = ex2(m_ref - m_new);
-            l_run *= alpha;
+          for (int c0 = 0; c0 < DH; c0 += 16) {
+            uint32_t r[16];
+            tc::tmem_ld16(o_addr + c0, r);
+            tc::tmem_ld_wait();
 #pragma unroll
-            for (int c0 = 0; c0 < OC; c0 += 16) {
-              uint32_t r[16];
-              tc::tmem_ld16(o_addr + c0, r);
-              tc::tmem_ld_wait();
-#pragma unroll
-              for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
-              tc::tmem_st16(o_addr + c0, r);
-            }
+            for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * alpha);
+            tc::tmem_st16(o_addr + c0, r);
           }
           m_ref = m_new;
-        }
-        // Exp phases of the two Q tiles alternate on the MUFU (A_j, B_j, A_{j+1}, ...):
-        // named barrier 1 = "tile 0 may start", 2 = "tile 1 may start".
-        const bool pingpong = ORBIT2_ATTN_PINGPONG && it.nq == 2;
-        if (pingpong) {
-          if (qt == 0 && j > 0) asm volatile("bar.sync 1, %0;" ::"r"(2 * C::SMT) : "memory");
-          if (qt == 1) asm volatile("bar.sync 2, %0;" ::"r"(2 * C::SMT) : "memory");
-        }
-        // Data dependency on a shared-memory load issued after the barrier: the
-        // scheduler otherwise hoists the MUFU work above BAR.SYNC (it only
-        // orders memory operations), re-colliding the two tiles' exp phases.
-        float zero_dep;
-        asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(zero_dep) : "r"(tc::smem_u32(zero_slot)) : "memory");
-        const float m_use = m_ref + zero_dep;
-        if (tlr) TL_STAMP(qt, cs, 7);
-        TL_WARP(cs, 0);
-        // probabilities -> bf16 P into TMEM (A operand of the PV MMA), fp32 row sums
-        float rs0 = 0.f, rs1 = 0.f;
-        if constexpr (C::P_TMEM) {
+        };
+        // p = 2^(s * log2(e)/sqrt(d) - m_ref) -> bf16 P (TMEM: A operand of the PV MMA;
+        // smem when TMEM is short), returns the fp32 row sum of this block
+        auto exps = [&]() {
+          float rs0 = 0.f, rs1 = 0.f;
+          if constexpr (C::P_TMEM) {
 #pragma unroll
-          for (int c0 = 0; c0 < KC; c0 += 64) {
-            uint32_t pk[32];
+            for (int c0 = 0; c0 < 128; c0 += 64) {
+              uint32_t pk[32];
 #pragma unroll
-            for (int e = 0; e < 64; e += 2) {
-              float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
-              ffma2(x0, x1, sl, -m_use);                   // FFMA2: both (s*c - m) in one instruction
-              const bool poly = (e & 15) < kPolyPer16;
-              const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
-              rs0 += p0;
-              rs1 += p1;
-              pk[e / 2] = tc::pack_bf16(p0, p1);           // column = keys (2c, 2c+1), lower key in low half
+              for (int e = 0; e < 64; e += 2) {
+                float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
+                ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
+                const bool poly = (e & 15) < kPolyPer16;
+                const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
+                rs0 += p0;
+                rs1 += p1;
+                pk[e / 2] = tc::pack_bf16(p0, p1);         // column = keys (2c, 2c+1), lower key in low half
+              }
+              tc::tmem_st32(p_tm + c0 / 2, pk);
             }
-            tc::tmem_st32(p_tm + c0 / 2, pk);
-          }
-        } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
-          uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_SMEM + i * 128;
-          const int sw = i & 7;
+          } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
+            uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_SMEM + i * 128;
+            const int sw = i & 7;
 #pragma unroll
-          for (int c0 = 0; c0 < KC; c0 += 16) {
-            uint32_t pk[8];
+            for (int c0 = 0; c0 < 128; c0 += 16) {
+              uint32_t pk[8];
 #pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
-              ffma2(x0, x1, sl, -m_use);
-              const float p0 = ex2(x0), p1 = ex2(x1);
-              rs0 += p0;
-              rs1 += p1;
-              pk[e / 2] = tc::pack_bf16(p0, p1);
+              for (int e = 0; e < 16; e += 2) {
+                float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
+                ffma2(x0, x1, sl, -m_ref);
+                const float p0 = ex2(x0), p1 = ex2(x1);
+                rs0 += p0;
+                rs1 += p1;
+                pk[e / 2] = tc::pack_bf16(p0, p1);
+              }
+              uint8_t* atom = prow + (c0 >> 6) * 16384;
+              const int cb = (c0 & 63) >> 3;
+              *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+              *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
-            const int ca = half * KC + c0;
-            uint8_t* atom = prow + (ca >> 6) * 16384;
-            const int cb = (ca & 63) >> 3;
-            *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
+          return rs0 + rs1;
+        };
+        // previous PV finished: P columns free and O complete
+        if (cs >= (uint32_t)C::PBUF) tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
+        tc::tc_fence_after();
+        if (tlr) TL_STAMP(qt, cs, 4);
+        // Conditional rescale (R18): the reference max moves only when the block max
+        // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
+        // Skip-max (blocks after the first): exponentiate against the reference
+        // directly and check the block's row sum afterwards: all p >= 0, so
+        // max p <= sum p, and sum <= 2^64 bounds every p (P in bf16 and O, l in fp32
+        // share fp32's exponent range: nothing is lost for p up to that bound).  A
+        // sum outside the range (larger, inf, NaN) redoes the block through the max
+        // path.  Both are the same softmax mathematically.  One call site for the
+        // unrolled exponential loop (instruction cache).
+        bool with_max = j == 0 || !kSkipMax;
+        float l_blk;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+          if (with_max) {
+            const float m_blk = row_max();
+            if (j == 0)
+              m_ref = m_blk;
+            else if (__any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2))
+              rescale(fmaxf(m_blk, m_ref));
+          }
+          if (tlr) TL_STAMP(qt, cs, 3);
+          l_blk = exps();
+          if (with_max || !__any_sync(0xffffffffu, row_valid && !(l_blk <= kSumMax))) break;
+          tc::tmem_st_wait();   // P is rewritten
+          with_max = true;
         }
-        l_run += rs0 + rs1;
-        if (pingpong) {
-          if (qt == 0) asm volatile("bar.arrive 2, %0;" ::"r"(2 * C::SMT) : "memory");
-          if (qt == 1 && j + 1 < it.nkb) asm volatile("bar.arrive 1, %0;" ::"r"(2 * C::SMT) : "memory");
-        }
+        l_run += l_blk;
         if (tlr) TL_STAMP(qt, cs, 5);
-        TL_WARP(cs, 1);
         tc::tmem_st_wait();
         if (!C::P_TMEM) tc::fence_proxy_async_smem();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
         if (tlr) TL_STAMP(qt, cs, 6);
       }
-      // epilogue: combined row sum, O / l for this warp's DH/SPLIT columns
-      if (SPLIT > 1) {
-        float* xs = xsum + qt * SPLIT * 128;
-        xs[half * 128 + i] = l_run;
-        asm volatile("bar.sync %0, %1;" ::"r"(xbar), "r"(C::SMT) : "memory");
-        l_run = 0.f;
-#pragma unroll
-        for (int h2 = 0; h2 < SPLIT; ++h2) l_run += xs[h2 * 128 + i];
-      }
+      // epilogue: O / l
       tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
       tc::tc_fence_after();
       const int qrow = it.q0 + qt * 128 + i;
       const float inv = 1.f / l_run;
 #pragma unroll
-      for (int c0 = 0; c0 < OC; c0 += 16) {
+      for (int c0 = 0; c0 < DH; c0 += 16) {
         uint32_t r[16];
         tc::tmem_ld16(o_addr + c0, r);
         tc::tmem_ld_wait();
         if (qrow < it.n) {
-          uint4* dst = reinterpret_cast<uint4*>(out + (it.base + qrow) * (int64_t)D + it.h * DH + half * OC + c0);
+          uint4* dst = reinterpret_cast<uint4*>(out + (it.base + qrow) * (int64_t)D + it.h * DH + c0);
 #pragma unroll
           for (int u = 0; u < 2; ++u)
             dst[u] = make_uint4(tc::pack_bf16(__uint_as_float(r[8 * u]) * inv, __uint_as_float(r[8 * u + 1]) * inv),

@@ -55,11 +55,65 @@ __global__ void gather_kernel(const float* __restrict__ x, T* __restrict__ patch
   for (int wr = threadIdx.x; wr < t.pad_w; wr += blockDim.x) rowinfo[row0 + wr] = make_int2(u, t.pad_x0 + wr);
 }
 
+// Staged variant: one CTA per (padded token row, tile, b) walks the row in
+// segments of GSEG tokens.  Input pixels are read row-contiguously (coalesced:
+// for each (v, dy) the p * GSEG pixels of one image row), scattered into a
+// shared-memory [token][din] block (row stride padded against bank conflicts),
+// then written out as whole 16-byte pieces of patch rows.
+constexpr int GSEG = 64;
+template <typename T>
+__global__ void __launch_bounds__(256) gather_staged_kernel(const float* __restrict__ x, T* __restrict__ patches,
+                                                            int2* __restrict__ rowinfo, ChunkDev ch, int V, int H,
+                                                            int W, int p, int din, int din_pad) {
+  extern __shared__ __align__(16) uint8_t gsm[];
+  T* sp = reinterpret_cast<T*>(gsm);
+  const int ld = din_pad + 16 / (int)sizeof(T);   // +16 bytes per row
+  const DevTile t = ch.tiles[ch.tb + blockIdx.y];
+  const int ur = blockIdx.x;
+  if (ur >= t.pad_h) return;
+  const int b = blockIdx.z;
+  const int64_t row0 = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0) + (int64_t)ur * t.pad_w;
+  const int u = t.pad_y0 + ur;
+  const int pp = p * p;
+  const float* xb = x + (int64_t)b * V * H * W;
+  constexpr int VEC = 16 / sizeof(T);
+  for (int w0 = 0; w0 < t.pad_w; w0 += GSEG) {
+    const int nw = min(GSEG, t.pad_w - w0);
+    const int npx = nw * p;                           // image columns of the segment
+    const int xpix0 = p * (t.pad_x0 + w0);
+    __syncthreads();                                   // previous segment's stores have read sp
+    for (int idx = threadIdx.x; idx < V * p * npx; idx += blockDim.x) {
+      const int vd = idx / npx, xl = idx - vd * npx;   // vd = v * p + dy
+      const int v = vd / p, dy = vd - v * p;
+      const int yy = min(max(p * u + dy, 0), H - 1);
+      const int xx = min(max(xpix0 + xl, 0), W - 1);
+      const int wr = xl / p, dx = xl - wr * p;
+      sp[wr * ld + v * pp + dy * p + dx] = to_out<T>(__ldg(xb + ((int64_t)v * H + yy) * W + xx));
+    }
+    for (int idx = threadIdx.x; idx < nw * (din_pad - din); idx += blockDim.x) {
+      const int wr = idx / (din_pad - din), c = din + idx - wr * (din_pad - din);
+      sp[wr * ld + c] = to_out<T>(0.f);
+    }
+    __syncthreads();
+    const int nv = din_pad / VEC;
+    for (int idx = threadIdx.x; idx < nw * nv; idx += blockDim.x) {
+      const int wr = idx / nv, c = (idx - wr * nv) * VEC;
+      *reinterpret_cast<uint4*>(patches + (row0 + w0 + wr) * din_pad + c) =
+          *reinterpret_cast<const uint4*>(sp + wr * ld + c);
+    }
+  }
+  for (int wr = threadIdx.x; wr < t.pad_w; wr += blockDim.x) rowinfo[row0 + wr] = make_int2(u, t.pad_x0 + wr);
+}
+
 template <typename T>
 void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch, int B, int V, int H, int W,
                    int p, int din, int din_pad, int max_pad_h, cudaStream_t st) {
   dim3 grid(max_pad_h, ch.tc, B);
-  gather_kernel<T><<<grid, 256, 0, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
+  const size_t smem = (size_t)GSEG * (din_pad + 16 / sizeof(T)) * sizeof(T);
+  if (din_pad % (16 / sizeof(T)) == 0 && smem <= 48 * 1024)
+    gather_staged_kernel<T><<<grid, 256, smem, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
+  else
+    gather_kernel<T><<<grid, 256, 0, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
 }
 template void launch_gather<float>(const float*, float*, int2*, const ChunkDev&, int, int, int, int, int, int, int,
                                    int, cudaStream_t);
@@ -231,11 +285,89 @@ __global__ void stitch_kernel(const T* __restrict__ tile_out, const float* __res
   }
 }
 
+// Vectorised variant for P % 4 == 0 (every shipped configuration): one CTA per
+// (token row ur of a tile's core, tile, b) writes the P x K output rows of that
+// token row.  A thread owns 4 consecutive output columns X (one float4 store per
+// (k, al), one 8-byte tile_out load: the 4 columns share a token and be..be+3);
+// column interpolation weights are computed once per thread, row weights once per
+// al, no integer division in the inner loops.  The token row's tile_out slab
+// (core_w x K P^2 values) is re-read across (k, al) from L1.
+template <typename T>
+__global__ void __launch_bounds__(128) stitch4_kernel(const T* __restrict__ tile_out, const float* __restrict__ x,
+                                                      float* __restrict__ out, ChunkDev ch,
+                                                      const int32_t* __restrict__ cmap, int V, int H, int W, int K,
+                                                      int s, int P) {
+  const DevTile t = ch.tiles[ch.tb + blockIdx.y];
+  const int ur = blockIdx.x;
+  if (ur >= t.core_h) return;
+  const int b = blockIdx.z;
+  const int X0 = t.core_x0 * P, NX4 = t.core_w * P / 4;
+  const int64_t sH = (int64_t)s * H, sW = (int64_t)s * W;
+  const int64_t trow0 = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0) + (int64_t)ur * t.core_w;
+  const int Nh = K * P * P;
+  const float inv_s = 1.0f / (float)s;
+  for (int c4 = threadIdx.x; c4 < NX4; c4 += blockDim.x) {
+    const int xr = 4 * c4;
+    const int wr = xr / P, be = xr - wr * P;
+    const int X = X0 + xr;
+    int xa[4], xb[4];
+    float lx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float sx = fmaxf(((float)(X + e) + 0.5f) * inv_s - 0.5f, 0.f);
+      xa[e] = min((int)sx, W - 1);
+      xb[e] = min(xa[e] + 1, W - 1);
+      lx[e] = sx - (float)xa[e];
+    }
+    const T* trow = tile_out + (trow0 + wr) * Nh + be;
+    for (int al = 0; al < P; ++al) {
+      const int Y = t.core_y0 * P + ur * P + al;
+      const float sy = fmaxf(((float)Y + 0.5f) * inv_s - 0.5f, 0.f);
+      const int y0 = min((int)sy, H - 1), y1 = min(y0 + 1, H - 1);
+      const float ly = sy - (float)y0;
+      for (int k = 0; k < K; ++k) {
+        float vit[4];
+        const T* src = trow + (k * P + al) * P;
+        if constexpr (sizeof(T) == 2) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(src);
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+          vit[0] = __low2float(lo); vit[1] = __high2float(lo);
+          vit[2] = __low2float(hi); vit[3] = __high2float(hi);
+        } else {
+          const float4 v = *reinterpret_cast<const float4*>(src);
+          vit[0] = v.x; vit[1] = v.y; vit[2] = v.z; vit[3] = v.w;
+        }
+        const float* pl = x + ((int64_t)b * V + cmap[k]) * H * W;
+        const float* r0 = pl + (int64_t)y0 * W;
+        const float* r1 = pl + (int64_t)y1 * W;
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a00 = __ldg(r0 + xa[e]), a01 = __ldg(r0 + xb[e]);
+          const float a10 = __ldg(r1 + xa[e]), a11 = __ldg(r1 + xb[e]);
+          const float up = (1.f - ly) * ((1.f - lx[e]) * a00 + lx[e] * a01) + ly * ((1.f - lx[e]) * a10 + lx[e] * a11);
+          o[e] = vit[e] + up;
+        }
+        *reinterpret_cast<float4*>(out + (((int64_t)b * K + k) * sH + Y) * sW + X) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
 template <typename T>
 void launch_stitch(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap, int B,
                    int V, int H, int W, int K, int s, int P, int max_core_h, cudaStream_t st) {
-  dim3 grid(max_core_h * P, ch.tc, B);
-  stitch_kernel<T><<<grid, 256, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+  // float4 stores need X and sW multiples of 4 (X0 = core_x0 * P: P % 4 == 0 and
+  // sW = s W = P (W / p) ...: checked explicitly)
+  const bool vec = P % 4 == 0 && ((int64_t)s * W) % 4 == 0;
+  if (vec) {
+    dim3 grid(max_core_h, ch.tc, B);
+    stitch4_kernel<T><<<grid, 128, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+  } else {
+    dim3 grid(max_core_h * P, ch.tc, B);
+    stitch_kernel<T><<<grid, 256, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+  }
 }
 template void launch_stitch<float>(const float*, const float*, float*, const ChunkDev&, const int32_t*, int, int,
                                    int, int, int, int, int, int, cudaStream_t);

@@ -158,6 +158,16 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _req(t, dtype, name):
+    """The ABI takes raw pointers: check what the C side cannot (dtype, device,
+    contiguity) so a float64 or strided tensor fails here instead of being
+    reinterpreted."""
+    if not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous CUDA {dtype} tensor, got {t.dtype} "
+                        f"on {t.device} (contiguous={t.is_contiguous()})")
+    return t
+
+
 def _stream(stream) -> int:
     import torch
     if stream is None:
@@ -207,10 +217,17 @@ class Context:
 
     # -- the graded calls --------------------------------------------------
     def orbit2_reslim_forward(self, packed, x_dev, tile_begin, tile_count, tile_out, stream=None):
+        import torch
+        _req(x_dev, torch.float32, "x_dev")
+        _req(tile_out, torch.bfloat16 if self.bf16 else torch.float32, "tile_out")
         _check(lib.orbit2_reslim_forward(self.handle, _ptr(packed), _ptr(x_dev), tile_begin, tile_count,
                                          _ptr(tile_out), _stream(stream)), "orbit2_reslim_forward")
 
     def orbit2_stitch(self, tile_out, x_dev, tile_begin, tile_count, out, stream=None):
+        import torch
+        _req(x_dev, torch.float32, "x_dev")
+        _req(out, torch.float32, "out")
+        _req(tile_out, torch.bfloat16 if self.bf16 else torch.float32, "tile_out")
         _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
                                  _stream(stream)), "orbit2_stitch")
 

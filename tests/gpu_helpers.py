@@ -31,7 +31,7 @@ def run_cuda(w, x: np.ndarray, blob: np.ndarray, precision: int, chunk_tiles: in
     wd = torch.from_numpy(np.ascontiguousarray(blob)).cuda()
     B = x.shape[0]
     if out is None:
-        out = torch.full((B, w.K, w.scale * w.H, w.scale * w.W), float("nan"), device="cuda")
+        out = torch.full((B, w.K, w.scale * w.H, w.scale * w.W), float("nan"), dtype=torch.float32, device="cuda")
     for r in (range(world_size) if ranks is None else ranks):
         cfg = o2.config_from(w, batch=B, precision=precision, chunk_tiles=chunk_tiles,
                              world_size=world_size, rank=r)

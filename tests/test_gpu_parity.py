@@ -213,3 +213,21 @@ def test_bench_configuration_sampled_samples():
         e = rel_err(got[b:b + 1], ref)
         print(f"C2 B=64 sample {b}: rel_err={e:.3e}")
         assert e <= BF16_TOL
+
+
+@pytest.mark.gpu
+def test_binding_rejects_wrong_dtypes():
+    """The ABI takes raw pointers: the binding refuses float64 / strided tensors
+    instead of letting the kernels reinterpret them (regression: a process-wide
+    float64 default dtype once produced a float64 output buffer)."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w, x, blob = _case("C1")
+    ctx = o2.Context(o2.config_from(w, precision=BF16))
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    xd = torch.from_numpy(x).cuda()
+    bad_out = torch.zeros((1, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float64, device="cuda")
+    with pytest.raises(TypeError):
+        ctx.forward(packed, xd, out=bad_out)
+    with pytest.raises(TypeError):
+        ctx.forward(packed, xd.double())

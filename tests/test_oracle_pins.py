@@ -16,7 +16,16 @@ import torch.nn.functional as F
 from oracle import reslim_tiles as O
 from workloads import get_config, make_input, make_weights, constant_input, ramp_input
 
-torch.set_default_dtype(torch.float64)
+
+
+@pytest.fixture(autouse=True)
+def _fp64_default():
+    """The torch library pins run in fp64; restored afterwards (a process-wide
+    float64 default would leak into the GPU tests' float32 buffers)."""
+    old = torch.get_default_dtype()
+    torch.set_default_dtype(torch.float64)
+    yield
+    torch.set_default_dtype(old)
 
 
 def small_problem(**kw):
