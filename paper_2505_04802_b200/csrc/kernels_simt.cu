@@ -62,7 +62,7 @@ __global__ void gather_kernel(const float* __restrict__ x, T* __restrict__ patch
 // then written out as whole 16-byte pieces of patch rows.
 constexpr int GSEG = 64;
 template <typename T>
-__global__ void __launch_bounds__(256) gather_staged_kernel(const float* __restrict__ x, T* __restrict__ patches,
+__global__ void __launch_bounds__(128) gather_staged_kernel(const float* __restrict__ x, T* __restrict__ patches,
                                                             int2* __restrict__ rowinfo, ChunkDev ch, int V, int H,
                                                             int W, int p, int din, int din_pad) {
   extern __shared__ __align__(16) uint8_t gsm[];
@@ -82,13 +82,14 @@ __global__ void __launch_bounds__(256) gather_staged_kernel(const float* __restr
     const int npx = nw * p;                           // image columns of the segment
     const int xpix0 = p * (t.pad_x0 + w0);
     __syncthreads();                                   // previous segment's stores have read sp
-    for (int idx = threadIdx.x; idx < V * p * npx; idx += blockDim.x) {
-      const int vd = idx / npx, xl = idx - vd * npx;   // vd = v * p + dy
-      const int v = vd / p, dy = vd - v * p;
-      const int yy = min(max(p * u + dy, 0), H - 1);
-      const int xx = min(max(xpix0 + xl, 0), W - 1);
+    for (int xl = threadIdx.x; xl < npx; xl += blockDim.x) {   // thread = image column
       const int wr = xl / p, dx = xl - wr * p;
-      sp[wr * ld + v * pp + dy * p + dx] = to_out<T>(__ldg(xb + ((int64_t)v * H + yy) * W + xx));
+      const float* src = xb + min(max(xpix0 + xl, 0), W - 1);
+      T* dst = sp + wr * ld + dx;
+      for (int dy = 0; dy < p; ++dy) {
+        const float* s0 = src + (int64_t)min(max(p * u + dy, 0), H - 1) * W;
+        for (int v = 0; v < V; ++v) dst[v * pp + dy * p] = to_out<T>(__ldg(s0 + (int64_t)v * H * W));
+      }
     }
     for (int idx = threadIdx.x; idx < nw * (din_pad - din); idx += blockDim.x) {
       const int wr = idx / (din_pad - din), c = din + idx - wr * (din_pad - din);
@@ -111,7 +112,7 @@ void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch
   dim3 grid(max_pad_h, ch.tc, B);
   const size_t smem = (size_t)GSEG * (din_pad + 16 / sizeof(T)) * sizeof(T);
   if (din_pad % (16 / sizeof(T)) == 0 && smem <= 48 * 1024)
-    gather_staged_kernel<T><<<grid, 256, smem, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
+    gather_staged_kernel<T><<<grid, 128, smem, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
   else
     gather_kernel<T><<<grid, 256, 0, st>>>(x, patches, rowinfo, ch, V, H, W, p, din, din_pad);
 }
