@@ -41,7 +41,9 @@ long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timel
 //   ping-pong of the two Q tiles' exp phases (FA4 style)        27.2
 //   two softmax warps per row (64 keys each), with ping-pong   25.9
 //   both tiles' softmax concurrently, one warp per row          24.5   <- kept
-//   + 4 of 16 exponentials on the FMA pipe (ex2_poly)           23.2   <- kept
+//   + 4 of 16 exponentials on the FMA pipe (ex2_poly)           23.2
+//   + packed f32x2 polynomial and row sums (fewer issue slots)  21.7
+//     with 2 of 16 on the FMA pipe                              21.4   <- kept
 // (ping-pong leaves one warp per SM sub-partition in an exp phase, which
 // reaches ~70% of the MUFU rate; two concurrent warps reach ~90%).
 // ORBIT2_ATTN_SKIPMAX: row max only on the first block and when the block's
@@ -49,6 +51,7 @@ long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timel
 #ifndef ORBIT2_ATTN_SKIPMAX
 #define ORBIT2_ATTN_SKIPMAX 0   // measured slower (C2: 26.0 vs 23.8 ms)
 #endif
+constexpr bool kSkipMaxBuild = ORBIT2_ATTN_SKIPMAX != 0;
 
 namespace {
 
@@ -74,8 +77,22 @@ __device__ __forceinline__ void ffma2(float& a, float& b, float s, float t) {
       : "f"(s), "f"(t));
 }
 
+// packed pair version: same arithmetic in f32x2 instructions (half the issue slots)
+__device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
+  float2 x = make_float2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+  if (kSkipMaxBuild) x = make_float2(fminf(x.x, 127.0f), fminf(x.y, 127.0f));
+  const float2 t = tc::add2(x, tc::splat2(12582912.0f));
+  const float2 f = tc::fma2(tc::add2(t, tc::splat2(-12582912.0f)), tc::splat2(-1.0f), x);
+  float2 p = tc::fma2(tc::splat2(0.05500886f), f, tc::splat2(0.24221101f));
+  p = tc::fma2(p, f, tc::splat2(0.69328296f));
+  p = tc::fma2(p, f, tc::splat2(1.0f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ float ex2_poly(float x) {
-  x = fminf(fmaxf(x, -125.0f), 127.0f);   // 2^127 for larger x: the skip-max range check sees it
+  x = fmaxf(x, -125.0f);
+  if (kSkipMaxBuild) x = fminf(x, 127.0f);   // 2^127 for larger x: the skip-max range check sees it
   const float t = x + 12582912.0f;
   const float f = x - (t - 12582912.0f);
   const float p = fmaf(fmaf(fmaf(0.05500886f, f, 0.24221101f), f, 0.69328296f), f, 1.0f);
@@ -134,7 +151,7 @@ constexpr float kRescaleLog2 = 8.0f;
 constexpr bool kSkipMax = ORBIT2_ATTN_SKIPMAX != 0;
 constexpr float kSumMax = 18446744073709551616.0f;   // 2^64: skip-max range bound of a block's row sum
 #ifndef ORBIT2_ATTN_POLY
-#define ORBIT2_ATTN_POLY 4
+#define ORBIT2_ATTN_POLY 2
 #endif
 // exponentials per 16 computed on the FMA pipe (ex2_poly) instead of the MUFU
 constexpr int kPolyPer16 = ORBIT2_ATTN_POLY;
@@ -454,15 +471,18 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             for (int c0 = 0; c0 < 128; c0 += 64) {
               uint32_t pk[32];
 #pragma unroll
+              float2 rs = make_float2(0.f, 0.f);
               for (int e = 0; e < 64; e += 2) {
                 float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
                 ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
-                const bool poly = (e & 15) < kPolyPer16;
-                const float p0 = poly ? ex2_poly(x0) : ex2(x0), p1 = poly ? ex2_poly(x1) : ex2(x1);
-                rs0 += p0;
-                rs1 += p1;
-                pk[e / 2] = tc::pack_bf16(p0, p1);         // column = keys (2c, 2c+1), lower key in low half
+                float2 pr;
+                if ((e & 15) < kPolyPer16) pr = ex2_poly2(x0, x1);
+                else pr = make_float2(ex2(x0), ex2(x1));
+                rs = tc::add2(rs, pr);                     // packed row-sum accumulation
+                pk[e / 2] = tc::pack_bf16(pr.x, pr.y);     // column = keys (2c, 2c+1), lower key in low half
               }
+              rs0 += rs.x;
+              rs1 += rs.y;
               tc::tmem_st32(p_tm + c0 / 2, pk);
             }
           } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
