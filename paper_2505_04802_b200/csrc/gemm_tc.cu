@@ -58,10 +58,25 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   return r == CUDA_SUCCESS;
 }
 
+// 2-D fp32 row-major tensor [rows][ld], box [box_rows][box_cols]
+bool make_tmap_f32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                   int box_cols, CUtensorMapSwizzle swz) {
+  if (!tma_available()) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
+constexpr int LN_CHUNK_BYTES = BM * 32 * 4;   // *_LN staging: 128 rows x 32 fp32 columns (16 KB)
 
 template <int EPI, bool OUT_BF16>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row, int n0, const uint32_t (&r)[32]) {
@@ -145,7 +160,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS>
 __global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const __grid_constant__ CUtensorMap tmC, int64_t M, int64_t Ncols, int K, EpiParams ep) {
+                   const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M,
+                   int64_t Ncols, int K, EpiParams ep) {
   // Persistent: CTA c owns output tiles c, c + gridDim.x, ...  Normal mode:
   // m-major, n fastest (consecutive CTAs share the activation block through
   // L2).  TRANS mode computes C^T = W X^T (A = weight rows, B = tokens) so the
@@ -157,16 +173,19 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS = 2 * BN;
+  constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
+  constexpr int STG_BYTES = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the __shared__ array (keeps the shared address space: STS, not generic ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + 8 * 2 * 2048);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;    // [2] accumulator ready
   uint64_t* tempty = tfull + 2;        // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* zfull = tempty + 2;        // *_LN: [2 warpgroups][2] z chunk landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zfull + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
@@ -178,20 +197,23 @@ __global__ void __launch_bounds__(384, 1)
     if (TRANS) { m0 = (tile % num_m) * BM; n0 = (tile / num_m) * BN; }
     else       { m0 = (tile / num_n) * BM; n0 = (tile % num_n) * BN; }
   };
-  uint8_t* stg = sB + STAGES * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16)
+  uint8_t* stg = sB + STAGES * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16);
+                                          // *_LN: 2 warpgroups x 2 x (128 x 32 fp32)
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
-    if (TMA_OUT) tc::prefetch_tmap(&tmC);
+    if (TMA_OUT || LN) tc::prefetch_tmap(&tmC);
+    if (LN) tc::prefetch_tmap(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], 256);
+      tc::mbar_init(&tempty[s], LN ? 128 : 256);   // *_LN: one warpgroup drains a buffer
     }
+    for (int s = 0; s < 4; ++s) tc::mbar_init(&zfull[s], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -242,6 +264,144 @@ __global__ void __launch_bounds__(384, 1)
         tc::mma_commit(&tfull[buf]);
       }
     }
+  } else if (LN && warp >= 4) {
+    // ---------------- LayerNorm-fused epilogue (BN == N == 256) ----------------
+    // Warpgroup wg owns TMEM buffer wg, i.e. every other tile; thread = row
+    // (TMEM lane), so the row statistics are thread-local.  Pass 1 over 8 chunks
+    // of 32 columns: z_new = acc + bias + (z | pi), written back to TMEM and
+    // stored through swizzled smem + TMA (z chunks of the RESID form arrive by
+    // TMA two chunks ahead); pass 2: sum (z_new - mean)^2 from TMEM (two-pass
+    // variance, as the LN kernel); pass 3: LN -> bf16 -> smem -> TMA store xn.
+    const int wg = (warp - 4) >> 2;
+    const int q = warp & 3;
+    const int rr = q * 32 + lane;                       // row within the tile
+    const bool issuer = q == 0 && lane == 0;
+    const uint32_t nb = 1 + wg;                         // named barrier of this warpgroup
+    uint8_t* zb = stg + wg * 2 * LN_CHUNK_BYTES;
+    uint64_t* zf = zfull + wg * 2;
+    uint32_t zuse[2] = {0, 0};                          // loads completed per buffer (parity)
+    uint32_t lt = 0;
+    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+      if ((int)(lt & 1) != wg) continue;
+      const uint32_t buf = lt & 1;
+      int64_t m0, n0;
+      tile_mn(tile, m0, n0);
+      const int64_t row = m0 + rr;
+      auto load_z = [&](int c) {                        // issuer only
+        tc::bulk_wait_read<0>();                        // the buffer's previous store has read it
+        tc::mbar_arrive_expect_tx(&zf[c & 1], LN_CHUNK_BYTES);
+        tc::tma_load_2d(&tmC, zb + (c & 1) * LN_CHUNK_BYTES, &zf[c & 1], c * 32, (int32_t)m0);
+      };
+      if (EPI == EPI_RESID_LN && issuer) {
+        load_z(0);
+        load_z(1);
+      }
+      tc::mbar_wait(&tfull[buf], (lt >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+      int2 uw = make_int2(0, 0);
+      if (EPI == EPI_EMBED_LN && row < M) uw = __ldg(ep.rowinfo + row);
+      float sum = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint8_t* sb = zb + (c & 1) * LN_CHUNK_BYTES + rr * 128;   // this row's 128 bytes (SW128)
+        if (EPI == EPI_RESID_LN) {
+          tc::mbar_wait(&zf[c & 1], zuse[c & 1] & 1);
+          ++zuse[c & 1];
+        } else {                                         // staging reuse: the buffer's last store has read it
+          if (issuer) tc::bulk_wait_read<1>();
+          asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
+        }
+        uint32_t r[32];
+        tc::tmem_ld32(taddr + c * 32, r);
+        tc::tmem_ld_wait();
+        float v[32];
+        const float4* b4 = reinterpret_cast<const float4*>(ep.bias + c * 32);
+        const float* pe = nullptr;
+        if (EPI == EPI_EMBED_LN)
+          pe = c * 32 < ep.half ? ep.pos_u + (int64_t)(uw.x + ep.pos_off) * ep.half + c * 32
+                                : ep.pos_w + (int64_t)(uw.y + ep.pos_off) * ep.half + (c * 32 - ep.half);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const float4 bb = __ldg(b4 + u);
+          float4 a;
+          if (EPI == EPI_RESID_LN) a = *reinterpret_cast<const float4*>(sb + ((u ^ (rr & 7)) << 4));
+          else a = __ldg(reinterpret_cast<const float4*>(pe) + u);
+          v[4 * u] = __uint_as_float(r[4 * u]) + bb.x + a.x;
+          v[4 * u + 1] = __uint_as_float(r[4 * u + 1]) + bb.y + a.y;
+          v[4 * u + 2] = __uint_as_float(r[4 * u + 2]) + bb.z + a.z;
+          v[4 * u + 3] = __uint_as_float(r[4 * u + 3]) + bb.w + a.w;
+          *reinterpret_cast<float4*>(sb + ((u ^ (rr & 7)) << 4)) =
+              make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sum += v[j];
+          r[j] = __float_as_uint(v[j]);
+        }
+        tc::tmem_st32(taddr + c * 32, r);
+        tc::fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
+        if (issuer) {
+          tc::tma_store_2d(&tmC, zb + (c & 1) * LN_CHUNK_BYTES, c * 32, (int32_t)m0);
+          tc::bulk_commit();
+          if (EPI == EPI_RESID_LN && c + 2 < 8) load_z(c + 2);
+        }
+      }
+      tc::tmem_st_wait();
+      const float mean = sum * (1.0f / 256.0f);
+      float var = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld32(taddr + c * 32, r);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float d = __uint_as_float(r[j]) - mean;
+          var += d * d;
+        }
+      }
+      const float rstd = rsqrtf(var * (1.0f / 256.0f) + 1e-5f);
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tc::tmem_ld32(taddr + c * 32, r);
+        tc::tmem_ld_wait();
+        if (c == 7) {                                   // accumulator buffer drained
+          tc::tc_fence_before();
+          tc::mbar_arrive(&tempty[buf]);
+        }
+        uint8_t* sb = zb + (c & 1) * LN_CHUNK_BYTES;    // bf16 box [128 rows][64 B], SWIZZLE_64B
+        if (issuer) tc::bulk_wait_read<1>();
+        asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
+        const float4* g4 = reinterpret_cast<const float4*>(ep.ln_g + c * 32);
+        const float4* e4 = reinterpret_cast<const float4*>(ep.ln_b + c * 32);
+        uint8_t* srow = sb + rr * 64;
+        const int sw = (rr >> 1) & 3;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 gg = __ldg(g4 + 2 * u + h), ee = __ldg(e4 + 2 * u + h);
+            const int j = 8 * u + 4 * h;
+            w[2 * h] = tc::pack_bf16((__uint_as_float(r[j]) - mean) * rstd * gg.x + ee.x,
+                                     (__uint_as_float(r[j + 1]) - mean) * rstd * gg.y + ee.y);
+            w[2 * h + 1] = tc::pack_bf16((__uint_as_float(r[j + 2]) - mean) * rstd * gg.z + ee.z,
+                                         (__uint_as_float(r[j + 3]) - mean) * rstd * gg.w + ee.w);
+          }
+          *reinterpret_cast<uint4*>(srow + ((u ^ sw) << 4)) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        tc::fence_proxy_async_smem();
+        asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
+        if (issuer) {
+          tc::tma_store_2d(&tmD, sb, c * 32, (int32_t)m0);
+          tc::bulk_commit();
+        }
+      }
+    }
+    if (issuer) tc::bulk_wait_all();
   } else if (warp >= 4) {
     // ---------------- epilogue: 2 warpgroups, each half of the columns ----------------
     const int q = warp & 3;                  // TMEM lane quarter of this warp
@@ -356,16 +516,22 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
   const GemmOperand& ka = TRANS ? Bw : A;
   const GemmOperand& kb = TRANS ? A : Bw;
   const int64_t Mk = TRANS ? N : M, Nk = TRANS ? M : N;
-  CUtensorMap ta, tb, tcm;
+  CUtensorMap ta, tb, tcm, tdm;
   if (!make_tmap_bf16(&ta, ka.ptr, ka.rows, K, ka.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
+  constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
+  tcm = ta;   // unused unless set below
+  tdm = ta;
   if (TMA_OUT) {
     if (!make_tmap_bf16(&tcm, ep.C, M, N, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
-  } else {
-    tcm = ta;   // unused
   }
-  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + 8 * 2 * 2048 + 1024 + 256;
+  if (LN) {   // z fp32 [M][N] in 128 x 32 boxes (SW128), xn bf16 [M][N] in 128 x 32 boxes (SW64)
+    if (!make_tmap_f32(&tcm, ep.C, M, N, ep.ldc, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+    if (!make_tmap_bf16(&tdm, ep.xn, M, N, N, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
+  }
+  constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
+  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + STG + 1024 + 256;
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
@@ -374,7 +540,7 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
   }
   const int64_t tiles = ((Mk + BM - 1) / BM) * ((Nk + BN - 1) / BN);
   const int grid = (int)std::min<int64_t>(tiles, num_sms());
-  kern<<<grid, 384, smem, st>>>(ta, tb, tcm, Mk, Nk, (int)K, ep);
+  kern<<<grid, 384, smem, st>>>(ta, tb, tcm, tdm, Mk, Nk, (int)K, ep);
   return true;
 }
 
@@ -383,6 +549,11 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
 bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
                     int64_t K, const EpiParams& ep, cudaStream_t st) {
   if (K % BK != 0 || M <= 0 || N <= 0) return false;
+  if (epi == EPI_RESID_LN || epi == EPI_EMBED_LN) {   // whole rows in one 256-column tile
+    if (N != 256 || ep.ldc != 256) return false;
+    return epi == EPI_RESID_LN ? launch_impl<256, 3, EPI_RESID_LN, false>(A, Bw, M, N, K, ep, st)
+                               : launch_impl<256, 3, EPI_EMBED_LN, false>(A, Bw, M, N, K, ep, st);
+  }
   // Residual update: transposed tiles (features on TMEM lanes) for coalesced z.
   if (epi == EPI_RESID && N % BM == 0) return launch_impl<256, 3, EPI_RESID, false, true>(A, Bw, M, N, K, ep, st);
   // BN = 256 halves the shared-memory operand traffic per FLOP; 128 when N is

@@ -14,6 +14,10 @@ enum Epi : int {
   EPI_GELU = 1,    // C[m,n] = T(gelu(acc + bias[n]))      (R9 exact-erf GELU)
   EPI_RESID = 2,   // z[m,n] += acc + bias[n]               (fp32 residual stream)
   EPI_EMBED = 3,   // z[m,n]  = acc + bias[n] + pi(u_m, w_m)  (R7, R8)
+  // LayerNorm-fused forms (N == 256 == one tile's columns: whole rows in the
+  // epilogue): the updated z row is written and LN(z) -> xn (bf16) as well
+  EPI_RESID_LN = 4,   // z += acc + bias; xn = LN(z)     (O-projection + LN2)
+  EPI_EMBED_LN = 5,   // z = acc + bias + pi; xn = LN(z) (patch embed + LN1 of block 0)
 };
 
 struct EpiParams {
@@ -26,6 +30,9 @@ struct EpiParams {
   const float* pos_w;      // EMBED: [(Wp+2h)][D/2]
   int32_t pos_off;         // halo h: table row = coord + h
   int32_t half;            // D/2
+  void* xn;                // *_LN: bf16 LayerNorm output [M][N]
+  const float* ln_g;       // *_LN: LayerNorm gain / bias [N]
+  const float* ln_b;
 };
 
 struct GemmOperand {

@@ -41,6 +41,7 @@ struct Ctx {
   std::map<std::string, std::pair<int64_t, double>> acc;
   bool sync_check = false;
   bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
+  bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -188,6 +189,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->sync_check = sc && sc[0] == '1';
   const char* um = std::getenv("ORBIT2_UNFUSED_MLP");
   c->unfused_mlp = um && um[0] == '1';
+  const char* ul = std::getenv("ORBIT2_UNFUSED_LN");
+  c->unfused_ln = ul && ul[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
@@ -359,13 +362,26 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       cudaError_t e = cudaMemsetAsync(qkv + M * 3 * D, 0, (size_t)(mrow - M) * 3 * D * sizeof(bf16), st);
       if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("memset: ") + cudaGetErrorString(e));
     }
-    ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    // D == 256: one GEMM tile holds whole rows, so LayerNorms that follow a GEMM
+    // run in its epilogue (embed -> LN1 of block 0, O-projection -> LN2)
+    const bool ln_fused = D == 256 && !c->unfused_ln;
+    if (ln_fused && cf.depth > 0) {
+      EpiParams e = emb;
+      e.xn = xn;
+      e.ln_g = wf(w.layers[0].ln1_g);
+      e.ln_b = wf(w.layers[0].ln1_b);
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED_LN, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, e));
+    } else {
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
-      ORBIT2_TRY(run(c, "layernorm", st, [&] {
-        launch_layernorm<bf16>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
-        return true;
-      }));
+      if (!(ln_fused && l == 0)) {
+        ORBIT2_TRY(run(c, "layernorm", st, [&] {
+          launch_layernorm<bf16>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
+          return true;
+        }));
+      }
       EpiParams e{};
       e.bias = wf(L.b_qkv); e.C = qkv; e.ldc = 3 * D;
       ORBIT2_TRY(gemm("qkv_gemm", EPI_BIAS, 1, xn, mrow, D, L.w_qkv, 3 * D, D, M, e));
@@ -373,11 +389,18 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
         return launch_attention_tc(qkv, mrow, ao, cd, B, (int)D, cf.heads, p.d, st);
       }));
       e = EpiParams{}; e.bias = wf(L.b_o); e.C = z; e.ldc = D;
-      ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID, 0, ao, mrow, D, L.w_o, D, D, M, e));
-      ORBIT2_TRY(run(c, "layernorm", st, [&] {
-        launch_layernorm<bf16>(z, wf(L.ln2_g), wf(L.ln2_b), xn, M, (int)D, nullptr, st);
-        return true;
-      }));
+      if (ln_fused) {
+        e.xn = xn;
+        e.ln_g = wf(L.ln2_g);
+        e.ln_b = wf(L.ln2_b);
+        ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID_LN, 0, ao, mrow, D, L.w_o, D, D, M, e));
+      } else {
+        ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID, 0, ao, mrow, D, L.w_o, D, D, M, e));
+        ORBIT2_TRY(run(c, "layernorm", st, [&] {
+          launch_layernorm<bf16>(z, wf(L.ln2_g), wf(L.ln2_b), xn, M, (int)D, nullptr, st);
+          return true;
+        }));
+      }
       if (D == 256 && !c->unfused_mlp) {   // hidden tile stays on chip
         ORBIT2_TRY(run(c, "mlp_fused", st, [&] {
           return launch_mlp_fused(xn, mrow, W8 + L.w_1, wf(L.b_1), W8 + L.w_2, wf(L.b_2), z, M, (int)D, st);

@@ -231,3 +231,18 @@ def test_binding_rejects_wrong_dtypes():
         ctx.forward(packed, xd, out=bad_out)
     with pytest.raises(TypeError):
         ctx.forward(packed, xd.double())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", ["ORBIT2_UNFUSED_LN", "ORBIT2_UNFUSED_MLP"])
+def test_unfused_paths_match_oracle(env, monkeypatch):
+    """The separate-kernel forms (LayerNorm after embed / O-projection; MLP as
+    two GEMMs) stay within tolerance of the oracle, like the fused default."""
+    w, x, blob = _case("C2", H=48, W=96, tiles_y=2, tiles_x=3)
+    ref = oracle_full(w, x, blob)[0]
+    fused = run_cuda(w, x, blob, BF16)
+    monkeypatch.setenv(env, "1")
+    sep = run_cuda(w, x, blob, BF16)
+    assert rel_err(sep, ref) < BF16_TOL
+    assert rel_err(fused, ref) < BF16_TOL
+    assert rel_err(sep, fused) < BF16_TOL
