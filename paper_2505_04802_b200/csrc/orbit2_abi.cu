@@ -376,7 +376,7 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
     }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
-      if (!(ln_fused && l == 0)) {
+      if (!(ln_fused && l == 0)) {   // block 0's LN1 runs in the embed epilogue
         ORBIT2_TRY(run(c, "layernorm", st, [&] {
           launch_layernorm<bf16>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
           return true;
