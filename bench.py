@@ -176,8 +176,11 @@ def class_work(w, info, B):
     # HBM kernels: unique algorithmic bytes
     out["tile_gather"] = ("hbm", B * (4.0 * V * w.H * w.W + 2.0 * npad * Din))
     out["stitch_residual"] = ("hbm", B * (2.0 * K * sH * sW + 4.0 * K * w.H * w.W + 4.0 * K * sH * sW))
-    # layernorm: (2L+1) launches, fp32 read + bf16 write of D per row
-    out["layernorm"] = ("hbm", B * (2 * L * npad * D * 6.0 + ncore * D * 6.0))
+    # layernorm launches: fp32 read + bf16 write of D per row.  D = 256: the LNs after
+    # the embedding and the O-projection run in those GEMMs' epilogues, leaving
+    # LN1 of blocks 1.. and the final (core rows) LN; otherwise 2L + 1 launches.
+    ln_full = max(L - 1, 0) if D == 256 else 2 * L
+    out["layernorm"] = ("hbm", B * (ln_full * npad * D * 6.0 + ncore * D * 6.0))
     return out
 
 

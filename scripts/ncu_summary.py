@@ -14,13 +14,13 @@ METRICS = {
     "gpu__time_duration.sum": "time_ns",
     "dram__bytes_read.sum": "dram_read_B",
     "dram__bytes_write.sum": "dram_write_B",
-    "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
     "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pct",
     "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tmem_tensor_pct",
     "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active": "xu_pct",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pct",
     "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active": "alu_pct",
-    "sm__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
+    "sm__issue_active.avg.pct_of_peak_sustained_elapsed": "issue_pct",
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
     "sm__cycles_elapsed.avg.per_second": "sm_hz",
 }
@@ -41,22 +41,32 @@ def main():
     rep, out = sys.argv[1], sys.argv[2]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, data = rows[0], rows[2:]
+    hdr, units, data = rows[0], rows[1], rows[2:]
     ik = hdr.index("Kernel Name")
+    scale = {"ns": 1.0, "us": 1e3, "ms": 1e6, "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+             "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     recs = []
     for r in data:
         rec = {"kernel": kernel_class(r[ik], None), "name": r[ik][:120]}
         for m, short in METRICS.items():
-            rec[short] = r[hdr.index(m)] if m in hdr else ""
+            if m not in hdr:
+                rec[short] = ""
+                continue
+            v, u = r[hdr.index(m)], units[hdr.index(m)]
+            if u in scale and v not in ("", "n/a"):   # normalise to ns / bytes
+                v = repr(float(v.replace(",", "")) * scale[u])
+            rec[short] = v
         recs.append(rec)
     with open(out, "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(recs[0].keys()))
         w.writeheader()
         w.writerows(recs)
     for rec in recs:
-        print(f"{rec['kernel']:28s} {float(rec['time_ns'] or 0) / 1e3:9.1f} us  dram {rec['dram_pct']:>6s}%  "
-              f"tensor {rec['tmem_tensor_pct']:>6s}%  xu {rec['xu_pct']:>6s}%  fma {rec['fma_pct']:>6s}%  "
-              f"issue {rec['issue_pct']:>6s}%")
+        print(f"{rec['kernel']:24s} {float(rec['time_ns'] or 0) / 1e3:8.1f} us  "
+              f"tensor {float(rec['tmem_tensor_pct'] or 0):5.1f}%  xu {float(rec['xu_pct'] or 0):5.1f}%  "
+              f"fma {float(rec['fma_pct'] or 0):5.1f}%  issue {float(rec['issue_pct'] or 0):5.1f}%  "
+              f"dram {(float(rec['dram_read_B'] or 0) + float(rec['dram_write_B'] or 0)) / 1e6:8.1f} MB "
+              f"= {(float(rec['dram_read_B'] or 0) + float(rec['dram_write_B'] or 0)) / max(float(rec['time_ns'] or 1), 1):6.0f} GB/s")
     if len(sys.argv) > 5:
         tj, batch, wl = sys.argv[3], int(sys.argv[4]), sys.argv[5]
         traffic = {}
