@@ -66,6 +66,15 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* s
                "r"(smem_u32(smem_src)), "r"(x), "r"(y)
                : "memory");
 }
+// 2-D tensor reduce-add (f32): global[box at (c0, c1)] += smem box (bulk async-group)
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* smem_src, int32_t c0,
+                                                  int32_t c1) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N committed bulk groups still READ their shared-memory source
 template <int N>
@@ -256,28 +265,29 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 splat2(float k) { return make_float2(k, k); }
 
-// gelu_erf_fast on a pair, with packed f32x2 arithmetic (same formula and
-// rounding-order as gelu_erf_fast up to the f32x2 instructions' own rounding)
+// GELU of a pair in packed f32x2 arithmetic, same erf approximation (A&S 7.1.28)
+// rearranged to save FMA-pipe work: with a = |x| and q = Phi(-a) = 0.5 erfc(a / sqrt2)
+// = (2^(1/16) p(a / sqrt2))^-16, GELU(x) = relu(x) - a q for both signs of x.  The
+// 1/sqrt2, the 0.5 and the 2^(1/16) are folded into the coefficients (c_k = 2^(1/16)
+// a_k 2^(-k/2)); the polynomial runs in na = -a (odd coefficients negated) so the
+// last step is one FMA: y = na * q + relu(x).  12 packed FMA-pipe instructions per
+// pair (fp32: |err| <= 7.1e-7 vs the exact GELU over [-12, 12]).
 __device__ __forceinline__ float2 gelu2_erf_fast(float2 x) {
-  const float2 u = mul2(make_float2(fabsf(x.x), fabsf(x.y)), splat2(0.70710678118654752f));
-  float2 p = fma2(splat2(0.0000430638f), u, splat2(0.0002765672f));
-  p = fma2(p, u, splat2(0.0001520143f));
-  p = fma2(p, u, splat2(0.0092705272f));
-  p = fma2(p, u, splat2(0.0422820123f));
-  p = fma2(p, u, splat2(0.0705230784f));
-  p = fma2(p, u, splat2(1.0f));
+  const float2 na = make_float2(-fabsf(x.x), -fabsf(x.y));
+  float2 p = fma2(splat2(5.6212996640e-06f), na, splat2(-5.1055209009e-05f));
+  p = fma2(p, na, splat2(3.9686137011e-05f));
+  p = fma2(p, na, splat2(-3.4227392389e-03f));
+  p = fma2(p, na, splat2(2.2076998457e-02f));
+  p = fma2(p, na, splat2(-5.2075163037e-02f));
+  p = fma2(p, na, splat2(1.0442737824e+00f));
   float2 t;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(p.x));
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(p.y));
   t = mul2(t, t);
   t = mul2(t, t);
   t = mul2(t, t);
-  t = mul2(t, t);
-  float2 e = fma2(t, splat2(-1.0f), splat2(1.0f));
-  e.x = copysignf(e.x, x.x);
-  e.y = copysignf(e.y, x.y);
-  const float2 h = mul2(x, splat2(0.5f));
-  return fma2(h, e, h);
+  t = mul2(t, t);   // q
+  return fma2(na, t, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
