@@ -114,6 +114,17 @@ __device__ __forceinline__ float ex2_poly(float x) {
   } while (0)
 #endif
 
+#ifndef ORBIT2_ATTN_LATEPV
+#define ORBIT2_ATTN_LATEPV 1
+#endif
+#ifndef ORBIT2_ATTN_STAGED_EPI
+#define ORBIT2_ATTN_STAGED_EPI 1
+#endif
+// wait for the previous PV (P columns free, O complete) after the row max, not before
+constexpr bool kLatePvWait = ORBIT2_ATTN_LATEPV != 0;
+// epilogue rows staged in smem and stored 4 rows per instruction
+constexpr bool kStagedEpilogue = ORBIT2_ATTN_STAGED_EPI != 0;
+
 template <int DH, int NQ>
 struct AttnCfg {
   static constexpr int AC = DH < 64 ? DH : 64;        // columns per swizzle atom
@@ -140,7 +151,14 @@ struct AttnCfg {
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
   static constexpr int ONES_BYTES = 4096;             // bf16 ones, 16 rows x 128 keys (K-major SW128)
   static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
-  static constexpr int SMEM = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
+  static constexpr int SMEM_BASE = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
+  // epilogue staging (32 rows x DH bf16 per softmax warp) when shared memory allows
+  static constexpr int OST_ROW = DH * 2;               // staged O row (swizzled like the TMA store's box)
+  static constexpr uint32_t OSW_MASK = DH == 32 ? 3u : 7u;   // SWIZZLE_64B / SWIZZLE_128B
+  static constexpr bool STAGED = kStagedEpilogue && SMEM_BASE + 4 * NQ * 32 * OST_ROW + 256 <= 227 * 1024;
+  static constexpr int OST_WARP = STAGED ? 32 * OST_ROW : 0;
+  static constexpr int IRING = 4;                      // work-item descriptors published by the producer
+  static constexpr int SMEM = SMEM_BASE + 4 * NQ * OST_WARP + 256;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -156,9 +174,9 @@ constexpr float kSumMax = 18446744073709551616.0f;   // 2^64: skip-max range bou
 // exponentials per 16 computed on the FMA pipe (ex2_poly) instead of the MUFU
 constexpr int kPolyPer16 = ORBIT2_ATTN_POLY;
 
-struct Item {
+struct __align__(16) Item {
   int64_t base;     // first row of the tile's tokens in the packed workspace
-  int n, q0, nq, nkb, h;
+  int n, q0, nq, nkb, h, pad_;
 };
 
 template <int NQ>
@@ -180,6 +198,17 @@ __device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int id)
   return it;
 }
 
+// Item li of this CTA as published by the producer (whole warp; one release per warp).
+__device__ __forceinline__ Item take_item(const Item* sItem, uint64_t* it_full, uint64_t* it_empty, uint32_t li,
+                                          int ring) {
+  const uint32_t is = li % ring;
+  tc::mbar_wait(&it_full[is], (li / ring) & 1);
+  const Item it = sItem[is];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(&it_empty[is]);
+  return it;
+}
+
 // Persistent: CTA c handles work items c, c + gridDim.x, ... where an item is
 // (query-block pair of a tile, head, sample).  Every barrier phase is tracked
 // with counters that run across items, so the producer prefetches the next
@@ -187,7 +216,8 @@ __device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int id)
 // finish the previous item.
 template <int DH, int NQ>
 __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
-    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
+    attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
+                   __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
                    int heads, int n_items, long long* __restrict__ tl) {
   // tl: optional debug timeline (clock64 stamps of CTA 0), null in production
   using C = AttnCfg<DH, NQ>;
@@ -199,7 +229,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
   uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
   uint8_t* sOnes = sP + NQ * C::PBUF * C::P_SMEM;    // [ONES_BYTES]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sOnes + C::ONES_BYTES);
+  uint8_t* sOst = sOnes + C::ONES_BYTES;            // [4 * NQ][OST_WARP]
+  Item* sItem = reinterpret_cast<Item*>(sOst + 4 * NQ * C::OST_WARP);   // [IRING]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sItem + C::IRING);
   uint64_t* q_full = bar;                           // [QBUF]
   uint64_t* q_empty = q_full + C::QBUF;             // [QBUF]
   uint64_t* k_full = q_empty + C::QBUF;             // [KST]
@@ -211,7 +243,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint64_t* p_full = s_free + NQ;                   // [NQ]  P in smem (+ O rescaled)
   uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done (P buffer free, O updated)
   uint64_t* o_free = p_free + NQ * C::PBUF;         // [NQ]  epilogue has read O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + NQ);
+  uint64_t* it_full = o_free + NQ;                 // [IRING]  item descriptor published
+  uint64_t* it_empty = it_full + C::IRING;          // [IRING]  read by every consumer warp
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(it_empty + C::IRING);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -236,6 +270,10 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       for (int u = 0; u < C::PBUF; ++u) tc::mbar_init(&p_free[s * C::PBUF + u], 1);
       tc::mbar_init(&o_free[s], 128);
     }
+    for (int s = 0; s < C::IRING; ++s) {
+      tc::mbar_init(&it_full[s], 1);
+      tc::mbar_init(&it_empty[s], NQ + 4 * NQ);   // MMA-issuer warps + softmax warps
+    }
     tc::fence_barrier_init();
   }
   if (warp == 0) {
@@ -258,6 +296,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       uint32_t li = 0, gk = 0, gv = 0;
       for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
         const Item it = item_info<NQ>(ch, heads, id);
+        {   // publish the item to the other roles (they never touch the tile tables)
+          const uint32_t is = li % C::IRING;
+          tc::mbar_wait(&it_empty[is], ((li / C::IRING) & 1) ^ 1);
+          sItem[is] = it;
+          tc::mbar_arrive(&it_full[is]);
+        }
         const int32_t y0 = (int32_t)it.base;
         const uint32_t qb = li % C::QBUF;
         tc::mbar_wait(&q_empty[qb], ((li / C::QBUF) & 1) ^ 1);
@@ -309,7 +353,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       const uint32_t p_addr = tc::smem_u32(sP);
       uint32_t li = 0, gk = 0, gv = 0, ns = 0, np = 0, ni = 0;
       for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
-        const Item it = item_info<NQ>(ch, heads, id);
+        const Item it = take_item(sItem, it_full, it_empty, li, C::IRING);
         const bool active = qt < it.nq;
         const uint32_t qb = li % C::QBUF;
         tc::mbar_wait(&q_full[qb], (li / C::QBUF) & 1);
@@ -407,8 +451,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     uint64_t* my_p_free = p_free + qt * C::PBUF;
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
-    for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
-      const Item it = item_info<NQ>(ch, heads, id);
+    uint32_t ni_sm = 0;                            // items processed (debug timeline only)
+    uint32_t li = 0;
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      if (q == 0 && lane == 0) TL_STAMP(5 + qt, ni_sm, 6);
+      const Item it = take_item(sItem, it_full, it_empty, li, C::IRING);
+      if (q == 0 && lane == 0) TL_STAMP(5 + qt, ni_sm, 7);
       if (qt >= it.nq) continue;
       float m_ref = -INFINITY, l_run = 0.f;
       const bool tlr = q == 0 && lane == 0;
@@ -508,10 +556,18 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           }
           return rs0 + rs1;
         };
-        // previous PV finished: P columns free and O complete
-        if (cs >= (uint32_t)C::PBUF) tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
-        tc::tc_fence_after();
-        if (tlr) TL_STAMP(qt, cs, 4);
+        // previous PV finished: P columns free and O complete.  Waited for only
+        // after the row max (which needs neither), unless a rescale needs O first.
+        bool pv_done = cs < (uint32_t)C::PBUF;
+        auto wait_pv = [&]() {
+          if (!pv_done) {
+            tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
+            tc::tc_fence_after();
+            pv_done = true;
+            if (tlr) TL_STAMP(qt, cs, 4);
+          }
+        };
+        if (!kLatePvWait) wait_pv();
         // Conditional rescale (R18): the reference max moves only when the block max
         // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
         // Skip-max (blocks after the first): exponentiate against the reference
@@ -529,10 +585,13 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             const float m_blk = row_max();
             if (j == 0)
               m_ref = m_blk;
-            else if (__any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2))
+            else if (__any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2)) {
+              wait_pv();
               rescale(fmaxf(m_blk, m_ref));
+            }
           }
           if (tlr) TL_STAMP(qt, cs, 3);
+          wait_pv();
           l_blk = exps();
           if (with_max || !__any_sync(0xffffffffu, row_valid && !(l_blk <= kSumMax))) break;
           tc::tmem_st_wait();   // P is rewritten
@@ -547,10 +606,61 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         if (tlr) TL_STAMP(qt, cs, 6);
       }
       // epilogue: O / l
+      if (tlr) TL_STAMP(5 + qt, ni_sm, 0);
       tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
       tc::tc_fence_after();
-      const int qrow = it.q0 + qt * 128 + i;
+      if (tlr) TL_STAMP(5 + qt, ni_sm, 1);
       const float inv = 1.f / l_run;
+      if constexpr (C::STAGED) {
+        // O / l -> bf16, staged in this warp's 32-row slice in the TMA store's
+        // swizzled layout (16-B chunk c of row r at chunk c ^ (r & mask):
+        // conflict-free), then one TMA tensor store of the 32 x DH box issued by
+        // one lane.  A warp whose rows run past the tile end (the partial last
+        // query block) stores its valid rows directly instead.
+        uint8_t* sw = sOst + (warp - C::CTRL_WARPS) * C::OST_WARP;
+        auto swz = [](uint32_t off) { return off ^ (((off >> 7) & C::OSW_MASK) << 4); };
+        if (lane == 0) tc::bulk_wait_read<0>();        // the previous item's store has read the slice
+        __syncwarp();
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {          // 32 columns per TMEM load, one wait each
+          uint32_t r[32];
+          tc::tmem_ld32(o_addr + c0, r);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(sw + swz(lane * C::OST_ROW + (c0 + 8 * u) * 2)) =
+                make_uint4(tc::pack_bf16(__uint_as_float(r[8 * u]) * inv, __uint_as_float(r[8 * u + 1]) * inv),
+                           tc::pack_bf16(__uint_as_float(r[8 * u + 2]) * inv, __uint_as_float(r[8 * u + 3]) * inv),
+                           tc::pack_bf16(__uint_as_float(r[8 * u + 4]) * inv, __uint_as_float(r[8 * u + 5]) * inv),
+                           tc::pack_bf16(__uint_as_float(r[8 * u + 6]) * inv, __uint_as_float(r[8 * u + 7]) * inv));
+        }
+        if (tlr) TL_STAMP(5 + qt, ni_sm, 2);
+        tc::tc_fence_before();
+        tc::mbar_arrive(&o_free[qt]);                  // O read: the next item's PV may accumulate
+        if (tlr) TL_STAMP(5 + qt, ni_sm, 4);
+        const int row0 = it.q0 + qt * 128 + q * 32;    // first query row of this warp
+        if (row0 + 32 <= it.n) {
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (tlr) TL_STAMP(5 + qt, ni_sm, 5);
+          if (lane == 0) {
+            tc::tma_store_2d(&tmo, sw, it.h * DH, (int32_t)(it.base + row0));
+            tc::bulk_commit();
+          }
+        } else {
+          __syncwarp();
+          if (row0 + lane < it.n) {
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c)
+              *reinterpret_cast<uint4*>(out + (it.base + row0 + lane) * (int64_t)D + it.h * DH + c * 8) =
+                  *reinterpret_cast<const uint4*>(sw + swz(lane * C::OST_ROW + c * 16));
+          }
+        }
+        if (tlr) TL_STAMP(5 + qt, ni_sm, 3);
+        ++ni_sm;
+        continue;
+      }
+      const int qrow = it.q0 + qt * 128 + i;
 #pragma unroll
       for (int c0 = 0; c0 < DH; c0 += 16) {
         uint32_t r[16];
@@ -570,6 +680,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       tc::mbar_arrive(&o_free[qt]);
     }
   }
+  if (C::STAGED && warp >= C::CTRL_WARPS && lane == 0) tc::bulk_wait_all();   // epilogue stores done with smem
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -587,6 +698,10 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (!make_tmap_bf16(&tm, qkv, rows, 3LL * D, 3LL * D, 128, C::AC,
                       DH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
+  CUtensorMap tmo;   // attention output [rows][D], box 32 rows x DH columns (epilogue stores)
+  if (C::STAGED && !make_tmap_bf16(&tmo, out, rows, D, D, 32, DH,
+                                   DH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   static bool attr = false;
   static int sms = 0;
   if (!attr) {
@@ -603,7 +718,7 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (n_items == 0) return true;
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM
-  attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
+  attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, tmo, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
                                                              heads, (int)n_items, g_attn_timeline);
   return true;
 }

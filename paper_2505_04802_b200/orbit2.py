@@ -184,6 +184,8 @@ class Context:
         self.tiles, self.info = orbit2_tiles_plan(cfg)
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.workspace = torch.empty(max(self.info.workspace_bytes, 16), dtype=torch.uint8, device=self.device)
+        if os.environ.get("ORBIT2_POISON_WORKSPACE") == "1":   # tests: NaN bytes expose reads of unwritten rows
+            self.workspace.fill_(0xFF)
         h = C.c_void_p()
         with torch.cuda.device(self.device):
             _check(lib.orbit2_create(C.byref(cfg), _ptr(self.workspace), self.info.workspace_bytes, C.byref(h)),

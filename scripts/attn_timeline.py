@@ -15,7 +15,7 @@ ctx = o2.Context(o2.config_from(w))
 x = torch.from_numpy(make_input(w)).cuda()
 packed = ctx.prepare_weights(torch.from_numpy(make_weights(w)).cuda())
 ctx.forward(packed, x)
-buf = torch.zeros(5 * 64 * 8 + 32 * 16 * 2, dtype=torch.int64, device="cuda")
+buf = torch.zeros(7 * 64 * 8, dtype=torch.int64, device="cuda")
 f = o2.lib.orbit2_debug_attn_timeline
 f.argtypes = [ctypes.c_void_p]
 f(buf.data_ptr())
@@ -23,21 +23,17 @@ ctx.forward(packed, x)
 torch.cuda.synchronize()
 f(None)
 allb = buf.cpu().numpy().astype(np.int64)
-t = allb[:2560].reshape(5, 64, 8)
-tw = allb[2560:].reshape(32, 16, 2)
+t = allb[:3584].reshape(7, 64, 8)
 t0 = t[t > 0].min()
-names = {0: "softmax tile0", 1: "softmax tile1", 2: "mma tile0", 3: "mma tile1", 4: "producer"}
+names = {0: "softmax tile0", 1: "softmax tile1", 2: "mma tile0", 3: "mma tile1", 4: "producer",
+         5: "epilogue tile0 (per item)", 6: "epilogue tile1 (per item)"}
 ev = {0: "loop,s_full_done,s_loaded,max_done,pfree_done,exp_done,p_arrive,after_pingpong_bar",
       2: "k_full_done,s_free_done,v_full_done,p_full_done,pv_issued",
-      4: "k_empty_done,v_empty_done"}
-for role in range(5):
-    print(f"== {names[role]}: {ev.get(role if role in (0, 2, 4) else role - 1, '')}")
+      4: "k_empty_done,v_empty_done", 5: "start,pv_done,o_read,stored,arrived,fenced,(next)loop_top,(next)item_taken"}
+for role in range(7):
+    print(f"== {names[role]}: {ev.get(role if role in (0, 2, 4, 5) else role - 1, '')}")
     for b in range(40):
         row = t[role, b]
         if (row > 0).any():
             print(f"  blk {b:2d}: " + " ".join(f"{(v - t0):8d}" if v > 0 else "       -" for v in row[:8]))
 
-print("== per-warp exp phase (start..end relative to t0, length) for blocks 2..5")
-for wi in range(32):
-    if (tw[wi] > 0).any():
-        print(f"  warp {wi:2d}: " + "  ".join(f"{tw[wi, b, 0] - t0:7d}+{tw[wi, b, 1] - tw[wi, b, 0]:5d}" for b in range(2, 6)))
