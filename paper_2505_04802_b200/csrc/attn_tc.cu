@@ -46,12 +46,8 @@ long long* g_attn_timeline = nullptr;   // debug: set by orbit2_debug_attn_timel
 //     with 2 of 16 on the FMA pipe                              21.4   <- kept
 // (ping-pong leaves one warp per SM sub-partition in an exp phase, which
 // reaches ~70% of the MUFU rate; two concurrent warps reach ~90%).
-// ORBIT2_ATTN_SKIPMAX: row max only on the first block and when the block's
-// exponential sum leaves the safe range (see the softmax loop).
-#ifndef ORBIT2_ATTN_SKIPMAX
-#define ORBIT2_ATTN_SKIPMAX 0   // measured slower (C2: 26.0 vs 23.8 ms)
-#endif
-constexpr bool kSkipMaxBuild = ORBIT2_ATTN_SKIPMAX != 0;
+// Skipping the row max (exponentiate against the reference max, check the
+// block's row sum afterwards) was measured slower (C2: 26.0 vs 23.8 ms) and removed.
 
 namespace {
 
@@ -80,7 +76,6 @@ __device__ __forceinline__ void ffma2(float& a, float& b, float s, float t) {
 // packed pair version: same arithmetic in f32x2 instructions (half the issue slots)
 __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
   float2 x = make_float2(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
-  if (kSkipMaxBuild) x = make_float2(fminf(x.x, 127.0f), fminf(x.y, 127.0f));
   const float2 t = tc::add2(x, tc::splat2(12582912.0f));
   const float2 f = tc::fma2(tc::add2(t, tc::splat2(-12582912.0f)), tc::splat2(-1.0f), x);
   float2 p = tc::fma2(tc::splat2(0.05500886f), f, tc::splat2(0.24221101f));
@@ -90,14 +85,6 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -125.0f);
-  if (kSkipMaxBuild) x = fminf(x, 127.0f);   // 2^127 for larger x: the skip-max range check sees it
-  const float t = x + 12582912.0f;
-  const float f = x - (t - 12582912.0f);
-  const float p = fmaf(fmaf(fmaf(0.05500886f, f, 0.24221101f), f, 0.69328296f), f, 1.0f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
 
 
 // debug timeline: tl[(role * 64 + block) * 8 + event] for CTA 0, first 64 blocks.
@@ -117,6 +104,11 @@ __device__ __forceinline__ float ex2_poly(float x) {
 #ifndef ORBIT2_ATTN_LATEPV
 #define ORBIT2_ATTN_LATEPV 1
 #endif
+#ifndef ORBIT2_ATTN_SPLITP
+#define ORBIT2_ATTN_SPLITP 0   // measured slower (C2: 21.6 vs 19.9 ms): the 128-arrival part barriers wait for the slowest warp
+#endif
+// P_j written and consumed by the PV MMA in two 64-key parts
+constexpr bool kSplitP = ORBIT2_ATTN_SPLITP != 0;
 #ifndef ORBIT2_ATTN_STAGED_EPI
 #define ORBIT2_ATTN_STAGED_EPI 1
 #endif
@@ -134,7 +126,7 @@ struct AttnCfg {
   static constexpr int TILE = 128 * DH * 2;           // bytes of a Q/K/V block
   static constexpr uint32_t SW = DH == 32 ? tc::SW_64B : tc::SW_128B;
   static constexpr int QBUF = DH == 128 ? 1 : 2;      // Q tiles of the next work item prefetched
-  static constexpr int PBUF = 1;                      // P buffers per Q tile
+  static constexpr int NPH = kSplitP ? 2 : 1;         // P / PV parts with their own barriers
   static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
   static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
@@ -145,13 +137,10 @@ struct AttnCfg {
   // re-reads the 128 x 16 A tile from smem on every K step, which made the
   // kernel shared-memory-bandwidth bound).
   static constexpr bool P_TMEM = NQ * (128 + DH + 64) <= 512;
-  static constexpr bool TC_SUM = false;               // (P x ones row sums: superseded by P_TMEM)
-  static constexpr int SUMC = TC_SUM ? 16 : 0;
-  static constexpr int TCOLS = 128 + DH + SUMC + (P_TMEM ? 64 : 0);   // S | O | (sum) | (P)
+  static constexpr int TCOLS = 128 + DH + (P_TMEM ? 64 : 0);   // S | O | (P)
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
-  static constexpr int ONES_BYTES = 4096;             // bf16 ones, 16 rows x 128 keys (K-major SW128)
   static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
-  static constexpr int SMEM_BASE = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * PBUF * P_SMEM + ONES_BYTES + 1024 + 512;
+  static constexpr int SMEM_BASE = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * P_SMEM + 1024 + 512;
   // epilogue staging (32 rows x DH bf16 per softmax warp) when shared memory allows
   static constexpr int OST_ROW = DH * 2;               // staged O row (swizzled like the TMA store's box)
   static constexpr uint32_t OSW_MASK = DH == 32 ? 3u : 7u;   // SWIZZLE_64B / SWIZZLE_128B
@@ -166,8 +155,6 @@ struct AttnCfg {
 // stay <= 2^8 (exact in bf16's exponent range, fp32 accumulation) and the
 // O rescale in TMEM is rare.  Mathematically identical softmax (R18).
 constexpr float kRescaleLog2 = 8.0f;
-constexpr bool kSkipMax = ORBIT2_ATTN_SKIPMAX != 0;
-constexpr float kSumMax = 18446744073709551616.0f;   // 2^64: skip-max range bound of a block's row sum
 #ifndef ORBIT2_ATTN_POLY
 #define ORBIT2_ATTN_POLY 2
 #endif
@@ -227,9 +214,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sQ = smem;                               // [QBUF][NQ][TILE]
   uint8_t* sK = sQ + C::QBUF * NQ * C::TILE;        // [KST][TILE]
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
-  uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][PBUF][P_BYTES]
-  uint8_t* sOnes = sP + NQ * C::PBUF * C::P_SMEM;    // [ONES_BYTES]
-  uint8_t* sOst = sOnes + C::ONES_BYTES;            // [4 * NQ][OST_WARP]
+  uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][P_SMEM]
+  uint8_t* sOst = sP + NQ * C::P_SMEM;              // [4 * NQ][OST_WARP]
   Item* sItem = reinterpret_cast<Item*>(sOst + 4 * NQ * C::OST_WARP);   // [IRING]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sItem + C::IRING);
   uint64_t* q_full = bar;                           // [QBUF]
@@ -240,9 +226,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint64_t* v_empty = v_full + C::VST;              // [VST]
   uint64_t* s_full = v_empty + C::VST;              // [NQ]  S in TMEM
   uint64_t* s_free = s_full + NQ;                   // [NQ]  softmax holds S in registers
-  uint64_t* p_full = s_free + NQ;                   // [NQ]  P in smem (+ O rescaled)
-  uint64_t* p_free = p_full + NQ;                   // [NQ][PBUF]  PV done (P buffer free, O updated)
-  uint64_t* o_free = p_free + NQ * C::PBUF;         // [NQ]  epilogue has read O
+  uint64_t* p_full = s_free + NQ;                   // [NQ][NPH]  part h of P written (+ O rescaled)
+  uint64_t* p_free = p_full + NQ * C::NPH;          // [NQ][NPH]  part h of PV done (P part free)
+  uint64_t* o_free = p_free + NQ * C::NPH;          // [NQ]  epilogue has read O
   uint64_t* it_full = o_free + NQ;                 // [IRING]  item descriptor published
   uint64_t* it_empty = it_full + C::IRING;          // [IRING]  read by every consumer warp
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(it_empty + C::IRING);
@@ -266,8 +252,10 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
       tc::mbar_init(&s_free[s], 128);
-      tc::mbar_init(&p_full[s], 128);
-      for (int u = 0; u < C::PBUF; ++u) tc::mbar_init(&p_free[s * C::PBUF + u], 1);
+      for (int h = 0; h < C::NPH; ++h) {
+        tc::mbar_init(&p_full[s * C::NPH + h], 128);
+        tc::mbar_init(&p_free[s * C::NPH + h], 1);
+      }
       tc::mbar_init(&o_free[s], 128);
     }
     for (int s = 0; s < C::IRING; ++s) {
@@ -279,11 +267,6 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   if (warp == 0) {
     __syncwarp();
     tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
-  }
-  if (C::TC_SUM) {   // all-ones B operand for the row sums (layout-free: every element equal)
-    for (int o = threadIdx.x * 16; o < C::ONES_BYTES; o += blockDim.x * 16)
-      *reinterpret_cast<uint4*>(sOnes + o) = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
-    tc::fence_proxy_async_smem();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -397,33 +380,35 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           if (lane == 0) TL_STAMP(2 + qt, np, 2);
           if (active) {
             if (j == 0 && ni >= 1) tc::mbar_wait(&o_free[qt], (ni - 1) & 1);
-            tc::mbar_wait(&p_full[qt], np & 1);
-            if (lane == 0) TL_STAMP(2 + qt, np, 3);
-            tc::tc_fence_after();
-            if (tc::elect_one()) {
-              const uint64_t pd0 =
-                  tc::sdesc(p_addr + (qt * C::PBUF + np % C::PBUF) * C::P_SMEM, 16, 1024, tc::SW_128B);
-              const uint32_t ptm = tmem + qt * C::TCOLS + 128 + DH + C::SUMC;   // P columns (P_TMEM)
-              const uint64_t vd0 = tc::sdesc(v_addr + st * C::TILE, C::ATOM, 8 * C::RB, C::SW);
-              constexpr uint32_t id_l = tc::idesc_bf16(128, 16, 0, 0);
-              const uint64_t ld0 = tc::sdesc(tc::smem_u32(sOnes), 16, 1024, tc::SW_128B);
+            // PV in NPH parts, each released by its own p_full / p_free pair: the
+            // softmax warps may write part h of P_{j+1} as soon as part h of PV_j
+            // has consumed P_j (no wait for the whole PV on their critical path).
+            const uint32_t ptm = tmem + qt * C::TCOLS + 128 + DH;   // P columns (P_TMEM)
+            const uint64_t pd0 = tc::sdesc(p_addr + qt * C::P_SMEM, 16, 1024, tc::SW_128B);
+            const uint64_t vd0 = tc::sdesc(v_addr + st * C::TILE, C::ATOM, 8 * C::RB, C::SW);
 #pragma unroll
-              for (int kk = 0; kk < 8; ++kk) {   // 128 keys, K = 16 per MMA
-                const uint32_t padv = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
-                const uint32_t vadv = (uint32_t)(kk * 16 * C::RB) >> 4;
-                const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
-                if (C::P_TMEM)
-                  tc::mma_bf16_ts(tmem + qt * C::TCOLS + 128, ptm + kk * 8, vd0 + vadv, id_o, acc);
-                else
-                  tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd0 + padv, vd0 + vadv, id_o, acc);
-                if (C::TC_SUM) {   // row sums: SUM[128 x 16] (+)= P x ones
-                  const uint32_t ladv = (uint32_t)((kk >> 2) * 2048 + (kk & 3) * 32) >> 4;
-                  tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128 + DH, pd0 + padv, ld0 + ladv, id_l, acc);
+            for (int h = 0; h < C::NPH; ++h) {
+              tc::mbar_wait(&p_full[qt * C::NPH + h], np & 1);
+              if (lane == 0 && h == 0) TL_STAMP(2 + qt, np, 3);
+              tc::tc_fence_after();
+              if (tc::elect_one()) {
+#pragma unroll
+                for (int kk = h * (8 / C::NPH); kk < (h + 1) * (8 / C::NPH); ++kk) {   // K = 16 keys per MMA
+                  const uint32_t padv = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
+                  const uint32_t vadv = (uint32_t)(kk * 16 * C::RB) >> 4;
+                  const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+                  if (C::P_TMEM)
+                    tc::mma_bf16_ts(tmem + qt * C::TCOLS + 128, ptm + kk * 8, vd0 + vadv, id_o, acc);
+                  else
+                    tc::mma_bf16_ss(tmem + qt * C::TCOLS + 128, pd0 + padv, vd0 + vadv, id_o, acc);
+                }
+                tc::mma_commit(&p_free[qt * C::NPH + h]);
+                if (h == C::NPH - 1) {
+                  tc::mma_commit(&v_empty[st]);
+                  if (lane == 0) TL_STAMP(2 + qt, np, 4);
                 }
               }
-              tc::mma_commit(&p_free[qt * C::PBUF + np % C::PBUF]);
-              tc::mma_commit(&v_empty[st]);
-              if (lane == 0) TL_STAMP(2 + qt, np, 4);
+              __syncwarp();
             }
             __syncwarp();
             ++np;
@@ -447,9 +432,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + qt * C::TCOLS;
     const uint32_t s_addr = lane_base;
     const uint32_t o_addr = lane_base + 128;
-    const uint32_t p_tm = lane_base + 128 + DH + C::SUMC;
+    const uint32_t p_tm = lane_base + 128 + DH;
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
-    uint64_t* my_p_free = p_free + qt * C::PBUF;
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
     uint32_t ni_sm = 0;                            // items processed (debug timeline only)
     uint32_t li = 0;
@@ -510,16 +494,43 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           }
           m_ref = m_new;
         };
+        // Part h of PV_{j-1} done: P columns of part h free (all parts: O complete).
+        uint32_t pv_done = cs == 0 ? (1u << C::NPH) - 1 : 0u;
+        auto wait_pv = [&](int h) {
+          if (!(pv_done >> h & 1u)) {
+            tc::mbar_wait(&p_free[qt * C::NPH + h], (cs - 1) & 1);
+            tc::tc_fence_after();
+            pv_done |= 1u << h;
+            if (tlr && h == 0) TL_STAMP(qt, cs, 4);
+          }
+        };
+        if (!kLatePvWait)
+          for (int h = 0; h < C::NPH; ++h) wait_pv(h);
+        // Conditional rescale (R18): the reference max moves only when the block max
+        // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
+        {
+          const float m_blk = row_max();
+          if (j == 0)
+            m_ref = m_blk;
+          else if (__any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2)) {
+            for (int h = 0; h < C::NPH; ++h) wait_pv(h);
+            rescale(fmaxf(m_blk, m_ref));
+          }
+        }
+        if (tlr) TL_STAMP(qt, cs, 3);
         // p = 2^(s * log2(e)/sqrt(d) - m_ref) -> bf16 P (TMEM: A operand of the PV MMA;
-        // smem when TMEM is short), returns the fp32 row sum of this block
-        auto exps = [&]() {
-          float rs0 = 0.f, rs1 = 0.f;
+        // smem when TMEM is short), part by part, with fp32 row sums
+        constexpr int KP = 128 / C::NPH;               // keys per part
+        float rs0 = 0.f, rs1 = 0.f;
+#pragma unroll
+        for (int h = 0; h < C::NPH; ++h) {
+          wait_pv(h);
           if constexpr (C::P_TMEM) {
 #pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 64) {
+            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
               uint32_t pk[32];
-#pragma unroll
               float2 rs = make_float2(0.f, 0.f);
+#pragma unroll
               for (int e = 0; e < 64; e += 2) {
                 float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
                 ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
@@ -533,11 +544,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               rs1 += rs.y;
               tc::tmem_st32(p_tm + c0 / 2, pk);
             }
+            tc::tmem_st_wait();
           } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
-            uint8_t* prow = sP + (qt * C::PBUF + cs % C::PBUF) * C::P_SMEM + i * 128;
+            uint8_t* prow = sP + qt * C::P_SMEM + i * 128;
             const int sw = i & 7;
 #pragma unroll
-            for (int c0 = 0; c0 < 128; c0 += 16) {
+            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 16) {
               uint32_t pk[8];
 #pragma unroll
               for (int e = 0; e < 16; e += 2) {
@@ -553,61 +565,17 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               *reinterpret_cast<uint4*>(atom + ((cb ^ sw) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
               *reinterpret_cast<uint4*>(atom + (((cb + 1) ^ sw) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
             }
+            tc::fence_proxy_async_smem();
           }
-          return rs0 + rs1;
-        };
-        // previous PV finished: P columns free and O complete.  Waited for only
-        // after the row max (which needs neither), unless a rescale needs O first.
-        bool pv_done = cs < (uint32_t)C::PBUF;
-        auto wait_pv = [&]() {
-          if (!pv_done) {
-            tc::mbar_wait(&my_p_free[cs % C::PBUF], ((cs / C::PBUF) - 1) & 1);
-            tc::tc_fence_after();
-            pv_done = true;
-            if (tlr) TL_STAMP(qt, cs, 4);
-          }
-        };
-        if (!kLatePvWait) wait_pv();
-        // Conditional rescale (R18): the reference max moves only when the block max
-        // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
-        // Skip-max (blocks after the first): exponentiate against the reference
-        // directly and check the block's row sum afterwards: all p >= 0, so
-        // max p <= sum p, and sum <= 2^64 bounds every p (P in bf16 and O, l in fp32
-        // share fp32's exponent range: nothing is lost for p up to that bound).  A
-        // sum outside the range (larger, inf, NaN) redoes the block through the max
-        // path.  Both are the same softmax mathematically.  One call site for the
-        // unrolled exponential loop (instruction cache).
-        bool with_max = j == 0 || !kSkipMax;
-        float l_blk;
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-          if (with_max) {
-            const float m_blk = row_max();
-            if (j == 0)
-              m_ref = m_blk;
-            else if (__any_sync(0xffffffffu, row_valid && m_blk > m_ref + kRescaleLog2)) {
-              wait_pv();
-              rescale(fmaxf(m_blk, m_ref));
-            }
-          }
-          if (tlr) TL_STAMP(qt, cs, 3);
-          wait_pv();
-          l_blk = exps();
-          if (with_max || !__any_sync(0xffffffffu, row_valid && !(l_blk <= kSumMax))) break;
-          tc::tmem_st_wait();   // P is rewritten
-          with_max = true;
+          tc::tc_fence_before();
+          tc::mbar_arrive(&p_full[qt * C::NPH + h]);
         }
-        l_run += l_blk;
+        l_run += rs0 + rs1;
         if (tlr) TL_STAMP(qt, cs, 5);
-        tc::tmem_st_wait();
-        if (!C::P_TMEM) tc::fence_proxy_async_smem();
-        tc::tc_fence_before();
-        tc::mbar_arrive(&p_full[qt]);
-        if (tlr) TL_STAMP(qt, cs, 6);
       }
       // epilogue: O / l
       if (tlr) TL_STAMP(5 + qt, ni_sm, 0);
-      tc::mbar_wait(&my_p_free[(cs - 1) % C::PBUF], ((cs - 1) / C::PBUF) & 1);
+      for (int h = 0; h < C::NPH; ++h) tc::mbar_wait(&p_free[qt * C::NPH + h], (cs - 1) & 1);
       tc::tc_fence_after();
       if (tlr) TL_STAMP(5 + qt, ni_sm, 1);
       const float inv = 1.f / l_run;
