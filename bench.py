@@ -172,6 +172,7 @@ def class_work(w, info, B):
         "head_gemm": 2.0 * ncore * D * Nh,
     }
     f["mlp_fused"] = f["mlp_up_gemm"] + f["mlp_down_gemm"]   # one kernel does both (D = 256)
+    f["block_tail"] = f["oproj_gemm"] + f["mlp_fused"]        # O-proj + LN2 + MLP in one kernel (D = 256)
     out = {k: ("tensor", v * B) for k, v in f.items()}
     # HBM kernels: unique algorithmic bytes
     out["tile_gather"] = ("hbm", B * (4.0 * V * w.H * w.W + 2.0 * npad * Din))

@@ -86,6 +86,12 @@ bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16,
 bool launch_mlp_fused(const void* xn, int64_t rows_alloc, const void* w1, const float* b1, const void* w2,
                       const float* b2, float* z, int64_t M, int D, cudaStream_t st);
 
+// Block tail for D = 256: z' = z + W_o o + b_o; z = z' + W2 GELU(W1 LN2(z') + b1) + b2
+// (z' and the hidden tile stay on chip).
+bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const float* bo, const float* ln2_g,
+                       const float* ln2_b, const void* w1, const float* b1, const void* w2, const float* b2,
+                       float* z, int64_t M, int D, cudaStream_t st);
+
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();
 

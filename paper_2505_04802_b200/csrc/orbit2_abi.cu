@@ -42,6 +42,7 @@ struct Ctx {
   bool sync_check = false;
   bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
+  bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -191,6 +192,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->unfused_mlp = um && um[0] == '1';
   const char* ul = std::getenv("ORBIT2_UNFUSED_LN");
   c->unfused_ln = ul && ul[0] == '1';
+  const char* ub = std::getenv("ORBIT2_UNFUSED_BLOCK");
+  c->unfused_block = ub && ub[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
@@ -388,6 +391,14 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       ORBIT2_TRY(run(c, "tile_attention", st, [&] {
         return launch_attention_tc(qkv, mrow, ao, cd, B, (int)D, cf.heads, p.d, st);
       }));
+      if (D == 256 && !c->unfused_mlp && !c->unfused_ln && !c->unfused_block) {
+        // O-projection + residual + LN2 + MLP + residual in one kernel (z' stays on chip)
+        ORBIT2_TRY(run(c, "block_tail", st, [&] {
+          return launch_block_tail(ao, mrow, W8 + L.w_o, wf(L.b_o), wf(L.ln2_g), wf(L.ln2_b), W8 + L.w_1,
+                                   wf(L.b_1), W8 + L.w_2, wf(L.b_2), z, M, (int)D, st);
+        }));
+        continue;
+      }
       e = EpiParams{}; e.bias = wf(L.b_o); e.C = z; e.ldc = D;
       if (ln_fused) {
         e.xn = xn;

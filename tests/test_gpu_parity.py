@@ -234,7 +234,7 @@ def test_binding_rejects_wrong_dtypes():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("env", ["ORBIT2_UNFUSED_LN", "ORBIT2_UNFUSED_MLP"])
+@pytest.mark.parametrize("env", ["ORBIT2_UNFUSED_LN", "ORBIT2_UNFUSED_MLP", "ORBIT2_UNFUSED_BLOCK"])
 def test_unfused_paths_match_oracle(env, monkeypatch):
     """The separate-kernel forms (LayerNorm after embed / O-projection; MLP as
     two GEMMs) stay within tolerance of the oracle, like the fused default."""
