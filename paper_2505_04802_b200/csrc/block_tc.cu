@@ -2,6 +2,7 @@
 // D = 256 (the 9.5M-class Reslim), fused into one persistent kernel:
 //     z'  = z + W_o . o + b_o                         (attention output o, R9)
 //     z'' = z' + W_2 . GELU(W_1 . LN2(z') + b_1) + b_2  (exact-erf GELU, LN eps 1e-5)
+//     xn  = LN1_{l+1}(z'')  (bf16, the next block's QKV input; not for the last block)
 // Per 128-token row block the residual row z' never leaves the SM: the
 // O-projection accumulates in TMEM, the epilogue warps add b_o and z (streamed
 // in by TMA) and write z' BACK into the TMEM accumulator that the MLP's second
@@ -30,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -41,7 +43,21 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
 bool make_tmap_f32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                    int box_cols, CUtensorMapSwizzle swz);
 
+extern long long* g_mlp_timeline;   // debug timeline buffer (orbit2_debug_mlp_timeline)
+
 namespace {
+
+// debug timeline (-DORBIT2_BLOCK_TIMELINE): tl[(role * 64 + block) * 8 + event], CTA 0
+#ifdef ORBIT2_BLOCK_TIMELINE
+#define BTL(role, b, ev)                                                                              \
+  do {                                                                                                \
+    if (tl != nullptr && blockIdx.x == 0 && (b) < 64) tl[((role) * 64 + (b)) * 8 + (ev)] = clock64(); \
+  } while (0)
+#else
+#define BTL(role, b, ev) \
+  do {                   \
+  } while (0)
+#endif
 
 constexpr int BM = 128;
 constexpr int DM = 256;           // model width D
@@ -61,26 +77,61 @@ constexpr int EW = 2;
 constexpr int CW = HC / EW;                         // hidden columns per warpgroup and chunk
 constexpr int ET = 128 * EW;                        // epilogue threads
 constexpr int THREADS = 128 + ET;
-constexpr int STATS_BYTES = EW * BM * 4;            // per-row partial sums of the two warpgroups
-constexpr int SMEM = X_BYTES + RS * SLOT + EW * STG_BYTES + STATS_BYTES + 1024 + 512;
+constexpr int STATS_BYTES = EW * BM * 4;            // per-row partials of the two warpgroups
+constexpr int SMEM = X_BYTES + RS * SLOT + EW * STG_BYTES + STATS_BYTES + 1024 + 256;
 static_assert(SMEM <= 227 * 1024, "shared memory");
+
+#ifndef ORBIT2_BLOCK_PREFETCH
+#define ORBIT2_BLOCK_PREFETCH 0   // L2 prefetch of the next block: faults at large M (unexplained), off
+#endif
+#ifndef ORBIT2_GELU_TANH
+#define ORBIT2_GELU_TANH 1
+#endif
+// tanh-form GELU on the MUFU (R28): the erf form is FMA-pipe bound here
+__device__ __forceinline__ float2 gelu2(float2 x) {
+  if (ORBIT2_GELU_TANH) return tc::gelu2_tanh_fast(x);
+  return tc::gelu2_erf_fast(x);
+}
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Row statistics over D = 256 features held by two warpgroups (128 each):
+// per warpgroup n = 128, mean_w = shift + sum / n, M2_w = sq - sum^2 / n
+// (about the warpgroup mean); mean = (mean_0 + mean_1) / 2 and
+// M2 = sum_w M2_w + n (mean_w - mean)^2 (Chan's pairwise combination), one
+// float per row and warpgroup exchanged at a time (named barrier 3).
+__device__ __forceinline__ void combine_stats(float* sStat, int wg, int r, float shift, float sum, float sq,
+                                              float& mean, float& rstd) {
+  const float mw = shift + sum * (1.f / 128);
+  const float m2 = fmaf(-sum, sum * (1.f / 128), sq);
+  sStat[wg * BM + r] = mw;
+  named_bar(3, ET);
+  mean = 0.5f * (mw + sStat[(wg ^ 1) * BM + r]);
+  const float dm = mw - mean;
+  const float m2g = fmaf(dm * dm, 128.f, m2);   // M2 of this warpgroup's values about the row mean
+  named_bar(3, ET);                             // both means read before the slots are reused
+  sStat[wg * BM + r] = m2g;
+  named_bar(3, ET);
+  const float var = (m2g + sStat[(wg ^ 1) * BM + r]) * (1.f / DM);
+  rstd = rsqrtf(fmaxf(var, 0.f) + 1e-5f);
+  named_bar(3, ET);                             // both read before the next exchange writes
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     block_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWo,
                     const __grid_constant__ CUtensorMap tmW1, const __grid_constant__ CUtensorMap tmW2,
-                    const __grid_constant__ CUtensorMap tmZ, const float* __restrict__ bo,
-                    const float* __restrict__ g2, const float* __restrict__ be2, const float* __restrict__ b1,
-                    const float* __restrict__ b2, int64_t M) {
+                    const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmXn,
+                    const float* __restrict__ bo, const float* __restrict__ g2, const float* __restrict__ be2,
+                    const float* __restrict__ b1, const float* __restrict__ b2, const float* __restrict__ g1n,
+                    const float* __restrict__ be1n, int64_t M, long long* __restrict__ tl) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;                      // o tile, then LN2(z') (SW128 K-major, 4 atoms of 64 columns)
   uint8_t* sW = sX + X_BYTES;              // [RS][SLOT]
   uint8_t* sZ = sW + RS * SLOT;            // [EW][STG_BYTES] store staging
-  float* sStat = reinterpret_cast<float*>(sZ + EW * STG_BYTES);   // [EW][BM]
+  float* sStat = reinterpret_cast<float*>(sZ + EW * STG_BYTES);   // [EW][BM] exchange slots
   uint64_t* bar = reinterpret_cast<uint64_t*>(sStat + EW * BM);
   uint64_t* x_full = bar;                  // o tile landed
   uint64_t* x_free = x_full + 1;           // GEMM1(7) done: X may take the next block's o
@@ -103,6 +154,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::prefetch_tmap(&tmW1);
     tc::prefetch_tmap(&tmW2);
     tc::prefetch_tmap(&tmZ);
+    if (g1n != nullptr) tc::prefetch_tmap(&tmXn);
     tc::mbar_init(x_full, 1);
     tc::mbar_init(x_free, 1);
     for (int s = 0; s < RS; ++s) {
@@ -146,7 +198,13 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tma_load_2d(&tmWo, dst, fb, ks * 64, 0);
           tc::tma_load_2d(&tmWo, dst + 16384, fb, ks * 64, 128);
         }
-        for (int zs = 0; zs < RI_Z; ++zs, ++it) {    // z rows m0.., features 64 zs .. 64 zs + 63
+        if (ORBIT2_BLOCK_PREFETCH && tile + gridDim.x < num_tiles) {   // warm the L2 with the next block's o, z
+          const int32_t mn = (int32_t)((tile + gridDim.x) * BM);
+          for (int a = 0; a < DM / 64; ++a) tc::tma_prefetch_2d(&tmA, a * 64, mn);
+          for (int c = 0; c < DM / ZC; ++c) tc::tma_prefetch_2d(&tmZ, c * ZC, mn);
+        }
+        for (int p = 0; p < RI_Z; ++p, ++it) {      // z rows m0.., features 64 zs .. 64 zs + 63,
+          const int zs = 2 * (p & 1) + (p >> 1);    // warpgroups interleaved: zs 0, 2, 1, 3
           uint8_t* dst = slot_begin();
           uint64_t* fb = &w_full[it % RS];
           tc::tma_load_2d(&tmZ, dst, fb, zs * 64, m0);
@@ -184,6 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // O-projection into the S region: both S/H buffers consumed by the
         // previous block's last two GEMM2s
         tc::mbar_wait(x_full, tl_ & 1);
+        BTL(0, tl_, 0);
         if (tl_ >= 1) {
           tc::mbar_wait(&h_free[0], 1);   // completion (8 tl_ - 2) / 2 = 4 tl_ - 1 of each: odd
           tc::mbar_wait(&h_free[1], 1);
@@ -202,8 +261,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::mma_commit(&w_empty[sl]);
         }
         tc::mma_commit(op_full);
+        BTL(0, tl_, 1);
         it += RI_Z;                          // z slices: consumed by the epilogue
         tc::mbar_wait(xn_full, tl_ & 1);     // z' in the O region, LN2(z') in X
+        BTL(0, tl_, 2);
         tc::tc_fence_after();
         for (int s = 0; s <= NCH; ++s) {
           if (s < NCH) {
@@ -245,7 +306,10 @@ __global__ void __launch_bounds__(THREADS, 1)
               tc::mma_commit(&w_empty[sl]);
             }
             tc::mma_commit(&h_free[hb]);
-            if (h == NCH - 1) tc::mma_commit(o_full);
+            if (h == NCH - 1) {
+              tc::mma_commit(o_full);
+              BTL(0, tl_, 3);
+            }
           }
         }
       }
@@ -257,7 +321,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int r = q * 32 + lane;                 // row within the block = TMEM lane
     const uint32_t lane_addr = tmem + ((uint32_t)(q * 32) << 16);
     const uint32_t nb = 1 + wg;                  // named barrier of this warpgroup (128 threads)
-    constexpr uint32_t NB_ALL = 3;               // both warpgroups (256 threads)
     const bool issuer = q == 0 && lane == 0;     // per warpgroup: ring releases, TMA stores
     const int f0 = wg * 128;                     // this warpgroup's residual features
     uint8_t* stg = sZ + wg * STG_BYTES;
@@ -266,12 +329,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl_) {
       const uint32_t ring0 = tl_ * RI_BLOCK + RI_WO;   // ring index of this block's first z slice
       // ---- z' = z + acc + b_o -> O region (TMEM); LN2 statistics (two-pass) ----
+      const bool stp = warp == 4 && lane == 0;
       tc::mbar_wait(op_full, tl_ & 1);
+      if (stp) BTL(1, tl_, 0);
       tc::tc_fence_after();
-      float sum = 0.f;
+      // single-pass statistics about a per-thread shift (the row's first value of
+      // this warpgroup: |mean - shift| ~ std, no cancellation), combined across
+      // the two warpgroups with Chan's pairwise formula
+      float sum = 0.f, sq = 0.f, shift = 0.f;
 #pragma unroll 1
       for (int zi = 0; zi < 2; ++zi) {
-        const uint32_t gi = ring0 + 2 * wg + zi, sl = gi % RS;
+        const uint32_t gi = ring0 + 2 * zi + wg, sl = gi % RS;
         tc::mbar_wait(&w_full[sl], (gi / RS) & 1);
         const uint8_t* zs = sW + sl * SLOT;
 #pragma unroll
@@ -290,7 +358,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float y1 = __uint_as_float(a[4 * u + 1]) + bq.y + zv.y;
             const float y2 = __uint_as_float(a[4 * u + 2]) + bq.z + zv.z;
             const float y3 = __uint_as_float(a[4 * u + 3]) + bq.w + zv.w;
-            sum += (y0 + y1) + (y2 + y3);
+            if (zi == 0 && hb == 0 && u == 0) shift = y0;
+            const float d0 = y0 - shift, d1 = y1 - shift, d2 = y2 - shift, d3 = y3 - shift;
+            sum += (d0 + d1) + (d2 + d3);
+            sq = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, sq))));
             a[4 * u] = __float_as_uint(y0);
             a[4 * u + 1] = __float_as_uint(y1);
             a[4 * u + 2] = __float_as_uint(y2);
@@ -302,25 +373,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (issuer) tc::mbar_arrive(&w_empty[sl]);
       }
       tc::tmem_st_wait();
-      sStat[wg * BM + r] = sum;
-      named_bar(NB_ALL, ET);
-      const float mean = (sStat[r] + sStat[BM + r]) * (1.f / DM);
-      float ss = 0.f;
-#pragma unroll
-      for (int c0 = 0; c0 < 128; c0 += 32) {
-        uint32_t a[32];
-        tc::tmem_ld32(lane_addr + 256 + f0 + c0, a);
-        tc::tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const float d = __uint_as_float(a[e]) - mean;
-          ss = fmaf(d, d, ss);
-        }
-      }
-      named_bar(NB_ALL, ET);                     // both partial sums read before reuse
-      sStat[wg * BM + r] = ss;
-      named_bar(NB_ALL, ET);
-      const float rstd = rsqrtf((sStat[r] + sStat[BM + r]) * (1.f / DM) + 1e-5f);
+      if (stp) BTL(1, tl_, 1);
+      float mean, rstd;
+      combine_stats(sStat, wg, r, shift, sum, sq, mean, rstd);
+      if (stp) BTL(1, tl_, 2);
       // ---- LN2(z') -> bf16 X (the o tile was consumed by the O-projection) ----
 #pragma unroll
       for (int c0 = 0; c0 < 128; c0 += 32) {
@@ -348,10 +404,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::fence_proxy_async_smem();
       tc::tc_fence_before();
       tc::mbar_arrive(xn_full);
+      if (stp) BTL(1, tl_, 3);
       // ---- MLP hidden chunks: bias + GELU, bf16 H over S ----
       for (int h = 0; h < NCH; ++h) {
         const uint32_t gc = tl_ * NCH + h, buf = gc & 1, use = gc >> 1;
         tc::mbar_wait(&s_full[buf], use & 1);
+        if (stp && h == 0) BTL(1, tl_, 4);
+        if (stp) BTL(2 + (h >> 3), tl_, h & 7);
         tc::tc_fence_after();
         const uint32_t scol = lane_addr + buf * HC + wg * CW;   // this warpgroup's S (and H) columns
         float v[CW];
@@ -364,10 +423,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c8 = 0; c8 < CW / 8; ++c8) {
           const float4 ba = __ldg(bb + 2 * c8), bc = __ldg(bb + 2 * c8 + 1);
           const float* x8 = v + 8 * c8;
-          const float2 q0 = tc::gelu2_erf_fast(tc::add2(make_float2(x8[0], x8[1]), make_float2(ba.x, ba.y)));
-          const float2 q1 = tc::gelu2_erf_fast(tc::add2(make_float2(x8[2], x8[3]), make_float2(ba.z, ba.w)));
-          const float2 q2 = tc::gelu2_erf_fast(tc::add2(make_float2(x8[4], x8[5]), make_float2(bc.x, bc.y)));
-          const float2 q3 = tc::gelu2_erf_fast(tc::add2(make_float2(x8[6], x8[7]), make_float2(bc.z, bc.w)));
+          const float2 q0 = gelu2(tc::add2(make_float2(x8[0], x8[1]), make_float2(ba.x, ba.y)));
+          const float2 q1 = gelu2(tc::add2(make_float2(x8[2], x8[3]), make_float2(ba.z, ba.w)));
+          const float2 q2 = gelu2(tc::add2(make_float2(x8[4], x8[5]), make_float2(bc.x, bc.y)));
+          const float2 q3 = gelu2(tc::add2(make_float2(x8[6], x8[7]), make_float2(bc.z, bc.w)));
           hv[4 * c8 + 0] = tc::pack_bf16(q0.x, q0.y);
           hv[4 * c8 + 1] = tc::pack_bf16(q1.x, q1.y);
           hv[4 * c8 + 2] = tc::pack_bf16(q2.x, q2.y);
@@ -380,8 +439,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       // ---- z'' = O + b_2 -> z (TMA tensor stores from swizzled staging) ----
       tc::mbar_wait(o_full, tl_ & 1);
+      if (stp) BTL(1, tl_, 5);
       tc::tc_fence_after();
       const int32_t m0 = (int32_t)(tile * BM);
+      float sum2 = 0.f, sq2 = 0.f, shift2 = 0.f;
 #pragma unroll 1
       for (int k = 0; k < 128 / ZC; ++k) {
         uint32_t o[ZC];
@@ -395,9 +456,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int u = 0; u < ZC / 4; ++u) {
           const float4 bq = __ldg(b4 + u);
-          *reinterpret_cast<float4*>(srow + ((u ^ sw) << 4)) =
-              make_float4(__uint_as_float(o[4 * u]) + bq.x, __uint_as_float(o[4 * u + 1]) + bq.y,
-                          __uint_as_float(o[4 * u + 2]) + bq.z, __uint_as_float(o[4 * u + 3]) + bq.w);
+          const float4 y = make_float4(__uint_as_float(o[4 * u]) + bq.x, __uint_as_float(o[4 * u + 1]) + bq.y,
+                                       __uint_as_float(o[4 * u + 2]) + bq.z, __uint_as_float(o[4 * u + 3]) + bq.w);
+          if (k == 0 && u == 0) shift2 = y.x;
+          const float d0 = y.x - shift2, d1 = y.y - shift2, d2 = y.z - shift2, d3 = y.w - shift2;
+          sum2 += (d0 + d1) + (d2 + d3);
+          sq2 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, sq2))));
+          *reinterpret_cast<float4*>(srow + ((u ^ sw) << 4)) = y;
         }
         tc::fence_proxy_async_smem();
         named_bar(nb, 128);
@@ -406,6 +471,48 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::bulk_commit();
         }
       }
+      if (stp) BTL(1, tl_, 6);
+      if (g1n != nullptr) {
+        // ---- LN1 of the next block: xn = LN1(z'') (bf16) -> HBM, the QKV GEMM's input ----
+        float mean1, rstd1;
+        combine_stats(sStat, wg, r, shift2, sum2, sq2, mean1, rstd1);
+        // two bf16 boxes of 128 rows x 64 features per warpgroup, one per staging buffer
+#pragma unroll 1
+        for (int xb = 0; xb < 2; ++xb) {
+          uint8_t* sb = stg + xb * ZBOX;
+          if (issuer) tc::bulk_wait_read<1>();
+          named_bar(nb, 128);
+#pragma unroll
+          for (int c0 = 0; c0 < 64; c0 += 32) {
+            const int k0 = f0 + xb * 64 + c0;
+            uint32_t a[32];
+            tc::tmem_ld32(lane_addr + 256 + k0, a);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int kk = k0 + 8 * u;
+              const float4 ba = __ldg(reinterpret_cast<const float4*>(b2 + kk)), bb = __ldg(reinterpret_cast<const float4*>(b2 + kk + 4));
+              const float4 ga = __ldg(reinterpret_cast<const float4*>(g1n + kk)), gb = __ldg(reinterpret_cast<const float4*>(g1n + kk + 4));
+              const float4 ea = __ldg(reinterpret_cast<const float4*>(be1n + kk)), eb = __ldg(reinterpret_cast<const float4*>(be1n + kk + 4));
+              const float* x8 = reinterpret_cast<const float*>(a + 8 * u);
+              const uint4 pk = make_uint4(
+                  tc::pack_bf16((x8[0] + ba.x - mean1) * rstd1 * ga.x + ea.x, (x8[1] + ba.y - mean1) * rstd1 * ga.y + ea.y),
+                  tc::pack_bf16((x8[2] + ba.z - mean1) * rstd1 * ga.z + ea.z, (x8[3] + ba.w - mean1) * rstd1 * ga.w + ea.w),
+                  tc::pack_bf16((x8[4] + bb.x - mean1) * rstd1 * gb.x + eb.x, (x8[5] + bb.y - mean1) * rstd1 * gb.y + eb.y),
+                  tc::pack_bf16((x8[6] + bb.z - mean1) * rstd1 * gb.z + eb.z, (x8[7] + bb.w - mean1) * rstd1 * gb.w + eb.w));
+              const int unit = (c0 >> 3) + u;
+              *reinterpret_cast<uint4*>(sb + r * 128 + ((unit ^ sw) << 4)) = pk;
+            }
+          }
+          tc::fence_proxy_async_smem();
+          named_bar(nb, 128);
+          if (issuer) {
+            tc::tma_store_2d(&tmXn, sb, f0 + xb * 64, m0);
+            tc::bulk_commit();
+          }
+        }
+      }
+      if (stp) BTL(1, tl_, 7);
       tc::tc_fence_before();                   // O region read: the next block's z' may overwrite it
     }
     if (issuer) tc::bulk_wait_all();
@@ -422,9 +529,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const float* bo, const float* ln2_g,
                        const float* ln2_b, const void* w1, const float* b1, const void* w2, const float* b2,
-                       float* z, int64_t M, int D, cudaStream_t st) {
+                       float* z, int64_t M, int D, const float* ln1n_g, const float* ln1n_b, void* xn_next,
+                       cudaStream_t st) {
   if (D != DM || M <= 0) return false;
-  CUtensorMap ta, two, t1, t2, tz;
+  CUtensorMap ta, two, t1, t2, tz, txn;
+  std::memset(&txn, 0, sizeof(txn));
+  if (ln1n_g != nullptr && !make_tmap_bf16(&txn, xn_next, M, DM, DM, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   if (!make_tmap_bf16(&ta, ao, rows_alloc, DM, DM, BM, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   if (!make_tmap_bf16(&two, wo, DM, DM, DM, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   if (!make_tmap_bf16(&t1, w1, FH, DM, DM, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
@@ -442,7 +553,8 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t tiles = (M + BM - 1) / BM;
   const int grid = (int)std::min<int64_t>(tiles, sms);
-  block_tc_kernel<<<grid, THREADS, SMEM, st>>>(ta, two, t1, t2, tz, bo, ln2_g, ln2_b, b1, b2, M);
+  block_tc_kernel<<<grid, THREADS, SMEM, st>>>(ta, two, t1, t2, tz, txn, bo, ln2_g, ln2_b, b1, b2, ln1n_g, ln1n_b,
+                                               M, g_mlp_timeline);
   return true;
 }
 

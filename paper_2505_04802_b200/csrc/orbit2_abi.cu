@@ -379,7 +379,9 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
     }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
-      if (!(ln_fused && l == 0)) {   // block 0's LN1 runs in the embed epilogue
+      // block 0's LN1 runs in the embed epilogue, later blocks' in the previous block_tail
+      const bool tail_fused = D == 256 && !c->unfused_mlp && !c->unfused_ln && !c->unfused_block;
+      if (!(ln_fused && l == 0) && !(tail_fused && l > 0)) {
         ORBIT2_TRY(run(c, "layernorm", st, [&] {
           launch_layernorm<bf16>(z, wf(L.ln1_g), wf(L.ln1_b), xn, M, (int)D, nullptr, st);
           return true;
@@ -391,11 +393,15 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       ORBIT2_TRY(run(c, "tile_attention", st, [&] {
         return launch_attention_tc(qkv, mrow, ao, cd, B, (int)D, cf.heads, p.d, st);
       }));
-      if (D == 256 && !c->unfused_mlp && !c->unfused_ln && !c->unfused_block) {
-        // O-projection + residual + LN2 + MLP + residual in one kernel (z' stays on chip)
+      if (tail_fused) {
+        // O-projection + residual + LN2 + MLP + residual (+ LN1 of the next block) in
+        // one kernel (z' stays on chip)
+        const bool nxt = l + 1 < cf.depth;
+        const float* g1n = nxt ? wf(w.layers[l + 1].ln1_g) : nullptr;
+        const float* b1n = nxt ? wf(w.layers[l + 1].ln1_b) : nullptr;
         ORBIT2_TRY(run(c, "block_tail", st, [&] {
           return launch_block_tail(ao, mrow, W8 + L.w_o, wf(L.b_o), wf(L.ln2_g), wf(L.ln2_b), W8 + L.w_1,
-                                   wf(L.b_1), W8 + L.w_2, wf(L.b_2), z, M, (int)D, st);
+                                   wf(L.b_1), W8 + L.w_2, wf(L.b_2), z, M, (int)D, g1n, b1n, xn, st);
         }));
         continue;
       }

@@ -60,6 +60,12 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, void* smem_dst
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
 }
+// warm the L2 with a 2-D box (no shared-memory destination, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int32_t x, int32_t y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+               "r"(x), "r"(y)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* m, const void* smem_src, int32_t x, int32_t y) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
@@ -294,6 +300,22 @@ __device__ __forceinline__ float2 gelu2_erf_fast(float2 x) {
   t = mul2(t, t);
   t = mul2(t, t);   // q
   return fma2(na, t, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
+}
+
+// GELU of a pair through the tanh form 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
+// with the MUFU tanh (one MUFU op per element, like the reciprocal of the erf form,
+// but 6 instead of 12 packed FMA-pipe instructions per pair).  |error| vs the exact
+// erf GELU <= 4.7e-4 (formula) + 2^-11 |x| / 2 (tanh.approx), below half a bf16 ulp
+// of the output it is rounded to (reading R28).
+__device__ __forceinline__ float2 gelu2_tanh_fast(float2 x) {
+  const float2 x2 = mul2(x, x);
+  const float2 in = fma2(x2, splat2(0.7978845608f * 0.044715f), splat2(0.7978845608f));
+  const float2 u = mul2(in, x);
+  float2 t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.x) : "f"(u.x));
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t.y) : "f"(u.y));
+  const float2 hx = mul2(x, splat2(0.5f));
+  return fma2(hx, t, hx);
 }
 
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
