@@ -177,10 +177,10 @@ def class_work(w, info, B):
     # HBM kernels: unique algorithmic bytes
     out["tile_gather"] = ("hbm", B * (4.0 * V * w.H * w.W + 2.0 * npad * Din))
     out["stitch_residual"] = ("hbm", B * (2.0 * K * sH * sW + 4.0 * K * w.H * w.W + 4.0 * K * sH * sW))
-    # layernorm launches: fp32 read + bf16 write of D per row.  D = 256: the LNs after
-    # the embedding and the O-projection run in those GEMMs' epilogues, leaving
-    # LN1 of blocks 1.. and the final (core rows) LN; otherwise 2L + 1 launches.
-    ln_full = max(L - 1, 0) if D == 256 else 2 * L
+    # layernorm launches: fp32 read + bf16 write of D per row.  D = 256: LN1 of block 0
+    # runs in the embedding GEMM's epilogue, LN2 and the next block's LN1 in the
+    # block-tail kernel, leaving the final (core rows) LN; otherwise 2L + 1 launches.
+    ln_full = 0 if D == 256 else 2 * L
     out["layernorm"] = ("hbm", B * (ln_full * npad * D * 6.0 + ncore * D * 6.0))
     return out
 
@@ -431,8 +431,10 @@ def run_ours(args, w, world, rank, local):
         if att and "tflops" in att:
             res["attn_tflops"] = att["tflops"]
             res["attn_frac_bf16_peak"] = att["tflops"] / pk["bf16_sus"]
-        gemm_ms = sum(classes[k]["ms_per_step"] for k in classes if k.endswith("_gemm"))
-        gemm_f = sum(work[k][1] for k in work if k.endswith("_gemm"))
+        # measured tensor-core classes other than attention (GEMMs, fused MLP / block tail)
+        tck = [k for k in classes if k in work and work[k][0] == "tensor" and k != "tile_attention"]
+        gemm_ms = sum(classes[k]["ms_per_step"] for k in tck)
+        gemm_f = sum(work[k][1] for k in tck)
         res["gemm_tflops"] = gemm_f / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
         tc_ms = gemm_ms + (att["ms_per_step"] if att else 0)
         tc_f = gemm_f + work["tile_attention"][1]

@@ -24,7 +24,7 @@ METRICS = {
     "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_pct",
     "sm__cycles_elapsed.avg.per_second": "sm_hz",
 }
-CLASS = [("attn_tc", "tile_attention"), ("mlp_tc", "mlp_fused"), ("layernorm", "layernorm"),
+CLASS = [("attn_tc", "tile_attention"), ("mlp_tc", "mlp_fused"), ("block_tc", "block_tail"), ("layernorm", "layernorm"),
          ("stitch", "stitch_residual"), ("gather", "tile_gather")]
 
 
