@@ -104,6 +104,17 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
 #ifndef ORBIT2_ATTN_LATEPV
 #define ORBIT2_ATTN_LATEPV 1
 #endif
+#ifndef ORBIT2_ATTN_REGREALLOC
+#define ORBIT2_ATTN_REGREALLOC 0   // measured slower (C2: 20.45 vs 20.08 ms)
+#endif
+// control warpgroup gives registers to the softmax warpgroups (no spills in the exp loop)
+constexpr bool kRegRealloc = ORBIT2_ATTN_REGREALLOC != 0;
+#ifndef ORBIT2_ATTN_PINGPONG
+#define ORBIT2_ATTN_PINGPONG 0   // measured slower (C2: 22.0 vs 19.5 ms): one warp per SM sub-partition reaches ~69% of the MUFU rate
+#endif
+// the two Q tiles' exponential phases alternate (named barriers 1 / 2): one
+// tile's row max, waits and epilogue overlap the other tile's exponentials
+constexpr bool kPingPong = ORBIT2_ATTN_PINGPONG != 0;
 #ifndef ORBIT2_ATTN_SPLITP
 #define ORBIT2_ATTN_SPLITP 0   // measured slower (C2: 21.6 vs 19.9 ms): the 128-arrival part barriers wait for the slowest warp
 #endif
@@ -130,7 +141,9 @@ struct AttnCfg {
   static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
   static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
-  static constexpr int CTRL_WARPS = 1 + NQ;          // producer (+TMEM alloc), one MMA issuer per Q tile
+  // producer (+TMEM alloc), one MMA issuer per Q tile; padded to a whole warpgroup
+  // when registers are reallocated (setmaxnreg acts per warpgroup)
+  static constexpr int CTRL_WARPS = kRegRealloc ? 4 : 1 + NQ;
   static constexpr int THREADS = 32 * CTRL_WARPS + 128 * NQ;   // + one softmax thread per query row
   // P lives in TMEM (64 columns of bf16 pairs) and feeds the PV MMA as the A
   // operand when TMEM allows: no shared-memory traffic for P (the SS form
@@ -272,6 +285,10 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (kRegRealloc) {
+    if (warp < C::CTRL_WARPS) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 224;" ::: "memory");
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -421,6 +438,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         if (active) ++ni;
       }
     }
+  } else if (warp < C::CTRL_WARPS) {
+    // spare warp of the control warpgroup (register reallocation): idle
   } else {
     // ---------------- softmax / correction / epilogue ----------------
     // Thread = query row i of Q tile qt (TMEM lane i: warp w reads lane quarter
@@ -436,12 +455,24 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
     uint32_t ni_sm = 0;                            // items processed (debug timeline only)
+    // ping-pong turns: barrier 1 + t = "tile t may exponentiate"; 256 = both tiles' warps
+    auto pp_sync = [](int id) { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); };
+    auto pp_arrive = [](int id) { asm volatile("bar.arrive %0, 256;" ::"r"(id) : "memory"); };
+    if (kPingPong && qt == 1) pp_arrive(1);        // tile 0 goes first
     uint32_t li = 0;
     for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
       if (q == 0 && lane == 0) TL_STAMP(5 + qt, ni_sm, 6);
       const Item it = take_item(sItem, it_full, it_empty, li, C::IRING);
       if (q == 0 && lane == 0) TL_STAMP(5 + qt, ni_sm, 7);
-      if (qt >= it.nq) continue;
+      if (qt >= it.nq) {
+        if constexpr (kPingPong) {   // keep the turn-taking aligned with the active tile
+          for (int j = 0; j < it.nkb; ++j) {
+            pp_sync(1 + qt);
+            pp_arrive(1 + (qt ^ 1));
+          }
+        }
+        continue;
+      }
       float m_ref = -INFINITY, l_run = 0.f;
       const bool tlr = q == 0 && lane == 0;
       // Only rows inside the tile take part in the (warp-uniform) range votes, so
@@ -522,6 +553,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         // smem when TMEM is short), part by part, with fp32 row sums
         constexpr int KP = 128 / C::NPH;               // keys per part
         float rs0 = 0.f, rs1 = 0.f;
+        if constexpr (kPingPong) pp_sync(1 + qt);   // this tile's turn on the MUFU
 #pragma unroll
         for (int h = 0; h < C::NPH; ++h) {
           wait_pv(h);
@@ -570,6 +602,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&p_full[qt * C::NPH + h]);
         }
+        if constexpr (kPingPong) pp_arrive(1 + (qt ^ 1));   // the other tile's turn
         l_run += rs0 + rs1;
         if (tlr) TL_STAMP(qt, cs, 5);
       }
