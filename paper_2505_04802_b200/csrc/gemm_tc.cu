@@ -157,7 +157,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
   }
 }
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS>
+#ifndef ORBIT2_GEMM_WS
+#define ORBIT2_GEMM_WS 1
+#endif
+
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS, bool WS = false>
 __global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M,
@@ -170,8 +174,14 @@ __global__ void __launch_bounds__(384, 1)
   // runs continuously across tiles; the fp32 accumulator is double-buffered
   // in TMEM (2 x BN columns) so the epilogue of tile i overlaps the MMAs of
   // tile i+1.
+  // WS (weight-stationary, K == 256): the CTA's BN x K weight slice is loaded once
+  // into shared memory and every tile of the CTA (the grid is a multiple of the
+  // number of column tiles, so a CTA keeps one column tile) streams only its
+  // activation block through the ring: 3x less L2 -> SM traffic for the QKV GEMM.
   constexpr int A_BYTES = BM * BK * 2;
   constexpr int B_BYTES = BN * BK * 2;
+  constexpr int WS_K = 256;
+  constexpr int B_RING = WS ? (WS_K / BK) : STAGES;   // B atoms resident (WS) or ring slots
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
   constexpr int STG_BYTES = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
@@ -180,12 +190,13 @@ __global__ void __launch_bounds__(384, 1)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES + STG_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + B_RING * B_BYTES + STG_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;    // [2] accumulator ready
   uint64_t* tempty = tfull + 2;        // [2] accumulator drained
   uint64_t* zfull = tempty + 2;        // *_LN: [2 warpgroups][2] z chunk landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zfull + 4);
+  uint64_t* wfull = zfull + 4;         // WS: weight slice landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
@@ -197,7 +208,7 @@ __global__ void __launch_bounds__(384, 1)
     if (TRANS) { m0 = (tile % num_m) * BM; n0 = (tile / num_m) * BN; }
     else       { m0 = (tile / num_n) * BM; n0 = (tile % num_n) * BN; }
   };
-  uint8_t* stg = sB + STAGES * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16);
+  uint8_t* stg = sB + B_RING * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16);
                                           // *_LN: 2 warpgroups x 2 x (128 x 32 fp32)
 
   if (warp == 0 && lane == 0) {
@@ -214,6 +225,7 @@ __global__ void __launch_bounds__(384, 1)
       tc::mbar_init(&tempty[s], LN ? 128 : 256);   // *_LN: one warpgroup drains a buffer
     }
     for (int s = 0; s < 4; ++s) tc::mbar_init(&zfull[s], 1);
+    tc::mbar_init(wfull, 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, TMEM_COLS);
@@ -226,15 +238,21 @@ __global__ void __launch_bounds__(384, 1)
     if (lane == 0) {
       // ---------------- TMA producer ----------------
       uint32_t it = 0;
+      if (WS && blockIdx.x < num_tiles) {   // the CTA's weight slice, once
+        int64_t m0, n0;
+        tile_mn(blockIdx.x, m0, n0);
+        tc::mbar_arrive_expect_tx(wfull, B_RING * B_BYTES);
+        for (int kb = 0; kb < B_RING; ++kb) tc::tma_load_2d(&tmB, sB + kb * B_BYTES, wfull, kb * BK, (int32_t)n0);
+      }
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
         int64_t m0, n0;
         tile_mn(tile, m0, n0);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           tc::mbar_wait(&empty[s], ph ^ 1);
-          tc::mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          tc::mbar_arrive_expect_tx(&full[s], WS ? A_BYTES : A_BYTES + B_BYTES);
           tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, (int32_t)m0);
-          tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, (int32_t)n0);
+          if (!WS) tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, (int32_t)n0);
         }
       }
     }
@@ -243,6 +261,7 @@ __global__ void __launch_bounds__(384, 1)
       // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
       uint32_t it = 0, lt = 0;
+      if (WS) tc::mbar_wait(wfull, 0);
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
         const uint32_t buf = lt & 1;
         tc::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
@@ -252,7 +271,7 @@ __global__ void __launch_bounds__(384, 1)
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           tc::mbar_wait(&full[s], ph);
           tc::tc_fence_after();
-          const uint32_t a0 = tc::smem_u32(sA + s * A_BYTES), b0 = tc::smem_u32(sB + s * B_BYTES);
+          const uint32_t a0 = tc::smem_u32(sA + s * A_BYTES), b0 = tc::smem_u32(sB + (WS ? kb : s) * B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = tc::sdesc(a0 + kk * 32, 16, 1024, tc::SW_128B);
@@ -508,7 +527,7 @@ int num_sms() {
   return n;
 }
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false>
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false, bool WS = false>
 bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                  cudaStream_t st) {
   // normal: kernel rows = activations A (M), cols = weights Bw (N)
@@ -531,15 +550,19 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
     if (!make_tmap_bf16(&tdm, ep.xn, M, N, N, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
   }
   constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
-  constexpr int smem = STAGES * (BM * BK * 2 + BN * BK * 2) + STG + 1024 + 256;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS>;
+  constexpr int smem = STAGES * BM * BK * 2 + (WS ? 256 / BK : STAGES) * BN * BK * 2 + STG + 1024 + 256;
+  static_assert(smem <= 227 * 1024, "shared memory");
+  if (WS && K != 256) return false;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS, WS>;
   static bool attr_set = false;   // per instantiation
   if (!attr_set) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
     attr_set = true;
   }
-  const int64_t tiles = ((Mk + BM - 1) / BM) * ((Nk + BN - 1) / BN);
-  const int grid = (int)std::min<int64_t>(tiles, num_sms());
+  const int64_t num_n = (Nk + BN - 1) / BN;
+  const int64_t tiles = ((Mk + BM - 1) / BM) * num_n;
+  int grid = (int)std::min<int64_t>(tiles, num_sms());
+  if (WS) grid = (int)std::max<int64_t>(num_n, grid / num_n * num_n);   // a CTA keeps one column tile
   kern<<<grid, 384, smem, st>>>(ta, tb, tcm, tdm, Mk, Nk, (int)K, ep);
   return true;
 }
@@ -562,6 +585,8 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
     constexpr int BN = 256, ST = 3;
     switch (epi) {
       case EPI_BIAS:
+        if (out_bf16 && K == 256 && ORBIT2_GEMM_WS)   // QKV at D = 256: weight-stationary
+          return launch_impl<BN, 4, EPI_BIAS, true, false, true>(A, Bw, M, N, K, ep, st);
         return out_bf16 ? launch_impl<BN, ST, EPI_BIAS, true>(A, Bw, M, N, K, ep, st)
                         : launch_impl<BN, ST, EPI_BIAS, false>(A, Bw, M, N, K, ep, st);
       case EPI_GELU: return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
