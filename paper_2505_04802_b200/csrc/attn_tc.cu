@@ -183,17 +183,28 @@ template <int NQ>
 __device__ __forceinline__ Item item_info(const ChunkDev& ch, int heads, int id) {
   // 32-bit division (n_items < 2^31 is checked at launch): a 64-bit one is a
   // subroutine call whose ABI spills registers in every role's loop
-  const int per_b = ch.nqp * heads;                   // item = (pair fastest, head, sample)
+  const int np = ch.core_pairs ? ch.nqc : ch.nqp;
+  const int per_b = np * heads;                       // item = (pair fastest, head, sample)
   Item it;
   const int b = id / per_b;
   const int r = id - b * per_b;
-  it.h = r / ch.nqp;
-  const int g = ch.qp0 + (r - it.h * ch.nqp);
-  const DevTile t = ch.tiles[ch.qpair_tile[g]];
+  it.h = r / np;
+  const int pr = r - it.h * np;
+  DevTile t;
+  int nq_max = NQ;
+  if (ch.core_pairs) {                                // last block: query blocks holding core tokens
+    const int e = ch.qpair_core[ch.qc0 + pr];
+    t = ch.tiles[e >> 16];
+    it.q0 = ((e & 0xFFFF) >> 1) * 128;
+    nq_max = min(NQ, (e & 1) + 1);
+  } else {
+    const int g = ch.qp0 + pr;
+    t = ch.tiles[ch.qpair_tile[g]];
+    it.q0 = (g - t.qp_off) * 128 * NQ;
+  }
   it.n = t.n_tokens;
   it.base = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0);
-  it.q0 = (g - t.qp_off) * 128 * NQ;
-  it.nq = min(NQ, (it.n - it.q0 + 127) / 128);
+  it.nq = min(nq_max, (it.n - it.q0 + 127) / 128);
   it.nkb = (it.n + 127) / 128;
   return it;
 }
@@ -715,7 +726,7 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
     if (sms <= 0) sms = 148;
     attr = true;
   }
-  const int64_t n_items = (int64_t)ch.nqp * heads * B;
+  const int64_t n_items = (int64_t)(ch.core_pairs ? ch.nqc : ch.nqp) * heads * B;
   if (n_items == 0) return true;
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM

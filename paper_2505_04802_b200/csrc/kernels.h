@@ -50,6 +50,9 @@ struct ChunkDev {
   int32_t qp0, nqp;
   const int32_t* qblk_tile;
   const int32_t* qpair_tile;
+  const int32_t* qpair_core;   // last block: (tile << 16 | first block << 1 | blocks - 1) holding core tokens
+  int32_t qc0, nqc;
+  int32_t core_pairs;          // attention over qpair_core instead of every pair
   const int32_t* core_row;
 };
 

@@ -43,6 +43,7 @@ struct Ctx {
   bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
+  bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -120,6 +121,10 @@ ChunkDev chunk_dev(const Ctx* c, const Chunk& ch) {
   d.nqp = ch.nqp;
   d.qblk_tile = c->at<int32_t>(p.lay.qblk_tile);
   d.qpair_tile = c->at<int32_t>(p.lay.qpair_tile);
+  d.qpair_core = c->at<int32_t>(p.lay.qpair_core);
+  d.qc0 = ch.qc0;
+  d.nqc = ch.nqc;
+  d.core_pairs = 0;
   d.core_row = c->at<int32_t>(p.lay.core_row);
   return d;
 }
@@ -194,12 +199,16 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->unfused_ln = ul && ul[0] == '1';
   const char* ub = std::getenv("ORBIT2_UNFUSED_BLOCK");
   c->unfused_block = ub && ub[0] == '1';
+  const char* aq = std::getenv("ORBIT2_ALL_QUERIES_LAST");
+  c->all_queries_last = aq && aq[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qblk_tile), p.qblk_tile.data(), p.qblk_tile.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qpair_tile.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qpair_tile), p.qpair_tile.data(), p.qpair_tile.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.qpair_core.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.qpair_core), p.qpair_core.data(), p.qpair_core.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.core_row.empty())
     e = cudaMemcpy(c->at<void>(p.lay.core_row), p.core_row.data(), p.core_row.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
@@ -391,7 +400,10 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       e.bias = wf(L.b_qkv); e.C = qkv; e.ldc = 3 * D;
       ORBIT2_TRY(gemm("qkv_gemm", EPI_BIAS, 1, xn, mrow, D, L.w_qkv, 3 * D, D, M, e));
       ORBIT2_TRY(run(c, "tile_attention", st, [&] {
-        return launch_attention_tc(qkv, mrow, ao, cd, B, (int)D, cf.heads, p.d, st);
+        // last block: only query pairs holding core tokens feed the head (R16)
+        ChunkDev ca = cd;
+        ca.core_pairs = l + 1 == cf.depth && !c->all_queries_last ? 1 : 0;
+        return launch_attention_tc(qkv, mrow, ao, ca, B, (int)D, cf.heads, p.d, st);
       }));
       if (tail_fused) {
         // O-projection + residual + LN2 + MLP + residual (+ LN1 of the next block) in

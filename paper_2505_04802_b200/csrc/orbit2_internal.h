@@ -36,12 +36,13 @@ struct Chunk {
   int64_t chunk_core;         // core tokens per sample in this chunk
   int32_t qb0, nqb;           // query blocks (per sample) of the chunk
   int32_t qp0, nqp;           // query-block pairs (per sample) of the chunk
+  int32_t qc0, nqc;           // last block: query-block pairs holding core tokens (per sample)
 };
 
 // Byte offsets of the workspace regions (from the workspace base).
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
-  int64_t tiles, qblk_tile, qpair_tile, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
+  int64_t tiles, qblk_tile, qpair_tile, qpair_core, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;
@@ -69,6 +70,10 @@ struct Plan {
   std::vector<DevTile> dev;             // rank-local device table
   std::vector<int32_t> qblk_tile;       // local q-block -> local tile index
   std::vector<int32_t> qpair_tile;      // local q-block pair -> local tile index
+  // last block (R16): only query pairs that hold core tokens are computed;
+  // entry = local tile index << 16 | first query block << 1 | (blocks - 1)
+  std::vector<int32_t> qpair_core;
+  std::vector<int32_t> qpc_off;         // per local tile (+ sentinel): first qpair_core entry
   std::vector<int32_t> core_row;        // local core token -> local padded token index
   orbit2_plan_info info;
   Layout lay;

@@ -167,6 +167,14 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     for (int32_t q = 0; q < nqb; ++q) p.qblk_tile.push_back(li);
     const int32_t nqp = (nqb + 1) / 2;
     for (int32_t q = 0; q < nqp; ++q) p.qpair_tile.push_back(li);
+    {   // core tokens of the tile span padded-rect tokens [c_first, c_last] (row-major)
+      const int32_t c_first = (dt.core_y0 - dt.pad_y0) * dt.pad_w + (dt.core_x0 - dt.pad_x0);
+      const int32_t c_last = (dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w + (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
+      p.qpc_off.push_back((int32_t)p.qpair_core.size());
+      const int32_t b0 = c_first / kQBlock, b1 = c_last / kQBlock;   // query blocks with core tokens
+      for (int32_t b = b0; b <= b1; b += 2)                           // entry: tile, first block, count - 1
+        p.qpair_core.push_back((li << 16) | (b << 1) | (b + 1 <= b1 ? 1 : 0));
+    }
     for (int32_t u = 0; u < dt.core_h; ++u)
       for (int32_t w = 0; w < dt.core_w; ++w)
         p.core_row.push_back((int32_t)(ltok + (int64_t)(u + dt.core_y0 - dt.pad_y0) * dt.pad_w +
@@ -179,6 +187,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     lcore += t.n_core_tokens;
     p.dev.push_back(dt);
   }
+  p.qpc_off.push_back((int32_t)p.qpair_core.size());
   // sentinel entry (offsets one past the end) simplifies chunk arithmetic
   {
     DevTile end{};
@@ -302,6 +311,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.tiles = take((int64_t)p.dev.size() * sizeof(DevTile));
   ly.qblk_tile = take((int64_t)p.qblk_tile.size() * 4);
   ly.qpair_tile = take((int64_t)p.qpair_tile.size() * 4);
+  ly.qpair_core = take((int64_t)p.qpair_core.size() * 4);
   ly.core_row = take((int64_t)p.core_row.size() * 4);
   ly.pos_u = take((int64_t)(p.Hp + 2 * h) * (p.D / 2) * 4);
   ly.pos_w = take((int64_t)(p.Wp + 2 * h) * (p.D / 2) * 4);
@@ -375,6 +385,8 @@ Chunk make_chunk(const Plan& p, int32_t tb, int32_t tc) {
   ch.nqb = p.dev[tb + tc].qb_off - ch.qb0;
   ch.qp0 = p.dev[tb].qp_off;
   ch.nqp = p.dev[tb + tc].qp_off - ch.qp0;
+  ch.qc0 = p.qpc_off[tb];
+  ch.nqc = p.qpc_off[tb + tc] - ch.qc0;
   return ch;
 }
 
