@@ -336,13 +336,18 @@ def run_ours(args, w, world, rank, local):
     clocks = clk.summary()
 
     # ---- end-to-end through the public API with host buffers ----
+    # Context.forward_host: pinned host input -> pinned host output for the whole
+    # batch, in groups of B / E2E_GROUPS samples so the PCIe copies (both
+    # directions) overlap the compute of the neighbouring groups
     h2d = x_pin.numel() * 4
     d2h = out.numel() * 4
+    groups = next(g for g in (8, 4, 2, 1) if B % g == 0)
+    ctx_h = o2.Context(o2.config_from(w, batch=B // groups, precision=o2.BF16, chunk_tiles=chunk)) \
+        if groups > 1 else ctx
+    packed_h = ctx_h.prepare_weights(torch.from_numpy(blob).cuda()) if groups > 1 else packed
 
     def e2e_step():
-        x_dev.copy_(x_pin, non_blocking=True)
-        step()
-        out_pin.copy_(out, non_blocking=True)
+        ctx_h.forward_host(packed_h, x_pin, out_pin, stream=stream)
 
     e2e_step()
     barrier(world)
@@ -384,7 +389,8 @@ def run_ours(args, w, world, rank, local):
         "gpu_launches": int(launches),
         "clocks": clocks,
         "e2e": {"value": px_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "api": "Context.forward_host",
+                "groups": groups},
     }
     if prof:
         work = class_work(w, info, B)

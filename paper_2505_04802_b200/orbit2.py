@@ -295,6 +295,61 @@ class Context:
             self.orbit2_stitch(tile_out, x_dev, tb, tc, out, stream)
         return out
 
+    # -- host buffers in, host buffers out (pipelined) ------------------------
+    def forward_host(self, packed, x_host, out_host, stream=None):
+        """The whole pass for N = k * cfg.batch samples held in PINNED host memory:
+        x_host [N,V,H,W] fp32 -> out_host [N,K,sH,sW] fp32.  Samples go through the
+        device in groups of cfg.batch; the host->device copy of group g+1 and the
+        device->host copy of group g-1 run on their own streams (copy engines, both
+        PCIe directions) while group g computes on `stream`.  Returns when the work
+        is queued; completion is ordered before later work on `stream`."""
+        import torch
+        G = self.cfg.batch
+        n = x_host.shape[0]
+        if n % G or out_host.shape[0] != n:
+            raise ValueError("forward_host: sample count must be a multiple of the context batch")
+        if not (x_host.is_pinned() and out_host.is_pinned()):
+            raise ValueError("forward_host: host buffers must be pinned")
+        comp = torch.cuda.current_stream(self.device) if stream is None else stream
+        if not hasattr(self, "_host_bufs"):
+            xs = tuple(torch.empty((G,) + tuple(x_host.shape[1:]), dtype=torch.float32, device=self.device)
+                       for _ in range(2))
+            os_ = tuple(torch.empty((G,) + tuple(out_host.shape[1:]), dtype=torch.float32, device=self.device)
+                        for _ in range(2))
+            self._host_bufs = (xs, os_, self.tile_out_buffer(),
+                               torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+        xs, os_, tile_out, s_in, s_out = self._host_bufs
+        start = torch.cuda.Event()
+        start.record(comp)
+        s_in.wait_event(start)
+        s_out.wait_event(start)
+        in_done = [torch.cuda.Event(), torch.cuda.Event()]
+        comp_done = [None, None]
+        out_done = [None, None]
+        for g in range(n // G):
+            b = g & 1
+            sl = slice(g * G, (g + 1) * G)
+            with torch.cuda.stream(s_in):
+                if comp_done[b] is not None:          # the compute that read xs[b] is done
+                    s_in.wait_event(comp_done[b])
+                xs[b].copy_(x_host[sl], non_blocking=True)
+                in_done[b].record(s_in)
+            comp.wait_event(in_done[b])
+            if out_done[b] is not None:               # os_[b] has been copied out
+                comp.wait_event(out_done[b])
+            self.forward(packed, xs[b], out=os_[b], tile_out=tile_out, stream=comp)
+            comp_done[b] = torch.cuda.Event()
+            comp_done[b].record(comp)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(comp_done[b])
+                out_host[sl].copy_(os_[b], non_blocking=True)
+                out_done[b] = torch.cuda.Event()
+                out_done[b].record(s_out)
+        for e in out_done:
+            if e is not None:
+                comp.wait_event(e)
+        return out_host
+
     # -- instrumentation ------------------------------------------------------
     def launch_count(self) -> int:
         return int(lib.orbit2_launch_count(self.handle))

@@ -246,3 +246,22 @@ def test_unfused_paths_match_oracle(env, monkeypatch):
     assert rel_err(sep, ref) < BF16_TOL
     assert rel_err(fused, ref) < BF16_TOL
     assert rel_err(sep, fused) < BF16_TOL
+
+
+@pytest.mark.gpu
+def test_forward_host_pipelined_matches_device_forward():
+    """Context.forward_host (pinned host in/out, groups of the context batch with
+    the PCIe copies overlapped on side streams) is bit-identical to the
+    device-resident forward of the whole batch (batch independence, I8)."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w, x, blob = _case("C2", batch=6, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    wd = torch.from_numpy(blob).cuda()
+    full = o2.Context(o2.config_from(w, batch=6, precision=BF16))
+    ref = full.forward(full.prepare_weights(wd), torch.from_numpy(x).cuda())
+    grp = o2.Context(o2.config_from(w, batch=2, precision=BF16))
+    x_pin = torch.from_numpy(x).pin_memory()
+    out_pin = torch.full(tuple(ref.shape), float("nan"), dtype=torch.float32).pin_memory()
+    grp.forward_host(grp.prepare_weights(wd), x_pin, out_pin)
+    torch.cuda.synchronize()
+    assert torch.equal(out_pin, ref.cpu())
