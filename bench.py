@@ -341,7 +341,7 @@ def run_ours(args, w, world, rank, local):
     # directions) overlap the compute of the neighbouring groups
     h2d = x_pin.numel() * 4
     d2h = out.numel() * 4
-    groups = next(g for g in (8, 4, 2, 1) if B % g == 0)
+    groups = int(os.environ.get("ORBIT2_E2E_GROUPS", "0")) or next(g for g in (8, 4, 2, 1) if B % g == 0)
     ctx_h = o2.Context(o2.config_from(w, batch=B // groups, precision=o2.BF16, chunk_tiles=chunk)) \
         if groups > 1 else ctx
     packed_h = ctx_h.prepare_weights(torch.from_numpy(blob).cuda()) if groups > 1 else packed

@@ -109,6 +109,9 @@ __device__ __forceinline__ float2 ex2_poly2(float x0, float x1) {
 #endif
 // control warpgroup gives registers to the softmax warpgroups (no spills in the exp loop)
 constexpr bool kRegRealloc = ORBIT2_ATTN_REGREALLOC != 0;
+#ifndef ORBIT2_ATTN_KVST
+#define ORBIT2_ATTN_KVST 2
+#endif
 #ifndef ORBIT2_ATTN_PINGPONG
 #define ORBIT2_ATTN_PINGPONG 0   // measured slower (C2: 22.0 vs 19.5 ms): one warp per SM sub-partition reaches ~69% of the MUFU rate
 #endif
@@ -138,8 +141,8 @@ struct AttnCfg {
   static constexpr uint32_t SW = DH == 32 ? tc::SW_64B : tc::SW_128B;
   static constexpr int QBUF = DH == 128 ? 1 : 2;      // Q tiles of the next work item prefetched
   static constexpr int NPH = kSplitP ? 2 : 1;         // P / PV parts with their own barriers
-  static constexpr int KST = DH == 128 ? 1 : 2;       // K ring (consumed by S_{j+1}, early)
-  static constexpr int VST = DH == 128 ? 1 : 2;       // V ring (consumed by PV_j, late)
+  static constexpr int KST = DH == 128 ? 1 : ORBIT2_ATTN_KVST;   // K ring (consumed by S_{j+1}, early)
+  static constexpr int VST = DH == 128 ? 1 : ORBIT2_ATTN_KVST;   // V ring (consumed by PV_j, late)
   static constexpr int P_BYTES = 128 * 128 * 2;
   // producer (+TMEM alloc), one MMA issuer per Q tile; padded to a whole warpgroup
   // when registers are reallocated (setmaxnreg acts per warpgroup)

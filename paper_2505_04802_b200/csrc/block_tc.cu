@@ -143,7 +143,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* o_full = h_free + 2;           // last GEMM2 of the block done
   uint64_t* op_full = o_full + 1;          // O-projection done
   uint64_t* xn_full = op_full + 1;         // z' in TMEM, LN2(z') in X
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xn_full + 1);
+  uint64_t* zready = xn_full + 1;          // [RI_Z] z slice p of this block landed (relayed by the MMA thread)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zready + RI_Z);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t num_tiles = (M + BM - 1) / BM;
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::mbar_init(o_full, 1);
     tc::mbar_init(op_full, 1);
     tc::mbar_init(xn_full, ET);
+    for (int z = 0; z < RI_Z; ++z) tc::mbar_init(&zready[z], 1);
     tc::fence_barrier_init();
   }
   if (warp == 2) tc::tmem_alloc(tmem_slot, 512);
@@ -262,7 +264,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::mma_commit(op_full);
         BTL(0, tl_, 1);
-        it += RI_Z;                          // z slices: consumed by the epilogue
+        // z slices: consumed by the epilogue.  The ring's full barriers are waited
+        // on by this thread only, in ring order (a parity wait is only safe when the
+        // slot's previous load is known to be complete), and relayed per slice.
+        for (int zp = 0; zp < RI_Z; ++zp, ++it) {
+          tc::mbar_wait(&w_full[it % RS], (it / RS) & 1);
+          tc::mbar_arrive(&zready[zp]);
+        }
         tc::mbar_wait(xn_full, tl_ & 1);     // z' in the O region, LN2(z') in X
         BTL(0, tl_, 2);
         tc::tc_fence_after();
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
       for (int zi = 0; zi < 2; ++zi) {
         const uint32_t gi = ring0 + 2 * zi + wg, sl = gi % RS;
-        tc::mbar_wait(&w_full[sl], (gi / RS) & 1);
+        tc::mbar_wait(&zready[2 * zi + wg], tl_ & 1);   // relayed by the MMA thread
         const uint8_t* zs = sW + sl * SLOT;
 #pragma unroll
         for (int hb = 0; hb < 2; ++hb) {

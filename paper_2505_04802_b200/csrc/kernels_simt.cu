@@ -88,7 +88,15 @@ __global__ void __launch_bounds__(128) gather_staged_kernel(const float* __restr
       T* dst = sp + wr * ld + dx;
       for (int dy = 0; dy < p; ++dy) {
         const float* s0 = src + (int64_t)min(max(p * u + dy, 0), H - 1) * W;
-        for (int v = 0; v < V; ++v) dst[v * pp + dy * p] = to_out<T>(__ldg(s0 + (int64_t)v * H * W));
+        int v = 0;
+        for (; v + 8 <= V; v += 8) {   // 8 independent loads in flight per thread
+          float f[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) f[k] = __ldg(s0 + (int64_t)(v + k) * H * W);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) dst[(v + k) * pp + dy * p] = to_out<T>(f[k]);
+        }
+        for (; v < V; ++v) dst[v * pp + dy * p] = to_out<T>(__ldg(s0 + (int64_t)v * H * W));
       }
     }
     for (int idx = threadIdx.x; idx < nw * (din_pad - din); idx += blockDim.x) {

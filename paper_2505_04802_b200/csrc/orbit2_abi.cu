@@ -40,6 +40,7 @@ struct Ctx {
   std::vector<cudaEvent_t> pool;
   std::map<std::string, std::pair<int64_t, double>> acc;
   bool sync_check = false;
+  bool trace = false;         // ORBIT2_TRACE=1: kernel names to stderr before each launch (hang hunting)
   bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
@@ -82,6 +83,10 @@ orbit2_status run(Ctx* c, const char* name, cudaStream_t st, F&& f) {
     a = take_event(c);
     b = take_event(c);
     cudaEventRecord(a, st);
+  }
+  if (c->trace) {
+    std::fprintf(stderr, "[orbit2] launch %s\n", name);
+    std::fflush(stderr);
   }
   bool ok = f();
   c->launches += 1;
@@ -193,6 +198,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->wl = weight_layout(p);
   const char* sc = std::getenv("ORBIT2_SYNC_CHECK");
   c->sync_check = sc && sc[0] == '1';
+  const char* tr = std::getenv("ORBIT2_TRACE");
+  c->trace = tr && tr[0] == '1';
   const char* um = std::getenv("ORBIT2_UNFUSED_MLP");
   c->unfused_mlp = um && um[0] == '1';
   const char* ul = std::getenv("ORBIT2_UNFUSED_LN");
