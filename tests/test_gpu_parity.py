@@ -265,3 +265,23 @@ def test_forward_host_pipelined_matches_device_forward():
     grp.forward_host(grp.prepare_weights(wd), x_pin, out_pin)
     torch.cuda.synchronize()
     assert torch.equal(out_pin, ref.cpu())
+
+
+@pytest.mark.gpu
+def test_repeated_small_batch_forwards_bit_identical():
+    """Regression for the block-tail ring race (an out-of-order parity wait on a
+    ring slot whose previous TMA load was still in flight): many small-batch
+    forwards of the D = 256 path, several row blocks per CTA, must all finish and
+    agree bit for bit."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w, x, blob = _case("C2", batch=4, depth=2)
+    ctx = o2.Context(o2.config_from(w, batch=4, precision=BF16))
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    xd = torch.from_numpy(x).cuda()
+    first = ctx.forward(packed, xd).clone()
+    out = torch.empty_like(first)
+    for _ in range(12):
+        ctx.forward(packed, xd, out=out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, first)
