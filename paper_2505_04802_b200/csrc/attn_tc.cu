@@ -118,6 +118,12 @@ constexpr bool kRegRealloc = ORBIT2_ATTN_REGREALLOC != 0;
 // the two Q tiles' exponential phases alternate (named barriers 1 / 2): one
 // tile's row max, waits and epilogue overlap the other tile's exponentials
 constexpr bool kPingPong = ORBIT2_ATTN_PINGPONG != 0;
+#ifndef ORBIT2_ATTN_SPLITROW
+#define ORBIT2_ATTN_SPLITROW 0   // measured slower (C2: 19.5 vs 19.1 ms)
+#endif
+// two softmax warps per query row (64 keys each) at head dim 64: four softmax
+// warps per SM sub-partition to hide the exponential loop's latencies
+constexpr bool kSplitRow = ORBIT2_ATTN_SPLITROW != 0;
 #ifndef ORBIT2_ATTN_SPLITP
 #define ORBIT2_ATTN_SPLITP 0   // measured slower (C2: 21.6 vs 19.9 ms): the 128-arrival part barriers wait for the slowest warp
 #endif
@@ -147,13 +153,18 @@ struct AttnCfg {
   // producer (+TMEM alloc), one MMA issuer per Q tile; padded to a whole warpgroup
   // when registers are reallocated (setmaxnreg acts per warpgroup)
   static constexpr int CTRL_WARPS = kRegRealloc ? 4 : 1 + NQ;
-  static constexpr int THREADS = 32 * CTRL_WARPS + 128 * NQ;   // + one softmax thread per query row
+  static constexpr int SPW_ = kSplitRow && DH == 64 ? 2 : 1;  // softmax warps per query row (see P_TMEM)
   // P lives in TMEM (64 columns of bf16 pairs) and feeds the PV MMA as the A
   // operand when TMEM allows: no shared-memory traffic for P (the SS form
   // re-reads the 128 x 16 A tile from smem on every K step, which made the
   // kernel shared-memory-bandwidth bound).
   static constexpr bool P_TMEM = NQ * (128 + DH + 64) <= 512;
   static constexpr int TCOLS = 128 + DH + (P_TMEM ? 64 : 0);   // S | O | (P)
+  static constexpr int SPW = (SPW_ > 1 && P_TMEM && NPH == 1 && !kPingPong) ? SPW_ : 1;
+  static constexpr int KC = 128 / SPW;                // keys per softmax thread and block
+  static constexpr int THREADS = 32 * CTRL_WARPS + 128 * NQ * SPW;   // + SPW softmax threads per query row
+  // row-max (2 block parities) and row-sum exchange between the warps of a row
+  static constexpr int XCH_BYTES = SPW > 1 ? NQ * (2 * 2 + 2) * 128 * 4 : 0;
   static constexpr int TMEM_COLS = NQ * TCOLS <= 256 ? 256 : 512;
   static constexpr int P_SMEM = P_TMEM ? 0 : P_BYTES;
   static constexpr int SMEM_BASE = QBUF * NQ * TILE + (KST + VST) * TILE + NQ * P_SMEM + 1024 + 512;
@@ -163,7 +174,7 @@ struct AttnCfg {
   static constexpr bool STAGED = kStagedEpilogue && SMEM_BASE + 4 * NQ * 32 * OST_ROW + 256 <= 227 * 1024;
   static constexpr int OST_WARP = STAGED ? 32 * OST_ROW : 0;
   static constexpr int IRING = 4;                      // work-item descriptors published by the producer
-  static constexpr int SMEM = SMEM_BASE + 4 * NQ * OST_WARP + 256;
+  static constexpr int SMEM = SMEM_BASE + 4 * NQ * OST_WARP + XCH_BYTES + 256;
 };
 
 // Conditional rescale threshold (log2 units): the reference max of a row is
@@ -243,7 +254,8 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
   uint8_t* sV = sK + C::KST * C::TILE;              // [VST][TILE]
   uint8_t* sP = sV + C::VST * C::TILE;              // [NQ][P_SMEM]
   uint8_t* sOst = sP + NQ * C::P_SMEM;              // [4 * NQ][OST_WARP]
-  Item* sItem = reinterpret_cast<Item*>(sOst + 4 * NQ * C::OST_WARP);   // [IRING]
+  float* sXch = reinterpret_cast<float*>(sOst + 4 * NQ * C::OST_WARP);   // [XCH_BYTES / 4]
+  Item* sItem = reinterpret_cast<Item*>(reinterpret_cast<uint8_t*>(sXch) + C::XCH_BYTES);   // [IRING]
   uint64_t* bar = reinterpret_cast<uint64_t*>(sItem + C::IRING);
   uint64_t* q_full = bar;                           // [QBUF]
   uint64_t* q_empty = q_full + C::QBUF;             // [QBUF]
@@ -278,16 +290,16 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     }
     for (int s = 0; s < NQ; ++s) {
       tc::mbar_init(&s_full[s], 1);
-      tc::mbar_init(&s_free[s], 128);
+      tc::mbar_init(&s_free[s], 128 * C::SPW);
       for (int h = 0; h < C::NPH; ++h) {
-        tc::mbar_init(&p_full[s * C::NPH + h], 128);
+        tc::mbar_init(&p_full[s * C::NPH + h], 128 * C::SPW);
         tc::mbar_init(&p_free[s * C::NPH + h], 1);
       }
-      tc::mbar_init(&o_free[s], 128);
+      tc::mbar_init(&o_free[s], 128 * C::SPW);
     }
     for (int s = 0; s < C::IRING; ++s) {
       tc::mbar_init(&it_full[s], 1);
-      tc::mbar_init(&it_empty[s], NQ + 4 * NQ);   // MMA-issuer warps + softmax warps
+      tc::mbar_init(&it_empty[s], NQ + 4 * NQ * C::SPW);   // MMA-issuer warps + softmax warps
     }
     tc::fence_barrier_init();
   }
@@ -459,13 +471,19 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     // Thread = query row i of Q tile qt (TMEM lane i: warp w reads lane quarter
     // w % 4; any 4 consecutive warps cover the quarters).  Both tiles' softmax
     // warps run concurrently (two warps per SM sub-partition feed the MUFU).
-    const int qt = (warp - C::CTRL_WARPS) / 4;
+    constexpr int SPW = C::SPW, KC = C::KC;
+    const int sidx = warp - C::CTRL_WARPS;
+    const int qt = sidx / (4 * SPW);
+    const int hh = (sidx / 4) % SPW;               // which KC keys of the block this warp owns
     const int q = warp & 3;
     const int i = q * 32 + lane;                   // query row within the Q tile
     const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + qt * C::TCOLS;
-    const uint32_t s_addr = lane_base;
+    const uint32_t s_addr = lane_base + hh * KC;
     const uint32_t o_addr = lane_base + 128;
-    const uint32_t p_tm = lane_base + 128 + DH;
+    const uint32_t p_tm = lane_base + 128 + DH + hh * (KC / 2);
+    constexpr int OC = DH / SPW;                   // O columns this warp rescales / stores
+    const uint32_t tile_bar = 1 + qt;              // both halves of a tile's rows (SPW > 1)
+    const uint32_t pair_bar = 3 + qt * 4 + q;      // the SPW warps of one 32-row slice
     const float sl = 1.4426950408889634f * rsqrtf((float)DH);   // log2(e)/sqrt(d)
     uint32_t cs = 0;                               // blocks processed by this Q tile (all items)
     uint32_t ni_sm = 0;                            // items processed (debug timeline only)
@@ -488,7 +506,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         continue;
       }
       float m_ref = -INFINITY, l_run = 0.f;
-      const bool tlr = q == 0 && lane == 0;
+      const bool tlr = q == 0 && lane == 0 && hh == 0;
       // Only rows inside the tile take part in the (warp-uniform) range votes, so
       // results do not depend on packing, chunking or the rank assignment.
       const bool row_valid = it.q0 + qt * 128 + i < it.n;
@@ -497,31 +515,38 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         tc::mbar_wait(&s_full[qt], cs & 1);
         if (tlr) TL_STAMP(qt, cs, 1);
         tc::tc_fence_after();
-        float sv[128];
+        float sv[KC];
         {
           uint32_t* r = reinterpret_cast<uint32_t*>(sv);
 #pragma unroll
-          for (int c0 = 0; c0 < 128; c0 += 32)
+          for (int c0 = 0; c0 < KC; c0 += 32)
             tc::tmem_ld32(s_addr + c0, *reinterpret_cast<uint32_t(*)[32]>(r + c0));
           tc::tmem_ld_wait();
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&s_free[qt]);               // TMEM S columns may take the next S
         if (tlr) TL_STAMP(qt, cs, 2);
-        const int kvalid = it.n - j * 128;
-        if (kvalid < 128) {
+        const int kvalid = it.n - j * 128 - hh * KC;
+        if (kvalid < KC) {
 #pragma unroll
-          for (int c = 0; c < 128; ++c)
+          for (int c = 0; c < KC; ++c)
             if (c >= kvalid) sv[c] = -INFINITY;
         }
         auto row_max = [&]() {
           float m0 = sv[0], m1 = sv[1], m2 = sv[2], m3 = sv[3];
 #pragma unroll
-          for (int c = 4; c < 128; c += 4) {
+          for (int c = 4; c < KC; c += 4) {
             m0 = fmaxf(m0, sv[c]); m1 = fmaxf(m1, sv[c + 1]);
             m2 = fmaxf(m2, sv[c + 2]); m3 = fmaxf(m3, sv[c + 3]);
           }
-          return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl;
+          float m = fmaxf(fmaxf(m0, m1), fmaxf(m2, m3));
+          if constexpr (SPW > 1) {   // the other warp of the row: exchange through smem
+            float* xm = sXch + (qt * 2 + (cs & 1)) * 2 * 128;
+            xm[hh * 128 + i] = m;
+            asm volatile("bar.sync %0, %1;" ::"r"(tile_bar), "r"(128 * SPW) : "memory");
+            m = fmaxf(m, xm[(hh ^ 1) * 128 + i]);
+          }
+          return m * sl;
         };
         // O rescale by 2^(m_ref - m_new) (tcgen05.ld/st are warp-collective: callers
         // take the decision warp-uniformly); needs the previous PV complete.
@@ -529,7 +554,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           const float alpha = ex2(m_ref - m_new);
           l_run *= alpha;
 #pragma unroll
-          for (int c0 = 0; c0 < DH; c0 += 16) {
+          for (int c0 = hh * OC; c0 < (hh + 1) * OC; c0 += 16) {
             uint32_t r[16];
             tc::tmem_ld16(o_addr + c0, r);
             tc::tmem_ld_wait();
@@ -565,7 +590,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         if (tlr) TL_STAMP(qt, cs, 3);
         // p = 2^(s * log2(e)/sqrt(d) - m_ref) -> bf16 P (TMEM: A operand of the PV MMA;
         // smem when TMEM is short), part by part, with fp32 row sums
-        constexpr int KP = 128 / C::NPH;               // keys per part
+        constexpr int KP = KC / C::NPH;                // keys per part
         float rs0 = 0.f, rs1 = 0.f;
         if constexpr (kPingPong) pp_sync(1 + qt);   // this tile's turn on the MUFU
 #pragma unroll
@@ -625,6 +650,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       for (int h = 0; h < C::NPH; ++h) tc::mbar_wait(&p_free[qt * C::NPH + h], (cs - 1) & 1);
       tc::tc_fence_after();
       if (tlr) TL_STAMP(5 + qt, ni_sm, 1);
+      if constexpr (SPW > 1) {   // row sum over both warps of the row
+        float* xl = sXch + NQ * 2 * 2 * 128 + qt * 2 * 128;
+        xl[hh * 128 + i] = l_run;
+        asm volatile("bar.sync %0, %1;" ::"r"(tile_bar), "r"(128 * SPW) : "memory");
+        l_run += xl[(hh ^ 1) * 128 + i];
+      }
       const float inv = 1.f / l_run;
       if constexpr (C::STAGED) {
         // O / l -> bf16, staged in this warp's 32-row slice in the TMA store's
@@ -632,12 +663,14 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         // conflict-free), then one TMA tensor store of the 32 x DH box issued by
         // one lane.  A warp whose rows run past the tile end (the partial last
         // query block) stores its valid rows directly instead.
-        uint8_t* sw = sOst + (warp - C::CTRL_WARPS) * C::OST_WARP;
+        uint8_t* sw = sOst + (qt * 4 + q) * C::OST_WARP;   // the 32-row slice of this warp (pair)
         auto swz = [](uint32_t off) { return off ^ (((off >> 7) & C::OSW_MASK) << 4); };
-        if (lane == 0) tc::bulk_wait_read<0>();        // the previous item's store has read the slice
-        __syncwarp();
+        const bool st_lane = lane == 0 && hh == 0;     // issues the slice's TMA store
+        if (st_lane) tc::bulk_wait_read<0>();          // the previous item's store has read the slice
+        if constexpr (SPW > 1) asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "r"(32 * SPW) : "memory");
+        else __syncwarp();
 #pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {          // 32 columns per TMEM load, one wait each
+        for (int c0 = hh * OC; c0 < (hh + 1) * OC; c0 += 32) {   // 32 columns per TMEM load
           uint32_t r[32];
           tc::tmem_ld32(o_addr + c0, r);
           tc::tmem_ld_wait();
@@ -656,9 +689,10 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         const int row0 = it.q0 + qt * 128 + q * 32;    // first query row of this warp
         if (row0 + 32 <= it.n) {
           tc::fence_proxy_async_smem();
-          __syncwarp();
+          if constexpr (SPW > 1) asm volatile("bar.sync %0, %1;" ::"r"(pair_bar), "r"(32 * SPW) : "memory");
+          else __syncwarp();
           if (tlr) TL_STAMP(5 + qt, ni_sm, 5);
-          if (lane == 0) {
+          if (st_lane) {
             tc::tma_store_2d(&tmo, sw, it.h * DH, (int32_t)(it.base + row0));
             tc::bulk_commit();
           }
@@ -666,7 +700,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
           __syncwarp();
           if (row0 + lane < it.n) {
 #pragma unroll
-            for (int c = 0; c < DH / 8; ++c)
+            for (int c = hh * OC / 8; c < (hh + 1) * OC / 8; ++c)
               *reinterpret_cast<uint4*>(out + (it.base + row0 + lane) * (int64_t)D + it.h * DH + c * 8) =
                   *reinterpret_cast<const uint4*>(sw + swz(lane * C::OST_ROW + c * 16));
           }
