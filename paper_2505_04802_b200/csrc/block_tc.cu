@@ -125,7 +125,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const __grid_constant__ CUtensorMap tmZ, const __grid_constant__ CUtensorMap tmXn,
                     const float* __restrict__ bo, const float* __restrict__ g2, const float* __restrict__ be2,
                     const float* __restrict__ b1, const float* __restrict__ b2, const float* __restrict__ g1n,
-                    const float* __restrict__ be1n, int64_t M, long long* __restrict__ tl) {
+                    const float* __restrict__ be1n, int64_t M, const int32_t* __restrict__ rblk,
+                    int32_t nrblk, long long* __restrict__ tl) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sX = smem;                      // o tile, then LN2(z') (SW128 K-major, 4 atoms of 64 columns)
@@ -147,7 +148,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(zready + RI_Z);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t num_tiles = (M + BM - 1) / BM;
+  // work list: every 128-row block, or (last block of the model) the listed ones
+  const int64_t num_tiles = rblk != nullptr ? (int64_t)nrblk : (M + BM - 1) / BM;
+  auto row_block = [&](int64_t k) -> int64_t { return rblk != nullptr ? (int64_t)__ldg(rblk + k) : k; };
 
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tmA);
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         return sW + s * SLOT;
       };
       for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++tl_) {
-        const int32_t m0 = (int32_t)(tile * BM);
+        const int32_t m0 = (int32_t)(row_block(tile) * BM);
         tc::mbar_wait(x_free, (tl_ & 1) ^ 1);
         tc::mbar_arrive_expect_tx(x_full, X_BYTES);
         for (int a = 0; a < DM / 64; ++a) tc::tma_load_2d(&tmA, sX + a * 16384, x_full, a * 64, m0);
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_wait(o_full, tl_ & 1);
       if (stp) BTL(1, tl_, 5);
       tc::tc_fence_after();
-      const int32_t m0 = (int32_t)(tile * BM);
+      const int32_t m0 = (int32_t)(row_block(tile) * BM);
       float sum2 = 0.f, sq2 = 0.f, shift2 = 0.f;
 #pragma unroll 1
       for (int k = 0; k < 128 / ZC; ++k) {
@@ -538,7 +541,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const float* bo, const float* ln2_g,
                        const float* ln2_b, const void* w1, const float* b1, const void* w2, const float* b2,
                        float* z, int64_t M, int D, const float* ln1n_g, const float* ln1n_b, void* xn_next,
-                       cudaStream_t st) {
+                       const int32_t* row_blocks, int32_t n_row_blocks, cudaStream_t st) {
   if (D != DM || M <= 0) return false;
   CUtensorMap ta, two, t1, t2, tz, txn;
   std::memset(&txn, 0, sizeof(txn));
@@ -559,10 +562,11 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t tiles = (M + BM - 1) / BM;
+  const int64_t tiles = row_blocks != nullptr ? (int64_t)n_row_blocks : (M + BM - 1) / BM;
+  if (tiles == 0) return true;
   const int grid = (int)std::min<int64_t>(tiles, sms);
   block_tc_kernel<<<grid, THREADS, SMEM, st>>>(ta, two, t1, t2, tz, txn, bo, ln2_g, ln2_b, b1, b2, ln1n_g, ln1n_b,
-                                               M, g_mlp_timeline);
+                                               M, row_blocks, n_row_blocks, g_mlp_timeline);
   return true;
 }
 

@@ -94,7 +94,9 @@ bool launch_mlp_fused(const void* xn, int64_t rows_alloc, const void* w1, const 
 bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const float* bo, const float* ln2_g,
                        const float* ln2_b, const void* w1, const float* b1, const void* w2, const float* b2,
                        float* z, int64_t M, int D, const float* ln1n_g /* null: no next-block LN1 */,
-                       const float* ln1n_b, void* xn_next, cudaStream_t st);
+                       const float* ln1n_b, void* xn_next,
+                       const int32_t* row_blocks /* null: every 128-row block */, int32_t n_row_blocks,
+                       cudaStream_t st);
 
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();

@@ -43,6 +43,7 @@ struct Chunk {
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
   int64_t tiles, qblk_tile, qpair_tile, qpair_core, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
+  int64_t core_rblk;          // last block: 128-row blocks holding core tokens (built per chunk)
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;

@@ -312,6 +312,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.qblk_tile = take((int64_t)p.qblk_tile.size() * 4);
   ly.qpair_tile = take((int64_t)p.qpair_tile.size() * 4);
   ly.qpair_core = take((int64_t)p.qpair_core.size() * 4);
+  ly.core_rblk = take((ly.mrow / kQBlock + 1) * 4);
   ly.core_row = take((int64_t)p.core_row.size() * 4);
   ly.pos_u = take((int64_t)(p.Hp + 2 * h) * (p.D / 2) * 4);
   ly.pos_w = take((int64_t)(p.Wp + 2 * h) * (p.D / 2) * 4);
