@@ -438,3 +438,24 @@ def test_constant_and_ramp_inputs_residual():
     want = 0.5 + 0.25 * Y[:, None] - 0.125 * X[None, :]
     inner = (slice(s, -s), slice(s, -s))
     np.testing.assert_allclose(up[0][inner], want[inner], rtol=0, atol=1e-12)
+
+
+def test_golden_paper_sequence_lengths():
+    """tests/golden/paper_sequence_lengths.txt: every sequence length the paper prints
+    (P:150), reproduced by the oracle's count at the paper's printed precision."""
+    import pathlib
+    path = pathlib.Path(__file__).parent / "golden" / "paper_sequence_lengths.txt"
+    rows = [ln.split() for ln in path.read_text().splitlines()
+            if ln.strip() and not ln.startswith("#")]
+    assert len(rows) == 6
+    for r in rows:
+        h, w, c, p = (int(x) for x in r[:4])
+        printed, unit = float(r[4]), float(r[5])
+        exact = O.paper_sequence_length(h, w, c, p)
+        digits = len(r[4].split(".")[1]) if "." in r[4] else 0
+        # the paper mixes truncation (298.6M -> "298M", 1.19B -> "1.1B") and rounding
+        # (4.199B -> "4.2B"): the exact count lies within one unit of the last printed digit
+        scale = unit / 10 ** digits
+        assert abs(exact - printed * unit) < scale, (r, exact)
+        assert round(exact / scale) * scale == printed * unit or \
+            int(exact // scale) * scale == printed * unit, (r, exact)
