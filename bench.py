@@ -201,6 +201,27 @@ def auto_chunk(o2, w, B):
     raise RuntimeError("workload does not fit one GPU even one tile at a time")
 
 
+def class_bytes_embed(w, info, B):
+    """Algorithmic HBM bytes of the embedding GEMM per step: bf16 patch rows in
+    (2 Din), fp32 z out (4 D) and, when LN1 of block 0 is fused (D = 256), bf16 xn
+    out (2 D); weights are negligible."""
+    ln = 2.0 * w.embed if (w.embed == 256 and w.depth > 0) else 0.0
+    return B * info.tokens_per_sample * (2.0 * w.din + 4.0 * w.embed + ln)
+
+
+def host_cpu():
+    """nproc and the /proc/cpuinfo model of the host the oracle runs on."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def attn_bytes(w, info, B):
     """Algorithmic HBM bytes of one attention launch: read Q,K,V (bf16) once,
     write the head outputs (bf16) once, over all padded tokens."""
@@ -283,7 +304,7 @@ def run_reference(args, w, world, rank):
         "data": "synthetic (ERA5-shaped, seeded)",
         "config": {"workload": w.name, "batch": 1, "step": "one (sample, tile) unit of the workload"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                         "sample": f"1 (sample, tile) unit of {w.name} per step (fp64 numpy oracle)"},
+                         "sample": f"1 (sample, tile) unit of {w.name} per step (fp64 numpy oracle)", **host_cpu()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -425,24 +446,43 @@ def run_ours(args, w, world, rank, local):
             traffic = tr["dram_bytes_per_launch"] * B / tr["batch"]
             traffic_note = (f"ncu --set full dram read+write of one {dom} launch at batch {tr['batch']} "
                             f"({tr['source']}), scaled linearly to batch {B}")
+        # Peak choice: the timed region is far below the 4 s over which MEASURED_PEAKS'
+        # sustained figure was taken (and runs at the clocks sampled above), so a kernel
+        # in it is compared with the BURST peak; the sustained ratio is reported beside it.
+        region_s = ms * 1e-3 * args.steps
+        peak_kind = "burst" if region_s < 4.0 else "sustained"
         if bound == "tensor":
             achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e12
-            peak = pk["bf16_sus"]
+            peak = pk["bf16"] if peak_kind == "burst" else pk["bf16_sus"]
             res["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": achieved, "peak": peak,
                                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                                "traffic_note": traffic_note,
                                "algorithmic_bytes_per_launch": attn_bytes(w, info, B) if dom == "tile_attention" else None,
-                               "peak_src": pk["src"] + " bf16_tflops_sustained (kernel timed inside the step)",
-                               "frac_of_burst": achieved / pk["bf16"]}
+                               "peak_src": f"{pk['src']} bf16_tflops ({peak_kind}: timed region {region_s:.2f} s "
+                                           f"at {clocks.get('sm_mhz')} MHz median)",
+                               "frac_of_burst": achieved / pk["bf16"], "frac_of_sustained": achieved / pk["bf16_sus"]}
         else:
             achieved = amount / launches_dom / (per_launch_ms * 1e-3) / 1e9
             res["roofline"] = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": pk["hbm"],
                                "unit": "GB/s", "frac": achieved / pk["hbm"], "traffic": traffic,
                                "traffic_note": traffic_note, "peak_src": pk["src"]}
+        for k, v in classes.items():      # every class against its own roofline
+            if "tflops" in v:
+                v["frac_of_burst"] = v["tflops"] / pk["bf16"]
+            if "gbs" in v:
+                v["frac_of_hbm"] = v["gbs"] / pk["hbm"]
         att = classes.get("tile_attention")
         if att and "tflops" in att:
             res["attn_tflops"] = att["tflops"]
-            res["attn_frac_bf16_peak"] = att["tflops"] / pk["bf16_sus"]
+            res["attn_frac_bf16_peak"] = att["tflops"] / pk["bf16"]
+            res["attn_frac_bf16_sustained"] = att["tflops"] / pk["bf16_sus"]
+        res["hbm_kernels"] = {k: {"gbs": classes[k]["gbs"], "frac_of_hbm": classes[k]["gbs"] / pk["hbm"]}
+                              for k in ("tile_gather", "stitch_residual", "layernorm") if k in classes
+                              and "gbs" in classes[k]}
+        if "embed_gemm" in classes:   # HBM-bound at Din = 80: patches in, z (+ LN1 xn) out
+            eb = class_bytes_embed(w, info, B)
+            g = eb / (classes["embed_gemm"]["ms_per_step"] * 1e-3) / 1e9
+            res["hbm_kernels"]["embed_gemm"] = {"gbs": g, "frac_of_hbm": g / pk["hbm"]}
         # measured tensor-core classes other than attention (GEMMs, fused MLP / block tail)
         tck = [k for k in classes if k in work and work[k][0] == "tensor" and k != "tile_attention"]
         gemm_ms = sum(classes[k]["ms_per_step"] for k in tck)
@@ -450,14 +490,17 @@ def run_ours(args, w, world, rank, local):
         res["gemm_tflops"] = gemm_f / (gemm_ms * 1e-3) / 1e12 if gemm_ms else None
         tc_ms = gemm_ms + (att["ms_per_step"] if att else 0)
         tc_f = gemm_f + work["tile_attention"][1]
-        res["attn_gemm_frac_bf16_peak"] = tc_f / (tc_ms * 1e-3) / 1e12 / pk["bf16_sus"] if tc_ms else None
+        res["attn_gemm_tflops"] = tc_f / (tc_ms * 1e-3) / 1e12 if tc_ms else None
+        res["attn_gemm_frac_bf16_peak"] = res["attn_gemm_tflops"] / pk["bf16"] if tc_ms else None
+        res["attn_gemm_frac_bf16_sustained"] = res["attn_gemm_tflops"] / pk["bf16_sus"] if tc_ms else None
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         xs = x_host[:1]
         done, px, dt, threads = oracle_units(w, blob, xs, seconds_budget=15.0)
         res["cpu_baseline"] = {"value": px / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
                                "sample": f"{done} (sample, tile) units of {w.name} sample 0 in {dt:.1f} s "
-                                         f"(fp64 numpy oracle, as it stands)"}
+                                         f"(fp64 numpy oracle, as it stands)",
+                               "cores_note": "threads of the BLAS pool the oracle's matmuls ran on", **host_cpu()}
     if rank == 0:
         print(json.dumps(res), flush=True)
 

@@ -27,6 +27,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
+
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -751,18 +753,9 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (C::STAGED && !make_tmap_bf16(&tmo, out, rows, D, D, 32, DH,
                                    DH == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
-  static bool attr = false;
-  static int sms = 0;
-  if (!attr) {
-    if (cudaFuncSetAttribute(attn_tc_kernel<DH, NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
-        cudaSuccess)
-      return false;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-    attr = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};
+  if (!smem_attr_once(reinterpret_cast<const void*>(attn_tc_kernel<DH, NQ>), C::SMEM, &attr_done)) return false;
+  const int sms = num_sms();
   const int64_t n_items = (int64_t)(ch.core_pairs ? ch.nqc : ch.nqp) * heads * B;
   if (n_items == 0) return true;
   if (n_items >= (int64_t)INT32_MAX) return false;

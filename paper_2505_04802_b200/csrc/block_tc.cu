@@ -1,7 +1,7 @@
 // block_tc.cu -- the second half of a pre-norm Reslim block on tcgen05 for
 // D = 256 (the 9.5M-class Reslim), fused into one persistent kernel:
 //     z'  = z + W_o . o + b_o                         (attention output o, R9)
-//     z'' = z' + W_2 . GELU(W_1 . LN2(z') + b_1) + b_2  (exact-erf GELU, LN eps 1e-5)
+//     z'' = z' + W_2 . GELU(W_1 . LN2(z') + b_1) + b_2  (tanh-form GELU, reading R28; LN eps 1e-5)
 //     xn  = LN1_{l+1}(z'')  (bf16, the next block's QKV input; not for the last block)
 // Per 128-token row block the residual row z' never leaves the SM: the
 // O-projection accumulates in TMEM, the epilogue warps add b_o and z (streamed
@@ -32,6 +32,8 @@
 
 #include <algorithm>
 #include <cstring>
+
+#include <atomic>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -553,15 +555,9 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
   if (!make_tmap_bf16(&t2, w2, DM, FH, FH, 128, 64, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   // residual stream z fp32 [M][256]: 128 x 32 boxes (loads zero-fill and stores clip past M)
   if (!make_tmap_f32(&tz, z, M, DM, DM, BM, ZC, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(block_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
-      return false;
-    attr = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<uint64_t> attr_done{0};
+  if (!smem_attr_once(reinterpret_cast<const void*>(block_tc_kernel), SMEM, &attr_done)) return false;
+  const int sms = num_sms();
   const int64_t tiles = row_blocks != nullptr ? (int64_t)n_row_blocks : (M + BM - 1) / BM;
   if (tiles == 0) return true;
   const int grid = (int)std::min<int64_t>(tiles, sms);

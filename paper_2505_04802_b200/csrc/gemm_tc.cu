@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "kernels.h"
@@ -70,6 +71,38 @@ bool make_tmap_f32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+// ---------------------------------------------------------------------------
+// Per-device launch state (a process may drive several devices: attributes and
+// SM counts are per device, cached by device ordinal)
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sms[kMaxDev];
+std::mutex g_attr_mu;
+}  // namespace
+
+int num_sms() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return 148;
+  int n = g_sms[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    g_sms[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
+
+bool smem_attr_once(const void* func, int bytes, std::atomic<uint64_t>* done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return false;
+  const uint64_t bit = 1ull << dev;
+  if (done->load(std::memory_order_acquire) & bit) return true;
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) != cudaSuccess) return false;
+  done->fetch_or(bit, std::memory_order_release);
+  return true;
 }
 
 namespace {
@@ -516,17 +549,6 @@ __global__ void __launch_bounds__(384, 1)
   }
 }
 
-int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
 template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false, bool WS = false>
 bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                  cudaStream_t st) {
@@ -554,11 +576,8 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
   static_assert(smem <= 227 * 1024, "shared memory");
   if (WS && K != 256) return false;
   auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS, WS>;
-  static bool attr_set = false;   // per instantiation
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-    attr_set = true;
-  }
+  static std::atomic<uint64_t> attr_done{0};   // per instantiation, per device
+  if (!smem_attr_once(reinterpret_cast<const void*>(kern), smem, &attr_done)) return false;
   const int64_t num_n = (Nk + BN - 1) / BN;
   const int64_t tiles = ((Mk + BM - 1) / BM) * num_n;
   int grid = (int)std::min<int64_t>(tiles, num_sms());

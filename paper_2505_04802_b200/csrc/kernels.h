@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 
 #include "orbit2_internal.h"
@@ -100,5 +101,10 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
 
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();
+
+// Per-device launch state: SM count of the current device, and the dynamic
+// shared-memory attribute of `func` set once per device (bit d of *done).
+int num_sms();
+bool smem_attr_once(const void* func, int bytes, std::atomic<uint64_t>* done);
 
 }  // namespace orbit2

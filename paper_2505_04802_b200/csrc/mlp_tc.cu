@@ -28,6 +28,8 @@
 
 #include <algorithm>
 
+#include <atomic>
+
 #include "kernels.h"
 #include "tc_common.cuh"
 
@@ -332,15 +334,9 @@ bool launch_mlp_fused(const void* xn, int64_t rows_alloc, const void* w1, const 
   // residual stream z fp32 [M][256]: 128 x 16 reduce boxes (rows past M are clipped)
   if (!make_tmap_f32(&tz, z, M, DM, DM, BM, ZC, ZC == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
-      return false;
-    attr = true;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<uint64_t> attr_done{0};
+  if (!smem_attr_once(reinterpret_cast<const void*>(mlp_tc_kernel), SMEM, &attr_done)) return false;
+  const int sms = num_sms();
   const int64_t tiles = (M + BM - 1) / BM;
   const int grid = (int)std::min<int64_t>(tiles, sms);
   mlp_tc_kernel<<<grid, THREADS, SMEM, st>>>(tx, t1, t2, tz, b1, b2, M, g_mlp_timeline);

@@ -45,9 +45,6 @@ struct Ctx {
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
   bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
-  // last block's block tail: the 128-row blocks holding core tokens, per chunk
-  // (uploaded into the workspace when the chunk changes)
-  int32_t rblk_tb = -1, rblk_tc = -1, rblk_n = 0;
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -219,6 +216,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
     e = cudaMemcpy(c->at<void>(p.lay.qpair_tile), p.qpair_tile.data(), p.qpair_tile.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qpair_core.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qpair_core), p.qpair_core.data(), p.qpair_core.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.core_rblk.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.core_rblk), p.core_rblk.data(), p.core_rblk.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.core_row.empty())
     e = cudaMemcpy(c->at<void>(p.lay.core_row), p.core_row.data(), p.core_row.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
@@ -423,33 +422,12 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
         const float* b1n = nxt ? wf(w.layers[l + 1].ln1_b) : nullptr;
         const int32_t* rblk = nullptr;
         int32_t nrblk = 0;
-        // last block: only row blocks holding core tokens (R16); the list is built once per
-        // context, so only when a call covers every rank-local tile (unchunked)
-        if (!nxt && !c->all_queries_last && tile_begin == 0 && tile_count == p.info.n_local_tiles) {
-          if (c->rblk_tb != tile_begin || c->rblk_tc != tile_count) {
-            std::vector<uint8_t> need((size_t)((M + kQBlock - 1) / kQBlock), 0);
-            for (int b = 0; b < B; ++b)
-              for (int32_t t = ch.tb; t < ch.tb + ch.tc; ++t) {
-                const DevTile& dt = p.dev[t];
-                const int64_t base = (int64_t)b * ch.chunk_tokens + (dt.tok_off - ch.tok0);
-                const int64_t cf0 = (dt.core_y0 - dt.pad_y0) * (int64_t)dt.pad_w + (dt.core_x0 - dt.pad_x0);
-                const int64_t cl0 = (dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * (int64_t)dt.pad_w +
-                                    (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
-                for (int64_t k = (base + cf0) / kQBlock; k <= (base + cl0) / kQBlock; ++k) need[(size_t)k] = 1;
-              }
-            std::vector<int32_t> list;
-            for (size_t k = 0; k < need.size(); ++k)
-              if (need[k]) list.push_back((int32_t)k);
-            cudaError_t e = cudaMemcpyAsync(c->at<void>(ly.core_rblk), list.data(), list.size() * 4,
-                                            cudaMemcpyHostToDevice, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // `list` is a host temporary
-            if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("row-block list: ") + cudaGetErrorString(e));
-            c->rblk_tb = tile_begin;
-            c->rblk_tc = tile_count;
-            c->rblk_n = (int32_t)list.size();
-          }
+        // last block: only row blocks holding core tokens (R16); the list is built by the
+        // planner for a call over every rank-local tile and uploaded by orbit2_create
+        if (!nxt && !c->all_queries_last && tile_begin == 0 && tile_count == p.info.n_local_tiles &&
+            !p.core_rblk.empty()) {
           rblk = c->at<int32_t>(ly.core_rblk);
-          nrblk = c->rblk_n;
+          nrblk = (int32_t)p.core_rblk.size();
         }
         ORBIT2_TRY(run(c, "block_tail", st, [&] {
           return launch_block_tail(ao, mrow, W8 + L.w_o, wf(L.b_o), wf(L.ln2_g), wf(L.ln2_b), W8 + L.w_1,

@@ -76,6 +76,9 @@ struct Plan {
   std::vector<int32_t> qpair_core;
   std::vector<int32_t> qpc_off;         // per local tile (+ sentinel): first qpair_core entry
   std::vector<int32_t> core_row;        // local core token -> local padded token index
+  // last block (R16) of a call over every rank-local tile (all B samples): the
+  // 128-row blocks of the packed token rows that hold core tokens (block tail)
+  std::vector<int32_t> core_rblk;
   orbit2_plan_info info;
   Layout lay;
   int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_core_h;

@@ -172,6 +172,11 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       const int32_t c_last = (dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w + (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
       p.qpc_off.push_back((int32_t)p.qpair_core.size());
       const int32_t b0 = c_first / kQBlock, b1 = c_last / kQBlock;   // query blocks with core tokens
+      if (li >= 32768 || b1 >= 32768) {   // entry packing: tile index < 2^15, first block < 2^15
+        if (msg) *msg = "tiles: more than 32767 tiles per rank or 32767 query blocks per tile (tile index / "
+                        "block packing of the last-block query list)";
+        return ORBIT2_E_UNSUPPORTED;
+      }
       for (int32_t b = b0; b <= b1; b += 2)                           // entry: tile, first block, count - 1
         p.qpair_core.push_back((li << 16) | (b << 1) | (b + 1 <= b1 ? 1 : 0));
     }
@@ -241,6 +246,23 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
         xl.elems = e;
         p.xfer.push_back(xl);
       }
+
+  // ---- last block: row blocks holding core tokens, unchunked call over all local tiles ----
+  {
+    const int64_t rows = (int64_t)c.batch * ltok;
+    std::vector<uint8_t> need((size_t)((rows + kQBlock - 1) / kQBlock), 0);
+    for (int b = 0; b < c.batch; ++b)
+      for (size_t li = 0; li + 1 < p.dev.size(); ++li) {
+        const DevTile& dt = p.dev[li];
+        const int64_t base = (int64_t)b * ltok + dt.tok_off;
+        const int64_t cf0 = (int64_t)(dt.core_y0 - dt.pad_y0) * dt.pad_w + (dt.core_x0 - dt.pad_x0);
+        const int64_t cl0 = (int64_t)(dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w +
+                            (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
+        for (int64_t k = (base + cf0) / kQBlock; k <= (base + cl0) / kQBlock; ++k) need[(size_t)k] = 1;
+      }
+    for (size_t k = 0; k < need.size(); ++k)
+      if (need[k]) p.core_rblk.push_back((int32_t)k);
+  }
 
   // ---- info ----
   orbit2_plan_info& in = p.info;

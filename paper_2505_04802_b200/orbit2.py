@@ -175,6 +175,25 @@ def _stream(stream) -> int:
     return stream.cuda_stream
 
 
+class _on_device:
+    """Run a library call with the ctx's device current (kernel attributes, SM
+    counts and launches are per device)."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    def __enter__(self):
+        import torch
+        self.prev = torch.cuda.current_device()
+        if self.prev != self.dev.index:
+            torch.cuda.set_device(self.dev)
+
+    def __exit__(self, *a):
+        import torch
+        if self.prev != self.dev.index:
+            torch.cuda.set_device(self.prev)
+
+
 class Context:
     """One orbit2 ctx bound to a torch-allocated workspace on the current device."""
 
@@ -206,8 +225,9 @@ class Context:
         assert canonical_dev.dtype == torch.float32 and canonical_dev.is_cuda
         assert canonical_dev.numel() == self.info.canonical_weight_count, "canonical blob size"
         packed = torch.empty(self.info.packed_weight_bytes, dtype=torch.uint8, device=self.device)
-        _check(lib.orbit2_prepare_weights(self.handle, _ptr(canonical_dev), _ptr(packed), _stream(stream)),
-               "orbit2_prepare_weights")
+        with _on_device(self.device):
+            _check(lib.orbit2_prepare_weights(self.handle, _ptr(canonical_dev), _ptr(packed), _stream(stream)),
+                   "orbit2_prepare_weights")
         return packed
 
     def tile_out_buffer(self, tile_count=None):
@@ -222,16 +242,18 @@ class Context:
         import torch
         _req(x_dev, torch.float32, "x_dev")
         _req(tile_out, torch.bfloat16 if self.bf16 else torch.float32, "tile_out")
-        _check(lib.orbit2_reslim_forward(self.handle, _ptr(packed), _ptr(x_dev), tile_begin, tile_count,
-                                         _ptr(tile_out), _stream(stream)), "orbit2_reslim_forward")
+        with _on_device(self.device):
+            _check(lib.orbit2_reslim_forward(self.handle, _ptr(packed), _ptr(x_dev), tile_begin, tile_count,
+                                             _ptr(tile_out), _stream(stream)), "orbit2_reslim_forward")
 
     def orbit2_stitch(self, tile_out, x_dev, tile_begin, tile_count, out, stream=None):
         import torch
         _req(x_dev, torch.float32, "x_dev")
         _req(out, torch.float32, "out")
         _req(tile_out, torch.bfloat16 if self.bf16 else torch.float32, "tile_out")
-        _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
-                                 _stream(stream)), "orbit2_stitch")
+        with _on_device(self.device):
+            _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
+                                     _stream(stream)), "orbit2_stitch")
 
     # -- multi-rank (TILES sequence parallelism) ------------------------------
     def orbit2_xfer_pack(self, kind, peer, x_dev, buf, stream=None):
@@ -258,6 +280,8 @@ class Context:
         tile_out (chunked calls write consecutive slices: needs B == 1 when
         chunk_tiles < n_local_tiles)."""
         n, ch = self.info.n_local_tiles, self.info.chunk_tiles
+        if n == 0:                      # a rank that owns no tiles (world_size > n_tiles)
+            return tile_out
         if ch < n and self.cfg.batch != 1:
             raise ValueError("rank-wide tile_out with chunked calls needs batch == 1")
         nh = tile_out.shape[1]
@@ -289,7 +313,7 @@ class Context:
         if tile_out is None:
             tile_out = self.tile_out_buffer()
         n, ch = self.info.n_local_tiles, self.info.chunk_tiles
-        for tb in range(0, n, ch):
+        for tb in range(0, n, max(ch, 1)):      # no iterations for a rank without tiles
             tc = min(ch, n - tb)
             self.orbit2_reslim_forward(packed, x_dev, tb, tc, tile_out, stream)
             self.orbit2_stitch(tile_out, x_dev, tb, tc, out, stream)

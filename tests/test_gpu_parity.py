@@ -44,7 +44,7 @@ def test_parity_small(name, over, precision, tol):
     print(f"{name} {over} prec={precision}: rel_err={e:.3e} vit_branch={ev:.3e}")
     assert np.isfinite(got).all()
     assert e <= tol
-    assert ev <= 2.5 * tol
+    assert ev <= tol
 
 
 @pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
@@ -56,48 +56,96 @@ def test_parity_C2_full_sample(precision, tol):
     got = run_cuda(w, x, blob, precision)
     e, ev = rel_err(got, ref), rel_err(got - up, ref_vit)
     print(f"C2 prec={precision}: rel_err={e:.3e} vit_branch={ev:.3e}")
-    assert e <= tol and ev <= 2.5 * tol
+    assert e <= tol and ev <= tol
 
 
-@pytest.mark.parametrize("name", ["C3", "C4"])
-def test_parity_sampled_tiles_bf16(name):
-    """C3 / C4 at full size: the oracle computes sampled tiles (corner, edge,
-    interior) exactly (tiles are independent, invariant I5)."""
-    w, x, blob = _case(name, batch=1)
-    got = run_cuda(w, x, blob, BF16)[0]
+# ---------------------------------------------------------------- full-size configs, sampled tiles
+# C3 / C4 / C5 at their full sizes: the oracle computes 1 corner, 1 edge and 2
+# interior tiles (SURVEY §8(c) parity gates; exact because tiles are independent,
+# invariant I5, and pinned on CPU by test_sampled_tiles_equal_full_forward_restricted).
+# Oracle results are cached per (config, sample, tile) so the bf16 and fp32 tests
+# share them.
+BENCH_BATCH = {"C3": 16, "C4": 1, "C5": 1}      # bench.py's batch per config
+_CASES, _ORACLE = {}, {}
+
+
+def _big_case(name):
+    if name not in _CASES:
+        w = get_config(name, batch=BENCH_BATCH[name])
+        _CASES.clear()                              # C5's input is 5.4 GB: keep one config at a time
+        _CASES[name] = (w, make_input(w), make_weights(w))
+    return _CASES[name]
+
+
+def _oracle_blocks(name, w, x, blob, b, ids):
     pr = O.Problem.from_config(w)
-    ids = sampled_tiles(w) if name == "C3" else [0, w.tiles_x * (w.tiles_y // 2) + w.tiles_x // 2]
-    res = O.tiles_forward_sampled(x[0], blob, pr, ids)
-    for t, (ys, xs, ref_blk, vit_blk) in res.items():
-        e = rel_err(got[:, ys, xs], ref_blk)
-        print(f"{name} tile {t}: rel_err={e:.3e}")
-        assert e <= BF16_TOL
+    need = [t for t in ids if (name, b, t) not in _ORACLE]
+    if need:
+        for t, v in O.tiles_forward_sampled(x[b], blob, pr, need).items():
+            _ORACLE[(name, b, t)] = v
+    return {t: _ORACLE[(name, b, t)] for t in ids}
 
 
-def test_parity_C5_chunked_sampled_tiles():
-    """C5 hyper-resolution (5400 x 10800 x 23 -> 21600 x 43200 x 18, 1296 tiles
-    of ~13k tokens) on one GPU, processed in chunks of 162 tiles (workspace
-    13.5 GB); an interior and a corner tile against the oracle.  Only the
-    sampled output blocks are copied back (the full field is 67 GB)."""
+def _check_blocks(label, got_of, ref, tol):
+    """got_of(ys, xs) -> [K, rows, cols] CUDA output block; ref = oracle blocks."""
+    for t, (ys, xs, ref_blk, vit_blk) in ref.items():
+        got = got_of(ys, xs)
+        e = rel_err(got, ref_blk)
+        ev = rel_err(got - (ref_blk - vit_blk), vit_blk)      # ViT branch: out - up (R21)
+        print(f"{label} tile {t}: rel_err={e:.3e} vit_branch={ev:.3e}")
+        assert np.isfinite(got).all()
+        assert e <= tol and ev <= tol
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_parity_sampled_tiles_bf16_bench_config(name):
+    """bf16 path at full size in the launch configuration bench.py times (C3: B = 16,
+    every tile in one call; C4: B = 1; C5: B = 1 in chunks of 162 tiles, 13.5 GB
+    workspace): 4 sampled tiles (corner, edge, 2 interior) of the first and last
+    sample against the fp64 oracle.  Only the sampled output blocks are copied back."""
     import torch
     from paper_2505_04802_b200 import orbit2 as o2
-    w = get_config("C5", batch=1)
-    x = make_input(w, batch=1)
-    blob = make_weights(w)
-    ctx = o2.Context(o2.config_from(w, precision=BF16, chunk_tiles=162))
+    w, x, blob = _big_case(name)
+    B = w.batch
+    ctx = o2.Context(o2.config_from(w, precision=BF16, chunk_tiles=162 if name == "C5" else 0))
     xd = torch.from_numpy(x).cuda()
     packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
-    out = torch.empty((1, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
+    out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
     ctx.forward(packed, xd, out=out)
     torch.cuda.synchronize()
-    pr = O.Problem.from_config(w)
-    ids = [w.tiles_x * (w.tiles_y // 2) + w.tiles_x // 2, 0]
-    res = O.tiles_forward_sampled(x[0], blob, pr, ids)
-    for t, (ys, xs, ref_blk, vit_blk) in res.items():
-        got = out[0, :, ys, xs].cpu().numpy()
-        e = rel_err(got, ref_blk)
-        print(f"C5 tile {t}: rel_err={e:.3e}")
-        assert e <= BF16_TOL
+    ids = sampled_tiles(w)
+    assert len(ids) == 4
+    for b in sorted({0, B - 1}):
+        ref = _oracle_blocks(name, w, x, blob, b, ids)
+        _check_blocks(f"{name} bf16 sample {b}", lambda ys, xs: out[b, :, ys, xs].cpu().numpy(), ref, BF16_TOL)
+    del out, xd, ctx
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_parity_sampled_tiles_fp32(name):
+    """fp32 path (<= 1e-4) at full size: only the 4 sampled tiles are run, one
+    orbit2_reslim_forward + orbit2_stitch call per tile (tile_begin = tile id at
+    world_size 1), sample 0."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    w, x, blob = _big_case(name)
+    w1 = w.replace(batch=1)
+    ctx = o2.Context(o2.config_from(w1, precision=FP32, chunk_tiles=1))
+    xd = torch.from_numpy(x[:1]).cuda()
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    out = torch.full((1, w.K, w.scale * w.H, w.scale * w.W), float("nan"), dtype=torch.float32, device="cuda")
+    tile_out = ctx.tile_out_buffer()
+    ids = sampled_tiles(w)
+    for t in ids:
+        assert ctx.tiles[t].local_index == t
+        ctx.orbit2_reslim_forward(packed, xd, t, 1, tile_out)
+        ctx.orbit2_stitch(tile_out, xd, t, 1, out)
+    torch.cuda.synchronize()
+    ref = _oracle_blocks(name, w, x, blob, 0, ids)
+    _check_blocks(f"{name} fp32", lambda ys, xs: out[0, :, ys, xs].cpu().numpy(), ref, FP32_TOL)
+    del out, xd, ctx
+    torch.cuda.empty_cache()
 
 
 def test_persistent_multi_item_batch():
@@ -136,6 +184,7 @@ def test_rank_emulation_bit_exact():
     separately, assemble a bit-identical field (R = 2, 3)."""
     w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
     a = run_cuda(w, x, blob, BF16)
+    assert rel_err(a, oracle_full(w, x, blob)[0]) <= BF16_TOL
     for R in (2, 3):
         assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=R))
 

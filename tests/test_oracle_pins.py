@@ -459,3 +459,78 @@ def test_golden_paper_sequence_lengths():
         assert abs(exact - printed * unit) < scale, (r, exact)
         assert round(exact / scale) * scale == printed * unit or \
             int(exact // scale) * scale == printed * unit, (r, exact)
+
+
+# ---------------------------------------------------------------- sampled-tile oracle
+@pytest.mark.parametrize("mode", [O.HALO_CLAMP, O.HALO_REPLICATE])
+def test_sampled_tiles_equal_full_forward_restricted(mode):
+    """tiles_forward_sampled (which supplies every C3/C4/C5 expected value) is
+    tiles_forward restricted to the tile's core output rectangle, bit for bit,
+    for EVERY tile of a 3 x 3 problem (the core outputs of a tile are
+    stitched into exactly its core rectangle; the residual is the same O7
+    formula evaluated on that rectangle).  A wrong core slice, reshape or
+    bilinear window in the sampled path fails here."""
+    pr = small_problem(H=36, W=44, tiles_y=3, tiles_x=3, halo=2, halo_mode=mode, channel_map=(2, 0))
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg, batch=2)
+    full, full_vit, _ = O.tiles_forward(x, blob, pr, return_parts=True)
+    tiles = pr.tiles()
+    covered = np.zeros(full.shape[1:], bool)
+    for b in range(2):
+        res = O.tiles_forward_sampled(x[b], blob, pr, range(len(tiles)))
+        assert sorted(res) == list(range(len(tiles)))
+        for t, (ys, xs, blk, vit) in res.items():
+            tile = tiles[t]
+            assert (ys.start, ys.stop) == (tile.core_y0 * pr.P, tile.core_y1 * pr.P)
+            assert (xs.start, xs.stop) == (tile.core_x0 * pr.P, tile.core_x1 * pr.P)
+            assert np.array_equal(blk, full[b][:, ys, xs])
+            assert np.array_equal(vit, full_vit[b][:, ys, xs])
+            if b == 0:
+                assert not covered[:, ys, xs].any()
+                covered[:, ys, xs] = True
+    assert covered.all()
+
+
+# ---------------------------------------------------------------- canonical weight blob
+def test_unpack_weights_marker_blob():
+    """The oracle's blob walk against the layout include/orbit2.h documents
+    (orbit2_prepare_weights comment), with closed-form offsets: value i at
+    canonical offset i, so every named array must hold exactly the offsets
+    the header assigns it.  W_e[D][V*p*p], b_e, e_s; per layer l at
+    base_l = Din*D + 2D + l*(12D^2 + 13D): ln1_g, ln1_b, W_qkv[3D][D], b_qkv[3D],
+    W_o[D][D], b_o, ln2_g, ln2_b, W_1[4D][D], b_1[4D], W_2[D][4D], b_2; then
+    lnf_g, lnf_b, W_h[K P^2][D], b_h[K P^2]; total Din*D + 2D + L(12D^2+13D) +
+    2D + D*K*P^2 + K*P^2."""
+    D, L, Din, Nh = 8, 3, 12, 5
+    total = Din * D + 2 * D + L * (12 * D * D + 13 * D) + 2 * D + D * Nh + Nh
+    blob = np.arange(total, dtype=np.float64)
+    Wt = O.unpack_weights(blob, D, L, Din, Nh)
+
+    def rng(off, *shape):
+        return off + np.arange(int(np.prod(shape)), dtype=np.float64).reshape(shape)
+
+    assert np.array_equal(Wt["W_e"], rng(0, D, Din))
+    assert Wt["W_e"][3, 7] == 3 * Din + 7          # row = output feature, column (v p + dy) p + dx
+    assert np.array_equal(Wt["b_e"], rng(Din * D, D))
+    assert np.array_equal(Wt["e_s"], rng(Din * D + D, D))
+    for l in range(L):
+        base = Din * D + 2 * D + l * (12 * D * D + 13 * D)
+        Lw = Wt["layers"][l]
+        want = {"ln1_g": rng(base, D), "ln1_b": rng(base + D, D),
+                "W_qkv": rng(base + 2 * D, 3 * D, D), "b_qkv": rng(base + 2 * D + 3 * D * D, 3 * D),
+                "W_o": rng(base + 5 * D + 3 * D * D, D, D), "b_o": rng(base + 5 * D + 4 * D * D, D),
+                "ln2_g": rng(base + 6 * D + 4 * D * D, D), "ln2_b": rng(base + 7 * D + 4 * D * D, D),
+                "W_1": rng(base + 8 * D + 4 * D * D, 4 * D, D), "b_1": rng(base + 8 * D + 8 * D * D, 4 * D),
+                "W_2": rng(base + 12 * D + 8 * D * D, D, 4 * D), "b_2": rng(base + 12 * D + 12 * D * D, D)}
+        assert sorted(Lw) == sorted(want)
+        for k, v in want.items():
+            assert np.array_equal(Lw[k], v), (l, k)
+        # rows Q | K | V, head h = rows [h d, (h+1) d) of each: K row 0 of layer l
+        assert Lw["W_qkv"][D, 0] == base + 2 * D + D * D
+    tail = Din * D + 2 * D + L * (12 * D * D + 13 * D)
+    assert np.array_equal(Wt["lnf_g"], rng(tail, D))
+    assert np.array_equal(Wt["lnf_b"], rng(tail + D, D))
+    assert np.array_equal(Wt["W_h"], rng(tail + 2 * D, Nh, D))
+    assert np.array_equal(Wt["b_h"], rng(tail + 2 * D + Nh * D, Nh))
+    with pytest.raises(ValueError):
+        O.unpack_weights(np.zeros(total + 1), D, L, Din, Nh)

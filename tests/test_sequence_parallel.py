@@ -217,3 +217,8 @@ def test_gpu_rank_emulation_halo_exchange_bit_exact(o2, R):
         root.orbit2_stitch_peer(s, touts[s], xs[0], out)
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+    # and against the fp64 oracle itself (P:527-532 TILES definition), not only R = 1
+    from oracle import reslim_tiles as O
+    from tests.gpu_helpers import BF16_TOL, rel_err
+    want = O.tiles_forward(full.cpu().numpy(), blob.cpu().numpy(), O.Problem.from_config(w))
+    assert rel_err(out.cpu().numpy(), want) <= BF16_TOL
