@@ -6,10 +6,12 @@
 One step = one pass of the whole hot path (gather -> embed -> L blocks ->
 head -> stitch + bilinear residual) over one batch of synthetic ERA5-shaped
 input (BASELINE.json configs[1] = C2 at N=1, B = 64 samples).  Multi-GPU
-(torchrun, one process per GPU): every rank runs its own batch of the same
-workload (weak scaling; units = (sample, tile) pairs sharded by sample, no
-data-path collective).  Timing: CUDA events on the
-launching stream, barrier + synchronize on both sides, max over ranks.
+(one process per GPU; `--gpus N` re-executes itself under torch.distributed.run
+when WORLD_SIZE is unset): the SAME batch's tiles are partitioned over the N
+GPUs (LPT), the halo exchange and the output gather run through NVLink peer
+memory inside the library (strong scaling); `--mode dp`
+instead gives every rank its own batch (weak scaling).  Timing: CUDA events on
+the launching stream, barrier + synchronize on both sides, max over ranks.
 
 Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement for every key.
 """
@@ -40,9 +42,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
     ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="dp", choices=["dp", "sp"],
-                    help="dp: every rank its own batch (weak scaling); sp: the tiles of one batch spread "
-                         "over the ranks with NCCL halo exchange + output gather (strong scaling)")
+    ap.add_argument("--mode", default="sp", choices=["dp", "sp"],
+                    help="N > 1 only.  sp (default): the tiles of one batch spread over the ranks, halo "
+                         "exchange + output gather through NVLink peer memory (strong scaling); dp: every "
+                         "rank its own batch (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--set", action="append", default=[], metavar="FIELD=INT",
@@ -506,55 +509,93 @@ def run_ours(args, w, world, rank, local):
 
 
 def run_sp(args, w, world, rank, local):
-    """TILES sequence parallelism: one batch, its tiles LPT-spread over the ranks.
-    Timed step = halo exchange (NCCL) + forward of the rank's tiles + output
-    gather (NCCL) + stitch of every tile on rank 0; inputs start as each
-    rank's owned core pixels (resident in HBM)."""
+    """TILES sequence parallelism (strong scaling): ONE batch, its tiles LPT-spread
+    over the N ranks; the library moves the data through NVLink peer memory
+    (sequence_parallel.PeerSP): halo push + barrier, forward chunks, stitch of each
+    chunk straight into rank 0's output field (side stream, overlapping the next
+    chunk), end barrier.  Every rank's input field holds only its owned core pixels
+    (plus what peers push)."""
     import torch
     import torch.distributed as dist
-    from paper_2505_04802_b200 import orbit2 as o2, sequence_parallel as sp
+    from paper_2505_04802_b200 import orbit2 as o2
+    from paper_2505_04802_b200.sequence_parallel import PeerSP
     from workloads import make_input, make_weights
     B = w.batch
-    cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world, rank=rank)
+    _, info0 = o2.orbit2_tiles_plan(o2.config_from(w, batch=B, world_size=world, rank=rank))
+    n_local = info0.n_local_tiles
+    chunk = args.chunk if args.chunk > 0 else max(1, -(-n_local // 4))   # <= 4 chunks: stitch overlaps compute
+    cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world, rank=rank, chunk_tiles=chunk)
     ctx = o2.Context(cfg)
     info = ctx.info
-    full = torch.from_numpy(make_input(w, batch=B)).cuda()
-    packed = ctx.prepare_weights(torch.from_numpy(make_weights(w)).cuda())
-    x0 = torch.zeros_like(full)
-    if world > 1:
-        cores, _ = o2.orbit2_xfer_plan(cfg, o2.XFER_CORES, (rank + 1) % world, o2.SEND)
-        for y0, y1, xa, xb in cores:
-            x0[:, :, y0:y1, xa:xb] = full[:, :, y0:y1, xa:xb]
-    else:
-        x0.copy_(full)
+    blob = make_weights(w)
+    x_host = make_input(w, batch=B)
+    x_pin = torch.from_numpy(x_host).pin_memory()
+    full = x_pin.to("cuda")
+    x = torch.full_like(full, float("nan"))
+    for t in ctx.tiles:                                   # owned core pixels only
+        if t.owner_rank == rank:
+            sl = (slice(None), slice(None), slice(t.core_y0 * w.patch, t.core_y1 * w.patch),
+                  slice(t.core_x0 * w.patch, t.core_x1 * w.patch))
+            x[sl] = full[sl]
     del full
-    out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), device="cuda") if rank == 0 else None
-    x = x0.clone()
-    dd = dist if world > 1 else None
-
-    def step():
-        x.copy_(x0)   # reset to owned pixels (the halo exchange refills the rest)
-        if world > 1:
-            sp.forward_sequence_parallel(ctx, packed, x, out, dd)
-        else:
-            ctx.forward(packed, x, out=out)
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda") \
+        if rank == 0 else None
+    sp = PeerSP(ctx, x, out, dist, gather_root=0)
+    stream = torch.cuda.current_stream()
 
     for _ in range(max(3, args.warmup)):
-        step()
+        sp.step(packed, stream)
     barrier(world)
-    times = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launch_count()
     with ClockSampler(local) as clk:
+        barrier(world)
+        ev0.record(stream)
         for _ in range(args.steps):
-            barrier(world)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            step()
-            e1.record()
-            barrier(world)
-            times.append(max_over_ranks(world, e0.elapsed_time(e1)))
+            sp.step(packed, stream)
+        ev1.record(stream)
+        barrier(world)
+    ms = max_over_ranks(world, ev0.elapsed_time(ev1) / args.steps)
     launches = (ctx.launch_count() - l0) // args.steps
-    ms = statistics.median(times)
+    clocks = clk.summary()
+    ctx.comm_status()
+
+    # ---- end to end: pinned host input -> every rank (H2D of the field), SP step,
+    # root -> pinned host output (D2H); an extra device barrier keeps the next step's
+    # stitches out of the root's field until its D2H has read it ----
+    out_pin = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() if rank == 0 else None
+
+    def e2e_step():
+        x.copy_(x_pin, non_blocking=True)
+        sp.step(packed, stream)
+        if rank == 0:
+            out_pin.copy_(out, non_blocking=True)
+        ctx.comm_barrier(stream)
+
+    e2e_step()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(2, args.steps // 2)
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier(world)
+    e2e_ms = max_over_ranks(world, e0.elapsed_time(e1) / e_steps)
+    ctx.comm_status()
+
+    # ---- per-kernel-class times of this rank (profiled pass, events per launch) ----
+    prof = {}
+    if not args.no_profile:
+        ctx.set_profiling(True)
+        for _ in range(3):
+            sp.step(packed, stream)
+        torch.cuda.synchronize()
+        prof = {k: (n / 3, t / 3) for k, (n, t) in ctx.kernel_times().items()}
+        ctx.set_profiling(False)
+    allprof = [None] * world
+    dist.all_gather_object(allprof, prof)
     px = B * w.scale * w.H * w.scale * w.W
     if rank == 0:
         pk = peaks()
@@ -562,15 +603,43 @@ def run_sp(args, w, world, rank, local):
             "metric": METRIC, "value": px / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields, random-init weights)",
-            "config": {"workload": w.name, "batch": B, "parallelism": f"tiles-sp{world} (LPT tiles, NCCL halo "
-                       "exchange + tile_out gather, stitch on rank 0)", "step_copy": "x reset from owned pixels (HBM copy)"},
+            "config": {"workload": w.name, "batch": B, "coarse": [w.H, w.W, w.V], "out": [w.scale * w.H,
+                       w.scale * w.W, w.K], "tiles": [w.tiles_y, w.tiles_x], "halo": w.halo,
+                       "vit": [w.embed, w.depth, w.heads],
+                       "parallelism": f"tiles-sp{world} (LPT tile partition; halo push + output gather through "
+                                      "NVLink peer memory, stitch fused with the gather)",
+                       "chunk_tiles": info.chunk_tiles, "gather_root": 0,
+                       "l2": "working set > L2 (126 MB) every step; no flush needed"},
+            "tokens_per_s": B * info.tokens_per_sample / (ms * 1e-3),
+            "core_tokens_per_s": B * info.core_tokens_per_sample / (ms * 1e-3),
             "path_tflops": B * info.flops_per_sample / (ms * 1e-3) / 1e12,
-            "gpu_launches_rank0": int(launches),
-            "clocks": clk.summary(),
-            "e2e": None,
-            "note": "strong-scaling mode (one batch over N GPUs); median of per-step max-over-ranks event times",
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": {"value": px / (e2e_ms * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": world * x_pin.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
+                    "ms_per_step": e2e_ms,
+                    "api": "PeerSP.step with the input field copied from pinned host on every rank and the "
+                           "gathered field copied to pinned host on rank 0"},
+            "per_rank_kernels": [{k: {"launches": round(n, 2), "ms": round(t, 4)} for k, (n, t) in (pr or {}).items()}
+                                 for pr in allprof],
+            "note": "strong scaling: one batch over N GPUs; CUDA-event time of K back-to-back steps, max over ranks",
         }
         print(json.dumps(res), flush=True)
+
+
+def relaunch_if_needed(args):
+    """`python bench.py --gpus N` without torchrun: re-exec under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def main():
@@ -586,9 +655,10 @@ def main():
         rank = int(os.environ.get("RANK", "0"))
         run_reference(args, w, int(os.environ.get("WORLD_SIZE", "1")), rank)
         return
+    relaunch_if_needed(args)
     world, rank, local = dist_init(args.gpus)
     try:
-        if args.mode == "sp":
+        if world > 1 and args.mode == "sp":
             run_sp(args, w, world, rank, local)
         else:
             run_ours(args, w, world, rank, local)

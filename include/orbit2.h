@@ -52,7 +52,7 @@ typedef enum {
   ORBIT2_E_CAPACITY = -2,     /* caller buffer / workspace too small (info still filled) */
   ORBIT2_E_UNSUPPORTED = -3,  /* valid but not implemented (e.g. head_dim not in {32,64,128}) */
   ORBIT2_E_CUDA = -4,         /* CUDA runtime / launch error */
-  ORBIT2_E_NCCL = -5,         /* reserved (collectives are issued by the caller in ABI v1) */
+  ORBIT2_E_NCCL = -5,         /* reserved (inter-GPU data movement is peer memory, orbit2_comm_*) */
   ORBIT2_E_STATE = -6         /* call made on a ctx in the wrong state */
 } orbit2_status;
 
@@ -204,9 +204,14 @@ orbit2_status orbit2_stitch(void *ctx, const void *tile_out_dev, const float *in
  * contiguous fp32 buffer; the caller moves the buffers (e.g. NCCL send/recv
  * over NVLink).  Message layout: rectangle by rectangle, each [B][V][rows][cols].
  *
- *   ORBIT2_XFER_HALO : halo exchange.  send = pixels of `peer`'s padded tile
+ *   ORBIT2_XFER_HALO : halo exchange.  send = pixels of `peer`'s needed tile
  *                      rectangles that lie in this rank's owned cores; recv =
- *                      pixels of this rank's padded rectangles owned by `peer`.
+ *                      pixels of this rank's needed rectangles owned by `peer`.
+ *                      Needed rectangle of a tile = bounding box of its padded
+ *                      rectangle (pixels, clamped to the grid) and its core
+ *                      dilated by 1 pixel (the bilinear residual's support, so
+ *                      the owner can stitch its tiles; equal to the padded
+ *                      rectangle whenever halo >= 1).
  *   ORBIT2_XFER_CORES: input gather to a root.  send = this rank's owned core
  *                      pixels (peer = root); recv (at root) = `peer`'s owned cores.
  * Owned cores: the core rectangles (pixels) of the rank's tiles; they partition
@@ -239,6 +244,73 @@ orbit2_status orbit2_xfer_unpack(void *ctx, int32_t kind, int32_t peer, const fl
  * coarse pixel) into out_dev.  peer may equal cfg->rank. */
 orbit2_status orbit2_stitch_peer(void *ctx, int32_t peer, const void *tile_out_dev, const float *input_dev,
                                  float *out_dev, void *stream);
+
+/*
+ * ---- Peer-memory TILES sequence parallelism (one process per GPU of one
+ * NVLink/NVSwitch node; "assigning each tile to a separate GPU"
+ * halo, "stitched together").  The library moves the data itself with
+ * loads/stores through NVLink peer mappings (CUDA IPC); the caller only swaps
+ * the export handles between processes (e.g. torch.distributed all_gather).
+ *
+ * Per step, on every rank, in stream order:
+ *   orbit2_halo_exchange  -- push: the pixels of this rank's owned cores that
+ *                            lie in a peer's padded rectangles (plus the 1-pixel
+ *                            bilinear support of the peer's cores) are stored
+ *                            straight into that peer's input field; then a
+ *                            device-side barrier across all ranks.
+ *   orbit2_reslim_forward / orbit2_stitch with out_dev = the pointer
+ *                            orbit2_comm_target returns: the stitch kernel
+ *                            writes this rank's tiles into the gather root's
+ *                            output field through NVLink (output gather fused
+ *                            into step (4)), or into the local field when
+ *                            gather_root = -1 (sharded output).
+ *   orbit2_comm_barrier   -- device-side barrier: every rank's stores of this
+ *                            step (halo pushes, output tiles) are visible.
+ * Precondition of a halo exchange: every rank has passed the previous step's
+ * orbit2_comm_barrier (the push overwrites peers' non-owned pixels).
+ * Barriers spin on flags in the peers' workspaces with a 30 s timeout; a
+ * timeout is reported by orbit2_comm_status (never a hang, never a trap).
+ */
+typedef struct {
+  uint8_t handle[64];   /* cudaIpcMemHandle_t of the allocation holding the buffer */
+  int64_t offset;       /* byte offset of the buffer inside that allocation */
+  int64_t bytes;        /* allocation size (checked against the plan on open) */
+} orbit2_ipc_handle;
+
+/* Host-only: export a device buffer (from cudaMalloc or the torch caching
+ * allocator, not from a cudaMallocAsync pool) for the peers of this process. */
+orbit2_status orbit2_ipc_export(const void *dev_ptr, orbit2_ipc_handle *out);
+
+/* Collective in the host sense (every rank calls it once, same order):
+ * bind the ctx (world_size R, rank r) to
+ *   input_dev   this rank's input field [B][V][H][W] fp32 (its owned core pixels
+ *               valid before each halo exchange; peers' pushes fill the rest),
+ *   out_dev     this rank's output field [B][K][sH][sW] fp32: required on the
+ *               gather root and when gather_root = -1 (sharded), else may be NULL,
+ *   and every rank's workspace, input field and output field through the R
+ *   export handles of each array (entry r = this rank's own, not opened).
+ * out_handles may be NULL when gather_root = -1.  Opens the peers' allocations
+ * with cudaIpcOpenMemHandle (P2P over NVLink), uploads the push table and
+ * zeroes this rank's barrier flags (synchronous; call on every rank before any
+ * rank's first halo exchange).  E_STATE if called twice; E_CUDA if a handle
+ * cannot be opened; E_INVALID if a peer buffer is smaller than the plan needs. */
+orbit2_status orbit2_comm_init(void *ctx, int32_t gather_root, float *input_dev, float *out_dev,
+                               const orbit2_ipc_handle *workspace_handles, const orbit2_ipc_handle *input_handles,
+                               const orbit2_ipc_handle *out_handles);
+
+/* The output field this rank's orbit2_stitch calls write: the gather root's
+ * field mapped into this process, or out_dev of orbit2_comm_init on the root
+ * and when the output is sharded (gather_root = -1). */
+orbit2_status orbit2_comm_target(void *ctx, float **out_dev);
+
+/* Halo push of this step (all B samples, all V channels) + barrier slot 0. */
+orbit2_status orbit2_halo_exchange(void *ctx, void *stream);
+/* End-of-step barrier (slot 1): every rank's earlier stores are visible. */
+orbit2_status orbit2_comm_barrier(void *ctx, void *stream);
+
+/* Synchronises the device and reports a barrier timeout (E_STATE, the message
+ * names the missing rank) or a CUDA error; OK otherwise. */
+orbit2_status orbit2_comm_status(void *ctx);
 
 /* Number of kernels the library launched on this ctx so far. */
 int64_t orbit2_launch_count(void *ctx);

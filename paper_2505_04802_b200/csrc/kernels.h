@@ -73,6 +73,12 @@ void launch_attention_f32(const float* qkv, float* out, const ChunkDev& ch, int 
                           cudaStream_t st);
 void launch_xfer(const DevRect* rects, int count, int B, int V, int H, int W, const float* src, float* dst, int pack,
                  cudaStream_t st);
+// ---- peer-memory SP (comm.cu) ----
+void launch_push(const DevPush* tab, int count, int B, int V, int H, int W, const float* src, cudaStream_t st);
+void launch_barrier(uint64_t* const* sigtab, int R, int me, int slot, uint64_t epoch, uint32_t* err,
+                    cudaStream_t st);
+// base and size of the device allocation holding p (driver cuMemGetAddressRange)
+bool alloc_range(const void* p, void** base, size_t* bytes);
 void launch_pos_tables(float* pos_u, float* pos_w, int Hp, int Wp, int h, int D, cudaStream_t st);
 void launch_convert_rows(const float* src, void* dst, int64_t rows, int64_t cols, int64_t ld_dst, int to_bf16,
                          cudaStream_t st);

@@ -45,6 +45,13 @@ struct Ctx {
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
   bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
+  // peer-memory SP (orbit2_comm_*)
+  bool comm = false;
+  int32_t gather_root = 0;
+  float* own_input = nullptr;         // this rank's input field (the push source)
+  float* target = nullptr;            // where this rank's stitch writes (root's field or its own)
+  uint64_t epoch[2] = {0, 0};         // per barrier slot: 0 = after halo push, 1 = end of step
+  std::vector<void*> opened;          // peer allocations opened with cudaIpcOpenMemHandle
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -216,6 +223,7 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
     e = cudaMemcpy(c->at<void>(p.lay.qpair_tile), p.qpair_tile.data(), p.qpair_tile.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qpair_core.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qpair_core), p.qpair_core.data(), p.qpair_core.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(c->at<void>(p.lay.sig), 0, 2ULL * p.cfg.world_size * 8 + 64);
   if (e == cudaSuccess && !p.core_rblk.empty())
     e = cudaMemcpy(c->at<void>(p.lay.core_rblk), p.core_rblk.data(), p.core_rblk.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.core_row.empty())
@@ -247,6 +255,7 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
 void orbit2_destroy(void* ctx) {
   Ctx* c = reinterpret_cast<Ctx*>(ctx);
   if (!c) return;
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   for (auto& t : c->pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
@@ -626,6 +635,169 @@ orbit2_status orbit2_stitch(void* ctx, const void* tile_out_dev, const float* in
                            cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h, st);
     return true;
   });
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory TILES sequence parallelism (include/orbit2.h, orbit2_comm_*)
+// ---------------------------------------------------------------------------
+orbit2_status orbit2_ipc_export(const void* dev_ptr, orbit2_ipc_handle* out) {
+  if (!dev_ptr || !out) return set_err(ORBIT2_E_INVALID, "dev_ptr/out: null");
+  void* base = nullptr;
+  size_t bytes = 0;
+  if (!alloc_range(dev_ptr, &base, &bytes))
+    return set_err(ORBIT2_E_CUDA, "orbit2_ipc_export: cuMemGetAddressRange failed (not a device allocation?)");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, base);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  std::memcpy(out->handle, &h, 64);
+  out->offset = reinterpret_cast<const uint8_t*>(dev_ptr) - reinterpret_cast<const uint8_t*>(base);
+  out->bytes = (int64_t)bytes;
+  return ORBIT2_OK;
+}
+
+namespace {
+// Open a peer allocation once per distinct handle (two buffers of a peer may share
+// one allocation of its caching allocator) and return the mapped buffer pointer.
+orbit2_status open_peer(Ctx* c, std::vector<std::pair<orbit2_ipc_handle, void*>>* seen, const orbit2_ipc_handle& h,
+                        int64_t need, void** out) {
+  if (h.offset < 0 || need < 0 || h.offset + need > h.bytes)
+    return set_err(ORBIT2_E_INVALID, "orbit2_comm_init: a peer buffer is smaller than the plan needs");
+  void* base = nullptr;
+  for (auto& s : *seen)
+    if (std::memcmp(s.first.handle, h.handle, 64) == 0) base = s.second;
+  if (!base) {
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, h.handle, 64);
+    cudaError_t e = cudaIpcOpenMemHandle(&base, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return set_err(ORBIT2_E_CUDA, std::string("cudaIpcOpenMemHandle (peer-to-peer over NVLink): ") +
+                                        cudaGetErrorString(e));
+    c->opened.push_back(base);
+    seen->push_back({h, base});
+  }
+  *out = reinterpret_cast<uint8_t*>(base) + h.offset;
+  return ORBIT2_OK;
+}
+}  // namespace
+
+orbit2_status orbit2_comm_init(void* ctx, int32_t gather_root, float* input_dev, float* out_dev,
+                               const orbit2_ipc_handle* ws_h, const orbit2_ipc_handle* in_h,
+                               const orbit2_ipc_handle* out_h) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (c->comm) return set_err(ORBIT2_E_STATE, "orbit2_comm_init: already initialised");
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const int R = cf.world_size, me = cf.rank;
+  if (!ws_h || !in_h) return set_err(ORBIT2_E_INVALID, "workspace_handles/input_handles: null");
+  if (!input_dev || !aligned16(input_dev)) return set_err(ORBIT2_E_INVALID, "input_dev: null or not 16-byte aligned");
+  if (gather_root < -1 || gather_root >= R) return set_err(ORBIT2_E_INVALID, "gather_root: outside [-1, world_size)");
+  const bool own_out = gather_root < 0 || gather_root == me;
+  if (own_out && (!out_dev || !aligned16(out_dev)))
+    return set_err(ORBIT2_E_INVALID, "out_dev: null or not 16-byte aligned on the gather root / sharded output");
+  if (gather_root >= 0 && gather_root != me && !out_h)
+    return set_err(ORBIT2_E_INVALID, "out_handles: null with gather_root >= 0");
+  const int64_t in_bytes = (int64_t)cf.batch * cf.V * cf.H * cf.W * 4;
+  std::vector<std::pair<orbit2_ipc_handle, void*>> seen;
+  std::vector<uint64_t*> sig(R, nullptr);
+  std::vector<float*> inputs(R, nullptr);
+  for (int r = 0; r < R; ++r) {
+    if (r == me) {
+      sig[r] = c->at<uint64_t>(p.lay.sig);
+      inputs[r] = input_dev;
+      continue;
+    }
+    void* w = nullptr;
+    ORBIT2_TRY(open_peer(c, &seen, ws_h[r], p.lay.sig + 2LL * R * 8 + 64, &w));
+    sig[r] = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(w) + p.lay.sig);
+    void* x = nullptr;
+    ORBIT2_TRY(open_peer(c, &seen, in_h[r], in_bytes, &x));
+    inputs[r] = reinterpret_cast<float*>(x);
+  }
+  float* target = out_dev;
+  if (!own_out) {
+    void* o = nullptr;
+    ORBIT2_TRY(open_peer(c, &seen, out_h[gather_root], p.info.out_bytes, &o));
+    target = reinterpret_cast<float*>(o);
+  }
+  // push table: this rank's HALO SEND rectangles of every peer, with the peer's field
+  std::vector<DevPush> push;
+  for (int peer = 0; peer < R; ++peer) {
+    if (peer == me) continue;
+    const XferList& xl = p.xfer[((size_t)ORBIT2_XFER_HALO * R + peer) * 2 + ORBIT2_SEND];
+    for (int i = 0; i < xl.count; ++i) {
+      const DevRect& d = p.rects[(size_t)xl.start + i];
+      push.push_back(DevPush{d.y0, d.y1, d.x0, d.x1, inputs[peer], 0});
+    }
+  }
+  cudaError_t e = cudaSuccess;
+  if (!push.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.push), push.data(), push.size() * sizeof(DevPush), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(c->at<void>(p.lay.sigtab), sig.data(), R * 8, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemset(c->at<void>(p.lay.sig), 0, 2ULL * R * 8 + 64);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("orbit2_comm_init: ") + cudaGetErrorString(e));
+  c->gather_root = gather_root;
+  c->own_input = input_dev;
+  c->target = target;
+  c->epoch[0] = c->epoch[1] = 0;
+  c->comm = true;
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_comm_target(void* ctx, float** out_dev) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !out_dev) return set_err(ORBIT2_E_INVALID, "ctx/out_dev: null");
+  if (!c->comm) return set_err(ORBIT2_E_STATE, "orbit2_comm_target: orbit2_comm_init not called");
+  *out_dev = c->target;
+  return ORBIT2_OK;
+}
+
+static orbit2_status comm_barrier(Ctx* c, int slot, cudaStream_t st) {
+  const Plan& p = c->plan;
+  const uint64_t ep = ++c->epoch[slot];
+  return run(c, "comm_barrier", st, [&] {
+    launch_barrier(c->at<uint64_t*>(p.lay.sigtab), p.cfg.world_size, p.cfg.rank, slot, ep,
+                   reinterpret_cast<uint32_t*>(c->at<uint8_t>(p.lay.sig) + 2LL * p.cfg.world_size * 8), st);
+    return true;
+  });
+}
+
+orbit2_status orbit2_halo_exchange(void* ctx, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->comm) return set_err(ORBIT2_E_STATE, "orbit2_halo_exchange: orbit2_comm_init not called");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  if (p.n_push > 0)
+    ORBIT2_TRY(run(c, "halo_push", st, [&] {
+      launch_push(c->at<DevPush>(p.lay.push), p.n_push, cf.batch, cf.V, cf.H, cf.W, c->own_input, st);
+      return true;
+    }));
+  return comm_barrier(c, 0, st);
+}
+
+orbit2_status orbit2_comm_barrier(void* ctx, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->comm) return set_err(ORBIT2_E_STATE, "orbit2_comm_barrier: orbit2_comm_init not called");
+  return comm_barrier(c, 1, reinterpret_cast<cudaStream_t>(stream));
+}
+
+orbit2_status orbit2_comm_status(void* ctx) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->comm) return set_err(ORBIT2_E_STATE, "orbit2_comm_status: orbit2_comm_init not called");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("orbit2_comm_status: ") + cudaGetErrorString(e));
+  uint32_t err = 0;
+  e = cudaMemcpy(&err, c->at<uint8_t>(c->plan.lay.sig) + 2LL * c->plan.cfg.world_size * 8, 4, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("orbit2_comm_status: ") + cudaGetErrorString(e));
+  if (err != 0)
+    return set_err(ORBIT2_E_STATE, "orbit2 comm barrier timed out (30 s) waiting for rank " + std::to_string(err - 1));
+  return ORBIT2_OK;
 }
 
 }  // extern "C"

@@ -43,7 +43,8 @@ struct Chunk {
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
   int64_t tiles, qblk_tile, qpair_tile, qpair_core, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
-  int64_t core_rblk;          // last block: 128-row blocks holding core tokens (built per chunk)
+  int64_t core_rblk;          // last block: 128-row blocks holding core tokens (unchunked call)
+  int64_t sig, push, sigtab;  // peer-memory SP: barrier flags, push table, peers' flag pointers
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;
@@ -89,7 +90,16 @@ struct Plan {
   std::vector<int64_t> local_core_by_rank;
   std::vector<DevRect> rects;                      // all lists back to back
   std::vector<XferList> xfer;                      // index ((kind * R) + peer) * 2 + direction
+  int32_t n_push = 0;                              // HALO SEND rectangles over all peers
 };
+// One halo-push rectangle (coarse pixels) with the peer's input field it goes to.
+struct DevPush {
+  int32_t y0, y1, x0, x1;
+  float* dst;       // the peer's input field [B][V][H][W], mapped into this process
+  int64_t pad_;
+};
+static_assert(sizeof(DevPush) == 32, "DevPush layout");
+
 // rectangles of one transfer (host side, pure)
 void xfer_rects(const Plan& p, int kind, int rank, int peer, int direction, std::vector<orbit2_rect>* out);
 

@@ -345,6 +345,16 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     ly.peer_tiles = take(n * (int64_t)sizeof(DevTile));
   }
   ly.rects = take((int64_t)p.rects.size() * (int64_t)sizeof(DevRect));
+  // peer-memory SP (orbit2_comm_*): barrier flags [2][R] u64 + error word, the push
+  // table (one entry per HALO SEND rectangle of every peer) and the signal pointers
+  ly.sig = take(2LL * c.world_size * 8 + 64);
+  {
+    int64_t n = 0;
+    for (int peer = 0; peer < c.world_size; ++peer) n += p.xfer[((size_t)ORBIT2_XFER_HALO * c.world_size + peer) * 2 + ORBIT2_SEND].count;
+    ly.push = take(n * 32);
+    p.n_push = (int32_t)n;
+  }
+  ly.sigtab = take((int64_t)c.world_size * 8);
   ly.total = off;
   in.workspace_bytes = ly.total;
   in.tile_out_bytes = (int64_t)c.batch * in.max_chunk_core_tokens * p.Nh * E;
@@ -359,9 +369,13 @@ namespace {
 orbit2_rect core_px(const orbit2_tile& t, int p) {
   return {t.core_y0 * p, t.core_y1 * p, t.core_x0 * p, t.core_x1 * p};
 }
-orbit2_rect pad_px(const orbit2_tile& t, int p, int H, int W) {   // clamped to the grid (R4)
-  return {std::max(0, t.pad_y0 * p), std::min(H, t.pad_y1 * p), std::max(0, t.pad_x0 * p),
-          std::min(W, t.pad_x1 * p)};
+// The pixels a rank needs for one of its tiles: the padded rectangle the gather
+// reads (clamped to the grid, R4) and the 1-pixel support of the bilinear
+// residual around the core (O7: y1 = y0 + 1) that the stitch reads -- the
+// bounding box of both (they are nested: equal to the padded rect when h >= 1).
+orbit2_rect pad_px(const orbit2_tile& t, int p, int H, int W) {
+  return {std::max(0, std::min(t.pad_y0 * p, t.core_y0 * p - 1)), std::min(H, std::max(t.pad_y1 * p, t.core_y1 * p + 1)),
+          std::max(0, std::min(t.pad_x0 * p, t.core_x0 * p - 1)), std::min(W, std::max(t.pad_x1 * p, t.core_x1 * p + 1))};
 }
 bool intersect(const orbit2_rect& a, const orbit2_rect& b, orbit2_rect* o) {
   o->y0 = std::max(a.y0, b.y0); o->y1 = std::min(a.y1, b.y1);

@@ -50,6 +50,10 @@ class orbit2_rect(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("y0", "y1", "x0", "x1")]
 
 
+class orbit2_ipc_handle(C.Structure):
+    _fields_ = [("handle", C.c_uint8 * 64), ("offset", C.c_int64), ("bytes", C.c_int64)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2505_04802_b200.build` "
@@ -68,6 +72,13 @@ def _load():
         "orbit2_xfer_pack": (i32, [vp, i32, i32, vp, vp, vp]),
         "orbit2_xfer_unpack": (i32, [vp, i32, i32, vp, vp, vp]),
         "orbit2_stitch_peer": (i32, [vp, i32, vp, vp, vp, vp]),
+        "orbit2_ipc_export": (i32, [vp, C.POINTER(orbit2_ipc_handle)]),
+        "orbit2_comm_init": (i32, [vp, i32, vp, vp, C.POINTER(orbit2_ipc_handle), C.POINTER(orbit2_ipc_handle),
+                                   C.POINTER(orbit2_ipc_handle)]),
+        "orbit2_comm_target": (i32, [vp, C.POINTER(vp)]),
+        "orbit2_halo_exchange": (i32, [vp, vp]),
+        "orbit2_comm_barrier": (i32, [vp, vp]),
+        "orbit2_comm_status": (i32, [vp]),
         "orbit2_launch_count": (i64, [vp]),
         "orbit2_set_profiling": (i32, [vp, i32]),
         "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
@@ -84,6 +95,8 @@ def _load():
 lib = _load()
 EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orbit2_reslim_forward",
             "orbit2_stitch", "orbit2_xfer_plan", "orbit2_xfer_pack", "orbit2_xfer_unpack", "orbit2_stitch_peer",
+            "orbit2_ipc_export", "orbit2_comm_init", "orbit2_comm_target", "orbit2_halo_exchange",
+            "orbit2_comm_barrier", "orbit2_comm_status",
             "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
             "orbit2_destroy")
 
@@ -254,6 +267,56 @@ class Context:
         with _on_device(self.device):
             _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, _ptr(out),
                                      _stream(stream)), "orbit2_stitch")
+
+    def _stitch_to(self, tile_out, x_dev, tile_begin, tile_count, out_ptr: int, stream=None):
+        """orbit2_stitch into a raw device address (a peer's field mapped into this
+        process, from comm_target())."""
+        import torch
+        _req(x_dev, torch.float32, "x_dev")
+        _req(tile_out, torch.bfloat16 if self.bf16 else torch.float32, "tile_out")
+        with _on_device(self.device):
+            _check(lib.orbit2_stitch(self.handle, _ptr(tile_out), _ptr(x_dev), tile_begin, tile_count, out_ptr,
+                                     _stream(stream)), "orbit2_stitch")
+
+    # -- peer-memory TILES sequence parallelism (orbit2_comm_*) ---------------
+    def ipc_handles(self, x_dev, out_dev):
+        """Export handles of this rank's workspace, input field and output field
+        (None -> zero handle) as raw bytes, for the all-gather between processes."""
+        def one(t):
+            h = orbit2_ipc_handle()
+            if t is not None:
+                _check(lib.orbit2_ipc_export(_ptr(t), C.byref(h)), "orbit2_ipc_export")
+            return bytes(h)
+        return one(self.workspace), one(x_dev), one(out_dev)
+
+    def comm_init(self, gather_root, x_dev, out_dev, handles):
+        """handles: per rank (workspace, input, output) export bytes, rank order."""
+        R = self.cfg.world_size
+        if len(handles) != R:
+            raise ValueError("comm_init: one handle triple per rank")
+        arrs = [(orbit2_ipc_handle * R)() for _ in range(3)]
+        for r, trip in enumerate(handles):
+            for a, b in zip(arrs, trip):
+                C.memmove(C.byref(a[r]), b, C.sizeof(orbit2_ipc_handle))
+        with _on_device(self.device):
+            _check(lib.orbit2_comm_init(self.handle, gather_root, _ptr(x_dev),
+                                        _ptr(out_dev) if out_dev is not None else None, arrs[0], arrs[1], arrs[2]),
+                   "orbit2_comm_init")
+        p = C.c_void_p()
+        _check(lib.orbit2_comm_target(self.handle, C.byref(p)), "orbit2_comm_target")
+        return p.value
+
+    def halo_exchange(self, stream=None):
+        with _on_device(self.device):
+            _check(lib.orbit2_halo_exchange(self.handle, _stream(stream)), "orbit2_halo_exchange")
+
+    def comm_barrier(self, stream=None):
+        with _on_device(self.device):
+            _check(lib.orbit2_comm_barrier(self.handle, _stream(stream)), "orbit2_comm_barrier")
+
+    def comm_status(self):
+        with _on_device(self.device):
+            _check(lib.orbit2_comm_status(self.handle), "orbit2_comm_status")
 
     # -- multi-rank (TILES sequence parallelism) ------------------------------
     def orbit2_xfer_pack(self, kind, peer, x_dev, buf, stream=None):

@@ -1,23 +1,82 @@
 """TILES sequence parallelism over the GPUs of one box ("assigning each
-tile to a separate GPU"; "stitched together").
+tile to a separate GPU"; P:530 halo; "stitched together").
 
-One process per GPU.  Every data movement is a library kernel (rectangle
-pack/unpack, stitch); NCCL (through torch.distributed point-to-point ops)
-only moves the packed buffers over NVLink:
+One process per GPU.  The product path is `PeerSP`: the library moves every
+byte itself through NVLink peer mappings (CUDA IPC), so there is no separate
+communication step and no host synchronisation inside a step:
 
-  1. halo exchange   -- each rank starts with its owned core pixels; it
-                        receives the pixels of its padded tile rectangles that
-                        neighbouring ranks own (orbit2_xfer_* HALO).
-  2. forward         -- steps (1)-(3) + head over the rank's LPT-assigned tiles.
-  3. output gather   -- the root receives every rank's tile_out (bf16 decoder
-                        outputs of the core tokens) and the owned input cores
-                        (for the residual), then stitches all tiles
-                        (orbit2_stitch_peer).  gather_root=None leaves the
-                        output sharded (each rank stitches its own tiles).
+  1. halo exchange  -- orbit2_halo_exchange: each rank stores the pixels of its
+                       owned cores that peers' tiles need straight into the
+                       peers' input fields (push kernel), then a device-side
+                       barrier (release/acquire flags, system scope).
+  2. forward        -- orbit2_reslim_forward over the rank's LPT-assigned tiles,
+                       chunk by chunk into two alternating tile_out buffers.
+  3. output gather  -- orbit2_stitch of each chunk writes the root's output
+                       field directly through NVLink (fused crop + stitch +
+                       residual + gather), on a side stream, so it overlaps
+                       the next chunk's forward; gather_root = -1 keeps the
+                       output sharded (each rank stitches into its own field).
+  4. end barrier    -- orbit2_comm_barrier: every rank's stores are visible.
+
+torch.distributed is plumbing only: one all_gather_object of the export
+handles at setup.  The NCCL point-to-point functions further down
+(`forward_sequence_parallel`) are the round-1 baseline transport (torch
+batch_isend_irecv of packed rectangles), kept for comparison.
 """
 from __future__ import annotations
 
 from . import orbit2 as o2
+
+
+class PeerSP:
+    """Peer-memory TILES SP for one rank (see the module docstring).
+
+    ctx    : orbit2.Context with world_size = R, rank = this rank
+    x_dev  : this rank's input field [B,V,H,W] (owned core pixels valid)
+    out_dev: this rank's output field [B,K,sH,sW] (root / sharded), else None
+    """
+
+    def __init__(self, ctx, x_dev, out_dev, dist, gather_root=0, group=None):
+        import torch
+        self.ctx, self.x = ctx, x_dev
+        world = ctx.cfg.world_size
+        mine = ctx.ipc_handles(x_dev, out_dev)
+        allh = [None] * world
+        dist.all_gather_object(allh, mine, group=group)
+        self.target = ctx.comm_init(gather_root, x_dev, out_dev, allh)
+        dist.barrier(group=group)             # every rank's flags zeroed before anyone signals
+        n, ch = ctx.info.n_local_tiles, max(ctx.info.chunk_tiles, 1)
+        self.chunks = [(tb, min(ch, n - tb)) for tb in range(0, n, ch)]
+        self.tile_out = [ctx.tile_out_buffer() for _ in range(min(2, len(self.chunks)))]
+        self.side = torch.cuda.Stream(ctx.device) if hasattr(torch.cuda, "Stream") and x_dev.is_cuda else None
+        self.ev_fwd = [None, None]
+        self.ev_st = [None, None]
+
+    def step(self, packed, stream=None):
+        """One TILES-SP step of this rank; stream-ordered, no host sync."""
+        import torch
+        ctx = self.ctx
+        cuda = self.x.is_cuda
+        if stream is None and cuda:
+            stream = torch.cuda.current_stream(ctx.device)
+        ctx.halo_exchange(stream)
+        side = self.side if self.side is not None else stream
+        for i, (tb, tc) in enumerate(self.chunks):
+            b = i & 1
+            if cuda and self.ev_st[b] is not None:
+                stream.wait_event(self.ev_st[b])           # tile_out[b] stitched (chunk i - 2)
+            ctx.orbit2_reslim_forward(packed, self.x, tb, tc, self.tile_out[b], stream)
+            if cuda:
+                self.ev_fwd[b] = torch.cuda.Event()
+                self.ev_fwd[b].record(stream)
+                side.wait_event(self.ev_fwd[b])
+            ctx._stitch_to(self.tile_out[b], self.x, tb, tc, self.target, side)
+            if cuda:
+                self.ev_st[b] = torch.cuda.Event()
+                self.ev_st[b].record(side)
+        if cuda:
+            stream.wait_stream(side)
+        ctx.comm_barrier(stream)
 
 
 def _sync(x_dev, stream):

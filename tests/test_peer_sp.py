@@ -1,0 +1,203 @@
+"""Peer-memory TILES sequence parallelism (orbit2_comm_*, sequence_parallel.PeerSP).
+
+GPU: R ranks as R processes sharing ONE GPU (CUDA IPC works between processes
+on the same device, so the whole NVLink data path -- export, open, halo push
+kernel, stitch into the root's mapped field, release/acquire barrier kernels --
+runs on a single B200; real multi-GPU runs use scripts/sp_peer_demo.py).  The
+assembled field must be bit-identical to the 1-rank forward (I11) and within
+the bf16 tolerance of the fp64 oracle.
+
+CPU: the orchestration of PeerSP (handle all-gather, chunk schedule, barrier
+order) over gloo with world size 2 and a stand-in ctx.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from workloads import get_config, make_input, make_weights
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _spawn(target, world, *args):
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in procs]
+    for p in procs:
+        p.join(timeout=120)
+    return res
+
+
+# ---------------------------------------------------------------- CPU: orchestration
+class _FakeCtx:
+    """Stand-in ctx recording the calls PeerSP makes (CPU tensors, no kernels)."""
+
+    def __init__(self, o2, cfg):
+        self.cfg = cfg
+        self.tiles, self.info = o2.orbit2_tiles_plan(cfg)
+        self.device = torch.device("cpu")
+        self.calls = []
+
+    def ipc_handles(self, x, out):
+        r = self.cfg.rank
+        return (bytes([r]) * 80, bytes([16 + r]) * 80, bytes([32 + r]) * 80)
+
+    def comm_init(self, root, x, out, handles):
+        self.calls.append(("init", root, [h[0][0] for h in handles]))
+        return 1000 + root
+
+    def tile_out_buffer(self):
+        return torch.zeros(1)
+
+    def halo_exchange(self, stream=None):
+        self.calls.append(("halo",))
+
+    def orbit2_reslim_forward(self, packed, x, tb, tc, tile_out, stream=None):
+        self.calls.append(("fwd", tb, tc))
+
+    def _stitch_to(self, tile_out, x, tb, tc, ptr, stream=None):
+        self.calls.append(("stitch", tb, tc, ptr))
+
+    def comm_barrier(self, stream=None):
+        self.calls.append(("barrier",))
+
+
+def _cpu_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2505_04802_b200 import orbit2 as o2
+        from paper_2505_04802_b200.sequence_parallel import PeerSP
+        w = get_config("C1", batch=2, H=36, W=60, tiles_y=3, tiles_x=4, halo=2)
+        ctx = _FakeCtx(o2, o2.config_from(w, world_size=world, rank=rank, chunk_tiles=2))
+        sp = PeerSP(ctx, torch.zeros(1), None, dist, gather_root=0)
+        sp.step(None)
+        q.put(("ok", rank, ctx.calls, ctx.info.n_local_tiles))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", rank, repr(e), 0))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_sp_orchestration_gloo_world2():
+    """Every rank gets every rank's handles in rank order; a step is halo ->
+    (forward, stitch into the target) per chunk -> barrier, chunks covering the
+    rank's tiles exactly once."""
+    res = _spawn(_cpu_worker, 2)
+    for r in res:
+        assert r[0] == "ok", r
+        _, rank, calls, n_local = r
+        assert calls[0] == ("init", 0, [0, 1])
+        assert calls[1] == ("halo",) and calls[-1] == ("barrier",)
+        fwd = [c for c in calls if c[0] == "fwd"]
+        st = [c for c in calls if c[0] == "stitch"]
+        assert [c[1:] for c in fwd] == [c[1:3] for c in st]
+        assert all(c[3] == 1000 for c in st)
+        covered = sorted(t for _, tb, tc in fwd for t in range(tb, tb + tc))
+        assert covered == list(range(n_local))
+
+
+# ---------------------------------------------------------------- GPU: R processes on one GPU
+def _gpu_worker(rank, world, port, q, name, over, gather_root):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        from paper_2505_04802_b200 import orbit2 as o2
+        from paper_2505_04802_b200.sequence_parallel import PeerSP
+        w = get_config(name, **over)
+        B = w.batch
+        full = torch.from_numpy(make_input(w)).cuda()
+        blob = torch.from_numpy(make_weights(w)).cuda()
+        cfg = o2.config_from(w, precision=o2.BF16, world_size=world, rank=rank, chunk_tiles=1)
+        ctx = o2.Context(cfg)
+        packed = ctx.prepare_weights(blob)
+        x = torch.full_like(full, float("nan"))          # only the owned core pixels are valid
+        P = w.scale * w.patch
+        for t in ctx.tiles:
+            if t.owner_rank == rank:
+                sl = (slice(None), slice(None), slice(t.core_y0 * w.patch, t.core_y1 * w.patch),
+                      slice(t.core_x0 * w.patch, t.core_x1 * w.patch))
+                x[sl] = full[sl]
+        own_out = gather_root < 0 or gather_root == rank
+        out = torch.full((B, w.K, w.scale * w.H, w.scale * w.W), float("nan"), device="cuda") if own_out else None
+        sp = PeerSP(ctx, x, out, dist, gather_root=gather_root)
+        for _ in range(2):                                # two steps: epochs advance, flags reused
+            sp.step(packed)
+        torch.cuda.synchronize()
+        ctx.comm_status()
+        dist.barrier()
+        got = out.cpu() if out is not None else None
+        mine = [(t.core_y0 * P, t.core_y1 * P, t.core_x0 * P, t.core_x1 * P) for t in ctx.tiles
+                if t.owner_rank == rank]
+        q.put(("ok", rank, got.numpy() if got is not None else None, mine))
+    except Exception as e:  # pragma: no cover
+        import traceback
+        q.put(("err", rank, traceback.format_exc(), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def _reference(name, over):
+    from paper_2505_04802_b200 import orbit2 as o2
+    w = get_config(name, **over)
+    x = make_input(w)
+    blob = make_weights(w)
+    ctx = o2.Context(o2.config_from(w, precision=o2.BF16))
+    out = ctx.forward(ctx.prepare_weights(torch.from_numpy(blob).cuda()), torch.from_numpy(x).cuda())
+    torch.cuda.synchronize()
+    return w, x, blob, out.cpu().numpy()
+
+
+PEER_CASES = [
+    ("C2", dict(batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2), 2),
+    ("C2", dict(batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2), 3),
+    ("C1", dict(batch=2, tiles_y=1, tiles_x=1, halo=0), 2),      # a rank without tiles; halo 0 (1-px support)
+    ("C1", dict(batch=2, halo_mode=1, tiles_y=3, tiles_x=5, halo=1), 2),   # REPLICATE, ragged
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,over,world", PEER_CASES)
+def test_peer_sp_processes_on_one_gpu_bit_exact(name, over, world):
+    from oracle import reslim_tiles as O
+    from tests.gpu_helpers import BF16_TOL, rel_err
+    w, x, blob, ref = _reference(name, over)
+    res = _spawn(_gpu_worker, world, name, over, 0)
+    for r in res:
+        assert r[0] == "ok", r[2]
+    root = next(r for r in res if r[1] == 0)[2]
+    assert np.array_equal(root, ref)
+    assert rel_err(root, O.tiles_forward(x, blob, O.Problem.from_config(w))) <= BF16_TOL
+
+
+@pytest.mark.gpu
+def test_peer_sp_sharded_output():
+    """gather_root = -1: each rank's own field holds exactly its tiles' outputs."""
+    name, over = PEER_CASES[0][:2]
+    _, _, _, ref = _reference(name, over)
+    res = _spawn(_gpu_worker, 2, name, over, -1)
+    seen = np.zeros(ref.shape, bool)
+    for r in res:
+        assert r[0] == "ok", r[2]
+        _, rank, got, rects = r
+        for y0, y1, x0, x1 in rects:
+            assert np.array_equal(got[:, :, y0:y1, x0:x1], ref[:, :, y0:y1, x0:x1])
+            seen[:, :, y0:y1, x0:x1] = True
+    assert seen.all()
