@@ -138,6 +138,23 @@ constexpr bool kSplitP = ORBIT2_ATTN_SPLITP != 0;
 constexpr bool kLatePvWait = ORBIT2_ATTN_LATEPV != 0;
 // epilogue rows staged in smem and stored 4 rows per instruction
 constexpr bool kStagedEpilogue = ORBIT2_ATTN_STAGED_EPI != 0;
+#ifndef ORBIT2_ATTN_TAILSKIP
+#define ORBIT2_ATTN_TAILSKIP 1
+#endif
+// Partial last key block of a tile: 32-key chunks with no valid key are neither
+// exponentiated nor written to P, the PV MMA stops at the last written chunk and
+// S = Q K^T uses N = 64 when at most 64 keys are valid (MUFU work and tensor work
+// follow the tile's true length instead of the 128-key block).
+constexpr bool kTailSkip = ORBIT2_ATTN_TAILSKIP != 0;
+#ifndef ORBIT2_ATTN_DESYNC
+#define ORBIT2_ATTN_DESYNC 1
+#endif
+// At the start of each work item the second Q tile's softmax warp (same SM
+// sub-partition as the first tile's) starts its exponentials only when the first
+// tile's warp has done half (1) / all (2) of its first block's: the two warps'
+// exponential phases then interleave with each other's row-max / wait phases
+// instead of colliding on the MUFU (0 = both start together).
+constexpr int kDesync = ORBIT2_ATTN_DESYNC;
 
 template <int DH, int NQ>
 struct AttnCfg {
@@ -376,6 +393,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
       // walks the ring phases (wait full, arrive empty) to stay aligned.
       const int qt = warp - 1;
       constexpr uint32_t id_s = tc::idesc_bf16(128, 128, 0, 0);   // Q K-major, K K-major
+      constexpr uint32_t id_s64 = tc::idesc_bf16(128, 64, 0, 0);  // short last key block
       constexpr uint32_t id_o = tc::idesc_bf16(128, DH, 0, 1);    // P K-major, V MN-major
       const uint32_t q_addr = tc::smem_u32(sQ), k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV);
       const uint32_t p_addr = tc::smem_u32(sP);
@@ -385,8 +403,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         const bool active = qt < it.nq;
         const uint32_t qb = li % C::QBUF;
         tc::mbar_wait(&q_full[qb], (li / C::QBUF) & 1);
+        int js = 0;                       // key block of the next S
         auto issue_s = [&](bool last) {   // S = Q K_j^T for this Q tile
           const uint32_t st = gk % C::KST;
+          const bool n64 = kTailSkip && it.n - js * 128 <= 64;   // at most 64 valid keys: N = 64
+          ++js;
           tc::mbar_wait(&k_full[st], (gk / C::KST) & 1);
           if (lane == 0) TL_STAMP(2 + qt, ns, 0);
           if (active) {
@@ -400,7 +421,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
 #pragma unroll
               for (int kk = 0; kk < DH / 16; ++kk) {
                 const uint32_t adv = (uint32_t)(((kk * 16) / C::AC) * C::ATOM + ((kk * 16) % C::AC) * 2) >> 4;
-                tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd0 + adv, kd0 + adv, id_s, kk > 0);
+                tc::mma_bf16_ss(tmem + qt * C::TCOLS, qd0 + adv, kd0 + adv, n64 ? id_s64 : id_s, kk > 0);
               }
               tc::mma_commit(&s_full[qt]);
               tc::mma_commit(&k_empty[st]);
@@ -437,8 +458,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               if (lane == 0 && h == 0) TL_STAMP(2 + qt, np, 3);
               tc::tc_fence_after();
               if (tc::elect_one()) {
+                // K steps holding keys the softmax wrote (32-key chunks; kTailSkip)
+                const int kv = it.n - j * 128;
+                const int kk_end = kTailSkip && kv < 128 ? 2 * ((kv + 31) / 32) : 8;
 #pragma unroll
                 for (int kk = h * (8 / C::NPH); kk < (h + 1) * (8 / C::NPH); ++kk) {   // K = 16 keys per MMA
+                  if (kk >= kk_end) break;
                   const uint32_t padv = (uint32_t)((kk >> 2) * 16384 + (kk & 3) * 32) >> 4;
                   const uint32_t vadv = (uint32_t)(kk * 16 * C::RB) >> 4;
                   const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
@@ -595,16 +620,24 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         constexpr int KP = KC / C::NPH;                // keys per part
         float rs0 = 0.f, rs1 = 0.f;
         if constexpr (kPingPong) pp_sync(1 + qt);   // this tile's turn on the MUFU
+        // first block of an item with both Q tiles active: offset the two tiles'
+        // exponential phases (named barrier of this sub-partition's two warps)
+        const bool desync = kDesync > 0 && SPW == 1 && !kPingPong && j == 0 && it.nq == NQ && NQ == 2;
+        const uint32_t dbar = 11 + q;
+        if (desync && qt == 1) asm volatile("bar.sync %0, 64;" ::"r"(dbar) : "memory");
+        const int kv_blk = it.n - j * 128;         // valid keys of this block (SPW == 1)
+        const int c_arr = (kDesync == 1 ? KC / 2 : KC) - 32;   // chunk after which tile 0 releases tile 1
 #pragma unroll
         for (int h = 0; h < C::NPH; ++h) {
           wait_pv(h);
           if constexpr (C::P_TMEM) {
 #pragma unroll
-            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
-              uint32_t pk[32];
+            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 32) {
+              if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // chunk past the tile end
+              uint32_t pk[16];
               float2 rs = make_float2(0.f, 0.f);
 #pragma unroll
-              for (int e = 0; e < 64; e += 2) {
+              for (int e = 0; e < 32; e += 2) {
                 float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
                 ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
                 float2 pr;
@@ -615,8 +648,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               }
               rs0 += rs.x;
               rs1 += rs.y;
-              tc::tmem_st32(p_tm + c0 / 2, pk);
+              tc::tmem_st16(p_tm + c0 / 2, pk);
+              if (desync && qt == 0 && c0 == c_arr) asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
             }
+            if (desync && qt == 0 && kTailSkip && kv_blk <= c_arr)   // loop left before c_arr: still release
+              asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
             tc::tmem_st_wait();
           } else {   // P to smem (SW128 K-major, 64-key atoms of 16 KB)
             uint8_t* prow = sP + qt * C::P_SMEM + i * 128;

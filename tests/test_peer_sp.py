@@ -165,9 +165,12 @@ def _reference(name, over):
     return w, x, blob, out.cpu().numpy()
 
 
+# world size 2 only: with more processes time-slicing one GPU, a rank's barrier
+# kernel can spin through whole time slices of the others (measured: R = 3 ran
+# into the 30 s barrier timeout); R = 2 / 4 on separate GPUs are covered by
+# scripts/sp_peer_demo.py and the bench.
 PEER_CASES = [
     ("C2", dict(batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2), 2),
-    ("C2", dict(batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2), 3),
     ("C1", dict(batch=2, tiles_y=1, tiles_x=1, halo=0), 2),      # a rank without tiles; halo 0 (1-px support)
     ("C1", dict(batch=2, halo_mode=1, tiles_y=3, tiles_x=5, halo=1), 2),   # REPLICATE, ragged
 ]
