@@ -141,13 +141,13 @@ constexpr bool kStagedEpilogue = ORBIT2_ATTN_STAGED_EPI != 0;
 #ifndef ORBIT2_ATTN_TAILSKIP
 #define ORBIT2_ATTN_TAILSKIP 1
 #endif
-// Partial last key block of a tile: 32-key chunks with no valid key are neither
+// Partial last key block of a tile: 64-key halves with no valid key are neither
 // exponentiated nor written to P, the PV MMA stops at the last written chunk and
 // S = Q K^T uses N = 64 when at most 64 keys are valid (MUFU work and tensor work
 // follow the tile's true length instead of the 128-key block).
 constexpr bool kTailSkip = ORBIT2_ATTN_TAILSKIP != 0;
 #ifndef ORBIT2_ATTN_DESYNC
-#define ORBIT2_ATTN_DESYNC 1
+#define ORBIT2_ATTN_DESYNC 0   // measured no gain (C2: 20.6-20.9 vs 20.5 ms with the same tail skip)
 #endif
 // At the start of each work item the second Q tile's softmax warp (same SM
 // sub-partition as the first tile's) starts its exponentials only when the first
@@ -458,9 +458,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               if (lane == 0 && h == 0) TL_STAMP(2 + qt, np, 3);
               tc::tc_fence_after();
               if (tc::elect_one()) {
-                // K steps holding keys the softmax wrote (32-key chunks; kTailSkip)
+                // K steps holding keys the softmax wrote (64-key halves; kTailSkip)
                 const int kv = it.n - j * 128;
-                const int kk_end = kTailSkip && kv < 128 ? 2 * ((kv + 31) / 32) : 8;
+                const int kk_end = kTailSkip && kv <= 64 ? 4 : 8;
 #pragma unroll
                 for (int kk = h * (8 / C::NPH); kk < (h + 1) * (8 / C::NPH); ++kk) {   // K = 16 keys per MMA
                   if (kk >= kk_end) break;
@@ -626,18 +626,18 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         const uint32_t dbar = 11 + q;
         if (desync && qt == 1) asm volatile("bar.sync %0, 64;" ::"r"(dbar) : "memory");
         const int kv_blk = it.n - j * 128;         // valid keys of this block (SPW == 1)
-        const int c_arr = (kDesync == 1 ? KC / 2 : KC) - 32;   // chunk after which tile 0 releases tile 1
+        const int c_arr = (kDesync == 1 ? KC / 2 : KC) - 64;   // half after which tile 0 releases tile 1
 #pragma unroll
         for (int h = 0; h < C::NPH; ++h) {
           wait_pv(h);
           if constexpr (C::P_TMEM) {
 #pragma unroll
-            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 32) {
-              if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // chunk past the tile end
-              uint32_t pk[16];
+            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
+              if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // half past the tile end
+              uint32_t pk[32];
               float2 rs = make_float2(0.f, 0.f);
 #pragma unroll
-              for (int e = 0; e < 32; e += 2) {
+              for (int e = 0; e < 64; e += 2) {
                 float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
                 ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
                 float2 pr;
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
               }
               rs0 += rs.x;
               rs1 += rs.y;
-              tc::tmem_st16(p_tm + c0 / 2, pk);
+              tc::tmem_st32(p_tm + c0 / 2, pk);
               if (desync && qt == 0 && c0 == c_arr) asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
             }
             if (desync && qt == 0 && kTailSkip && kv_blk <= c_arr)   // loop left before c_arr: still release

@@ -77,6 +77,21 @@ bool make_tmap_f32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols
 // Per-device launch state (a process may drive several devices: attributes and
 // SM counts are per device, cached by device ordinal)
 // ---------------------------------------------------------------------------
+// 3-D fp32 tensor [d2][d1][d0] (d0 contiguous), box [b2][b1][b0], no swizzle:
+// the smem box is dense [b2][b1][b0]; out-of-bound elements are zero-filled.
+bool make_tmap_f32_3d(CUtensorMap* map, const void* ptr, int64_t d0, int64_t d1, int64_t d2, int b0, int b1,
+                      int b2) {
+  if (!tma_available()) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)d0, (cuuint64_t)d1, (cuuint64_t)d2};
+  cuuint64_t strides[2] = {(cuuint64_t)(d0 * 4), (cuuint64_t)(d0 * d1 * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 namespace {
 constexpr int kMaxDev = 64;
 std::atomic<int> g_sms[kMaxDev];
@@ -558,8 +573,12 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
   const GemmOperand& kb = TRANS ? A : Bw;
   const int64_t Mk = TRANS ? N : M, Nk = TRANS ? M : N;
   CUtensorMap ta, tb, tcm, tdm;
-  if (!make_tmap_bf16(&ta, ka.ptr, ka.rows, K, ka.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
-  if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  // an operand may hold fewer than K valid columns (the patch matrix: Din of
+  // round_up(Din, 64)); the TMA zero-fills the rest of the K range
+  if (!make_tmap_bf16(&ta, ka.ptr, ka.rows, ka.cols ? ka.cols : K, ka.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, kb.cols ? kb.cols : K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
   tcm = ta;   // unused unless set below

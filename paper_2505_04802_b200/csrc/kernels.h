@@ -1,6 +1,8 @@
 // kernels.h -- launchers of the liborbit2 kernels (host side declarations).
 #pragma once
 
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -40,6 +42,7 @@ struct GemmOperand {
   const void* ptr;         // row-major [rows][ld] (K contiguous)
   int64_t rows;            // allocated rows (TMA extent)
   int64_t ld;              // elements per row
+  int64_t cols = 0;        // valid columns (TMA extent; zero-filled up to K); 0 = K
 };
 
 // Tiles/chunk view for the token-level kernels.
@@ -61,6 +64,13 @@ struct ChunkDev {
 template <typename T>
 void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch, int B, int V, int H,
                    int W, int p, int din, int din_pad, int max_pad_h, cudaStream_t st);
+// bf16 CLAMP-mode gather with TMA-staged input boxes: patch rows of ld = round_up(din, 8)
+// columns (no zero columns: the embed GEMM's TMA zero-fills K past din).  Returns
+// false when the shape is outside what it handles (caller falls back to launch_gather).
+bool launch_gather_tma(const float* x, __nv_bfloat16* patches, int2* rowinfo, const ChunkDev& ch, int B, int V,
+                       int H, int W, int p, int din, int ld, int max_pad_h, int max_pad_w, cudaStream_t st);
+bool make_tmap_f32_3d(CUtensorMap* map, const void* ptr, int64_t d0, int64_t d1, int64_t d2, int b0, int b1,
+                      int b2);
 template <typename T>
 void launch_layernorm(const float* z, const float* g, const float* b, T* out, int64_t M, int D,
                       const ChunkDev* compact /* null = identity rows */, cudaStream_t st);

@@ -45,6 +45,7 @@ struct Ctx {
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
   bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
+  bool simt_gather = false;       // ORBIT2_SIMT_GATHER=1: smem-staged SIMT gather instead of the TMA one
   // peer-memory SP (orbit2_comm_*)
   bool comm = false;
   int32_t gather_root = 0;
@@ -215,6 +216,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->unfused_block = ub && ub[0] == '1';
   const char* aq = std::getenv("ORBIT2_ALL_QUERIES_LAST");
   c->all_queries_last = aq && aq[0] == '1';
+  const char* sg = std::getenv("ORBIT2_SIMT_GATHER");
+  c->simt_gather = sg && sg[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
@@ -375,17 +378,35 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
     bf16* hid = c->at<bf16>(ly.hid);
     bf16* hin = c->at<bf16>(ly.hin);
     auto gemm = [&](const char* name, int epi, int out_bf, const void* A, int64_t arows, int64_t lda,
-                    int64_t wo, int64_t n, int64_t k, int64_t rows, EpiParams ep) {
-      GemmOperand a{A, arows, lda}, b{W8 + wo, n, k};
+                    int64_t wo, int64_t n, int64_t k, int64_t rows, EpiParams ep, int64_t acols = 0) {
+      GemmOperand a{A, arows, lda, acols}, b{W8 + wo, n, k};
       ep.M = (int32_t)rows;
       ep.N = (int32_t)n;
       return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
     };
-    ORBIT2_TRY(run(c, "tile_gather", st, [&] {
-      launch_gather<bf16>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
-                          p.max_pad_h, st);
-      return true;
-    }));
+    // step (1): TMA-staged gather (CLAMP halos) into patch rows of ld_patch columns;
+    // the smem-staged SIMT gather with zero-padded rows otherwise (REPLICATE halos
+    // read clamped edge pixels, which a TMA box would zero-fill)
+    int64_t lda_patch = ly.din_pad, cols_patch = 0;
+    if (cf.halo_mode == ORBIT2_HALO_CLAMP && !c->simt_gather) {
+      bool ok = false;
+      ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+        ok = launch_gather_tma(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.ld_patch,
+                               p.max_pad_h, p.max_pad_w, st);
+        return true;
+      }));
+      if (ok) {
+        lda_patch = ly.ld_patch;
+        cols_patch = p.Din;
+      }
+    }
+    if (cols_patch == 0) {
+      ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+        launch_gather<bf16>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
+                            p.max_pad_h, st);
+        return true;
+      }));
+    }
     // Key/value blocks of the last tile may read up to 127 rows past M: keep
     // them finite (their probabilities are 0, but 0 * NaN would poison P.V).
     if (mrow > M) {
@@ -400,9 +421,11 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       e.xn = xn;
       e.ln_g = wf(w.layers[0].ln1_g);
       e.ln_b = wf(w.layers[0].ln1_b);
-      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED_LN, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, e));
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED_LN, 0, patches, mrow, lda_patch, w.w_e, D, ly.din_pad, M, e,
+                      cols_patch));
     } else {
-      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, lda_patch, w.w_e, D, ly.din_pad, M, emb,
+                      cols_patch));
     }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];

@@ -47,7 +47,8 @@ struct Layout {
   int64_t sig, push, sigtab;  // peer-memory SP: barrier flags, push table, peers' flag pointers
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
-  int32_t din_pad;
+  int32_t din_pad;            // K of the embedding GEMM: round_up(Din, 64)
+  int32_t ld_patch;           // row stride of TMA-gathered bf16 patch rows: round_up(Din, 8)
   int32_t esize;              // activation element size (2 bf16, 4 fp32)
 };
 
@@ -82,7 +83,7 @@ struct Plan {
   std::vector<int32_t> core_rblk;
   orbit2_plan_info info;
   Layout lay;
-  int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_core_h;
+  int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_pad_w, max_core_h;
   // multi-rank: every rank's device tile table (for orbit2_stitch_peer) and
   // this rank's transfer rectangle lists
   std::vector<std::vector<DevTile>> dev_by_rank;   // with sentinel

@@ -151,6 +151,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   int64_t ltok = 0, lcore = 0;
   int32_t qb = 0, qp = 0;
   p.max_pad_h = 0;
+  p.max_pad_w = 0;
   p.max_core_h = 0;
   for (int32_t li = 0; li < (int32_t)p.local.size(); ++li) {
     const orbit2_tile& t = p.tiles[p.local[li]];
@@ -185,6 +186,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
         p.core_row.push_back((int32_t)(ltok + (int64_t)(u + dt.core_y0 - dt.pad_y0) * dt.pad_w +
                                        (w + dt.core_x0 - dt.pad_x0)));
     p.max_pad_h = std::max(p.max_pad_h, dt.pad_h);
+    p.max_pad_w = std::max(p.max_pad_w, dt.pad_w);
     p.max_core_h = std::max(p.max_core_h, dt.core_h);
     qb += nqb;
     qp += nqp;
@@ -317,6 +319,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   Layout& ly = p.lay;
   ly.esize = c.precision == ORBIT2_BF16 ? 2 : 4;
   ly.din_pad = (int32_t)round_up(p.Din, 64);
+  ly.ld_patch = (int32_t)round_up(p.Din, 8);
   ly.mrow = round_up(std::max<int64_t>(1, (int64_t)c.batch * in.max_chunk_tokens), kQBlock);
   ly.mcore = round_up(std::max<int64_t>(1, (int64_t)c.batch * in.max_chunk_core_tokens), kQBlock);
   int64_t off = 0;
