@@ -34,10 +34,13 @@ template <int P_>   // P_ = 2: specialised (every shipped config); 0: runtime p
 __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__ CUtensorMap tx,
                                                          __nv_bfloat16* __restrict__ patches,
                                                          int2* __restrict__ rowinfo, ChunkDev ch, int V, int p_rt,
-                                                         int din, int ld, int segw) {
+                                                         int din, int ld, int segw, int sw) {
   const int p = P_ ? P_ : p_rt;
   extern __shared__ __align__(128) uint8_t gsm[];
-  const int sw = segw * p;                                   // box width (pixels)
+  // sw = box width (pixels) >= p * segw + 3: the box starts at the 16-byte aligned
+  // column at or left of the segment (a TMA box must start on a 16-byte boundary
+  // in its innermost dimension; measured: an unaligned start is an illegal
+  // instruction), `o` pixels before the segment's first one
   float* sin = reinterpret_cast<float*>(gsm);               // [V][p][sw]
   uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + (((size_t)V * p * sw * 4 + 15) & ~(size_t)15));
   const DevTile t = ch.tiles[ch.tb + blockIdx.y];
@@ -58,9 +61,11 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
   uint32_t phase = 0;
   for (int w0 = 0; w0 < t.pad_w; w0 += segw) {
     const int nw = min(segw, t.pad_w - w0);
+    const int xs = p * (t.pad_x0 + w0);
+    const int xa = xs & ~3, o = xs - xa;                     // o in {0, 2} for p = 2
     if (threadIdx.x == 0) {
       tc::mbar_arrive_expect_tx(bar, box_bytes);
-      tc::tma_load_3d(&tx, sin, bar, p * (t.pad_x0 + w0), p * u, b * V);
+      tc::tma_load_3d(&tx, sin, bar, xa, p * u, b * V);
     }
     tc::mbar_wait(bar, phase);
     phase ^= 1;
@@ -74,8 +79,8 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
           const int v = 2 * c + h;
           float2 r0 = make_float2(0.f, 0.f), r1 = r0;
           if (v < V) {
-            r0 = *reinterpret_cast<const float2*>(sin + (v * 2 + 0) * sw + tw * 2);
-            r1 = *reinterpret_cast<const float2*>(sin + (v * 2 + 1) * sw + tw * 2);
+            r0 = *reinterpret_cast<const float2*>(sin + (v * 2 + 0) * sw + o + tw * 2);
+            r1 = *reinterpret_cast<const float2*>(sin + (v * 2 + 1) * sw + o + tw * 2);
           }
           o[2 * h] = tc::pack_bf16(r0.x, r0.y);
           o[2 * h + 1] = tc::pack_bf16(r1.x, r1.y);
@@ -88,7 +93,7 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
           f[e] = 0.f;
           if (col < din) {
             const int v = col / pp, r = col - v * pp, dy = r / p, dx = r - dy * p;
-            f[e] = sin[(v * p + dy) * sw + tw * p + dx];
+            f[e] = sin[(v * p + dy) * sw + o + tw * p + dx];
           }
         }
 #pragma unroll
@@ -108,23 +113,24 @@ bool launch_gather_tma(const float* x, __nv_bfloat16* patches, int2* rowinfo, co
   if (ld % 8 != 0 || ld < din || V > 256 || p > 8 || (W * 4) % 16 != 0) return false;
   // segment of tokens per box: box width p * segw <= 256 pixels, a multiple of 4
   // (16-byte rows); as wide as the widest padded row when that fits
-  const int m = p % 4 == 0 ? 1 : (p % 2 == 0 ? 2 : 4);      // segw multiple of m <=> segw * p % 4 == 0
-  int segw = (std::min(max_pad_w, 256 / p) + m - 1) / m * m;
-  if (segw * p > 256) segw -= m;
-  if (segw < 1 || (segw * p) % 4 || segw * p > 256) return false;
-  const size_t smem = (((size_t)V * p * segw * p * 4 + 15) & ~(size_t)15) + 16;
+  // tokens per box: the box (p * segw + 3 pixels rounded up to 16 bytes, <= 256)
+  // covers the widest padded row when that fits
+  const int segw = std::min(max_pad_w, (256 - 3) / p);
+  const int sw = (segw * p + 3 + 3) & ~3;
+  if (segw < 1 || sw > 256) return false;
+  const size_t smem = (((size_t)V * p * sw * 4 + 15) & ~(size_t)15) + 16;
   if (smem > 200 * 1024) return false;
   CUtensorMap tx;
-  if (!make_tmap_f32_3d(&tx, x, W, H, (int64_t)B * V, segw * p, p, V)) return false;
+  if (!make_tmap_f32_3d(&tx, x, W, H, (int64_t)B * V, sw, p, V)) return false;
   dim3 grid(max_pad_h, ch.tc, B);
   if (p == 2) {
     static std::atomic<uint64_t> done{0};
     if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<2>), (int)smem, &done)) return false;
-    gather_tma_kernel<2><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw);
+    gather_tma_kernel<2><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw, sw);
   } else {
     static std::atomic<uint64_t> done{0};
     if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<0>), (int)smem, &done)) return false;
-    gather_tma_kernel<0><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw);
+    gather_tma_kernel<0><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw, sw);
   }
   return true;
 }

@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <mutex>
 
@@ -56,6 +58,9 @@ bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t col
   CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && std::getenv("ORBIT2_DEBUG_TMAP"))
+    std::fprintf(stderr, "[orbit2] cuTensorMapEncodeTiled(bf16) = %d: ptr %p dims %lld x %lld ld %lld box %d x %d swz %d\n",
+                 (int)r, ptr, (long long)cols, (long long)rows, (long long)ld, box_cols, box_rows, (int)swz);
   return r == CUDA_SUCCESS;
 }
 

@@ -69,6 +69,11 @@ void launch_gather(const float* x, T* patches, int2* rowinfo, const ChunkDev& ch
 // false when the shape is outside what it handles (caller falls back to launch_gather).
 bool launch_gather_tma(const float* x, __nv_bfloat16* patches, int2* rowinfo, const ChunkDev& ch, int B, int V,
                        int H, int W, int p, int din, int ld, int max_pad_h, int max_pad_w, cudaStream_t st);
+// bf16 stitch for P = 8 with TMA-staged tile_out boxes and a separable residual;
+// false when the shape is outside what it handles (caller falls back to launch_stitch).
+bool launch_stitch_tma(const __nv_bfloat16* tile_out, int64_t tile_out_rows, const float* x, float* out,
+                       const ChunkDev& ch, const int32_t* cmap, int B, int V, int H, int W, int K, int s, int P,
+                       int max_core_h, int max_core_w, cudaStream_t st);
 bool make_tmap_f32_3d(CUtensorMap* map, const void* ptr, int64_t d0, int64_t d1, int64_t d2, int b0, int b1,
                       int b2);
 template <typename T>

@@ -83,7 +83,7 @@ struct Plan {
   std::vector<int32_t> core_rblk;
   orbit2_plan_info info;
   Layout lay;
-  int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_pad_w, max_core_h;
+  int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_pad_w, max_core_h, max_core_w;
   // multi-rank: every rank's device tile table (for orbit2_stitch_peer) and
   // this rank's transfer rectangle lists
   std::vector<std::vector<DevTile>> dev_by_rank;   // with sentinel

@@ -153,6 +153,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   p.max_pad_h = 0;
   p.max_pad_w = 0;
   p.max_core_h = 0;
+  p.max_core_w = 0;
   for (int32_t li = 0; li < (int32_t)p.local.size(); ++li) {
     const orbit2_tile& t = p.tiles[p.local[li]];
     DevTile dt{};
@@ -188,6 +189,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     p.max_pad_h = std::max(p.max_pad_h, dt.pad_h);
     p.max_pad_w = std::max(p.max_pad_w, dt.pad_w);
     p.max_core_h = std::max(p.max_core_h, dt.core_h);
+    p.max_core_w = std::max(p.max_core_w, dt.core_w);
     qb += nqb;
     qp += nqp;
     ltok += t.n_tokens;
@@ -221,6 +223,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       rcore[r] += tt.n_core_tokens;
       p.dev_by_rank[r].push_back(dt);
       p.max_core_h = std::max(p.max_core_h, dt.core_h);
+      p.max_core_w = std::max(p.max_core_w, dt.core_w);
     }
     int64_t off = 0;
     for (int r = 0; r < c.world_size; ++r) {
