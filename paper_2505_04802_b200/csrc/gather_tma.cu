@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
   // sw = box width (pixels) >= p * segw + 3: the box starts at the 16-byte aligned
   // column at or left of the segment (a TMA box must start on a 16-byte boundary
   // in its innermost dimension; measured: an unaligned start is an illegal
-  // instruction), `o` pixels before the segment's first one
+  // instruction), `xo` pixels before the segment's first one
   float* sin = reinterpret_cast<float*>(gsm);               // [V][p][sw]
   uint64_t* bar = reinterpret_cast<uint64_t*>(gsm + (((size_t)V * p * sw * 4 + 15) & ~(size_t)15));
   const DevTile t = ch.tiles[ch.tb + blockIdx.y];
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
   for (int w0 = 0; w0 < t.pad_w; w0 += segw) {
     const int nw = min(segw, t.pad_w - w0);
     const int xs = p * (t.pad_x0 + w0);
-    const int xa = xs & ~3, o = xs - xa;                     // o in {0, 2} for p = 2
+    const int xa = xs & ~3, xo = xs - xa;                    // xo in {0, 2} for p = 2
     if (threadIdx.x == 0) {
       tc::mbar_arrive_expect_tx(bar, box_bytes);
       tc::tma_load_3d(&tx, sin, bar, xa, p * u, b * V);
@@ -79,8 +79,8 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
           const int v = 2 * c + h;
           float2 r0 = make_float2(0.f, 0.f), r1 = r0;
           if (v < V) {
-            r0 = *reinterpret_cast<const float2*>(sin + (v * 2 + 0) * sw + o + tw * 2);
-            r1 = *reinterpret_cast<const float2*>(sin + (v * 2 + 1) * sw + o + tw * 2);
+            r0 = *reinterpret_cast<const float2*>(sin + (v * 2 + 0) * sw + xo + tw * 2);
+            r1 = *reinterpret_cast<const float2*>(sin + (v * 2 + 1) * sw + xo + tw * 2);
           }
           o[2 * h] = tc::pack_bf16(r0.x, r0.y);
           o[2 * h + 1] = tc::pack_bf16(r1.x, r1.y);
@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(128) gather_tma_kernel(const __grid_constant__
           f[e] = 0.f;
           if (col < din) {
             const int v = col / pp, r = col - v * pp, dy = r / p, dx = r - dy * p;
-            f[e] = sin[(v * p + dy) * sw + o + tw * p + dx];
+            f[e] = sin[(v * p + dy) * sw + xo + tw * p + dx];
           }
         }
 #pragma unroll
