@@ -125,11 +125,11 @@ bool launch_gather_tma(const float* x, __nv_bfloat16* patches, int2* rowinfo, co
   dim3 grid(max_pad_h, ch.tc, B);
   if (p == 2) {
     static std::atomic<uint64_t> done{0};
-    if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<2>), (int)smem, &done)) return false;
+    if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<2>), 200 * 1024, &done)) return false;
     gather_tma_kernel<2><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw, sw);
   } else {
     static std::atomic<uint64_t> done{0};
-    if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<0>), (int)smem, &done)) return false;
+    if (!smem_attr_once(reinterpret_cast<const void*>(gather_tma_kernel<0>), 200 * 1024, &done)) return false;
     gather_tma_kernel<0><<<grid, 128, smem, st>>>(tx, patches, rowinfo, ch, V, p, din, ld, segw, sw);
   }
   return true;

@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -364,6 +365,97 @@ __global__ void __launch_bounds__(128) stitch4_kernel(const T* __restrict__ tile
   }
 }
 
+// Separable variant (every shipped configuration: P % 4 == 0, p = P / s <= 2): the
+// P output rows of a token row read at most p + 2 = 4 input rows, so each thread
+// interpolates its 4 columns along X on those rows ONCE per variable (8 loads per
+// row) and the P output rows only lerp in Y from registers -- 32 loads per
+// (thread, k) instead of 16 per output row (the 4-load-per-element form is
+// issue-bound: ncu issue 68 % at 2.7 TB/s).
+// ORBIT2_STITCH_PER_ELEMENT=1: the 4-loads-per-element stitch4_kernel (A/B runs)
+static bool stitch_per_element() {
+  static const bool v = [] {
+    const char* e = std::getenv("ORBIT2_STITCH_PER_ELEMENT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) stitch4s_kernel(const T* __restrict__ tile_out, const float* __restrict__ x,
+                                                       float* __restrict__ out, ChunkDev ch,
+                                                       const int32_t* __restrict__ cmap, int V, int H, int W, int K,
+                                                       int s, int P) {
+  constexpr int NR = 4;
+  const DevTile t = ch.tiles[ch.tb + blockIdx.y];
+  const int ur = blockIdx.x;
+  if (ur >= t.core_h) return;
+  const int b = blockIdx.z;
+  const int X0 = t.core_x0 * P, NX4 = t.core_w * P / 4;
+  const int64_t sH = (int64_t)s * H, sW = (int64_t)s * W;
+  const int64_t trow0 = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0) + (int64_t)ur * t.core_w;
+  const int Nh = K * P * P;
+  const float inv_s = 1.0f / (float)s;
+  const int Yb = (t.core_y0 + ur) * P;
+  const int ylo = min((int)fmaxf(((float)Yb + 0.5f) * inv_s - 0.5f, 0.f), H - 1);
+  for (int c4 = threadIdx.x; c4 < NX4; c4 += blockDim.x) {
+    const int xr = 4 * c4;
+    const int wr = xr / P, be = xr - wr * P;
+    const int X = X0 + xr;
+    int xa[4], xb[4];
+    float lx[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float sx = fmaxf(((float)(X + e) + 0.5f) * inv_s - 0.5f, 0.f);
+      xa[e] = min((int)sx, W - 1);
+      xb[e] = min(xa[e] + 1, W - 1);
+      lx[e] = sx - (float)xa[e];
+    }
+    const T* trow = tile_out + (trow0 + wr) * Nh + be;
+    for (int k = 0; k < K; ++k) {
+      const float* pl = x + ((int64_t)b * V + cmap[k]) * H * W;
+      float hx[NR][4];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const float* row = pl + (int64_t)min(ylo + r, H - 1) * W;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) hx[r][e] = (1.f - lx[e]) * __ldg(row + xa[e]) + lx[e] * __ldg(row + xb[e]);
+      }
+      for (int al = 0; al < P; ++al) {
+        const int Y = Yb + al;
+        const float sy = fmaxf(((float)Y + 0.5f) * inv_s - 0.5f, 0.f);
+        const int y0 = min((int)sy, H - 1), y1 = min(y0 + 1, H - 1);
+        const float ly = sy - (float)y0;
+        const int r0 = y0 - ylo, r1 = y1 - ylo;   // in [0, NR) since P / s <= 2
+        float vit[4];
+        const T* src = trow + (k * P + al) * P;
+        if constexpr (sizeof(T) == 2) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(src);
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+          vit[0] = __low2float(lo); vit[1] = __high2float(lo);
+          vit[2] = __low2float(hi); vit[3] = __high2float(hi);
+        } else {
+          const float4 v = *reinterpret_cast<const float4*>(src);
+          vit[0] = v.x; vit[1] = v.y; vit[2] = v.z; vit[3] = v.w;
+        }
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          // registers indexed by the (warp-uniform) row offsets: select, not local memory
+          float h0 = hx[0][e], h1 = hx[1][e];
+#pragma unroll
+          for (int r = 1; r < NR; ++r) {
+            if (r0 == r) h0 = hx[r][e];
+            if (r1 == r) h1 = hx[r][e];
+          }
+          o[e] = vit[e] + ((1.f - ly) * h0 + ly * h1);
+        }
+        *reinterpret_cast<float4*>(out + (((int64_t)b * K + k) * sH + Y) * sW + X) = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+  }
+}
+
 template <typename T>
 void launch_stitch(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap, int B,
                    int V, int H, int W, int K, int s, int P, int max_core_h, cudaStream_t st) {
@@ -372,7 +464,10 @@ void launch_stitch(const T* tile_out, const float* x, float* out, const ChunkDev
   const bool vec = P % 4 == 0 && ((int64_t)s * W) % 4 == 0;
   if (vec) {
     dim3 grid(max_core_h, ch.tc, B);
-    stitch4_kernel<T><<<grid, 128, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+    if (P / s <= 2 && !stitch_per_element())
+      stitch4s_kernel<T><<<grid, 128, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
+    else
+      stitch4_kernel<T><<<grid, 128, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);
   } else {
     dim3 grid(max_core_h * P, ch.tc, B);
     stitch_kernel<T><<<grid, 256, 0, st>>>(tile_out, x, out, ch, cmap, V, H, W, K, s, P);

@@ -46,7 +46,7 @@ struct Ctx {
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
   bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
   bool simt_gather = false;       // ORBIT2_SIMT_GATHER=1: smem-staged SIMT gather instead of the TMA one
-  bool simt_stitch = false;       // ORBIT2_SIMT_STITCH=1: per-element stitch4 kernel instead of the TMA one
+  bool tma_stitch = false;        // ORBIT2_TMA_STITCH=1: TMA-staged stitch (measured slower than the SIMT one)
   // peer-memory SP (orbit2_comm_*)
   bool comm = false;
   int32_t gather_root = 0;
@@ -219,8 +219,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->all_queries_last = aq && aq[0] == '1';
   const char* sg = std::getenv("ORBIT2_SIMT_GATHER");
   c->simt_gather = sg && sg[0] == '1';
-  const char* ss = std::getenv("ORBIT2_SIMT_STITCH");
-  c->simt_stitch = ss && ss[0] == '1';
+  const char* ss = std::getenv("ORBIT2_TMA_STITCH");
+  c->tma_stitch = ss && ss[0] == '1';
   cudaError_t e = cudaSuccess;
   e = cudaMemcpy(c->at<void>(p.lay.tiles), p.dev.data(), p.dev.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qblk_tile.empty())
@@ -629,7 +629,7 @@ orbit2_status orbit2_stitch_peer(void* ctx, int32_t peer, const void* tile_out_d
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
   return run(c, "stitch_residual", st, [&] {
-    if (cf.precision == ORBIT2_BF16 && !c->simt_stitch &&
+    if (cf.precision == ORBIT2_BF16 && c->tma_stitch &&
         launch_stitch_tma(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), (int64_t)cf.batch * cd.chunk_core,
                           input_dev, out_dev, cd, cmap, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h,
                           p.max_core_w, st))
@@ -658,7 +658,7 @@ orbit2_status orbit2_stitch(void* ctx, const void* tile_out_dev, const float* in
   const ChunkDev cd = chunk_dev(c, make_chunk(p, tile_begin, tile_count));
   const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
   return run(c, "stitch_residual", st, [&] {
-    if (cf.precision == ORBIT2_BF16 && !c->simt_stitch &&
+    if (cf.precision == ORBIT2_BF16 && c->tma_stitch &&
         launch_stitch_tma(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), (int64_t)cf.batch * cd.chunk_core,
                           input_dev, out_dev, cd, cmap, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, p.max_core_h,
                           p.max_core_w, st))

@@ -136,7 +136,7 @@ bool launch_stitch_tma(const __nv_bfloat16* tile_out, int64_t tile_out_rows, con
                       CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
   static std::atomic<uint64_t> done{0};
-  if (!smem_attr_once(reinterpret_cast<const void*>(stitch_tma_kernel), (int)smem, &done)) return false;
+  if (!smem_attr_once(reinterpret_cast<const void*>(stitch_tma_kernel), 200 * 1024, &done)) return false;
   dim3 grid(max_core_h, ch.tc, B);
   stitch_tma_kernel<<<grid, 256, smem, st>>>(tt, x, out, ch, cmap, V, H, W, K, s, boxr, nx_max, nr_max);
   return true;
