@@ -328,6 +328,9 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   int64_t off = 0;
   auto take = [&](int64_t bytes) { int64_t o = off; off = round_up(off + std::max<int64_t>(bytes, 1), kAlign); return o; };
   const int64_t E = ly.esize;
+  // peer-memory SP barrier flags [2][R] u64 + error word FIRST: peers address this
+  // region in each other's workspaces, so its offset must not depend on the rank
+  ly.sig = take(2LL * c.world_size * 8 + 64);
   ly.rowinfo = take(ly.mrow * 8);
   ly.patches = take(ly.mrow * ly.din_pad * E);
   ly.z = take(ly.mrow * (int64_t)p.D * 4);
@@ -351,9 +354,8 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     ly.peer_tiles = take(n * (int64_t)sizeof(DevTile));
   }
   ly.rects = take((int64_t)p.rects.size() * (int64_t)sizeof(DevRect));
-  // peer-memory SP (orbit2_comm_*): barrier flags [2][R] u64 + error word, the push
-  // table (one entry per HALO SEND rectangle of every peer) and the signal pointers
-  ly.sig = take(2LL * c.world_size * 8 + 64);
+  // peer-memory SP (orbit2_comm_*): the push table (one entry per HALO SEND
+  // rectangle of every peer) and the peers' signal pointers
   {
     int64_t n = 0;
     for (int peer = 0; peer < c.world_size; ++peer) n += p.xfer[((size_t)ORBIT2_XFER_HALO * c.world_size + peer) * 2 + ORBIT2_SEND].count;
