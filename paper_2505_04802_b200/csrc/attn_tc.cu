@@ -28,7 +28,6 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
-#include <cstdlib>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -74,13 +73,6 @@ __device__ __forceinline__ void ffma2(float& a, float& b, float s, float t) {
       "mov.b64 {%0, %1}, x;\n\t}"
       : "+f"(a), "+f"(b)
       : "f"(s), "f"(t));
-}
-
-// max of three (sm_100a 3-input FMNMX)
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
 }
 
 // packed pair version: same arithmetic in f32x2 instructions (half the issue slots)
@@ -163,20 +155,6 @@ constexpr bool kTailSkip = ORBIT2_ATTN_TAILSKIP != 0;
 // exponential phases then interleave with each other's row-max / wait phases
 // instead of colliding on the MUFU (0 = both start together).
 constexpr int kDesync = ORBIT2_ATTN_DESYNC;
-#ifndef ORBIT2_ATTN_LAZYMAX
-#define ORBIT2_ATTN_LAZYMAX 1
-#endif
-// Row max folded into the exponential pass (blocks j >= 1): p = 2^(s c - m_ref) is
-// computed against the current reference max while the same pass takes the row max
-// of s c - m_ref (one 3-input FMNMX per pair, issue slots the MUFU-bound loop has
-// spare).  A row whose block max exceeds the reference by more than kRescaleLog2
-// moves its reference at the NEXT block (O and l rescaled once PV_j is done: P_j,
-// O and l all stay relative to the same reference, so O / l is unchanged); a block
-// max more than kLazyLimit above it (p would leave the range the exponentials are
-// exact in) is recomputed against the new max before P is released.  Removes the
-// separate row-max pass (~370 of ~850 non-exponential cycles per block).
-constexpr bool kLazyMax = ORBIT2_ATTN_LAZYMAX != 0;
-constexpr float kLazyLimit = 64.0f;
 
 template <int DH, int NQ>
 struct AttnCfg {
@@ -284,7 +262,7 @@ template <int DH, int NQ>
 __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
                    __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
-                   int heads, int n_items, long long* __restrict__ tl, int lazy_max) {
+                   int heads, int n_items, long long* __restrict__ tl) {
   // tl: optional debug timeline (clock64 stamps of CTA 0), null in production
   using C = AttnCfg<DH, NQ>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -555,8 +533,6 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         continue;
       }
       float m_ref = -INFINITY, l_run = 0.f;
-      float m_pend = -INFINITY;   // lazy max: the reference the next block moves to
-      bool pend = false;          // (warp-uniform) a row of this warp moves its reference
       const bool tlr = q == 0 && lane == 0 && hh == 0;
       // Only rows inside the tile take part in the (warp-uniform) range votes, so
       // results do not depend on packing, chunking or the rank assignment.
@@ -627,11 +603,9 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         };
         if (!kLatePvWait)
           for (int h = 0; h < C::NPH; ++h) wait_pv(h);
-        // lazy: decisions after the pass (no-ops at j = 0, where m_ref is the exact max)
-        const bool lazy = kLazyMax && SPW == 1 && C::P_TMEM && C::NPH == 1 && !kPingPong && lazy_max;
-        if (!lazy || j == 0) {
-          // Conditional rescale (R18): the reference max moves only when the block max
-          // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
+        // Conditional rescale (R18): the reference max moves only when the block max
+        // exceeds it by more than kRescaleLog2 (p <= 2^8, the O rescale is rare).
+        {
           const float m_blk = row_max();
           if (j == 0)
             m_ref = m_blk;
@@ -639,17 +613,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             for (int h = 0; h < C::NPH; ++h) wait_pv(h);
             rescale(fmaxf(m_blk, m_ref));
           }
-        } else if (pend) {   // move the reference decided by the previous block (PV_{j-1} done)
-          for (int h = 0; h < C::NPH; ++h) wait_pv(h);
-          rescale(fmaxf(m_pend, m_ref));
-          pend = false;
         }
         if (tlr) TL_STAMP(qt, cs, 3);
         // p = 2^(s * log2(e)/sqrt(d) - m_ref) -> bf16 P (TMEM: A operand of the PV MMA;
         // smem when TMEM is short), part by part, with fp32 row sums
         constexpr int KP = KC / C::NPH;                // keys per part
         float rs0 = 0.f, rs1 = 0.f;
-        (void)m_pend;
         if constexpr (kPingPong) pp_sync(1 + qt);   // this tile's turn on the MUFU
         // first block of an item with both Q tiles active: offset the two tiles'
         // exponential phases (named barrier of this sub-partition's two warps)
@@ -662,56 +631,26 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         for (int h = 0; h < C::NPH; ++h) {
           wait_pv(h);
           if constexpr (C::P_TMEM) {
-            // one exponential pass over the block (optionally taking the row max of
-            // s c - m_ref on the side: lazy max)
-            auto exp_pass = [&]() {
-              float mx = -INFINITY;
-              rs0 = 0.f;
-              rs1 = 0.f;
 #pragma unroll
-              for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
-                if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // half past the tile end
-                uint32_t pk[32];
-                float2 rs = make_float2(0.f, 0.f);
+            for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
+              if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // half past the tile end
+              uint32_t pk[32];
+              float2 rs = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int e = 0; e < 64; e += 2) {
-                  float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
-                  ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
-                  mx = fmax3(mx, x0, x1);   // the lazy row max (unused otherwise: cheap, no branch)
-                  float2 pr;
-                  if ((e & 15) < kPolyPer16) pr = ex2_poly2(x0, x1);
-                  else pr = make_float2(ex2(x0), ex2(x1));
-                  rs = tc::add2(rs, pr);                     // packed row-sum accumulation
-                  pk[e / 2] = tc::pack_bf16(pr.x, pr.y);     // column = keys (2c, 2c+1), lower key in low half
-                }
-                rs0 += rs.x;
-                rs1 += rs.y;
-                tc::tmem_st32(p_tm + c0 / 2, pk);
-                if (desync && qt == 0 && c0 == c_arr) asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
+              for (int e = 0; e < 64; e += 2) {
+                float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
+                ffma2(x0, x1, sl, -m_ref);                 // FFMA2: both (s*c - m) in one instruction
+                float2 pr;
+                if ((e & 15) < kPolyPer16) pr = ex2_poly2(x0, x1);
+                else pr = make_float2(ex2(x0), ex2(x1));
+                rs = tc::add2(rs, pr);                     // packed row-sum accumulation
+                pk[e / 2] = tc::pack_bf16(pr.x, pr.y);     // column = keys (2c, 2c+1), lower key in low half
               }
-              return mx;
-            };
-            // one copy of the pass (a second, rare iteration redoes the block when p
-            // left the exact range: the reference is moved first -- PV_{j-1} is done)
-            bool again;
-            do {
-              const float mx = exp_pass();
-              again = false;
-              // opaque re-read of the switch: keeps the compiler from unswitching the
-              // loop into two copies of the (register-heavy) exponential pass
-              int lz;
-              asm volatile("mov.b32 %0, %1;" : "=r"(lz) : "r"((int)lazy));
-              if (lz) {
-                if (__any_sync(0xffffffffu, row_valid && mx > kLazyLimit)) {
-                  tc::tmem_st_wait();
-                  rescale(fmaxf(m_ref + mx, m_ref));   // mx <= 0 after this for every row
-                  again = true;
-                } else if (__any_sync(0xffffffffu, row_valid && mx > kRescaleLog2)) {
-                  pend = true;
-                  m_pend = m_ref + fmaxf(mx, 0.f);
-                }
-              }
-            } while (again);
+              rs0 += rs.x;
+              rs1 += rs.y;
+              tc::tmem_st32(p_tm + c0 / 2, pk);
+              if (desync && qt == 0 && c0 == c_arr) asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
+            }
             if (desync && qt == 0 && kTailSkip && kv_blk <= c_arr)   // loop left before c_arr: still release
               asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
             tc::tmem_st_wait();
@@ -857,11 +796,8 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (n_items == 0) return true;
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM
-  // ORBIT2_ATTN_EAGER_MAX=1: the separate row-max pass for every block (A/B and tests)
-  const char* eager = std::getenv("ORBIT2_ATTN_EAGER_MAX");
-  const int lazy = eager && eager[0] == '1' ? 0 : 1;
   attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, tmo, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
-                                                             heads, (int)n_items, g_attn_timeline, lazy);
+                                                             heads, (int)n_items, g_attn_timeline);
   return true;
 }
 
