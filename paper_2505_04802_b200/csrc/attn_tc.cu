@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "tc_common.cuh"
@@ -806,7 +807,12 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
 bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B, int D,
                          int heads, int d, cudaStream_t st) {
   if (d == 32) return launch_dh<32>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
-  if (d == 64) return launch_dh<64>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+  if (d == 64) {
+    // ORBIT2_ATTN2=1: the two-Q-tile / 128-key kernel below instead of attn3_tc.cu
+    const char* e = std::getenv("ORBIT2_ATTN2");
+    if (!(e && e[0] == '1')) return launch_attention3_tc(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+    return launch_dh<64>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+  }
   if (d == 128) return launch_dh<128>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
   return false;
 }

@@ -57,6 +57,9 @@ struct ChunkDev {
   const int32_t* qpair_core;   // last block: (tile << 16 | first block << 1 | blocks - 1) holding core tokens
   int32_t qc0, nqc;
   int32_t core_pairs;          // attention over qpair_core instead of every pair
+  const int32_t* qg3;          // groups of 3 query blocks (tile << 16 | first block << 2 | blocks - 1)
+  const int32_t* qg3c;         // last block: groups holding core tokens
+  int32_t qg0, nqg, qgc0, nqgc;
   const int32_t* core_row;
 };
 
@@ -106,6 +109,9 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
                     int64_t K, const EpiParams& ep, cudaStream_t st);
 bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B,
                          int D, int heads, int d, cudaStream_t st);
+// head dim 64: three Q tiles per CTA on 64-key blocks (attn3_tc.cu)
+bool launch_attention3_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B, int D,
+                          int heads, cudaStream_t st);
 
 // Fused MLP for D = 256: z += W2 GELU(W1 x + b1) + b2 (hidden stays on chip).
 bool launch_mlp_fused(const void* xn, int64_t rows_alloc, const void* w1, const float* b1, const void* w2,

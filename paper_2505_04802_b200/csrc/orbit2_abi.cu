@@ -138,6 +138,12 @@ ChunkDev chunk_dev(const Ctx* c, const Chunk& ch) {
   d.qpair_core = c->at<int32_t>(p.lay.qpair_core);
   d.qc0 = ch.qc0;
   d.nqc = ch.nqc;
+  d.qg3 = c->at<int32_t>(p.lay.qg3);
+  d.qg3c = c->at<int32_t>(p.lay.qg3c);
+  d.qg0 = ch.qg0;
+  d.nqg = ch.nqg;
+  d.qgc0 = ch.qgc0;
+  d.nqgc = ch.nqgc;
   d.core_pairs = 0;
   d.core_row = c->at<int32_t>(p.lay.core_row);
   return d;
@@ -227,6 +233,10 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
     e = cudaMemcpy(c->at<void>(p.lay.qblk_tile), p.qblk_tile.data(), p.qblk_tile.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qpair_tile.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qpair_tile), p.qpair_tile.data(), p.qpair_tile.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.qg3.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.qg3), p.qg3.data(), p.qg3.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !p.qg3c.empty())
+    e = cudaMemcpy(c->at<void>(p.lay.qg3c), p.qg3c.data(), p.qg3c.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !p.qpair_core.empty())
     e = cudaMemcpy(c->at<void>(p.lay.qpair_core), p.qpair_core.data(), p.qpair_core.size() * 4, cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMemset(c->at<void>(p.lay.sig), 0, 2ULL * p.cfg.world_size * 8 + 64);

@@ -37,12 +37,14 @@ struct Chunk {
   int32_t qb0, nqb;           // query blocks (per sample) of the chunk
   int32_t qp0, nqp;           // query-block pairs (per sample) of the chunk
   int32_t qc0, nqc;           // last block: query-block pairs holding core tokens (per sample)
+  int32_t qg0, nqg, qgc0, nqgc;  // groups of 3 query blocks: all / holding core tokens (per sample)
 };
 
 // Byte offsets of the workspace regions (from the workspace base).
 struct Layout {
   int64_t rowinfo, patches, z, xn, qkv, ao, hid, hin;
   int64_t tiles, qblk_tile, qpair_tile, qpair_core, core_row, pos_u, pos_w, cmap, peer_tiles, rects;
+  int64_t qg3, qg3c;
   int64_t core_rblk;          // last block: 128-row blocks holding core tokens (unchunked call)
   int64_t sig, push, sigtab;  // peer-memory SP: barrier flags, push table, peers' flag pointers
   int64_t total;
@@ -77,6 +79,10 @@ struct Plan {
   // entry = local tile index << 16 | first query block << 1 | (blocks - 1)
   std::vector<int32_t> qpair_core;
   std::vector<int32_t> qpc_off;         // per local tile (+ sentinel): first qpair_core entry
+  // groups of 3 query blocks (attention at head dim 64: three Q tiles share each
+  // 64-key K/V block); entry = local tile << 16 | first block << 2 | (blocks - 1)
+  std::vector<int32_t> qg3, qg3_off;    // every group; per local tile (+ sentinel) first entry
+  std::vector<int32_t> qg3c, qg3c_off;  // last block: groups holding core tokens
   std::vector<int32_t> core_row;        // local core token -> local padded token index
   // last block (R16) of a call over every rank-local tile (all B samples): the
   // 128-row blocks of the packed token rows that hold core tokens (block tail)

@@ -174,13 +174,17 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       const int32_t c_last = (dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w + (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
       p.qpc_off.push_back((int32_t)p.qpair_core.size());
       const int32_t b0 = c_first / kQBlock, b1 = c_last / kQBlock;   // query blocks with core tokens
-      if (li >= 32768 || b1 >= 32768) {   // entry packing: tile index < 2^15, first block < 2^15
-        if (msg) *msg = "tiles: more than 32767 tiles per rank or 32767 query blocks per tile (tile index / "
-                        "block packing of the last-block query list)";
+      if (li >= 32768 || nqb > 16384) {   // entry packing: tile index < 2^15, first block < 2^14
+        if (msg) *msg = "tiles: more than 32767 tiles per rank or 16384 query blocks per tile (tile index / "
+                        "block packing of the attention work lists)";
         return ORBIT2_E_UNSUPPORTED;
       }
       for (int32_t b = b0; b <= b1; b += 2)                           // entry: tile, first block, count - 1
         p.qpair_core.push_back((li << 16) | (b << 1) | (b + 1 <= b1 ? 1 : 0));
+      p.qg3_off.push_back((int32_t)p.qg3.size());
+      p.qg3c_off.push_back((int32_t)p.qg3c.size());
+      for (int32_t b = 0; b < nqb; b += 3) p.qg3.push_back((li << 16) | (b << 2) | (std::min(3, nqb - b) - 1));
+      for (int32_t b = b0; b <= b1; b += 3) p.qg3c.push_back((li << 16) | (b << 2) | (std::min(3, b1 + 1 - b) - 1));
     }
     for (int32_t u = 0; u < dt.core_h; ++u)
       for (int32_t w = 0; w < dt.core_w; ++w)
@@ -197,6 +201,8 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     p.dev.push_back(dt);
   }
   p.qpc_off.push_back((int32_t)p.qpair_core.size());
+  p.qg3_off.push_back((int32_t)p.qg3.size());
+  p.qg3c_off.push_back((int32_t)p.qg3c.size());
   // sentinel entry (offsets one past the end) simplifies chunk arithmetic
   {
     DevTile end{};
@@ -343,6 +349,8 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.qblk_tile = take((int64_t)p.qblk_tile.size() * 4);
   ly.qpair_tile = take((int64_t)p.qpair_tile.size() * 4);
   ly.qpair_core = take((int64_t)p.qpair_core.size() * 4);
+  ly.qg3 = take((int64_t)p.qg3.size() * 4);
+  ly.qg3c = take((int64_t)p.qg3c.size() * 4);
   ly.core_rblk = take((ly.mrow / kQBlock + 1) * 4);
   ly.core_row = take((int64_t)p.core_row.size() * 4);
   ly.pos_u = take((int64_t)(p.Hp + 2 * h) * (p.D / 2) * 4);
@@ -432,6 +440,10 @@ Chunk make_chunk(const Plan& p, int32_t tb, int32_t tc) {
   ch.nqp = p.dev[tb + tc].qp_off - ch.qp0;
   ch.qc0 = p.qpc_off[tb];
   ch.nqc = p.qpc_off[tb + tc] - ch.qc0;
+  ch.qg0 = p.qg3_off[tb];
+  ch.nqg = p.qg3_off[tb + tc] - ch.qg0;
+  ch.qgc0 = p.qg3c_off[tb];
+  ch.nqgc = p.qg3c_off[tb + tc] - ch.qgc0;
   return ch;
 }
 
