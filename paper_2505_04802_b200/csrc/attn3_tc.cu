@@ -44,7 +44,10 @@ constexpr int RB = DH * 2;              // bytes per smem row (one 128-byte swiz
 constexpr int QT = 128 * RB;            // bytes of a Q tile (128 rows)
 constexpr int KVT = KB * RB;            // bytes of a K or V block
 constexpr int QBUF = 2;                 // Q tile sets (the next item's Q is prefetched)
-constexpr int KST = 3, VST = 3;         // K / V ring slots
+#ifndef ORBIT2_ATTN3_KVST
+#define ORBIT2_ATTN3_KVST 3
+#endif
+constexpr int KST = ORBIT2_ATTN3_KVST, VST = ORBIT2_ATTN3_KVST;   // K / V ring slots
 constexpr int TCOLS = KB + DH + KB / 2; // S | O | P per Q tile (160)
 constexpr int CTRL_WARPS = 4;           // producer + 3 MMA issuers (one warpgroup)
 constexpr int THREADS = 32 * CTRL_WARPS + 128 * NQ;   // 512
@@ -52,7 +55,13 @@ constexpr int OST_WARP = 32 * RB;       // epilogue staging per softmax warp (32
 constexpr int IRING = 4;
 constexpr int SMEM = QBUF * NQ * QT + (KST + VST) * KVT + 4 * NQ * OST_WARP + 1024 + 512;
 constexpr float kRescaleLog2 = 8.0f;    // conditional rescale threshold (attn_tc.cu)
-constexpr int kPolyPer16 = 2;           // exponentials per 16 on the FMA pipe
+#ifndef ORBIT2_ATTN3_POLY
+#define ORBIT2_ATTN3_POLY 2
+#endif
+constexpr int kPolyPer16 = ORBIT2_ATTN3_POLY;   // exponentials per 16 on the FMA pipe
+#ifndef ORBIT2_ATTN3_REGREALLOC
+#define ORBIT2_ATTN3_REGREALLOC 1
+#endif
 static_assert(NQ * TCOLS <= 512, "TMEM");
 static_assert(SMEM <= 227 * 1024, "shared memory");
 
@@ -119,7 +128,18 @@ __device__ __forceinline__ Item take_item(const Item* sItem, uint64_t* it_full, 
 __global__ void __launch_bounds__(THREADS, 1)
     attn3_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv,
                     const __grid_constant__ CUtensorMap tmo, __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
-                    int heads, int n_items) {
+                    int heads, int n_items, long long* __restrict__ tl) {
+  // tl: debug timeline (-DORBIT2_ATTN3_TIMELINE): clock64 of CTA 0, [role][block][event]
+#ifdef ORBIT2_ATTN3_TIMELINE
+#define TL3(role, blk, ev)                                                                        \
+  do {                                                                                            \
+    if (tl != nullptr && blockIdx.x == 0 && (blk) < 64) tl[((role) * 64 + (blk)) * 8 + (ev)] = clock64(); \
+  } while (0)
+#else
+#define TL3(role, blk, ev) \
+  do {                     \
+  } while (0)
+#endif
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                               // [QBUF][NQ][QT]
@@ -182,8 +202,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // the control warpgroup needs few registers: give them to the softmax warpgroups
-  if (warp < CTRL_WARPS) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
-  else asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
+  if (ORBIT2_ATTN3_REGREALLOC) {
+    if (warp < CTRL_WARPS) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;" ::: "memory");
+    else asm volatile("setmaxnreg.inc.sync.aligned.u32 152;" ::: "memory");
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -241,7 +263,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t st = gk % KST;
         tc::mbar_wait(&k_full[st], (gk / KST) & 1);
         if (active) {
+          if (lane == 0) TL3(3 + qt, ns, 0);
           if (ns >= 1) tc::mbar_wait(&s_free[qt], (ns - 1) & 1);
+          if (lane == 0) TL3(3 + qt, ns, 1);
           tc::tc_fence_after();
           if (tc::elect_one()) {
             const uint64_t qd0 = tc::sdesc(q_addr + (qb * NQ + qt) * QT, 16, 8 * RB, tc::SW_128B);
@@ -272,7 +296,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (active) {
           if (j == 0 && ni >= 1) tc::mbar_wait(&o_free[qt], (ni - 1) & 1);
           const uint64_t vd0 = tc::sdesc(v_addr + st * KVT, KVT, 8 * RB, tc::SW_128B);
+          if (lane == 0) TL3(3 + qt, np, 2);
           tc::mbar_wait(&p_full[qt], np & 1);
+          if (lane == 0) TL3(3 + qt, np, 3);
           tc::tc_fence_after();
           if (tc::elect_one()) {
 #pragma unroll
@@ -307,8 +333,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (qt >= it.nq) continue;
       float m_ref = -INFINITY, l_run = 0.f;
       const bool row_valid = it.q0 + qt * 128 + i < it.n;
+      const bool tlr = q == 0 && lane == 0;
       for (int j = 0; j < it.nkb; ++j, ++cs) {
+        if (tlr) TL3(qt, cs, 0);
         tc::mbar_wait(&s_full[qt], cs & 1);
+        if (tlr) TL3(qt, cs, 1);
         tc::tc_fence_after();
         float sv[KB];
         {
@@ -319,6 +348,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tc::tc_fence_before();
         tc::mbar_arrive(&s_free[qt]);
+        if (tlr) TL3(qt, cs, 2);
         const int kvalid = it.n - j * KB;
         if (kvalid < KB) {
 #pragma unroll
@@ -365,7 +395,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           m_ref = m_new;
         }
+        if (tlr) TL3(qt, cs, 3);
         wait_pv();
+        if (tlr) TL3(qt, cs, 4);
         // p = 2^(s log2(e)/sqrt(d) - m_ref) -> bf16 P in TMEM (A operand of PV), fp32 row sums
         uint32_t pk[KB / 2];
         float2 rs = make_float2(0.f, 0.f);
@@ -383,6 +415,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tmem_st_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
+        if (tlr) TL3(qt, cs, 5);
         l_run += rs.x + rs.y;
       }
       // epilogue: O / l  (wait for the item's last PV)
@@ -438,6 +471,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 }  // namespace
 
+extern long long* g_attn_timeline;   // attn_tc.cu: set by orbit2_debug_attn_timeline
+
 bool launch_attention3_tc(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int B, int D, int heads,
                           cudaStream_t st) {
   CUtensorMap tmq, tmkv, tmo;
@@ -451,7 +486,7 @@ bool launch_attention3_tc(const void* qkv, int64_t rows, void* out, const ChunkD
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, num_sms());
   attn3_tc_kernel<<<grid, THREADS, SMEM, st>>>(tmq, tmkv, tmo, reinterpret_cast<__nv_bfloat16*>(out), ch, D, heads,
-                                               (int)n_items);
+                                               (int)n_items, g_attn_timeline);
   return true;
 }
 
