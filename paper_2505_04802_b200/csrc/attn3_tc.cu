@@ -59,6 +59,9 @@ constexpr float kRescaleLog2 = 8.0f;    // conditional rescale threshold (attn_t
 #define ORBIT2_ATTN3_POLY 2
 #endif
 constexpr int kPolyPer16 = ORBIT2_ATTN3_POLY;   // exponentials per 16 on the FMA pipe
+#ifndef ORBIT2_ATTN3_DESYNC_CLK
+#define ORBIT2_ATTN3_DESYNC_CLK 0
+#endif
 #ifndef ORBIT2_ATTN3_REGREALLOC
 #define ORBIT2_ATTN3_REGREALLOC 1
 #endif
@@ -396,6 +399,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           m_ref = m_new;
         }
         if (tlr) TL3(qt, cs, 3);
+        if (ORBIT2_ATTN3_DESYNC_CLK > 0 && j == 0 && qt > 0) {
+          // stagger the Q tiles' exponential phases at the start of an item
+          const long long t0 = clock64();
+          while (clock64() - t0 < (long long)qt * ORBIT2_ATTN3_DESYNC_CLK) {
+          }
+        }
         wait_pv();
         if (tlr) TL3(qt, cs, 4);
         // p = 2^(s log2(e)/sqrt(d) - m_ref) -> bf16 P in TMEM (A operand of PV), fp32 row sums

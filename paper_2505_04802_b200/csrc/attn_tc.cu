@@ -808,9 +808,14 @@ bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16,
                          int heads, int d, cudaStream_t st) {
   if (d == 32) return launch_dh<32>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
   if (d == 64) {
-    // ORBIT2_ATTN2=1: the two-Q-tile / 128-key kernel below instead of attn3_tc.cu
-    const char* e = std::getenv("ORBIT2_ATTN2");
-    if (!(e && e[0] == '1')) return launch_attention3_tc(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+    // Short tiles (mean under 768 tokens, e.g. C3's 312-432): three Q tiles on 64-key
+    // blocks (attn3_tc.cu; less padding of the last key block, three softmax warps per
+    // sub-partition): measured 12.4 vs 14.8 ms at C3.  Long tiles (C2 / C4 / C5):
+    // this kernel (19.0 vs 19.3-19.7 ms at C2).  ORBIT2_ATTN=2 / 3 forces one.
+    const char* e = std::getenv("ORBIT2_ATTN");
+    const int64_t mean_n = ch.tc > 0 ? ch.chunk_tokens / ch.tc : 0;
+    const bool use3 = e && e[0] == '3' ? true : (e && e[0] == '2' ? false : mean_n < 768);
+    if (use3) return launch_attention3_tc(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
     return launch_dh<64>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
   }
   if (d == 128) return launch_dh<128>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
