@@ -335,3 +335,18 @@ def test_repeated_small_batch_forwards_bit_identical():
         torch.cuda.synchronize()
         assert torch.equal(out, first)
 
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["2", "3"])
+def test_both_attention_kernels_match_oracle(kernel, monkeypatch):
+    """Head dim 64 has two attention kernels (two Q tiles on 128-key blocks; three
+    Q tiles on 64-key blocks, chosen by mean tile length).  Both, forced, against
+    the oracle on ragged > 128-token tiles, and bit-identical across chunkings."""
+    monkeypatch.setenv("ORBIT2_ATTN", kernel)
+    w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    got = run_cuda(w, x, blob, BF16)
+    e = rel_err(got, oracle_full(w, x, blob)[0])
+    print(f"attention kernel {kernel}: rel_err={e:.3e}")
+    assert e <= BF16_TOL
+    assert np.array_equal(got, run_cuda(w, x, blob, BF16, chunk_tiles=1))
