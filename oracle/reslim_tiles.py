@@ -23,6 +23,11 @@ What is computed (the method, step by step, in the paper's order):
   O5 head      -- LN_f + linear decoder head   P:480, R10, R11
   O6 stitch    -- halo outputs discarded, cores placed   P:532, R16
   O7 residual  -- bilinear upsample added      P:487-498 [Residual Learning], R12, R13
+  O8 residual convolutional path (optional, res_hidden > 0) -- P:498 "the residual
+                  convolutional path reintroduces upsampling outside the main ViT
+                  path, using lightweight convolutional layers", reading R31:
+                  res = up + conv_b(GELU(conv_a(up))), 3x3 convolutions, zero
+                  padding outside the high-resolution field
 
 Everything is float64.  fp32 inputs and weights are promoted exactly.
 Library primitives used as single steps: numpy matmul, numpy exp, scipy erf.
@@ -272,9 +277,31 @@ def upsample_bilinear(plane: np.ndarray, s: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# O8  Residual convolutional path (reading R31)
+# ---------------------------------------------------------------------------
+def conv3x3(x: np.ndarray, Wc: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """y[o, Y, X] = b[o] + sum_{i, dy, dx} Wc[o, i, dy, dx] x[i, Y + dy - 1, X + dx - 1],
+    x taken as 0 outside its extent (zero padding)."""
+    Cin, Y, X = x.shape
+    xp = np.zeros((Cin, Y + 2, X + 2))
+    xp[:, 1:-1, 1:-1] = x
+    out = np.zeros((Wc.shape[0], Y, X)) + np.asarray(b, np.float64)[:, None, None]
+    for dy in range(3):
+        for dx in range(3):
+            out += np.einsum("oi,iyx->oyx", Wc[:, :, dy, dx], xp[:, dy:dy + Y, dx:dx + X])
+    return out
+
+
+def residual_conv(up: np.ndarray, Wt: dict) -> np.ndarray:
+    """res = up + conv_b(GELU(conv_a(up))) over a [K, Y, X] field (R31)."""
+    return up + conv3x3(gelu(conv3x3(up, Wt["W_ra"], Wt["b_ra"])), Wt["W_rb"], Wt["b_rb"])
+
+
+# ---------------------------------------------------------------------------
 # Canonical weight blob -> named fp64 arrays (order: include/orbit2.h, restated here)
 # ---------------------------------------------------------------------------
-def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int) -> dict:
+def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int, K: int = 0,
+                   res_hidden: int = 0) -> dict:
     blob = np.asarray(blob, dtype=np.float64)
     F = 4 * D
     off = 0
@@ -298,6 +325,9 @@ def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int) -> d
         Wt["layers"].append(Lw)
     Wt["lnf_g"], Wt["lnf_b"] = take(D), take(D)
     Wt["W_h"], Wt["b_h"] = take(n_head, D), take(n_head)
+    if res_hidden:   # O8: W_ra[C_r][K][3][3], b_ra[C_r], W_rb[K][C_r][3][3], b_rb[K]
+        Wt["W_ra"], Wt["b_ra"] = take(res_hidden, K, 3, 3), take(res_hidden)
+        Wt["W_rb"], Wt["b_rb"] = take(K, res_hidden, 3, 3), take(K)
     if off != blob.size:
         raise ValueError(f"weight blob has {blob.size} values, layout needs {off}")
     return Wt
@@ -324,12 +354,14 @@ class Problem:
     heads: int
     halo_mode: int = HALO_CLAMP
     channel_map: tuple | None = None
+    res_hidden: int = 0      # O8 hidden channels (0: no residual convolutions)
 
     @classmethod
     def from_config(cls, cfg) -> "Problem":
         return cls(cfg.H, cfg.W, cfg.V, cfg.K, cfg.scale, cfg.patch, cfg.tiles_y, cfg.tiles_x,
                    cfg.halo, cfg.embed, cfg.depth, cfg.heads, cfg.halo_mode,
-                   tuple(cfg.out_channel_map) if cfg.out_channel_map is not None else None)
+                   tuple(cfg.out_channel_map) if cfg.out_channel_map is not None else None,
+                   getattr(cfg, "res_hidden", 0))
 
     @property
     def P(self) -> int:
@@ -344,7 +376,7 @@ class Problem:
 
     def weights(self, blob) -> dict:
         return unpack_weights(blob, self.embed, self.depth, self.V * self.patch ** 2,
-                              self.K * self.P * self.P)
+                              self.K * self.P * self.P, self.K, self.res_hidden)
 
 
 def tile_forward(x_b: np.ndarray, tile: Tile, pr: Problem, Wt: dict) -> np.ndarray:
@@ -355,8 +387,10 @@ def tile_forward(x_b: np.ndarray, tile: Tile, pr: Problem, Wt: dict) -> np.ndarr
     return head(z[core_rows(tile)], Wt)
 
 
-def residual_up(x_b: np.ndarray, pr: Problem) -> np.ndarray:
-    return np.stack([upsample_bilinear(x_b[m], pr.scale) for m in pr.cmap()])
+def residual_up(x_b: np.ndarray, pr: Problem, Wt: dict | None = None) -> np.ndarray:
+    """The residual path over the whole field: O7 upsample (+ O8 convolutions)."""
+    up = np.stack([upsample_bilinear(x_b[m], pr.scale) for m in pr.cmap()])
+    return residual_conv(up, Wt) if pr.res_hidden else up
 
 
 def tiles_forward(x: np.ndarray, blob: np.ndarray, pr: Problem, tile_order=None,
@@ -375,7 +409,7 @@ def tiles_forward(x: np.ndarray, blob: np.ndarray, pr: Problem, tile_order=None,
     for b in range(B):
         for t in order:
             stitch_tile(out_vit[b], tile_forward(x[b], tiles[t], pr, Wt), tiles[t], pr.K, pr.P)
-        up[b] = residual_up(x[b], pr)
+        up[b] = residual_up(x[b], pr, Wt)
     out = out_vit + up
     return (out, out_vit, up) if return_parts else out
 
@@ -395,7 +429,18 @@ def tiles_forward_sampled(x_b: np.ndarray, blob: np.ndarray, pr: Problem, tile_i
             pr.K, ch * pr.P, cw * pr.P)
         ys = slice(tile.core_y0 * pr.P, tile.core_y1 * pr.P)
         xs = slice(tile.core_x0 * pr.P, tile.core_x1 * pr.P)
-        up = np.stack([upsample_bilinear_region(x_b[m], pr.scale, ys, xs) for m in pr.cmap()])
+        if pr.res_hidden:
+            # O8 needs up within 2 output pixels of the rectangle: evaluate O7 on the
+            # rectangle grown by 2 (clipped to the field, where zero padding applies),
+            # convolve, keep the centre
+            sH, sW = pr.scale * pr.H, pr.scale * pr.W
+            y0, y1 = max(0, ys.start - 2), min(sH, ys.stop + 2)
+            x0, x1 = max(0, xs.start - 2), min(sW, xs.stop + 2)
+            upx = np.stack([upsample_bilinear_region(x_b[m], pr.scale, slice(y0, y1), slice(x0, x1))
+                            for m in pr.cmap()])
+            up = residual_conv(upx, Wt)[:, ys.start - y0:ys.stop - y0, xs.start - x0:xs.stop - x0]
+        else:
+            up = np.stack([upsample_bilinear_region(x_b[m], pr.scale, ys, xs) for m in pr.cmap()])
         res[t] = (ys, xs, vit + up, vit)
     return res
 
@@ -416,7 +461,7 @@ def global_forward(x: np.ndarray, blob: np.ndarray, pr: Problem) -> np.ndarray:
             z = block(z, Lw, pr.heads)
         g = head(z, Wt)
         out[b] = g.reshape(Hp, Wp, K, P, P).transpose(2, 0, 3, 1, 4).reshape(K, Hp * P, Wp * P)
-        out[b] += residual_up(x[b], pr)
+        out[b] += residual_up(x[b], pr, Wt)
     return out
 
 

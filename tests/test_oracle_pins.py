@@ -35,11 +35,11 @@ def small_problem(**kw):
     return O.Problem(**base)
 
 
-def blob_for(pr, seed=7, head_gain=1.0, sharp=True):
+def blob_for(pr, seed=7, head_gain=1.0, sharp=True, res_gain=1.0):
     cfg = get_config("C1", H=pr.H, W=pr.W, V=pr.V, K=pr.K, scale=pr.scale, patch=pr.patch,
                      tiles_y=pr.tiles_y, tiles_x=pr.tiles_x, halo=pr.halo, embed=pr.embed,
-                     depth=pr.depth, heads=pr.heads, halo_mode=pr.halo_mode)
-    return make_weights(cfg, seed=seed, head_gain=head_gain, sharp=sharp), cfg
+                     depth=pr.depth, heads=pr.heads, halo_mode=pr.halo_mode, res_hidden=pr.res_hidden)
+    return make_weights(cfg, seed=seed, head_gain=head_gain, sharp=sharp, res_gain=res_gain), cfg
 
 
 def input_for(cfg, batch=1, seed=11):
@@ -462,15 +462,17 @@ def test_golden_paper_sequence_lengths():
 
 
 # ---------------------------------------------------------------- sampled-tile oracle
+@pytest.mark.parametrize("res_hidden", [0, 4])
 @pytest.mark.parametrize("mode", [O.HALO_CLAMP, O.HALO_REPLICATE])
-def test_sampled_tiles_equal_full_forward_restricted(mode):
+def test_sampled_tiles_equal_full_forward_restricted(mode, res_hidden):
     """tiles_forward_sampled (which supplies every C3/C4/C5 expected value) is
     tiles_forward restricted to the tile's core output rectangle, bit for bit,
     for EVERY tile of a 3 x 3 problem (the core outputs of a tile are
     stitched into exactly its core rectangle; the residual is the same O7
     formula evaluated on that rectangle).  A wrong core slice, reshape or
     bilinear window in the sampled path fails here."""
-    pr = small_problem(H=36, W=44, tiles_y=3, tiles_x=3, halo=2, halo_mode=mode, channel_map=(2, 0))
+    pr = small_problem(H=36, W=44, tiles_y=3, tiles_x=3, halo=2, halo_mode=mode, channel_map=(2, 0),
+                       res_hidden=res_hidden)
     blob, cfg = blob_for(pr)
     x = input_for(cfg, batch=2)
     full, full_vit, _ = O.tiles_forward(x, blob, pr, return_parts=True)
@@ -483,7 +485,10 @@ def test_sampled_tiles_equal_full_forward_restricted(mode):
             tile = tiles[t]
             assert (ys.start, ys.stop) == (tile.core_y0 * pr.P, tile.core_y1 * pr.P)
             assert (xs.start, xs.stop) == (tile.core_x0 * pr.P, tile.core_x1 * pr.P)
-            assert np.array_equal(blk, full[b][:, ys, xs])
+            if res_hidden:   # O8 on a grown window: same sums, different array extents
+                np.testing.assert_allclose(blk, full[b][:, ys, xs], rtol=0, atol=1e-12)
+            else:
+                assert np.array_equal(blk, full[b][:, ys, xs])
             assert np.array_equal(vit, full_vit[b][:, ys, xs])
             if b == 0:
                 assert not covered[:, ys, xs].any()
@@ -534,3 +539,62 @@ def test_unpack_weights_marker_blob():
     assert np.array_equal(Wt["b_h"], rng(tail + 2 * D + Nh * D, Nh))
     with pytest.raises(ValueError):
         O.unpack_weights(np.zeros(total + 1), D, L, Din, Nh)
+
+
+# ---------------------------------------------------------------- O8 residual convolutions (R31)
+def test_conv3x3_matches_torch_conv2d():
+    """O8's 3x3 convolution (zero padding) is torch.nn.functional.conv2d(padding=1) in fp64."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((3, 11, 17))
+    Wc = rng.standard_normal((5, 3, 3, 3))
+    b = rng.standard_normal(5)
+    want = F.conv2d(torch.from_numpy(x)[None], torch.from_numpy(Wc), torch.from_numpy(b), padding=1)[0].numpy()
+    np.testing.assert_allclose(O.conv3x3(x, Wc, b), want, rtol=1e-12, atol=1e-12)
+    # one-hot kernel = shift: output[o, y, x] = x[i, y + 1, x - 1] inside, 0 past the edge
+    Wd = np.zeros((1, 3, 3, 3))
+    Wd[0, 1, 2, 0] = 1.0
+    got = O.conv3x3(x, Wd, np.zeros(1))[0]
+    assert np.array_equal(got[:-1, 1:], x[1, 1:, :-1]) and not got[-1].any() and not got[:, 0].any()
+
+
+def test_residual_conv_path_torch_model_and_init_contract():
+    """The whole pass with the residual convolutional path (T = 1, h = 0) equals an
+    untiled torch model (conv2d -> gelu -> conv2d on the interpolated field + identity
+    skip); zero second convolution -> the path is exactly the bilinear upsample (the
+    initialization contract: P:498 'high-resolution approximation' = the upsample)."""
+    pr = small_problem(tiles_y=1, tiles_x=1, halo=0, res_hidden=4)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg, batch=2)
+    Wt = pr.weights(blob)
+    got = O.tiles_forward(x, blob, pr)
+    import dataclasses
+    n_conv = 2 * 9 * 4 * pr.K + 4 + pr.K
+    base = torch_global_model(x, blob[:-n_conv], dataclasses.replace(pr, res_hidden=0))
+    xt = torch.from_numpy(x.astype(np.float64))
+    with torch.no_grad():
+        up = F.interpolate(xt[:, list(pr.cmap())], scale_factor=pr.scale, mode="bilinear", align_corners=False)
+        h = F.gelu(F.conv2d(up, torch.from_numpy(Wt["W_ra"]), torch.from_numpy(Wt["b_ra"]), padding=1))
+        conv = F.conv2d(h, torch.from_numpy(Wt["W_rb"]), torch.from_numpy(Wt["b_rb"]), padding=1)
+    np.testing.assert_allclose(got, base + conv.numpy(), rtol=1e-10, atol=1e-10)
+    z = blob.copy()
+    z[-(9 * 4 * pr.K + pr.K):] = 0.0          # W_rb, b_rb = 0
+    out, vit, res = O.tiles_forward(x, z, pr, return_parts=True)
+    up = np.stack([np.stack([O.upsample_bilinear(x[b][m], pr.scale) for m in pr.cmap()]) for b in range(2)])
+    assert np.array_equal(res, up)
+
+
+def test_residual_conv_locality():
+    """I5 with the convolutions: perturbing input pixels outside a tile's padded
+    rectangle leaves its core output unchanged (halo 1 patch = 2 px covers the
+    conv + bilinear support of ceil(2/s) + 1 = 2 coarse px at s = 4)."""
+    pr = small_problem(tiles_y=2, tiles_x=3, halo=1, res_hidden=4)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg)
+    t = pr.tiles()[4]
+    a = O.tiles_forward_sampled(x[0], blob, pr, [4])[4]
+    x2 = x.copy()
+    mask = np.ones(x.shape[2:], bool)
+    mask[max(0, t.pad_y0 * pr.patch):t.pad_y1 * pr.patch, max(0, t.pad_x0 * pr.patch):t.pad_x1 * pr.patch] = False
+    x2[0][:, mask] += 5.0
+    b2 = O.tiles_forward_sampled(x2[0], blob, pr, [4])[4]
+    assert np.array_equal(a[2], b2[2])

@@ -48,6 +48,7 @@ class Config:
     batch: int        # bench batch B
     halo_mode: int = 0          # 0 = CLAMP (reading R4), 1 = REPLICATE
     out_channel_map: tuple | None = None   # K entries in [0,V); None = identity
+    res_hidden: int = 0         # residual-path conv hidden channels (reading R31); 0 = none
 
     @property
     def mlp_hidden(self) -> int:
@@ -170,7 +171,10 @@ def ramp_input(cfg: Config, batch: int = 1) -> np.ndarray:
 def weight_count(cfg: Config) -> int:
     D, L, F = cfg.embed, cfg.depth, cfg.mlp_hidden
     per_layer = 2 * D + 3 * D * D + 3 * D + D * D + D + 2 * D + F * D + F + D * F + D
-    return cfg.din * D + 2 * D + L * per_layer + 2 * D + cfg.head_out * D + cfg.head_out
+    n = cfg.din * D + 2 * D + L * per_layer + 2 * D + cfg.head_out * D + cfg.head_out
+    if cfg.res_hidden:
+        n += 2 * 9 * cfg.res_hidden * cfg.K + cfg.res_hidden + cfg.K
+    return n
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:
@@ -183,7 +187,7 @@ def bf16_round(a: np.ndarray) -> np.ndarray:
 
 
 def make_weights(cfg: Config, seed: int | None = None, sharp: bool = True,
-                 head_gain: float = 1.0, round_bf16: bool = True) -> np.ndarray:
+                 head_gain: float = 1.0, round_bf16: bool = True, res_gain: float = 1.0) -> np.ndarray:
     """Flat fp32 canonical blob.
 
     W ~ N(0, 1/fan_in); biases ~ N(0, 0.02^2); LN gamma ~ 1+U(-0.1,0.1),
@@ -223,6 +227,9 @@ def make_weights(cfg: Config, seed: int | None = None, sharp: bool = True,
         lin(D, F); bias(D)                            # W_2, b_2
     ln(D)                                             # lnf
     lin(Nh, D, head_gain); bias(Nh)                   # W_h, b_h
+    if cfg.res_hidden:                                # residual convs W_ra, b_ra, W_rb, b_rb
+        lin(cfg.res_hidden, cfg.K * 9); bias(cfg.res_hidden)
+        lin(cfg.K, cfg.res_hidden * 9, res_gain); bias(cfg.K)
     blob = np.concatenate(parts).astype(np.float32)
     assert blob.size == weight_count(cfg)
     return bf16_round(blob) if round_bf16 else blob
