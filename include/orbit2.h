@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define ORBIT2_ABI_VERSION 1
+#define ORBIT2_ABI_VERSION 2   /* 2: res_hidden (residual convolutional path) */
 
 typedef enum {
   ORBIT2_OK = 0,
@@ -83,6 +83,9 @@ typedef struct {
   int32_t world_size;      /* ranks the tiles are partitioned over (>= 1) */
   int32_t rank;            /* 0 <= rank < world_size */
   int32_t chunk_tiles;     /* max rank-local tiles per forward/stitch call; 0 = all */
+  int32_t res_hidden;      /* residual convolutional path (reading R31): hidden
+                              channels C_r of res = up + conv_b(GELU(conv_a(up))), 3x3,
+                              0 <= C_r <= 64; 0 = the bilinear upsample alone */
   const int32_t *out_channel_map; /* K entries in [0,V) selecting the residual input
                                      channel of each output variable (R13); NULL = identity */
 } orbit2_config;
@@ -162,7 +165,9 @@ orbit2_status orbit2_create(const orbit2_config *cfg, void *workspace_dev, size_
  *     ln1_g[D] ln1_b[D] W_qkv[3D][D] (rows Q|K|V; head h = rows [h*d,(h+1)*d) of each)
  *     b_qkv[3D] W_o[D][D] b_o[D] ln2_g[D] ln2_b[D] W_1[4D][D] b_1[4D] W_2[D][4D] b_2[D]
  *   lnf_g[D] lnf_b[D] W_h[K*P*P][D] (row (k*P+a)*P+b, P = s*p) b_h[K*P*P]
- * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2, Din = V*p*p.
+ *   if res_hidden = C_r > 0: W_ra[C_r][K][3][3] b_ra[C_r] W_rb[K][C_r][3][3] b_rb[K]
+ * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2 (+ 18 C_r K + C_r + K),
+ * Din = V*p*p.
  * Stream-ordered; canonical_dev may be freed once the stream passes this call.
  */
 orbit2_status orbit2_prepare_weights(void *ctx, const float *canonical_dev, void *packed_dev,
@@ -188,7 +193,10 @@ orbit2_status orbit2_reslim_forward(void *ctx, const void *packed_w, const float
  * orbit2_stitch -- steps (4)-(5) for the same tile range: crop (halo outputs
  * were never formed), place the core outputs of tile_out_dev (layout above)
  * into out_dev fp32 [B][K][s*H][s*W], and add the bilinear (align_corners =
- * False, edge clamp; R12) x`s upsample of input channel out_channel_map[k].
+ * False, edge clamp; R12) x`s upsample of input channel out_channel_map[k] --
+ * with res_hidden > 0 the residual convolutional path up + conv_b(GELU(conv_a(up)))
+ * (R31; 3x3, zero padding outside the field; needs input pixels within
+ * ceil(2/s) + 1 of the cores, inside the padded rectangles whenever halo >= 1).
  * Writes exactly the output pixels of the requested tiles' cores; other
  * pixels of out_dev are untouched.  Stream-ordered.
  */

@@ -47,6 +47,7 @@ struct Layout {
   int64_t qg3, qg3c;
   int64_t core_rblk;          // last block: 128-row blocks holding core tokens (unchunked call)
   int64_t sig, push, sigtab;  // peer-memory SP: barrier flags, push table, peers' flag pointers
+  int64_t rconv;              // residual convolution weights (fp32; staged by prepare_weights)
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;            // K of the embedding GEMM: round_up(Din, 64)
@@ -120,10 +121,11 @@ struct LayerW {
 };
 struct WeightLayout {
   int64_t w_e, bias_e, lnf_g, lnf_b, w_h, b_h;
+  int64_t rconv;              // residual convolution weights (fp32 copy of the canonical tail)
   std::vector<LayerW> layers;
   int64_t total;
   // canonical (fp32 element) offsets, same names
-  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h;
+  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h, c_rconv;
   std::vector<LayerW> c_layers;
   int64_t c_total;
 };

@@ -55,6 +55,7 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
     return fail(msg, "world_size/rank: need 0 <= rank < world_size");
   if (c->chunk_tiles < 0) return fail(msg, "chunk_tiles: must be >= 0");
+  if (c->res_hidden < 0 || c->res_hidden > 64) return fail(msg, "res_hidden: must be in [0, 64]");
   if (c->out_channel_map) {
     for (int k = 0; k < c->K; ++k)
       if (c->out_channel_map[k] < 0 || c->out_channel_map[k] >= c->V)
@@ -322,7 +323,12 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   in.stitch_bytes_per_sample = (double)esz_out * c.K * sH * sW + 4.0 * c.K * c.H * c.W + 4.0 * c.K * sH * sW;
   in.canonical_weight_count = (int64_t)p.Din * p.D + 2LL * p.D +
                               (int64_t)c.depth * (12LL * p.D * p.D + 13LL * p.D) + 2LL * p.D +
-                              (int64_t)p.D * p.Nh + p.Nh;
+                              (int64_t)p.D * p.Nh + p.Nh +
+                              (c.res_hidden ? 18LL * c.res_hidden * c.K + c.res_hidden + c.K : 0);
+  if (c.res_hidden) {   // the two 3x3 convolutions on every output pixel (R31)
+    in.flops_per_sample += 36.0 * c.K * c.res_hidden * sH * sW;
+    in.local_flops_per_sample += 36.0 * c.K * c.res_hidden * (double)lcore * p.P * p.P;
+  }
 
   // ---- workspace layout ----
   Layout& ly = p.lay;
@@ -371,6 +377,8 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     p.n_push = (int32_t)n;
   }
   ly.sigtab = take((int64_t)c.world_size * 8);
+  // residual convolution weights, staged by orbit2_prepare_weights for orbit2_stitch
+  ly.rconv = take(c.res_hidden ? (18LL * c.res_hidden * c.K + c.res_hidden + c.K) * 4 : 0);
   ly.total = off;
   in.workspace_bytes = ly.total;
   in.tile_out_bytes = (int64_t)c.batch * in.max_chunk_core_tokens * p.Nh * E;
@@ -389,9 +397,9 @@ orbit2_rect core_px(const orbit2_tile& t, int p) {
 // reads (clamped to the grid, R4) and the 1-pixel support of the bilinear
 // residual around the core (O7: y1 = y0 + 1) that the stitch reads -- the
 // bounding box of both (they are nested: equal to the padded rect when h >= 1).
-orbit2_rect pad_px(const orbit2_tile& t, int p, int H, int W) {
-  return {std::max(0, std::min(t.pad_y0 * p, t.core_y0 * p - 1)), std::min(H, std::max(t.pad_y1 * p, t.core_y1 * p + 1)),
-          std::max(0, std::min(t.pad_x0 * p, t.core_x0 * p - 1)), std::min(W, std::max(t.pad_x1 * p, t.core_x1 * p + 1))};
+orbit2_rect pad_px(const orbit2_tile& t, int p, int H, int W, int dil) {
+  return {std::max(0, std::min(t.pad_y0 * p, t.core_y0 * p - dil)), std::min(H, std::max(t.pad_y1 * p, t.core_y1 * p + dil)),
+          std::max(0, std::min(t.pad_x0 * p, t.core_x0 * p - dil)), std::min(W, std::max(t.pad_x1 * p, t.core_x1 * p + dil))};
 }
 bool intersect(const orbit2_rect& a, const orbit2_rect& b, orbit2_rect* o) {
   o->y0 = std::max(a.y0, b.y0); o->y1 = std::min(a.y1, b.y1);
@@ -413,7 +421,10 @@ void xfer_rects(const Plan& p, int kind, int rank, int peer, int direction, std:
   }
   for (const orbit2_tile& t : p.tiles) {          // dst's padded rects
     if (t.owner_rank != dst) continue;
-    const orbit2_rect need = pad_px(t, pp, H, W);
+    // bilinear support: 1 coarse pixel; with the residual convolutions (R31) their
+    // 2-output-pixel receptive field adds ceil(2 / s) coarse pixels
+    const int dil = 1 + (p.cfg.res_hidden ? (2 + p.cfg.scale - 1) / p.cfg.scale : 0);
+    const orbit2_rect need = pad_px(t, pp, H, W, dil);
     for (const orbit2_tile& u : p.tiles) {        // src's cores
       if (u.owner_rank != src) continue;
       orbit2_rect o;
@@ -468,6 +479,8 @@ WeightLayout weight_layout(const Plan& p) {
   }
   w.lnf_g = take(D * 4); w.lnf_b = take(D * 4);
   w.w_h = take(Nh * D * E); w.b_h = take(Nh * 4);
+  const int64_t CR = p.cfg.res_hidden, K = p.cfg.K;
+  w.rconv = CR ? take((18 * CR * K + CR + K) * 4) : 0;   // fp32, canonical order (W_ra b_ra W_rb b_rb)
   w.total = off;
   // canonical fp32 element offsets (include/orbit2.h order)
   int64_t c = 0;
@@ -485,6 +498,7 @@ WeightLayout weight_layout(const Plan& p) {
   }
   w.c_lnf_g = ctake(D); w.c_lnf_b = ctake(D);
   w.c_w_h = ctake(Nh * D); w.c_b_h = ctake(Nh);
+  w.c_rconv = CR ? ctake(18 * CR * K + CR + K) : 0;
   w.c_total = c;
   return w;
 }

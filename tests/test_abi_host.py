@@ -148,3 +148,36 @@ def test_create_rejects_bad_workspace(o2):
     h = C.c_void_p()
     st = o2.lib.orbit2_create(C.byref(cfg), None, 0, C.byref(h))
     assert st == o2.E_INVALID and b"workspace" in o2.lib.orbit2_last_error()
+
+
+def test_residual_conv_config_counts_and_halo(o2):
+    """res_hidden (ABI v2, reading R31): the canonical blob grows by the two 3x3
+    convolutions (18 C_r K + C_r + K, the workloads generator agrees), out-of-range
+    values are rejected, and with halo 0 the rectangles a rank receives cover every
+    owned core + 1 + ceil(2 / s) coarse pixels (the convolutions' receptive field)."""
+    from workloads import weight_count
+    w = get_config("C1", res_hidden=8)
+    _, info = o2.orbit2_tiles_plan(o2.config_from(w))
+    assert info.canonical_weight_count == weight_count(w)
+    assert info.canonical_weight_count == weight_count(w.replace(res_hidden=0)) + 18 * 8 * w.K + 8 + w.K
+    with pytest.raises(o2.Orbit2Error, match="res_hidden"):
+        o2.orbit2_tiles_plan(o2.config_from(w, res_hidden=65))
+    w0 = get_config("C1", H=36, W=60, tiles_y=3, tiles_x=4, halo=0, res_hidden=4)
+    dil = 1 + -(-2 // w0.scale)
+    for R in (2, 3):
+        for r in range(R):
+            cfg = o2.config_from(w0, world_size=R, rank=r)
+            tiles, _ = o2.orbit2_tiles_plan(cfg)
+            have = np.zeros((w0.H, w0.W), bool)
+            for t in tiles:
+                if t.owner_rank == r:
+                    have[t.core_y0 * 2:t.core_y1 * 2, t.core_x0 * 2:t.core_x1 * 2] = True
+            for s in range(R):
+                if s != r:
+                    for y0, y1, x0, x1 in o2.orbit2_xfer_plan(cfg, o2.XFER_HALO, s, o2.RECV)[0]:
+                        have[y0:y1, x0:x1] = True
+            for t in tiles:
+                if t.owner_rank == r:
+                    y0, y1 = max(0, t.core_y0 * 2 - dil), min(w0.H, t.core_y1 * 2 + dil)
+                    x0, x1 = max(0, t.core_x0 * 2 - dil), min(w0.W, t.core_x1 * 2 + dil)
+                    assert have[y0:y1, x0:x1].all()

@@ -350,3 +350,41 @@ def test_both_attention_kernels_match_oracle(kernel, monkeypatch):
     print(f"attention kernel {kernel}: rel_err={e:.3e}")
     assert e <= BF16_TOL
     assert np.array_equal(got, run_cuda(w, x, blob, BF16, chunk_tiles=1))
+
+
+# ---------------------------------------------------------------- residual convolutional path (R31)
+RCONV = [
+    ("C1", dict(res_hidden=8)),
+    ("C1", dict(res_hidden=4, tiles_y=3, tiles_x=5, halo=1, K=2, out_channel_map=(2, 0))),
+    ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=2, res_hidden=8)),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
+@pytest.mark.parametrize("name,over", RCONV)
+def test_residual_conv_path_parity(name, over, precision, tol):
+    """P:498 residual convolutional path (oracle O8): up + conv_b(GELU(conv_a(up)))
+    fused into the stitch, against the fp64 oracle (both precisions), and the
+    residual branch on its own (out - ViT branch)."""
+    w, x, blob = _case(name, **over)
+    ref, ref_vit, res = oracle_full(w, x, blob)
+    got = run_cuda(w, x, blob, precision)
+    e = rel_err(got, ref)
+    print(f"rconv {name} {over} prec={precision}: rel_err={e:.3e}")
+    assert np.isfinite(got).all() and e <= tol
+
+
+@pytest.mark.gpu
+def test_residual_conv_zero_second_conv_is_upsample_and_chunk_invariant():
+    """Zero conv_b (initialization contract) -> the fused kernel's output equals the
+    plain stitch's to fp32 rounding; chunking and rank splits are bit-identical."""
+    w, x, blob = _case("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2, res_hidden=8)
+    z = blob.copy()
+    z[-(9 * 8 * w.K + w.K):] = 0.0
+    plain = run_cuda(w.replace(res_hidden=0), x, z[:-(18 * 8 * w.K + 8 + w.K)], BF16)
+    conv0 = run_cuda(w, x, z, BF16)
+    assert np.abs(conv0 - plain).max() <= 1e-5 * np.abs(plain).max()
+    a = run_cuda(w, x, blob, BF16)
+    assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=1))
+    assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=3))
