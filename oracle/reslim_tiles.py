@@ -23,6 +23,12 @@ What is computed (the method, step by step, in the paper's order):
   O5 head      -- LN_f + linear decoder head   P:480, R10, R11
   O6 stitch    -- halo outputs discarded, cores placed   P:532, R16
   O7 residual  -- bilinear upsample added      P:487-498 [Residual Learning], R12, R13
+  O5b decoder convolutions (optional, dec_hidden > 0) -- P:480 "a decoder comprising
+                  convolutional layers and linear projections", reading R32: the
+                  linear head (O5) runs on the tile's core tokens plus a ring of
+                  ceil(2/P) patches (clipped to the grid), is unpatchified, and
+                  conv_db(GELU(conv_da(.))) (3x3, zero padding outside that region)
+                  gives the core output; the ring is then discarded with the halo
   O8 residual convolutional path (optional, res_hidden > 0) -- P:498 "the residual
                   convolutional path reintroduces upsampling outside the main ViT
                   path, using lightweight convolutional layers", reading R31:
@@ -301,7 +307,7 @@ def residual_conv(up: np.ndarray, Wt: dict) -> np.ndarray:
 # Canonical weight blob -> named fp64 arrays (order: include/orbit2.h, restated here)
 # ---------------------------------------------------------------------------
 def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int, K: int = 0,
-                   res_hidden: int = 0) -> dict:
+                   res_hidden: int = 0, dec_hidden: int = 0) -> dict:
     blob = np.asarray(blob, dtype=np.float64)
     F = 4 * D
     off = 0
@@ -328,6 +334,9 @@ def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int, K: i
     if res_hidden:   # O8: W_ra[C_r][K][3][3], b_ra[C_r], W_rb[K][C_r][3][3], b_rb[K]
         Wt["W_ra"], Wt["b_ra"] = take(res_hidden, K, 3, 3), take(res_hidden)
         Wt["W_rb"], Wt["b_rb"] = take(K, res_hidden, 3, 3), take(K)
+    if dec_hidden:   # O5b: W_da[C_d][K][3][3], b_da[C_d], W_db[K][C_d][3][3], b_db[K]
+        Wt["W_da"], Wt["b_da"] = take(dec_hidden, K, 3, 3), take(dec_hidden)
+        Wt["W_db"], Wt["b_db"] = take(K, dec_hidden, 3, 3), take(K)
     if off != blob.size:
         raise ValueError(f"weight blob has {blob.size} values, layout needs {off}")
     return Wt
@@ -355,13 +364,14 @@ class Problem:
     halo_mode: int = HALO_CLAMP
     channel_map: tuple | None = None
     res_hidden: int = 0      # O8 hidden channels (0: no residual convolutions)
+    dec_hidden: int = 0      # O5b hidden channels (0: linear decoder head only)
 
     @classmethod
     def from_config(cls, cfg) -> "Problem":
         return cls(cfg.H, cfg.W, cfg.V, cfg.K, cfg.scale, cfg.patch, cfg.tiles_y, cfg.tiles_x,
                    cfg.halo, cfg.embed, cfg.depth, cfg.heads, cfg.halo_mode,
                    tuple(cfg.out_channel_map) if cfg.out_channel_map is not None else None,
-                   getattr(cfg, "res_hidden", 0))
+                   getattr(cfg, "res_hidden", 0), getattr(cfg, "dec_hidden", 0))
 
     @property
     def P(self) -> int:
@@ -376,15 +386,37 @@ class Problem:
 
     def weights(self, blob) -> dict:
         return unpack_weights(blob, self.embed, self.depth, self.V * self.patch ** 2,
-                              self.K * self.P * self.P, self.K, self.res_hidden)
+                              self.K * self.P * self.P, self.K, self.res_hidden, self.dec_hidden)
+
+
+def decoder_rect(tile: Tile, pr: Problem):
+    """O5b: the tile's core grown by r = ceil(2/P) patches (the two 3x3 convolutions'
+    reach at the output resolution), clipped to the patch grid (patch units)."""
+    r = -(-2 // pr.P)
+    Hp, Wp = pr.H // pr.patch, pr.W // pr.patch
+    return (max(0, tile.core_y0 - r), min(Hp, tile.core_y1 + r),
+            max(0, tile.core_x0 - r), min(Wp, tile.core_x1 + r))
 
 
 def tile_forward(x_b: np.ndarray, tile: Tile, pr: Problem, Wt: dict) -> np.ndarray:
-    """Steps O2-O5 for one tile of one sample: returns g [n_core, K*P*P]."""
+    """Steps O2-O5 (+ O5b) for one tile of one sample: returns g [n_core, K*P*P]."""
     z = embed_tile(gather_tile(x_b, tile, pr.patch), tile, pr.patch, Wt)
     for Lw in Wt["layers"]:
         z = block(z, Lw, pr.heads)
-    return head(z[core_rows(tile)], Wt)
+    if not pr.dec_hidden:
+        return head(z[core_rows(tile)], Wt)
+    # O5b: head over the decoder rectangle, unpatchify, two 3x3 convolutions, keep the core
+    K, P = pr.K, pr.P
+    oy0, oy1, ox0, ox1 = decoder_rect(tile, pr)
+    uu, ww = np.meshgrid(np.arange(oy0, oy1), np.arange(ox0, ox1), indexing="ij")
+    rows = ((uu - tile.pad_y0) * tile.pad_w + (ww - tile.pad_x0)).ravel()
+    g = head(z[rows], Wt)
+    oh, ow = oy1 - oy0, ox1 - ox0
+    field = g.reshape(oh, ow, K, P, P).transpose(2, 0, 3, 1, 4).reshape(K, oh * P, ow * P)
+    dec = conv3x3(gelu(conv3x3(field, Wt["W_da"], Wt["b_da"])), Wt["W_db"], Wt["b_db"])
+    ch, cw = tile.core_y1 - tile.core_y0, tile.core_x1 - tile.core_x0
+    core = dec[:, (tile.core_y0 - oy0) * P:(tile.core_y1 - oy0) * P, (tile.core_x0 - ox0) * P:(tile.core_x1 - ox0) * P]
+    return core.reshape(K, ch, P, cw, P).transpose(1, 3, 0, 2, 4).reshape(ch * cw, K * P * P)
 
 
 def residual_up(x_b: np.ndarray, pr: Problem, Wt: dict | None = None) -> np.ndarray:
@@ -461,6 +493,8 @@ def global_forward(x: np.ndarray, blob: np.ndarray, pr: Problem) -> np.ndarray:
             z = block(z, Lw, pr.heads)
         g = head(z, Wt)
         out[b] = g.reshape(Hp, Wp, K, P, P).transpose(2, 0, 3, 1, 4).reshape(K, Hp * P, Wp * P)
+        if pr.dec_hidden:
+            out[b] = conv3x3(gelu(conv3x3(out[b], Wt["W_da"], Wt["b_da"])), Wt["W_db"], Wt["b_db"])
         out[b] += residual_up(x[b], pr, Wt)
     return out
 

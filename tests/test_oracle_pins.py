@@ -38,7 +38,8 @@ def small_problem(**kw):
 def blob_for(pr, seed=7, head_gain=1.0, sharp=True, res_gain=1.0):
     cfg = get_config("C1", H=pr.H, W=pr.W, V=pr.V, K=pr.K, scale=pr.scale, patch=pr.patch,
                      tiles_y=pr.tiles_y, tiles_x=pr.tiles_x, halo=pr.halo, embed=pr.embed,
-                     depth=pr.depth, heads=pr.heads, halo_mode=pr.halo_mode, res_hidden=pr.res_hidden)
+                     depth=pr.depth, heads=pr.heads, halo_mode=pr.halo_mode, res_hidden=pr.res_hidden,
+                     dec_hidden=pr.dec_hidden)
     return make_weights(cfg, seed=seed, head_gain=head_gain, sharp=sharp, res_gain=res_gain), cfg
 
 
@@ -462,9 +463,9 @@ def test_golden_paper_sequence_lengths():
 
 
 # ---------------------------------------------------------------- sampled-tile oracle
-@pytest.mark.parametrize("res_hidden", [0, 4])
+@pytest.mark.parametrize("res_hidden,dec_hidden", [(0, 0), (4, 0), (4, 3)])
 @pytest.mark.parametrize("mode", [O.HALO_CLAMP, O.HALO_REPLICATE])
-def test_sampled_tiles_equal_full_forward_restricted(mode, res_hidden):
+def test_sampled_tiles_equal_full_forward_restricted(mode, res_hidden, dec_hidden):
     """tiles_forward_sampled (which supplies every C3/C4/C5 expected value) is
     tiles_forward restricted to the tile's core output rectangle, bit for bit,
     for EVERY tile of a 3 x 3 problem (the core outputs of a tile are
@@ -472,7 +473,7 @@ def test_sampled_tiles_equal_full_forward_restricted(mode, res_hidden):
     formula evaluated on that rectangle).  A wrong core slice, reshape or
     bilinear window in the sampled path fails here."""
     pr = small_problem(H=36, W=44, tiles_y=3, tiles_x=3, halo=2, halo_mode=mode, channel_map=(2, 0),
-                       res_hidden=res_hidden)
+                       res_hidden=res_hidden, dec_hidden=dec_hidden)
     blob, cfg = blob_for(pr)
     x = input_for(cfg, batch=2)
     full, full_vit, _ = O.tiles_forward(x, blob, pr, return_parts=True)
@@ -598,3 +599,48 @@ def test_residual_conv_locality():
     x2[0][:, mask] += 5.0
     b2 = O.tiles_forward_sampled(x2[0], blob, pr, [4])[4]
     assert np.array_equal(a[2], b2[2])
+
+
+# ---------------------------------------------------------------- O5b decoder convolutions (R32)
+def test_decoder_convs_untiled_match_torch():
+    """T = 1, h = 0: the decoder rectangle is the whole grid, so the tiled pass with
+    decoder convolutions equals an untiled torch model (linear head, pixel_shuffle,
+    conv2d -> gelu -> conv2d with zero padding at the field border), and the oracle's
+    separate untiled global_forward too."""
+    import dataclasses
+    pr = small_problem(tiles_y=1, tiles_x=1, halo=0, dec_hidden=3)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg, batch=2)
+    Wt = pr.weights(blob)
+    n_dec = 2 * 9 * 3 * pr.K + 3 + pr.K
+    base = dataclasses.replace(pr, dec_hidden=0)
+    xt = torch.from_numpy(x.astype(np.float64))
+    with torch.no_grad():
+        vit = torch.from_numpy(torch_global_model(x, blob[:-n_dec], base)) - F.interpolate(
+            xt[:, list(pr.cmap())], scale_factor=pr.scale, mode="bilinear", align_corners=False)
+        h = F.gelu(F.conv2d(vit, torch.from_numpy(Wt["W_da"]), torch.from_numpy(Wt["b_da"]), padding=1))
+        dec = F.conv2d(h, torch.from_numpy(Wt["W_db"]), torch.from_numpy(Wt["b_db"]), padding=1)
+        up = F.interpolate(xt[:, list(pr.cmap())], scale_factor=pr.scale, mode="bilinear", align_corners=False)
+    want = (dec + up).numpy()
+    np.testing.assert_allclose(O.tiles_forward(x, blob, pr), want, rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(O.global_forward(x, blob, pr), want, rtol=1e-10, atol=1e-10)
+
+
+def test_decoder_convs_full_halo_equals_global_and_locality():
+    """I6 with the decoder convolutions: a halo covering the grid gives every tile all
+    tokens, so its ring outputs are the global ones and tiled == untiled; I5: a tile's
+    output is unchanged by input pixels outside its padded rectangle."""
+    pr = small_problem(halo=50, dec_hidden=3, res_hidden=2)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg)
+    np.testing.assert_allclose(O.tiles_forward(x, blob, pr), O.global_forward(x, blob, pr), rtol=1e-11, atol=1e-11)
+    pr = small_problem(tiles_y=2, tiles_x=3, halo=1, dec_hidden=3)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg)
+    t = pr.tiles()[1]
+    a = O.tiles_forward_sampled(x[0], blob, pr, [1])[1]
+    x2 = x.copy()
+    mask = np.ones(x.shape[2:], bool)
+    mask[max(0, t.pad_y0 * pr.patch):t.pad_y1 * pr.patch, max(0, t.pad_x0 * pr.patch):t.pad_x1 * pr.patch] = False
+    x2[0][:, mask] -= 3.0
+    assert np.array_equal(a[3], O.tiles_forward_sampled(x2[0], blob, pr, [1])[1][3])

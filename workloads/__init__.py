@@ -49,6 +49,7 @@ class Config:
     halo_mode: int = 0          # 0 = CLAMP (reading R4), 1 = REPLICATE
     out_channel_map: tuple | None = None   # K entries in [0,V); None = identity
     res_hidden: int = 0         # residual-path conv hidden channels (reading R31); 0 = none
+    dec_hidden: int = 0         # decoder conv hidden channels (reading R32); 0 = linear head only
 
     @property
     def mlp_hidden(self) -> int:
@@ -172,8 +173,9 @@ def weight_count(cfg: Config) -> int:
     D, L, F = cfg.embed, cfg.depth, cfg.mlp_hidden
     per_layer = 2 * D + 3 * D * D + 3 * D + D * D + D + 2 * D + F * D + F + D * F + D
     n = cfg.din * D + 2 * D + L * per_layer + 2 * D + cfg.head_out * D + cfg.head_out
-    if cfg.res_hidden:
-        n += 2 * 9 * cfg.res_hidden * cfg.K + cfg.res_hidden + cfg.K
+    for c in (cfg.res_hidden, cfg.dec_hidden):
+        if c:
+            n += 2 * 9 * c * cfg.K + c + cfg.K
     return n
 
 
@@ -230,6 +232,9 @@ def make_weights(cfg: Config, seed: int | None = None, sharp: bool = True,
     if cfg.res_hidden:                                # residual convs W_ra, b_ra, W_rb, b_rb
         lin(cfg.res_hidden, cfg.K * 9); bias(cfg.res_hidden)
         lin(cfg.K, cfg.res_hidden * 9, res_gain); bias(cfg.K)
+    if cfg.dec_hidden:                                # decoder convs W_da, b_da, W_db, b_db
+        lin(cfg.dec_hidden, cfg.K * 9); bias(cfg.dec_hidden)
+        lin(cfg.K, cfg.dec_hidden * 9); bias(cfg.K)
     blob = np.concatenate(parts).astype(np.float32)
     assert blob.size == weight_count(cfg)
     return bf16_round(blob) if round_bf16 else blob
