@@ -86,6 +86,11 @@ typedef struct {
   int32_t res_hidden;      /* residual convolutional path (reading R31): hidden
                               channels C_r of res = up + conv_b(GELU(conv_a(up))), 3x3,
                               0 <= C_r <= 64; 0 = the bilinear upsample alone */
+  int32_t dec_hidden;      /* decoder convolutions (reading R32): hidden channels
+                              C_d of conv_db(GELU(conv_da(.))) applied to the
+                              unpatchified head output of a tile's core + a ring of
+                              ceil(2/P) patches; 0 <= C_d <= 64 (needs halo >= that
+                              ring); 0 = the linear head alone (R11) */
   const int32_t *out_channel_map; /* K entries in [0,V) selecting the residual input
                                      channel of each output variable (R13); NULL = identity */
 } orbit2_config;
@@ -101,6 +106,9 @@ typedef struct {
                                                in CLAMP mode, not in REPLICATE */
   int32_t n_tokens;                 /* (pad_y1-pad_y0)*(pad_x1-pad_x0) */
   int32_t n_core_tokens;            /* (core_y1-core_y0)*(core_x1-core_x0) */
+  int32_t n_out_tokens;             /* tokens whose head outputs tile_out holds: the core,
+                                       grown by ceil(2/P) patches (clipped to the grid)
+                                       when dec_hidden > 0 (R32) */
   int64_t token_offset;             /* offset in one sample's packed list of ALL tiles */
   int64_t core_token_offset;        /* offset in one sample's list of ALL core tokens */
 } orbit2_tile;
@@ -113,7 +121,7 @@ typedef struct {
   int64_t tokens_per_sample;        /* sum of n_tokens over all tiles (N_pad) */
   int64_t core_tokens_per_sample;   /* (H/p)*(W/p) */
   int64_t local_tokens;             /* per sample, rank-local tiles */
-  int64_t local_core_tokens;        /* per sample, rank-local tiles */
+  int64_t local_core_tokens;        /* per sample, rank-local tiles: OUTPUT tokens (n_out_tokens) */
   int64_t max_chunk_tokens;         /* per sample, max over windows of chunk_tiles local tiles */
   int64_t max_chunk_core_tokens;
   int64_t sum_n2_per_sample;        /* sum_t n_t^2 (attention cost, P:527 O(N^2/T)) */
@@ -166,7 +174,9 @@ orbit2_status orbit2_create(const orbit2_config *cfg, void *workspace_dev, size_
  *     b_qkv[3D] W_o[D][D] b_o[D] ln2_g[D] ln2_b[D] W_1[4D][D] b_1[4D] W_2[D][4D] b_2[D]
  *   lnf_g[D] lnf_b[D] W_h[K*P*P][D] (row (k*P+a)*P+b, P = s*p) b_h[K*P*P]
  *   if res_hidden = C_r > 0: W_ra[C_r][K][3][3] b_ra[C_r] W_rb[K][C_r][3][3] b_rb[K]
- * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2 (+ 18 C_r K + C_r + K),
+ *   if dec_hidden = C_d > 0: W_da[C_d][K][3][3] b_da[C_d] W_db[K][C_d][3][3] b_db[K]
+ * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2 (+ 18 C K + C + K per
+ * convolution pair),
  * Din = V*p*p.
  * Stream-ordered; canonical_dev may be freed once the stream passes this call.
  */

@@ -77,11 +77,12 @@ bool launch_gather_tma(const float* x, __nv_bfloat16* patches, int2* rowinfo, co
 bool launch_stitch_tma(const __nv_bfloat16* tile_out, int64_t tile_out_rows, const float* x, float* out,
                        const ChunkDev& ch, const int32_t* cmap, int B, int V, int H, int W, int K, int s, int P,
                        int max_core_h, int max_core_w, cudaStream_t st);
-// stitch + residual convolutional path (R31), fp32 CUDA-core convolutions (rconv.cu)
+// stitch with the residual-path (R31) and / or decoder (R32) convolutions, fp32
+// CUDA-core convolutions (rconv.cu); wres / wdec null when CR / CD == 0
 template <typename T>
-bool launch_stitch_rconv(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap,
-                         const float* wconv, int B, int V, int H, int W, int K, int s, int P, int CR, int max_core_h,
-                         int max_core_w, cudaStream_t st);
+bool launch_stitch_conv(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap,
+                        const float* wres, const float* wdec, int B, int V, int H, int W, int K, int s, int P, int CR,
+                        int CD, int max_core_h, int max_core_w, cudaStream_t st);
 bool make_tmap_f32_3d(CUtensorMap* map, const void* ptr, int64_t d0, int64_t d1, int64_t d2, int b0, int b1,
                       int b2);
 template <typename T>

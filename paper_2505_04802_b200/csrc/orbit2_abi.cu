@@ -349,10 +349,14 @@ orbit2_status orbit2_prepare_weights(void* ctx, const float* canonical_dev, void
   ORBIT2_TRY(conv(w.c_lnf_b, w.lnf_b, 1, D, D, 0));
   ORBIT2_TRY(conv(w.c_w_h, w.w_h, p.Nh, D, D, bf));
   ORBIT2_TRY(conv(w.c_b_h, w.b_h, 1, p.Nh, p.Nh, 0));
-  if (p.cfg.res_hidden) {   // R31 residual convolutions: fp32 into the packed blob and the workspace
-    const int64_t n = 18LL * p.cfg.res_hidden * p.cfg.K + p.cfg.res_hidden + p.cfg.K;
-    ORBIT2_TRY(conv(w.c_rconv, w.rconv, 1, n, n, 0));
-    cudaError_t e = cudaMemcpyAsync(c->at<void>(p.lay.rconv), canonical_dev + w.c_rconv, n * 4,
+  // R31 / R32 convolutions: fp32 into the packed blob and the workspace (orbit2_stitch reads them there)
+  const int32_t convs[2] = {p.cfg.res_hidden, p.cfg.dec_hidden};
+  const int64_t c_off[2] = {w.c_rconv, w.c_dconv}, p_off[2] = {w.rconv, w.dconv}, ws_off[2] = {p.lay.rconv, p.lay.dconv};
+  for (int i = 0; i < 2; ++i) {
+    if (!convs[i]) continue;
+    const int64_t n = 18LL * convs[i] * p.cfg.K + convs[i] + p.cfg.K;
+    ORBIT2_TRY(conv(c_off[i], p_off[i], 1, n, n, 0));
+    cudaError_t e = cudaMemcpyAsync(c->at<void>(ws_off[i]), canonical_dev + c_off[i], n * 4,
                                     cudaMemcpyDeviceToDevice, st);
     if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("prepare_weights: ") + cudaGetErrorString(e));
   }
@@ -646,15 +650,16 @@ orbit2_status orbit2_stitch_peer(void* ctx, int32_t peer, const void* tile_out_d
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
   return run(c, "stitch_residual", st, [&] {
-    if (cf.res_hidden) {   // residual convolutional path (R31)
-      const float* wc = c->at<float>(p.lay.rconv);
+    if (cf.res_hidden || cf.dec_hidden) {   // residual (R31) / decoder (R32) convolutions
+      const float* wr = c->at<float>(p.lay.rconv);
+      const float* wd = c->at<float>(p.lay.dconv);
       if (cf.precision == ORBIT2_BF16)
-        return launch_stitch_rconv<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev,
-                                                  out_dev, cd, cmap, wc, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale,
-                                                  p.P, cf.res_hidden, p.max_core_h, p.max_core_w, st);
-      return launch_stitch_rconv<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, wc,
-                                        cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, cf.res_hidden, p.max_core_h,
-                                        p.max_core_w, st);
+        return launch_stitch_conv<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev,
+                                                 out_dev, cd, cmap, wr, wd, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale,
+                                                 p.P, cf.res_hidden, cf.dec_hidden, p.max_core_h, p.max_core_w, st);
+      return launch_stitch_conv<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, wr,
+                                       wd, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, cf.res_hidden,
+                                       cf.dec_hidden, p.max_core_h, p.max_core_w, st);
     }
     if (cf.precision == ORBIT2_BF16 && c->tma_stitch &&
         launch_stitch_tma(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), (int64_t)cf.batch * cd.chunk_core,
@@ -685,15 +690,16 @@ orbit2_status orbit2_stitch(void* ctx, const void* tile_out_dev, const float* in
   const ChunkDev cd = chunk_dev(c, make_chunk(p, tile_begin, tile_count));
   const int32_t* cmap = c->at<int32_t>(p.lay.cmap);
   return run(c, "stitch_residual", st, [&] {
-    if (cf.res_hidden) {   // residual convolutional path (R31)
-      const float* wc = c->at<float>(p.lay.rconv);
+    if (cf.res_hidden || cf.dec_hidden) {   // residual (R31) / decoder (R32) convolutions
+      const float* wr = c->at<float>(p.lay.rconv);
+      const float* wd = c->at<float>(p.lay.dconv);
       if (cf.precision == ORBIT2_BF16)
-        return launch_stitch_rconv<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev,
-                                                  out_dev, cd, cmap, wc, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale,
-                                                  p.P, cf.res_hidden, p.max_core_h, p.max_core_w, st);
-      return launch_stitch_rconv<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, wc,
-                                        cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, cf.res_hidden, p.max_core_h,
-                                        p.max_core_w, st);
+        return launch_stitch_conv<__nv_bfloat16>(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), input_dev,
+                                                 out_dev, cd, cmap, wr, wd, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale,
+                                                 p.P, cf.res_hidden, cf.dec_hidden, p.max_core_h, p.max_core_w, st);
+      return launch_stitch_conv<float>(reinterpret_cast<const float*>(tile_out_dev), input_dev, out_dev, cd, cmap, wr,
+                                       wd, cf.batch, cf.V, cf.H, cf.W, cf.K, cf.scale, p.P, cf.res_hidden,
+                                       cf.dec_hidden, p.max_core_h, p.max_core_w, st);
     }
     if (cf.precision == ORBIT2_BF16 && c->tma_stitch &&
         launch_stitch_tma(reinterpret_cast<const __nv_bfloat16*>(tile_out_dev), (int64_t)cf.batch * cd.chunk_core,

@@ -20,13 +20,16 @@ inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 struct DevTile {
   int32_t pad_y0, pad_x0, pad_h, pad_w;      // padded rect (patch units)
   int32_t core_y0, core_x0, core_h, core_w;  // core rect (patch units)
-  int32_t n_tokens, n_core;
+  int32_t n_tokens, n_core;                   // n_core: tokens with decoder outputs (= core tokens
+                                              // unless dec_hidden > 0: core + ring, R32)
   int32_t qb_off;                             // first query block (local numbering)
   int32_t qp_off;                             // first query-block PAIR (local numbering)
   int64_t tok_off;                            // token offset in local packing (one sample)
-  int64_t core_off;                           // core-token offset in local packing
+  int64_t core_off;                           // offset of the tile's output tokens in the output packing
+  int32_t out_y0, out_x0, out_h, out_w;       // output-token rect (patch units): the core grown by
+                                              // ceil(2/P) patches when dec_hidden > 0, clipped to the grid
 };
-static_assert(sizeof(DevTile) == 64, "DevTile layout");
+static_assert(sizeof(DevTile) == 80, "DevTile layout");
 
 // Per-call geometry of a chunk of rank-local tiles [tb, tb+tc) for B samples.
 struct Chunk {
@@ -47,7 +50,7 @@ struct Layout {
   int64_t qg3, qg3c;
   int64_t core_rblk;          // last block: 128-row blocks holding core tokens (unchunked call)
   int64_t sig, push, sigtab;  // peer-memory SP: barrier flags, push table, peers' flag pointers
-  int64_t rconv;              // residual convolution weights (fp32; staged by prepare_weights)
+  int64_t rconv, dconv;       // residual / decoder convolution weights (fp32; staged by prepare_weights)
   int64_t total;
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;            // K of the embedding GEMM: round_up(Din, 64)
@@ -121,11 +124,11 @@ struct LayerW {
 };
 struct WeightLayout {
   int64_t w_e, bias_e, lnf_g, lnf_b, w_h, b_h;
-  int64_t rconv;              // residual convolution weights (fp32 copy of the canonical tail)
+  int64_t rconv, dconv;       // residual / decoder convolution weights (fp32 copies of the canonical tail)
   std::vector<LayerW> layers;
   int64_t total;
   // canonical (fp32 element) offsets, same names
-  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h, c_rconv;
+  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h, c_rconv, c_dconv;
   std::vector<LayerW> c_layers;
   int64_t c_total;
 };

@@ -56,6 +56,9 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
     return fail(msg, "world_size/rank: need 0 <= rank < world_size");
   if (c->chunk_tiles < 0) return fail(msg, "chunk_tiles: must be >= 0");
   if (c->res_hidden < 0 || c->res_hidden > 64) return fail(msg, "res_hidden: must be in [0, 64]");
+  if (c->dec_hidden < 0 || c->dec_hidden > 64) return fail(msg, "dec_hidden: must be in [0, 64]");
+  if (c->dec_hidden > 0 && c->halo < (2 + c->scale * c->patch - 1) / (c->scale * c->patch))
+    return fail(msg, "halo: the decoder convolutions need halo >= ceil(2 / (scale * patch)) patches");
   if (c->out_channel_map) {
     for (int k = 0; k < c->K; ++k)
       if (c->out_channel_map[k] < 0 || c->out_channel_map[k] >= c->V)
@@ -126,6 +129,23 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   }
   const int T = (int)p.tiles.size();
   const double D = p.D, L = c.depth;
+  // output tokens of a tile (R32): the core, grown by ceil(2/P) patches when the decoder
+  // convolutions need the ViT output around it, clipped to the grid
+  const int32_t ring = c.dec_hidden ? (2 + p.P - 1) / p.P : 0;
+  auto set_out = [&](DevTile& dt) {
+    dt.out_y0 = std::max(0, dt.core_y0 - ring);
+    dt.out_x0 = std::max(0, dt.core_x0 - ring);
+    dt.out_h = std::min(p.Hp, dt.core_y0 + dt.core_h + ring) - dt.out_y0;
+    dt.out_w = std::min(p.Wp, dt.core_x0 + dt.core_w + ring) - dt.out_x0;
+    dt.n_core = dt.out_h * dt.out_w;
+  };
+  for (orbit2_tile& t : p.tiles) {
+    DevTile dt{};
+    dt.core_y0 = t.core_y0; dt.core_x0 = t.core_x0;
+    dt.core_h = t.core_y1 - t.core_y0; dt.core_w = t.core_x1 - t.core_x0;
+    set_out(dt);
+    t.n_out_tokens = dt.n_core;
+  }
 
   // ---- rank assignment: LPT on the per-tile cost model ----
   std::vector<double> cost(T);
@@ -162,7 +182,8 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     dt.pad_h = t.pad_y1 - t.pad_y0; dt.pad_w = t.pad_x1 - t.pad_x0;
     dt.core_y0 = t.core_y0; dt.core_x0 = t.core_x0;
     dt.core_h = t.core_y1 - t.core_y0; dt.core_w = t.core_x1 - t.core_x0;
-    dt.n_tokens = t.n_tokens; dt.n_core = t.n_core_tokens;
+    dt.n_tokens = t.n_tokens;
+    set_out(dt);
     dt.qb_off = qb;
     dt.qp_off = qp;
     dt.tok_off = ltok; dt.core_off = lcore;
@@ -170,9 +191,9 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     for (int32_t q = 0; q < nqb; ++q) p.qblk_tile.push_back(li);
     const int32_t nqp = (nqb + 1) / 2;
     for (int32_t q = 0; q < nqp; ++q) p.qpair_tile.push_back(li);
-    {   // core tokens of the tile span padded-rect tokens [c_first, c_last] (row-major)
-      const int32_t c_first = (dt.core_y0 - dt.pad_y0) * dt.pad_w + (dt.core_x0 - dt.pad_x0);
-      const int32_t c_last = (dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w + (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
+    {   // output tokens of the tile span padded-rect tokens [c_first, c_last] (row-major)
+      const int32_t c_first = (dt.out_y0 - dt.pad_y0) * dt.pad_w + (dt.out_x0 - dt.pad_x0);
+      const int32_t c_last = (dt.out_y0 + dt.out_h - 1 - dt.pad_y0) * dt.pad_w + (dt.out_x0 + dt.out_w - 1 - dt.pad_x0);
       p.qpc_off.push_back((int32_t)p.qpair_core.size());
       const int32_t b0 = c_first / kQBlock, b1 = c_last / kQBlock;   // query blocks with core tokens
       if (li >= 32768 || nqb > 16384) {   // entry packing: tile index < 2^15, first block < 2^14
@@ -187,10 +208,10 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       for (int32_t b = 0; b < nqb; b += 3) p.qg3.push_back((li << 16) | (b << 2) | (std::min(3, nqb - b) - 1));
       for (int32_t b = b0; b <= b1; b += 3) p.qg3c.push_back((li << 16) | (b << 2) | (std::min(3, b1 + 1 - b) - 1));
     }
-    for (int32_t u = 0; u < dt.core_h; ++u)
-      for (int32_t w = 0; w < dt.core_w; ++w)
-        p.core_row.push_back((int32_t)(ltok + (int64_t)(u + dt.core_y0 - dt.pad_y0) * dt.pad_w +
-                                       (w + dt.core_x0 - dt.pad_x0)));
+    for (int32_t u = 0; u < dt.out_h; ++u)
+      for (int32_t w = 0; w < dt.out_w; ++w)
+        p.core_row.push_back((int32_t)(ltok + (int64_t)(u + dt.out_y0 - dt.pad_y0) * dt.pad_w +
+                                       (w + dt.out_x0 - dt.pad_x0)));
     p.max_pad_h = std::max(p.max_pad_h, dt.pad_h);
     p.max_pad_w = std::max(p.max_pad_w, dt.pad_w);
     p.max_core_h = std::max(p.max_core_h, dt.core_h);
@@ -198,7 +219,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
     qb += nqb;
     qp += nqp;
     ltok += t.n_tokens;
-    lcore += t.n_core_tokens;
+    lcore += dt.n_core;
     p.dev.push_back(dt);
   }
   p.qpc_off.push_back((int32_t)p.qpair_core.size());
@@ -224,10 +245,11 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       dt.pad_h = tt.pad_y1 - tt.pad_y0; dt.pad_w = tt.pad_x1 - tt.pad_x0;
       dt.core_y0 = tt.core_y0; dt.core_x0 = tt.core_x0;
       dt.core_h = tt.core_y1 - tt.core_y0; dt.core_w = tt.core_x1 - tt.core_x0;
-      dt.n_tokens = tt.n_tokens; dt.n_core = tt.n_core_tokens;
+      dt.n_tokens = tt.n_tokens;
+      set_out(dt);
       dt.tok_off = rtok[r]; dt.core_off = rcore[r];
       rtok[r] += tt.n_tokens;
-      rcore[r] += tt.n_core_tokens;
+      rcore[r] += dt.n_core;
       p.dev_by_rank[r].push_back(dt);
       p.max_core_h = std::max(p.max_core_h, dt.core_h);
       p.max_core_w = std::max(p.max_core_w, dt.core_w);
@@ -267,9 +289,9 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
       for (size_t li = 0; li + 1 < p.dev.size(); ++li) {
         const DevTile& dt = p.dev[li];
         const int64_t base = (int64_t)b * ltok + dt.tok_off;
-        const int64_t cf0 = (int64_t)(dt.core_y0 - dt.pad_y0) * dt.pad_w + (dt.core_x0 - dt.pad_x0);
-        const int64_t cl0 = (int64_t)(dt.core_y0 + dt.core_h - 1 - dt.pad_y0) * dt.pad_w +
-                            (dt.core_x0 + dt.core_w - 1 - dt.pad_x0);
+        const int64_t cf0 = (int64_t)(dt.out_y0 - dt.pad_y0) * dt.pad_w + (dt.out_x0 - dt.pad_x0);
+        const int64_t cl0 = (int64_t)(dt.out_y0 + dt.out_h - 1 - dt.pad_y0) * dt.pad_w +
+                            (dt.out_x0 + dt.out_w - 1 - dt.pad_x0);
         for (int64_t k = (base + cf0) / kQBlock; k <= (base + cl0) / kQBlock; ++k) need[(size_t)k] = 1;
       }
     for (size_t k = 0; k < need.size(); ++k)
@@ -324,10 +346,14 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   in.canonical_weight_count = (int64_t)p.Din * p.D + 2LL * p.D +
                               (int64_t)c.depth * (12LL * p.D * p.D + 13LL * p.D) + 2LL * p.D +
                               (int64_t)p.D * p.Nh + p.Nh +
-                              (c.res_hidden ? 18LL * c.res_hidden * c.K + c.res_hidden + c.K : 0);
-  if (c.res_hidden) {   // the two 3x3 convolutions on every output pixel (R31)
-    in.flops_per_sample += 36.0 * c.K * c.res_hidden * sH * sW;
-    in.local_flops_per_sample += 36.0 * c.K * c.res_hidden * (double)lcore * p.P * p.P;
+                              (c.res_hidden ? 18LL * c.res_hidden * c.K + c.res_hidden + c.K : 0) +
+                              (c.dec_hidden ? 18LL * c.dec_hidden * c.K + c.dec_hidden + c.K : 0);
+  {   // the 3x3 convolution pairs on every output pixel (R31 residual, R32 decoder)
+    const double cc = (double)c.res_hidden + c.dec_hidden;
+    double lc = 0;
+    for (int t : p.local) lc += p.tiles[t].n_core_tokens;
+    in.flops_per_sample += 36.0 * c.K * cc * sH * sW;
+    in.local_flops_per_sample += 36.0 * c.K * cc * lc * p.P * p.P;
   }
 
   // ---- workspace layout ----
@@ -379,6 +405,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.sigtab = take((int64_t)c.world_size * 8);
   // residual convolution weights, staged by orbit2_prepare_weights for orbit2_stitch
   ly.rconv = take(c.res_hidden ? (18LL * c.res_hidden * c.K + c.res_hidden + c.K) * 4 : 0);
+  ly.dconv = take(c.dec_hidden ? (18LL * c.dec_hidden * c.K + c.dec_hidden + c.K) * 4 : 0);
   ly.total = off;
   in.workspace_bytes = ly.total;
   in.tile_out_bytes = (int64_t)c.batch * in.max_chunk_core_tokens * p.Nh * E;
@@ -481,6 +508,8 @@ WeightLayout weight_layout(const Plan& p) {
   w.w_h = take(Nh * D * E); w.b_h = take(Nh * 4);
   const int64_t CR = p.cfg.res_hidden, K = p.cfg.K;
   w.rconv = CR ? take((18 * CR * K + CR + K) * 4) : 0;   // fp32, canonical order (W_ra b_ra W_rb b_rb)
+  const int64_t CD = p.cfg.dec_hidden;
+  w.dconv = CD ? take((18 * CD * K + CD + K) * 4) : 0;   // fp32 (W_da b_da W_db b_db)
   w.total = off;
   // canonical fp32 element offsets (include/orbit2.h order)
   int64_t c = 0;
@@ -499,6 +528,7 @@ WeightLayout weight_layout(const Plan& p) {
   w.c_lnf_g = ctake(D); w.c_lnf_b = ctake(D);
   w.c_w_h = ctake(Nh * D); w.c_b_h = ctake(Nh);
   w.c_rconv = CR ? ctake(18 * CR * K + CR + K) : 0;
+  w.c_dconv = CD ? ctake(18 * CD * K + CD + K) : 0;
   w.c_total = c;
   return w;
 }

@@ -25,13 +25,13 @@ class orbit2_config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "abi_version", "batch", "H", "W", "V", "K", "scale", "patch", "tiles_y", "tiles_x", "halo",
         "halo_mode", "embed", "depth", "heads", "mlp_hidden", "precision", "world_size", "rank",
-        "chunk_tiles", "res_hidden")] + [("out_channel_map", C.POINTER(C.c_int32))]
+        "chunk_tiles", "res_hidden", "dec_hidden")] + [("out_channel_map", C.POINTER(C.c_int32))]
 
 
 class orbit2_tile(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "tile_id", "tile_y", "tile_x", "owner_rank", "local_index", "core_y0", "core_y1", "core_x0",
-        "core_x1", "pad_y0", "pad_y1", "pad_x0", "pad_x1", "n_tokens", "n_core_tokens")] + [
+        "core_x1", "pad_y0", "pad_y1", "pad_x0", "pad_x1", "n_tokens", "n_core_tokens", "n_out_tokens")] + [
         ("token_offset", C.c_int64), ("core_token_offset", C.c_int64)]
 
 
@@ -115,11 +115,11 @@ def _check(st: int, where: str):
 
 def make_config(*, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, embed, depth, heads, batch=1,
                 halo_mode=HALO_CLAMP, precision=BF16, world_size=1, rank=0, chunk_tiles=0,
-                out_channel_map=None, res_hidden=0) -> orbit2_config:
+                out_channel_map=None, res_hidden=0, dec_hidden=0) -> orbit2_config:
     """Build an orbit2_config (the paper's problem statement, north star)."""
     cfg = orbit2_config(ABI_VERSION, batch, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, halo_mode,
                         embed, depth, heads, 4 * embed, precision, world_size, rank, chunk_tiles, res_hidden,
-                        None)
+                        dec_hidden, None)
     if out_channel_map is not None:
         arr = (C.c_int32 * K)(*out_channel_map)
         cfg.out_channel_map = C.cast(arr, C.POINTER(C.c_int32))
@@ -132,7 +132,7 @@ def config_from(w, **over) -> orbit2_config:
     kw = dict(H=w.H, W=w.W, V=w.V, K=w.K, scale=w.scale, patch=w.patch, tiles_y=w.tiles_y,
               tiles_x=w.tiles_x, halo=w.halo, embed=w.embed, depth=w.depth, heads=w.heads,
               batch=w.batch, halo_mode=w.halo_mode, out_channel_map=w.out_channel_map,
-              res_hidden=getattr(w, "res_hidden", 0))
+              res_hidden=getattr(w, "res_hidden", 0), dec_hidden=getattr(w, "dec_hidden", 0))
     kw.update(over)
     return make_config(**kw)
 
@@ -364,7 +364,7 @@ class Context:
             offs, acc = [], 0
             for t in mine:
                 offs.append(acc)
-                acc += t.n_core_tokens
+                acc += t.n_out_tokens
             offs.append(acc)
             self._core_off = offs
         return self._core_off[tb]

@@ -177,6 +177,11 @@ def test_packing_invariance_full_grid_bit_exact():
     a = run_cuda(w, x, blob, BF16)
     assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=1))
     assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=3))
+    wd = w.replace(dec_hidden=4)          # decoder convolutions too: same invariances
+    bd = make_weights(wd)
+    a = run_cuda(wd, x, bd, BF16)
+    assert np.array_equal(a, run_cuda(wd, x, bd, BF16, chunk_tiles=1))
+    assert np.array_equal(a, run_cuda(wd, x, bd, BF16, world_size=3))
 
 
 def test_rank_emulation_bit_exact():
@@ -357,6 +362,11 @@ RCONV = [
     ("C1", dict(res_hidden=8)),
     ("C1", dict(res_hidden=4, tiles_y=3, tiles_x=5, halo=1, K=2, out_channel_map=(2, 0))),
     ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=2, res_hidden=8)),
+    # decoder convolutions (R32): head on core + ring, conv(GELU(conv)) per tile
+    ("C1", dict(dec_hidden=4)),
+    ("C1", dict(dec_hidden=4, res_hidden=4, tiles_y=3, tiles_x=5, halo=1)),
+    ("C1", dict(dec_hidden=3, halo_mode=1)),
+    ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=2, dec_hidden=8, res_hidden=8)),
 ]
 
 
@@ -388,3 +398,8 @@ def test_residual_conv_zero_second_conv_is_upsample_and_chunk_invariant():
     a = run_cuda(w, x, blob, BF16)
     assert np.array_equal(a, run_cuda(w, x, blob, BF16, chunk_tiles=1))
     assert np.array_equal(a, run_cuda(w, x, blob, BF16, world_size=3))
+    wd = w.replace(dec_hidden=4)          # decoder convolutions too: same invariances
+    bd = make_weights(wd)
+    a = run_cuda(wd, x, bd, BF16)
+    assert np.array_equal(a, run_cuda(wd, x, bd, BF16, chunk_tiles=1))
+    assert np.array_equal(a, run_cuda(wd, x, bd, BF16, world_size=3))

@@ -211,6 +211,7 @@ MULTI_GPU_CASES = [
     ["C1", "2", "oracle", "halo_mode=1", "tiles_y=3", "tiles_x=5", "halo=1"],   # REPLICATE, ragged tiles
     ["C2", "2", "oracle"],                                               # full C2 grid, 16 tiles
     ["C1", "2", "oracle", "halo=0", "res_hidden=4"],                     # residual convs: dilated halo push
+    ["C1", "2", "oracle", "halo=1", "res_hidden=4", "dec_hidden=4"],     # + decoder convs (core + ring outputs)
 ]
 
 
