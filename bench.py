@@ -46,6 +46,8 @@ def parse():
                     help="N > 1 only.  sp (default): the tiles of one batch spread over the ranks, halo "
                          "exchange + output gather through NVLink peer memory (strong scaling); dp: every "
                          "rank its own batch (weak scaling)")
+    ap.add_argument("--sp-groups", type=int, default=0,
+                    help="N > 1: sample groups per rank (default 4 when the batch allows, else 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
     ap.add_argument("--set", action="append", default=[], metavar="FIELD=INT",
@@ -523,10 +525,16 @@ def run_sp(args, w, world, rank, local):
     B = w.batch
     _, info0 = o2.orbit2_tiles_plan(o2.config_from(w, batch=B, world_size=world, rank=rank))
     n_local = info0.n_local_tiles
-    chunk = args.chunk if args.chunk > 0 else max(1, -(-n_local // 4))   # <= 4 chunks: stitch overlaps compute
+    # Work split of a rank's share: G sample groups x all its tiles (kernels keep B/G x n_local
+    # tile-samples per launch; the last group's stitch, the only one not overlapped with
+    # compute, carries 1/G of the rank's output), or, for small batches, <= 4 tile chunks.
+    groups = args.sp_groups if args.sp_groups > 0 else (4 if B % 4 == 0 and B >= 16 else 1)
+    chunk = args.chunk if args.chunk > 0 else (0 if groups > 1 else max(1, -(-n_local // 4)))
     cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world, rank=rank, chunk_tiles=chunk)
     ctx = o2.Context(cfg)
     info = ctx.info
+    wctx = o2.Context(o2.config_from(w, batch=B // groups, precision=o2.BF16, world_size=world, rank=rank,
+                                     chunk_tiles=chunk)) if groups > 1 else None
     blob = make_weights(w)
     x_host = make_input(w, batch=B)
     x_pin = torch.from_numpy(x_host).pin_memory()
@@ -541,14 +549,15 @@ def run_sp(args, w, world, rank, local):
     packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
     out = torch.empty((B, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda") \
         if rank == 0 else None
-    sp = PeerSP(ctx, x, out, dist, gather_root=0)
+    sp = PeerSP(ctx, x, out, dist, gather_root=0, work_ctx=wctx)
     stream = torch.cuda.current_stream()
 
     for _ in range(max(3, args.warmup)):
         sp.step(packed, stream)
     barrier(world)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    l0 = ctx.launch_count()
+    lctx = [ctx] + ([wctx] if wctx is not None else [])
+    l0 = sum(c.launch_count() for c in lctx)
     with ClockSampler(local) as clk:
         barrier(world)
         ev0.record(stream)
@@ -557,7 +566,7 @@ def run_sp(args, w, world, rank, local):
         ev1.record(stream)
         barrier(world)
     ms = max_over_ranks(world, ev0.elapsed_time(ev1) / args.steps)
-    launches = (ctx.launch_count() - l0) // args.steps
+    launches = (sum(c.launch_count() for c in lctx) - l0) // args.steps
     clocks = clk.summary()
     ctx.comm_status()
 
@@ -588,12 +597,16 @@ def run_sp(args, w, world, rank, local):
     # ---- per-kernel-class times of this rank (profiled pass, events per launch) ----
     prof = {}
     if not args.no_profile:
-        ctx.set_profiling(True)
+        for c in lctx:
+            c.set_profiling(True)
         for _ in range(3):
             sp.step(packed, stream)
         torch.cuda.synchronize()
-        prof = {k: (n / 3, t / 3) for k, (n, t) in ctx.kernel_times().items()}
-        ctx.set_profiling(False)
+        for c in lctx:
+            for k, (n, t) in c.kernel_times().items():
+                n0, t0 = prof.get(k, (0.0, 0.0))
+                prof[k] = (n0 + n / 3, t0 + t / 3)
+            c.set_profiling(False)
     allprof = [None] * world
     dist.all_gather_object(allprof, prof)
     px = B * w.scale * w.H * w.scale * w.W
@@ -608,7 +621,7 @@ def run_sp(args, w, world, rank, local):
                        "vit": [w.embed, w.depth, w.heads],
                        "parallelism": f"tiles-sp{world} (LPT tile partition; halo push + output gather through "
                                       "NVLink peer memory, stitch fused with the gather)",
-                       "chunk_tiles": info.chunk_tiles, "gather_root": 0,
+                       "chunk_tiles": (wctx or ctx).info.chunk_tiles, "sample_groups": groups, "gather_root": 0,
                        "l2": "working set > L2 (126 MB) every step; no flush needed"},
             "tokens_per_s": B * info.tokens_per_sample / (ms * 1e-3),
             "core_tokens_per_s": B * info.core_tokens_per_sample / (ms * 1e-3),

@@ -36,18 +36,30 @@ class PeerSP:
     out_dev: this rank's output field [B,K,sH,sW] (root / sharded), else None
     """
 
-    def __init__(self, ctx, x_dev, out_dev, dist, gather_root=0, group=None):
+    def __init__(self, ctx, x_dev, out_dev, dist, gather_root=0, group=None, work_ctx=None):
+        """work_ctx: optional Context of the same problem with batch B / G (G sample
+        groups): the forward and stitch run group by group (a smaller last stitch into
+        the root's field is exposed at the end of the step); halo exchange and
+        barriers stay on `ctx` (the whole batch)."""
         import torch
         self.ctx, self.x = ctx, x_dev
+        self.wctx = work_ctx if work_ctx is not None else ctx
         world = ctx.cfg.world_size
         mine = ctx.ipc_handles(x_dev, out_dev)
         allh = [None] * world
         dist.all_gather_object(allh, mine, group=group)
         self.target = ctx.comm_init(gather_root, x_dev, out_dev, allh)
         dist.barrier(group=group)             # every rank's flags zeroed before anyone signals
-        n, ch = ctx.info.n_local_tiles, max(ctx.info.chunk_tiles, 1)
-        self.chunks = [(tb, min(ch, n - tb)) for tb in range(0, n, ch)]
-        self.tile_out = [ctx.tile_out_buffer() for _ in range(min(2, len(self.chunks)))]
+        wc = self.wctx
+        if ctx.cfg.batch % wc.cfg.batch:
+            raise ValueError("work_ctx batch must divide the batch")
+        self.groups = ctx.cfg.batch // wc.cfg.batch
+        n, ch = wc.info.n_local_tiles, max(wc.info.chunk_tiles, 1)
+        self.chunks = [(g, tb, min(ch, n - tb)) for g in range(self.groups) for tb in range(0, n, ch)]
+        self.tile_out = [wc.tile_out_buffer() for _ in range(min(2, len(self.chunks)))]
+        c = wc.cfg
+        self.x_step = c.batch * c.V * c.H * c.W                        # elements per sample group
+        self.out_step = c.batch * c.K * (c.scale * c.H) * (c.scale * c.W) * 4   # bytes per sample group
         self.side = torch.cuda.Stream(ctx.device) if hasattr(torch.cuda, "Stream") and x_dev.is_cuda else None
         self.ev_fwd = [None, None]
         self.ev_st = [None, None]
@@ -61,16 +73,19 @@ class PeerSP:
             stream = torch.cuda.current_stream(ctx.device)
         ctx.halo_exchange(stream)
         side = self.side if self.side is not None else stream
-        for i, (tb, tc) in enumerate(self.chunks):
+        wc = self.wctx
+        for i, (g, tb, tc) in enumerate(self.chunks):
             b = i & 1
             if cuda and self.ev_st[b] is not None:
                 stream.wait_event(self.ev_st[b])           # tile_out[b] stitched (chunk i - 2)
-            ctx.orbit2_reslim_forward(packed, self.x, tb, tc, self.tile_out[b], stream)
+            xg = self.x if self.groups == 1 else self.x.view(-1)[g * self.x_step:(g + 1) * self.x_step].view(
+                (wc.cfg.batch,) + tuple(self.x.shape[1:]))
+            wc.orbit2_reslim_forward(packed, xg, tb, tc, self.tile_out[b], stream)
             if cuda:
                 self.ev_fwd[b] = torch.cuda.Event()
                 self.ev_fwd[b].record(stream)
                 side.wait_event(self.ev_fwd[b])
-            ctx._stitch_to(self.tile_out[b], self.x, tb, tc, self.target, side)
+            wc._stitch_to(self.tile_out[b], xg, tb, tc, self.target + g * self.out_step, side)
             if cuda:
                 self.ev_st[b] = torch.cuda.Event()
                 self.ev_st[b].record(side)

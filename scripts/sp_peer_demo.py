@@ -18,6 +18,7 @@ from workloads import get_config, make_input, make_weights  # noqa: E402
 
 args = [a for a in sys.argv[1:] if "=" not in a]
 over = {k: int(v) for k, v in (a.split("=") for a in sys.argv[1:] if "=" in a)}   # e.g. tiles_y=1 halo=0
+groups = over.pop("groups", 1)     # sample groups per rank (PeerSP work_ctx)
 name = args[0] if len(args) > 0 else "C2"
 batch = int(args[1]) if len(args) > 1 else 1
 check_oracle = len(args) > 2 and args[2] == "oracle"
@@ -39,7 +40,9 @@ for t in ctx.tiles:
               slice(t.core_x0 * w.patch, t.core_x1 * w.patch))
         x[sl] = full[sl]
 out = torch.full((batch, w.K, w.scale * w.H, w.scale * w.W), float("nan"), device="cuda") if rank == 0 else None
-sp = PeerSP(ctx, x, out, dist, gather_root=0)
+wctx = o2.Context(o2.config_from(w, batch=batch // groups, world_size=world, rank=rank,
+                                 chunk_tiles=ctx.info.chunk_tiles)) if groups > 1 else None
+sp = PeerSP(ctx, x, out, dist, gather_root=0, work_ctx=wctx)
 sp.step(packed)
 torch.cuda.synchronize()
 ctx.comm_status()

@@ -212,6 +212,7 @@ MULTI_GPU_CASES = [
     ["C2", "2", "oracle"],                                               # full C2 grid, 16 tiles
     ["C1", "2", "oracle", "halo=0", "res_hidden=4"],                     # residual convs: dilated halo push
     ["C1", "2", "oracle", "halo=1", "res_hidden=4", "dec_hidden=4"],     # + decoder convs (core + ring outputs)
+    ["C2", "4", "oracle", "H=48", "W=96", "tiles_y=2", "tiles_x=3", "depth=2", "groups=2"],   # sample groups
 ]
 
 
