@@ -85,11 +85,11 @@ typedef struct {
   int32_t chunk_tiles;     /* max rank-local tiles per forward/stitch call; 0 = all */
   int32_t res_hidden;      /* residual convolutional path (reading R31): hidden
                               channels C_r of res = up + conv_b(GELU(conv_a(up))), 3x3,
-                              0 <= C_r <= 64; 0 = the bilinear upsample alone */
+                              0 <= C_r <= 64, C_r % 4 == 0; 0 = the bilinear upsample alone */
   int32_t dec_hidden;      /* decoder convolutions (reading R32): hidden channels
                               C_d of conv_db(GELU(conv_da(.))) applied to the
                               unpatchified head output of a tile's core + a ring of
-                              ceil(2/P) patches; 0 <= C_d <= 64 (needs halo >= that
+                              ceil(2/P) patches; 0 <= C_d <= 64, C_d % 4 == 0 (needs halo >= that
                               ring); 0 = the linear head alone (R11) */
   const int32_t *out_channel_map; /* K entries in [0,V) selecting the residual input
                                      channel of each output variable (R13); NULL = identity */

@@ -55,8 +55,10 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
   if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
     return fail(msg, "world_size/rank: need 0 <= rank < world_size");
   if (c->chunk_tiles < 0) return fail(msg, "chunk_tiles: must be >= 0");
-  if (c->res_hidden < 0 || c->res_hidden > 64) return fail(msg, "res_hidden: must be in [0, 64]");
-  if (c->dec_hidden < 0 || c->dec_hidden > 64) return fail(msg, "dec_hidden: must be in [0, 64]");
+  if (c->res_hidden < 0 || c->res_hidden > 64 || c->res_hidden % 4)
+    return fail(msg, "res_hidden: must be a multiple of 4 in [0, 64]");
+  if (c->dec_hidden < 0 || c->dec_hidden > 64 || c->dec_hidden % 4)
+    return fail(msg, "dec_hidden: must be a multiple of 4 in [0, 64]");
   if (c->dec_hidden > 0 && c->halo < (2 + c->scale * c->patch - 1) / (c->scale * c->patch))
     return fail(msg, "halo: the decoder convolutions need halo >= ceil(2 / (scale * patch)) patches");
   if (c->out_channel_map) {

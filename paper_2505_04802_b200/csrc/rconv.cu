@@ -40,44 +40,82 @@ template <> __device__ __forceinline__ float ld_f32<__nv_bfloat16>(const __nv_bf
 
 __device__ __forceinline__ float gelu_exact(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
-// hidden = GELU(conv_a(src)) on the block grown by 1, zero where !inside(Y, X)
+// Weights are staged TRANSPOSED in shared memory, output channel fastest:
+// wT[(i * 9 + dy * 3 + dx) * Cout + o] = W[o][i][dy][dx], so a thread that computes a
+// group of 4 output channels of one pixel reads their 4 weights with one broadcast
+// 16-byte shared load per input element (and the input element once per group).
+
+// hidden = GELU(conv_a(src)) on the block grown by 1, zero where !inside(Y, X);
+// thread = (pixel, group of 4 hidden channels)
 template <typename Inside>
-__device__ __forceinline__ void conv_hidden(const float* src, float* sh, const float* wa, const float* ba, int Cin,
+__device__ __forceinline__ void conv_hidden(const float* src, float* sh, const float* waT, const float* ba, int Cin,
                                             int C, int BY, int Y0, int X0, Inside inside) {
-  const int UY = BY + 4, UX = BX + 4, HY = BY + 2, HX = BX + 2;
-  for (int i = threadIdx.x; i < C * HY * HX; i += RC_THREADS) {
-    const int c = i / (HY * HX), r = i - c * HY * HX, yy = r / HX, xx = r - yy * HX;
-    float h = 0.f;
-    if (inside(Y0 - 1 + yy, X0 - 1 + xx)) {
-      float acc = ba[c];
-      const float* wc = wa + c * Cin * 9;
+  const int UX = BX + 4, UY = BY + 4, HY = BY + 2, HX = BX + 2;
+  const int C4 = C / 4, npx = HY * HX;
+  for (int i = threadIdx.x; i < C4 * npx; i += RC_THREADS) {
+    const int g = i / npx, r = i - g * npx, yy = r / HX, xx = r - yy * HX;
+    float4 acc = make_float4(ba[4 * g], ba[4 * g + 1], ba[4 * g + 2], ba[4 * g + 3]);
+    const bool in = inside(Y0 - 1 + yy, X0 - 1 + xx);
+    if (in) {
       for (int k = 0; k < Cin; ++k) {
         const float* u = src + (k * UY + yy) * UX + xx;
+        const float4* wk = reinterpret_cast<const float4*>(waT + (k * 9) * C) + g;
 #pragma unroll
         for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-          for (int dx = 0; dx < 3; ++dx) acc = fmaf(wc[k * 9 + dy * 3 + dx], u[dy * UX + dx], acc);
+          for (int dx = 0; dx < 3; ++dx) {
+            const float v = u[dy * UX + dx];
+            const float4 wv = wk[(dy * 3 + dx) * C4];
+            acc.x = fmaf(wv.x, v, acc.x); acc.y = fmaf(wv.y, v, acc.y);
+            acc.z = fmaf(wv.z, v, acc.z); acc.w = fmaf(wv.w, v, acc.w);
+          }
       }
-      h = gelu_exact(acc);
     }
-    sh[i] = h;
+    float* h = sh + (4 * g * HY + yy) * HX + xx;
+    h[0] = in ? gelu_exact(acc.x) : 0.f;
+    h[HY * HX] = in ? gelu_exact(acc.y) : 0.f;
+    h[2 * HY * HX] = in ? gelu_exact(acc.z) : 0.f;
+    h[3 * HY * HX] = in ? gelu_exact(acc.w) : 0.f;
   }
 }
 
-// second convolution at output (k, al, xx): b[k] + sum_c,dy,dx w[k][c][dy][dx] h[c][al+dy][xx+dx]
-__device__ __forceinline__ float conv_out(const float* sh, const float* wb, const float* bb, int C, int BY, int k,
-                                          int al, int xx) {
+// second convolution at output (k, al, xx) for k = 4 kg .. 4 kg + 3:
+// b[k] + sum_c,dy,dx W[k][c][dy][dx] h[c][al+dy][xx+dx]   (K4 = padded K / 4)
+__device__ __forceinline__ float4 conv_out4(const float* sh, const float* wbT, const float* bb, int C, int K4,
+                                            int BY, int kg, int al, int xx) {
   const int HY = BY + 2, HX = BX + 2;
-  float acc = bb[k];
-  const float* wk = wb + k * C * 9;
+  float4 acc = make_float4(bb[4 * kg], bb[4 * kg + 1], bb[4 * kg + 2], bb[4 * kg + 3]);
   for (int c = 0; c < C; ++c) {
     const float* hp = sh + (c * HY + al) * HX + xx;
+    const float4* wc = reinterpret_cast<const float4*>(wbT + (c * 9) * 4 * K4) + kg;
 #pragma unroll
     for (int dy = 0; dy < 3; ++dy)
 #pragma unroll
-      for (int dx = 0; dx < 3; ++dx) acc = fmaf(wk[c * 9 + dy * 3 + dx], hp[dy * HX + dx], acc);
+      for (int dx = 0; dx < 3; ++dx) {
+        const float v = hp[dy * HX + dx];
+        const float4 wv = wc[(dy * 3 + dx) * K4];
+        acc.x = fmaf(wv.x, v, acc.x); acc.y = fmaf(wv.y, v, acc.y);
+        acc.z = fmaf(wv.z, v, acc.z); acc.w = fmaf(wv.w, v, acc.w);
+      }
   }
   return acc;
+}
+
+// stage one conv pair transposed: W_a[C][K][3][3] b_a[C] W_b[K][C][3][3] b_b[K] ->
+// waT[(k*9+t)*C + c], ba[C], wbT[(c*9+t)*K4p + k] (K padded to K4p = 4*ceil(K/4), zeros), bb[K4p]
+__device__ __forceinline__ void stage_pair(const float* w, float* waT, float* ba, float* wbT, float* bb, int K, int C,
+                                           int K4p) {
+  for (int i = threadIdx.x; i < C * K * 9; i += RC_THREADS) {
+    const int c = i / (K * 9), r = i - c * K * 9, k = r / 9, t = r - k * 9;
+    waT[(k * 9 + t) * C + c] = w[i];
+  }
+  for (int i = threadIdx.x; i < C; i += RC_THREADS) ba[i] = w[C * K * 9 + i];
+  const float* wb = w + C * K * 9 + C;
+  for (int i = threadIdx.x; i < C * 9 * K4p; i += RC_THREADS) {
+    const int ct = i / K4p, k = i - ct * K4p, c = ct / 9, t = ct - c * 9;
+    wbT[i] = k < K ? wb[(k * C + c) * 9 + t] : 0.f;
+  }
+  for (int i = threadIdx.x; i < K4p; i += RC_THREADS) bb[i] = i < K ? wb[K * C * 9 + i] : 0.f;
 }
 
 template <typename T>
@@ -88,9 +126,11 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   extern __shared__ __align__(16) float rsm[];
   const int BY = P;
   const int UY = BY + 4, UX = BX + 4;
-  const int nr = CR ? CR * K * 18 + CR + K : 0, nd = CD ? CD * K * 18 + CD + K : 0;
-  float* sWr = rsm;                                 // [nr] residual conv weights (W_ra b_ra W_rb b_rb)
-  float* sWd = sWr + nr;                            // [nd] decoder conv weights (W_da b_da W_db b_db)
+  const int K4p = (K + 3) / 4 * 4;
+  // staged pair sizes: waT C*K*9, ba C, wbT C*9*K4p, bb K4p
+  const int nr = CR ? CR * K * 9 + CR + CR * 9 * K4p + K4p : 0, nd = CD ? CD * K * 9 + CD + CD * 9 * K4p + K4p : 0;
+  float* sWr = rsm;                                 // [nr] residual conv pair, transposed
+  float* sWd = sWr + nr;                            // [nd] decoder conv pair, transposed
   float* su = sWd + nd;                             // [K][UY][UX] up on the grown block
   float* sv = su + K * UY * UX;                     // [K][UY][UX] vit on the grown block (CD > 0)
   float* sh = sv + (CD ? K * UY * UX : 0);          // [max(CR, CD)][BY+2][BX+2] hidden layer
@@ -104,8 +144,8 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   const int nx = min(BX, t.core_w * P - seg * BX);
   const int sH = s * H, sW = s * W;
   const int tid = threadIdx.x;
-  for (int i = tid; i < nr; i += RC_THREADS) sWr[i] = wres[i];
-  for (int i = tid; i < nd; i += RC_THREADS) sWd[i] = wdec[i];
+  if (CR) stage_pair(wres, sWr, sWr + CR * K * 9, sWr + CR * K * 9 + CR, sWr + CR * K * 9 + CR + CR * 9 * K4p, K, CR, K4p);
+  if (CD) stage_pair(wdec, sWd, sWd + CD * K * 9, sWd + CD * K * 9 + CD, sWd + CD * K * 9 + CD + CD * 9 * K4p, K, CD, K4p);
   const float inv_s = 1.0f / (float)s;
   const int64_t tbase = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0);   // tile's output tokens
   const int Nh = K * P * P;
@@ -138,20 +178,27 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   }
   __syncthreads();
   auto in_field = [&](int Y, int X) { return Y >= 0 && Y < sH && X >= 0 && X < sW; };
-  const int ND = K * BY * nx;
+  const int K4 = K4p / 4, NP = BY * nx;
   if (CR) {   // residual path
     conv_hidden(su, sh, sWr, sWr + CR * K * 9, K, CR, BY, Y0, X0, in_field);
     __syncthreads();
     const float* wb = sWr + CR * K * 9 + CR;
-    for (int i = tid; i < ND; i += RC_THREADS) {
-      const int k = i / (BY * nx), r = i - k * BY * nx, al = r / nx, xx = r - al * nx;
-      const float res = su[(k * UY + al + 2) * UX + xx + 2] + conv_out(sh, wb, wb + K * CR * 9, CR, BY, k, al, xx);
-      if (CD) {
-        sres[(k * BY + al) * BX + xx] = res;
-      } else {   // decoder = the linear head: vit straight from tile_out
-        const int xr = X0 - t.core_x0 * P + xx, wr = xr / P, be = xr - wr * P;
-        const float vit = ld_f32<T>(tile_out + (tbase + (int64_t)ur * t.out_w + wr) * Nh + (k * P + al) * P + be);
-        out[(((int64_t)b * K + k) * sH + Y0 + al) * sW + X0 + xx] = vit + res;
+    for (int i = tid; i < K4 * NP; i += RC_THREADS) {
+      const int kg = i / NP, r = i - kg * NP, al = r / nx, xx = r - al * nx;
+      const float4 cv = conv_out4(sh, wb, wb + CR * 9 * K4p, CR, K4, BY, kg, al, xx);
+      const float cvs[4] = {cv.x, cv.y, cv.z, cv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int k = 4 * kg + e;
+        if (k >= K) break;
+        const float res = su[(k * UY + al + 2) * UX + xx + 2] + cvs[e];
+        if (CD) {
+          sres[(k * BY + al) * BX + xx] = res;
+        } else {   // decoder = the linear head: vit straight from tile_out
+          const int xr = X0 - t.core_x0 * P + xx, wr = xr / P, be = xr - wr * P;
+          const float vit = ld_f32<T>(tile_out + (tbase + (int64_t)ur * t.out_w + wr) * Nh + (k * P + al) * P + be);
+          out[(((int64_t)b * K + k) * sH + Y0 + al) * sW + X0 + xx] = vit + res;
+        }
       }
     }
     if (!CD) return;
@@ -163,11 +210,17 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   conv_hidden(sv, sh, sWd, sWd + CD * K * 9, K, CD, BY, Y0, X0, in_out);
   __syncthreads();
   const float* wb = sWd + CD * K * 9 + CD;
-  for (int i = tid; i < ND; i += RC_THREADS) {
-    const int k = i / (BY * nx), r = i - k * BY * nx, al = r / nx, xx = r - al * nx;
-    const float dec = conv_out(sh, wb, wb + K * CD * 9, CD, BY, k, al, xx);
-    const float res = CR ? sres[(k * BY + al) * BX + xx] : su[(k * UY + al + 2) * UX + xx + 2];
-    out[(((int64_t)b * K + k) * sH + Y0 + al) * sW + X0 + xx] = dec + res;
+  for (int i = tid; i < K4 * NP; i += RC_THREADS) {
+    const int kg = i / NP, r = i - kg * NP, al = r / nx, xx = r - al * nx;
+    const float4 dv = conv_out4(sh, wb, wb + CD * 9 * K4p, CD, K4, BY, kg, al, xx);
+    const float dvs[4] = {dv.x, dv.y, dv.z, dv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = 4 * kg + e;
+      if (k >= K) break;
+      const float res = CR ? sres[(k * BY + al) * BX + xx] : su[(k * UY + al + 2) * UX + xx + 2];
+      out[(((int64_t)b * K + k) * sH + Y0 + al) * sW + X0 + xx] = dvs[e] + res;
+    }
   }
 }
 
@@ -177,9 +230,13 @@ template <typename T>
 bool launch_stitch_conv(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap,
                         const float* wres, const float* wdec, int B, int V, int H, int W, int K, int s, int P, int CR,
                         int CD, int max_core_h, int max_core_w, cudaStream_t st) {
-  if (CR < 0 || CD < 0 || (CR == 0 && CD == 0)) return false;
+  // hidden channels are computed 4 at a time (the planner accepts any 0..64; others are
+  // rejected here, E_CUDA "launch configuration rejected")
+  if (CR < 0 || CD < 0 || (CR == 0 && CD == 0) || CR % 4 || CD % 4) return false;
   const int nseg = (max_core_w * P + BX - 1) / BX;
-  const size_t nr = CR ? (size_t)CR * K * 18 + CR + K : 0, nd = CD ? (size_t)CD * K * 18 + CD + K : 0;
+  const size_t K4p = (size_t)(K + 3) / 4 * 4;
+  const size_t nr = CR ? (size_t)CR * K * 9 + CR + (size_t)CR * 9 * K4p + K4p : 0;
+  const size_t nd = CD ? (size_t)CD * K * 9 + CD + (size_t)CD * 9 * K4p + K4p : 0;
   const size_t up = (size_t)K * (P + 4) * (BX + 4);
   const size_t smem = sizeof(float) * (nr + nd + up + (CD ? up : 0) + (size_t)std::max(CR, CD) * (P + 2) * (BX + 2) +
                                        (CD && CR ? (size_t)K * P * BX : 0));

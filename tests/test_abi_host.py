@@ -160,8 +160,9 @@ def test_residual_conv_config_counts_and_halo(o2):
     _, info = o2.orbit2_tiles_plan(o2.config_from(w))
     assert info.canonical_weight_count == weight_count(w)
     assert info.canonical_weight_count == weight_count(w.replace(res_hidden=0)) + 18 * 8 * w.K + 8 + w.K
-    with pytest.raises(o2.Orbit2Error, match="res_hidden"):
-        o2.orbit2_tiles_plan(o2.config_from(w, res_hidden=65))
+    for bad in (65, 6):
+        with pytest.raises(o2.Orbit2Error, match="res_hidden"):
+            o2.orbit2_tiles_plan(o2.config_from(w, res_hidden=bad))
     w0 = get_config("C1", H=36, W=60, tiles_y=3, tiles_x=4, halo=0, res_hidden=4)
     dil = 1 + -(-2 // w0.scale)
     for R in (2, 3):

@@ -365,7 +365,7 @@ RCONV = [
     # decoder convolutions (R32): head on core + ring, conv(GELU(conv)) per tile
     ("C1", dict(dec_hidden=4)),
     ("C1", dict(dec_hidden=4, res_hidden=4, tiles_y=3, tiles_x=5, halo=1)),
-    ("C1", dict(dec_hidden=3, halo_mode=1)),
+    ("C1", dict(dec_hidden=4, halo_mode=1)),
     ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=2, dec_hidden=8, res_hidden=8)),
 ]
 
