@@ -528,7 +528,10 @@ def run_sp(args, w, world, rank, local):
     # Work split of a rank's share: G sample groups x all its tiles (kernels keep B/G x n_local
     # tile-samples per launch; the last group's stitch, the only one not overlapped with
     # compute, carries 1/G of the rank's output), or, for small batches, <= 4 tile chunks.
-    groups = args.sp_groups if args.sp_groups > 0 else (4 if B % 4 == 0 and B >= 16 else 1)
+    # default: the most groups (<= 4) that keep >= 4 waves of 128-row blocks per launch
+    rows_min = 4 * 148 * 128
+    groups = args.sp_groups if args.sp_groups > 0 else next(
+        g for g in (4, 2, 1) if B % g == 0 and (g == 1 or (B // g) * info0.local_tokens >= rows_min))
     chunk = args.chunk if args.chunk > 0 else (0 if groups > 1 else max(1, -(-n_local // 4)))
     cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world, rank=rank, chunk_tiles=chunk)
     ctx = o2.Context(cfg)
