@@ -17,6 +17,13 @@ What is computed (the method, step by step, in the paper's order):
   O2 gather    -- padded tile pixels           P:530 (Fig.4 caption P:515)
   O3 embed     -- patch tokens + res-embedding + sincos position
                   P:475-479 [Reslim main path], P:150 (p=2), R1, R2, R7, R8
+  O3b variable aggregation (optional, var_agg = 1) -- P:479 "the main path uses a
+                  cross-attention module to aggregate multi-variable embeddings into
+                  a unified representation, effectively collapsing the variable
+                  dimension", reading R33: per-variable tokens t_v = W_t[v] a_v +
+                  e_var[v]; one learned query attends over the V tokens of each
+                  patch (multi-head, keys / values W_ak t + b_ak, W_av t + b_av);
+                  z0 = W_ao o + b_ao + e_s + pi(u, w)  (replaces W_e a + b_e)
   O4 blocks    -- pre-norm MHSA + GELU MLP, attention restricted to the tile
                   P:54, P:404, P:527 ("self-attention is restricted within
                   each tile"), R9, R17, R18
@@ -163,15 +170,38 @@ def patch_tokens(xt: np.ndarray, p: int) -> np.ndarray:
     return a.reshape(ph * pw, V * p * p)
 
 
-def embed_tile(xt: np.ndarray, tile: Tile, p: int, Wt: dict) -> np.ndarray:
+def aggregate_variables(a: np.ndarray, Wt: dict, heads: int, p: int) -> np.ndarray:
+    """O3b (R33): a [n, V*p*p] patch rows -> [n, D].  Per-variable tokens
+    t_v = W_t[v] a_v + e_var[v]; per head h a learned query q_h scores the V
+    tokens, s_{h,v} = <q_h, (W_ak t_v + b_ak)_h> / sqrt(d); softmax over v;
+    o_h = sum_v alpha_{h,v} (W_av t_v + b_av)_h; result W_ao o + b_ao."""
+    n = a.shape[0]
+    V, D = Wt["W_t"].shape[0], Wt["W_t"].shape[1]
+    d = D // heads
+    pp = p * p
+    t = np.stack([a[:, v * pp:(v + 1) * pp] @ Wt["W_t"][v].T + Wt["e_var"][v] for v in range(V)], axis=1)  # [n,V,D]
+    k = t @ Wt["W_ak"].T + Wt["b_ak"]
+    val = t @ Wt["W_av"].T + Wt["b_av"]
+    o = np.zeros((n, D))
+    for h in range(heads):
+        sl = slice(h * d, (h + 1) * d)
+        sc = k[:, :, sl] @ Wt["q_agg"][sl] / math.sqrt(d)              # [n, V]
+        al = softmax_rows(sc)
+        o[:, sl] = np.einsum("nv,nvd->nd", al, val[:, :, sl])
+    return o @ Wt["W_ao"].T + Wt["b_ao"]
+
+
+def embed_tile(xt: np.ndarray, tile: Tile, p: int, Wt: dict, heads: int = 1) -> np.ndarray:
     """z0 = W_e a + b_e + e_s + pi(u,w)   (resolution embedding 'added to
-    the feature embedding')."""
+    the feature embedding'); with the variable aggregation (O3b) the joint
+    linear W_e a + b_e is replaced by aggregate_variables(a)."""
     a = patch_tokens(xt, p)
     D = Wt["W_e"].shape[0]
     uu, ww = np.meshgrid(np.arange(tile.pad_y0, tile.pad_y1),
                          np.arange(tile.pad_x0, tile.pad_x1), indexing="ij")
     pos = sincos_pos(uu.ravel(), ww.ravel(), D)
-    return a @ Wt["W_e"].T + Wt["b_e"] + Wt["e_s"] + pos
+    feat = aggregate_variables(a, Wt, heads, p) if "W_t" in Wt else a @ Wt["W_e"].T + Wt["b_e"]
+    return feat + Wt["e_s"] + pos
 
 
 # ---------------------------------------------------------------------------
@@ -307,7 +337,7 @@ def residual_conv(up: np.ndarray, Wt: dict) -> np.ndarray:
 # Canonical weight blob -> named fp64 arrays (order: include/orbit2.h, restated here)
 # ---------------------------------------------------------------------------
 def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int, K: int = 0,
-                   res_hidden: int = 0, dec_hidden: int = 0) -> dict:
+                   res_hidden: int = 0, dec_hidden: int = 0, var_agg: int = 0, V: int = 0) -> dict:
     blob = np.asarray(blob, dtype=np.float64)
     F = 4 * D
     off = 0
@@ -337,6 +367,12 @@ def unpack_weights(blob: np.ndarray, D: int, L: int, din: int, n_head: int, K: i
     if dec_hidden:   # O5b: W_da[C_d][K][3][3], b_da[C_d], W_db[K][C_d][3][3], b_db[K]
         Wt["W_da"], Wt["b_da"] = take(dec_hidden, K, 3, 3), take(dec_hidden)
         Wt["W_db"], Wt["b_db"] = take(K, dec_hidden, 3, 3), take(K)
+    if var_agg:      # O3b: W_t[V][D][p*p], e_var[V][D], q_agg[D], W_ak, b_ak, W_av, b_av, W_ao, b_ao
+        pp = din // V
+        Wt["W_t"], Wt["e_var"], Wt["q_agg"] = take(V, D, pp), take(V, D), take(D)
+        Wt["W_ak"], Wt["b_ak"] = take(D, D), take(D)
+        Wt["W_av"], Wt["b_av"] = take(D, D), take(D)
+        Wt["W_ao"], Wt["b_ao"] = take(D, D), take(D)
     if off != blob.size:
         raise ValueError(f"weight blob has {blob.size} values, layout needs {off}")
     return Wt
@@ -365,13 +401,14 @@ class Problem:
     channel_map: tuple | None = None
     res_hidden: int = 0      # O8 hidden channels (0: no residual convolutions)
     dec_hidden: int = 0      # O5b hidden channels (0: linear decoder head only)
+    var_agg: int = 0         # O3b per-variable tokens + cross-attention aggregation (R33)
 
     @classmethod
     def from_config(cls, cfg) -> "Problem":
         return cls(cfg.H, cfg.W, cfg.V, cfg.K, cfg.scale, cfg.patch, cfg.tiles_y, cfg.tiles_x,
                    cfg.halo, cfg.embed, cfg.depth, cfg.heads, cfg.halo_mode,
                    tuple(cfg.out_channel_map) if cfg.out_channel_map is not None else None,
-                   getattr(cfg, "res_hidden", 0), getattr(cfg, "dec_hidden", 0))
+                   getattr(cfg, "res_hidden", 0), getattr(cfg, "dec_hidden", 0), getattr(cfg, "var_agg", 0))
 
     @property
     def P(self) -> int:
@@ -386,7 +423,8 @@ class Problem:
 
     def weights(self, blob) -> dict:
         return unpack_weights(blob, self.embed, self.depth, self.V * self.patch ** 2,
-                              self.K * self.P * self.P, self.K, self.res_hidden, self.dec_hidden)
+                              self.K * self.P * self.P, self.K, self.res_hidden, self.dec_hidden, self.var_agg,
+                              self.V)
 
 
 def decoder_rect(tile: Tile, pr: Problem):
@@ -400,7 +438,7 @@ def decoder_rect(tile: Tile, pr: Problem):
 
 def tile_forward(x_b: np.ndarray, tile: Tile, pr: Problem, Wt: dict) -> np.ndarray:
     """Steps O2-O5 (+ O5b) for one tile of one sample: returns g [n_core, K*P*P]."""
-    z = embed_tile(gather_tile(x_b, tile, pr.patch), tile, pr.patch, Wt)
+    z = embed_tile(gather_tile(x_b, tile, pr.patch), tile, pr.patch, Wt, pr.heads)
     for Lw in Wt["layers"]:
         z = block(z, Lw, pr.heads)
     if not pr.dec_hidden:
@@ -488,7 +526,8 @@ def global_forward(x: np.ndarray, blob: np.ndarray, pr: Problem) -> np.ndarray:
     for b in range(B):
         a = patch_tokens(x[b].astype(np.float64), p)
         uu, ww = np.meshgrid(np.arange(Hp), np.arange(Wp), indexing="ij")
-        z = a @ Wt["W_e"].T + Wt["b_e"] + Wt["e_s"] + sincos_pos(uu.ravel(), ww.ravel(), pr.embed)
+        feat = aggregate_variables(a, Wt, pr.heads, p) if pr.var_agg else a @ Wt["W_e"].T + Wt["b_e"]
+        z = feat + Wt["e_s"] + sincos_pos(uu.ravel(), ww.ravel(), pr.embed)
         for Lw in Wt["layers"]:
             z = block(z, Lw, pr.heads)
         g = head(z, Wt)

@@ -39,7 +39,7 @@ def blob_for(pr, seed=7, head_gain=1.0, sharp=True, res_gain=1.0):
     cfg = get_config("C1", H=pr.H, W=pr.W, V=pr.V, K=pr.K, scale=pr.scale, patch=pr.patch,
                      tiles_y=pr.tiles_y, tiles_x=pr.tiles_x, halo=pr.halo, embed=pr.embed,
                      depth=pr.depth, heads=pr.heads, halo_mode=pr.halo_mode, res_hidden=pr.res_hidden,
-                     dec_hidden=pr.dec_hidden)
+                     dec_hidden=pr.dec_hidden, var_agg=pr.var_agg)
     return make_weights(cfg, seed=seed, head_gain=head_gain, sharp=sharp, res_gain=res_gain), cfg
 
 
@@ -644,3 +644,56 @@ def test_decoder_convs_full_halo_equals_global_and_locality():
     mask[max(0, t.pad_y0 * pr.patch):t.pad_y1 * pr.patch, max(0, t.pad_x0 * pr.patch):t.pad_x1 * pr.patch] = False
     x2[0][:, mask] -= 3.0
     assert np.array_equal(a[3], O.tiles_forward_sampled(x2[0], blob, pr, [1])[1][3])
+
+
+# ---------------------------------------------------------------- O3b variable aggregation (R33)
+def test_variable_aggregation_matches_torch_multihead_attention():
+    """O3b against torch.nn.functional.multi_head_attention_forward (fp64): one learned
+    query per patch (identity query projection), keys / values = the V per-variable
+    tokens t_v = W_t[v] a_v + e_var[v] with in-projections W_ak / W_av, output
+    projection W_ao -- the library routine the paper's citation (ClimaX) uses."""
+    pr = small_problem(var_agg=1, V=5, embed=16, heads=4)
+    blob, cfg = blob_for(pr)
+    Wt = pr.weights(blob)
+    rng = np.random.default_rng(5)
+    n, pp, D = 7, pr.patch ** 2, pr.embed
+    a = rng.standard_normal((n, pr.V * pp))
+    got = O.aggregate_variables(a, Wt, pr.heads, pr.patch)
+    t = np.stack([a[:, v * pp:(v + 1) * pp] @ Wt["W_t"][v].T + Wt["e_var"][v] for v in range(pr.V)], axis=0)  # [V,n,D]
+    q = np.broadcast_to(Wt["q_agg"], (1, n, D)).copy()
+    in_w = np.concatenate([np.eye(D), Wt["W_ak"], Wt["W_av"]])
+    in_b = np.concatenate([np.zeros(D), Wt["b_ak"], Wt["b_av"]])
+    T = lambda z: torch.from_numpy(np.ascontiguousarray(z))
+    want, _ = F.multi_head_attention_forward(T(q), T(t), T(t), D, pr.heads, T(in_w), T(in_b), None, None, False,
+                                             0.0, T(Wt["W_ao"]), T(Wt["b_ao"]), training=False, need_weights=False)
+    np.testing.assert_allclose(got, want[0].numpy(), rtol=1e-11, atol=1e-11)
+    # identical variable tokens -> uniform weights: the result is the value path of one token
+    a1 = np.tile(a[:, :pp], (1, pr.V))
+    W1 = dict(Wt, W_t=np.repeat(Wt["W_t"][:1], pr.V, 0), e_var=np.repeat(Wt["e_var"][:1], pr.V, 0))
+    one = (a1[:, :pp] @ W1["W_t"][0].T + W1["e_var"][0]) @ Wt["W_av"].T + Wt["b_av"]
+    np.testing.assert_allclose(O.aggregate_variables(a1, W1, pr.heads, pr.patch), one @ Wt["W_ao"].T + Wt["b_ao"],
+                               rtol=1e-12, atol=1e-12)
+
+
+def test_variable_aggregation_permutation_and_tiling():
+    """Permuting the input variables together with their tokenizer weights and
+    variable embeddings leaves the pass unchanged (the aggregation is a set
+    function of the variables); the sampled-tile path equals the full pass."""
+    pr = small_problem(var_agg=1, V=4, tiles_y=2, tiles_x=2, halo=1)
+    blob, cfg = blob_for(pr)
+    x = input_for(cfg)
+    out = O.tiles_forward(x, blob, pr)
+    perm = [2, 0, 3, 1]
+    Wt = pr.weights(blob)
+    n_agg = pr.V * pr.embed * pr.patch ** 2 + pr.V * pr.embed + pr.embed + 3 * (pr.embed ** 2 + pr.embed)
+    tail = blob[-n_agg:].copy()
+    D, pp = pr.embed, pr.patch ** 2
+    wt = tail[:pr.V * D * pp].reshape(pr.V, D, pp)[perm]
+    ev = tail[pr.V * D * pp:pr.V * D * pp + pr.V * D].reshape(pr.V, D)[perm]
+    tail2 = np.concatenate([wt.ravel(), ev.ravel(), tail[pr.V * D * pp + pr.V * D:]])
+    blob2 = np.concatenate([blob[:-n_agg], tail2]).astype(blob.dtype)
+    x2 = x[:, perm]
+    pr2 = O.Problem(**{**pr.__dict__, "channel_map": tuple(perm.index(k) for k in range(pr.K))})
+    np.testing.assert_allclose(O.tiles_forward(x2, blob2, pr2), out, rtol=1e-10, atol=1e-10)
+    res = O.tiles_forward_sampled(x[0], blob, pr, [3])[3]
+    assert np.array_equal(res[2], out[0][:, res[0], res[1]])

@@ -50,6 +50,7 @@ class Config:
     out_channel_map: tuple | None = None   # K entries in [0,V); None = identity
     res_hidden: int = 0         # residual-path conv hidden channels (reading R31); 0 = none
     dec_hidden: int = 0         # decoder conv hidden channels (reading R32); 0 = linear head only
+    var_agg: int = 0            # per-variable tokens + cross-attention aggregation (reading R33)
 
     @property
     def mlp_hidden(self) -> int:
@@ -176,6 +177,8 @@ def weight_count(cfg: Config) -> int:
     for c in (cfg.res_hidden, cfg.dec_hidden):
         if c:
             n += 2 * 9 * c * cfg.K + c + cfg.K
+    if cfg.var_agg:
+        n += cfg.V * D * cfg.patch ** 2 + cfg.V * D + D + 3 * (D * D + D)
     return n
 
 
@@ -235,6 +238,13 @@ def make_weights(cfg: Config, seed: int | None = None, sharp: bool = True,
     if cfg.dec_hidden:                                # decoder convs W_da, b_da, W_db, b_db
         lin(cfg.dec_hidden, cfg.K * 9); bias(cfg.dec_hidden)
         lin(cfg.K, cfg.dec_hidden * 9); bias(cfg.K)
+    if cfg.var_agg:                                   # variable aggregation (R33)
+        pp = cfg.patch ** 2
+        parts.append((rng.standard_normal((cfg.V, D, pp)) / math.sqrt(pp)).ravel())   # W_t[v]
+        parts.append(rng.standard_normal(cfg.V * D) * 0.5)                            # e_var
+        parts.append(rng.standard_normal(D) * 2.0)                                    # q_agg (sharp-ish)
+        for _ in range(3):                                                             # W_ak, W_av, W_ao + biases
+            lin(D, D); bias(D)
     blob = np.concatenate(parts).astype(np.float32)
     assert blob.size == weight_count(cfg)
     return bf16_round(blob) if round_bf16 else blob
