@@ -91,6 +91,9 @@ typedef struct {
                               unpatchified head output of a tile's core + a ring of
                               ceil(2/P) patches; 0 <= C_d <= 64, C_d % 4 == 0 (needs halo >= that
                               ring); 0 = the linear head alone (R11) */
+  int32_t var_agg;         /* 1: per-variable tokens + cross-attention variable
+                              aggregation replace the joint patch embedding (P:479,
+                              reading R33); 0: joint linear embedding (R1) */
   const int32_t *out_channel_map; /* K entries in [0,V) selecting the residual input
                                      channel of each output variable (R13); NULL = identity */
 } orbit2_config;
@@ -175,6 +178,8 @@ orbit2_status orbit2_create(const orbit2_config *cfg, void *workspace_dev, size_
  *   lnf_g[D] lnf_b[D] W_h[K*P*P][D] (row (k*P+a)*P+b, P = s*p) b_h[K*P*P]
  *   if res_hidden = C_r > 0: W_ra[C_r][K][3][3] b_ra[C_r] W_rb[K][C_r][3][3] b_rb[K]
  *   if dec_hidden = C_d > 0: W_da[C_d][K][3][3] b_da[C_d] W_db[K][C_d][3][3] b_db[K]
+ *   if var_agg: W_t[V][D][p*p] e_var[V][D] q_agg[D] W_ak[D][D] b_ak[D] W_av[D][D] b_av[D]
+ *               W_ao[D][D] b_ao[D]   (W_e and b_e are then unused)
  * Count = Din*D + 2D + L*(12D^2 + 13D) + 2D + D*K*P^2 + K*P^2 (+ 18 C K + C + K per
  * convolution pair),
  * Din = V*p*p.

@@ -83,6 +83,14 @@ template <typename T>
 bool launch_stitch_conv(const T* tile_out, const float* x, float* out, const ChunkDev& ch, const int32_t* cmap,
                         const float* wres, const float* wdec, int B, int V, int H, int W, int K, int s, int P, int CR,
                         int CD, int max_core_h, int max_core_w, cudaStream_t st);
+// R33 variable aggregation as one GEMM (varagg.cu): fused weights at prepare time,
+// per-token score / softmax prologue writing the GEMM A rows
+template <typename T>
+bool launch_agg_prepare(const float* canon, const float* e_s, T* Bm, float* w, float* cc, float* bias, int V, int D,
+                        int H, int pp, int KA, cudaStream_t st);
+template <typename T>
+bool launch_agg_prologue(const T* patches, int64_t ldp, T* agg, int64_t lda, const float* w, const float* cc,
+                         int64_t M, int V, int H, int pp, cudaStream_t st);
 bool make_tmap_f32_3d(CUtensorMap* map, const void* ptr, int64_t d0, int64_t d1, int64_t d2, int b0, int b1,
                       int b2);
 template <typename T>

@@ -349,6 +349,21 @@ orbit2_status orbit2_prepare_weights(void* ctx, const float* canonical_dev, void
   ORBIT2_TRY(conv(w.c_lnf_b, w.lnf_b, 1, D, D, 0));
   ORBIT2_TRY(conv(w.c_w_h, w.w_h, p.Nh, D, D, bf));
   ORBIT2_TRY(conv(w.c_b_h, w.b_h, 1, p.Nh, p.Nh, 0));
+  if (p.cfg.var_agg) {   // R33: fold tokenizer + key / value / output projections into the GEMM weights
+    const int pp = p.cfg.patch * p.cfg.patch;
+    ORBIT2_TRY(run(c, "prepare_weights", st, [&] {
+      float* fw = reinterpret_cast<float*>(pk + w.agg_w);
+      float* fc = reinterpret_cast<float*>(pk + w.agg_c);
+      float* fb = reinterpret_cast<float*>(pk + w.bias_e);
+      if (bf)
+        return launch_agg_prepare<__nv_bfloat16>(canonical_dev + w.c_agg, canonical_dev + w.c_e_s,
+                                                 reinterpret_cast<__nv_bfloat16*>(pk + w.agg_b), fw, fc, fb,
+                                                 p.cfg.V, p.D, p.cfg.heads, pp, p.lay.k_agg_pad, st);
+      return launch_agg_prepare<float>(canonical_dev + w.c_agg, canonical_dev + w.c_e_s,
+                                       reinterpret_cast<float*>(pk + w.agg_b), fw, fc, fb, p.cfg.V, p.D, p.cfg.heads,
+                                       pp, p.lay.k_agg_pad, st);
+    }));
+  }
   // R31 / R32 convolutions: fp32 into the packed blob and the workspace (orbit2_stitch reads them there)
   const int32_t convs[2] = {p.cfg.res_hidden, p.cfg.dec_hidden};
   const int64_t c_off[2] = {w.c_rconv, w.c_dconv}, p_off[2] = {w.rconv, w.dconv}, ws_off[2] = {p.lay.rconv, p.lay.dconv};
@@ -437,6 +452,21 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       cudaError_t e = cudaMemsetAsync(qkv + M * 3 * D, 0, (size_t)(mrow - M) * 3 * D * sizeof(bf16), st);
       if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("memset: ") + cudaGetErrorString(e));
     }
+    // the embedding GEMM's A / B operands: patch rows x W_e, or (R33) the aggregation
+    // rows [alpha a | alpha] x the folded [G | E]
+    const void* embA = patches;
+    int64_t embW = w.w_e, embK = ly.din_pad, embLd = lda_patch, embCols = cols_patch;
+    if (cf.var_agg) {
+      bf16* agg = c->at<bf16>(ly.agg);
+      ORBIT2_TRY(run(c, "var_aggregate", st, [&] {
+        return launch_agg_prologue<bf16>(patches, lda_patch, agg, ly.k_agg_pad, wf(w.agg_w), wf(w.agg_c), M, cf.V,
+                                         cf.heads, cf.patch * cf.patch, st);
+      }));
+      embA = agg;
+      embW = w.agg_b;
+      embK = embLd = ly.k_agg_pad;
+      embCols = 0;
+    }
     // D == 256: one GEMM tile holds whole rows, so LayerNorms that follow a GEMM
     // run in its epilogue (embed -> LN1 of block 0, O-projection -> LN2)
     const bool ln_fused = D == 256 && !c->unfused_ln;
@@ -445,11 +475,9 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       e.xn = xn;
       e.ln_g = wf(w.layers[0].ln1_g);
       e.ln_b = wf(w.layers[0].ln1_b);
-      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED_LN, 0, patches, mrow, lda_patch, w.w_e, D, ly.din_pad, M, e,
-                      cols_patch));
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED_LN, 0, embA, mrow, embLd, embW, D, embK, M, e, embCols));
     } else {
-      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, patches, mrow, lda_patch, w.w_e, D, ly.din_pad, M, emb,
-                      cols_patch));
+      ORBIT2_TRY(gemm("embed_gemm", EPI_EMBED, 0, embA, mrow, embLd, embW, D, embK, M, emb, embCols));
     }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
@@ -544,7 +572,16 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
                            p.max_pad_h, st);
       return true;
     }));
-    ORBIT2_TRY(sg("embed_gemm", EPI_EMBED, patches, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    if (cf.var_agg) {   // R33 (fp32 path)
+      float* agg = c->at<float>(ly.agg);
+      ORBIT2_TRY(run(c, "var_aggregate", st, [&] {
+        return launch_agg_prologue<float>(patches, ly.din_pad, agg, ly.k_agg_pad, wf(w.agg_w), wf(w.agg_c), M, cf.V,
+                                          cf.heads, cf.patch * cf.patch, st);
+      }));
+      ORBIT2_TRY(sg("embed_gemm", EPI_EMBED, agg, ly.k_agg_pad, w.agg_b, D, ly.k_agg_pad, M, emb));
+    } else {
+      ORBIT2_TRY(sg("embed_gemm", EPI_EMBED, patches, ly.din_pad, w.w_e, D, ly.din_pad, M, emb));
+    }
     for (int l = 0; l < cf.depth; ++l) {
       const LayerW& L = w.layers[l];
       ORBIT2_TRY(run(c, "layernorm", st, [&] {

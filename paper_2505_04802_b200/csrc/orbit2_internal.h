@@ -55,6 +55,8 @@ struct Layout {
   int64_t mrow, mcore;        // rows of the token and core-token buffers
   int32_t din_pad;            // K of the embedding GEMM: round_up(Din, 64)
   int32_t ld_patch;           // row stride of TMA-gathered bf16 patch rows: round_up(Din, 8)
+  int32_t k_agg_pad;          // R33: K of the aggregation GEMM (round_up(H V (p^2 + 1), 64)); 0 = off
+  int64_t agg;                // R33: aggregation A-operand rows [rows][k_agg_pad]
   int32_t esize;              // activation element size (2 bf16, 4 fp32)
 };
 
@@ -94,6 +96,7 @@ struct Plan {
   orbit2_plan_info info;
   Layout lay;
   int32_t Hp, Wp, P, D, d, Din, Nh, max_pad_h, max_pad_w, max_core_h, max_core_w;
+  int32_t k_agg = 0;                    // R33: H V (p^2 + 1)
   // multi-rank: every rank's device tile table (for orbit2_stitch_peer) and
   // this rank's transfer rectangle lists
   std::vector<std::vector<DevTile>> dev_by_rank;   // with sentinel
@@ -125,10 +128,11 @@ struct LayerW {
 struct WeightLayout {
   int64_t w_e, bias_e, lnf_g, lnf_b, w_h, b_h;
   int64_t rconv, dconv;       // residual / decoder convolution weights (fp32 copies of the canonical tail)
+  int64_t agg_b, agg_w, agg_c;  // R33 fused aggregation: GEMM B [D][k_agg_pad], score weights, score offsets
   std::vector<LayerW> layers;
   int64_t total;
   // canonical (fp32 element) offsets, same names
-  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h, c_rconv, c_dconv;
+  int64_t c_w_e, c_b_e, c_e_s, c_lnf_g, c_lnf_b, c_w_h, c_b_h, c_rconv, c_dconv, c_agg;
   std::vector<LayerW> c_layers;
   int64_t c_total;
 };

@@ -59,6 +59,7 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
     return fail(msg, "res_hidden: must be a multiple of 4 in [0, 64]");
   if (c->dec_hidden < 0 || c->dec_hidden > 64 || c->dec_hidden % 4)
     return fail(msg, "dec_hidden: must be a multiple of 4 in [0, 64]");
+  if (c->var_agg != 0 && c->var_agg != 1) return fail(msg, "var_agg: must be 0 or 1");
   if (c->dec_hidden > 0 && c->halo < (2 + c->scale * c->patch - 1) / (c->scale * c->patch))
     return fail(msg, "halo: the decoder convolutions need halo >= ceil(2 / (scale * patch)) patches");
   if (c->out_channel_map) {
@@ -349,7 +350,16 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
                               (int64_t)c.depth * (12LL * p.D * p.D + 13LL * p.D) + 2LL * p.D +
                               (int64_t)p.D * p.Nh + p.Nh +
                               (c.res_hidden ? 18LL * c.res_hidden * c.K + c.res_hidden + c.K : 0) +
-                              (c.dec_hidden ? 18LL * c.dec_hidden * c.K + c.dec_hidden + c.K : 0);
+                              (c.dec_hidden ? 18LL * c.dec_hidden * c.K + c.dec_hidden + c.K : 0) +
+                              (c.var_agg ? (int64_t)c.V * p.D * c.patch * c.patch + (int64_t)c.V * p.D + p.D +
+                                               3LL * ((int64_t)p.D * p.D + p.D) : 0);
+  if (c.var_agg) {   // R33: the aggregation replaces the joint embedding (2 Din D per token):
+    // tokenize + key/value projections + scores + weighted sum + output projection
+    const double Vd = c.V, pp = (double)c.patch * c.patch;
+    const double per_tok = 2.0 * Vd * pp * D + 4.0 * Vd * D * D + 4.0 * Vd * D + 2.0 * D * D - 2.0 * p.Din * D;
+    in.flops_per_sample += per_tok * (double)tok;
+    in.local_flops_per_sample += per_tok * (double)ltok;
+  }
   {   // the 3x3 convolution pairs on every output pixel (R31 residual, R32 decoder)
     const double cc = (double)c.res_hidden + c.dec_hidden;
     double lc = 0;
@@ -362,6 +372,9 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   Layout& ly = p.lay;
   ly.esize = c.precision == ORBIT2_BF16 ? 2 : 4;
   ly.din_pad = (int32_t)round_up(p.Din, 64);
+  // R33 aggregation as one GEMM: A row = [alpha_{h,v} a_v (H V p^2) | alpha_{h,v} (H V)], K padded to 64
+  p.k_agg = c.var_agg ? c.heads * c.V * (c.patch * c.patch + 1) : 0;
+  ly.k_agg_pad = c.var_agg ? (int32_t)round_up(p.k_agg, 64) : 0;
   ly.ld_patch = (int32_t)round_up(p.Din, 8);
   ly.mrow = round_up(std::max<int64_t>(1, (int64_t)c.batch * in.max_chunk_tokens), kQBlock);
   ly.mcore = round_up(std::max<int64_t>(1, (int64_t)c.batch * in.max_chunk_core_tokens), kQBlock);
@@ -373,6 +386,7 @@ orbit2_status build_plan(const orbit2_config* cfg, Plan* pl, std::string* msg) {
   ly.sig = take(2LL * c.world_size * 8 + 64);
   ly.rowinfo = take(ly.mrow * 8);
   ly.patches = take(ly.mrow * ly.din_pad * E);
+  ly.agg = take(c.var_agg ? ly.mrow * ly.k_agg_pad * E : 0);
   ly.z = take(ly.mrow * (int64_t)p.D * 4);
   ly.xn = take(ly.mrow * (int64_t)p.D * E);
   ly.qkv = take(ly.mrow * 3LL * p.D * E);
@@ -512,6 +526,12 @@ WeightLayout weight_layout(const Plan& p) {
   w.rconv = CR ? take((18 * CR * K + CR + K) * 4) : 0;   // fp32, canonical order (W_ra b_ra W_rb b_rb)
   const int64_t CD = p.cfg.dec_hidden;
   w.dconv = CD ? take((18 * CD * K + CD + K) * 4) : 0;   // fp32 (W_da b_da W_db b_db)
+  // R33 fused aggregation: B operand [D][k_agg_pad] (G | E), score weights w[H V p^2] and
+  // offsets c[H V] (fp32); the fused bias goes into bias_e
+  const int64_t KA = p.lay.k_agg_pad, HVP = (int64_t)p.cfg.heads * p.cfg.V * p.cfg.patch * p.cfg.patch;
+  w.agg_b = p.cfg.var_agg ? take(D * KA * E) : 0;
+  w.agg_w = p.cfg.var_agg ? take(HVP * 4) : 0;
+  w.agg_c = p.cfg.var_agg ? take((int64_t)p.cfg.heads * p.cfg.V * 4) : 0;
   w.total = off;
   // canonical fp32 element offsets (include/orbit2.h order)
   int64_t c = 0;
@@ -531,6 +551,8 @@ WeightLayout weight_layout(const Plan& p) {
   w.c_w_h = ctake(Nh * D); w.c_b_h = ctake(Nh);
   w.c_rconv = CR ? ctake(18 * CR * K + CR + K) : 0;
   w.c_dconv = CD ? ctake(18 * CD * K + CD + K) : 0;
+  const int64_t Vv = p.cfg.V, pp2 = (int64_t)p.cfg.patch * p.cfg.patch;
+  w.c_agg = p.cfg.var_agg ? ctake(Vv * D * pp2 + Vv * D + D + 3 * (D * D + D)) : 0;
   w.c_total = c;
   return w;
 }

@@ -1,0 +1,190 @@
+// varagg.cu -- per-variable tokens + cross-attention variable aggregation (P:479,
+// reading R33) as ONE dense contraction.
+//
+// The oracle's O3b (plain form):  t_v = W_t[v] a_v + e_var[v];
+//   s_{h,v} = <q_h, (W_ak t_v + b_ak)_h> / sqrt(d);  alpha = softmax_v(s_h);
+//   o_h = sum_v alpha_{h,v} (W_av t_v + b_av)_h;     z0 = W_ao o + b_ao (+ e_s + pi)
+// Every step except the softmax is linear in the patch values a_v, so with
+//   w_{h,v} = W_t[v]^T W_ak,h^T q_h / sqrt(d)             (p^2 numbers)
+//   c_{h,v} = q_h . (W_ak,h e_var[v] + b_ak,h) / sqrt(d)
+//   G_{h,v} = W_ao[:, h] W_av,h W_t[v]                   (D x p^2)
+//   E_{h,v} = W_ao[:, h] W_av,h e_var[v]                 (D)
+//   bias    = W_ao b_av + b_ao + e_s
+// the aggregation is exactly (sum alpha = 1)
+//   s_{h,v} = w_{h,v} . a_v + c_{h,v};  alpha = softmax_v(s_h)
+//   z0 = [G | E] . [alpha_{h,v} a_v ; alpha_{h,v}] + bias + pi
+// i.e. a per-token prologue (H V p^2 multiply-adds + H V exponentials) and one
+// tcgen05 GEMM of K = H V (p^2 + 1) -- the tokenizer and the H V (2 D^2) key /
+// value projections per token are folded into weights at orbit2_prepare_weights.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "kernels.h"
+
+namespace orbit2 {
+
+namespace {
+
+// Canonical block (fp32): W_t[V][D][pp] e_var[V][D] q[D] W_ak[D][D] b_ak[D] W_av[D][D] b_av[D] W_ao[D][D] b_ao[D]
+struct AggCanon {
+  const float *wt, *ev, *q, *wak, *bak, *wav, *bav, *wao, *bao;
+};
+__host__ __device__ inline AggCanon agg_canon(const float* c, int V, int D, int pp) {
+  AggCanon a;
+  a.wt = c;
+  a.ev = a.wt + (int64_t)V * D * pp;
+  a.q = a.ev + (int64_t)V * D;
+  a.wak = a.q + D;
+  a.bak = a.wak + (int64_t)D * D;
+  a.wav = a.bak + D;
+  a.bav = a.wav + (int64_t)D * D;
+  a.wao = a.bav + D;
+  a.bao = a.wao + (int64_t)D * D;
+  return a;
+}
+
+// one block per GEMM-B column: G_{h,v}[:, pix] or E_{h,v} (or a zero pad column)
+template <typename T>
+__global__ void agg_bcol_kernel(const float* __restrict__ canon, T* __restrict__ Bm, int V, int D, int H, int pp,
+                                int KA) {
+  extern __shared__ float y[];            // [d]
+  const AggCanon a = agg_canon(canon, V, D, pp);
+  const int d = D / H, col = blockIdx.x;
+  const int nG = H * V * pp, nE = H * V;
+  if (col >= nG + nE) {                   // K padding
+    for (int r = threadIdx.x; r < D; r += blockDim.x) Bm[(int64_t)r * KA + col] = (T)0.f;
+    return;
+  }
+  int h, v, pix = -1;
+  if (col < nG) {
+    h = col / (V * pp);
+    const int rr = col - h * V * pp;
+    v = rr / pp;
+    pix = rr - v * pp;
+  } else {
+    h = (col - nG) / V;
+    v = (col - nG) - h * V;
+  }
+  // y = W_av,h src, src = W_t[v][:, pix] or e_var[v]
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    const float* wrow = a.wav + (int64_t)(h * d + i) * D;
+    double acc = 0.0;
+    for (int j = 0; j < D; ++j)
+      acc += (double)wrow[j] * (pix >= 0 ? a.wt[((int64_t)v * D + j) * pp + pix] : a.ev[(int64_t)v * D + j]);
+    y[i] = (float)acc;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < D; r += blockDim.x) {
+    const float* orow = a.wao + (int64_t)r * D + h * d;
+    double acc = 0.0;
+    for (int i = 0; i < d; ++i) acc += (double)orow[i] * y[i];
+    Bm[(int64_t)r * KA + col] = (T)(float)acc;
+  }
+}
+
+// score weights w[(h V + v) pp + pix], offsets c[h V + v], fused bias[D]
+__global__ void agg_score_kernel(const float* __restrict__ canon, const float* __restrict__ e_s,
+                                 float* __restrict__ w, float* __restrict__ cc, float* __restrict__ bias, int V, int D,
+                                 int H, int pp) {
+  extern __shared__ float u[];            // [D]: W_ak,h^T q_h for head h = blockIdx.x
+  const AggCanon a = agg_canon(canon, V, D, pp);
+  const int d = D / H, h = blockIdx.x;
+  const double isd = 1.0 / sqrt((double)d);
+  if (h < H) {
+    for (int j = threadIdx.x; j < D; j += blockDim.x) {
+      double acc = 0.0;
+      for (int i = 0; i < d; ++i) acc += (double)a.wak[(int64_t)(h * d + i) * D + j] * a.q[h * d + i];
+      u[j] = (float)acc;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < V * (pp + 1); e += blockDim.x) {
+      const int v = e / (pp + 1), pix = e - v * (pp + 1);
+      double acc = 0.0;
+      if (pix < pp) {
+        for (int j = 0; j < D; ++j) acc += (double)a.wt[((int64_t)v * D + j) * pp + pix] * u[j];
+        w[(h * V + v) * pp + pix] = (float)(acc * isd);
+      } else {
+        for (int j = 0; j < D; ++j) acc += (double)u[j] * a.ev[(int64_t)v * D + j];
+        for (int i = 0; i < d; ++i) acc += (double)a.q[h * d + i] * a.bak[h * d + i];
+        cc[h * V + v] = (float)(acc * isd);
+      }
+    }
+  } else {   // last block: bias = W_ao b_av + b_ao + e_s
+    for (int r = threadIdx.x; r < D; r += blockDim.x) {
+      double acc = (double)a.bao[r] + e_s[r];
+      for (int i = 0; i < D; ++i) acc += (double)a.wao[(int64_t)r * D + i] * a.bav[i];
+      bias[r] = (float)acc;
+    }
+  }
+}
+
+template <typename T> __device__ __forceinline__ float to_f(T v);
+template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+// per token row and head: scores, softmax over the V variables, GEMM A row segment
+template <typename T>
+__global__ void agg_prologue_kernel(const T* __restrict__ patches, int64_t ldp, T* __restrict__ agg, int64_t lda,
+                                    const float* __restrict__ w, const float* __restrict__ cc, int64_t M, int V,
+                                    int H, int pp) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / H;
+  const int h = (int)(gid - row * H);
+  if (row >= M) return;
+  const T* a = patches + row * ldp;
+  T* out = agg + row * lda;
+  float s[64];                            // V <= 64 (checked at launch)
+  float mx = -INFINITY;
+  for (int v = 0; v < V; ++v) {
+    float acc = cc[h * V + v];
+    for (int pix = 0; pix < pp; ++pix) acc = fmaf(w[(h * V + v) * pp + pix], to_f<T>(a[v * pp + pix]), acc);
+    s[v] = acc;
+    mx = fmaxf(mx, acc);
+  }
+  float sum = 0.f;
+  for (int v = 0; v < V; ++v) {
+    s[v] = __expf(s[v] - mx);
+    sum += s[v];
+  }
+  const float inv = 1.f / sum;
+  for (int v = 0; v < V; ++v) {
+    const float al = s[v] * inv;
+    for (int pix = 0; pix < pp; ++pix) out[(h * V + v) * pp + pix] = (T)(al * to_f<T>(a[v * pp + pix]));
+    out[H * V * pp + h * V + v] = (T)al;
+  }
+  if (h == 0)                             // K padding columns
+    for (int k = H * V * (pp + 1); k < lda; ++k) out[k] = (T)0.f;
+}
+
+}  // namespace
+
+template <typename T>
+bool launch_agg_prepare(const float* canon, const float* e_s, T* Bm, float* w, float* cc, float* bias, int V, int D,
+                        int H, int pp, int KA, cudaStream_t st) {
+  if (V > 64 || D % H) return false;
+  agg_bcol_kernel<T><<<KA, 256, (D / H) * sizeof(float), st>>>(canon, Bm, V, D, H, pp, KA);
+  agg_score_kernel<<<H + 1, 256, D * sizeof(float), st>>>(canon, e_s, w, cc, bias, V, D, H, pp);
+  return true;
+}
+
+template <typename T>
+bool launch_agg_prologue(const T* patches, int64_t ldp, T* agg, int64_t lda, const float* w, const float* cc,
+                         int64_t M, int V, int H, int pp, cudaStream_t st) {
+  if (V > 64 || M <= 0) return M == 0;
+  const int64_t n = M * H;
+  agg_prologue_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(patches, ldp, agg, lda, w, cc, M, V, H, pp);
+  return true;
+}
+
+template bool launch_agg_prepare<float>(const float*, const float*, float*, float*, float*, float*, int, int, int,
+                                        int, int, cudaStream_t);
+template bool launch_agg_prepare<__nv_bfloat16>(const float*, const float*, __nv_bfloat16*, float*, float*, float*,
+                                                int, int, int, int, int, cudaStream_t);
+template bool launch_agg_prologue<float>(const float*, int64_t, float*, int64_t, const float*, const float*, int64_t,
+                                         int, int, int, cudaStream_t);
+template bool launch_agg_prologue<__nv_bfloat16>(const __nv_bfloat16*, int64_t, __nv_bfloat16*, int64_t,
+                                                 const float*, const float*, int64_t, int, int, int, cudaStream_t);
+
+}  // namespace orbit2

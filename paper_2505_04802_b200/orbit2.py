@@ -25,7 +25,7 @@ class orbit2_config(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "abi_version", "batch", "H", "W", "V", "K", "scale", "patch", "tiles_y", "tiles_x", "halo",
         "halo_mode", "embed", "depth", "heads", "mlp_hidden", "precision", "world_size", "rank",
-        "chunk_tiles", "res_hidden", "dec_hidden")] + [("out_channel_map", C.POINTER(C.c_int32))]
+        "chunk_tiles", "res_hidden", "dec_hidden", "var_agg")] + [("out_channel_map", C.POINTER(C.c_int32))]
 
 
 class orbit2_tile(C.Structure):
@@ -115,11 +115,11 @@ def _check(st: int, where: str):
 
 def make_config(*, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, embed, depth, heads, batch=1,
                 halo_mode=HALO_CLAMP, precision=BF16, world_size=1, rank=0, chunk_tiles=0,
-                out_channel_map=None, res_hidden=0, dec_hidden=0) -> orbit2_config:
+                out_channel_map=None, res_hidden=0, dec_hidden=0, var_agg=0) -> orbit2_config:
     """Build an orbit2_config (the paper's problem statement, north star)."""
     cfg = orbit2_config(ABI_VERSION, batch, H, W, V, K, scale, patch, tiles_y, tiles_x, halo, halo_mode,
                         embed, depth, heads, 4 * embed, precision, world_size, rank, chunk_tiles, res_hidden,
-                        dec_hidden, None)
+                        dec_hidden, var_agg, None)
     if out_channel_map is not None:
         arr = (C.c_int32 * K)(*out_channel_map)
         cfg.out_channel_map = C.cast(arr, C.POINTER(C.c_int32))
@@ -132,7 +132,8 @@ def config_from(w, **over) -> orbit2_config:
     kw = dict(H=w.H, W=w.W, V=w.V, K=w.K, scale=w.scale, patch=w.patch, tiles_y=w.tiles_y,
               tiles_x=w.tiles_x, halo=w.halo, embed=w.embed, depth=w.depth, heads=w.heads,
               batch=w.batch, halo_mode=w.halo_mode, out_channel_map=w.out_channel_map,
-              res_hidden=getattr(w, "res_hidden", 0), dec_hidden=getattr(w, "dec_hidden", 0))
+              res_hidden=getattr(w, "res_hidden", 0), dec_hidden=getattr(w, "dec_hidden", 0),
+              var_agg=getattr(w, "var_agg", 0))
     kw.update(over)
     return make_config(**kw)
 

@@ -182,3 +182,17 @@ def test_residual_conv_config_counts_and_halo(o2):
                     y0, y1 = max(0, t.core_y0 * 2 - dil), min(w0.H, t.core_y1 * 2 + dil)
                     x0, x1 = max(0, t.core_x0 * 2 - dil), min(w0.W, t.core_x1 * 2 + dil)
                     assert have[y0:y1, x0:x1].all()
+
+
+def test_variable_aggregation_config_counts(o2):
+    """var_agg (ABI v2, reading R33): the canonical blob grows by the tokenizer, the
+    variable embeddings, the query and three D x D projections (+ biases); the
+    workloads generator agrees; other values are rejected."""
+    from workloads import weight_count
+    w = get_config("C1", var_agg=1, embed=64, heads=2)
+    _, info = o2.orbit2_tiles_plan(o2.config_from(w))
+    D, V = w.embed, w.V
+    assert info.canonical_weight_count == weight_count(w)
+    assert info.canonical_weight_count == weight_count(w.replace(var_agg=0)) + V * D * 4 + V * D + D + 3 * (D * D + D)
+    with pytest.raises(o2.Orbit2Error, match="var_agg"):
+        o2.orbit2_tiles_plan(o2.config_from(w, var_agg=2))

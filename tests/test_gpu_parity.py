@@ -403,3 +403,28 @@ def test_residual_conv_zero_second_conv_is_upsample_and_chunk_invariant():
     a = run_cuda(wd, x, bd, BF16)
     assert np.array_equal(a, run_cuda(wd, x, bd, BF16, chunk_tiles=1))
     assert np.array_equal(a, run_cuda(wd, x, bd, BF16, world_size=3))
+
+
+
+# ---------------------------------------------------------------- variable aggregation (R33)
+VARAGG = [
+    ("C1", dict(var_agg=1)),
+    ("C1", dict(var_agg=1, embed=128, heads=2, depth=2, tiles_y=3, tiles_x=5, halo=1)),
+    ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=2, var_agg=1)),
+    ("C2", dict(H=48, W=96, tiles_y=2, tiles_x=3, depth=1, var_agg=1, res_hidden=4, dec_hidden=4)),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
+@pytest.mark.parametrize("name,over", VARAGG)
+def test_variable_aggregation_parity(name, over, precision, tol):
+    """P:479 per-variable tokens + cross-attention aggregation (oracle O3b, plain
+    form) against the library's folded form (score prologue + one tcgen05 / SIMT
+    GEMM of K = H V (p^2 + 1)): the identity holds to rounding."""
+    w, x, blob = _case(name, **over)
+    ref = oracle_full(w, x, blob)[0]
+    got = run_cuda(w, x, blob, precision)
+    e = rel_err(got, ref)
+    print(f"var_agg {name} {over} prec={precision}: rel_err={e:.3e}")
+    assert np.isfinite(got).all() and e <= tol
