@@ -60,6 +60,7 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
   if (c->dec_hidden < 0 || c->dec_hidden > 64 || c->dec_hidden % 4)
     return fail(msg, "dec_hidden: must be a multiple of 4 in [0, 64]");
   if (c->var_agg != 0 && c->var_agg != 1) return fail(msg, "var_agg: must be 0 or 1");
+  if (c->var_agg && c->V > 32) return fail(msg, "V: the variable aggregation supports at most 32 variables");
   if (c->dec_hidden > 0 && c->halo < (2 + c->scale * c->patch - 1) / (c->scale * c->patch))
     return fail(msg, "halo: the decoder convolutions need halo >= ceil(2 / (scale * patch)) patches");
   if (c->out_channel_map) {

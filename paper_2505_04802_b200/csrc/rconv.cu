@@ -22,6 +22,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -118,6 +119,94 @@ __device__ __forceinline__ void stage_pair(const float* w, float* waT, float* ba
   for (int i = threadIdx.x; i < K4p; i += RC_THREADS) bb[i] = i < K ? wb[K * C * 9 + i] : 0.f;
 }
 
+// ---- tensor-core form (bf16 path): the 3x3 convolution as an implicit GEMM on
+// mma.sync.m16n8k16 (bf16 in, fp32 accumulate): rows = output pixels of an OY x OX
+// grid, columns = output channels, K = Cin * 9 (im2col from the shared-memory input
+// block of (OY + 2) x (OX + 2)).  The convolutions are 27-576 long per pixel, far
+// below a tcgen05 tile, so the warp-level MMA is the right size.
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// weight fragments in mma order: frag[(s * NB + j) * 32 + lane] = (b0, b1) for k-step s, n-block j
+__device__ __forceinline__ void stage_bfrag(const float* W, uint2* frag, int Cin, int Cout, int KS, int NB) {
+  // W[o][ci][dy][dx] (PyTorch layout), B[kk][n] = W[n][kk] for kk < Cin * 9, n < Cout
+  for (int i = threadIdx.x; i < KS * NB * 32; i += RC_THREADS) {
+    const int lane = i & 31, sj = i >> 5, st = sj / NB, j = sj - st * NB;
+    const int g = lane >> 2, tg = lane & 3, n = 8 * j + g;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int kk = 16 * st + 2 * tg + (e & 1) + (e >> 1) * 8;
+      v[e] = (n < Cout && kk < Cin * 9) ? W[(int64_t)n * Cin * 9 + kk] : 0.f;
+    }
+    frag[i] = make_uint2(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]));
+  }
+}
+
+// dst[n][y][x] = act(bias[n] + conv(src)[n][y][x]) for the OY x OX grid (0 where !inside)
+template <bool GELU, typename Inside>
+__device__ __forceinline__ void mma_conv(const float* src, int Cin, const uint2* frag, const float* bias, int Cout,
+                                         int KS, int NB, int OY, int OX, float* dst, int dstX, Inside inside) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tg = lane & 3;
+  const int SX = OX + 2, SY = OY + 2, npx = OY * OX, ntiles = (npx + 15) / 16;
+  for (int tile = warp; tile < ntiles; tile += RC_THREADS / 32) {
+    float acc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    int rowoff[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = min(tile * 16 + g + 8 * h, npx - 1);
+      const int y = m / OX, x = m - y * OX;
+      rowoff[h] = y * SX + x;
+    }
+    for (int st = 0; st < KS; ++st) {
+      uint32_t a[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {   // a0: (g, k), a1: (g+8, k), a2: (g, k+8), a3: (g+8, k+8); k = 2 tg, 2 tg + 1
+        float v2[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int kk = 16 * st + 2 * tg + e + (r >> 1) * 8;
+          float v = 0.f;
+          if (kk < Cin * 9) {
+            const int ci = kk / 9, t9 = kk - ci * 9, dy = t9 / 3, dx = t9 - dy * 3;
+            v = src[ci * SY * SX + rowoff[r & 1] + dy * SX + dx];
+          }
+          v2[e] = v;
+        }
+        a[r] = pack_bf16x2(v2[0], v2[1]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= NB) break;
+        const uint2 b = frag[(st * NB + j) * 32 + lane];
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+            "{%0,%1,%2,%3};"
+            : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b.x), "r"(b.y));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (j >= NB) break;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {   // c0, c1: row g; c2, c3: row g + 8; cols 2 tg, 2 tg + 1
+        const int m = tile * 16 + g + 8 * (e >> 1), n = 8 * j + 2 * tg + (e & 1);
+        if (m >= npx || n >= Cout) continue;
+        const int y = m / OX, x = m - y * OX;
+        float v = acc[j][e] + bias[n];
+        if (GELU) v = inside(y, x) ? gelu_exact(v) : 0.f;
+        dst[(n * OY + y) * dstX + x] = v;
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
     const T* __restrict__ tile_out, const float* __restrict__ x, float* __restrict__ out, ChunkDev ch,
@@ -135,6 +224,15 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   float* sv = su + K * UY * UX;                     // [K][UY][UX] vit on the grown block (CD > 0)
   float* sh = sv + (CD ? K * UY * UX : 0);          // [max(CR, CD)][BY+2][BX+2] hidden layer
   float* sres = sh + max(CR, CD) * (BY + 2) * (BX + 2);   // [K][BY][BX] residual (CD > 0 && CR > 0)
+  // tensor-core form (bf16 path): second-convolution results and the weight fragments
+  constexpr bool MMA = std::is_same<T, __nv_bfloat16>::value;
+  const int KSa = (K * 9 + 15) / 16, NBo = (K + 7) / 8;
+  const int KSr = (CR * 9 + 15) / 16, NBr = (CR + 7) / 8, KSd = (CD * 9 + 15) / 16, NBd = (CD + 7) / 8;
+  float* scv = sres + (CD && CR ? K * BY * BX : 0);             // [K][BY][BX] conv_b + bias
+  uint2* fra = reinterpret_cast<uint2*>(scv + (MMA ? K * BY * BX : 0));   // residual conv_a fragments
+  uint2* frb = fra + (MMA && CR ? KSa * NBr * 32 : 0);                    // residual conv_b
+  uint2* fda = frb + (MMA && CR ? KSr * NBo * 32 : 0);                    // decoder conv_a
+  uint2* fdb = fda + (MMA && CD ? KSa * NBd * 32 : 0);                    // decoder conv_b
   const DevTile t = ch.tiles[ch.tb + blockIdx.y];
   const int ur = blockIdx.x / nseg, seg = blockIdx.x - ur * nseg;
   if (ur >= t.core_h || seg * BX >= t.core_w * P) return;
@@ -146,6 +244,16 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   const int tid = threadIdx.x;
   if (CR) stage_pair(wres, sWr, sWr + CR * K * 9, sWr + CR * K * 9 + CR, sWr + CR * K * 9 + CR + CR * 9 * K4p, K, CR, K4p);
   if (CD) stage_pair(wdec, sWd, sWd + CD * K * 9, sWd + CD * K * 9 + CD, sWd + CD * K * 9 + CD + CD * 9 * K4p, K, CD, K4p);
+  if (MMA) {
+    if (CR) {
+      stage_bfrag(wres, fra, K, CR, KSa, NBr);
+      stage_bfrag(wres + CR * K * 9 + CR, frb, CR, K, KSr, NBo);
+    }
+    if (CD) {
+      stage_bfrag(wdec, fda, K, CD, KSa, NBd);
+      stage_bfrag(wdec + CD * K * 9 + CD, fdb, CD, K, KSd, NBo);
+    }
+  }
   const float inv_s = 1.0f / (float)s;
   const int64_t tbase = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0);   // tile's output tokens
   const int Nh = K * P * P;
@@ -179,13 +287,28 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   __syncthreads();
   auto in_field = [&](int Y, int X) { return Y >= 0 && Y < sH && X >= 0 && X < sW; };
   const int K4 = K4p / 4, NP = BY * nx;
+  auto in_field_h = [&](int yy, int xx) { return in_field(Y0 - 1 + yy, X0 - 1 + xx); };
+  auto all_in = [](int, int) { return true; };
   if (CR) {   // residual path
-    conv_hidden(su, sh, sWr, sWr + CR * K * 9, K, CR, BY, Y0, X0, in_field);
-    __syncthreads();
     const float* wb = sWr + CR * K * 9 + CR;
+    if (MMA) {
+      mma_conv<true>(su, K, fra, sWr + CR * K * 9, CR, KSa, NBr, BY + 2, BX + 2, sh, BX + 2, in_field_h);
+      __syncthreads();
+      mma_conv<false>(sh, CR, frb, wb + CR * 9 * K4p, K, KSr, NBo, BY, BX, scv, BX, all_in);
+    } else {
+      conv_hidden(su, sh, sWr, sWr + CR * K * 9, K, CR, BY, Y0, X0, in_field);
+    }
+    __syncthreads();
     for (int i = tid; i < K4 * NP; i += RC_THREADS) {
       const int kg = i / NP, r = i - kg * NP, al = r / nx, xx = r - al * nx;
-      const float4 cv = conv_out4(sh, wb, wb + CR * 9 * K4p, CR, K4, BY, kg, al, xx);
+      float4 cv;
+      if (MMA) {
+        cv = make_float4(scv[((4 * kg) * BY + al) * BX + xx], 4 * kg + 1 < K ? scv[((4 * kg + 1) * BY + al) * BX + xx] : 0.f,
+                         4 * kg + 2 < K ? scv[((4 * kg + 2) * BY + al) * BX + xx] : 0.f,
+                         4 * kg + 3 < K ? scv[((4 * kg + 3) * BY + al) * BX + xx] : 0.f);
+      } else {
+        cv = conv_out4(sh, wb, wb + CR * 9 * K4p, CR, K4, BY, kg, al, xx);
+      }
       const float cvs[4] = {cv.x, cv.y, cv.z, cv.w};
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -207,12 +330,26 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   // decoder convolutions (CD > 0)
   const int oy0 = t.out_y0 * P, oy1 = (t.out_y0 + t.out_h) * P, ox0 = t.out_x0 * P, ox1 = (t.out_x0 + t.out_w) * P;
   auto in_out = [&](int Y, int X) { return Y >= oy0 && Y < oy1 && X >= ox0 && X < ox1; };
-  conv_hidden(sv, sh, sWd, sWd + CD * K * 9, K, CD, BY, Y0, X0, in_out);
-  __syncthreads();
   const float* wb = sWd + CD * K * 9 + CD;
+  if (MMA) {
+    auto in_out_h = [&](int yy, int xx) { return in_out(Y0 - 1 + yy, X0 - 1 + xx); };
+    mma_conv<true>(sv, K, fda, sWd + CD * K * 9, CD, KSa, NBd, BY + 2, BX + 2, sh, BX + 2, in_out_h);
+    __syncthreads();
+    mma_conv<false>(sh, CD, fdb, wb + CD * 9 * K4p, K, KSd, NBo, BY, BX, scv, BX, all_in);
+  } else {
+    conv_hidden(sv, sh, sWd, sWd + CD * K * 9, K, CD, BY, Y0, X0, in_out);
+  }
+  __syncthreads();
   for (int i = tid; i < K4 * NP; i += RC_THREADS) {
     const int kg = i / NP, r = i - kg * NP, al = r / nx, xx = r - al * nx;
-    const float4 dv = conv_out4(sh, wb, wb + CD * 9 * K4p, CD, K4, BY, kg, al, xx);
+    float4 dv;
+    if (MMA) {
+      dv = make_float4(scv[((4 * kg) * BY + al) * BX + xx], 4 * kg + 1 < K ? scv[((4 * kg + 1) * BY + al) * BX + xx] : 0.f,
+                       4 * kg + 2 < K ? scv[((4 * kg + 2) * BY + al) * BX + xx] : 0.f,
+                       4 * kg + 3 < K ? scv[((4 * kg + 3) * BY + al) * BX + xx] : 0.f);
+    } else {
+      dv = conv_out4(sh, wb, wb + CD * 9 * K4p, CD, K4, BY, kg, al, xx);
+    }
     const float dvs[4] = {dv.x, dv.y, dv.z, dv.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -238,8 +375,13 @@ bool launch_stitch_conv(const T* tile_out, const float* x, float* out, const Chu
   const size_t nr = CR ? (size_t)CR * K * 9 + CR + (size_t)CR * 9 * K4p + K4p : 0;
   const size_t nd = CD ? (size_t)CD * K * 9 + CD + (size_t)CD * 9 * K4p + K4p : 0;
   const size_t up = (size_t)K * (P + 4) * (BX + 4);
+  const bool mma = std::is_same<T, __nv_bfloat16>::value;
+  const size_t KSa = (K * 9 + 15) / 16, NBo = (K + 7) / 8;
+  const size_t frags = !mma ? 0 : (CR ? KSa * ((CR + 7) / 8) * 32 + ((CR * 9 + 15) / 16) * NBo * 32 : 0) +
+                                      (CD ? KSa * ((CD + 7) / 8) * 32 + ((CD * 9 + 15) / 16) * NBo * 32 : 0);
   const size_t smem = sizeof(float) * (nr + nd + up + (CD ? up : 0) + (size_t)std::max(CR, CD) * (P + 2) * (BX + 2) +
-                                       (CD && CR ? (size_t)K * P * BX : 0));
+                                       (CD && CR ? (size_t)K * P * BX : 0) + (mma ? (size_t)K * P * BX : 0)) +
+                      sizeof(uint2) * frags;
   if (smem > 200 * 1024) return false;
   static std::atomic<uint64_t> done{0};
   if (!smem_attr_once(reinterpret_cast<const void*>(stitch_conv_kernel<T>), 200 * 1024, &done)) return false;

@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "kernels.h"
@@ -124,38 +125,60 @@ template <typename T> __device__ __forceinline__ float to_f(T v);
 template <> __device__ __forceinline__ float to_f<float>(float v) { return v; }
 template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
 
-// per token row and head: scores, softmax over the V variables, GEMM A row segment
+// One warp per token row: lanes take the (head, variable) scores, softmax per head by
+// warp reductions (V <= 32: lane = variable), then the A row [alpha a | alpha | 0-pad]
+// is written in 16-byte pieces by consecutive lanes (coalesced row stores).
+constexpr int AGG_WARPS = 8;
 template <typename T>
-__global__ void agg_prologue_kernel(const T* __restrict__ patches, int64_t ldp, T* __restrict__ agg, int64_t lda,
-                                    const float* __restrict__ w, const float* __restrict__ cc, int64_t M, int V,
-                                    int H, int pp) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gid / H;
-  const int h = (int)(gid - row * H);
-  if (row >= M) return;
-  const T* a = patches + row * ldp;
-  T* out = agg + row * lda;
-  float s[64];                            // V <= 64 (checked at launch)
-  float mx = -INFINITY;
-  for (int v = 0; v < V; ++v) {
-    float acc = cc[h * V + v];
-    for (int pix = 0; pix < pp; ++pix) acc = fmaf(w[(h * V + v) * pp + pix], to_f<T>(a[v * pp + pix]), acc);
-    s[v] = acc;
-    mx = fmaxf(mx, acc);
+__global__ void __launch_bounds__(32 * AGG_WARPS) agg_prologue_kernel(
+    const T* __restrict__ patches, int64_t ldp, T* __restrict__ agg, int64_t lda, const float* __restrict__ w,
+    const float* __restrict__ cc, int64_t M, int V, int H, int pp) {
+  extern __shared__ float asm_[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int din = V * pp, HV = H * V;
+  float* sa = asm_ + warp * (din + HV);            // this warp's patch row (fp32)
+  float* sal = sa + din;                           // alpha[h][v]
+  for (int64_t row = (int64_t)blockIdx.x * AGG_WARPS + warp; row < M; row += (int64_t)gridDim.x * AGG_WARPS) {
+    const T* a = patches + row * ldp;
+    for (int e = lane; e < din; e += 32) sa[e] = to_f<T>(a[e]);
+    __syncwarp();
+    for (int h = 0; h < H; ++h) {                  // lane = variable (V <= 32)
+      float sv = -INFINITY;
+      if (lane < V) {
+        float acc = cc[h * V + lane];
+        for (int pix = 0; pix < pp; ++pix) acc = fmaf(w[(h * V + lane) * pp + pix], sa[lane * pp + pix], acc);
+        sv = acc;
+      }
+      float mx = sv;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float ex = lane < V ? __expf(sv - mx) : 0.f;
+      float sum = ex;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane < V) sal[h * V + lane] = ex / sum;
+    }
+    __syncwarp();
+    T* out = agg + row * lda;
+    constexpr int VE = 16 / sizeof(T);             // elements per 16-byte piece
+    for (int e0 = lane * VE; e0 < lda; e0 += 32 * VE) {
+      T piece[VE];
+#pragma unroll
+      for (int u = 0; u < VE; ++u) {
+        const int e = e0 + u;
+        float val = 0.f;
+        if (e < HV * pp) {
+          const int hv = e / pp, pix = e - hv * pp, v = hv % V;
+          val = sal[hv] * sa[v * pp + pix];
+        } else if (e < HV * (pp + 1)) {
+          val = sal[e - HV * pp];
+        }
+        piece[u] = (T)val;
+      }
+      *reinterpret_cast<uint4*>(out + e0) = *reinterpret_cast<const uint4*>(piece);
+    }
+    __syncwarp();
   }
-  float sum = 0.f;
-  for (int v = 0; v < V; ++v) {
-    s[v] = __expf(s[v] - mx);
-    sum += s[v];
-  }
-  const float inv = 1.f / sum;
-  for (int v = 0; v < V; ++v) {
-    const float al = s[v] * inv;
-    for (int pix = 0; pix < pp; ++pix) out[(h * V + v) * pp + pix] = (T)(al * to_f<T>(a[v * pp + pix]));
-    out[H * V * pp + h * V + v] = (T)al;
-  }
-  if (h == 0)                             // K padding columns
-    for (int k = H * V * (pp + 1); k < lda; ++k) out[k] = (T)0.f;
 }
 
 }  // namespace
@@ -163,7 +186,7 @@ __global__ void agg_prologue_kernel(const T* __restrict__ patches, int64_t ldp, 
 template <typename T>
 bool launch_agg_prepare(const float* canon, const float* e_s, T* Bm, float* w, float* cc, float* bias, int V, int D,
                         int H, int pp, int KA, cudaStream_t st) {
-  if (V > 64 || D % H) return false;
+  if (V > 32 || D % H) return false;
   agg_bcol_kernel<T><<<KA, 256, (D / H) * sizeof(float), st>>>(canon, Bm, V, D, H, pp, KA);
   agg_score_kernel<<<H + 1, 256, D * sizeof(float), st>>>(canon, e_s, w, cc, bias, V, D, H, pp);
   return true;
@@ -172,9 +195,11 @@ bool launch_agg_prepare(const float* canon, const float* e_s, T* Bm, float* w, f
 template <typename T>
 bool launch_agg_prologue(const T* patches, int64_t ldp, T* agg, int64_t lda, const float* w, const float* cc,
                          int64_t M, int V, int H, int pp, cudaStream_t st) {
-  if (V > 64 || M <= 0) return M == 0;
-  const int64_t n = M * H;
-  agg_prologue_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(patches, ldp, agg, lda, w, cc, M, V, H, pp);
+  if (V > 32 || M <= 0 || lda % (16 / sizeof(T))) return M == 0;
+  const size_t smem = (size_t)AGG_WARPS * (V * pp + H * V) * sizeof(float);
+  if (smem > 48 * 1024) return false;
+  const int64_t blocks = std::min<int64_t>((M + AGG_WARPS - 1) / AGG_WARPS, (int64_t)num_sms() * 16);
+  agg_prologue_kernel<T><<<(unsigned)blocks, 32 * AGG_WARPS, smem, st>>>(patches, ldp, agg, lda, w, cc, M, V, H, pp);
   return true;
 }
 
