@@ -156,6 +156,9 @@ constexpr bool kTailSkip = ORBIT2_ATTN_TAILSKIP != 0;
 // exponential phases then interleave with each other's row-max / wait phases
 // instead of colliding on the MUFU (0 = both start together).
 constexpr int kDesync = ORBIT2_ATTN_DESYNC;
+#ifndef ORBIT2_ATTN_SPIN_CLK
+#define ORBIT2_ATTN_SPIN_CLK 0
+#endif
 
 template <int DH, int NQ>
 struct AttnCfg {
@@ -626,6 +629,12 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         const bool desync = kDesync > 0 && SPW == 1 && !kPingPong && j == 0 && it.nq == NQ && NQ == 2;
         const uint32_t dbar = 11 + q;
         if (desync && qt == 1) asm volatile("bar.sync %0, 64;" ::"r"(dbar) : "memory");
+        if (ORBIT2_ATTN_SPIN_CLK > 0 && j == 0 && qt == 1 && it.nq == NQ) {
+          // stagger the second Q tile's first exponential phase by a fixed delay
+          const long long t0 = clock64();
+          while (clock64() - t0 < (long long)ORBIT2_ATTN_SPIN_CLK) {
+          }
+        }
         const int kv_blk = it.n - j * 128;         // valid keys of this block (SPW == 1)
         const int c_arr = (kDesync == 1 ? KC / 2 : KC) - 64;   // half after which tile 0 releases tile 1
 #pragma unroll

@@ -119,6 +119,13 @@ __device__ __forceinline__ void stage_pair(const float* w, float* waT, float* ba
   for (int i = threadIdx.x; i < K4p; i += RC_THREADS) bb[i] = i < K ? wb[K * C * 9 + i] : 0.f;
 }
 
+// ORBIT2_CONV_MMA=1: the tensor-core form below for the bf16 path.  Measured slower
+// than the FFMA form at C2 (res + dec hidden 8: 30.7 vs 13.0 ms per step; 16: 44.3 ms):
+// the per-element im2col fragment loads (index arithmetic + scattered shared loads)
+// cost more than the FFMAs they replace at these tiny channel counts.
+#ifndef ORBIT2_CONV_MMA
+#define ORBIT2_CONV_MMA 0
+#endif
 // ---- tensor-core form (bf16 path): the 3x3 convolution as an implicit GEMM on
 // mma.sync.m16n8k16 (bf16 in, fp32 accumulate): rows = output pixels of an OY x OX
 // grid, columns = output channels, K = Cin * 9 (im2col from the shared-memory input
@@ -225,7 +232,7 @@ __global__ void __launch_bounds__(RC_THREADS) stitch_conv_kernel(
   float* sh = sv + (CD ? K * UY * UX : 0);          // [max(CR, CD)][BY+2][BX+2] hidden layer
   float* sres = sh + max(CR, CD) * (BY + 2) * (BX + 2);   // [K][BY][BX] residual (CD > 0 && CR > 0)
   // tensor-core form (bf16 path): second-convolution results and the weight fragments
-  constexpr bool MMA = std::is_same<T, __nv_bfloat16>::value;
+  constexpr bool MMA = ORBIT2_CONV_MMA && std::is_same<T, __nv_bfloat16>::value;
   const int KSa = (K * 9 + 15) / 16, NBo = (K + 7) / 8;
   const int KSr = (CR * 9 + 15) / 16, NBr = (CR + 7) / 8, KSd = (CD * 9 + 15) / 16, NBd = (CD + 7) / 8;
   float* scv = sres + (CD && CR ? K * BY * BX : 0);             // [K][BY][BX] conv_b + bias
@@ -375,7 +382,7 @@ bool launch_stitch_conv(const T* tile_out, const float* x, float* out, const Chu
   const size_t nr = CR ? (size_t)CR * K * 9 + CR + (size_t)CR * 9 * K4p + K4p : 0;
   const size_t nd = CD ? (size_t)CD * K * 9 + CD + (size_t)CD * 9 * K4p + K4p : 0;
   const size_t up = (size_t)K * (P + 4) * (BX + 4);
-  const bool mma = std::is_same<T, __nv_bfloat16>::value;
+  const bool mma = ORBIT2_CONV_MMA && std::is_same<T, __nv_bfloat16>::value;
   const size_t KSa = (K * 9 + 15) / 16, NBo = (K + 7) / 8;
   const size_t frags = !mma ? 0 : (CR ? KSa * ((CR + 7) / 8) * 32 + ((CR * 9 + 15) / 16) * NBo * 32 : 0) +
                                       (CD ? KSa * ((CD + 7) / 8) * 32 + ((CD * 9 + 15) / 16) * NBo * 32 : 0);
