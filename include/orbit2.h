@@ -336,6 +336,58 @@ orbit2_status orbit2_comm_barrier(void *ctx, void *stream);
 orbit2_status orbit2_comm_status(void *ctx);
 
 /* Number of kernels the library launched on this ctx so far. */
+/* ==========================================================================
+ * Training step.  The paper's throughput numbers are
+ * training numbers ("Only the mixed-precision BFLOAT16 results"); the step is
+ *   out = TILES forward (every query of every block kept for the backward)
+ *   L   = Bayesian loss (readings R34, R35): per sample
+ *         (1/(K N)) [ sum_i w_row(i) (y_i - x_i)^2 + lambda sum_i sum_{j in C(i)} b_ij h(x_i - x_j) ],
+ *         C(i) the 8 neighbours inside the field, b_ij = 1/euclidean distance,
+ *         h the Huber-smoothed |.| with width delta, w_row = cos(lat) / mean cos(lat)
+ *         (geo != 0; else 1); the batch loss is the mean over the B samples
+ *   dL/dweights by reverse-mode differentiation of the tiled forward, written into a
+ *         caller buffer in the CANONICAL blob order (fp32, same count), for the
+ *         rank-local tiles (summing the ranks' gradients, or averaging data-parallel
+ *         replicas' with one all-reduce, is the caller's once-per-batch step, R36)
+ * Scope (E_UNSUPPORTED otherwise): BF16 precision, head_dim 64, embed <= 1024,
+ * var_agg = res_hidden = dec_hidden = 0, one call over every rank-local tile.
+ * The oracle is oracle/train.py.
+ * ========================================================================== */
+typedef struct {
+  int64_t workspace_bytes;          /* device bytes orbit2_train_bind needs: the activations
+                                       every block keeps for the backward, the backward's
+                                       scratch and transposed bf16 weights */
+  int64_t canonical_weight_count;   /* fp32 values of the gradient (= the canonical blob) */
+  double fwd_flops_per_sample;      /* training forward, rank-local tiles */
+  double flops_per_sample;          /* forward + backward algorithmic FLOPs, rank-local tiles */
+  double attn_bwd_flops_per_sample; /* attention backward alone (S, dP, dV, dK, dQ) */
+} orbit2_train_info;
+
+/* Sizing (host only). */
+orbit2_status orbit2_train_plan(void *ctx, orbit2_train_info *info);
+/* Bind a caller-owned device buffer of >= info.workspace_bytes (16-byte aligned) to the
+ * context; zero-fills it on `stream` (rows past the batch's tokens must stay zero). */
+orbit2_status orbit2_train_bind(void *ctx, void *train_ws_dev, size_t bytes, void *stream);
+/* Transposed bf16 copies of the weights the input-gradient GEMMs read, from the
+ * canonical fp32 blob; call after every weight update (with orbit2_prepare_weights). */
+orbit2_status orbit2_train_prepare(void *ctx, const float *canonical_dev, void *stream);
+/* Forward over every rank-local tile (steps 1-3 + head, all queries of every block),
+ * keeping the activations in the training workspace; tile_out as orbit2_reslim_forward.
+ * The output field is then assembled by orbit2_stitch as for inference. */
+orbit2_status orbit2_train_forward(void *ctx, const void *packed_w, const float *input_dev,
+                                   void *tile_out_dev, void *stream);
+/* Bayesian loss of out_dev [B][K][sH][sW] against truth_dev (same shape), fp32:
+ * loss_dev[b] (double, per sample, overwritten) and dout_dev = d(mean_b loss_b)/d out
+ * (fp32, same shape, overwritten).  delta > 0, lambda >= 0 (E_INVALID otherwise). */
+orbit2_status orbit2_loss(void *ctx, const float *out_dev, const float *truth_dev, float lambda, float delta,
+                          int32_t geo, double *loss_dev, float *dout_dev, void *stream);
+/* Backward of the last orbit2_train_forward given dout_dev [B][K][sH][sW] (the stitch
+ * read backwards: only the rank-local tiles' core pixels are read).  grad_dev
+ * (canonical order, info.canonical_weight_count floats, 16-byte aligned) is
+ * overwritten with the gradient of the rank-local tiles' contribution. */
+orbit2_status orbit2_train_backward(void *ctx, const void *packed_w, const float *dout_dev, float *grad_dev,
+                                    void *stream);
+
 int64_t orbit2_launch_count(void *ctx);
 
 /*

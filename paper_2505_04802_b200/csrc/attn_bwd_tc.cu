@@ -1,0 +1,389 @@
+// attn_bwd_tc.cu -- backward of the per-tile attention on tcgen05 (training step,
+// SURVEY.md §8(f) row 3; oracle/train.py _attn_bwd).
+//
+// For one (tile, head, sample) with S = Q K^T c (c = 1/sqrt(d)), P = softmax_rows(S),
+// O = P V and the incoming dO:
+//     dV = P^T dO;   dP = dO V^T;   dS = P (dP - Delta),  Delta_q = sum_d dO_q O_q;
+//     dQ = c dS K;   dK = c dS^T Q
+// P is recomputed from the forward's per-row log-sum-exp (log2 units:
+// P = 2^(S log2(e) c - lse2)).  Attention stays inside the tile.
+//
+// Work item = (key block of 128 keys of a tile, head, sample); the CTA walks
+// every 128-query block of the tile (persistent, one CTA per SM):
+//   warp 0 lane 0 : TMA producer (K, V of the item into a 2-slot ring; Q_j, dO_j
+//                   into a 2-slot ring)
+//   warp 1        : tcgen05.mma issuer
+//       S^T  = K Q_j^T          (SS, both K-major)           -> TMEM [0,128)
+//       dP^T = V dO_j^T         (SS, both K-major)           -> TMEM [128,256)
+//       dV  += P^T dO_j         (TS: P^T bf16 in TMEM, dO_j MN-major) -> [320,384)
+//       dK  += dS^T Q_j         (SS: dS^T K-major in smem, Q_j MN-major) -> [384,448)
+//       dQ_j = dS K             (SS: dS MN-major = the same smem, K MN-major) -> [448,512)
+//   warp 2        : TMEM allocator (512 columns)
+//   warps 4..7    : thread = key row r (TMEM lane r): P^T, dS^T for block j,
+//                   P^T -> TMEM [256,320) (bf16 pairs), dS^T -> smem (SW128);
+//                   at the item's end dK c, dV -> dqkv (bf16)
+//   warps 8..11   : thread = query row of block j: dQ_j c -> fp32 atomics into dq_acc
+// The same TMA tile [128 rows][64 bf16] (one SW128 atom) is a K-major operand when
+// the contraction runs over head dim and an MN-major one when it runs over tokens.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace orbit2 {
+
+bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                    int box_cols, CUtensorMapSwizzle swz);
+
+namespace {
+
+constexpr int DH = 64;
+constexpr int TILE = 128 * DH * 2;          // 16 KB: one SW128 atom of 128 rows
+constexpr int QST = 2;                      // Q_j / dO_j ring
+constexpr int KVST = 2;                     // K / V ring (next item prefetched)
+constexpr int IRING = 4;
+constexpr int THREADS = 384;
+constexpr uint32_t C_S = 0, C_DP = 128, C_P = 256, C_DV = 320, C_DK = 384, C_DQ = 448;
+constexpr int SMEM = KVST * 2 * TILE + QST * 2 * TILE + 2 * TILE + 2 * 2 * 128 * 4 + 1024 + 512;
+
+struct __align__(16) BItem {
+  int64_t base;     // first row of the tile's tokens
+  int n, k0, nq, h;
+};
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ BItem bitem(const ChunkDev& ch, int heads, int id) {
+  const int per_b = ch.nqb * heads;        // item = (key block fastest, head, sample)
+  BItem it;
+  const int b = id / per_b;
+  const int r = id - b * per_b;
+  it.h = r / ch.nqb;
+  const int g = ch.qb0 + (r - it.h * ch.nqb);
+  const DevTile t = ch.tiles[ch.qblk_tile[g]];
+  it.k0 = (g - t.qb_off) * 128;
+  it.n = t.n_tokens;
+  it.nq = (it.n + 127) / 128;
+  it.base = (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0);
+  return it;
+}
+
+__device__ __forceinline__ BItem take(const BItem* sItem, uint64_t* full, uint64_t* empty, uint32_t li) {
+  const uint32_t s = li % IRING;
+  tc::mbar_wait(&full[s], (li / IRING) & 1);
+  const BItem it = sItem[s];
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) tc::mbar_arrive(&empty[s]);
+  return it;
+}
+
+__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    attn_bwd_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
+                    const float* __restrict__ lse, const float* __restrict__ delta, int64_t ld_stat,
+                    float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, ChunkDev ch, int D, int heads,
+                    int n_items) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sK = smem;                               // [KVST][TILE]
+  uint8_t* sV = sK + KVST * TILE;                   // [KVST][TILE]
+  uint8_t* sQ = sV + KVST * TILE;                   // [QST][TILE]
+  uint8_t* sDO = sQ + QST * TILE;                   // [QST][TILE]
+  uint8_t* sDS = sDO + QST * TILE;                  // dS^T [128 keys][128 q] as 2 atoms
+  float* sL = reinterpret_cast<float*>(sDS + 2 * TILE);   // [2][128] lse2 of the block's queries
+  float* sDl = sL + 2 * 128;                        // [2][128] Delta
+  BItem* sItem = reinterpret_cast<BItem*>(sDl + 2 * 128);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sItem + IRING);
+  uint64_t* kv_full = bar;                          // [KVST]
+  uint64_t* kv_empty = kv_full + KVST;              // [KVST]
+  uint64_t* q_full = kv_empty + KVST;               // [QST]
+  uint64_t* q_empty = q_full + QST;                 // [QST]
+  uint64_t* s_full = q_empty + QST;                 // S^T, dP^T in TMEM (and the previous block's MMAs done)
+  uint64_t* p_full = s_full + 1;                    // P^T (TMEM) and dS^T (smem) written
+  uint64_t* dq_full = p_full + 1;
+  uint64_t* dq_free = dq_full + 1;
+  uint64_t* dkv_full = dq_free + 1;
+  uint64_t* dkv_free = dkv_full + 1;
+  uint64_t* it_full = dkv_free + 1;                 // [IRING]
+  uint64_t* it_empty = it_full + IRING;             // [IRING]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(it_empty + IRING);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&tqkv);
+    tc::prefetch_tmap(&tdo);
+    for (int s = 0; s < KVST; ++s) {
+      tc::mbar_init(&kv_full[s], 1);
+      tc::mbar_init(&kv_empty[s], 1);
+    }
+    for (int s = 0; s < QST; ++s) {
+      tc::mbar_init(&q_full[s], 1);
+      tc::mbar_init(&q_empty[s], 1);
+    }
+    tc::mbar_init(s_full, 1);
+    tc::mbar_init(p_full, 128);
+    tc::mbar_init(dq_full, 1);
+    tc::mbar_init(dq_free, 128);
+    tc::mbar_init(dkv_full, 1);
+    tc::mbar_init(dkv_free, 128);
+    for (int s = 0; s < IRING; ++s) {
+      tc::mbar_init(&it_full[s], 1);
+      tc::mbar_init(&it_empty[s], 9);   // MMA warp + 4 softmax warps + 4 dQ warps
+    }
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) {
+    __syncwarp();
+    tc::tmem_alloc(tmem_slot, 512);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const float cs = rsqrtf((float)DH);                    // c = 1/sqrt(d)
+  const float sl = 1.4426950408889634f * cs;             // log2(e) c
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      uint32_t li = 0, gq = 0;
+      for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+        const BItem it = bitem(ch, heads, id);
+        {
+          const uint32_t s = li % IRING;
+          tc::mbar_wait(&it_empty[s], ((li / IRING) & 1) ^ 1);
+          sItem[s] = it;
+          tc::mbar_arrive(&it_full[s]);
+        }
+        const int32_t y0 = (int32_t)it.base;
+        const uint32_t kv = li % KVST;
+        tc::mbar_wait(&kv_empty[kv], ((li / KVST) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&kv_full[kv], 2 * TILE);
+        tc::tma_load_2d(&tqkv, sK + kv * TILE, &kv_full[kv], D + it.h * DH, y0 + it.k0);
+        tc::tma_load_2d(&tqkv, sV + kv * TILE, &kv_full[kv], 2 * D + it.h * DH, y0 + it.k0);
+        for (int j = 0; j < it.nq; ++j, ++gq) {
+          const uint32_t s = gq % QST;
+          tc::mbar_wait(&q_empty[s], ((gq / QST) & 1) ^ 1);
+          tc::mbar_arrive_expect_tx(&q_full[s], 2 * TILE);
+          tc::tma_load_2d(&tqkv, sQ + s * TILE, &q_full[s], it.h * DH, y0 + j * 128);
+          tc::tma_load_2d(&tdo, sDO + s * TILE, &q_full[s], it.h * DH, y0 + j * 128);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (whole warp walks the loop; one lane issues) ----------------
+    constexpr uint32_t id_ss = tc::idesc_bf16(128, 128, 0, 0);   // S^T, dP^T: K-major x K-major
+    constexpr uint32_t id_kb = tc::idesc_bf16(128, DH, 0, 1);    // dV, dK: A K-major, B MN-major
+    constexpr uint32_t id_mm = tc::idesc_bf16(128, DH, 1, 1);    // dQ: A (dS) MN-major, B (K) MN-major
+    const uint32_t k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV), q_addr = tc::smem_u32(sQ);
+    const uint32_t do_addr = tc::smem_u32(sDO), ds_addr = tc::smem_u32(sDS);
+    uint32_t li = 0, gq = 0;
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      const BItem it = take(sItem, it_full, it_empty, li);
+      const uint32_t kv = li % KVST;
+      tc::mbar_wait(&kv_full[kv], (li / KVST) & 1);
+      for (int j = 0; j < it.nq; ++j, ++gq) {
+        const uint32_t s = gq % QST;
+        tc::mbar_wait(&q_full[s], (gq / QST) & 1);
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint64_t kd = tc::sdesc(k_addr + kv * TILE, 16, 1024, tc::SW_128B);
+          const uint64_t vd = tc::sdesc(v_addr + kv * TILE, 16, 1024, tc::SW_128B);
+          const uint64_t qd = tc::sdesc(q_addr + s * TILE, 16, 1024, tc::SW_128B);
+          const uint64_t dod = tc::sdesc(do_addr + s * TILE, 16, 1024, tc::SW_128B);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            tc::mma_bf16_ss(tmem + C_S, kd + kk * 2, qd + kk * 2, id_ss, kk > 0);
+#pragma unroll
+          for (int kk = 0; kk < DH / 16; ++kk)
+            tc::mma_bf16_ss(tmem + C_DP, vd + kk * 2, dod + kk * 2, id_ss, kk > 0);
+          tc::mma_commit(s_full);
+        }
+        __syncwarp();
+        tc::mbar_wait(p_full, gq & 1);                    // P^T in TMEM, dS^T in smem
+        if (j == 0 && li > 0) tc::mbar_wait(dkv_free, (li - 1) & 1);   // dK / dV of the last item read
+        if (gq > 0) tc::mbar_wait(dq_free, (gq - 1) & 1);              // dQ of the last block read
+        tc::tc_fence_after();
+        if (tc::elect_one()) {
+          const uint64_t q_mn = tc::sdesc(q_addr + s * TILE, TILE, 1024, tc::SW_128B);
+          const uint64_t do_mn = tc::sdesc(do_addr + s * TILE, TILE, 1024, tc::SW_128B);
+          const uint64_t k_mn = tc::sdesc(k_addr + kv * TILE, TILE, 1024, tc::SW_128B);
+          const uint64_t ds_k = tc::sdesc(ds_addr, 16, 1024, tc::SW_128B);
+          const uint64_t ds_mn = tc::sdesc(ds_addr, TILE, 1024, tc::SW_128B);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {               // K = 128 queries, 16 per MMA
+            const uint32_t acc = (j > 0 || kk > 0) ? 1u : 0u;
+            const uint32_t mn_adv = (uint32_t)(kk * 2048) >> 4;
+            tc::mma_bf16_ts(tmem + C_DV, tmem + C_P + kk * 8, do_mn + mn_adv, id_kb, acc);
+            const uint32_t k_adv = (uint32_t)((kk >> 2) * TILE + (kk & 3) * 32) >> 4;
+            tc::mma_bf16_ss(tmem + C_DK, ds_k + k_adv, q_mn + mn_adv, id_kb, acc);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {               // K = 128 keys
+            const uint32_t mn_adv = (uint32_t)(kk * 2048) >> 4;
+            tc::mma_bf16_ss(tmem + C_DQ, ds_mn + mn_adv, k_mn + mn_adv, id_mm, kk > 0);
+          }
+          tc::mma_commit(&q_empty[s]);
+          tc::mma_commit(dq_full);
+          if (j + 1 == it.nq) {
+            tc::mma_commit(dkv_full);
+            tc::mma_commit(&kv_empty[kv]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // ---------------- P^T / dS^T (thread = key row) ----------------
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
+    uint8_t* dsrow = sDS + r * 128;
+    const int sw = r & 7;
+    uint32_t li = 0, gq = 0;
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      const BItem it = take(sItem, it_full, it_empty, li);
+      const bool kval = it.k0 + r < it.n;
+      for (int j = 0; j < it.nq; ++j, ++gq) {
+        const int buf = gq & 1;
+        {   // stage this block's lse2 / Delta (query j*128 + r)
+          const int q = j * 128 + r;
+          const int64_t o = (int64_t)it.h * ld_stat + it.base + q;
+          sL[buf * 128 + r] = q < it.n ? __ldg(lse + o) : 0.f;
+          sDl[buf * 128 + r] = q < it.n ? __ldg(delta + o) : 0.f;
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+        const float* L = sL + buf * 128;
+        const float* Dl = sDl + buf * 128;
+        const int qv = it.n - j * 128;                     // valid queries in this block
+        tc::mbar_wait(s_full, gq & 1);
+        tc::tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t sr[32], dr[32];
+          tc::tmem_ld32(lb + C_S + c0, sr);
+          tc::tmem_ld32(lb + C_DP + c0, dr);
+          tc::tmem_ld_wait();
+          uint32_t pk[16], dk[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            float p0 = 0.f, p1 = 0.f;
+            if (kval && c0 + e < qv) p0 = ex2f(__uint_as_float(sr[e]) * sl - L[c0 + e]);
+            if (kval && c0 + e + 1 < qv) p1 = ex2f(__uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1]);
+            const float d0 = p0 * (__uint_as_float(dr[e]) - Dl[c0 + e]);
+            const float d1 = p1 * (__uint_as_float(dr[e + 1]) - Dl[c0 + e + 1]);
+            pk[e / 2] = tc::pack_bf16(p0, p1);
+            dk[e / 2] = tc::pack_bf16(d0, d1);
+          }
+          tc::tmem_st16(lb + C_P + c0 / 2, pk);
+          uint8_t* atom = dsrow + (c0 >> 6) * TILE;
+          const int cb = (c0 & 63) >> 3;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            *reinterpret_cast<uint4*>(atom + (((cb + u) ^ sw) << 4)) =
+                make_uint4(dk[4 * u], dk[4 * u + 1], dk[4 * u + 2], dk[4 * u + 3]);
+        }
+        tc::tmem_st_wait();
+        tc::fence_proxy_async_smem();
+        tc::tc_fence_before();
+        tc::mbar_arrive(p_full);
+      }
+      // item end: dK c and dV of this key row -> dqkv
+      tc::mbar_wait(dkv_full, li & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {             // 0: dV, 1: dK
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(lb + (part ? C_DK : C_DV) + c0, v);
+          tc::tmem_ld_wait();
+          if (kval) {
+            const float f = part ? cs : 1.f;
+            __nv_bfloat16* dst = dqkv + (it.base + it.k0 + r) * (int64_t)(3 * D) + (part ? D : 2 * D) +
+                                 it.h * DH + c0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              reinterpret_cast<uint4*>(dst)[u] =
+                  make_uint4(tc::pack_bf16(__uint_as_float(v[8 * u]) * f, __uint_as_float(v[8 * u + 1]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 2]) * f, __uint_as_float(v[8 * u + 3]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 4]) * f, __uint_as_float(v[8 * u + 5]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 6]) * f, __uint_as_float(v[8 * u + 7]) * f));
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(dkv_free);
+    }
+  } else if (warp >= 8) {
+    // ---------------- dQ_j c -> fp32 atomics (thread = query row of the block) ----------------
+    const int q4 = warp & 3;
+    const int i = q4 * 32 + lane;
+    const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
+    uint32_t li = 0, gq = 0;
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
+      const BItem it = take(sItem, it_full, it_empty, li);
+      for (int j = 0; j < it.nq; ++j, ++gq) {
+        tc::mbar_wait(dq_full, gq & 1);
+        tc::tc_fence_after();
+        const bool valid = j * 128 + i < it.n;
+        float* dst = dq_acc + (it.base + j * 128 + i) * (int64_t)D + it.h * DH;
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(lb + C_DQ + c0, v);
+          tc::tmem_ld_wait();
+          if (valid) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+              red_add_v4(dst + c0 + 4 * u, __uint_as_float(v[4 * u]) * cs, __uint_as_float(v[4 * u + 1]) * cs,
+                         __uint_as_float(v[4 * u + 2]) * cs, __uint_as_float(v[4 * u + 3]) * cs);
+          }
+        }
+        tc::tc_fence_before();
+        tc::mbar_arrive(dq_free);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+bool launch_attention_bwd_tc(const void* qkv, const void* dout, int64_t rows, const float* lse, const float* delta,
+                             int64_t ld_stat, float* dq_acc, void* dqkv, const ChunkDev& ch, int B, int D, int heads,
+                             int d, cudaStream_t st) {
+  if (d != DH) return false;
+  CUtensorMap tq, tdo;
+  if (!make_tmap_bf16(&tq, qkv, rows, 3LL * D, 3LL * D, 128, DH, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  if (!make_tmap_bf16(&tdo, dout, rows, D, D, 128, DH, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  static std::atomic<uint64_t> attr_done{0};
+  if (!smem_attr_once(reinterpret_cast<const void*>(attn_bwd_kernel), SMEM, &attr_done)) return false;
+  const int64_t n_items = (int64_t)ch.nqb * heads * B;
+  if (n_items == 0) return true;
+  if (n_items >= (int64_t)INT32_MAX) return false;
+  const unsigned grid = (unsigned)std::min<int64_t>(n_items, num_sms());
+  attn_bwd_kernel<<<grid, THREADS, SMEM, st>>>(tq, tdo, lse, delta, ld_stat, dq_acc,
+                                               reinterpret_cast<__nv_bfloat16*>(dqkv), ch, D, heads, (int)n_items);
+  return true;
+}
+
+}  // namespace orbit2

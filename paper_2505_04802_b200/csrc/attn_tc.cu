@@ -266,7 +266,8 @@ template <int DH, int NQ>
 __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tmo,
                    __nv_bfloat16* __restrict__ out, ChunkDev ch, int D,
-                   int heads, int n_items, long long* __restrict__ tl) {
+                   int heads, int n_items, long long* __restrict__ tl, float* __restrict__ lse,
+                   int64_t ld_stat) {
   // tl: optional debug timeline (clock64 stamps of CTA 0), null in production
   using C = AttnCfg<DH, NQ>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -705,6 +706,10 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
         l_run += xl[(hh ^ 1) * 128 + i];
       }
       const float inv = 1.f / l_run;
+      if (lse != nullptr && hh == 0) {   // training: per-row log-sum-exp (log2 units) for the backward
+        const int qr = it.q0 + qt * 128 + i;
+        if (qr < it.n) lse[(int64_t)it.h * ld_stat + it.base + qr] = m_ref + log2f(l_run);
+      }
       if constexpr (C::STAGED) {
         // O / l -> bf16, staged in this warp's 32-row slice in the TMA store's
         // swizzled layout (16-B chunk c of row r at chunk c ^ (r & mask):
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
 
 template <int DH>
 bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int B, int D, int heads,
-               cudaStream_t st) {
+               cudaStream_t st, float* lse, int64_t ld_stat) {
   constexpr int NQ = 2;
   using C = AttnCfg<DH, NQ>;
   CUtensorMap tm;
@@ -807,15 +812,15 @@ bool launch_dh(const void* qkv, int64_t rows, void* out, const ChunkDev& ch, int
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, sms);   // persistent: one CTA per SM
   attn_tc_kernel<DH, NQ><<<grid, C::THREADS, C::SMEM, st>>>(tm, tmo, reinterpret_cast<__nv_bfloat16*>(out), ch, D,
-                                                             heads, (int)n_items, g_attn_timeline);
+                                                             heads, (int)n_items, g_attn_timeline, lse, ld_stat);
   return true;
 }
 
 }  // namespace
 
 bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B, int D,
-                         int heads, int d, cudaStream_t st) {
-  if (d == 32) return launch_dh<32>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+                         int heads, int d, cudaStream_t st, float* lse, int64_t ld_stat) {
+  if (d == 32) return launch_dh<32>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st, lse, ld_stat);
   if (d == 64) {
     // Short tiles (mean under 768 tokens, e.g. C3's 312-432): three Q tiles on 64-key
     // blocks (attn3_tc.cu; less padding of the last key block, three softmax warps per
@@ -823,11 +828,12 @@ bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16,
     // this kernel (19.0 vs 19.3-19.7 ms at C2).  ORBIT2_ATTN=2 / 3 forces one.
     const char* e = std::getenv("ORBIT2_ATTN");
     const int64_t mean_n = ch.tc > 0 ? ch.chunk_tokens / ch.tc : 0;
-    const bool use3 = e && e[0] == '3' ? true : (e && e[0] == '2' ? false : mean_n < 768);
+    // (training forward, lse != null: this kernel, which also writes the row log-sum-exp)
+    const bool use3 = lse == nullptr && (e && e[0] == '3' ? true : (e && e[0] == '2' ? false : mean_n < 768));
     if (use3) return launch_attention3_tc(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
-    return launch_dh<64>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+    return launch_dh<64>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st, lse, ld_stat);
   }
-  if (d == 128) return launch_dh<128>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st);
+  if (d == 128) return launch_dh<128>(qkv_bf16, qkv_rows, out_bf16, ch, B, D, heads, st, lse, ld_stat);
   return false;
 }
 

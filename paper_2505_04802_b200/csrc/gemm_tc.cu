@@ -137,7 +137,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
   const bool full = n0 + 32 <= ep.N;
-  if (full) {
+  if constexpr (EPI == EPI_DGELU) {
+  } else if (full) {
     const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
@@ -150,10 +151,23 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
       if (n0 + j < ep.N) v[j] += __ldg(ep.bias + n0 + j);
   }
   if constexpr (EPI == EPI_GELU) {
+    if (ep.aux) {   // training: keep the pre-activation
+      __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(ep.aux)) + row * ep.ldc + n0;
+      for (int j = 0; j < 32; ++j)
+        if (n0 + j < ep.N) h[j] = __float2bfloat16_rn(v[j]);
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = 0.5f * v[j] * (1.0f + erff(v[j] * 0.70710678118654752f));
   }
-  if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU) {
+  if constexpr (EPI == EPI_DGELU) {   // v = acc (no bias): dh = dgelu * GELU'(h)
+    const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ldc + n0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float x = n0 + j < ep.N ? __bfloat162float(h[j]) : 0.f;
+      v[j] = v[j] * (0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x));
+    }
+  }
+  if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) {
     if constexpr (OUT_BF16) {
       __nv_bfloat16* c = reinterpret_cast<__nv_bfloat16*>(ep.C) + row * ep.ldc + n0;
       if (full) {
@@ -184,17 +198,18 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
     }
   } else if constexpr (EPI == EPI_RESID) {
     float* z = reinterpret_cast<float*>(ep.C) + row * ep.ldc + n0;
+    const float* zs = ep.aux ? reinterpret_cast<const float*>(ep.aux) + row * ep.ldc + n0 : z;
     if (full) {
       float4* z4 = reinterpret_cast<float4*>(z);
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        float4 o = z4[j];
+        float4 o = reinterpret_cast<const float4*>(zs)[j];
         o.x += v[4 * j]; o.y += v[4 * j + 1]; o.z += v[4 * j + 2]; o.w += v[4 * j + 3];
         z4[j] = o;
       }
     } else {
       for (int j = 0; j < 32; ++j)
-        if (n0 + j < ep.N) z[j] += v[j];
+        if (n0 + j < ep.N) z[j] = zs[j] + v[j];
     }
   } else {  // EPI_EMBED: z = acc + bias + pi(u,w); 32-column chunks never straddle D/2 (D % 64 == 0)
     const int2 uw = __ldg(ep.rowinfo + row);
@@ -502,16 +517,18 @@ __global__ void __launch_bounds__(384, 1)
           if (row < M) {
             const float bf = __ldg(ep.bias + row);
             float* zc = reinterpret_cast<float*>(ep.C) + (n0 + c0) * ep.ldc + row;
+            // training: residual input from aux (the forward keeps z_in), else in place
+            const float* zs = ep.aux ? reinterpret_cast<const float*>(ep.aux) + (n0 + c0) * ep.ldc + row : zc;
             const int64_t t0 = n0 + c0;
             if (t0 + 32 <= ep.M) {
               float zv[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) zv[j] = zc[(int64_t)j * ep.ldc];
+              for (int j = 0; j < 32; ++j) zv[j] = zs[(int64_t)j * ep.ldc];
 #pragma unroll
               for (int j = 0; j < 32; ++j) zc[(int64_t)j * ep.ldc] = zv[j] + (__uint_as_float(r[j]) + bf);
             } else {
               for (int j = 0; j < 32; ++j)
-                if (t0 + j < ep.M) zc[(int64_t)j * ep.ldc] += __uint_as_float(r[j]) + bf;
+                if (t0 + j < ep.M) zc[(int64_t)j * ep.ldc] = zs[(int64_t)j * ep.ldc] + (__uint_as_float(r[j]) + bf);
             }
           }
         } else if constexpr (TMA_OUT) {
@@ -533,6 +550,17 @@ __global__ void __launch_bounds__(384, 1)
                 v[j] = __uint_as_float(r[j]) + (n0 + c0 + j < ep.N ? __ldg(ep.bias + n0 + c0 + j) : 0.f);
             }
             if constexpr (EPI == EPI_GELU) {
+              if (ep.aux != nullptr && row < M) {   // training: keep the pre-activation (64 B per row)
+                uint4* h = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(ep.aux)) +
+                                                    row * ep.ldc + n0 + c0);
+                if (n0 + c0 + 32 <= ep.N) {
+#pragma unroll
+                  for (int u = 0; u < 4; ++u)
+                    h[u] = make_uint4(tc::pack_bf16(v[8 * u], v[8 * u + 1]), tc::pack_bf16(v[8 * u + 2], v[8 * u + 3]),
+                                      tc::pack_bf16(v[8 * u + 4], v[8 * u + 5]),
+                                      tc::pack_bf16(v[8 * u + 6], v[8 * u + 7]));
+                }
+              }
 #pragma unroll
               for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
             }
@@ -635,6 +663,7 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
       case EPI_GELU: return launch_impl<BN, ST, EPI_GELU, true>(A, Bw, M, N, K, ep, st);
       case EPI_RESID: return launch_impl<BN, ST, EPI_RESID, false>(A, Bw, M, N, K, ep, st);
       case EPI_EMBED: return launch_impl<BN, ST, EPI_EMBED, false>(A, Bw, M, N, K, ep, st);
+      case EPI_DGELU: return launch_impl<BN, ST, EPI_DGELU, true>(A, Bw, M, N, K, ep, st);
     }
   } else {
     constexpr int BN = 128, ST = 5;

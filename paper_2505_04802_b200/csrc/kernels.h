@@ -21,6 +21,9 @@ enum Epi : int {
   // epilogue): the updated z row is written and LN(z) -> xn (bf16) as well
   EPI_RESID_LN = 4,   // z += acc + bias; xn = LN(z)     (O-projection + LN2)
   EPI_EMBED_LN = 5,   // z = acc + bias + pi; xn = LN(z) (patch embed + LN1 of block 0)
+  // training backward: C[m,n] = bf16(acc * GELU'(aux[m,n]))  (aux = the forward's
+  // pre-activation, bf16 [M][ldc]; GELU' = Phi(x) + x phi(x), R9)
+  EPI_DGELU = 6,
 };
 
 struct EpiParams {
@@ -36,6 +39,10 @@ struct EpiParams {
   void* xn;                // *_LN: bf16 LayerNorm output [M][N]
   const float* ln_g;       // *_LN: LayerNorm gain / bias [N]
   const float* ln_b;
+  // training: EPI_GELU also stores the pre-activation (bf16, same ldc) here; EPI_RESID
+  // reads the residual input from here (fp32, same ldc) instead of C (C = aux + acc + bias);
+  // EPI_DGELU: the pre-activation it differentiates
+  const void* aux = nullptr;
 };
 
 struct GemmOperand {
@@ -122,7 +129,13 @@ void launch_add_vec(const float* a, const float* b, float* out, int64_t n, cudaS
 bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N,
                     int64_t K, const EpiParams& ep, cudaStream_t st);
 bool launch_attention_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B,
-                         int D, int heads, int d, cudaStream_t st);
+                         int D, int heads, int d, cudaStream_t st, float* lse = nullptr, int64_t ld_stat = 0);
+// training: attention backward (attn_bwd_tc.cu), head dim 64.  dO [rows][D] bf16; lse / delta
+// [heads][ld_stat] fp32 (log2-unit row log-sum-exp of the forward, sum_d dO O); dq_acc [rows][D]
+// fp32 zeroed by the caller (atomics: c dS K); dK c and dV written into dqkv's K / V columns
+bool launch_attention_bwd_tc(const void* qkv, const void* dout, int64_t rows, const float* lse, const float* delta,
+                             int64_t ld_stat, float* dq_acc, void* dqkv, const ChunkDev& ch, int B, int D, int heads,
+                             int d, cudaStream_t st);
 // head dim 64: three Q tiles per CTA on 64-key blocks (attn3_tc.cu)
 bool launch_attention3_tc(const void* qkv_bf16, int64_t qkv_rows, void* out_bf16, const ChunkDev& ch, int B, int D,
                           int heads, cudaStream_t st);
@@ -139,6 +152,25 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
                        const float* ln1n_b, void* xn_next,
                        const int32_t* row_blocks /* null: every 128-row block */, int32_t n_row_blocks,
                        cudaStream_t st);
+
+// training: weight gradients dW[n][k] += sum_m dY[m][n] X[m][k] (+ db[n] += sum_m dY[m][n] when
+// db != null) with MN-major operands, split-K over the tokens, fp32 atomics (wgrad_tc.cu)
+bool launch_wgrad_tc(const GemmOperand& dY, const GemmOperand& X, int64_t M, int N, int Kc, float* dW, int64_t ldo,
+                     float* db, cudaStream_t st);
+
+// ---- training step, SIMT / HBM-bound parts (train_simt.cu) ----
+void launch_lat_weights(float* w, int sH, cudaStream_t st);
+void launch_loss(const float* out, const float* truth, int B, int K, int sH, int sW, float lam, float delta, int geo,
+                 const float* latw, double* loss, float* dout, cudaStream_t st);
+void launch_stitch_bwd(const float* dout, __nv_bfloat16* dg, int64_t ldg, const ChunkDev& ch, int B, int K, int P,
+                       int sH, int sW, cudaStream_t st);
+bool launch_ln_bwd(const float* dy, int64_t ldy, const float* z, const float* g, const float* dres, float* dz,
+                   __nv_bfloat16* dz_bf, int64_t M, int D, const int32_t* rowmap, int64_t map_per_b,
+                   int64_t chunk_tokens, int64_t tok0, float* dgamma, float* dbeta, cudaStream_t st);
+void launch_delta(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* delta, int64_t M, int D, int heads,
+                  int64_t ld_stat, cudaStream_t st);
+void launch_dq_convert(const float* dq, __nv_bfloat16* dqkv, int64_t M, int D, cudaStream_t st);
+void launch_transpose_bf16(const float* W, int n, int k, __nv_bfloat16* Wt, int64_t ld, cudaStream_t st);
 
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();

@@ -30,6 +30,20 @@ struct Timing {
   cudaEvent_t a, b;
 };
 
+// Training workspace (orbit2_train_bind): activations the backward needs, kept per block,
+// the backward's scratch and the transposed bf16 weights of the input-gradient GEMMs.
+struct TrainLay {
+  int64_t rows = 0, rows_core = 0;       // mrow, mcore of the plan
+  int64_t nh_pad = 0;                    // K P^2 rounded up to 64 (GEMM K of dhin = dG W_h)
+  std::vector<int64_t> zin, xn1, qkv, ao, lse, zmid, xn2, hpre, hact;   // per block
+  int64_t zfin = 0, hin = 0;
+  int64_t dz = 0, dz_bf = 0, dzm = 0, dzm_bf = 0, dh = 0, dxn = 0, dao = 0, delta = 0, dq = 0, dqkv = 0;
+  int64_t dg = 0, dhin = 0, latw = 0, zero = 0;
+  std::vector<int64_t> wqkv_t, wo_t, w1_t, w2_t;   // per block, bf16 [in][out]
+  int64_t wh_t = 0;                      // bf16 [D][nh_pad]
+  int64_t total = 0;
+};
+
 struct Ctx {
   Plan plan;
   WeightLayout wl;
@@ -54,6 +68,13 @@ struct Ctx {
   float* target = nullptr;            // where this rank's stitch writes (root's field or its own)
   uint64_t epoch[2] = {0, 0};         // per barrier slot: 0 = after halo push, 1 = end of step
   std::vector<void*> opened;          // peer allocations opened with cudaIpcOpenMemHandle
+  // training (orbit2_train_*)
+  TrainLay tl;
+  uint8_t* tws = nullptr;
+  bool train_prepared = false;
+  int64_t tl_lda_patch = 0, tl_cols_patch = 0;   // patch rows of the last training forward
+  template <typename T>
+  T* tat(int64_t off) const { return reinterpret_cast<T*>(tws + off); }
 
   template <typename T>
   T* at(int64_t off) const { return reinterpret_cast<T*>(ws + off); }
@@ -913,6 +934,385 @@ orbit2_status orbit2_comm_status(void* ctx) {
   if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("orbit2_comm_status: ") + cudaGetErrorString(e));
   if (err != 0)
     return set_err(ORBIT2_E_STATE, "orbit2 comm barrier timed out (30 s) waiting for rank " + std::to_string(err - 1));
+  return ORBIT2_OK;
+}
+
+
+/* ------------------------------------------------------------------------------
+ * Training step (oracle/train.py T1-T4, readings R34-R36)
+ * ---------------------------------------------------------------------------- */
+static orbit2_status train_scope(const Ctx* c) {
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  if (cf.precision != ORBIT2_BF16) return set_err(ORBIT2_E_UNSUPPORTED, "training: BF16 precision only");
+  if (p.d != 64) return set_err(ORBIT2_E_UNSUPPORTED, "training: head_dim 64 only (attention backward kernel)");
+  if (cf.var_agg || cf.res_hidden || cf.dec_hidden)
+    return set_err(ORBIT2_E_UNSUPPORTED, "training: var_agg / res_hidden / dec_hidden stages are out of scope (R36)");
+  if (p.info.chunk_tiles < p.info.n_local_tiles)
+    return set_err(ORBIT2_E_UNSUPPORTED, "training: one call over every rank-local tile (chunk_tiles = 0)");
+  if (p.D > 1024) return set_err(ORBIT2_E_UNSUPPORTED, "training: embed <= 1024 (LayerNorm backward kernel)");
+  return ORBIT2_OK;
+}
+
+static TrainLay train_layout(const Plan& p) {
+  TrainLay t;
+  const int64_t D = p.D, L = p.cfg.depth, H = p.cfg.heads;
+  t.rows = p.lay.mrow;
+  t.rows_core = p.lay.mcore;
+  t.nh_pad = round_up(p.Nh, 64);
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) { int64_t o = off; off = round_up(off + bytes, 1024); return o; };
+  const int64_t R = t.rows, RC = t.rows_core;
+  for (int64_t l = 0; l < L; ++l) {
+    t.zin.push_back(take(R * D * 4));
+    t.xn1.push_back(take(R * D * 2));
+    t.qkv.push_back(take(R * 3 * D * 2));
+    t.ao.push_back(take(R * D * 2));
+    t.lse.push_back(take(H * R * 4));
+    t.zmid.push_back(take(R * D * 4));
+    t.xn2.push_back(take(R * D * 2));
+    t.hpre.push_back(take(R * 4 * D * 2));
+    t.hact.push_back(take(R * 4 * D * 2));
+  }
+  t.zfin = take(R * D * 4);
+  t.hin = take(RC * D * 2);
+  t.dz = take(R * D * 4);
+  t.dz_bf = take(R * D * 2);
+  t.dzm = take(R * D * 4);
+  t.dzm_bf = take(R * D * 2);
+  t.dh = take(R * 4 * D * 2);
+  t.dxn = take(R * D * 4);
+  t.dao = take(R * D * 2);
+  t.delta = take(H * R * 4);
+  t.dq = take(R * D * 4);
+  t.dqkv = take(R * 3 * D * 2);
+  t.dg = take(RC * t.nh_pad * 2);
+  t.dhin = take(RC * D * 4);
+  t.latw = take((int64_t)p.cfg.scale * p.cfg.H * 4);
+  t.zero = take(4 * D * 4 + t.nh_pad * 4);
+  for (int64_t l = 0; l < L; ++l) {
+    t.wqkv_t.push_back(take(D * 3 * D * 2));
+    t.wo_t.push_back(take(D * D * 2));
+    t.w1_t.push_back(take(D * 4 * D * 2));
+    t.w2_t.push_back(take(4 * D * D * 2));
+  }
+  t.wh_t = take(D * t.nh_pad * 2);
+  t.total = off;
+  return t;
+}
+
+orbit2_status orbit2_train_plan(void* ctx, orbit2_train_info* info) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c || !info) return set_err(ORBIT2_E_INVALID, "ctx/info: null");
+  ORBIT2_TRY(train_scope(c));
+  const Plan& p = c->plan;
+  const TrainLay t = train_layout(p);
+  info->workspace_bytes = t.total;
+  info->canonical_weight_count = c->wl.c_total;
+  // algorithmic FLOPs per sample: forward (every query of every block) + backward
+  // (input and weight gradients of every GEMM except the patches' input gradient;
+  // attention: S recomputed, dP, dV, dK, dQ = 2.5x its forward)
+  const double D = p.D, L = p.cfg.depth, Din = p.Din, Nh = p.Nh;
+  const double n = (double)p.info.local_tokens, nc = (double)p.info.local_core_tokens;
+  double n2 = 0.0;
+  for (int32_t i = 0; i < p.info.n_local_tiles; ++i) n2 += (double)p.dev[i].n_tokens * p.dev[i].n_tokens;
+  const double gemm = L * 24.0 * D * D * n + 2.0 * Din * D * n + 2.0 * D * Nh * nc;
+  const double attn = L * 4.0 * D * n2;
+  info->fwd_flops_per_sample = gemm + attn;
+  info->flops_per_sample = (gemm + attn) + (2.0 * gemm - 2.0 * Din * D * n) + 2.5 * attn;
+  info->attn_bwd_flops_per_sample = 2.5 * attn;
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_train_bind(void* ctx, void* train_ws_dev, size_t bytes, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  ORBIT2_TRY(train_scope(c));
+  if (!train_ws_dev || !aligned16(train_ws_dev)) return set_err(ORBIT2_E_INVALID, "train_ws_dev: null or unaligned");
+  TrainLay t = train_layout(c->plan);
+  if ((int64_t)bytes < t.total)
+    return set_err(ORBIT2_E_INVALID, "train workspace: " + std::to_string(bytes) + " bytes < " +
+                                         std::to_string(t.total) + " (orbit2_train_plan)");
+  c->tl = t;
+  c->tws = reinterpret_cast<uint8_t*>(train_ws_dev);
+  c->train_prepared = false;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // rows past M of every buffer stay zero (TMA tiles read up to the 128-row padding)
+  cudaError_t e = cudaMemsetAsync(c->tws, 0, (size_t)t.total, st);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("train_bind memset: ") + cudaGetErrorString(e));
+  const int sH = c->plan.cfg.scale * c->plan.cfg.H;
+  return run(c, "lat_weights", st, [&] {
+    launch_lat_weights(c->tat<float>(t.latw), sH, st);
+    return true;
+  });
+}
+
+orbit2_status orbit2_train_prepare(void* ctx, const float* canonical_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->tws) return set_err(ORBIT2_E_STATE, "orbit2_train_prepare: orbit2_train_bind not called");
+  if (!canonical_dev) return set_err(ORBIT2_E_INVALID, "canonical_dev: null");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const WeightLayout& w = c->wl;
+  const TrainLay& t = c->tl;
+  const int D = p.D;
+  typedef __nv_bfloat16 bf16;
+  ORBIT2_TRY(run(c, "weight_transpose", st, [&] {
+    for (int l = 0; l < p.cfg.depth; ++l) {
+      const LayerW& L = w.c_layers[l];
+      launch_transpose_bf16(canonical_dev + L.w_qkv, 3 * D, D, c->tat<bf16>(t.wqkv_t[l]), 3 * D, st);
+      launch_transpose_bf16(canonical_dev + L.w_o, D, D, c->tat<bf16>(t.wo_t[l]), D, st);
+      launch_transpose_bf16(canonical_dev + L.w_1, 4 * D, D, c->tat<bf16>(t.w1_t[l]), 4 * D, st);
+      launch_transpose_bf16(canonical_dev + L.w_2, D, 4 * D, c->tat<bf16>(t.w2_t[l]), D, st);
+    }
+    launch_transpose_bf16(canonical_dev + w.c_w_h, p.Nh, D, c->tat<bf16>(t.wh_t), t.nh_pad, st);
+    return true;
+  }));
+  c->train_prepared = true;
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_train_forward(void* ctx, const void* packed_w, const float* input_dev, void* tile_out_dev,
+                                   void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->tws) return set_err(ORBIT2_E_STATE, "orbit2_train_forward: orbit2_train_bind not called");
+  if (!packed_w || !input_dev || !tile_out_dev || !aligned16(packed_w) || !aligned16(input_dev) ||
+      !aligned16(tile_out_dev))
+    return set_err(ORBIT2_E_INVALID, "packed_w/input_dev/tile_out_dev: null or not 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const Layout& ly = p.lay;
+  const WeightLayout& w = c->wl;
+  const TrainLay& t = c->tl;
+  typedef __nv_bfloat16 bf16;
+  const uint8_t* W8 = reinterpret_cast<const uint8_t*>(packed_w);
+  auto wf = [&](int64_t off) { return reinterpret_cast<const float*>(W8 + off); };
+  const Chunk ch = make_chunk(p, 0, p.info.n_local_tiles);
+  const ChunkDev cd = chunk_dev(c, ch);
+  const int B = cf.batch;
+  const int64_t M = (int64_t)B * ch.chunk_tokens, Mc = (int64_t)B * ch.chunk_core;
+  const int64_t D = p.D, F = 4LL * p.D, R = t.rows;
+  int2* rowinfo = c->at<int2>(ly.rowinfo);
+  bf16* patches = c->at<bf16>(ly.patches);
+  auto gemm = [&](const char* name, int epi, int out_bf, const void* A, int64_t lda, int64_t wo, int64_t n,
+                  int64_t k, int64_t rows, EpiParams ep, int64_t acols = 0) {
+    GemmOperand a{A, R, lda, acols}, b{W8 + wo, n, k};
+    ep.M = (int32_t)rows;
+    ep.N = (int32_t)n;
+    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+  };
+  int64_t lda_patch = ly.din_pad, cols_patch = 0;
+  if (cf.halo_mode == ORBIT2_HALO_CLAMP && !c->simt_gather) {
+    bool ok = false;
+    ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+      ok = launch_gather_tma(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.ld_patch,
+                             p.max_pad_h, p.max_pad_w, st);
+      return true;
+    }));
+    if (ok) {
+      lda_patch = ly.ld_patch;
+      cols_patch = p.Din;
+    }
+  }
+  if (cols_patch == 0)
+    ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+      launch_gather<bf16>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
+                          p.max_pad_h, st);
+      return true;
+    }));
+  c->tl_lda_patch = lda_patch;
+  c->tl_cols_patch = cols_patch ? cols_patch : p.Din;
+  EpiParams emb{};
+  emb.bias = wf(w.bias_e); emb.ldc = D;
+  emb.rowinfo = rowinfo; emb.pos_u = c->at<float>(ly.pos_u); emb.pos_w = c->at<float>(ly.pos_w);
+  emb.pos_off = cf.halo; emb.half = (int32_t)(D / 2);
+  emb.C = cf.depth > 0 ? c->tat<float>(t.zin[0]) : c->tat<float>(t.zfin);
+  {
+    GemmOperand a{patches, ly.mrow, lda_patch, cols_patch}, b{W8 + w.w_e, D, ly.din_pad};
+    emb.M = (int32_t)M;
+    emb.N = (int32_t)D;
+    ORBIT2_TRY(run(c, "embed_gemm", st, [&] { return launch_gemm_tc(EPI_EMBED, 0, a, b, M, D, ly.din_pad, emb, st); }));
+  }
+  for (int l = 0; l < cf.depth; ++l) {
+    const LayerW& L = w.layers[l];
+    float* zin = c->tat<float>(t.zin[l]);
+    float* zmid = c->tat<float>(t.zmid[l]);
+    float* zout = l + 1 < cf.depth ? c->tat<float>(t.zin[l + 1]) : c->tat<float>(t.zfin);
+    bf16* xn1 = c->tat<bf16>(t.xn1[l]);
+    bf16* qkv = c->tat<bf16>(t.qkv[l]);
+    bf16* ao = c->tat<bf16>(t.ao[l]);
+    bf16* xn2 = c->tat<bf16>(t.xn2[l]);
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<bf16>(zin, wf(L.ln1_g), wf(L.ln1_b), xn1, M, (int)D, nullptr, st);
+      return true;
+    }));
+    EpiParams e{};
+    e.bias = wf(L.b_qkv); e.C = qkv; e.ldc = 3 * D;
+    ORBIT2_TRY(gemm("qkv_gemm", EPI_BIAS, 1, xn1, D, L.w_qkv, 3 * D, D, M, e));
+    ORBIT2_TRY(run(c, "tile_attention", st, [&] {
+      return launch_attention_tc(qkv, R, ao, cd, B, (int)D, cf.heads, p.d, st, c->tat<float>(t.lse[l]), R);
+    }));
+    e = EpiParams{}; e.bias = wf(L.b_o); e.C = zmid; e.ldc = D; e.aux = zin;
+    ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID, 0, ao, D, L.w_o, D, D, M, e));
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<bf16>(zmid, wf(L.ln2_g), wf(L.ln2_b), xn2, M, (int)D, nullptr, st);
+      return true;
+    }));
+    e = EpiParams{}; e.bias = wf(L.b_1); e.C = c->tat<bf16>(t.hact[l]); e.ldc = F; e.aux = c->tat<bf16>(t.hpre[l]);
+    ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn2, D, L.w_1, F, D, M, e));
+    e = EpiParams{}; e.bias = wf(L.b_2); e.C = zout; e.ldc = D; e.aux = zmid;
+    ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, c->tat<bf16>(t.hact[l]), F, L.w_2, D, F, M, e));
+  }
+  bf16* hin = c->tat<bf16>(t.hin);
+  ORBIT2_TRY(run(c, "layernorm", st, [&] {
+    launch_layernorm<bf16>(c->tat<float>(t.zfin), wf(w.lnf_g), wf(w.lnf_b), hin, Mc, (int)D, &cd, st);
+    return true;
+  }));
+  EpiParams e{};
+  e.bias = wf(w.b_h); e.C = tile_out_dev; e.ldc = p.Nh; e.M = (int32_t)Mc; e.N = p.Nh;
+  {
+    GemmOperand a{hin, t.rows_core, D, 0}, b{W8 + w.w_h, p.Nh, D};
+    ORBIT2_TRY(run(c, "head_gemm", st, [&] { return launch_gemm_tc(EPI_BIAS, 1, a, b, Mc, p.Nh, D, e, st); }));
+  }
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_loss(void* ctx, const float* out_dev, const float* truth_dev, float lambda, float delta,
+                          int32_t geo, double* loss_dev, float* dout_dev, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->tws) return set_err(ORBIT2_E_STATE, "orbit2_loss: orbit2_train_bind not called");
+  if (!out_dev || !truth_dev || !loss_dev || !dout_dev) return set_err(ORBIT2_E_INVALID, "loss: null pointer");
+  if (!(delta > 0.f) || !(lambda >= 0.f)) return set_err(ORBIT2_E_INVALID, "loss: delta must be > 0, lambda >= 0");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const orbit2_config& cf = c->plan.cfg;
+  const int sH = cf.scale * cf.H, sW = cf.scale * cf.W;
+  cudaError_t e = cudaMemsetAsync(loss_dev, 0, sizeof(double) * cf.batch, st);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("loss memset: ") + cudaGetErrorString(e));
+  return run(c, "bayesian_loss", st, [&] {
+    launch_loss(out_dev, truth_dev, cf.batch, cf.K, sH, sW, lambda, delta, geo ? 1 : 0, c->tat<float>(c->tl.latw),
+                loss_dev, dout_dev, st);
+    return true;
+  });
+}
+
+orbit2_status orbit2_train_backward(void* ctx, const void* packed_w, const float* dout_dev, float* grad_dev,
+                                    void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  if (!c->tws || !c->train_prepared)
+    return set_err(ORBIT2_E_STATE, "orbit2_train_backward: orbit2_train_bind / orbit2_train_prepare not called");
+  if (!packed_w || !dout_dev || !grad_dev || !aligned16(grad_dev))
+    return set_err(ORBIT2_E_INVALID, "packed_w/dout_dev/grad_dev: null or not 16-byte aligned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const Layout& ly = p.lay;
+  const WeightLayout& w = c->wl;
+  const TrainLay& t = c->tl;
+  typedef __nv_bfloat16 bf16;
+  const uint8_t* W8 = reinterpret_cast<const uint8_t*>(packed_w);
+  auto wf = [&](int64_t off) { return reinterpret_cast<const float*>(W8 + off); };
+  const Chunk ch = make_chunk(p, 0, p.info.n_local_tiles);
+  const ChunkDev cd = chunk_dev(c, ch);
+  const int B = cf.batch;
+  const int64_t M = (int64_t)B * ch.chunk_tokens, Mc = (int64_t)B * ch.chunk_core;
+  const int D = p.D, F = 4 * p.D;
+  const int64_t R = t.rows;
+  const float* zero = c->tat<float>(t.zero);
+  auto memset0 = [&](void* ptr, size_t bytes) {
+    cudaError_t e = cudaMemsetAsync(ptr, 0, bytes, st);
+    return e == cudaSuccess ? ORBIT2_OK : set_err(ORBIT2_E_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  };
+  // input-gradient GEMM: C[rows][n] = A[rows][k] W^T-operand[n][k] (the transposed weights)
+  auto dx = [&](const char* name, int epi, int out_bf, const void* A, int64_t arows, int64_t lda, const void* Bt,
+                int64_t n, int64_t k, int64_t rows, void* C, int64_t ldc, const void* aux, int64_t acols = 0) {
+    GemmOperand a{A, arows, lda, acols}, b{Bt, n, k};
+    EpiParams ep{};
+    ep.M = (int32_t)rows; ep.N = (int32_t)n; ep.bias = zero; ep.C = C; ep.ldc = ldc; ep.aux = aux;
+    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+  };
+  auto wg = [&](const char* name, const void* dY, int64_t ldy, const void* X, int64_t ldx, int64_t rows, int n,
+                int kc, int64_t gw, int64_t gb) {
+    GemmOperand a{dY, rows, ldy, 0}, x{X, rows, ldx, 0};
+    return run(c, name, st, [&] {
+      return launch_wgrad_tc(a, x, rows, n, kc, grad_dev + gw, kc, gb >= 0 ? grad_dev + gb : nullptr, st);
+    });
+  };
+  ORBIT2_TRY(memset0(grad_dev, (size_t)w.c_total * 4));
+  // O6 backwards, then the head (g = LN_f(z_core) W_h^T + b_h)
+  bf16* dg = c->tat<bf16>(t.dg);
+  ORBIT2_TRY(run(c, "stitch_bwd", st, [&] {
+    launch_stitch_bwd(dout_dev, dg, t.nh_pad, cd, B, cf.K, p.P, cf.scale * cf.H, cf.scale * cf.W, st);
+    return true;
+  }));
+  bf16* hin = c->tat<bf16>(t.hin);
+  ORBIT2_TRY(wg("wgrad_head", dg, t.nh_pad, hin, D, Mc, p.Nh, D, w.c_w_h, w.c_b_h));
+  float* dhin = c->tat<float>(t.dhin);
+  ORBIT2_TRY(dx("dx_head", EPI_BIAS, 0, dg, t.rows_core, t.nh_pad, c->tat<bf16>(t.wh_t), D, t.nh_pad, Mc, dhin, D,
+                nullptr));
+  float* dz = c->tat<float>(t.dz);
+  bf16* dz_bf = c->tat<bf16>(t.dz_bf);
+  ORBIT2_TRY(memset0(dz, (size_t)R * D * 4));
+  ORBIT2_TRY(memset0(dz_bf, (size_t)R * D * 2));
+  ORBIT2_TRY(run(c, "ln_bwd", st, [&] {   // LN_f over the core rows (R16: halo rows get no gradient)
+    return launch_ln_bwd(dhin, D, c->tat<float>(t.zfin), wf(w.lnf_g), nullptr, dz, dz_bf, Mc, D, cd.core_row + ch.core0,
+                         ch.chunk_core, ch.chunk_tokens, ch.tok0, grad_dev + w.c_lnf_g, grad_dev + w.c_lnf_b, st);
+  }));
+  float* dzm = c->tat<float>(t.dzm);
+  bf16* dzm_bf = c->tat<bf16>(t.dzm_bf);
+  bf16* dh = c->tat<bf16>(t.dh);
+  float* dxn = c->tat<float>(t.dxn);
+  bf16* dao = c->tat<bf16>(t.dao);
+  bf16* dqkv = c->tat<bf16>(t.dqkv);
+  float* dq = c->tat<float>(t.dq);
+  float* dlt = c->tat<float>(t.delta);
+  for (int l = cf.depth - 1; l >= 0; --l) {
+    const LayerW& CL = w.c_layers[l];
+    const LayerW& L = w.layers[l];
+    // z_out = zmid + GELU(h) W_2^T + b_2,  h = LN2(zmid) W_1^T + b_1
+    ORBIT2_TRY(wg("wgrad_w2", dz_bf, D, c->tat<bf16>(t.hact[l]), F, M, D, F, CL.w_2, CL.b_2));
+    ORBIT2_TRY(dx("dx_mlp_down", EPI_DGELU, 1, dz_bf, R, D, c->tat<bf16>(t.w2_t[l]), F, D, M, dh, F,
+                  c->tat<bf16>(t.hpre[l])));
+    ORBIT2_TRY(wg("wgrad_w1", dh, F, c->tat<bf16>(t.xn2[l]), D, M, F, D, CL.w_1, CL.b_1));
+    ORBIT2_TRY(dx("dx_mlp_up", EPI_BIAS, 0, dh, R, F, c->tat<bf16>(t.w1_t[l]), D, F, M, dxn, D, nullptr));
+    ORBIT2_TRY(run(c, "ln_bwd", st, [&] {
+      return launch_ln_bwd(dxn, D, c->tat<float>(t.zmid[l]), wf(L.ln2_g), dz, dzm, dzm_bf, M, D, nullptr, 0, 0, 0,
+                           grad_dev + CL.ln2_g, grad_dev + CL.ln2_b, st);
+    }));
+    // zmid = z_in + attn W_o^T + b_o
+    bf16* ao = c->tat<bf16>(t.ao[l]);
+    ORBIT2_TRY(wg("wgrad_wo", dzm_bf, D, ao, D, M, D, D, CL.w_o, CL.b_o));
+    ORBIT2_TRY(dx("dx_oproj", EPI_BIAS, 1, dzm_bf, R, D, c->tat<bf16>(t.wo_t[l]), D, D, M, dao, D, nullptr));
+    // attention (per tile, per head)
+    ORBIT2_TRY(run(c, "attn_delta", st, [&] {
+      launch_delta(dao, ao, dlt, M, D, cf.heads, R, st);
+      return true;
+    }));
+    ORBIT2_TRY(memset0(dq, (size_t)M * D * 4));
+    ORBIT2_TRY(run(c, "attn_bwd", st, [&] {
+      return launch_attention_bwd_tc(c->tat<bf16>(t.qkv[l]), dao, R, c->tat<float>(t.lse[l]), dlt, R, dq, dqkv, cd, B,
+                                     D, cf.heads, p.d, st);
+    }));
+    ORBIT2_TRY(run(c, "dq_convert", st, [&] {
+      launch_dq_convert(dq, dqkv, M, D, st);
+      return true;
+    }));
+    // qkv = LN1(z_in) W_qkv^T + b_qkv
+    ORBIT2_TRY(wg("wgrad_wqkv", dqkv, 3 * D, c->tat<bf16>(t.xn1[l]), D, M, 3 * D, D, CL.w_qkv, CL.b_qkv));
+    ORBIT2_TRY(dx("dx_qkv", EPI_BIAS, 0, dqkv, R, 3 * D, c->tat<bf16>(t.wqkv_t[l]), D, 3 * D, M, dxn, D, nullptr));
+    ORBIT2_TRY(run(c, "ln_bwd", st, [&] {
+      return launch_ln_bwd(dxn, D, c->tat<float>(t.zin[l]), wf(L.ln1_g), dzm, dz, dz_bf, M, D, nullptr, 0, 0, 0,
+                           grad_dev + CL.ln1_g, grad_dev + CL.ln1_b, st);
+    }));
+  }
+  // z0 = patches W_e^T + b_e + e_s + pi
+  ORBIT2_TRY(wg("wgrad_embed", dz_bf, D, c->at<bf16>(ly.patches), c->tl_lda_patch, M, D, p.Din, w.c_w_e, w.c_b_e));
+  cudaError_t e = cudaMemcpyAsync(grad_dev + w.c_e_s, grad_dev + w.c_b_e, (size_t)D * 4, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("grad e_s copy: ") + cudaGetErrorString(e));
   return ORBIT2_OK;
 }
 

@@ -1,0 +1,321 @@
+// train_simt.cu -- the HBM-bound kernels of the training step:
+// the Bayesian loss (readings R34 / R35), the stitch read backwards,
+// LayerNorm backward, the attention backward's row statistics and the weight
+// transposes the input-gradient GEMMs use.  The oracle is oracle/train.py.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "kernels.h"
+
+namespace orbit2 {
+
+namespace {
+
+__device__ __forceinline__ float huber(float r, float delta) {
+  const float a = fabsf(r);
+  return a <= delta ? r * r / (2.f * delta) : a - 0.5f * delta;
+}
+__device__ __forceinline__ float huber_grad(float r, float delta) {
+  return fabsf(r) <= delta ? r / delta : copysignf(1.f, r);
+}
+
+// One thread per output pixel (b, k, Y, X) of out [B][K][sH][sW]:
+//   loss_b += ( w_Y (y - x)^2 + lambda sum_{j in C(i)} b_ij h(x_i - x_j) ) / n
+//   dout    = ( -2 w_Y (y - x) + 2 lambda sum_j b_ij h'(x_i - x_j) ) / (n B)
+// (C(i) symmetric and h' odd: the pairs (i, j) and (j, i) contribute equally to x_i.)
+// Row weights w_Y (R35) are computed in double from the closed form; block partial
+// sums in double, one atomicAdd per block and sample.
+constexpr int LOSS_THREADS = 256;
+__global__ void __launch_bounds__(LOSS_THREADS) loss_kernel(const float* __restrict__ out,
+                                                            const float* __restrict__ truth, int B, int K, int sH,
+                                                            int sW, float lam, float delta, int geo,
+                                                            const float* __restrict__ latw, double* __restrict__ loss,
+                                                            float* __restrict__ dout) {
+  const int64_t plane = (int64_t)sH * sW;
+  const int64_t per_b = (int64_t)K * plane;
+  const int b = blockIdx.y;
+  const double n = (double)per_b;
+  double part = 0.0;
+  for (int64_t e = (int64_t)blockIdx.x * LOSS_THREADS + threadIdx.x; e < per_b;
+       e += (int64_t)gridDim.x * LOSS_THREADS) {
+    const int64_t pix = e % plane;
+    const int Y = (int)(pix / sW), X = (int)(pix - (int64_t)Y * sW);
+    const float* o = out + (int64_t)b * per_b + (e - pix);
+    const float x = __ldg(o + pix);
+    const float y = __ldg(truth + (int64_t)b * per_b + e);
+    const float w = geo ? __ldg(latw + Y) : 1.f;
+    float tv = 0.f, g = 0.f;
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy) {
+#pragma unroll
+      for (int dx = -1; dx <= 1; ++dx) {
+        if (dy == 0 && dx == 0) continue;
+        const int yy = Y + dy, xx = X + dx;
+        if (yy < 0 || yy >= sH || xx < 0 || xx >= sW) continue;
+        const float bij = (dy != 0 && dx != 0) ? 0.70710678118654752f : 1.f;
+        const float r = x - __ldg(o + (int64_t)yy * sW + xx);
+        tv += bij * huber(r, delta);
+        g += bij * huber_grad(r, delta);
+      }
+    }
+    const float dif = y - x;
+    part += (double)w * dif * dif + (double)lam * tv;
+    dout[(int64_t)b * per_b + e] = (float)((-2.0 * w * dif + 2.0 * lam * g) / (n * B));
+  }
+  __shared__ double red[LOSS_THREADS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < LOSS_THREADS / 32; ++i) s += red[i];
+    atomicAdd(loss + b, s / n);
+  }
+}
+
+__global__ void lat_weights_kernel(float* w, int sH) {
+  // w_r = cos(lat_r) / mean cos, lat_r = 90 - 180 (r + 1/2) / sH degrees (R35); one block
+  __shared__ double sum;
+  if (threadIdx.x == 0) sum = 0.0;
+  __syncthreads();
+  double loc = 0.0;
+  for (int r = threadIdx.x; r < sH; r += blockDim.x) loc += cos((90.0 - 180.0 * (r + 0.5) / sH) * (M_PI / 180.0));
+  atomicAdd(&sum, loc);
+  __syncthreads();
+  const double mean = sum / sH;
+  for (int r = threadIdx.x; r < sH; r += blockDim.x)
+    w[r] = (float)(cos((90.0 - 180.0 * (r + 0.5) / sH) * (M_PI / 180.0)) / mean);
+}
+
+// O6 read backwards: dG[b * chunk_core + t][(k P + al) P + be] = dout[b][k][P u + al][P w + be]
+// for the chunk's output tokens t = (tile, u, w) (dec_hidden == 0: output = core tokens).
+// One block per (token row, sample); threads over the K P^2 columns.
+__global__ void stitch_bwd_kernel(const float* __restrict__ dout, __nv_bfloat16* __restrict__ dg, int64_t ldg,
+                                  ChunkDev ch, int K, int P, int sH, int sW) {
+  const int64_t t = blockIdx.x;   // output token within the chunk (one sample)
+  const int b = blockIdx.y;
+  __shared__ int s_tile;
+  if (threadIdx.x == 0) {
+    int lo = 0;
+    for (int i = 1; i < ch.tc; ++i)
+      if (ch.tiles[ch.tb + i].core_off - ch.core0 <= t) lo = i;
+    s_tile = lo;
+  }
+  __syncthreads();
+  const DevTile tl = ch.tiles[ch.tb + s_tile];
+  const int64_t loc = t - (tl.core_off - ch.core0);
+  const int u = tl.out_y0 + (int)(loc / tl.out_w), w = tl.out_x0 + (int)(loc % tl.out_w);
+  const int Nh = K * P * P;
+  __nv_bfloat16* row = dg + ((int64_t)b * ch.chunk_core + t) * ldg;
+  for (int e = threadIdx.x; e < Nh; e += blockDim.x) {
+    const int k = e / (P * P), ab = e - k * P * P, al = ab / P, be = ab - al * P;
+    row[e] = __float2bfloat16_rn(
+        __ldg(dout + (((int64_t)b * K + k) * sH + (int64_t)P * u + al) * sW + (int64_t)P * w + be));
+  }
+  for (int e = Nh + threadIdx.x; e < ldg; e += blockDim.x) row[e] = __float2bfloat16_rn(0.f);
+}
+
+// LayerNorm backward, one warp per row (D % 32 == 0, D <= 1024 held in registers):
+//   xh = (z - mu) rstd;  dxh = dy g;  dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
+// out = dres + dz (fp32) and bf16 copy; dgamma += dy xh, dbeta += dy (block sums, atomics).
+// With a row map (LN_f over core rows): input row i reads z[zrow(i)] and writes dz there.
+template <int PER>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy, int64_t ldy,
+                                                     const float* __restrict__ z, const float* __restrict__ g,
+                                                     const float* __restrict__ dres, float* __restrict__ dz,
+                                                     __nv_bfloat16* __restrict__ dz_bf, int64_t M, int D,
+                                                     const int32_t* __restrict__ rowmap, int64_t map_per_b,
+                                                     int64_t chunk_tokens, int64_t tok0,
+                                                     float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float ag[PER], ab[PER];
+#pragma unroll
+  for (int i = 0; i < PER; ++i) ag[i] = ab[i] = 0.f;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += (int64_t)gridDim.x * 8) {
+    int64_t zr = row;
+    if (rowmap) {
+      const int64_t b = row / map_per_b, rr = row - b * map_per_b;
+      zr = b * chunk_tokens + (rowmap[rr] - tok0);
+    }
+    float zv[PER], dv[PER];
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int c = lane + 32 * i;
+      zv[i] = c < D ? z[zr * D + c] : 0.f;
+      dv[i] = c < D ? dy[row * ldy + c] : 0.f;
+      s += zv[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mu = s / D;
+    float vs = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const float t = lane + 32 * i < D ? zv[i] - mu : 0.f;
+      vs += t * t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) vs += __shfl_xor_sync(0xffffffffu, vs, o);
+    const float rstd = rsqrtf(vs / D + 1e-5f);
+    float m1 = 0.f, m2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int c = lane + 32 * i;
+      if (c < D) {
+        const float xh = (zv[i] - mu) * rstd;
+        const float dxh = dv[i] * __ldg(g + c);
+        m1 += dxh;
+        m2 += dxh * xh;
+        ag[i] += dv[i] * xh;
+        ab[i] += dv[i];
+        zv[i] = xh;
+        dv[i] = dxh;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      m1 += __shfl_xor_sync(0xffffffffu, m1, o);
+      m2 += __shfl_xor_sync(0xffffffffu, m2, o);
+    }
+    m1 /= D;
+    m2 /= D;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int c = lane + 32 * i;
+      if (c < D) {
+        float r = rstd * (dv[i] - m1 - zv[i] * m2);
+        if (dres) r += dres[zr * D + c];
+        dz[zr * D + c] = r;
+        dz_bf[zr * D + c] = __float2bfloat16_rn(r);
+      }
+    }
+  }
+  __shared__ float red[8][PER * 32];   // block column sums: dgamma, then dbeta
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) red[warp][lane + 32 * i] = pass ? ab[i] : ag[i];
+    __syncthreads();
+    for (int c = threadIdx.x; c < D; c += blockDim.x) {
+      float a = 0.f;
+      for (int w = 0; w < 8; ++w) a += red[w][c];
+      atomicAdd((pass ? dbeta : dgamma) + c, a);
+    }
+    __syncthreads();
+  }
+}
+
+// Delta[h][row] = sum_{d < dh} dO[row][h dh + d] O[row][h dh + d]  (fp32), one thread per (row, head)
+__global__ void delta_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
+                             float* __restrict__ delta, int64_t M, int D, int heads, int64_t ld_stat) {
+  const int dh = D / heads;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M * heads;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = e / heads;
+    const int h = (int)(e - row * heads);
+    const uint4* a = reinterpret_cast<const uint4*>(dO + row * D + h * dh);
+    const uint4* o = reinterpret_cast<const uint4*>(O + row * D + h * dh);
+    float s = 0.f;
+    for (int c = 0; c < dh / 8; ++c) {
+      const uint4 x = __ldg(a + c), y = __ldg(o + c);
+      const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
+      const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 xf = __bfloat1622float2(xp[u]), yf = __bfloat1622float2(yp[u]);
+        s += xf.x * yf.x + xf.y * yf.y;
+      }
+    }
+    delta[(int64_t)h * ld_stat + row] = s;
+  }
+}
+
+// dqkv[row][0:D] = bf16(dq_acc[row][0:D])   (the Q columns; K / V written by the backward kernel)
+__global__ void dq_convert_kernel(const float* __restrict__ dq, __nv_bfloat16* __restrict__ dqkv, int64_t M, int D) {
+  const int64_t n4 = M * D / 4;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = (e * 4) / D, c = e * 4 - row * D;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(dq) + e);
+    __nv_bfloat162* d = reinterpret_cast<__nv_bfloat162*>(dqkv + row * 3 * D + c);
+    d[0] = __floats2bfloat162_rn(v.x, v.y);
+    d[1] = __floats2bfloat162_rn(v.z, v.w);
+  }
+}
+
+// W [n][k] fp32 (canonical, row-major) -> W^T [k][ld] bf16 (32 x 32 tiles through smem)
+__global__ void transpose_bf16_kernel(const float* __restrict__ W, int n, int k, __nv_bfloat16* __restrict__ Wt,
+                                      int64_t ld) {
+  __shared__ float t[32][33];
+  const int n0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int nn = n0 + i, kk = k0 + threadIdx.x;
+    t[i][threadIdx.x] = (nn < n && kk < k) ? W[(int64_t)nn * k + kk] : 0.f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int kk = k0 + i, nn = n0 + threadIdx.x;
+    if (kk < k && nn < ld) Wt[(int64_t)kk * ld + nn] = __float2bfloat16_rn(nn < n ? t[threadIdx.x][i] : 0.f);
+  }
+}
+
+}  // namespace
+
+void launch_lat_weights(float* w, int sH, cudaStream_t st) { lat_weights_kernel<<<1, 256, 0, st>>>(w, sH); }
+
+void launch_loss(const float* out, const float* truth, int B, int K, int sH, int sW, float lam, float delta, int geo,
+                 const float* latw, double* loss, float* dout, cudaStream_t st) {
+  const int64_t per_b = (int64_t)K * sH * sW;
+  const int64_t blocks = std::min<int64_t>((per_b + LOSS_THREADS - 1) / LOSS_THREADS,
+                                           std::max<int64_t>(1, 4LL * num_sms() / std::max(1, B)) * 4);
+  loss_kernel<<<dim3((unsigned)blocks, (unsigned)B), LOSS_THREADS, 0, st>>>(out, truth, B, K, sH, sW, lam, delta, geo,
+                                                                           latw, loss, dout);
+}
+
+void launch_stitch_bwd(const float* dout, __nv_bfloat16* dg, int64_t ldg, const ChunkDev& ch, int B, int K, int P,
+                       int sH, int sW, cudaStream_t st) {
+  if (ch.chunk_core <= 0) return;
+  stitch_bwd_kernel<<<dim3((unsigned)ch.chunk_core, (unsigned)B), 192, 0, st>>>(dout, dg, ldg, ch, K, P, sH, sW);
+}
+
+bool launch_ln_bwd(const float* dy, int64_t ldy, const float* z, const float* g, const float* dres, float* dz,
+                   __nv_bfloat16* dz_bf, int64_t M, int D, const int32_t* rowmap, int64_t map_per_b,
+                   int64_t chunk_tokens, int64_t tok0, float* dgamma, float* dbeta, cudaStream_t st) {
+  if (M <= 0) return true;
+  const int blocks = (int)std::min<int64_t>((M + 7) / 8, 4LL * num_sms());
+#define LNB(P_)                                                                                                \
+  ln_bwd_kernel<P_><<<blocks, 256, 0, st>>>(dy, ldy, z, g, dres, dz, dz_bf, M, D, rowmap, map_per_b, chunk_tokens, \
+                                            tok0, dgamma, dbeta);                                              \
+  return true
+  if (D <= 256) { LNB(8); }
+  if (D <= 512) { LNB(16); }
+  if (D <= 1024) { LNB(32); }
+#undef LNB
+  return false;
+}
+
+void launch_delta(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* delta, int64_t M, int D, int heads,
+                  int64_t ld_stat, cudaStream_t st) {
+  const int64_t n = M * heads;
+  if (n <= 0) return;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 16LL * num_sms());
+  delta_kernel<<<blocks, 256, 0, st>>>(dO, O, delta, M, D, heads, ld_stat);
+}
+
+void launch_dq_convert(const float* dq, __nv_bfloat16* dqkv, int64_t M, int D, cudaStream_t st) {
+  const int64_t n4 = M * D / 4;
+  if (n4 <= 0) return;
+  const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, 16LL * num_sms());
+  dq_convert_kernel<<<blocks, 256, 0, st>>>(dq, dqkv, M, D);
+}
+
+void launch_transpose_bf16(const float* W, int n, int k, __nv_bfloat16* Wt, int64_t ld, cudaStream_t st) {
+  dim3 grid((unsigned)((k + 31) / 32), (unsigned)((ld + 31) / 32));
+  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, st>>>(W, n, k, Wt, ld);
+}
+
+}  // namespace orbit2

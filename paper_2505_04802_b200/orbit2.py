@@ -46,6 +46,12 @@ class orbit2_plan_info(C.Structure):
                 "stitch_bytes_per_sample")]
 
 
+class orbit2_train_info(C.Structure):
+    _fields_ = [("workspace_bytes", C.c_int64), ("canonical_weight_count", C.c_int64),
+                ("fwd_flops_per_sample", C.c_double), ("flops_per_sample", C.c_double),
+                ("attn_bwd_flops_per_sample", C.c_double)]
+
+
 class orbit2_rect(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("y0", "y1", "x0", "x1")]
 
@@ -79,6 +85,12 @@ def _load():
         "orbit2_halo_exchange": (i32, [vp, vp]),
         "orbit2_comm_barrier": (i32, [vp, vp]),
         "orbit2_comm_status": (i32, [vp]),
+        "orbit2_train_plan": (i32, [vp, C.POINTER(orbit2_train_info)]),
+        "orbit2_train_bind": (i32, [vp, vp, C.c_size_t, vp]),
+        "orbit2_train_prepare": (i32, [vp, vp, vp]),
+        "orbit2_train_forward": (i32, [vp, vp, vp, vp, vp]),
+        "orbit2_loss": (i32, [vp, vp, vp, C.c_float, C.c_float, i32, vp, vp, vp]),
+        "orbit2_train_backward": (i32, [vp, vp, vp, vp, vp]),
         "orbit2_launch_count": (i64, [vp]),
         "orbit2_set_profiling": (i32, [vp, i32]),
         "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
@@ -97,6 +109,8 @@ EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orb
             "orbit2_stitch", "orbit2_xfer_plan", "orbit2_xfer_pack", "orbit2_xfer_unpack", "orbit2_stitch_peer",
             "orbit2_ipc_export", "orbit2_comm_init", "orbit2_comm_target", "orbit2_halo_exchange",
             "orbit2_comm_barrier", "orbit2_comm_status",
+            "orbit2_train_plan", "orbit2_train_bind", "orbit2_train_prepare", "orbit2_train_forward",
+            "orbit2_loss", "orbit2_train_backward",
             "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
             "orbit2_destroy")
 
@@ -439,6 +453,81 @@ class Context:
             if e is not None:
                 comp.wait_event(e)
         return out_host
+
+    # -- training step (include/orbit2.h "Training step") ----
+    def train_info(self) -> orbit2_train_info:
+        ti = orbit2_train_info()
+        _check(lib.orbit2_train_plan(self.handle, C.byref(ti)), "orbit2_train_plan")
+        return ti
+
+    def train_bind(self, stream=None):
+        """Allocate and bind the training workspace (activations kept for the backward)."""
+        import torch
+        ti = self.train_info()
+        self.train_workspace = torch.empty(max(ti.workspace_bytes, 16), dtype=torch.uint8, device=self.device)
+        with _on_device(self.device):
+            _check(lib.orbit2_train_bind(self.handle, _ptr(self.train_workspace), ti.workspace_bytes,
+                                         _stream(stream)), "orbit2_train_bind")
+        self.tinfo = ti
+        return ti
+
+    def train_prepare(self, canonical_dev, stream=None):
+        import torch
+        _req(canonical_dev, torch.float32, "canonical_dev")
+        with _on_device(self.device):
+            _check(lib.orbit2_train_prepare(self.handle, _ptr(canonical_dev), _stream(stream)),
+                   "orbit2_train_prepare")
+
+    def train_forward(self, packed, x_dev, tile_out, stream=None):
+        import torch
+        _req(x_dev, torch.float32, "x_dev")
+        _req(tile_out, torch.bfloat16, "tile_out")
+        with _on_device(self.device):
+            _check(lib.orbit2_train_forward(self.handle, _ptr(packed), _ptr(x_dev), _ptr(tile_out), _stream(stream)),
+                   "orbit2_train_forward")
+
+    def loss(self, out, truth, lam, delta, geo, loss_dev, dout, stream=None):
+        import torch
+        _req(out, torch.float32, "out")
+        _req(truth, torch.float32, "truth")
+        _req(loss_dev, torch.float64, "loss_dev")
+        _req(dout, torch.float32, "dout")
+        with _on_device(self.device):
+            _check(lib.orbit2_loss(self.handle, _ptr(out), _ptr(truth), float(lam), float(delta), 1 if geo else 0,
+                                   _ptr(loss_dev), _ptr(dout), _stream(stream)), "orbit2_loss")
+
+    def train_backward(self, packed, dout, grad, stream=None):
+        import torch
+        _req(dout, torch.float32, "dout")
+        _req(grad, torch.float32, "grad")
+        with _on_device(self.device):
+            _check(lib.orbit2_train_backward(self.handle, _ptr(packed), _ptr(dout), _ptr(grad), _stream(stream)),
+                   "orbit2_train_backward")
+
+    def train_step(self, packed, x_dev, truth, lam=1e-3, delta=1e-3, geo=True, bufs=None, stream=None):
+        """One training step's forward, loss and backward over every rank-local tile:
+        returns (loss per sample [B] float64, grad [canonical count] fp32, out).  The
+        once-per-batch gradient all-reduce and the weight update are the caller's."""
+        import torch
+        cfg = self.cfg
+        if bufs is None:
+            bufs = self.train_buffers()
+        tile_out, out, dout, loss_dev, grad = bufs
+        self.train_forward(packed, x_dev, tile_out, stream)
+        self.orbit2_stitch(tile_out, x_dev, 0, self.info.n_local_tiles, out, stream)
+        self.loss(out, truth, lam, delta, geo, loss_dev, dout, stream)
+        self.train_backward(packed, dout, grad, stream)
+        return loss_dev, grad, out
+
+    def train_buffers(self):
+        import torch
+        cfg = self.cfg
+        tile_out = self.rank_tile_out()
+        out = torch.empty((cfg.batch, cfg.K, self.sH, self.sW), dtype=torch.float32, device=self.device)
+        dout = torch.empty_like(out)
+        loss_dev = torch.empty(cfg.batch, dtype=torch.float64, device=self.device)
+        grad = torch.empty(self.info.canonical_weight_count, dtype=torch.float32, device=self.device)
+        return tile_out, out, dout, loss_dev, grad
 
     # -- instrumentation ------------------------------------------------------
     def launch_count(self) -> int:
