@@ -42,10 +42,13 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
     ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="sp", choices=["dp", "sp"],
+    ap.add_argument("--mode", default="sp", choices=["dp", "sp", "train"],
                     help="N > 1 only.  sp (default): the tiles of one batch spread over the ranks, halo "
                          "exchange + output gather through NVLink peer memory (strong scaling); dp: every "
-                         "rank its own batch (weak scaling)")
+                         "rank its own batch (weak scaling).  train (any N): the training step (SURVEY "
+                         "§8(f) row 3): forward, Bayesian loss, backward, one gradient all-reduce per batch")
+    ap.add_argument("--lam", type=float, default=1e-3, help="train: TV prior weight lambda (R34)")
+    ap.add_argument("--delta", type=float, default=1e-3, help="train: Huber width delta (R34)")
     ap.add_argument("--sp-groups", type=int, default=0,
                     help="N > 1: sample groups per rank (default 4 when the batch allows, else 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -643,6 +646,147 @@ def run_sp(args, w, world, rank, local):
         print(json.dumps(res), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# the training step
+# ---------------------------------------------------------------------------
+def class_work_train(w, info, B):
+    """Algorithmic FLOPs per step of every kernel class of the training step (all
+    queries of every block; backward = input and weight gradients, attention 2.5x)."""
+    D, L, Din, Nh = w.embed, w.depth, w.din, w.head_out
+    n, nc, n2 = info.tokens_per_sample, info.core_tokens_per_sample, info.sum_n2_per_sample
+    f = {"embed_gemm": 2.0 * n * Din * D, "head_gemm": 2.0 * nc * D * Nh,
+         "qkv_gemm": L * 6.0 * n * D * D, "oproj_gemm": L * 2.0 * n * D * D,
+         "mlp_up_gemm": L * 8.0 * n * D * D, "mlp_down_gemm": L * 8.0 * n * D * D,
+         "tile_attention": L * 4.0 * D * n2, "attn_bwd": L * 10.0 * D * n2,
+         "wgrad_w2": L * 8.0 * n * D * D, "dx_mlp_down": L * 8.0 * n * D * D,
+         "wgrad_w1": L * 8.0 * n * D * D, "dx_mlp_up": L * 8.0 * n * D * D,
+         "wgrad_wo": L * 2.0 * n * D * D, "dx_oproj": L * 2.0 * n * D * D,
+         "wgrad_wqkv": L * 6.0 * n * D * D, "dx_qkv": L * 6.0 * n * D * D,
+         "wgrad_head": 2.0 * nc * D * Nh, "dx_head": 2.0 * nc * D * Nh, "wgrad_embed": 2.0 * n * Din * D}
+    return {k: v * B for k, v in f.items()}
+
+
+def run_train(args, w, world, rank, local):
+    """Data-parallel training step: every rank its own batch of B samples over all tiles
+    (forward keeping activations, stitch, Bayesian loss, backward), then ONE NCCL
+    all-reduce (average) of the gradient per batch (reading R36)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2505_04802_b200 import orbit2 as o2
+    from workloads import make_input, make_weights
+    B = w.batch
+    free, _ = torch.cuda.mem_get_info()
+    while True:   # the largest batch (<= the config's) whose training workspace fits 85% of HBM
+        cfg = o2.config_from(w, batch=B, precision=o2.BF16)
+        ctx = o2.Context(cfg)
+        ti = ctx.train_info()
+        need = ti.workspace_bytes + 4 * cfg.batch * w.K * w.scale * w.H * w.scale * w.W * 4 + ctx.info.tile_out_bytes
+        if need < 0.85 * torch.cuda.mem_get_info()[0] or B == 1:
+            break
+        del ctx
+        torch.cuda.empty_cache()
+        B //= 2
+    ctx.train_bind()
+    info = ctx.info
+    blob = torch.from_numpy(make_weights(w)).cuda()
+    packed = ctx.prepare_weights(blob)
+    ctx.train_prepare(blob)
+    x_host = make_input(w, batch=B, seed=2000 + 97 * rank)
+    rng = np.random.default_rng(3000 + rank)
+    y_host = rng.standard_normal((B, w.K, w.scale * w.H, w.scale * w.W)).astype(np.float32)
+    x_pin, y_pin = torch.from_numpy(x_host).pin_memory(), torch.from_numpy(y_host).pin_memory()
+    x_dev, y_dev = x_pin.cuda(), y_pin.cuda()
+    bufs = ctx.train_buffers()
+    grad = bufs[4]
+    loss_pin = torch.empty(B, dtype=torch.float64).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def step():
+        loss, g, _ = ctx.train_step(packed, x_dev, y_dev, args.lam, args.delta, True, bufs, stream)
+        if world > 1:
+            dist.all_reduce(g, op=dist.ReduceOp.AVG)   # once per batch (P:532)
+        return loss
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier(world)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    with ClockSampler(local) as clk:
+        barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        barrier(world)
+    ms = max_over_ranks(world, ev0.elapsed_time(ev1) / args.steps)
+    launches = (ctx.launch_count() - l0) // args.steps
+    clocks = clk.summary()
+
+    def e2e_step():   # pinned host input and truth in, per-sample loss out
+        x_dev.copy_(x_pin, non_blocking=True)
+        y_dev.copy_(y_pin, non_blocking=True)
+        loss = step()
+        loss_pin.copy_(loss, non_blocking=True)
+
+    e2e_step()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_steps = max(2, args.steps // 2)
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier(world)
+    e2e_ms = max_over_ranks(world, e0.elapsed_time(e1) / e_steps)
+
+    prof = {}
+    if not args.no_profile:
+        ctx.set_profiling(True)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        prof = {k: (n / 3, t / 3) for k, (n, t) in ctx.kernel_times().items()}
+        ctx.set_profiling(False)
+    px = world * B * w.scale * w.H * w.scale * w.W
+    flops = world * B * ti.flops_per_sample
+    pk = peaks()
+    res = {
+        "metric": "training high-res px/s (forward + Bayesian loss + backward + gradient all-reduce)",
+        "value": px / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields and truth, random-init weights)",
+        "config": {"workload": w.name, "batch_per_gpu": B, "mode": "train", "lambda": args.lam, "delta": args.delta,
+                   "parallelism": f"dp{world} (one gradient all-reduce per batch)",
+                   "l2": "working set > L2 (126 MB) every step; no flush needed"},
+        "train_tflops": flops / (ms * 1e-3) / 1e12,
+        "train_frac_bf16_peak": flops / (ms * 1e-3) / 1e12 / pk["bf16"],
+        "gpu_launches": int(launches),
+        "clocks": clocks,
+        "e2e": {"value": px / (e2e_ms * 1e-3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": (x_pin.numel() + y_pin.numel()) * 4, "d2h_bytes_per_step": B * 8,
+                "api": "Context.train_step with input and truth copied from pinned host, per-sample loss to host"},
+    }
+    if prof:
+        work = class_work_train(w, info, B)
+        total = sum(t for _, t in prof.values())
+        classes = {}
+        for k, (n, t) in prof.items():
+            e = {"share": t / total, "ms_per_step": t, "launches_per_step": n}
+            if k in work:
+                e["tflops"] = work[k] / (t * 1e-3) / 1e12
+                e["frac_of_burst"] = e["tflops"] / pk["bf16"]
+            classes[k] = e
+        res["kernels"] = classes
+        dom = max((k for k in classes if k in work), key=lambda k: classes[k]["share"])
+        ach = classes[dom]["tflops"]
+        res["roofline"] = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["bf16"], "unit": "TFLOP/s",
+                           "frac": ach / pk["bf16"], "traffic": None, "peak_src": f"{pk['src']} bf16_tflops (burst)"}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+
+
 def relaunch_if_needed(args):
     """`python bench.py --gpus N` without torchrun: re-exec under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
@@ -674,7 +818,9 @@ def main():
     relaunch_if_needed(args)
     world, rank, local = dist_init(args.gpus)
     try:
-        if world > 1 and args.mode == "sp":
+        if args.mode == "train":
+            run_train(args, w, world, rank, local)
+        elif world > 1 and args.mode == "sp":
             run_sp(args, w, world, rank, local)
         else:
             run_ours(args, w, world, rank, local)
