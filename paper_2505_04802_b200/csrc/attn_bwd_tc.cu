@@ -22,7 +22,7 @@
 //   warps 4..7    : thread = key row r (TMEM lane r): P^T, dS^T for block j,
 //                   P^T -> TMEM [256,320) (bf16 pairs), dS^T -> smem (SW128);
 //                   at the item's end dK c, dV -> dqkv (bf16)
-//   warps 8..11   : thread = query row of block j: dQ_j c -> fp32 atomics into dq_acc
+//   warps 8..11   : thread = query row of block j: dQ_j c -> smem -> TMA reduce-add into dq_acc (fp32)
 // The same TMA tile [128 rows][64 bf16] (one SW128 atom) is a K-major operand when
 // the contraction runs over head dim and an MN-major one when it runs over tokens.
 #include <cuda.h>
@@ -39,8 +39,17 @@ namespace orbit2 {
 
 bool make_tmap_bf16(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
                     int box_cols, CUtensorMapSwizzle swz);
+bool make_tmap_f32(CUtensorMap* map, const void* ptr, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                   int box_cols, CUtensorMapSwizzle swz);
 
 namespace {
+
+#ifndef ORBIT2_BWD_NODQ
+#define ORBIT2_BWD_NODQ 0   // experiment: skip the dQ atomics (wrong dQ; timing only)
+#endif
+#ifndef ORBIT2_BWD_NOSM
+#define ORBIT2_BWD_NOSM 0   // experiment: skip the exponentials (wrong P; timing only)
+#endif
 
 constexpr int DH = 64;
 constexpr int TILE = 128 * DH * 2;          // 16 KB: one SW128 atom of 128 rows
@@ -49,7 +58,8 @@ constexpr int KVST = 2;                     // K / V ring (next item prefetched)
 constexpr int IRING = 4;
 constexpr int THREADS = 384;
 constexpr uint32_t C_S = 0, C_DP = 128, C_P = 256, C_DV = 320, C_DK = 384, C_DQ = 448;
-constexpr int SMEM = KVST * 2 * TILE + QST * 2 * TILE + 2 * TILE + 2 * 2 * 128 * 4 + 1024 + 512;
+constexpr int DQ_STG = 4 * 2 * 32 * 32 * 4;   // dQ staging: 4 warps x 2 boxes [32 rows][32 fp32] (SW128)
+constexpr int SMEM = KVST * 2 * TILE + QST * 2 * TILE + 2 * TILE + DQ_STG + 2 * 2 * 128 * 4 + 1024 + 512;
 
 struct __align__(16) BItem {
   int64_t base;     // first row of the tile's tokens
@@ -86,13 +96,9 @@ __device__ __forceinline__ BItem take(const BItem* sItem, uint64_t* full, uint64
   return it;
 }
 
-__device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
-
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap tqkv, const __grid_constant__ CUtensorMap tdo,
+                    const __grid_constant__ CUtensorMap tdq,
                     const float* __restrict__ lse, const float* __restrict__ delta, int64_t ld_stat,
                     float* __restrict__ dq_acc, __nv_bfloat16* __restrict__ dqkv, ChunkDev ch, int D, int heads,
                     int n_items) {
@@ -103,7 +109,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* sQ = sV + KVST * TILE;                   // [QST][TILE]
   uint8_t* sDO = sQ + QST * TILE;                   // [QST][TILE]
   uint8_t* sDS = sDO + QST * TILE;                  // dS^T [128 keys][128 q] as 2 atoms
-  float* sL = reinterpret_cast<float*>(sDS + 2 * TILE);   // [2][128] lse2 of the block's queries
+  uint8_t* sDQ = sDS + 2 * TILE;                    // [4 warps][2 boxes][32 rows][128 B]
+  float* sL = reinterpret_cast<float*>(sDQ + DQ_STG);   // [2][128] lse2 of the block's queries
   float* sDl = sL + 2 * 128;                        // [2][128] Delta
   BItem* sItem = reinterpret_cast<BItem*>(sDl + 2 * 128);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sItem + IRING);
@@ -125,6 +132,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&tqkv);
     tc::prefetch_tmap(&tdo);
+    tc::prefetch_tmap(&tdq);
     for (int s = 0; s < KVST; ++s) {
       tc::mbar_init(&kv_full[s], 1);
       tc::mbar_init(&kv_empty[s], 1);
@@ -281,8 +289,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int e = 0; e < 32; e += 2) {
             float p0 = 0.f, p1 = 0.f;
-            if (kval && c0 + e < qv) p0 = ex2f(__uint_as_float(sr[e]) * sl - L[c0 + e]);
-            if (kval && c0 + e + 1 < qv) p1 = ex2f(__uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1]);
+            if (ORBIT2_BWD_NOSM) {
+              p0 = __uint_as_float(sr[e]) * sl - L[c0 + e];
+              p1 = __uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1];
+            } else {
+              if (kval && c0 + e < qv) p0 = ex2f(__uint_as_float(sr[e]) * sl - L[c0 + e]);
+              if (kval && c0 + e + 1 < qv) p1 = ex2f(__uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1]);
+            }
             const float d0 = p0 * (__uint_as_float(dr[e]) - Dl[c0 + e]);
             const float d1 = p1 * (__uint_as_float(dr[e + 1]) - Dl[c0 + e + 1]);
             pk[e / 2] = tc::pack_bf16(p0, p1);
@@ -329,34 +342,45 @@ __global__ void __launch_bounds__(THREADS, 1)
       tc::mbar_arrive(dkv_free);
     }
   } else if (warp >= 8) {
-    // ---------------- dQ_j c -> fp32 atomics (thread = query row of the block) ----------------
+    // ---------------- dQ_j c -> dq_acc: staged in smem, one TMA reduce-add per 32 x 32 box ----------------
+    // (rows of queries past the tile end hold exact zeros: their dS columns are 0)
     const int q4 = warp & 3;
     const int i = q4 * 32 + lane;
     const uint32_t lb = tmem + ((uint32_t)(q4 * 32) << 16);
+    uint8_t* stg = sDQ + q4 * 2 * 4096;
     uint32_t li = 0, gq = 0;
     for (int id = blockIdx.x; id < n_items; id += gridDim.x, ++li) {
       const BItem it = take(sItem, it_full, it_empty, li);
       for (int j = 0; j < it.nq; ++j, ++gq) {
         tc::mbar_wait(dq_full, gq & 1);
         tc::tc_fence_after();
-        const bool valid = j * 128 + i < it.n;
-        float* dst = dq_acc + (it.base + j * 128 + i) * (int64_t)D + it.h * DH;
+        if (lane == 0) tc::bulk_wait_read<0>();       // the previous block's reduce has read the staging
+        __syncwarp();
 #pragma unroll
-        for (int c0 = 0; c0 < DH; c0 += 32) {
+        for (int half = 0; half < 2; ++half) {
           uint32_t v[32];
-          tc::tmem_ld32(lb + C_DQ + c0, v);
+          tc::tmem_ld32(lb + C_DQ + half * 32, v);
           tc::tmem_ld_wait();
-          if (valid) {
+          uint8_t* row = stg + half * 4096 + lane * 128;
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-              red_add_v4(dst + c0 + 4 * u, __uint_as_float(v[4 * u]) * cs, __uint_as_float(v[4 * u + 1]) * cs,
-                         __uint_as_float(v[4 * u + 2]) * cs, __uint_as_float(v[4 * u + 3]) * cs);
-          }
+          for (int u = 0; u < 8; ++u)
+            *reinterpret_cast<float4*>(row + ((u ^ (lane & 7)) << 4)) =
+                make_float4(__uint_as_float(v[4 * u]) * cs, __uint_as_float(v[4 * u + 1]) * cs,
+                            __uint_as_float(v[4 * u + 2]) * cs, __uint_as_float(v[4 * u + 3]) * cs);
         }
         tc::tc_fence_before();
         tc::mbar_arrive(dq_free);
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        const int row0 = j * 128 + q4 * 32;          // first query of this warp's slice
+        if (lane == 0 && row0 < it.n && !ORBIT2_BWD_NODQ) {
+          tc::tma_reduce_add_2d(&tdq, stg, it.h * DH, (int32_t)(it.base + row0));
+          tc::tma_reduce_add_2d(&tdq, stg + 4096, it.h * DH + 32, (int32_t)(it.base + row0));
+          tc::bulk_commit();
+        }
       }
     }
+    if (lane == 0) tc::bulk_wait_all();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -372,16 +396,17 @@ bool launch_attention_bwd_tc(const void* qkv, const void* dout, int64_t rows, co
                              int64_t ld_stat, float* dq_acc, void* dqkv, const ChunkDev& ch, int B, int D, int heads,
                              int d, cudaStream_t st) {
   if (d != DH) return false;
-  CUtensorMap tq, tdo;
+  CUtensorMap tq, tdo, tdq;
   if (!make_tmap_bf16(&tq, qkv, rows, 3LL * D, 3LL * D, 128, DH, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   if (!make_tmap_bf16(&tdo, dout, rows, D, D, 128, DH, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
+  if (!make_tmap_f32(&tdq, dq_acc, rows, D, D, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
   static std::atomic<uint64_t> attr_done{0};
   if (!smem_attr_once(reinterpret_cast<const void*>(attn_bwd_kernel), SMEM, &attr_done)) return false;
   const int64_t n_items = (int64_t)ch.nqb * heads * B;
   if (n_items == 0) return true;
   if (n_items >= (int64_t)INT32_MAX) return false;
   const unsigned grid = (unsigned)std::min<int64_t>(n_items, num_sms());
-  attn_bwd_kernel<<<grid, THREADS, SMEM, st>>>(tq, tdo, lse, delta, ld_stat, dq_acc,
+  attn_bwd_kernel<<<grid, THREADS, SMEM, st>>>(tq, tdo, tdq, lse, delta, ld_stat, dq_acc,
                                                reinterpret_cast<__nv_bfloat16*>(dqkv), ch, D, heads, (int)n_items);
   return true;
 }

@@ -151,21 +151,22 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
       if (n0 + j < ep.N) v[j] += __ldg(ep.bias + n0 + j);
   }
   if constexpr (EPI == EPI_GELU) {
-    if (ep.aux) {   // training: keep the pre-activation
+    if (ep.aux) {   // training: keep GELU'(pre-activation) for the backward
       __nv_bfloat16* h = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(ep.aux)) + row * ep.ldc + n0;
       for (int j = 0; j < 32; ++j)
-        if (n0 + j < ep.N) h[j] = __float2bfloat16_rn(v[j]);
+        if (n0 + j < ep.N) {
+          const float x = v[j];
+          h[j] = __float2bfloat16_rn(0.5f * (1.0f + erff(x * 0.70710678118654752f)) +
+                                     x * 0.39894228040143268f * __expf(-0.5f * x * x));
+        }
     }
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = 0.5f * v[j] * (1.0f + erff(v[j] * 0.70710678118654752f));
   }
-  if constexpr (EPI == EPI_DGELU) {   // v = acc (no bias): dh = dgelu * GELU'(h)
+  if constexpr (EPI == EPI_DGELU) {   // v = acc (no bias): dh = dgelu * GELU'(h) (aux = GELU'(h))
     const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(ep.aux) + row * ep.ldc + n0;
 #pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float x = n0 + j < ep.N ? __bfloat162float(h[j]) : 0.f;
-      v[j] = v[j] * (0.5f * (1.0f + erff(x * 0.70710678118654752f)) + x * 0.39894228040143268f * __expf(-0.5f * x * x));
-    }
+    for (int j = 0; j < 32; ++j) v[j] *= n0 + j < ep.N ? __bfloat162float(h[j]) : 0.f;
   }
   if constexpr (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) {
     if constexpr (OUT_BF16) {
@@ -252,7 +253,8 @@ __global__ void __launch_bounds__(384, 1)
   constexpr int B_RING = WS ? (WS_K / BK) : STAGES;   // B atoms resident (WS) or ring slots
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
-  constexpr int STG_BYTES = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
+  // GELU: a second staging set for the training forward's GELU' store (aux)
+  constexpr int STG_BYTES = LN ? 2 * 2 * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the __shared__ array (keeps the shared address space: STS, not generic ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wfull + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
+  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) && OUT_BF16 && !TRANS;
   const int nk = K / BK;
   const int64_t num_n = (Ncols + BN - 1) / BN;
   const int64_t num_m = (M + BM - 1) / BM;
@@ -283,7 +285,7 @@ __global__ void __launch_bounds__(384, 1)
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
     if (TMA_OUT || LN) tc::prefetch_tmap(&tmC);
-    if (LN) tc::prefetch_tmap(&tmD);
+    if (EPI == EPI_GELU || LN) tc::prefetch_tmap(&tmD);
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
@@ -534,7 +536,32 @@ __global__ void __launch_bounds__(384, 1)
         } else if constexpr (TMA_OUT) {
           if (n0 + c0 < ep.N) {
             float v[32];
-            if (n0 + c0 + 32 <= ep.N) {
+            if constexpr (EPI == EPI_DGELU) {   // dh = acc * GELU'(h): aux row chunk (64 B)
+              float gd[32];
+              if (row < M && n0 + c0 + 32 <= ep.N) {
+                const uint4* a4 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
+                                                                 row * ep.ldc + n0 + c0);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const uint4 w = __ldg(a4 + u);
+                  const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(hp[e]);
+                    gd[8 * u + 2 * e] = f.x;
+                    gd[8 * u + 2 * e + 1] = f.y;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  gd[j] = (row < M && n0 + c0 + j < ep.N)
+                              ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(ep.aux)[row * ep.ldc + n0 + c0 + j])
+                              : 0.f;
+              }
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]) * gd[j];
+            } else if (n0 + c0 + 32 <= ep.N) {
               const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c0);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
@@ -549,20 +576,16 @@ __global__ void __launch_bounds__(384, 1)
               for (int j = 0; j < 32; ++j)
                 v[j] = __uint_as_float(r[j]) + (n0 + c0 + j < ep.N ? __ldg(ep.bias + n0 + c0 + j) : 0.f);
             }
+            const bool keep_grad = EPI == EPI_GELU && ep.aux != nullptr;   // training forward
+            float gd[EPI == EPI_GELU ? 32 : 1];
             if constexpr (EPI == EPI_GELU) {
-              if (ep.aux != nullptr && row < M) {   // training: keep the pre-activation (64 B per row)
-                uint4* h = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(ep.aux)) +
-                                                    row * ep.ldc + n0 + c0);
-                if (n0 + c0 + 32 <= ep.N) {
+              if (keep_grad) {
 #pragma unroll
-                  for (int u = 0; u < 4; ++u)
-                    h[u] = make_uint4(tc::pack_bf16(v[8 * u], v[8 * u + 1]), tc::pack_bf16(v[8 * u + 2], v[8 * u + 3]),
-                                      tc::pack_bf16(v[8 * u + 4], v[8 * u + 5]),
-                                      tc::pack_bf16(v[8 * u + 6], v[8 * u + 7]));
-                }
+                for (int j = 0; j < 32; ++j) tc::gelu_and_grad_fast(v[j], v[j], gd[j]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
               }
-#pragma unroll
-              for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
             }
             uint8_t* sb = my_stg + (nst & 1) * 2048;
             if (lane == 0) tc::bulk_wait_read<1>();   // this buffer's previous store has read it
@@ -574,10 +597,22 @@ __global__ void __launch_bounds__(384, 1)
               *reinterpret_cast<uint4*>(srow + ((u ^ sw) << 4)) =
                   make_uint4(tc::pack_bf16(v[8 * u], v[8 * u + 1]), tc::pack_bf16(v[8 * u + 2], v[8 * u + 3]),
                              tc::pack_bf16(v[8 * u + 4], v[8 * u + 5]), tc::pack_bf16(v[8 * u + 6], v[8 * u + 7]));
+            if constexpr (EPI == EPI_GELU) {
+              if (keep_grad) {   // GELU'(pre-activation) -> aux through the second staging set
+                uint8_t* grow = sb + 8 * 2 * 2048 + lane * 64;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                  *reinterpret_cast<uint4*>(grow + ((u ^ sw) << 4)) =
+                      make_uint4(tc::pack_bf16(gd[8 * u], gd[8 * u + 1]), tc::pack_bf16(gd[8 * u + 2], gd[8 * u + 3]),
+                                 tc::pack_bf16(gd[8 * u + 4], gd[8 * u + 5]),
+                                 tc::pack_bf16(gd[8 * u + 6], gd[8 * u + 7]));
+              }
+            }
             tc::fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
               tc::tma_store_2d(&tmC, sb, (int32_t)(n0 + c0), (int32_t)(m0 + q * 32));
+              if (keep_grad) tc::tma_store_2d(&tmD, sb + 8 * 2 * 2048, (int32_t)(n0 + c0), (int32_t)(m0 + q * 32));
               tc::bulk_commit();
             }
             ++nst;
@@ -612,18 +647,21 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
     return false;
   if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, kb.cols ? kb.cols : K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
-  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU) && OUT_BF16 && !TRANS;
+  constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) && OUT_BF16 && !TRANS;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
   tcm = ta;   // unused unless set below
   tdm = ta;
   if (TMA_OUT) {
     if (!make_tmap_bf16(&tcm, ep.C, M, N, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
+    if (EPI == EPI_GELU && ep.aux != nullptr &&   // training forward: GELU' store
+        !make_tmap_bf16(&tdm, ep.aux, M, N, ep.ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+      return false;
   }
   if (LN) {   // z fp32 [M][N] in 128 x 32 boxes (SW128), xn bf16 [M][N] in 128 x 32 boxes (SW64)
     if (!make_tmap_f32(&tcm, ep.C, M, N, ep.ldc, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
     if (!make_tmap_bf16(&tdm, ep.xn, M, N, N, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
   }
-  constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : 8 * 2 * 2048;
+  constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
   constexpr int smem = STAGES * BM * BK * 2 + (WS ? 256 / BK : STAGES) * BN * BK * 2 + STG + 1024 + 256;
   static_assert(smem <= 227 * 1024, "shared memory");
   if (WS && K != 256) return false;

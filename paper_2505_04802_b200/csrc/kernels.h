@@ -21,8 +21,8 @@ enum Epi : int {
   // epilogue): the updated z row is written and LN(z) -> xn (bf16) as well
   EPI_RESID_LN = 4,   // z += acc + bias; xn = LN(z)     (O-projection + LN2)
   EPI_EMBED_LN = 5,   // z = acc + bias + pi; xn = LN(z) (patch embed + LN1 of block 0)
-  // training backward: C[m,n] = bf16(acc * GELU'(aux[m,n]))  (aux = the forward's
-  // pre-activation, bf16 [M][ldc]; GELU' = Phi(x) + x phi(x), R9)
+  // training backward: C[m,n] = bf16(acc * aux[m,n]), aux = GELU'(pre-activation) (bf16
+  // [M][ldc], GELU' = Phi(x) + x phi(x), R9) that the training forward's EPI_GELU kept
   EPI_DGELU = 6,
 };
 
@@ -39,9 +39,9 @@ struct EpiParams {
   void* xn;                // *_LN: bf16 LayerNorm output [M][N]
   const float* ln_g;       // *_LN: LayerNorm gain / bias [N]
   const float* ln_b;
-  // training: EPI_GELU also stores the pre-activation (bf16, same ldc) here; EPI_RESID
+  // training: EPI_GELU also stores GELU'(pre-activation) (bf16, same ldc) here; EPI_RESID
   // reads the residual input from here (fp32, same ldc) instead of C (C = aux + acc + bias);
-  // EPI_DGELU: the pre-activation it differentiates
+  // EPI_DGELU: the GELU' factor it multiplies by
   const void* aux = nullptr;
 };
 

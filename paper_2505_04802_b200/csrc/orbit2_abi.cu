@@ -35,7 +35,8 @@ struct Timing {
 struct TrainLay {
   int64_t rows = 0, rows_core = 0;       // mrow, mcore of the plan
   int64_t nh_pad = 0;                    // K P^2 rounded up to 64 (GEMM K of dhin = dG W_h)
-  std::vector<int64_t> zin, xn1, qkv, ao, lse, zmid, xn2, hpre, hact;   // per block
+  // per block; gdash = GELU'(MLP pre-activation) (bf16), written by the MLP-up epilogue
+  std::vector<int64_t> zin, xn1, qkv, ao, lse, zmid, xn2, gdash, hact;
   int64_t zfin = 0, hin = 0;
   int64_t dz = 0, dz_bf = 0, dzm = 0, dzm_bf = 0, dh = 0, dxn = 0, dao = 0, delta = 0, dq = 0, dqkv = 0;
   int64_t dg = 0, dhin = 0, latw = 0, zero = 0;
@@ -950,7 +951,8 @@ static orbit2_status train_scope(const Ctx* c) {
     return set_err(ORBIT2_E_UNSUPPORTED, "training: var_agg / res_hidden / dec_hidden stages are out of scope (R36)");
   if (p.info.chunk_tiles < p.info.n_local_tiles)
     return set_err(ORBIT2_E_UNSUPPORTED, "training: one call over every rank-local tile (chunk_tiles = 0)");
-  if (p.D > 1024) return set_err(ORBIT2_E_UNSUPPORTED, "training: embed <= 1024 (LayerNorm backward kernel)");
+  if (p.D > 1024 || p.D % 128)
+    return set_err(ORBIT2_E_UNSUPPORTED, "training: embed a multiple of 128 up to 1024 (LayerNorm backward kernel)");
   return ORBIT2_OK;
 }
 
@@ -971,7 +973,7 @@ static TrainLay train_layout(const Plan& p) {
     t.lse.push_back(take(H * R * 4));
     t.zmid.push_back(take(R * D * 4));
     t.xn2.push_back(take(R * D * 2));
-    t.hpre.push_back(take(R * 4 * D * 2));
+    t.gdash.push_back(take(R * 4 * D * 2));
     t.hact.push_back(take(R * 4 * D * 2));
   }
   t.zfin = take(R * D * 4);
@@ -1161,7 +1163,7 @@ orbit2_status orbit2_train_forward(void* ctx, const void* packed_w, const float*
       launch_layernorm<bf16>(zmid, wf(L.ln2_g), wf(L.ln2_b), xn2, M, (int)D, nullptr, st);
       return true;
     }));
-    e = EpiParams{}; e.bias = wf(L.b_1); e.C = c->tat<bf16>(t.hact[l]); e.ldc = F; e.aux = c->tat<bf16>(t.hpre[l]);
+    e = EpiParams{}; e.bias = wf(L.b_1); e.C = c->tat<bf16>(t.hact[l]); e.ldc = F; e.aux = c->tat<bf16>(t.gdash[l]);
     ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn2, D, L.w_1, F, D, M, e));
     e = EpiParams{}; e.bias = wf(L.b_2); e.C = zout; e.ldc = D; e.aux = zmid;
     ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, c->tat<bf16>(t.hact[l]), F, L.w_2, D, F, M, e));
@@ -1276,7 +1278,7 @@ orbit2_status orbit2_train_backward(void* ctx, const void* packed_w, const float
     // z_out = zmid + GELU(h) W_2^T + b_2,  h = LN2(zmid) W_1^T + b_1
     ORBIT2_TRY(wg("wgrad_w2", dz_bf, D, c->tat<bf16>(t.hact[l]), F, M, D, F, CL.w_2, CL.b_2));
     ORBIT2_TRY(dx("dx_mlp_down", EPI_DGELU, 1, dz_bf, R, D, c->tat<bf16>(t.w2_t[l]), F, D, M, dh, F,
-                  c->tat<bf16>(t.hpre[l])));
+                  c->tat<bf16>(t.gdash[l])));
     ORBIT2_TRY(wg("wgrad_w1", dh, F, c->tat<bf16>(t.xn2[l]), D, M, F, D, CL.w_1, CL.b_1));
     ORBIT2_TRY(dx("dx_mlp_up", EPI_BIAS, 0, dh, R, F, c->tat<bf16>(t.w1_t[l]), D, F, M, dxn, D, nullptr));
     ORBIT2_TRY(run(c, "ln_bwd", st, [&] {

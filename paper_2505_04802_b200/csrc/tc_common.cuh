@@ -254,6 +254,30 @@ __device__ __forceinline__ float gelu_erf_fast(float x) {
   return 0.5f * x * (1.0f + copysignf(erf_abs, x));
 }
 
+// GELU(x) and GELU'(x) = Phi(x) + x phi(x) together (training forward: the backward
+// multiplies the incoming gradient by GELU'(pre-activation)).  Same erfc polynomial as
+// gelu_erf_fast (Phi(-|x|) = 0.5 erfc(|x| / sqrt2)); phi(x) = exp(-x^2 / 2) / sqrt(2 pi)
+// with one MUFU ex2.
+__device__ __forceinline__ void gelu_and_grad_fast(float x, float& g, float& dg) {
+  const float u = fabsf(x) * 0.70710678118654752f;
+  float p = fmaf(0.0000430638f, u, 0.0002765672f);
+  p = fmaf(p, u, 0.0001520143f);
+  p = fmaf(p, u, 0.0092705272f);
+  p = fmaf(p, u, 0.0422820123f);
+  p = fmaf(p, u, 0.0705230784f);
+  float t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(p, u, 1.0f)));
+  t = t * t;
+  t = t * t;
+  t = t * t;
+  t = t * t;                                   // erfc(u)
+  const float Phi = x >= 0.f ? 1.0f - 0.5f * t : 0.5f * t;
+  float e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-0.72134752044448170f * x * x));   // exp(-x^2/2)
+  g = x * Phi;
+  dg = fmaf(x * 0.39894228040143268f, e, Phi);
+}
+
 // ---- packed fp32 pairs (sm_100a f32x2 FMA-pipe instructions: one issue slot
 // for two lanes' worth of work; the pipe throughput per element is unchanged) ----
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {

@@ -22,30 +22,40 @@ __device__ __forceinline__ float huber_grad(float r, float delta) {
   return fabsf(r) <= delta ? r / delta : copysignf(1.f, r);
 }
 
-// One thread per output pixel (b, k, Y, X) of out [B][K][sH][sW]:
+// Per output pixel i = (b, k, Y, X) of out [B][K][sH][sW]:
 //   loss_b += ( w_Y (y - x)^2 + lambda sum_{j in C(i)} b_ij h(x_i - x_j) ) / n
 //   dout    = ( -2 w_Y (y - x) + 2 lambda sum_j b_ij h'(x_i - x_j) ) / (n B)
 // (C(i) symmetric and h' odd: the pairs (i, j) and (j, i) contribute equally to x_i.)
-// Row weights w_Y (R35) are computed in double from the closed form; block partial
-// sums in double, one atomicAdd per block and sample.
-constexpr int LOSS_THREADS = 256;
+// Block = a 32 x 64 pixel tile of one (b, k) plane, staged with its 1-pixel ring in
+// shared memory (coalesced row loads; every pixel read from HBM once); per-block sum
+// in double, one atomicAdd per block.
+constexpr int LT_Y = 32, LT_X = 64, LOSS_THREADS = 256;
 __global__ void __launch_bounds__(LOSS_THREADS) loss_kernel(const float* __restrict__ out,
                                                             const float* __restrict__ truth, int B, int K, int sH,
                                                             int sW, float lam, float delta, int geo,
                                                             const float* __restrict__ latw, double* __restrict__ loss,
                                                             float* __restrict__ dout) {
-  const int64_t plane = (int64_t)sH * sW;
-  const int64_t per_b = (int64_t)K * plane;
-  const int b = blockIdx.y;
-  const double n = (double)per_b;
+  __shared__ float t[LT_Y + 2][LT_X + 2];
+  const int plane = blockIdx.z;                 // b * K + k
+  const int b = plane / K;
+  const int Y0 = blockIdx.y * LT_Y, X0 = blockIdx.x * LT_X;
+  const float* o = out + (int64_t)plane * sH * sW;
+  for (int e = threadIdx.x; e < (LT_Y + 2) * (LT_X + 2); e += LOSS_THREADS) {
+    const int ty = e / (LT_X + 2), tx = e - ty * (LT_X + 2);
+    const int Y = Y0 + ty - 1, X = X0 + tx - 1;
+    t[ty][tx] = (Y >= 0 && Y < sH && X >= 0 && X < sW) ? __ldg(o + (int64_t)Y * sW + X) : 0.f;
+  }
+  __syncthreads();
+  const double n = (double)K * sH * sW;
+  const float gscale = (float)(1.0 / (n * B));
   double part = 0.0;
-  for (int64_t e = (int64_t)blockIdx.x * LOSS_THREADS + threadIdx.x; e < per_b;
-       e += (int64_t)gridDim.x * LOSS_THREADS) {
-    const int64_t pix = e % plane;
-    const int Y = (int)(pix / sW), X = (int)(pix - (int64_t)Y * sW);
-    const float* o = out + (int64_t)b * per_b + (e - pix);
-    const float x = __ldg(o + pix);
-    const float y = __ldg(truth + (int64_t)b * per_b + e);
+  const int tx = threadIdx.x & (LT_X - 1);
+  for (int ty = threadIdx.x / LT_X; ty < LT_Y; ty += LOSS_THREADS / LT_X) {
+    const int Y = Y0 + ty, X = X0 + tx;
+    if (Y >= sH || X >= sW) continue;
+    const float x = t[ty + 1][tx + 1];
+    const int64_t gi = ((int64_t)plane * sH + Y) * sW + X;
+    const float y = __ldg(truth + gi);
     const float w = geo ? __ldg(latw + Y) : 1.f;
     float tv = 0.f, g = 0.f;
 #pragma unroll
@@ -56,24 +66,24 @@ __global__ void __launch_bounds__(LOSS_THREADS) loss_kernel(const float* __restr
         const int yy = Y + dy, xx = X + dx;
         if (yy < 0 || yy >= sH || xx < 0 || xx >= sW) continue;
         const float bij = (dy != 0 && dx != 0) ? 0.70710678118654752f : 1.f;
-        const float r = x - __ldg(o + (int64_t)yy * sW + xx);
+        const float r = x - t[ty + 1 + dy][tx + 1 + dx];
         tv += bij * huber(r, delta);
         g += bij * huber_grad(r, delta);
       }
     }
     const float dif = y - x;
-    part += (double)w * dif * dif + (double)lam * tv;
-    dout[(int64_t)b * per_b + e] = (float)((-2.0 * w * dif + 2.0 * lam * g) / (n * B));
+    part += (double)(w * dif * dif + lam * tv);
+    dout[gi] = (-2.f * w * dif + 2.f * lam * g) * gscale;
   }
   __shared__ double red[LOSS_THREADS / 32];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  for (int off = 16; off > 0; off >>= 1) part += __shfl_xor_sync(0xffffffffu, part, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < LOSS_THREADS / 32; ++i) s += red[i];
-    atomicAdd(loss + b, s / n);
+    double sum = 0.0;
+    for (int i = 0; i < LOSS_THREADS / 32; ++i) sum += red[i];
+    atomicAdd(loss + b, sum / n);
   }
 }
 
@@ -119,11 +129,13 @@ __global__ void stitch_bwd_kernel(const float* __restrict__ dout, __nv_bfloat16*
   for (int e = Nh + threadIdx.x; e < ldg; e += blockDim.x) row[e] = __float2bfloat16_rn(0.f);
 }
 
-// LayerNorm backward, one warp per row (D % 32 == 0, D <= 1024 held in registers):
+// LayerNorm backward, one warp per row; lane l owns the float4 columns 4 l + 128 k
+// (k < D / 128: coalesced 16-byte accesses):
 //   xh = (z - mu) rstd;  dxh = dy g;  dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
-// out = dres + dz (fp32) and bf16 copy; dgamma += dy xh, dbeta += dy (block sums, atomics).
-// With a row map (LN_f over core rows): input row i reads z[zrow(i)] and writes dz there.
-template <int PER>
+// out = dres + dz (fp32) and a bf16 copy; dgamma += dy xh, dbeta += dy (per-lane partial
+// sums, block reduction, atomics).  With a row map (LN_f over core rows): input row i
+// reads z[zrow(i)] and writes dz there.
+template <int P4>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ dy, int64_t ldy,
                                                      const float* __restrict__ z, const float* __restrict__ g,
                                                      const float* __restrict__ dres, float* __restrict__ dz,
@@ -132,79 +144,90 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
                                                      int64_t chunk_tokens, int64_t tok0,
                                                      float* __restrict__ dgamma, float* __restrict__ dbeta) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float ag[PER], ab[PER];
+  float4 ag[P4], ab[P4], gg[P4];
 #pragma unroll
-  for (int i = 0; i < PER; ++i) ag[i] = ab[i] = 0.f;
+  for (int i = 0; i < P4; ++i) {
+    ag[i] = ab[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    gg[i] = __ldg(reinterpret_cast<const float4*>(g) + lane + 32 * i);
+  }
+  const float invD = 1.f / D;
   for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < M; row += (int64_t)gridDim.x * 8) {
     int64_t zr = row;
     if (rowmap) {
       const int64_t b = row / map_per_b, rr = row - b * map_per_b;
       zr = b * chunk_tokens + (rowmap[rr] - tok0);
     }
-    float zv[PER], dv[PER];
+    const float4* z4 = reinterpret_cast<const float4*>(z + zr * D);
+    const float4* d4 = reinterpret_cast<const float4*>(dy + row * ldy);
+    float4 zv[P4], dv[P4], rv[P4];
+#pragma unroll
+    for (int i = 0; i < P4; ++i) {
+      zv[i] = __ldcs(z4 + lane + 32 * i);
+      dv[i] = __ldcs(d4 + lane + 32 * i);
+      rv[i] = dres ? __ldcs(reinterpret_cast<const float4*>(dres + zr * D) + lane + 32 * i)
+                   : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float s = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int c = lane + 32 * i;
-      zv[i] = c < D ? z[zr * D + c] : 0.f;
-      dv[i] = c < D ? dy[row * ldy + c] : 0.f;
-      s += zv[i];
-    }
+    for (int i = 0; i < P4; ++i) s += (zv[i].x + zv[i].y) + (zv[i].z + zv[i].w);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float mu = s / D;
+    const float mu = s * invD;
     float vs = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const float t = lane + 32 * i < D ? zv[i] - mu : 0.f;
-      vs += t * t;
+    for (int i = 0; i < P4; ++i) {
+      zv[i].x -= mu; zv[i].y -= mu; zv[i].z -= mu; zv[i].w -= mu;
+      vs += zv[i].x * zv[i].x + zv[i].y * zv[i].y + zv[i].z * zv[i].z + zv[i].w * zv[i].w;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) vs += __shfl_xor_sync(0xffffffffu, vs, o);
-    const float rstd = rsqrtf(vs / D + 1e-5f);
+    const float rstd = rsqrtf(vs * invD + 1e-5f);
     float m1 = 0.f, m2 = 0.f;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int c = lane + 32 * i;
-      if (c < D) {
-        const float xh = (zv[i] - mu) * rstd;
-        const float dxh = dv[i] * __ldg(g + c);
-        m1 += dxh;
-        m2 += dxh * xh;
-        ag[i] += dv[i] * xh;
-        ab[i] += dv[i];
-        zv[i] = xh;
-        dv[i] = dxh;
-      }
+    for (int i = 0; i < P4; ++i) {
+      float4 xh = make_float4(zv[i].x * rstd, zv[i].y * rstd, zv[i].z * rstd, zv[i].w * rstd);
+      ag[i].x += dv[i].x * xh.x; ag[i].y += dv[i].y * xh.y; ag[i].z += dv[i].z * xh.z; ag[i].w += dv[i].w * xh.w;
+      ab[i].x += dv[i].x; ab[i].y += dv[i].y; ab[i].z += dv[i].z; ab[i].w += dv[i].w;
+      dv[i].x *= gg[i].x; dv[i].y *= gg[i].y; dv[i].z *= gg[i].z; dv[i].w *= gg[i].w;
+      m1 += (dv[i].x + dv[i].y) + (dv[i].z + dv[i].w);
+      m2 += dv[i].x * xh.x + dv[i].y * xh.y + dv[i].z * xh.z + dv[i].w * xh.w;
+      zv[i] = xh;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       m1 += __shfl_xor_sync(0xffffffffu, m1, o);
       m2 += __shfl_xor_sync(0xffffffffu, m2, o);
     }
-    m1 /= D;
-    m2 /= D;
+    m1 *= invD;
+    m2 *= invD;
+    float4* o4 = reinterpret_cast<float4*>(dz + zr * D);
+    uint2* ob = reinterpret_cast<uint2*>(dz_bf + zr * D);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) {
-      const int c = lane + 32 * i;
-      if (c < D) {
-        float r = rstd * (dv[i] - m1 - zv[i] * m2);
-        if (dres) r += dres[zr * D + c];
-        dz[zr * D + c] = r;
-        dz_bf[zr * D + c] = __float2bfloat16_rn(r);
-      }
+    for (int i = 0; i < P4; ++i) {
+      float4 r;
+      r.x = rv[i].x + rstd * (dv[i].x - m1 - zv[i].x * m2);
+      r.y = rv[i].y + rstd * (dv[i].y - m1 - zv[i].y * m2);
+      r.z = rv[i].z + rstd * (dv[i].z - m1 - zv[i].z * m2);
+      r.w = rv[i].w + rstd * (dv[i].w - m1 - zv[i].w * m2);
+      o4[lane + 32 * i] = r;
+      __nv_bfloat162 lo = __floats2bfloat162_rn(r.x, r.y), hi = __floats2bfloat162_rn(r.z, r.w);
+      ob[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
     }
   }
-  __shared__ float red[8][PER * 32];   // block column sums: dgamma, then dbeta
+  __shared__ float4 red[8][P4 * 32];   // block column sums: dgamma, then dbeta
 #pragma unroll
   for (int pass = 0; pass < 2; ++pass) {
 #pragma unroll
-    for (int i = 0; i < PER; ++i) red[warp][lane + 32 * i] = pass ? ab[i] : ag[i];
+    for (int i = 0; i < P4; ++i) red[warp][lane + 32 * i] = pass ? ab[i] : ag[i];
     __syncthreads();
-    for (int c = threadIdx.x; c < D; c += blockDim.x) {
-      float a = 0.f;
-      for (int w = 0; w < 8; ++w) a += red[w][c];
-      atomicAdd((pass ? dbeta : dgamma) + c, a);
+    for (int c4 = threadIdx.x; c4 < D / 4; c4 += blockDim.x) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int w = 0; w < 8; ++w) {
+        const float4 t = red[w][c4];
+        a.x += t.x; a.y += t.y; a.z += t.z; a.w += t.w;
+      }
+      float* dst = (pass ? dbeta : dgamma) + 4 * c4;
+      atomicAdd(dst, a.x); atomicAdd(dst + 1, a.y); atomicAdd(dst + 2, a.z); atomicAdd(dst + 3, a.w);
     }
     __syncthreads();
   }
@@ -269,11 +292,8 @@ void launch_lat_weights(float* w, int sH, cudaStream_t st) { lat_weights_kernel<
 
 void launch_loss(const float* out, const float* truth, int B, int K, int sH, int sW, float lam, float delta, int geo,
                  const float* latw, double* loss, float* dout, cudaStream_t st) {
-  const int64_t per_b = (int64_t)K * sH * sW;
-  const int64_t blocks = std::min<int64_t>((per_b + LOSS_THREADS - 1) / LOSS_THREADS,
-                                           std::max<int64_t>(1, 4LL * num_sms() / std::max(1, B)) * 4);
-  loss_kernel<<<dim3((unsigned)blocks, (unsigned)B), LOSS_THREADS, 0, st>>>(out, truth, B, K, sH, sW, lam, delta, geo,
-                                                                           latw, loss, dout);
+  dim3 grid((unsigned)((sW + LT_X - 1) / LT_X), (unsigned)((sH + LT_Y - 1) / LT_Y), (unsigned)(B * K));
+  loss_kernel<<<grid, LOSS_THREADS, 0, st>>>(out, truth, B, K, sH, sW, lam, delta, geo, latw, loss, dout);
 }
 
 void launch_stitch_bwd(const float* dout, __nv_bfloat16* dg, int64_t ldg, const ChunkDev& ch, int B, int K, int P,
@@ -286,14 +306,22 @@ bool launch_ln_bwd(const float* dy, int64_t ldy, const float* z, const float* g,
                    __nv_bfloat16* dz_bf, int64_t M, int D, const int32_t* rowmap, int64_t map_per_b,
                    int64_t chunk_tokens, int64_t tok0, float* dgamma, float* dbeta, cudaStream_t st) {
   if (M <= 0) return true;
-  const int blocks = (int)std::min<int64_t>((M + 7) / 8, 4LL * num_sms());
+  if (D % 128 || ldy % 4) return false;
+  const int blocks = (int)std::min<int64_t>((M + 7) / 8, 32LL * num_sms());
 #define LNB(P_)                                                                                                \
   ln_bwd_kernel<P_><<<blocks, 256, 0, st>>>(dy, ldy, z, g, dres, dz, dz_bf, M, D, rowmap, map_per_b, chunk_tokens, \
                                             tok0, dgamma, dbeta);                                              \
   return true
-  if (D <= 256) { LNB(8); }
-  if (D <= 512) { LNB(16); }
-  if (D <= 1024) { LNB(32); }
+  switch (D / 128) {
+    case 1: LNB(1);
+    case 2: LNB(2);
+    case 3: LNB(3);
+    case 4: LNB(4);
+    case 5: LNB(5);
+    case 6: LNB(6);
+    case 7: LNB(7);
+    case 8: LNB(8);
+  }
 #undef LNB
   return false;
 }

@@ -110,8 +110,8 @@ def test_loss_kernel_matches_oracle_elementwise():
     oracle's T2 (fp32 kernel, double accumulation: 1e-5 relative)."""
     import torch
     from paper_2505_04802_b200 import orbit2 as o2
-    w = get_config("C1", H=16, W=20, V=2, K=2, scale=3, patch=2, tiles_y=1, tiles_x=1, halo=0, embed=64, depth=0,
-                   heads=1)
+    w = get_config("C1", H=16, W=20, V=2, K=2, scale=3, patch=2, tiles_y=1, tiles_x=1, halo=0, embed=128, depth=0,
+                   heads=2)
     cfg = o2.config_from(w, batch=2, precision=o2.BF16)
     ctx = o2.Context(cfg)
     ctx.train_bind()
