@@ -316,8 +316,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int q = j * 128 + h * 64 + r;
         const int64_t o = (int64_t)it.h * ld_stat + it.base + q;
         const bool ok = r < 64 && j < it.nq && q < it.n;
-        l = ok ? __ldg(lse + o) : 0.f;
-        dl = ok ? __ldg(delta + o) : 0.f;
+        l = ok ? -__ldg(lse + o) : 0.f;      // staged negated: the inner loop is FFMA2 / FADD2
+        dl = ok ? -__ldg(delta + o) : 0.f;
       };
       float nl, nd;
       ld_stats(0, nl, nd);
@@ -330,9 +330,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (ORBIT2_BWD_PF) ld_stats(j + 1, nl, nd);
         asm volatile("bar.sync %0, 128;" ::"r"(1 + h) : "memory");
-        const float* L = hL + buf * 64;
-        const float* Dl = hDl + buf * 64;
+        const float* nL = hL + buf * 64;                  // -lse2 of the half's queries
+        const float* nD = hDl + buf * 64;                 // -Delta
         const int qv = it.n - j * 128 - h * 64;            // valid queries in this half
+        // no masking unless this key block or this query half runs past the tile end
+        // (block-uniform): invalid keys / queries get P = dS = 0
+        const bool fast = it.k0 + 128 <= it.n && qv >= 64;
         uint8_t* atom = sDS + (gq & 1) * DS_BYTES + h * TILE + r * 128;   // half h = atom h of dS^T
         tc::mbar_wait(&s_full[h], gq & 1);
         tc::tc_fence_after();
@@ -345,19 +348,37 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::tmem_ld_wait();
           uint32_t pk[8], dk[8];
 #pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            float p0 = 0.f, p1 = 0.f;
+          for (int e = 0; e < 16; e += 4) {
+            const float4 nl = *reinterpret_cast<const float4*>(nL + c0 + e);
+            const float4 nd = *reinterpret_cast<const float4*>(nD + c0 + e);
+            const float2 x0 = tc::fma2(make_float2(__uint_as_float(sr[e]), __uint_as_float(sr[e + 1])),
+                                       tc::splat2(sl), make_float2(nl.x, nl.y));
+            const float2 x1 = tc::fma2(make_float2(__uint_as_float(sr[e + 2]), __uint_as_float(sr[e + 3])),
+                                       tc::splat2(sl), make_float2(nl.z, nl.w));
+            float2 p0, p1;
             if (ORBIT2_BWD_NOSM) {
-              p0 = __uint_as_float(sr[e]) * sl - L[c0 + e];
-              p1 = __uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1];
+              p0 = x0;
+              p1 = x1;
             } else {
-              if (kval && c0 + e < qv) p0 = ex2f(__uint_as_float(sr[e]) * sl - L[c0 + e]);
-              if (kval && c0 + e + 1 < qv) p1 = ex2f(__uint_as_float(sr[e + 1]) * sl - L[c0 + e + 1]);
+              p0 = make_float2(ex2f(x0.x), ex2f(x0.y));
+              p1 = make_float2(ex2f(x1.x), ex2f(x1.y));
             }
-            const float d0 = p0 * (__uint_as_float(dr[e]) - Dl[c0 + e]);
-            const float d1 = p1 * (__uint_as_float(dr[e + 1]) - Dl[c0 + e + 1]);
-            pk[e / 2] = tc::pack_bf16(p0, p1);
-            dk[e / 2] = tc::pack_bf16(d0, d1);
+            if (!fast) {
+              const int lim = kval ? qv : 0;
+              p0.x = c0 + e < lim ? p0.x : 0.f;
+              p0.y = c0 + e + 1 < lim ? p0.y : 0.f;
+              p1.x = c0 + e + 2 < lim ? p1.x : 0.f;
+              p1.y = c0 + e + 3 < lim ? p1.y : 0.f;
+            }
+            const float2 d0 = tc::mul2(p0, tc::add2(make_float2(__uint_as_float(dr[e]), __uint_as_float(dr[e + 1])),
+                                                    make_float2(nd.x, nd.y)));
+            const float2 d1 = tc::mul2(p1, tc::add2(make_float2(__uint_as_float(dr[e + 2]),
+                                                                __uint_as_float(dr[e + 3])),
+                                                    make_float2(nd.z, nd.w)));
+            pk[e / 2] = tc::pack_bf16(p0.x, p0.y);
+            pk[e / 2 + 1] = tc::pack_bf16(p1.x, p1.y);
+            dk[e / 2] = tc::pack_bf16(d0.x, d0.y);
+            dk[e / 2 + 1] = tc::pack_bf16(d1.x, d1.y);
           }
           tc::tmem_st8(lb + C_P + h * 32 + c0 / 2, pk);
           const int cb = c0 >> 3;

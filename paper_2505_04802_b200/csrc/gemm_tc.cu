@@ -581,7 +581,11 @@ __global__ void __launch_bounds__(384, 1)
             if constexpr (EPI == EPI_GELU) {
               if (keep_grad) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) tc::gelu_and_grad_fast(v[j], v[j], gd[j]);
+                for (int j = 0; j < 32; j += 2) {
+                  float2 g2, d2;
+                  tc::gelu2_and_grad_fast(make_float2(v[j], v[j + 1]), g2, d2);
+                  v[j] = g2.x; v[j + 1] = g2.y; gd[j] = d2.x; gd[j + 1] = d2.y;
+                }
               } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);

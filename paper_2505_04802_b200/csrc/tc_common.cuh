@@ -340,6 +340,34 @@ __device__ __forceinline__ float2 gelu2_erf_fast(float2 x) {
   return fma2(na, t, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
 }
 
+// GELU and GELU' of a pair in packed f32x2 arithmetic (training forward): with
+// q = Phi(-|x|) from the same polynomial as gelu2_erf_fast, Phi(x) = x >= 0 ? 1 - q : q,
+// GELU = relu(x) - |x| q, GELU' = Phi(x) + x phi(x), phi(x) = exp(-x^2/2) / sqrt(2 pi)
+// (one MUFU ex2 per element besides the reciprocal).
+__device__ __forceinline__ void gelu2_and_grad_fast(float2 x, float2& g, float2& dg) {
+  const float2 na = make_float2(-fabsf(x.x), -fabsf(x.y));
+  float2 p = fma2(splat2(5.6212996640e-06f), na, splat2(-5.1055209009e-05f));
+  p = fma2(p, na, splat2(3.9686137011e-05f));
+  p = fma2(p, na, splat2(-3.4227392389e-03f));
+  p = fma2(p, na, splat2(2.2076998457e-02f));
+  p = fma2(p, na, splat2(-5.2075163037e-02f));
+  p = fma2(p, na, splat2(1.0442737824e+00f));
+  float2 t;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.x) : "f"(p.x));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t.y) : "f"(p.y));
+  t = mul2(t, t);
+  t = mul2(t, t);
+  t = mul2(t, t);
+  t = mul2(t, t);   // q = Phi(-|x|)
+  g = fma2(na, t, make_float2(fmaxf(x.x, 0.f), fmaxf(x.y, 0.f)));
+  const float2 x2 = mul2(x, mul2(x, splat2(-0.72134752044448170f)));   // -x^2/2 * log2(e)
+  float2 e;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.x) : "f"(x2.x));
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e.y) : "f"(x2.y));
+  const float2 Phi = make_float2(x.x >= 0.f ? 1.f - t.x : t.x, x.y >= 0.f ? 1.f - t.y : t.y);
+  dg = fma2(mul2(x, splat2(0.39894228040143268f)), e, Phi);
+}
+
 // GELU of a pair through the tanh form 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3)))
 // with the MUFU tanh (one MUFU op per element, like the reciprocal of the erf form,
 // but 6 instead of 12 packed FMA-pipe instructions per pair).  |error| vs the exact
