@@ -388,6 +388,53 @@ orbit2_status orbit2_loss(void *ctx, const float *out_dev, const float *truth_de
 orbit2_status orbit2_train_backward(void *ctx, const void *packed_w, const float *dout_dev, float *grad_dev,
                                     void *stream);
 
+/* ==========================================================================
+ * Adaptive spatial compression (readings R37-R40).
+ * "the model projects the embedding back into image space and recursively partitions it
+ * into spatial quadrants using a quad-tree structure.  Partitioning continues for any
+ * quadrant where the estimated feature density -- computed via Canny edge detection --
+ * exceeds a predefined threshold, terminating when a minimum patch size is reached"
+ * (P:483).  Context-free calls on caller-owned device buffers; the oracle is
+ * oracle/compress.py.  Fields are [B][H][W] (partition) / [B][C][H][W] (features), with H, W
+ * multiples of max_side (pad by edge replication first); max_side = min_side * 2^k,
+ * 1 <= k <= 6; sigma in (0, 8/3]; 0 < low_frac <= high_frac.
+ * ========================================================================== */
+typedef struct {
+  int32_t batch;            /* B fields */
+  int32_t H, W;             /* pixels */
+  int32_t C;                /* feature channels (tokenize / detokenize) */
+  int32_t min_side;         /* the smallest leaf = the token's pooled size m (pixels) */
+  int32_t max_side;         /* the quad-tree root cells */
+  int32_t embed;            /* D: token width */
+  float threshold;          /* split iff edge pixels / area > threshold (R38) */
+  float sigma, low_frac, high_frac;   /* Canny (R37) */
+} orbit2_compress_config;
+
+/* Sizing (host only): device workspace bytes of orbit2_compress_partition and the
+ * capacity of the leaf list (B * (H/min_side) * (W/min_side)). */
+orbit2_status orbit2_compress_plan(const orbit2_compress_config *cfg, int64_t *workspace_bytes,
+                                   int64_t *max_patches);
+/* Canny edge map + quad-tree of every field: patches_dev [max_patches][4] int32 receives the
+ * leaves (image, row, col, side) in (image, row, col) order, offsets_dev [B + 1] the first
+ * leaf of every image (offsets[B] = total), *n_host the total (the call synchronises the
+ * stream once per hysteresis pass: the leaf count is data-dependent).  edges_dev (nullable,
+ * [B][H][W] uint8) receives the edge map (1 = edge). */
+orbit2_status orbit2_compress_partition(const orbit2_compress_config *cfg, const float *image_dev,
+                                        void *workspace_dev, size_t workspace_bytes, uint8_t *edges_dev,
+                                        int32_t *patches_dev, int32_t *offsets_dev, int32_t *n_host,
+                                        void *stream);
+/* tokens_dev [n][D] = W_tok pool(leaf) + b_tok + e_scale[log2(side / min_side)]; w_tok
+ * [D][C m m] (column (c m + i) m + j), b_tok [D], e_scale [k + 1][D] (R39). */
+orbit2_status orbit2_compress_tokenize(const orbit2_compress_config *cfg, const float *feat_dev,
+                                       const int32_t *patches_dev, int32_t n, const float *w_tok,
+                                       const float *b_tok, const float *e_scale, float *tokens_dev, void *stream);
+/* out_dev [B][C][H][W] = smooth(broadcast(W_dec t + b_dec)); w_dec [C m m][D], b_dec [C m m],
+ * w_sm [C][C][3][3], b_sm [C]; work_dev: [B][C][H][W] scratch (R40). */
+orbit2_status orbit2_compress_detokenize(const orbit2_compress_config *cfg, const float *tokens_dev,
+                                         const int32_t *patches_dev, int32_t n, const float *w_dec,
+                                         const float *b_dec, const float *w_sm, const float *b_sm,
+                                         float *work_dev, float *out_dev, void *stream);
+
 int64_t orbit2_launch_count(void *ctx);
 
 /*

@@ -172,6 +172,24 @@ void launch_delta(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* delta,
 void launch_dq_convert(const float* dq, __nv_bfloat16* dqkv, int64_t M, int D, cudaStream_t st);
 void launch_transpose_bf16(const float* W, int n, int k, __nv_bfloat16* Wt, int64_t ld, cudaStream_t st);
 
+// ---- adaptive spatial compression (compress.cu) ----
+bool compress_taps(float sigma, float* w, int* r);
+// Canny over B images [B][H][W]: lab = 2 on edge pixels (hysteresis on the host-driven loop);
+// *passes = hysteresis passes over the field
+void launch_canny(const float* img, float* tmp, float* tmp2, float* mag, uint8_t* dir, uint8_t* lab, unsigned* gmax,
+                  int* changed, int B, int H, int W, float sigma, float low_frac, float high_frac, cudaStream_t st,
+                  int* passes);
+void launch_edges(const uint8_t* lab, uint8_t* e, int64_t n, cudaStream_t st);
+// quad-tree leaves -> patches [n][4] (image, row, col, side) in (image, row, col) order,
+// offsets[b] = first leaf of image b, *total = n (= offsets[B])
+void launch_quadtree(const uint8_t* lab, int32_t* flag, int32_t* bsum, int32_t* total, int32_t* patches,
+                     int32_t* offsets, int B, int H, int W, int mn, int mx, double thr, cudaStream_t st);
+void launch_tokenize(const float* feat, const int32_t* patches, int n, int C, int H, int W, int m, int D,
+                     const float* wt, const float* bt, const float* es, float* tok, cudaStream_t st);
+void launch_detokenize(const float* tok, const int32_t* patches, int n, int B, int C, int H, int W, int m, int D,
+                       const float* wd, const float* bd, const float* ws, const float* bs, float* work, float* out,
+                       cudaStream_t st);
+
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)
 bool tma_available();
 

@@ -1318,4 +1318,117 @@ orbit2_status orbit2_train_backward(void* ctx, const void* packed_w, const float
   return ORBIT2_OK;
 }
 
+
+/* ------------------------------------------------------------------------------
+ * Adaptive spatial compression (oracle/compress.py, R37-R40)
+ * ---------------------------------------------------------------------------- */
+struct CompressLay {
+  int64_t tmp, tmp2, mag, dir, lab, gmax, changed, flag, bsum, total;
+};
+
+static orbit2_status compress_check(const orbit2_compress_config* c, CompressLay* ly) {
+  if (!c) return set_err(ORBIT2_E_INVALID, "compress cfg: null");
+  if (c->batch < 1 || c->H < 3 || c->W < 3) return set_err(ORBIT2_E_INVALID, "compress: batch >= 1, H, W >= 3");
+  if (c->min_side < 1 || c->max_side < 2 * c->min_side || c->max_side % c->min_side ||
+      ((c->max_side / c->min_side) & (c->max_side / c->min_side - 1)) || c->max_side / c->min_side > 64)
+    return set_err(ORBIT2_E_INVALID, "compress: max_side must be min_side * 2^k, 1 <= k <= 6");
+  if (c->H % c->max_side || c->W % c->max_side)
+    return set_err(ORBIT2_E_INVALID, "compress: H, W must be multiples of max_side (pad by edge replication)");
+  float w[32];
+  int r = 0;
+  if (!compress_taps(c->sigma, w, &r)) return set_err(ORBIT2_E_INVALID, "compress: sigma must be in (0, 8/3]");
+  if (!(c->low_frac > 0.f) || !(c->low_frac <= c->high_frac) || !(c->threshold >= 0.f))
+    return set_err(ORBIT2_E_INVALID, "compress: 0 < low_frac <= high_frac, threshold >= 0");
+  const int64_t n = (int64_t)c->batch * c->H * c->W;
+  const int64_t cells = (int64_t)c->batch * (c->H / c->min_side) * (c->W / c->min_side);
+  int64_t off = 0;
+  auto take = [&](int64_t b) { int64_t o = off; off = round_up(off + b, 256); return o; };
+  ly->tmp = take(n * 4);
+  ly->tmp2 = take(n * 4);
+  ly->mag = take(n * 4);
+  ly->dir = take(n);
+  ly->lab = take(n);
+  ly->gmax = take((int64_t)c->batch * 4);
+  ly->changed = take(4);
+  ly->flag = take(cells * 4);
+  ly->bsum = take(((cells + 1023) / 1024) * 4);
+  ly->total = off;
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_compress_plan(const orbit2_compress_config* cfg, int64_t* workspace_bytes, int64_t* max_patches) {
+  CompressLay ly;
+  ORBIT2_TRY(compress_check(cfg, &ly));
+  if (workspace_bytes) *workspace_bytes = ly.total;
+  if (max_patches) *max_patches = (int64_t)cfg->batch * (cfg->H / cfg->min_side) * (cfg->W / cfg->min_side);
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_compress_partition(const orbit2_compress_config* cfg, const float* image_dev, void* ws,
+                                        size_t ws_bytes, uint8_t* edges_dev, int32_t* patches_dev,
+                                        int32_t* offsets_dev, int32_t* n_host, void* stream) {
+  CompressLay ly;
+  ORBIT2_TRY(compress_check(cfg, &ly));
+  if (!image_dev || !ws || !patches_dev || !offsets_dev) return set_err(ORBIT2_E_INVALID, "compress: null pointer");
+  if ((int64_t)ws_bytes < ly.total) return set_err(ORBIT2_E_INVALID, "compress: workspace smaller than planned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  const int B = cfg->batch, H = cfg->H, W = cfg->W;
+  int passes = 0;
+  launch_canny(image_dev, reinterpret_cast<float*>(w8 + ly.tmp), reinterpret_cast<float*>(w8 + ly.tmp2),
+               reinterpret_cast<float*>(w8 + ly.mag), w8 + ly.dir, w8 + ly.lab,
+               reinterpret_cast<unsigned*>(w8 + ly.gmax), reinterpret_cast<int*>(w8 + ly.changed), B, H, W,
+               cfg->sigma, cfg->low_frac, cfg->high_frac, st, &passes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compress canny: ") + cudaGetErrorString(e));
+  if (edges_dev) launch_edges(w8 + ly.lab, edges_dev, (int64_t)B * H * W, st);
+  launch_quadtree(w8 + ly.lab, reinterpret_cast<int32_t*>(w8 + ly.flag), reinterpret_cast<int32_t*>(w8 + ly.bsum),
+                  offsets_dev + B, patches_dev, offsets_dev, B, H, W, cfg->min_side, cfg->max_side,
+                  (double)cfg->threshold, st);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compress quadtree: ") + cudaGetErrorString(e));
+  if (n_host) {
+    e = cudaMemcpyAsync(n_host, offsets_dev + B, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compress count: ") + cudaGetErrorString(e));
+  }
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_compress_tokenize(const orbit2_compress_config* cfg, const float* feat_dev,
+                                       const int32_t* patches_dev, int32_t n, const float* w_tok, const float* b_tok,
+                                       const float* e_scale, float* tokens_dev, void* stream) {
+  CompressLay ly;
+  ORBIT2_TRY(compress_check(cfg, &ly));
+  if (cfg->C < 1 || cfg->embed < 1) return set_err(ORBIT2_E_INVALID, "compress tokenize: C, embed >= 1");
+  if (n < 0 || (n > 0 && (!feat_dev || !patches_dev || !w_tok || !b_tok || !e_scale || !tokens_dev)))
+    return set_err(ORBIT2_E_INVALID, "compress tokenize: null pointer or n < 0");
+  if ((int64_t)cfg->C * cfg->min_side * cfg->min_side * 4 > 48 * 1024)
+    return set_err(ORBIT2_E_UNSUPPORTED, "compress tokenize: C * min_side^2 too large for shared memory");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  launch_tokenize(feat_dev, patches_dev, n, cfg->C, cfg->H, cfg->W, cfg->min_side, cfg->embed, w_tok, b_tok, e_scale,
+                  tokens_dev, st);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ORBIT2_OK : set_err(ORBIT2_E_CUDA, std::string("compress tokenize: ") + cudaGetErrorString(e));
+}
+
+orbit2_status orbit2_compress_detokenize(const orbit2_compress_config* cfg, const float* tokens_dev,
+                                         const int32_t* patches_dev, int32_t n, const float* w_dec, const float* b_dec,
+                                         const float* w_sm, const float* b_sm, float* work_dev, float* out_dev,
+                                         void* stream) {
+  CompressLay ly;
+  ORBIT2_TRY(compress_check(cfg, &ly));
+  if (cfg->C < 1 || cfg->embed < 1) return set_err(ORBIT2_E_INVALID, "compress detokenize: C, embed >= 1");
+  if (n < 0 || !w_sm || !b_sm || !work_dev || !out_dev || (n > 0 && (!tokens_dev || !patches_dev || !w_dec || !b_dec)))
+    return set_err(ORBIT2_E_INVALID, "compress detokenize: null pointer or n < 0");
+  if ((int64_t)cfg->C * cfg->min_side * cfg->min_side * 4 > 48 * 1024)
+    return set_err(ORBIT2_E_UNSUPPORTED, "compress detokenize: C * min_side^2 too large for shared memory");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  launch_detokenize(tokens_dev, patches_dev, n, cfg->batch, cfg->C, cfg->H, cfg->W, cfg->min_side, cfg->embed, w_dec,
+                    b_dec, w_sm, b_sm, work_dev, out_dev, st);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ORBIT2_OK
+                          : set_err(ORBIT2_E_CUDA, std::string("compress detokenize: ") + cudaGetErrorString(e));
+}
+
 }  // extern "C"

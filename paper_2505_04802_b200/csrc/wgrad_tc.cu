@@ -176,8 +176,9 @@ bool launch_bn(const GemmOperand& A, const GemmOperand& X, int64_t M, int N, int
   const int n_tiles_n = (N + 127) / 128, n_tiles_k = (Kc + BN - 1) / BN;
   const int tiles = n_tiles_n * n_tiles_k;
   const int64_t chunks = (M + TK - 1) / TK;
-  // split the token range so every SM gets ~2 tile-splits, each of >= 16 chunks (1024 tokens)
-  int64_t splits = std::max<int64_t>(1, (2LL * num_sms() + tiles - 1) / tiles);
+  // split the token range so the grid is at most two full waves (tiles x splits <= 2 x SMs:
+  // no partial third wave), each split >= 16 chunks (1024 tokens)
+  int64_t splits = std::max<int64_t>(1, (2LL * num_sms()) / tiles);
   splits = std::max<int64_t>(1, std::min<int64_t>(splits, chunks / 16));
   if (splits > 65535) splits = 65535;
   dim3 grid((unsigned)tiles, (unsigned)splits);

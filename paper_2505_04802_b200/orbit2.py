@@ -8,6 +8,8 @@ raises.
 from __future__ import annotations
 
 import ctypes as C
+
+_ct = C   # ctypes under a name no parameter shadows
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -52,6 +54,11 @@ class orbit2_train_info(C.Structure):
                 ("attn_bwd_flops_per_sample", C.c_double)]
 
 
+class orbit2_compress_config(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("batch", "H", "W", "C", "min_side", "max_side", "embed")] + [
+        (n, C.c_float) for n in ("threshold", "sigma", "low_frac", "high_frac")]
+
+
 class orbit2_rect(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("y0", "y1", "x0", "x1")]
 
@@ -91,6 +98,12 @@ def _load():
         "orbit2_train_forward": (i32, [vp, vp, vp, vp, vp]),
         "orbit2_loss": (i32, [vp, vp, vp, C.c_float, C.c_float, i32, vp, vp, vp]),
         "orbit2_train_backward": (i32, [vp, vp, vp, vp, vp]),
+        "orbit2_compress_plan": (i32, [C.POINTER(orbit2_compress_config), C.POINTER(i64), C.POINTER(i64)]),
+        "orbit2_compress_partition": (i32, [C.POINTER(orbit2_compress_config), vp, vp, C.c_size_t, vp, vp, vp,
+                                            C.POINTER(i32), vp]),
+        "orbit2_compress_tokenize": (i32, [C.POINTER(orbit2_compress_config), vp, vp, i32, vp, vp, vp, vp, vp]),
+        "orbit2_compress_detokenize": (i32, [C.POINTER(orbit2_compress_config), vp, vp, i32, vp, vp, vp, vp, vp,
+                                             vp, vp]),
         "orbit2_launch_count": (i64, [vp]),
         "orbit2_set_profiling": (i32, [vp, i32]),
         "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
@@ -111,6 +124,8 @@ EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orb
             "orbit2_comm_barrier", "orbit2_comm_status",
             "orbit2_train_plan", "orbit2_train_bind", "orbit2_train_prepare", "orbit2_train_forward",
             "orbit2_loss", "orbit2_train_backward",
+            "orbit2_compress_plan", "orbit2_compress_partition", "orbit2_compress_tokenize",
+            "orbit2_compress_detokenize",
             "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
             "orbit2_destroy")
 
@@ -543,3 +558,56 @@ class Context:
         ms = (C.c_double * n)()
         lib.orbit2_kernel_times(self.handle, names, launches, ms, n)
         return {names[i].decode(): (int(launches[i]), float(ms[i])) for i in range(n)}
+
+
+class Compressor:
+    """Adaptive spatial compression (include/orbit2.h): Canny +
+    quad-tree partition of B fields, variable-size tokens and their decompression."""
+
+    def __init__(self, *, batch, H, W, C, min_side, max_side, embed, threshold=0.05, sigma=1.0, low_frac=0.1,
+                 high_frac=0.2, device=None):
+        import torch
+        self.cfg = orbit2_compress_config(batch, H, W, C, min_side, max_side, embed, threshold, sigma, low_frac,
+                                          high_frac)
+        ws, mp = _ct.c_int64(), _ct.c_int64()
+        _check(lib.orbit2_compress_plan(_ct.byref(self.cfg), _ct.byref(ws), _ct.byref(mp)), "orbit2_compress_plan")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.workspace = torch.empty(max(ws.value, 16), dtype=torch.uint8, device=self.device)
+        self.max_patches = mp.value
+        self.patches = torch.empty((max(mp.value, 1), 4), dtype=torch.int32, device=self.device)
+        self.offsets = torch.empty(batch + 1, dtype=torch.int32, device=self.device)
+
+    def partition(self, image_dev, edges=False, stream=None):
+        """-> (patches [n, 4] int32 (image, row, col, side), offsets [B + 1], n, edge map or None)"""
+        import torch
+        _req(image_dev, torch.float32, "image_dev")
+        e = torch.empty(image_dev.shape, dtype=torch.uint8, device=self.device) if edges else None
+        n = _ct.c_int32()
+        with _on_device(self.device):
+            _check(lib.orbit2_compress_partition(_ct.byref(self.cfg), _ptr(image_dev), _ptr(self.workspace),
+                                                 self.workspace.numel(), _ptr(e) if e is not None else None,
+                                                 _ptr(self.patches), _ptr(self.offsets), _ct.byref(n), _stream(stream)),
+                   "orbit2_compress_partition")
+        return self.patches[:n.value], self.offsets, n.value, e
+
+    def tokenize(self, feat_dev, patches, n, w_tok, b_tok, e_scale, stream=None):
+        import torch
+        for t, name in ((feat_dev, "feat_dev"), (w_tok, "w_tok"), (b_tok, "b_tok"), (e_scale, "e_scale")):
+            _req(t, torch.float32, name)
+        tok = torch.empty((max(n, 1), self.cfg.embed), dtype=torch.float32, device=self.device)
+        with _on_device(self.device):
+            _check(lib.orbit2_compress_tokenize(_ct.byref(self.cfg), _ptr(feat_dev), _ptr(patches), n, _ptr(w_tok),
+                                                _ptr(b_tok), _ptr(e_scale), _ptr(tok), _stream(stream)),
+                   "orbit2_compress_tokenize")
+        return tok[:n]
+
+    def detokenize(self, tokens, patches, n, w_dec, b_dec, w_sm, b_sm, stream=None):
+        import torch
+        cf = self.cfg
+        out = torch.empty((cf.batch, cf.C, cf.H, cf.W), dtype=torch.float32, device=self.device)
+        work = torch.empty_like(out)
+        with _on_device(self.device):
+            _check(lib.orbit2_compress_detokenize(_ct.byref(cf), _ptr(tokens), _ptr(patches), n, _ptr(w_dec),
+                                                  _ptr(b_dec), _ptr(w_sm), _ptr(b_sm), _ptr(work), _ptr(out),
+                                                  _stream(stream)), "orbit2_compress_detokenize")
+        return out

@@ -1,0 +1,101 @@
+"""GPU parity of the adaptive spatial compression against
+oracle/compress.py, through the C ABI (orbit2_compress_*).
+
+The edge map and the leaf list are integer / boolean results: bit-exact (the Canny
+arithmetic is float32 in the same operation order on both sides, R37).  Tokens and the
+decompressed field are fp32 sums of products: 1e-5 of the field's scale.
+"""
+import numpy as np
+import pytest
+
+from oracle import compress as K
+from workloads import get_config, make_input
+
+pytestmark = pytest.mark.gpu
+
+
+def _fields(B, H, W, seed):
+    """ERA5-shaped synthetic fields (workloads.make_input channel 0 of C2, cropped / edge
+    padded) plus a step and a diagonal step: smooth regions and sharp fronts."""
+    w = get_config("C2")
+    x = make_input(w, batch=B, seed=seed)[:, 0].astype(np.float32)     # [B, 180, 360]
+    x = np.pad(x, ((0, 0), (0, max(0, H - x.shape[1])), (0, max(0, W - x.shape[2]))), mode="edge")[:, :H, :W]
+    yy, xx = np.mgrid[0:H, 0:W]
+    if B > 1:
+        x[1] = np.where(xx >= W // 3, 1.0, 0.0) + 0.1 * x[1] / (np.abs(x[1]).max() + 1e-6)
+    if B > 2:
+        x[2] = np.where(xx - yy >= 7, 2.0, -1.0).astype(np.float32)
+    return np.ascontiguousarray(x, np.float32)
+
+
+def _run(B, H, W, mn, mx, thr, C=3, D=16, seed=0, sigma=1.0):
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    img = _fields(B, H, W, seed)
+    comp = o2.Compressor(batch=B, H=H, W=W, C=C, min_side=mn, max_side=mx, embed=D, threshold=thr, sigma=sigma)
+    patches, offsets, n, edges = comp.partition(torch.from_numpy(img).cuda(), edges=True)
+    torch.cuda.synchronize()
+    return comp, img, patches, offsets.cpu().numpy(), n, edges.cpu().numpy().astype(bool)
+
+
+@pytest.mark.parametrize("shape,mn,mx,thr,sigma", [((64, 96), 2, 16, 0.05, 1.0), ((48, 48), 4, 16, 0.0, 1.0),
+                                                 ((96, 160), 2, 32, 0.1, 2.0)])
+def test_partition_bit_exact(shape, mn, mx, thr, sigma):
+    """Edge maps and leaf lists (order, offsets) equal the oracle's exactly, per image."""
+    H, W = shape
+    B = 3
+    comp, img, patches, offsets, n, edges = _run(B, H, W, mn, mx, thr, sigma=sigma)
+    p = patches.cpu().numpy()
+    assert offsets[0] == 0 and offsets[B] == n
+    for b in range(B):
+        e_ref = K.canny(img[b], sigma)
+        assert np.array_equal(edges[b], e_ref), (b, int((edges[b] != e_ref).sum()))
+        ref = K.quadtree(e_ref, mn, mx, thr)
+        got = [tuple(int(v) for v in r[1:]) for r in p[offsets[b]:offsets[b + 1]]]
+        assert (p[offsets[b]:offsets[b + 1], 0] == b).all()
+        assert got == ref
+
+
+def test_tokenize_and_detokenize_match_oracle():
+    import torch
+    B, H, W, C, mn, mx, D = 2, 64, 96, 3, 2, 16, 24
+    comp, img, patches, offsets, n, edges = _run(B, H, W, mn, mx, 0.05, C=C, D=D, seed=3)
+    rng = np.random.default_rng(4)
+    feat = rng.standard_normal((B, C, H, W)).astype(np.float32)
+    levels = int(np.log2(mx // mn)) + 1
+    Wt, bt, E = (rng.standard_normal((D, C * mn * mn)).astype(np.float32), rng.standard_normal(D).astype(np.float32),
+                 rng.standard_normal((levels, D)).astype(np.float32))
+    Wd, bd = rng.standard_normal((C * mn * mn, D)).astype(np.float32), rng.standard_normal(C * mn * mn).astype(np.float32)
+    Ws, bs = (0.2 * rng.standard_normal((C, C, 3, 3))).astype(np.float32), rng.standard_normal(C).astype(np.float32)
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    tok = comp.tokenize(cu(feat), patches, n, cu(Wt), cu(bt), cu(E))
+    out = comp.detokenize(tok, patches, n, cu(Wd), cu(bd), cu(Ws), cu(bs))
+    torch.cuda.synchronize()
+    tok, out = tok.cpu().numpy(), out.cpu().numpy()
+    p = patches.cpu().numpy()
+    for b in range(B):
+        leaves = [tuple(int(v) for v in r[1:]) for r in p[offsets[b]:offsets[b + 1]]]
+        ref_t = K.tokenize(feat[b].astype(np.float64), leaves, mn, Wt, bt, E)
+        np.testing.assert_allclose(tok[offsets[b]:offsets[b + 1]], ref_t, rtol=0, atol=1e-5 * np.abs(ref_t).max())
+        # decompress the oracle's tokens of the GPU's own tokens (isolates K4)
+        ref_o = K.detokenize(tok[offsets[b]:offsets[b + 1]].astype(np.float64), leaves, mn, C, H, W, Wd, bd, Ws, bs)
+        np.testing.assert_allclose(out[b], ref_o, rtol=0, atol=1e-5 * np.abs(ref_o).max())
+
+
+def test_partition_full_c2_field_batch():
+    """The C2 coarse field size (180 x 360, edge padded to 192 x 368 for max_side 16), B = 8:
+    the leaf lists of images 0 and 7 equal the oracle's; every image's leaves tile its field;
+    the compression ratio is > 1 on these smooth fields."""
+    B, H, W = 8, 192, 368
+    comp, img, patches, offsets, n, edges = _run(B, H, W, 2, 16, 0.05, seed=5)
+    p = patches.cpu().numpy()
+    for b in (0, B - 1):
+        ref = K.quadtree(K.canny(img[b]), 2, 16, 0.05)
+        got = [tuple(int(v) for v in r[1:]) for r in p[offsets[b]:offsets[b + 1]]]
+        assert got == ref
+    for b in range(B):
+        cover = np.zeros((H, W), np.int32)
+        for _, r, c, s in p[offsets[b]:offsets[b + 1]]:
+            cover[r:r + s, c:c + s] += 1
+        assert (cover == 1).all()
+    assert n < B * (H // 2) * (W // 2)
