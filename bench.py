@@ -42,11 +42,13 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
     ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="sp", choices=["dp", "sp", "train"],
+    ap.add_argument("--mode", default="sp", choices=["dp", "sp", "train", "compress"],
                     help="N > 1 only.  sp (default): the tiles of one batch spread over the ranks, halo "
                          "exchange + output gather through NVLink peer memory (strong scaling); dp: every "
                          "rank its own batch (weak scaling).  train (any N): the training step (SURVEY "
-                         "§8(f) row 3): forward, Bayesian loss, backward, one gradient all-reduce per batch")
+                         "§8(f) row 3): forward, Bayesian loss, backward, one gradient all-reduce per batch.  "
+                         "compress (N = 1): adaptive spatial compression (§8(f) row 4) of the batch's coarse "
+                         "fields: Canny + quad-tree partition, variable-size tokens, decompression")
     ap.add_argument("--lam", type=float, default=1e-3, help="train: TV prior weight lambda (R34)")
     ap.add_argument("--delta", type=float, default=1e-3, help="train: Huber width delta (R34)")
     ap.add_argument("--sp-groups", type=int, default=0,
@@ -787,6 +789,66 @@ def run_train(args, w, world, rank, local):
         print(json.dumps(res), flush=True)
 
 
+# ---------------------------------------------------------------------------
+# adaptive spatial compression
+# ---------------------------------------------------------------------------
+def run_compress(args, w, world, rank, local):
+    """Partition (Canny on variable 0 + quad-tree, min_side = p, max_side = 16 p), tokenize
+    the V input variables of every leaf into D-wide tokens, decompress back to V fields:
+    the batch's coarse fields edge-padded to a multiple of max_side."""
+    import numpy as np
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from workloads import make_input
+    B, V, D, mn = w.batch, w.V, w.embed, w.patch
+    mx = 16 * mn
+    x = make_input(w, batch=B)
+    H, W = -(-w.H // mx) * mx, -(-w.W // mx) * mx
+    x = np.pad(x, ((0, 0), (0, 0), (0, H - w.H), (0, W - w.W)), mode="edge").astype(np.float32)
+    feat = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    img = feat[:, 0].contiguous()
+    # sigma 2 / threshold 0.13: ~2-5x fewer tokens on these synthetic fields (the paper's runs: 4-32x)
+    thr, sigma = 0.13, 2.0
+    comp = o2.Compressor(batch=B, H=H, W=W, C=V, min_side=mn, max_side=mx, embed=D, threshold=thr, sigma=sigma)
+    rng = np.random.default_rng(0)
+    levels = int(np.log2(mx // mn)) + 1
+    cu = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).cuda()
+    Wt, bt, E = cu(0.05 * rng.standard_normal((D, V * mn * mn))), cu(rng.standard_normal(D)), \
+        cu(rng.standard_normal((levels, D)))
+    Wd, bd = cu(0.05 * rng.standard_normal((V * mn * mn, D))), cu(rng.standard_normal(V * mn * mn))
+    Ws, bs = cu(0.05 * rng.standard_normal((V, V, 3, 3))), cu(rng.standard_normal(V))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        patches, _, n, _ = comp.partition(img)
+        tok = comp.tokenize(feat, patches, n, Wt, bt, E)
+        comp.detokenize(tok, patches, n, Wd, bd, Ws, bs)
+        return n
+
+    for _ in range(max(3, args.warmup)):
+        n = step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            n = step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    uniform = B * (H // mn) * (W // mn)
+    res = {"metric": "adaptive compression: coarse px/s through partition + tokenize + decompress",
+           "value": B * H * W / (ms * 1e-3), "unit": "coarse px/s", "n_gpus": 1, "steps": args.steps,
+           "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic ERA5-shaped fields (edge padded)",
+           "config": {"workload": w.name, "batch": B, "field": [H, W], "channels": V, "embed": D,
+                      "min_side": mn, "max_side": mx, "threshold": thr, "sigma": sigma, "mode": "compress"},
+           "tokens": n, "uniform_tokens": uniform, "compression_ratio": uniform / max(n, 1),
+           "clocks": clk.summary(), "host_s_per_step": (time.perf_counter() - t0) / args.steps}
+    print(json.dumps(res), flush=True)
+
+
 def relaunch_if_needed(args):
     """`python bench.py --gpus N` without torchrun: re-exec under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
@@ -820,6 +882,8 @@ def main():
     try:
         if args.mode == "train":
             run_train(args, w, world, rank, local)
+        elif args.mode == "compress":
+            run_compress(args, w, world, rank, local)
         elif world > 1 and args.mode == "sp":
             run_sp(args, w, world, rank, local)
         else:

@@ -245,3 +245,49 @@ def detokenize(tokens: np.ndarray, patches: list, m: int, C: int, H: int, W: int
         idx = (np.arange(s) * m) // s
         img[:, r:r + s, c:c + s] = proj[:, idx][:, :, idx]
     return conv3x3_same(img, np.asarray(W_sm, np.float64), b_sm)
+
+
+# ---------------------------------------------------------------------------
+# K5 the Reslim forward on compressed tokens (R41)
+# ---------------------------------------------------------------------------
+def compression_field(z0: np.ndarray, Hp: int, Wp: int) -> np.ndarray:
+    """R41: the embedding projected back into image space by the channel-averaging
+    projection: f[u, w] = mean_d z0[u Wp + w, d] (float64 here; the kernel's is fp32)."""
+    return np.asarray(z0, np.float64).mean(axis=1).reshape(Hp, Wp)
+
+
+def partition_tokens(z0: np.ndarray, Hp: int, Wp: int, max_side: int, threshold: float, sigma: float = 1.0,
+                     low_frac: float = 0.1, high_frac: float = 0.2) -> list:
+    """Leaves (u0, w0, side) over the patch grid (min_side = 1 patch): Canny on the field
+    edge-padded to a multiple of max_side, quad-tree, leaves rooted in the padding dropped."""
+    f = pad_replicate(compression_field(z0, Hp, Wp), max_side).astype(F32)
+    leaves = quadtree(canny(f, sigma, low_frac, high_frac), 1, max_side, threshold)
+    return [(u, w, s) for (u, w, s) in leaves if u < Hp and w < Wp]
+
+
+def compressed_forward(x_b: np.ndarray, pr, Wt: dict, E_scale: np.ndarray, leaves: list) -> np.ndarray:
+    """K5 for one sample, T = 1 tile, halo 0 (R41): z0 = the O3 embedding of every patch;
+    token of a leaf = mean of z0 over its patches inside the grid + E_scale[log2 side]; the
+    ViT blocks attend over the sample's compressed tokens; the head (O5) per token; every
+    patch takes its leaf's head output (nearest decompression); stitch (O6) and the
+    bilinear residual (O7).  Returns out [K, sH, sW]."""
+    from . import reslim_tiles as O
+    p, P, K = pr.patch, pr.P, pr.K
+    Hp, Wp = pr.H // p, pr.W // p
+    tile = O.plan_tiles(Hp, Wp, 1, 1, 0)[0]
+    z0 = O.embed_tile(O.gather_tile(x_b, tile, p), tile, p, Wt, pr.heads)
+    zg = z0.reshape(Hp, Wp, -1)
+    toks = []
+    for u, w, s in leaves:
+        blk = zg[u:min(u + s, Hp), w:min(w + s, Wp)].reshape(-1, zg.shape[2])
+        toks.append(blk.mean(axis=0) + E_scale[int(round(math.log2(s)))])
+    z = np.array(toks)
+    for Lw in Wt["layers"]:
+        z = O.block(z, Lw, pr.heads)
+    g = O.head(z, Wt)                                   # [n, K P^2]
+    gp = np.zeros((Hp, Wp, g.shape[1]))
+    for (u, w, s), gi in zip(leaves, g):
+        gp[u:min(u + s, Hp), w:min(w + s, Wp)] = gi
+    out_vit = np.zeros((K, P * Hp, P * Wp))
+    O.stitch_tile(out_vit, gp.reshape(Hp * Wp, -1), tile, K, P)
+    return out_vit + O.residual_up(x_b, pr)

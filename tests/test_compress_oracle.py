@@ -207,3 +207,58 @@ def test_detokenize_single_patch_is_nearest_broadcast():
     got = K.detokenize(tok, [(0, 0, s)], m, C, s, s, Wd, bd, Ws, np.zeros(C))
     proj = (Wd @ tok[0] + bd).reshape(C, m, m)
     np.testing.assert_allclose(got[0], np.kron(proj[0], np.ones((s // m, s // m))), atol=1e-12)
+
+
+# ---------------------------------------------------------------- K5
+def _k5_problem(**kw):
+    from oracle import reslim_tiles as O
+    base = dict(H=16, W=24, V=2, K=2, scale=2, patch=2, tiles_y=1, tiles_x=1, halo=0, embed=16, depth=2, heads=2)
+    base.update(kw)
+    return O.Problem(**base)
+
+
+def _k5_data(pr, seed=3):
+    from workloads import get_config, make_input, make_weights
+    cfg = get_config("C1", H=pr.H, W=pr.W, V=pr.V, K=pr.K, scale=pr.scale, patch=pr.patch, tiles_y=1, tiles_x=1,
+                     halo=0, embed=pr.embed, depth=pr.depth, heads=pr.heads)
+    return make_input(cfg, batch=1, seed=seed)[0].astype(np.float64), make_weights(cfg, seed=seed).astype(np.float64)
+
+
+def test_compressed_forward_full_refinement_is_the_uncompressed_forward():
+    """R41: with every leaf one patch (threshold -1: every density > -1 splits) and a zero
+    level-0 scale embedding the compressed forward IS the T = 1 TILES forward."""
+    from oracle import reslim_tiles as O
+    pr = _k5_problem()
+    x, blob = _k5_data(pr)
+    Wt = pr.weights(blob)
+    Hp, Wp = pr.H // pr.patch, pr.W // pr.patch
+    tile = O.plan_tiles(Hp, Wp, 1, 1, 0)[0]
+    z0 = O.embed_tile(O.gather_tile(x, tile, pr.patch), tile, pr.patch, Wt, pr.heads)
+    leaves = K.partition_tokens(z0, Hp, Wp, 4, -1.0)
+    assert leaves == [(u, w, 1) for u in range(Hp) for w in range(Wp)]
+    E = np.zeros((3, pr.embed))
+    np.testing.assert_allclose(K.compressed_forward(x, pr, Wt, E, leaves), O.tiles_forward(x[None], blob, pr)[0],
+                               rtol=1e-12, atol=1e-12)
+
+
+def test_compressed_forward_coarse_leaves_decompress_piecewise():
+    """One leaf per max cell (threshold above every density): every patch of a leaf holds the
+    same head output (decompression is a nearest broadcast), so out - residual repeats the
+    same P x P pattern over the leaf's patches; the leaf clipped at the grid edge averages
+    only real patches (grid 8 x 12 patches, max_side 8: padded to 8 x 16)."""
+    from oracle import reslim_tiles as O
+    pr = _k5_problem()
+    x, blob = _k5_data(pr, seed=5)
+    Wt = pr.weights(blob)
+    Hp, Wp = pr.H // pr.patch, pr.W // pr.patch
+    tile = O.plan_tiles(Hp, Wp, 1, 1, 0)[0]
+    z0 = O.embed_tile(O.gather_tile(x, tile, pr.patch), tile, pr.patch, Wt, pr.heads)
+    leaves = K.partition_tokens(z0, Hp, Wp, 8, 2.0)
+    assert leaves == [(0, 0, 8), (0, 8, 8)]
+    E = np.random.default_rng(0).standard_normal((4, pr.embed))
+    out = K.compressed_forward(x, pr, Wt, E, leaves) - O.residual_up(x, pr)
+    P = pr.P
+    for (u, w, s) in leaves:
+        nu, nw = min(u + s, Hp) - u, min(w + s, Wp) - w
+        blk = out[:, u * P:(u + nu) * P, w * P:(w + nw) * P].reshape(pr.K, nu, P, nw, P)
+        np.testing.assert_allclose(blk, np.broadcast_to(blk[:, :1, :, :1, :], blk.shape), atol=1e-12)
