@@ -406,7 +406,7 @@ typedef struct {
   int32_t min_side;         /* the smallest leaf = the token's pooled size m (pixels) */
   int32_t max_side;         /* the quad-tree root cells */
   int32_t embed;            /* D: token width */
-  float threshold;          /* split iff edge pixels / area > threshold (R38) */
+  float threshold;          /* split iff edge pixels / area > threshold (R38); < 0: split to min_side */
   float sigma, low_frac, high_frac;   /* Canny (R37) */
 } orbit2_compress_config;
 
@@ -424,16 +424,43 @@ orbit2_status orbit2_compress_partition(const orbit2_compress_config *cfg, const
                                         int32_t *patches_dev, int32_t *offsets_dev, int32_t *n_host,
                                         void *stream);
 /* tokens_dev [n][D] = W_tok pool(leaf) + b_tok + e_scale[log2(side / min_side)]; w_tok
- * [D][C m m] (column (c m + i) m + j), b_tok [D], e_scale [k + 1][D] (R39). */
-orbit2_status orbit2_compress_tokenize(const orbit2_compress_config *cfg, const float *feat_dev,
-                                       const int32_t *patches_dev, int32_t n, const float *w_tok,
-                                       const float *b_tok, const float *e_scale, float *tokens_dev, void *stream);
+ * [D][C m m] (column (c m + i) m + j), b_tok [D], e_scale [k + 1][D] (R39).  One fp32 GEMM
+ * over all leaves (the scale embedding on one-hot columns); workspace as planned. */
+orbit2_status orbit2_compress_tokenize(const orbit2_compress_config *cfg, void *workspace_dev, size_t workspace_bytes,
+                                       const float *feat_dev, const int32_t *patches_dev, int32_t n,
+                                       const float *w_tok, const float *b_tok, const float *e_scale,
+                                       float *tokens_dev, void *stream);
 /* out_dev [B][C][H][W] = smooth(broadcast(W_dec t + b_dec)); w_dec [C m m][D], b_dec [C m m],
  * w_sm [C][C][3][3], b_sm [C]; work_dev: [B][C][H][W] scratch (R40). */
-orbit2_status orbit2_compress_detokenize(const orbit2_compress_config *cfg, const float *tokens_dev,
+orbit2_status orbit2_compress_detokenize(const orbit2_compress_config *cfg, void *workspace_dev,
+                                         size_t workspace_bytes, const float *tokens_dev,
                                          const int32_t *patches_dev, int32_t n, const float *w_dec,
                                          const float *b_dec, const float *w_sm, const float *b_sm,
                                          float *work_dev, float *out_dev, void *stream);
+
+/* The Reslim forward on compressed tokens (R41): z0 = the patch embedding of every patch
+ * (O2, O3); the compression field = z0 averaged over its D channels on the patch grid
+ * (edge-padded to a multiple of max_side); leaves = orbit2_compress_partition of that field
+ * with min_side = 1 patch (leaves rooted in the padding dropped); token = mean of z0 over
+ * the leaf's patches + e_scale[log2 side]; the ViT blocks attend over each sample's
+ * tokens; LN_f + head per token; every patch of a leaf gets its token's head output in
+ * tile_out ([B][Hp Wp][K P^2] bf16, the layout of a one-tile orbit2_reslim_forward), which
+ * orbit2_stitch turns into the field.  The context must be BF16, one tile (tiles 1 x 1),
+ * halo 0, one rank, without var_agg / dec_hidden / res_hidden (E_UNSUPPORTED otherwise).
+ * Synchronises the stream once per hysteresis pass and once for the token count. */
+typedef struct {
+  int32_t max_side;         /* quad-tree root cells (patches), a power of two >= 2 */
+  float threshold, sigma, low_frac, high_frac;   /* R37 / R38 */
+} orbit2_compression;
+/* workspace bytes of orbit2_compressed_forward; *levels = log2(max_side) + 1 rows of e_scale */
+orbit2_status orbit2_compressed_plan(void *ctx, const orbit2_compression *cp, int64_t *workspace_bytes,
+                                     int32_t *levels);
+/* e_scale_dev [levels][D] fp32; leaves_dev (nullable) receives the leaves [n][4] (image, u0,
+ * w0, side in patches); *n_tokens_host the token count. */
+orbit2_status orbit2_compressed_forward(void *ctx, const void *packed_w, const float *input_dev,
+                                        const orbit2_compression *cp, const float *e_scale_dev, void *workspace_dev,
+                                        size_t workspace_bytes, void *tile_out_dev, int32_t *leaves_dev,
+                                        int32_t *n_tokens_host, void *stream);
 
 int64_t orbit2_launch_count(void *ctx);
 

@@ -5,14 +5,16 @@
 //               hysteresis) -> per max_side cell a quad-tree of edge densities -> leaves
 //               compacted in (image, row, col) order
 //   tokenize  : each leaf average-pooled to min_side^2 per channel, linear embedding + the
-//               leaf level's scale embedding
-//   detokenize: linear projection, nearest-neighbour broadcast over the leaf, 3x3 smoothing
+//               leaf level's scale embedding (one fp32 GEMM over all leaves)
+//   detokenize: linear projection (one fp32 GEMM), nearest-neighbour broadcast over the
+//               leaf, 3x3 smoothing
 //
 // The Canny decision is boolean, so its arithmetic is the oracle's: float32 with every
 // product and sum rounded separately (__fmul_rn / __fadd_rn: no contraction into FMA),
 // correctly rounded sqrt, the same summation order.  HBM-bound stencils: one thread per
 // pixel, coalesced rows; hysteresis propagates inside 32 x 32 shared-memory tiles and
 // repeats over the field until nothing changes (host loop on a device flag).
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -162,7 +164,9 @@ __global__ void __launch_bounds__(HT * 8) hyst_kernel(uint8_t* __restrict__ lab,
 // shared memory, then every min cell walks down from the max cell (split iff side > min
 // and count > thr * area, in double) and flags the leaf at its top-left min cell.
 __global__ void quadtree_kernel(const uint8_t* __restrict__ lab, int H, int W, int mn, int levels, double thr,
-                                int32_t* __restrict__ flag) {
+                                int hr, int wr, int32_t* __restrict__ flag) {
+  // hr x wr: the min cells of the real field (the rest is edge padding): leaves whose
+  // top-left cell lies in the padding are not emitted
   extern __shared__ int cnt[];           // pyramid: level l has (R >> l)^2 entries
   const int R = 1 << (levels - 1);       // min cells per max-cell side
   const int b = blockIdx.z;
@@ -204,7 +208,8 @@ __global__ void quadtree_kernel(const uint8_t* __restrict__ lab, int H, int W, i
       const int c = lvl[l][(cy >> l) * n + (cx >> l)];
       if (!((double)c > thr * (double)side * (double)side)) break;
     }
-    const bool origin = ((cy & ((1 << l) - 1)) == 0) && ((cx & ((1 << l) - 1)) == 0);
+    const bool origin = ((cy & ((1 << l) - 1)) == 0) && ((cx & ((1 << l) - 1)) == 0) && cy0 + cy < hr &&
+                        cx0 + cx < wr;
     flag[((int64_t)b * Hc + cy0 + cy) * Wc + cx0 + cx] = origin ? (mn << l) : 0;
   }
 }
@@ -274,56 +279,53 @@ __global__ void scatter_kernel(const int32_t* __restrict__ flag, int64_t n, cons
   }
 }
 
-// tokens: one block per leaf; pooled [C][m][m] in shared memory, then D dot products
-__global__ void tokenize_kernel(const float* __restrict__ feat, const int32_t* __restrict__ patches, int C, int H,
-                                int W, int m, int D, const float* __restrict__ wt, const float* __restrict__ bt,
-                                const float* __restrict__ es, float* __restrict__ tok) {
-  extern __shared__ float pooled[];   // C m m
-  const int32_t* p = patches + (int64_t)blockIdx.x * 4;
+// tokens as one GEMM: the pooled leaf row [C m m | one-hot(level)] times [W_tok | E_scale^T]
+// (the scale embedding rides on the one-hot columns), + b_tok.  One warp per leaf here.
+__global__ void pool_kernel(const float* __restrict__ feat, const int32_t* __restrict__ patches, int n, int C, int H,
+                            int W, int m, int levels, float* __restrict__ rows, int ldr) {
+  const int leaf = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (leaf >= n) return;
+  const int32_t* p = patches + (int64_t)leaf * 4;
   const int b = p[0], r = p[1], c = p[2], s = p[3];
   const int f = s / m, K = C * m * m;
   const float inv = 1.f / (float)(f * f);
-  for (int e = threadIdx.x; e < K; e += blockDim.x) {
+  float* row = rows + (int64_t)leaf * ldr;
+  for (int e = lane; e < K; e += 32) {
     const int ch = e / (m * m), ij = e - ch * m * m, i = ij / m, j = ij - i * m;
     const float* src = feat + (((int64_t)b * C + ch) * H + r + i * f) * W + c + j * f;
     float acc = 0.f;
     for (int yy = 0; yy < f; ++yy)
       for (int xx = 0; xx < f; ++xx) acc += __ldg(src + (int64_t)yy * W + xx);
-    pooled[e] = acc * inv;
+    row[e] = acc * inv;
   }
-  __syncthreads();
   int lvl = 0;
   while ((m << lvl) < s) ++lvl;
-  for (int o = threadIdx.x; o < D; o += blockDim.x) {
-    const float* w = wt + (int64_t)o * K;
-    float acc = 0.f;
-    for (int k = 0; k < K; ++k) acc = fmaf(__ldg(w + k), pooled[k], acc);
-    tok[(int64_t)blockIdx.x * D + o] = acc + __ldg(bt + o) + __ldg(es + (int64_t)lvl * D + o);
+  for (int e = lane; e < levels; e += 32) row[K + e] = e == lvl ? 1.f : 0.f;
+}
+
+// W_ext [D][K + levels] = [W_tok | E_scale^T]
+__global__ void wext_kernel(const float* __restrict__ wt, const float* __restrict__ es, int D, int K, int levels,
+                            float* __restrict__ wext) {
+  const int ld = K + levels;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)D * ld;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int o = (int)(e / ld), k = (int)(e - (int64_t)o * ld);
+    wext[e] = k < K ? wt[(int64_t)o * K + k] : es[(int64_t)(k - K) * D + o];
   }
 }
 
-// decompression: one block per leaf: proj [C m m] = W_dec t + b_dec, nearest broadcast
-__global__ void detokenize_kernel(const float* __restrict__ tok, const int32_t* __restrict__ patches, int C, int H,
-                                  int W, int m, int D, const float* __restrict__ wd, const float* __restrict__ bd,
-                                  float* __restrict__ img) {
-  extern __shared__ float proj[];   // C m m
+// decompression: proj rows [n][C m m] (one GEMM) broadcast nearest over each leaf
+__global__ void broadcast_kernel(const float* __restrict__ proj, const int32_t* __restrict__ patches, int C, int H,
+                                 int W, int m, float* __restrict__ img) {
   const int32_t* p = patches + (int64_t)blockIdx.x * 4;
   const int b = p[0], r = p[1], c = p[2], s = p[3];
-  const int K = C * m * m;
-  const float* t = tok + (int64_t)blockIdx.x * D;
-  for (int o = threadIdx.x; o < K; o += blockDim.x) {
-    const float* w = wd + (int64_t)o * D;
-    float acc = 0.f;
-    for (int k = 0; k < D; ++k) acc = fmaf(__ldg(w + k), __ldg(t + k), acc);
-    proj[o] = acc + __ldg(bd + o);
-  }
-  __syncthreads();
+  const float* pr = proj + (int64_t)blockIdx.x * C * m * m;
   const int64_t px = (int64_t)C * s * s;
   for (int64_t e = threadIdx.x; e < px; e += blockDim.x) {
     const int ch = (int)(e / ((int64_t)s * s));
     const int rem = (int)(e - (int64_t)ch * s * s);
     const int y = rem / s, x = rem - y * s;
-    img[(((int64_t)b * C + ch) * H + r + y) * W + c + x] = proj[(ch * m + (y * m) / s) * m + (x * m) / s];
+    img[(((int64_t)b * C + ch) * H + r + y) * W + c + x] = __ldg(pr + (ch * m + (y * m) / s) * m + (x * m) / s);
   }
 }
 
@@ -353,6 +355,56 @@ __global__ void smooth_kernel(const float* __restrict__ in, const float* __restr
 }
 
 }  // namespace
+
+// ---- R41: compression inside the Reslim forward (patch grid, min_side = 1 patch) ----
+// f[b][u][w] = mean_d z0[b Hp Wp + u Wp + w][d] on the padded grid (edge replication)
+__global__ void cfield_kernel(const float* __restrict__ z0, int B, int Hp, int Wp, int D, int Hq, int Wq,
+                              float* __restrict__ f) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int64_t total = (int64_t)B * Hq * Wq;
+  if (warp >= total) return;
+  const int b = (int)(warp / ((int64_t)Hq * Wq));
+  const int rem = (int)(warp - (int64_t)b * Hq * Wq);
+  const int u = min(rem / Wq, Hp - 1), w = min(rem % Wq, Wp - 1);
+  const float* row = z0 + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * D;
+  float s = 0.f;
+  for (int d = lane; d < D; d += 32) s += row[d];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) f[warp] = s / D;
+}
+
+// token of a leaf = mean of z0 over its patches inside the grid + E_scale[log2 side]
+__global__ void ctoken_kernel(const float* __restrict__ z0, const int32_t* __restrict__ leaves, int Hp, int Wp, int D,
+                              const float* __restrict__ es, float* __restrict__ tok) {
+  const int32_t* p = leaves + (int64_t)blockIdx.x * 4;
+  const int b = p[0], u0 = p[1], w0 = p[2], s = p[3];
+  const int u1 = min(u0 + s, Hp), w1 = min(w0 + s, Wp);
+  const float inv = 1.f / (float)((u1 - u0) * (w1 - w0));
+  int lvl = 0;
+  while ((1 << lvl) < s) ++lvl;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int u = u0; u < u1; ++u)
+      for (int w = w0; w < w1; ++w) acc += __ldg(z0 + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * D + d);
+    tok[(int64_t)blockIdx.x * D + d] = acc * inv + __ldg(es + (int64_t)lvl * D + d);
+  }
+}
+
+// decompression: every patch of a leaf inside the grid gets the leaf's head output row
+__global__ void decompress_kernel(const __nv_bfloat16* __restrict__ g, const int32_t* __restrict__ leaves, int Hp,
+                                  int Wp, int Nh, __nv_bfloat16* __restrict__ tile_out) {
+  const int32_t* p = leaves + (int64_t)blockIdx.x * 4;
+  const int b = p[0], u0 = p[1], w0 = p[2], s = p[3];
+  const int u1 = min(u0 + s, Hp), w1 = min(w0 + s, Wp);
+  const int nw = w1 - w0, npatch = (u1 - u0) * nw, n8 = Nh / 8;
+  const uint4* src = reinterpret_cast<const uint4*>(g + (int64_t)blockIdx.x * Nh);
+  for (int e = threadIdx.x; e < npatch * n8; e += blockDim.x) {
+    const int q = e / n8, c = e - q * n8;
+    const int u = u0 + q / nw, w = w0 + q % nw;
+    reinterpret_cast<uint4*>(tile_out + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * Nh)[c] = __ldg(src + c);
+  }
+}
 
 bool compress_taps(float sigma, float* w, int* r) {
   const int rr = (int)std::ceil(3.0 * sigma);
@@ -390,14 +442,18 @@ void launch_canny(const float* img, float* tmp, float* tmp2, float* mag, uint8_t
 }
 
 void launch_quadtree(const uint8_t* lab, int32_t* flag, int32_t* bsum, int32_t* total, int32_t* patches,
-                     int32_t* offsets, int B, int H, int W, int mn, int mx, double thr, cudaStream_t st) {
+                     int32_t* offsets, int B, int H, int W, int mn, int mx, double thr, cudaStream_t st, int hr,
+                     int wr) {
+  if (hr <= 0) hr = H / mn;
+  if (wr <= 0) wr = W / mn;
   int levels = 1;
   while ((mn << (levels - 1)) < mx) ++levels;
   const int R = 1 << (levels - 1);
   int words = 0;
   for (int l = 0; l < levels; ++l) words += (R >> l) * (R >> l);
   const dim3 grid(W / mx, H / mx, B);
-  quadtree_kernel<<<grid, std::min(R * R, 1024), words * sizeof(int), st>>>(lab, H, W, mn, levels, thr, flag);
+  quadtree_kernel<<<grid, std::min(R * R, 1024), words * sizeof(int), st>>>(lab, H, W, mn, levels, thr, hr, wr,
+                                                                            flag);
   const int64_t n = (int64_t)B * (H / mn) * (W / mn);
   const int64_t nb = (n + SCAN_B - 1) / SCAN_B;
   scan_blocks_kernel<<<(unsigned)nb, SCAN_B, 0, st>>>(flag, n, bsum);
@@ -410,17 +466,44 @@ void launch_edges(const uint8_t* lab, uint8_t* e, int64_t n, cudaStream_t st) {
 }
 
 void launch_tokenize(const float* feat, const int32_t* patches, int n, int C, int H, int W, int m, int D,
-                     const float* wt, const float* bt, const float* es, float* tok, cudaStream_t st) {
+                     int levels, const float* wt, const float* bt, const float* es, float* rows, float* wext,
+                     float* tok, cudaStream_t st) {
+  const int K = C * m * m, ld = K + levels;
+  wext_kernel<<<(unsigned)std::min<int64_t>(((int64_t)D * ld + 255) / 256, 1024), 256, 0, st>>>(wt, es, D, K, levels,
+                                                                                            wext);
   if (n <= 0) return;
-  tokenize_kernel<<<n, 256, C * m * m * sizeof(float), st>>>(feat, patches, C, H, W, m, D, wt, bt, es, tok);
+  pool_kernel<<<(n + 7) / 8, 256, 0, st>>>(feat, patches, n, C, H, W, m, levels, rows, ld);
+  EpiParams ep{};
+  ep.M = n; ep.N = D; ep.bias = bt; ep.C = tok; ep.ldc = D;
+  launch_sgemm(EPI_BIAS, rows, ld, wext, ld, n, D, ld, ep, st);
 }
 
 void launch_detokenize(const float* tok, const int32_t* patches, int n, int B, int C, int H, int W, int m, int D,
-                       const float* wd, const float* bd, const float* ws, const float* bs, float* work, float* out,
-                       cudaStream_t st) {
-  if (n > 0)
-    detokenize_kernel<<<n, 256, C * m * m * sizeof(float), st>>>(tok, patches, C, H, W, m, D, wd, bd, work);
+                       const float* wd, const float* bd, const float* ws, const float* bs, float* proj, float* work,
+                       float* out, cudaStream_t st) {
+  if (n > 0) {
+    const int K = C * m * m;
+    EpiParams ep{};
+    ep.M = n; ep.N = K; ep.bias = bd; ep.C = proj; ep.ldc = K;
+    launch_sgemm(EPI_BIAS, tok, D, wd, D, n, K, D, ep, st);
+    broadcast_kernel<<<n, 256, 0, st>>>(proj, patches, C, H, W, m, work);
+  }
   smooth_kernel<<<dim3((W + 127) / 128, H, B * C), 128, 0, st>>>(work, ws, bs, out, C, H, W);
+}
+
+void launch_cfield(const float* z0, int B, int Hp, int Wp, int D, int Hq, int Wq, float* f, cudaStream_t st) {
+  const int64_t warps = (int64_t)B * Hq * Wq;
+  cfield_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(z0, B, Hp, Wp, D, Hq, Wq, f);
+}
+
+void launch_ctokens(const float* z0, const int32_t* leaves, int n, int Hp, int Wp, int D, const float* es, float* tok,
+                    cudaStream_t st) {
+  if (n > 0) ctoken_kernel<<<n, std::min(D, 256), 0, st>>>(z0, leaves, Hp, Wp, D, es, tok);
+}
+
+void launch_decompress(const __nv_bfloat16* g, const int32_t* leaves, int n, int Hp, int Wp, int Nh,
+                       __nv_bfloat16* tile_out, cudaStream_t st) {
+  if (n > 0) decompress_kernel<<<n, 128, 0, st>>>(g, leaves, Hp, Wp, Nh, tile_out);
 }
 
 }  // namespace orbit2

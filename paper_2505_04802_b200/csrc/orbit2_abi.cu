@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -1323,7 +1324,10 @@ orbit2_status orbit2_train_backward(void* ctx, const void* packed_w, const float
  * Adaptive spatial compression (oracle/compress.py, R37-R40)
  * ---------------------------------------------------------------------------- */
 struct CompressLay {
-  int64_t tmp, tmp2, mag, dir, lab, gmax, changed, flag, bsum, total;
+  int64_t tmp, tmp2, mag, dir, lab, gmax, changed, flag, bsum;
+  int64_t rows, wext, proj;   // tokenize / detokenize (C, embed > 0)
+  int64_t total;
+  int levels;
 };
 
 static orbit2_status compress_check(const orbit2_compress_config* c, CompressLay* ly) {
@@ -1337,8 +1341,8 @@ static orbit2_status compress_check(const orbit2_compress_config* c, CompressLay
   float w[32];
   int r = 0;
   if (!compress_taps(c->sigma, w, &r)) return set_err(ORBIT2_E_INVALID, "compress: sigma must be in (0, 8/3]");
-  if (!(c->low_frac > 0.f) || !(c->low_frac <= c->high_frac) || !(c->threshold >= 0.f))
-    return set_err(ORBIT2_E_INVALID, "compress: 0 < low_frac <= high_frac, threshold >= 0");
+  if (!(c->low_frac > 0.f) || !(c->low_frac <= c->high_frac) || !std::isfinite(c->threshold))
+    return set_err(ORBIT2_E_INVALID, "compress: 0 < low_frac <= high_frac, finite threshold");
   const int64_t n = (int64_t)c->batch * c->H * c->W;
   const int64_t cells = (int64_t)c->batch * (c->H / c->min_side) * (c->W / c->min_side);
   int64_t off = 0;
@@ -1352,6 +1356,13 @@ static orbit2_status compress_check(const orbit2_compress_config* c, CompressLay
   ly->changed = take(4);
   ly->flag = take(cells * 4);
   ly->bsum = take(((cells + 1023) / 1024) * 4);
+  ly->levels = 1;
+  while ((c->min_side << (ly->levels - 1)) < c->max_side) ++ly->levels;
+  const int64_t K = (int64_t)std::max(c->C, 0) * c->min_side * c->min_side;
+  const int64_t D = std::max(c->embed, 0);
+  ly->rows = take(cells * (K + ly->levels) * 4);
+  ly->wext = take(D * (K + ly->levels) * 4);
+  ly->proj = take(cells * K * 4);
   ly->total = off;
   return ORBIT2_OK;
 }
@@ -1395,40 +1406,307 @@ orbit2_status orbit2_compress_partition(const orbit2_compress_config* cfg, const
   return ORBIT2_OK;
 }
 
-orbit2_status orbit2_compress_tokenize(const orbit2_compress_config* cfg, const float* feat_dev,
-                                       const int32_t* patches_dev, int32_t n, const float* w_tok, const float* b_tok,
-                                       const float* e_scale, float* tokens_dev, void* stream) {
+orbit2_status orbit2_compress_tokenize(const orbit2_compress_config* cfg, void* ws, size_t ws_bytes,
+                                       const float* feat_dev, const int32_t* patches_dev, int32_t n,
+                                       const float* w_tok, const float* b_tok, const float* e_scale,
+                                       float* tokens_dev, void* stream) {
   CompressLay ly;
   ORBIT2_TRY(compress_check(cfg, &ly));
   if (cfg->C < 1 || cfg->embed < 1) return set_err(ORBIT2_E_INVALID, "compress tokenize: C, embed >= 1");
-  if (n < 0 || (n > 0 && (!feat_dev || !patches_dev || !w_tok || !b_tok || !e_scale || !tokens_dev)))
+  if (!ws || (int64_t)ws_bytes < ly.total) return set_err(ORBIT2_E_INVALID, "compress tokenize: workspace");
+  if (n < 0 || !w_tok || !e_scale || (n > 0 && (!feat_dev || !patches_dev || !b_tok || !tokens_dev)))
     return set_err(ORBIT2_E_INVALID, "compress tokenize: null pointer or n < 0");
-  if ((int64_t)cfg->C * cfg->min_side * cfg->min_side * 4 > 48 * 1024)
-    return set_err(ORBIT2_E_UNSUPPORTED, "compress tokenize: C * min_side^2 too large for shared memory");
+  if (n > (int64_t)cfg->batch * (cfg->H / cfg->min_side) * (cfg->W / cfg->min_side))
+    return set_err(ORBIT2_E_INVALID, "compress tokenize: n exceeds the leaf capacity");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  launch_tokenize(feat_dev, patches_dev, n, cfg->C, cfg->H, cfg->W, cfg->min_side, cfg->embed, w_tok, b_tok, e_scale,
-                  tokens_dev, st);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
+  launch_tokenize(feat_dev, patches_dev, n, cfg->C, cfg->H, cfg->W, cfg->min_side, cfg->embed, ly.levels, w_tok, b_tok,
+                  e_scale, reinterpret_cast<float*>(w8 + ly.rows), reinterpret_cast<float*>(w8 + ly.wext), tokens_dev,
+                  st);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ORBIT2_OK : set_err(ORBIT2_E_CUDA, std::string("compress tokenize: ") + cudaGetErrorString(e));
 }
 
-orbit2_status orbit2_compress_detokenize(const orbit2_compress_config* cfg, const float* tokens_dev,
-                                         const int32_t* patches_dev, int32_t n, const float* w_dec, const float* b_dec,
-                                         const float* w_sm, const float* b_sm, float* work_dev, float* out_dev,
-                                         void* stream) {
+orbit2_status orbit2_compress_detokenize(const orbit2_compress_config* cfg, void* ws, size_t ws_bytes,
+                                         const float* tokens_dev, const int32_t* patches_dev, int32_t n,
+                                         const float* w_dec, const float* b_dec, const float* w_sm, const float* b_sm,
+                                         float* work_dev, float* out_dev, void* stream) {
   CompressLay ly;
   ORBIT2_TRY(compress_check(cfg, &ly));
   if (cfg->C < 1 || cfg->embed < 1) return set_err(ORBIT2_E_INVALID, "compress detokenize: C, embed >= 1");
+  if (!ws || (int64_t)ws_bytes < ly.total) return set_err(ORBIT2_E_INVALID, "compress detokenize: workspace");
   if (n < 0 || !w_sm || !b_sm || !work_dev || !out_dev || (n > 0 && (!tokens_dev || !patches_dev || !w_dec || !b_dec)))
     return set_err(ORBIT2_E_INVALID, "compress detokenize: null pointer or n < 0");
-  if ((int64_t)cfg->C * cfg->min_side * cfg->min_side * 4 > 48 * 1024)
-    return set_err(ORBIT2_E_UNSUPPORTED, "compress detokenize: C * min_side^2 too large for shared memory");
+  if (n > (int64_t)cfg->batch * (cfg->H / cfg->min_side) * (cfg->W / cfg->min_side))
+    return set_err(ORBIT2_E_INVALID, "compress detokenize: n exceeds the leaf capacity");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  uint8_t* w8 = reinterpret_cast<uint8_t*>(ws);
   launch_detokenize(tokens_dev, patches_dev, n, cfg->batch, cfg->C, cfg->H, cfg->W, cfg->min_side, cfg->embed, w_dec,
-                    b_dec, w_sm, b_sm, work_dev, out_dev, st);
+                    b_dec, w_sm, b_sm, reinterpret_cast<float*>(w8 + ly.proj), work_dev, out_dev, st);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? ORBIT2_OK
                           : set_err(ORBIT2_E_CUDA, std::string("compress detokenize: ") + cudaGetErrorString(e));
+}
+
+/* ------------------------------------------------------------------------------
+ * The Reslim forward on compressed tokens (R41; oracle/compress.py K5)
+ * ---------------------------------------------------------------------------- */
+struct CfwdLay {
+  int64_t field, cws_part, leaves, offsets, tok, g, tiles, qblk, qpair, qpc, qg3, qg3c, core_row, total;
+  int64_t part_bytes, cap, tabcap;
+  int Hq, Wq;
+};
+
+static orbit2_status cfwd_layout(const Ctx* c, const orbit2_compression* cp, CfwdLay* L,
+                                 orbit2_compress_config* cc) {
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  if (!cp) return set_err(ORBIT2_E_INVALID, "compression: null");
+  if (cf.precision != ORBIT2_BF16 || p.info.n_tiles != 1 || cf.halo != 0 || cf.world_size != 1 || cf.var_agg ||
+      cf.dec_hidden || cf.res_hidden)
+    return set_err(ORBIT2_E_UNSUPPORTED, "compressed forward: a BF16 context with one tile, halo 0, one rank, "
+                                         "no var_agg / dec_hidden / res_hidden (R41)");
+  const int mx = cp->max_side;
+  L->Hq = (int)round_up(p.Hp, mx);
+  L->Wq = (int)round_up(p.Wp, mx);
+  *cc = orbit2_compress_config{cf.batch, L->Hq, L->Wq, 1, 1, mx, p.D, cp->threshold, cp->sigma, cp->low_frac,
+                               cp->high_frac};
+  int64_t ws = 0, maxp = 0;
+  ORBIT2_TRY(orbit2_compress_plan(cc, &ws, &maxp));
+  const int64_t B = cf.batch;
+  L->cap = maxp;                                         // leaves (upper bound)
+  L->tabcap = L->cap / 128 + 2 * B + 2;                  // 128-token blocks of all images
+  int64_t off = 0;
+  auto take = [&](int64_t b) { int64_t o = off; off = round_up(off + b, 256); return o; };
+  L->field = take(B * L->Hq * L->Wq * 4);
+  L->part_bytes = ws;
+  L->cws_part = take(ws);
+  L->leaves = take(L->cap * 16);
+  L->offsets = take((B + 1) * 4);
+  L->tok = take(L->cap * p.D * 4);
+  L->g = take(L->cap * round_up(p.Nh, 8) * 2);
+  L->tiles = take((B + 1) * (int64_t)sizeof(DevTile));
+  L->qblk = take(L->tabcap * 4);
+  L->qpair = take(L->tabcap * 4);
+  L->qpc = take(L->tabcap * 4);
+  L->qg3 = take(L->tabcap * 4);
+  L->qg3c = take(L->tabcap * 4);
+  L->core_row = take(4);
+  L->total = off;
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_compressed_plan(void* ctx, const orbit2_compression* cp, int64_t* workspace_bytes,
+                                     int32_t* levels) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  CfwdLay L;
+  orbit2_compress_config cc;
+  ORBIT2_TRY(cfwd_layout(c, cp, &L, &cc));
+  if (workspace_bytes) *workspace_bytes = L.total;
+  if (levels) {
+    int l = 1;
+    while ((1 << (l - 1)) < cp->max_side) ++l;
+    *levels = l;
+  }
+  return ORBIT2_OK;
+}
+
+orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const float* input_dev,
+                                        const orbit2_compression* cp, const float* e_scale_dev, void* cws,
+                                        size_t cws_bytes, void* tile_out_dev, int32_t* leaves_dev,
+                                        int32_t* n_tokens_host, void* stream) {
+  Ctx* c = reinterpret_cast<Ctx*>(ctx);
+  if (!c) return set_err(ORBIT2_E_INVALID, "ctx: null");
+  CfwdLay L;
+  orbit2_compress_config cc;
+  ORBIT2_TRY(cfwd_layout(c, cp, &L, &cc));
+  if (!packed_w || !input_dev || !e_scale_dev || !cws || !tile_out_dev || !aligned16(cws) || !aligned16(tile_out_dev))
+    return set_err(ORBIT2_E_INVALID, "compressed forward: null or unaligned pointer");
+  if ((int64_t)cws_bytes < L.total) return set_err(ORBIT2_E_INVALID, "compressed forward: workspace < planned");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const Plan& p = c->plan;
+  const orbit2_config& cf = p.cfg;
+  const Layout& ly = p.lay;
+  const WeightLayout& w = c->wl;
+  typedef __nv_bfloat16 bf16;
+  const uint8_t* W8 = reinterpret_cast<const uint8_t*>(packed_w);
+  auto wf = [&](int64_t off) { return reinterpret_cast<const float*>(W8 + off); };
+  uint8_t* cw = reinterpret_cast<uint8_t*>(cws);
+  const int B = cf.batch, Hp = p.Hp, Wp = p.Wp;
+  const int64_t D = p.D, F = 4LL * p.D, mrow = ly.mrow;
+  // 1-2: gather + patch embedding (O2, O3) of every patch: z0 = the ctx's z
+  const Chunk ch = make_chunk(p, 0, 1);
+  const ChunkDev cd = chunk_dev(c, ch);
+  const int64_t M0 = (int64_t)B * ch.chunk_tokens;
+  int2* rowinfo = c->at<int2>(ly.rowinfo);
+  float* z = c->at<float>(ly.z);
+  bf16* patches = c->at<bf16>(ly.patches);
+  ORBIT2_TRY(run(c, "tile_gather", st, [&] {
+    launch_gather<bf16>(input_dev, patches, rowinfo, cd, B, cf.V, cf.H, cf.W, cf.patch, p.Din, ly.din_pad,
+                        p.max_pad_h, st);
+    return true;
+  }));
+  {
+    EpiParams emb{};
+    emb.M = (int32_t)M0; emb.N = (int32_t)D; emb.bias = wf(w.bias_e); emb.C = z; emb.ldc = D;
+    emb.rowinfo = rowinfo; emb.pos_u = c->at<float>(ly.pos_u); emb.pos_w = c->at<float>(ly.pos_w);
+    emb.pos_off = cf.halo; emb.half = (int32_t)(D / 2);
+    GemmOperand a{patches, mrow, ly.din_pad, 0}, b{W8 + w.w_e, D, ly.din_pad};
+    ORBIT2_TRY(run(c, "embed_gemm", st, [&] { return launch_gemm_tc(EPI_EMBED, 0, a, b, M0, D, ly.din_pad, emb, st); }));
+  }
+  // 3: the compression field and its partition (Canny + quad-tree over the patch grid)
+  float* field = reinterpret_cast<float*>(cw + L.field);
+  ORBIT2_TRY(run(c, "compress_field", st, [&] {
+    launch_cfield(z, B, Hp, Wp, (int)D, L.Hq, L.Wq, field, st);
+    return true;
+  }));
+  int32_t* leaves = reinterpret_cast<int32_t*>(cw + L.leaves);
+  int32_t* offsets = reinterpret_cast<int32_t*>(cw + L.offsets);
+  {
+    CompressLay cl;
+    ORBIT2_TRY(compress_check(&cc, &cl));
+    uint8_t* pw = cw + L.cws_part;
+    int passes = 0;
+    ORBIT2_TRY(run(c, "compress_partition", st, [&] {
+      launch_canny(field, reinterpret_cast<float*>(pw + cl.tmp), reinterpret_cast<float*>(pw + cl.tmp2),
+                   reinterpret_cast<float*>(pw + cl.mag), pw + cl.dir, pw + cl.lab,
+                   reinterpret_cast<unsigned*>(pw + cl.gmax), reinterpret_cast<int*>(pw + cl.changed), B, L.Hq, L.Wq,
+                   cc.sigma, cc.low_frac, cc.high_frac, st, &passes);
+      launch_quadtree(pw + cl.lab, reinterpret_cast<int32_t*>(pw + cl.flag), reinterpret_cast<int32_t*>(pw + cl.bsum),
+                      offsets + B, leaves, offsets, B, L.Hq, L.Wq, 1, cp->max_side, (double)cc.threshold, st, Hp, Wp);
+      return true;
+    }));
+  }
+  std::vector<int32_t> off(B + 1);
+  cudaError_t e = cudaMemcpyAsync(off.data(), offsets, (B + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e));
+  const int32_t n = off[B];
+  if (n_tokens_host) *n_tokens_host = n;
+  if (leaves_dev) {
+    e = cudaMemcpyAsync(leaves_dev, leaves, (size_t)n * 16, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e));
+  }
+  // 4: tokens (then into the ctx's z: the blocks below use its buffers)
+  float* tok = reinterpret_cast<float*>(cw + L.tok);
+  ORBIT2_TRY(run(c, "compress_tokens", st, [&] {
+    launch_ctokens(z, leaves, n, Hp, Wp, (int)D, e_scale_dev, tok, st);
+    return true;
+  }));
+  e = cudaMemcpyAsync(z, tok, (size_t)n * D * 4, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e));
+  // the images as the "tiles" of one call: per image its compressed tokens
+  std::vector<DevTile> dt(B + 1);
+  std::vector<int32_t> qblk, qpair, qg3;
+  int32_t qb = 0, qp = 0;
+  for (int b = 0; b <= B; ++b) {
+    DevTile t{};
+    const int32_t nb = b < B ? off[b + 1] - off[b] : 0;
+    t.n_tokens = t.n_core = nb;
+    t.tok_off = t.core_off = off[std::min(b, B)];
+    t.qb_off = qb;
+    t.qp_off = qp;
+    t.pad_h = t.core_h = t.out_h = 1;
+    t.pad_w = t.core_w = t.out_w = nb;
+    dt[b] = t;
+    if (b == B) break;
+    const int32_t nqb = (nb + 127) / 128;
+    for (int32_t i = 0; i < nqb; ++i) qblk.push_back(b);
+    for (int32_t i = 0; i < (nqb + 1) / 2; ++i) qpair.push_back(b);
+    for (int32_t i = 0; i < nqb; i += 3) qg3.push_back((b << 16) | (i << 2) | (std::min(3, nqb - i) - 1));
+    qb += nqb;
+    qp += (nqb + 1) / 2;
+  }
+  if ((int64_t)qblk.size() > L.tabcap || B >= 32768)
+    return set_err(ORBIT2_E_CAPACITY, "compressed forward: work-list capacity");
+  e = cudaMemcpy(cw + L.tiles, dt.data(), dt.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !qblk.empty()) e = cudaMemcpy(cw + L.qblk, qblk.data(), qblk.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !qpair.empty())
+    e = cudaMemcpy(cw + L.qpair, qpair.data(), qpair.size() * 4, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && !qg3.empty()) e = cudaMemcpy(cw + L.qg3, qg3.data(), qg3.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward tables: ") + cudaGetErrorString(e));
+  ChunkDev cc2{};
+  cc2.tiles = reinterpret_cast<const DevTile*>(cw + L.tiles);
+  cc2.tb = 0; cc2.tc = B; cc2.tok0 = 0; cc2.core0 = 0; cc2.chunk_tokens = n; cc2.chunk_core = n;
+  cc2.qb0 = 0; cc2.nqb = qb; cc2.qp0 = 0; cc2.nqp = qp;
+  cc2.qblk_tile = reinterpret_cast<const int32_t*>(cw + L.qblk);
+  cc2.qpair_tile = reinterpret_cast<const int32_t*>(cw + L.qpair);
+  cc2.qpair_core = reinterpret_cast<const int32_t*>(cw + L.qpc);
+  cc2.qg3 = reinterpret_cast<const int32_t*>(cw + L.qg3);
+  cc2.qg3c = reinterpret_cast<const int32_t*>(cw + L.qg3c);
+  cc2.qg0 = 0; cc2.nqg = (int32_t)qg3.size(); cc2.qgc0 = 0; cc2.nqgc = 0; cc2.qc0 = 0; cc2.nqc = 0;
+  cc2.core_pairs = 0;
+  cc2.core_row = reinterpret_cast<const int32_t*>(cw + L.core_row);
+  // 5: the blocks over the compressed tokens (unfused LN; block tail at D = 256)
+  const int64_t M = n;
+  bf16* xn = c->at<bf16>(ly.xn);
+  bf16* qkv = c->at<bf16>(ly.qkv);
+  bf16* ao = c->at<bf16>(ly.ao);
+  bf16* hid = c->at<bf16>(ly.hid);
+  if (mrow > M) {
+    e = cudaMemsetAsync(qkv + M * 3 * D, 0, (size_t)(mrow - M) * 3 * D * sizeof(bf16), st);
+    if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("memset: ") + cudaGetErrorString(e));
+  }
+  auto gemm = [&](const char* name, int epi, int out_bf, const void* A, int64_t lda, int64_t wo, int64_t nn,
+                  int64_t k, EpiParams ep) {
+    GemmOperand a{A, mrow, lda, 0}, b{W8 + wo, nn, k};
+    ep.M = (int32_t)M;
+    ep.N = (int32_t)nn;
+    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, M, nn, k, ep, st); });
+  };
+  const bool tail_fused = D == 256;
+  for (int l = 0; l < cf.depth && M > 0; ++l) {
+    const LayerW& Lw = w.layers[l];
+    if (!(tail_fused && l > 0))
+      ORBIT2_TRY(run(c, "layernorm", st, [&] {
+        launch_layernorm<bf16>(z, wf(Lw.ln1_g), wf(Lw.ln1_b), xn, M, (int)D, nullptr, st);
+        return true;
+      }));
+    EpiParams ep{};
+    ep.bias = wf(Lw.b_qkv); ep.C = qkv; ep.ldc = 3 * D;
+    ORBIT2_TRY(gemm("qkv_gemm", EPI_BIAS, 1, xn, D, Lw.w_qkv, 3 * D, D, ep));
+    ORBIT2_TRY(run(c, "tile_attention", st, [&] {
+      return launch_attention_tc(qkv, mrow, ao, cc2, 1, (int)D, cf.heads, p.d, st);
+    }));
+    if (tail_fused) {
+      const bool nxt = l + 1 < cf.depth;
+      ORBIT2_TRY(run(c, "block_tail", st, [&] {
+        return launch_block_tail(ao, mrow, W8 + Lw.w_o, wf(Lw.b_o), wf(Lw.ln2_g), wf(Lw.ln2_b), W8 + Lw.w_1,
+                                 wf(Lw.b_1), W8 + Lw.w_2, wf(Lw.b_2), z, M, (int)D,
+                                 nxt ? wf(w.layers[l + 1].ln1_g) : nullptr, nxt ? wf(w.layers[l + 1].ln1_b) : nullptr,
+                                 xn, nullptr, 0, st);
+      }));
+      continue;
+    }
+    ep = EpiParams{}; ep.bias = wf(Lw.b_o); ep.C = z; ep.ldc = D;
+    ORBIT2_TRY(gemm("oproj_gemm", EPI_RESID, 0, ao, D, Lw.w_o, D, D, ep));
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<bf16>(z, wf(Lw.ln2_g), wf(Lw.ln2_b), xn, M, (int)D, nullptr, st);
+      return true;
+    }));
+    ep = EpiParams{}; ep.bias = wf(Lw.b_1); ep.C = hid; ep.ldc = F;
+    ORBIT2_TRY(gemm("mlp_up_gemm", EPI_GELU, 1, xn, D, Lw.w_1, F, D, ep));
+    ep = EpiParams{}; ep.bias = wf(Lw.b_2); ep.C = z; ep.ldc = D;
+    ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, hid, F, Lw.w_2, D, F, ep));
+  }
+  // 6: LN_f + head per compressed token, decompression to every patch (tile_out: one tile)
+  bf16* hin = c->at<bf16>(ly.hin);
+  bf16* g = reinterpret_cast<bf16*>(cw + L.g);
+  if (M > 0) {
+    ORBIT2_TRY(run(c, "layernorm", st, [&] {
+      launch_layernorm<bf16>(z, wf(w.lnf_g), wf(w.lnf_b), hin, M, (int)D, nullptr, st);
+      return true;
+    }));
+    EpiParams ep{};
+    ep.bias = wf(w.b_h); ep.C = g; ep.ldc = p.Nh; ep.M = (int32_t)M; ep.N = p.Nh;
+    GemmOperand a{hin, ly.mcore, D, 0}, b{W8 + w.w_h, p.Nh, D};
+    ORBIT2_TRY(run(c, "head_gemm", st, [&] { return launch_gemm_tc(EPI_BIAS, 1, a, b, M, p.Nh, D, ep, st); }));
+  }
+  return run(c, "decompress", st, [&] {
+    launch_decompress(g, leaves, n, Hp, Wp, p.Nh, reinterpret_cast<bf16*>(tile_out_dev), st);
+    return true;
+  });
 }
 
 }  // extern "C"

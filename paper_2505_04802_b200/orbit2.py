@@ -59,6 +59,10 @@ class orbit2_compress_config(C.Structure):
         (n, C.c_float) for n in ("threshold", "sigma", "low_frac", "high_frac")]
 
 
+class orbit2_compression(C.Structure):
+    _fields_ = [("max_side", C.c_int32)] + [(n, C.c_float) for n in ("threshold", "sigma", "low_frac", "high_frac")]
+
+
 class orbit2_rect(C.Structure):
     _fields_ = [(n, C.c_int32) for n in ("y0", "y1", "x0", "x1")]
 
@@ -101,9 +105,13 @@ def _load():
         "orbit2_compress_plan": (i32, [C.POINTER(orbit2_compress_config), C.POINTER(i64), C.POINTER(i64)]),
         "orbit2_compress_partition": (i32, [C.POINTER(orbit2_compress_config), vp, vp, C.c_size_t, vp, vp, vp,
                                             C.POINTER(i32), vp]),
-        "orbit2_compress_tokenize": (i32, [C.POINTER(orbit2_compress_config), vp, vp, i32, vp, vp, vp, vp, vp]),
-        "orbit2_compress_detokenize": (i32, [C.POINTER(orbit2_compress_config), vp, vp, i32, vp, vp, vp, vp, vp,
-                                             vp, vp]),
+        "orbit2_compress_tokenize": (i32, [C.POINTER(orbit2_compress_config), vp, C.c_size_t, vp, vp, i32, vp,
+                                           vp, vp, vp, vp]),
+        "orbit2_compress_detokenize": (i32, [C.POINTER(orbit2_compress_config), vp, C.c_size_t, vp, vp, i32, vp,
+                                             vp, vp, vp, vp, vp, vp]),
+        "orbit2_compressed_plan": (i32, [vp, C.POINTER(orbit2_compression), C.POINTER(i64), C.POINTER(i32)]),
+        "orbit2_compressed_forward": (i32, [vp, vp, vp, C.POINTER(orbit2_compression), vp, vp, C.c_size_t, vp, vp,
+                                            C.POINTER(i32), vp]),
         "orbit2_launch_count": (i64, [vp]),
         "orbit2_set_profiling": (i32, [vp, i32]),
         "orbit2_kernel_times": (i32, [vp, C.POINTER(C.c_char_p), C.POINTER(i64), C.POINTER(C.c_double), i32]),
@@ -125,7 +133,7 @@ EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orb
             "orbit2_train_plan", "orbit2_train_bind", "orbit2_train_prepare", "orbit2_train_forward",
             "orbit2_loss", "orbit2_train_backward",
             "orbit2_compress_plan", "orbit2_compress_partition", "orbit2_compress_tokenize",
-            "orbit2_compress_detokenize",
+            "orbit2_compress_detokenize", "orbit2_compressed_plan", "orbit2_compressed_forward",
             "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
             "orbit2_destroy")
 
@@ -544,6 +552,35 @@ class Context:
         grad = torch.empty(self.info.canonical_weight_count, dtype=torch.float32, device=self.device)
         return tile_out, out, dout, loss_dev, grad
 
+    # -- the forward on compressed tokens (R41; include/orbit2.h) -------------------
+    def compressed_forward(self, packed, x_dev, e_scale, max_side=8, threshold=0.1, sigma=1.0, low_frac=0.1,
+                           high_frac=0.2, out=None, stream=None):
+        """-> (out [B, K, sH, sW], leaves [n, 4] (image, u0, w0, side in patches), n)."""
+        import torch
+        _req(x_dev, torch.float32, "x_dev")
+        _req(e_scale, torch.float32, "e_scale")
+        cp = orbit2_compression(max_side, threshold, sigma, low_frac, high_frac)
+        ws, lv = C.c_int64(), C.c_int32()
+        _check(lib.orbit2_compressed_plan(self.handle, C.byref(cp), C.byref(ws), C.byref(lv)),
+               "orbit2_compressed_plan")
+        if e_scale.shape[0] < lv.value:
+            raise ValueError(f"e_scale needs {lv.value} rows")
+        if getattr(self, "_cws", None) is None or self._cws.numel() < ws.value:
+            self._cws = torch.empty(max(ws.value, 16), dtype=torch.uint8, device=self.device)
+        cfg = self.cfg
+        cap = cfg.batch * self.info.core_tokens_per_sample
+        leaves = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=self.device)
+        tile_out = self.tile_out_buffer()
+        if out is None:
+            out = torch.empty((cfg.batch, cfg.K, self.sH, self.sW), dtype=torch.float32, device=self.device)
+        n = C.c_int32()
+        with _on_device(self.device):
+            _check(lib.orbit2_compressed_forward(self.handle, _ptr(packed), _ptr(x_dev), C.byref(cp), _ptr(e_scale),
+                                                 _ptr(self._cws), self._cws.numel(), _ptr(tile_out), _ptr(leaves),
+                                                 C.byref(n), _stream(stream)), "orbit2_compressed_forward")
+        self.orbit2_stitch(tile_out, x_dev, 0, 1, out, stream)
+        return out, leaves[:n.value], n.value
+
     # -- instrumentation ------------------------------------------------------
     def launch_count(self) -> int:
         return int(lib.orbit2_launch_count(self.handle))
@@ -596,7 +633,8 @@ class Compressor:
             _req(t, torch.float32, name)
         tok = torch.empty((max(n, 1), self.cfg.embed), dtype=torch.float32, device=self.device)
         with _on_device(self.device):
-            _check(lib.orbit2_compress_tokenize(_ct.byref(self.cfg), _ptr(feat_dev), _ptr(patches), n, _ptr(w_tok),
+            _check(lib.orbit2_compress_tokenize(_ct.byref(self.cfg), _ptr(self.workspace), self.workspace.numel(),
+                                                _ptr(feat_dev), _ptr(patches), n, _ptr(w_tok),
                                                 _ptr(b_tok), _ptr(e_scale), _ptr(tok), _stream(stream)),
                    "orbit2_compress_tokenize")
         return tok[:n]
@@ -607,7 +645,8 @@ class Compressor:
         out = torch.empty((cf.batch, cf.C, cf.H, cf.W), dtype=torch.float32, device=self.device)
         work = torch.empty_like(out)
         with _on_device(self.device):
-            _check(lib.orbit2_compress_detokenize(_ct.byref(cf), _ptr(tokens), _ptr(patches), n, _ptr(w_dec),
+            _check(lib.orbit2_compress_detokenize(_ct.byref(cf), _ptr(self.workspace), self.workspace.numel(),
+                                                  _ptr(tokens), _ptr(patches), n, _ptr(w_dec),
                                                   _ptr(b_dec), _ptr(w_sm), _ptr(b_sm), _ptr(work), _ptr(out),
                                                   _stream(stream)), "orbit2_compress_detokenize")
         return out

@@ -99,3 +99,60 @@ def test_partition_full_c2_field_batch():
             cover[r:r + s, c:c + s] += 1
         assert (cover == 1).all()
     assert n < B * (H // 2) * (W // 2)
+
+
+def _cf_setup(B=2, depth=2, embed=256, heads=4, seed=8):
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from oracle import reslim_tiles as O
+    from workloads import make_weights
+    w = get_config("C2", batch=B, H=48, W=80, tiles_y=1, tiles_x=1, halo=0, depth=depth, embed=embed, heads=heads)
+    pr = O.Problem.from_config(w)
+    x = make_input(w, batch=B, seed=seed)
+    blob = make_weights(w, seed=seed)
+    ctx = o2.Context(o2.config_from(w, precision=o2.BF16))
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    return w, pr, x, blob, ctx, packed
+
+
+def test_compressed_forward_matches_oracle_on_its_leaves():
+    """R41 end to end: the GPU forward on compressed tokens (24 x 40 patch grid, max_side 8)
+    against oracle K5 given the same leaves (the leaves are an integer result of the GPU's bf16 embedding; the partition
+    kernels are pinned bit-exact above), bf16 tolerance 2e-2 of the field per variable."""
+    import torch
+    from oracle import reslim_tiles as O
+    from tests.gpu_helpers import rel_err
+    w, pr, x, blob, ctx, packed = _cf_setup()
+    levels = 4
+    E = (0.1 * np.random.default_rng(1).standard_normal((levels, w.embed))).astype(np.float32)
+    out, leaves, n = ctx.compressed_forward(packed, torch.from_numpy(x).cuda(), torch.from_numpy(E).cuda(),
+                                            max_side=8, threshold=0.12, sigma=1.0)
+    torch.cuda.synchronize()
+    out, lv = out.cpu().numpy(), leaves.cpu().numpy()
+    Hp, Wp = w.H // w.patch, w.W // w.patch
+    assert n < w.batch * Hp * Wp                       # something was compressed
+    Wt = pr.weights(blob)
+    for b in range(w.batch):
+        lb = [tuple(int(v) for v in r[1:]) for r in lv if r[0] == b]
+        cover = np.zeros((Hp, Wp), np.int32)
+        for u, v, s in lb:
+            cover[u:u + s, v:v + s] += 1
+        assert (cover == 1).all()
+        ref = K.compressed_forward(x[b].astype(np.float64), pr, Wt, E.astype(np.float64), lb)
+        assert rel_err(out[b], ref) <= 2e-2, rel_err(out[b], ref)
+
+
+def test_compressed_forward_full_refinement_equals_uncompressed():
+    """Threshold -1 (every density > -1: every leaf one patch) and E_scale[0] = 0: the
+    compressed forward equals the uncompressed one-tile forward (both on the GPU, bf16;
+    the only differences are rounding order: 1e-2 of the field)."""
+    import torch
+    from tests.gpu_helpers import rel_err
+    w, pr, x, blob, ctx, packed = _cf_setup(seed=9)
+    E = np.zeros((4, w.embed), np.float32)
+    xd = torch.from_numpy(x).cuda()
+    out_c, leaves, n = ctx.compressed_forward(packed, xd, torch.from_numpy(E).cuda(), max_side=8, threshold=-1.0)
+    out_u = ctx.forward(packed, xd)
+    torch.cuda.synchronize()
+    assert n == w.batch * (w.H // w.patch) * (w.W // w.patch)
+    assert rel_err(out_c.cpu().numpy(), out_u.cpu().numpy()) <= 1e-2
