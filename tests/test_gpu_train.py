@@ -163,3 +163,15 @@ def test_train_step_c2_full_size_properties():
     got_bh = grad[off:off + K * P * P]
     # dG is rounded to bf16 before the column sums: 2^-9 relative per term
     np.testing.assert_allclose(got_bh, want_bh, rtol=5e-3, atol=5e-3 * np.abs(want_bh).max())
+
+
+def test_train_step_wide_model_matches_oracle():
+    """The C3 / C4 model width (D = 1024, 16 heads of 64: the LayerNorm backward's 8-float4
+    rows, weight-gradient tiles of 256 columns over K = 1024) on a small grid, one block."""
+    w, pr, blob, x, y = _problem_and_data(H=16, W=24, embed=1024, heads=16, depth=1, batch=1, seed=11)
+    lam, delta = 0.05, 0.02
+    _, loss, grad, _ = _gpu_step(w, x, y, blob, lam, delta)
+    ref_loss, ref_grad = T.train_step_grads(x.astype(np.float64), y.astype(np.float64), blob.astype(np.float64),
+                                            pr, lam, delta)
+    assert abs(loss.mean() - ref_loss) <= LOSS_TOL * abs(ref_loss)
+    _check_grads(pr, grad, ref_grad)
