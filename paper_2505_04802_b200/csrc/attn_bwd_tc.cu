@@ -23,8 +23,8 @@
 //   warps 4..11   : thread = key row r (TMEM lane r), warps 4-7 query half A, 8-11 half B
 //                   (two warps per SM sub-partition): P^T_h, dS^T_h of block j,
 //                   P^T_h -> TMEM (bf16 pairs), dS^T_h -> smem (SW128, double-buffered);
-//                   at the item's end dV (half A warps), dK c (half B warps) -> dqkv (bf16)
-//   warps 12..15  : thread = query row of block j: dQ_j c -> smem -> TMA reduce-add into dq_acc (fp32)
+//   warps 12..15  : thread = query row of block j: dQ_j c -> smem -> TMA reduce-add into dq_acc (fp32);
+//                   at the item's end (thread = key row) dV and dK c -> dqkv (bf16)
 // The same TMA tile [128 rows][64 bf16] (one SW128 atom) is a K-major operand when
 // the contraction runs over head dim and an MN-major one when it runs over tokens.
 #include <cuda.h>
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc::mbar_init(dq_full, 1);
     tc::mbar_init(dq_free, 128);
     tc::mbar_init(dkv_full, 1);
-    tc::mbar_init(dkv_free, 256);
+    tc::mbar_init(dkv_free, 128);
     for (int s = 0; s < IRING; ++s) {
       tc::mbar_init(&it_full[s], 1);
       tc::mbar_init(&it_empty[s], 13);   // MMA warp + 8 softmax warps + 4 dQ warps
@@ -216,25 +216,29 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t k_addr = tc::smem_u32(sK), v_addr = tc::smem_u32(sV), q_addr = tc::smem_u32(sQ);
     const uint32_t do_addr = tc::smem_u32(sDO), ds_addr = tc::smem_u32(sDS);
     uint32_t li = 0, gq = 0;
-    auto issue_sp = [&](uint32_t kv, uint32_t s, int h) {   // elected lane
+    // live = the half holds a valid query (a last block of <= 64 queries skips half B's MMAs;
+    // its commits still arrive so every barrier phase advances)
+    auto issue_sp = [&](uint32_t kv, uint32_t s, int h, bool live) {   // elected lane
       const uint64_t kd = tc::sdesc(k_addr + kv * TILE, 16, 1024, tc::SW_128B);
       const uint64_t vd = tc::sdesc(v_addr + kv * TILE, 16, 1024, tc::SW_128B);
       const uint64_t qd = tc::sdesc(q_addr + s * TILE + h * (TILE / 2), 16, 1024, tc::SW_128B);
       const uint64_t dod = tc::sdesc(do_addr + s * TILE + h * (TILE / 2), 16, 1024, tc::SW_128B);
+      if (live) {
 #pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk)
-        tc::mma_bf16_ss(tmem + h * 128 + C_S, kd + kk * 2, qd + kk * 2, id_sp, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16_ss(tmem + h * 128 + C_S, kd + kk * 2, qd + kk * 2, id_sp, kk > 0);
 #pragma unroll
-      for (int kk = 0; kk < DH / 16; ++kk)
-        tc::mma_bf16_ss(tmem + h * 128 + C_DP, vd + kk * 2, dod + kk * 2, id_sp, kk > 0);
+        for (int kk = 0; kk < DH / 16; ++kk)
+          tc::mma_bf16_ss(tmem + h * 128 + C_DP, vd + kk * 2, dod + kk * 2, id_sp, kk > 0);
+      }
       tc::mma_commit(&s_full[h]);
     };
-    auto issue_g = [&](uint32_t kv, uint32_t s, uint32_t dsb, int h, bool first) {   // elected lane
+    auto issue_g = [&](uint32_t kv, uint32_t s, uint32_t dsb, int h, bool first, bool live) {   // elected lane
       const uint64_t q_mn = tc::sdesc(q_addr + s * TILE + h * (TILE / 2), TILE, 1024, tc::SW_128B);
       const uint64_t do_mn = tc::sdesc(do_addr + s * TILE + h * (TILE / 2), TILE, 1024, tc::SW_128B);
       const uint64_t ds_k = tc::sdesc(ds_addr + dsb * DS_BYTES + h * TILE, 16, 1024, tc::SW_128B);
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {                  // K = 64 queries of the half, 16 per MMA
+      for (int kk = 0; kk < 4 && live; ++kk) {          // K = 64 queries of the half, 16 per MMA
         const uint32_t acc = (!first || kk > 0) ? 1u : 0u;
         const uint32_t mn_adv = (uint32_t)(kk * 2048) >> 4;
         tc::mma_bf16_ts(tmem + C_DV, tmem + C_P + h * 32 + kk * 8, do_mn + mn_adv, id_kb, acc);
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           tc::mbar_wait(&q_full[s], (gq / QST) & 1);
           tc::tc_fence_after();
           if (tc::elect_one()) {
-            issue_sp(kv, s, 0);
-            issue_sp(kv, s, 1);
+            issue_sp(kv, s, 0, true);
+            issue_sp(kv, s, 1, j * 128 + 64 < it.n);
           }
           __syncwarp();
         }
@@ -274,8 +278,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (more) tc::mbar_wait(&q_full[s1], ((gq + 1) / QST) & 1);
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          issue_g(kv, s, dsb, 0, j == 0);
-          if (more) issue_sp(kv, s1, 0);
+          issue_g(kv, s, dsb, 0, j == 0, true);
+          if (more) issue_sp(kv, s1, 0, true);
         }
         __syncwarp();
         // half B of block j
@@ -283,14 +287,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (gq > 0) tc::mbar_wait(dq_free, (gq - 1) & 1);              // dQ of the last block read
         tc::tc_fence_after();
         if (tc::elect_one()) {
-          issue_g(kv, s, dsb, 1, false);
+          issue_g(kv, s, dsb, 1, false, j * 128 + 64 < it.n);
           tc::mma_commit(dq_full);
           tc::mma_commit(&q_empty[s]);
           if (!more) {
             tc::mma_commit(dkv_full);
             tc::mma_commit(&kv_empty[kv]);
           } else {
-            issue_sp(kv, s1, 1);
+            issue_sp(kv, s1, 1, (j + 1) * 128 + 64 < it.n);
           }
         }
         __syncwarp();
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t sb = lb + h * 128;
 #pragma unroll
         for (int c0 = 0; c0 < 64; c0 += 16) {
+          if (qv <= 0) break;                              // a half without queries: nothing to do
           uint32_t sr[16], dr[16];
           tc::tmem_ld16(sb + C_S + c0, sr);
           tc::tmem_ld16(sb + C_DP + c0, dr);
@@ -390,28 +395,6 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[h]);
       }
-      // item end: half A's warps write dV, half B's write dK c (this key row) -> dqkv
-      tc::mbar_wait(dkv_full, li & 1);
-      tc::tc_fence_after();
-#pragma unroll
-      for (int c0 = 0; c0 < DH; c0 += 32) {
-        uint32_t v[32];
-        tc::tmem_ld32(lb + (h ? C_DK : C_DV) + c0, v);
-        tc::tmem_ld_wait();
-        if (kval) {
-          const float f = h ? cs : 1.f;
-          __nv_bfloat16* dst = dqkv + (it.base + it.k0 + r) * (int64_t)(3 * D) + (h ? D : 2 * D) + it.h * DH + c0;
-#pragma unroll
-          for (int u = 0; u < 4; ++u)
-            reinterpret_cast<uint4*>(dst)[u] =
-                make_uint4(tc::pack_bf16(__uint_as_float(v[8 * u]) * f, __uint_as_float(v[8 * u + 1]) * f),
-                           tc::pack_bf16(__uint_as_float(v[8 * u + 2]) * f, __uint_as_float(v[8 * u + 3]) * f),
-                           tc::pack_bf16(__uint_as_float(v[8 * u + 4]) * f, __uint_as_float(v[8 * u + 5]) * f),
-                           tc::pack_bf16(__uint_as_float(v[8 * u + 6]) * f, __uint_as_float(v[8 * u + 7]) * f));
-        }
-      }
-      tc::tc_fence_before();
-      tc::mbar_arrive(dkv_free);
     }
   } else if (warp >= 12) {
     // ---------------- dQ_j c -> dq_acc: staged in smem, one TMA reduce-add per 32 x 32 box ----------------
@@ -450,6 +433,34 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      // item end (off the softmax warps' path): dV and dK c of key row r -> dqkv
+      const int r = q4 * 32 + lane;
+      const bool kval = it.k0 + r < it.n;
+      tc::mbar_wait(dkv_full, li & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {             // 0: dV, 1: dK
+#pragma unroll
+        for (int c0 = 0; c0 < DH; c0 += 32) {
+          uint32_t v[32];
+          tc::tmem_ld32(lb + (part ? C_DK : C_DV) + c0, v);
+          tc::tmem_ld_wait();
+          if (kval) {
+            const float f = part ? cs : 1.f;
+            __nv_bfloat16* dst = dqkv + (it.base + it.k0 + r) * (int64_t)(3 * D) + (part ? D : 2 * D) +
+                                 it.h * DH + c0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+              reinterpret_cast<uint4*>(dst)[u] =
+                  make_uint4(tc::pack_bf16(__uint_as_float(v[8 * u]) * f, __uint_as_float(v[8 * u + 1]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 2]) * f, __uint_as_float(v[8 * u + 3]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 4]) * f, __uint_as_float(v[8 * u + 5]) * f),
+                             tc::pack_bf16(__uint_as_float(v[8 * u + 6]) * f, __uint_as_float(v[8 * u + 7]) * f));
+          }
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(dkv_free);
     }
     if (lane == 0) tc::bulk_wait_all();
   }

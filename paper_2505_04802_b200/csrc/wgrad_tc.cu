@@ -176,10 +176,21 @@ bool launch_bn(const GemmOperand& A, const GemmOperand& X, int64_t M, int N, int
   const int n_tiles_n = (N + 127) / 128, n_tiles_k = (Kc + BN - 1) / BN;
   const int tiles = n_tiles_n * n_tiles_k;
   const int64_t chunks = (M + TK - 1) / TK;
-  // split the token range so the grid is at most two full waves (tiles x splits <= 2 x SMs:
-  // no partial third wave), each split >= 16 chunks (1024 tokens)
-  int64_t splits = std::max<int64_t>(1, (2LL * num_sms()) / tiles);
-  splits = std::max<int64_t>(1, std::min<int64_t>(splits, chunks / 16));
+  // split the token range (each split >= 16 chunks = 1024 tokens) so the grid fills whole
+  // waves of SMs as well as possible: tiles x splits / (SMs x waves), the fewest splits among
+  // the best (fewer fp32 atomics); at most 16 splits
+  const int sms = num_sms();
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(16, chunks / 16));
+  int64_t splits = 1;
+  double best = 0.0;
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const int64_t ctas = tiles * sp, waves = (ctas + sms - 1) / sms;
+    const double eff = (double)ctas / (double)(waves * sms);
+    if (eff > best + 0.02) {
+      best = eff;
+      splits = sp;
+    }
+  }
   if (splits > 65535) splits = 65535;
   dim3 grid((unsigned)tiles, (unsigned)splits);
   wgrad_kernel<BN, STAGES><<<grid, 256, C::SMEM, st>>>(ta, tb, out, ldo, N, Kc, M, n_tiles_k, chunks, (int)splits,
