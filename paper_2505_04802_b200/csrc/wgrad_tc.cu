@@ -178,9 +178,9 @@ bool launch_bn(const GemmOperand& A, const GemmOperand& X, int64_t M, int N, int
   const int64_t chunks = (M + TK - 1) / TK;
   // split the token range (each split >= 16 chunks = 1024 tokens) so the grid fills whole
   // waves of SMs as well as possible: tiles x splits / (SMs x waves), the fewest splits among
-  // the best (fewer fp32 atomics); at most 16 splits
+  // the best (fewer fp32 atomics); at most max(8 splits, 4 waves)
   const int sms = num_sms();
-  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(16, chunks / 16));
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 4LL * sms / tiles), chunks / 16));
   int64_t splits = 1;
   double best = 0.0;
   for (int64_t sp = 1; sp <= smax; ++sp) {
