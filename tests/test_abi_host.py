@@ -196,3 +196,30 @@ def test_variable_aggregation_config_counts(o2):
     assert info.canonical_weight_count == weight_count(w.replace(var_agg=0)) + V * D * 4 + V * D + D + 3 * (D * D + D)
     with pytest.raises(o2.Orbit2Error, match="var_agg"):
         o2.orbit2_tiles_plan(o2.config_from(w, var_agg=2))
+
+
+def test_compress_plan_validation_and_sizes(o2):
+    """orbit2_compress_plan (host only): sizes grow with the field; every invalid field is
+    rejected with E_INVALID and a message naming it (R37 / R38 constraints)."""
+    import ctypes as C
+    ws, mp = C.c_int64(), C.c_int64()
+
+    def plan(**kw):
+        base = dict(batch=2, H=64, W=96, C=3, min_side=2, max_side=16, embed=32, threshold=0.05, sigma=1.0,
+                    low_frac=0.1, high_frac=0.2)
+        base.update(kw)
+        cfg = o2.orbit2_compress_config(*[base[k] for k in ("batch", "H", "W", "C", "min_side", "max_side", "embed",
+                                                             "threshold", "sigma", "low_frac", "high_frac")])
+        return o2.lib.orbit2_compress_plan(C.byref(cfg), C.byref(ws), C.byref(mp)), o2.lib.orbit2_last_error().decode()
+
+    st, _ = plan()
+    assert st == o2.OK and mp.value == 2 * 32 * 48
+    w0 = ws.value
+    assert plan(H=128)[0] == o2.OK and ws.value > w0
+    for kw, word in [(dict(max_side=12), "max_side"), (dict(max_side=2), "max_side"), (dict(H=60), "multiples"),
+                     (dict(sigma=3.0), "sigma"), (dict(sigma=0.0), "sigma"), (dict(low_frac=0.3), "low_frac"),
+                     (dict(low_frac=0.0), "low_frac"), (dict(batch=0), "batch"), (dict(max_side=256), "max_side"),
+                     (dict(threshold=float("nan")), "threshold")]:
+        st, msg = plan(**kw)
+        assert st == o2.E_INVALID and word in msg, (kw, msg)
+    assert plan(threshold=-1.0)[0] == o2.OK          # < 0: split down to min_side
