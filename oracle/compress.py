@@ -291,3 +291,56 @@ def compressed_forward(x_b: np.ndarray, pr, Wt: dict, E_scale: np.ndarray, leave
     out_vit = np.zeros((K, P * Hp, P * Wp))
     O.stitch_tile(out_vit, gp.reshape(Hp * Wp, -1), tile, K, P)
     return out_vit + O.residual_up(x_b, pr)
+
+
+# ---------------------------------------------------------------------------
+# K6 compressed tokens inside TILES tiles (R42)
+# ---------------------------------------------------------------------------
+def tile_field_shape(tiles, max_side: int):
+    """(Hq, Wq): the largest padded rectangle over the tiles, rounded up to max_side (every
+    tile's field is edge-padded to this one shape)."""
+    hq = max(t.pad_h for t in tiles)
+    wq = max(t.pad_w for t in tiles)
+    return -(-hq // max_side) * max_side, -(-wq // max_side) * max_side
+
+
+def tile_leaves(z0: np.ndarray, tile, Hq: int, Wq: int, max_side: int, threshold: float, sigma: float = 1.0,
+                low_frac: float = 0.1, high_frac: float = 0.2) -> list:
+    """Leaves (u0, w0, side) of one tile in its padded-rectangle coordinates: Canny on the
+    channel-mean field of its z0 edge-padded to Hq x Wq, quad-tree, leaves rooted outside the
+    rectangle dropped."""
+    f = compression_field(z0, tile.pad_h, tile.pad_w)
+    f = np.pad(f, ((0, Hq - tile.pad_h), (0, Wq - tile.pad_w)), mode="edge").astype(F32)
+    leaves = quadtree(canny(f, sigma, low_frac, high_frac), 1, max_side, threshold)
+    return [(u, w, s) for (u, w, s) in leaves if u < tile.pad_h and w < tile.pad_w]
+
+
+def tiles_compressed_forward(x_b: np.ndarray, pr, Wt: dict, E_scale: np.ndarray, leaves_by_tile=None,
+                             max_side: int = 8, threshold: float = 0.1, sigma: float = 1.0):
+    """K6 for one sample (R42): every tile's padded rectangle compressed on its own (K5 within
+    the tile: field, quad-tree, pooled tokens + scale embedding), the blocks attend within the
+    tile over its compressed tokens, the head per token, decompression to the tile's CORE
+    patches only (the halo is discarded), stitch and residual.  Returns (out, leaves)."""
+    from . import reslim_tiles as O
+    p, P, K = pr.patch, pr.P, pr.K
+    tiles = pr.tiles()
+    Hq, Wq = tile_field_shape(tiles, max_side)
+    sH, sW = pr.scale * pr.H, pr.scale * pr.W
+    out_vit = np.zeros((K, sH, sW))
+    got = []
+    for ti, t in enumerate(tiles):
+        z0 = O.embed_tile(O.gather_tile(x_b, t, p), t, p, Wt, pr.heads)
+        lv = tile_leaves(z0, t, Hq, Wq, max_side, threshold, sigma) if leaves_by_tile is None else leaves_by_tile[ti]
+        got.append(lv)
+        zg = z0.reshape(t.pad_h, t.pad_w, -1)
+        z = np.array([zg[u:min(u + s, t.pad_h), w:min(w + s, t.pad_w)].reshape(-1, zg.shape[2]).mean(axis=0)
+                      + E_scale[int(round(math.log2(s)))] for (u, w, s) in lv])
+        for Lw in Wt["layers"]:
+            z = O.block(z, Lw, pr.heads)
+        g = O.head(z, Wt)
+        gp = np.zeros((t.pad_h, t.pad_w, g.shape[1]))
+        for (u, w, s), gi in zip(lv, g):
+            gp[u:min(u + s, t.pad_h), w:min(w + s, t.pad_w)] = gi
+        core = gp[t.core_y0 - t.pad_y0:t.core_y1 - t.pad_y0, t.core_x0 - t.pad_x0:t.core_x1 - t.pad_x0]
+        O.stitch_tile(out_vit, core.reshape(-1, g.shape[1]), t, K, P)
+    return out_vit + O.residual_up(x_b, pr), got

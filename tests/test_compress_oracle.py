@@ -262,3 +262,32 @@ def test_compressed_forward_coarse_leaves_decompress_piecewise():
         nu, nw = min(u + s, Hp) - u, min(w + s, Wp) - w
         blk = out[:, u * P:(u + nu) * P, w * P:(w + nw) * P].reshape(pr.K, nu, P, nw, P)
         np.testing.assert_allclose(blk, np.broadcast_to(blk[:, :1, :, :1, :], blk.shape), atol=1e-12)
+
+
+# ---------------------------------------------------------------- K6
+def test_tiles_compressed_forward_reductions():
+    """R42: (a) one tile, halo 0 == K5; (b) full refinement with a zero level-0 scale
+    embedding == the uncompressed TILES forward (2 x 2 tiles, halo 1: every tile's tokens
+    are its padded patches, the halo discarded after the blocks)."""
+    from oracle import reslim_tiles as O
+    pr1 = _k5_problem()
+    x, blob = _k5_data(pr1, seed=7)
+    Wt = pr1.weights(blob)
+    E = np.random.default_rng(2).standard_normal((4, pr1.embed))
+    out6, lv6 = K.tiles_compressed_forward(x, pr1, Wt, E, max_side=8, threshold=0.05)
+    np.testing.assert_allclose(out6, K.compressed_forward(x, pr1, Wt, E, lv6[0]), rtol=1e-12, atol=1e-12)
+    pr = _k5_problem(tiles_y=2, tiles_x=2, halo=1)
+    out, lv = K.tiles_compressed_forward(x, pr, Wt, np.zeros((4, pr.embed)), max_side=4, threshold=-1.0)
+    assert all(all(s == 1 for _, _, s in l) for l in lv)
+    np.testing.assert_allclose(out, O.tiles_forward(x[None], blob, pr)[0], rtol=1e-12, atol=1e-12)
+
+
+def test_tiles_compressed_leaves_cover_each_padded_rectangle():
+    pr = _k5_problem(tiles_y=2, tiles_x=3, halo=2)
+    x, blob = _k5_data(pr, seed=9)
+    _, lv = K.tiles_compressed_forward(x, pr, pr.weights(blob), np.zeros((4, pr.embed)), max_side=4, threshold=0.2)
+    for t, l in zip(pr.tiles(), lv):
+        cover = np.zeros((t.pad_h, t.pad_w), np.int32)
+        for u, w, s in l:
+            cover[u:u + s, w:w + s] += 1
+        assert (cover == 1).all()
