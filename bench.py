@@ -846,16 +846,25 @@ def run_compress(args, w, world, rank, local):
                       "min_side": mn, "max_side": mx, "threshold": thr, "sigma": sigma, "mode": "compress"},
            "tokens": n, "uniform_tokens": uniform, "compression_ratio": uniform / max(n, 1),
            "clocks": clk.summary(), "host_s_per_step": (time.perf_counter() - t0) / args.steps}
-    # the Reslim forward on compressed tokens (R41) vs the same one-tile forward uncompressed
-    # (the paper's compression rows run untiled, Tab. P:376-378): C2 model, max_side 8 patches
+    # the Reslim forward on compressed tokens vs the same forward uncompressed: one tile (R41,
+    # the paper's compression rows run untiled, Tab. P:376-378) and the C2 tiling (R42, every
+    # tile compressed on its own), C2 model, max_side 8 patches
     from workloads import make_weights
     Bf = min(B, 16)
-    wf = w.replace(batch=Bf, tiles_y=1, tiles_x=1, halo=0)
+    for key, wf in (("forward_on_compressed_tokens", w.replace(batch=Bf, tiles_y=1, tiles_x=1, halo=0)),
+                    ("forward_on_compressed_tokens_tiles", w.replace(batch=Bf))):
+        res[key] = _compressed_vs_uncompressed(o2, wf, Bf, D, thr, sigma, stream)
+    print(json.dumps(res), flush=True)
+
+
+def _compressed_vs_uncompressed(o2, wf, Bf, D, thr, sigma, stream):
+    import torch
+    from workloads import make_input, make_weights
     ctx = o2.Context(o2.config_from(wf, precision=o2.BF16))
     packed = ctx.prepare_weights(torch.from_numpy(make_weights(wf)).cuda())
     xf = torch.from_numpy(make_input(wf, batch=Bf)).cuda()
     Ef = torch.zeros((4, D), dtype=torch.float32, device="cuda")
-    outf = torch.empty((Bf, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
+    outf = torch.empty((Bf, wf.K, wf.scale * wf.H, wf.scale * wf.W), dtype=torch.float32, device="cuda")
     fwd = {}
     for name, fn in (("uncompressed", lambda: ctx.forward(packed, xf, out=outf)),
                      ("compressed", lambda: ctx.compressed_forward(packed, xf, Ef, max_side=8, threshold=thr,
@@ -872,13 +881,13 @@ def run_compress(args, w, world, rank, local):
         fwd[name] = {"ms_per_step": e0.elapsed_time(e1) / 3}
         if name == "compressed":
             fwd[name]["tokens"] = r[2]
-    fwd["uncompressed"]["tokens"] = Bf * (wf.H // wf.patch) * (wf.W // wf.patch)
+    fwd["uncompressed"]["tokens"] = Bf * ctx.info.local_tokens
     fwd["speedup"] = fwd["uncompressed"]["ms_per_step"] / fwd["compressed"]["ms_per_step"]
     fwd["token_reduction"] = fwd["uncompressed"]["tokens"] / max(fwd["compressed"]["tokens"], 1)
-    fwd["config"] = {"batch": Bf, "tiles": [1, 1], "halo": 0, "max_side_patches": 8, "threshold": thr, "sigma": sigma,
+    fwd["config"] = {"batch": Bf, "tiles": [wf.tiles_y, wf.tiles_x], "halo": wf.halo, "max_side_patches": 8,
+                     "threshold": thr, "sigma": sigma,
                      "note": "event time incl. the host syncs of the partition (hysteresis passes, token count)"}
-    res["forward_on_compressed_tokens"] = fwd
-    print(json.dumps(res), flush=True)
+    return fwd
 
 
 def relaunch_if_needed(args):

@@ -438,16 +438,20 @@ orbit2_status orbit2_compress_detokenize(const orbit2_compress_config *cfg, void
                                          const float *b_dec, const float *w_sm, const float *b_sm,
                                          float *work_dev, float *out_dev, void *stream);
 
-/* The Reslim forward on compressed tokens (R41): z0 = the patch embedding of every patch
- * (O2, O3); the compression field = z0 averaged over its D channels on the patch grid
- * (edge-padded to a multiple of max_side); leaves = orbit2_compress_partition of that field
- * with min_side = 1 patch (leaves rooted in the padding dropped); token = mean of z0 over
- * the leaf's patches + e_scale[log2 side]; the ViT blocks attend over each sample's
- * tokens; LN_f + head per token; every patch of a leaf gets its token's head output in
- * tile_out ([B][Hp Wp][K P^2] bf16, the layout of a one-tile orbit2_reslim_forward), which
- * orbit2_stitch turns into the field.  The context must be BF16, one tile (tiles 1 x 1),
- * halo 0, one rank, without var_agg / dec_hidden / res_hidden (E_UNSUPPORTED otherwise).
- * Synchronises the stream once per hysteresis pass and once for the token count. */
+/* The Reslim forward on compressed tokens (R41, R42), per (sample, tile) "image" i = b T + t
+ * of the T rank-local tiles: z0 = the patch embedding of every patch of the tile's padded
+ * rectangle (O2, O3); the compression field = z0 averaged over its D channels, edge-padded
+ * to one shape for all tiles (the largest padded rectangle rounded up to max_side); leaves =
+ * orbit2_compress_partition of that field with min_side = 1 patch (leaves rooted outside
+ * the rectangle dropped); token = mean of z0 over the leaf's rectangle patches +
+ * e_scale[log2 side]; the ViT blocks attend over each image's tokens (attention stays in the
+ * tile); LN_f + head per token; every CORE patch of a leaf gets its token's head
+ * output in tile_out ([B][core tokens of all local tiles][K P^2] bf16, the layout of
+ * orbit2_reslim_forward over every local tile), which orbit2_stitch turns into the field
+ * (the halo is discarded).  The context must be BF16 with one call over every
+ * rank-local tile (chunk_tiles = 0), without var_agg / dec_hidden / res_hidden
+ * (E_UNSUPPORTED otherwise).  Synchronises the stream once per hysteresis pass and once for
+ * the token count. */
 typedef struct {
   int32_t max_side;         /* quad-tree root cells (patches), a power of two >= 2 */
   float threshold, sigma, low_frac, high_frac;   /* R37 / R38 */
@@ -455,8 +459,8 @@ typedef struct {
 /* workspace bytes of orbit2_compressed_forward; *levels = log2(max_side) + 1 rows of e_scale */
 orbit2_status orbit2_compressed_plan(void *ctx, const orbit2_compression *cp, int64_t *workspace_bytes,
                                      int32_t *levels);
-/* e_scale_dev [levels][D] fp32; leaves_dev (nullable) receives the leaves [n][4] (image, u0,
- * w0, side in patches); *n_tokens_host the token count. */
+/* e_scale_dev [levels][D] fp32; leaves_dev (nullable) receives the leaves [n][4] (image
+ * b T + t, u0, w0 in the tile's padded rectangle, side; patches); *n_tokens_host the count. */
 orbit2_status orbit2_compressed_forward(void *ctx, const void *packed_w, const float *input_dev,
                                         const orbit2_compression *cp, const float *e_scale_dev, void *workspace_dev,
                                         size_t workspace_bytes, void *tile_out_dev, int32_t *leaves_dev,

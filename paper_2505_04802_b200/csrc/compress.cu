@@ -164,12 +164,16 @@ __global__ void __launch_bounds__(HT * 8) hyst_kernel(uint8_t* __restrict__ lab,
 // shared memory, then every min cell walks down from the max cell (split iff side > min
 // and count > thr * area, in double) and flags the leaf at its top-left min cell.
 __global__ void quadtree_kernel(const uint8_t* __restrict__ lab, int H, int W, int mn, int levels, double thr,
-                                int hr, int wr, int32_t* __restrict__ flag) {
-  // hr x wr: the min cells of the real field (the rest is edge padding): leaves whose
-  // top-left cell lies in the padding are not emitted
+                                int hr, int wr, const int32_t* __restrict__ ext, int32_t* __restrict__ flag) {
+  // hr x wr (or ext[2 b], ext[2 b + 1] per image): the min cells of the real field (the rest is
+  // edge padding): leaves whose top-left cell lies in the padding are not emitted
   extern __shared__ int cnt[];           // pyramid: level l has (R >> l)^2 entries
   const int R = 1 << (levels - 1);       // min cells per max-cell side
   const int b = blockIdx.z;
+  if (ext) {
+    hr = ext[2 * b];
+    wr = ext[2 * b + 1];
+  }
   const int cy0 = blockIdx.y * R, cx0 = blockIdx.x * R;   // first min cell of the max cell
   const int Wc = W / mn, Hc = H / mn;
   const uint8_t* img = lab + (int64_t)b * H * W;
@@ -356,17 +360,25 @@ __global__ void smooth_kernel(const float* __restrict__ in, const float* __restr
 
 }  // namespace
 
-// ---- R41: compression inside the Reslim forward (patch grid, min_side = 1 patch) ----
-// f[b][u][w] = mean_d z0[b Hp Wp + u Wp + w][d] on the padded grid (edge replication)
-__global__ void cfield_kernel(const float* __restrict__ z0, int B, int Hp, int Wp, int D, int Hq, int Wq,
+// ---- R41 / R42: compression inside the Reslim forward, per (sample, tile) image ----
+// image i = b T + t: the tile's padded rectangle (pad_h x pad_w patches) of sample b; its
+// z0 rows are b chunk_tokens + (tok_off - tok0) + u pad_w + w (the forward's packing)
+__device__ __forceinline__ int64_t z0_row(const ChunkDev& ch, const DevTile& t, int b, int u, int w) {
+  return (int64_t)b * ch.chunk_tokens + (t.tok_off - ch.tok0) + (int64_t)u * t.pad_w + w;
+}
+
+// f[i][y][x] = mean_d z0[row(i, min(y, pad_h - 1), min(x, pad_w - 1))][d]  (edge padding to Hq x Wq)
+__global__ void cfield_kernel(const float* __restrict__ z0, ChunkDev ch, int T, int B, int D, int Hq, int Wq,
                               float* __restrict__ f) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  const int64_t total = (int64_t)B * Hq * Wq;
-  if (warp >= total) return;
-  const int b = (int)(warp / ((int64_t)Hq * Wq));
-  const int rem = (int)(warp - (int64_t)b * Hq * Wq);
-  const int u = min(rem / Wq, Hp - 1), w = min(rem % Wq, Wp - 1);
-  const float* row = z0 + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * D;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= (int64_t)B * T * Hq * Wq) return;
+  const int img = (int)(warp / ((int64_t)Hq * Wq));
+  const int rem = (int)(warp - (int64_t)img * Hq * Wq);
+  const int b = img / T, ti = img - b * T;
+  const DevTile t = ch.tiles[ch.tb + ti];
+  const int u = min(rem / Wq, t.pad_h - 1), w = min(rem % Wq, t.pad_w - 1);
+  const float* row = z0 + z0_row(ch, t, b, u, w) * D;
   float s = 0.f;
   for (int d = lane; d < D; d += 32) s += row[d];
 #pragma unroll
@@ -374,35 +386,44 @@ __global__ void cfield_kernel(const float* __restrict__ z0, int B, int Hp, int W
   if (lane == 0) f[warp] = s / D;
 }
 
-// token of a leaf = mean of z0 over its patches inside the grid + E_scale[log2 side]
-__global__ void ctoken_kernel(const float* __restrict__ z0, const int32_t* __restrict__ leaves, int Hp, int Wp, int D,
-                              const float* __restrict__ es, float* __restrict__ tok) {
+// token of a leaf = mean of z0 over its patches inside the rectangle + E_scale[log2 side]
+__global__ void ctoken_kernel(const float* __restrict__ z0, ChunkDev ch, int T, const int32_t* __restrict__ leaves,
+                              int D, const float* __restrict__ es, float* __restrict__ tok) {
   const int32_t* p = leaves + (int64_t)blockIdx.x * 4;
-  const int b = p[0], u0 = p[1], w0 = p[2], s = p[3];
-  const int u1 = min(u0 + s, Hp), w1 = min(w0 + s, Wp);
+  const int img = p[0], u0 = p[1], w0 = p[2], s = p[3];
+  const int b = img / T;
+  const DevTile t = ch.tiles[ch.tb + img - b * T];
+  const int u1 = min(u0 + s, t.pad_h), w1 = min(w0 + s, t.pad_w);
   const float inv = 1.f / (float)((u1 - u0) * (w1 - w0));
   int lvl = 0;
   while ((1 << lvl) < s) ++lvl;
   for (int d = threadIdx.x; d < D; d += blockDim.x) {
     float acc = 0.f;
     for (int u = u0; u < u1; ++u)
-      for (int w = w0; w < w1; ++w) acc += __ldg(z0 + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * D + d);
+      for (int w = w0; w < w1; ++w) acc += __ldg(z0 + z0_row(ch, t, b, u, w) * D + d);
     tok[(int64_t)blockIdx.x * D + d] = acc * inv + __ldg(es + (int64_t)lvl * D + d);
   }
 }
 
-// decompression: every patch of a leaf inside the grid gets the leaf's head output row
-__global__ void decompress_kernel(const __nv_bfloat16* __restrict__ g, const int32_t* __restrict__ leaves, int Hp,
-                                  int Wp, int Nh, __nv_bfloat16* __restrict__ tile_out) {
+// decompression: every CORE patch of a leaf gets the leaf's head output row, at its row of
+// tile_out [B][chunk core tokens][Nh] (the halo patches are discarded)
+__global__ void decompress_kernel(const __nv_bfloat16* __restrict__ g, ChunkDev ch, int T,
+                                  const int32_t* __restrict__ leaves, int Nh, __nv_bfloat16* __restrict__ tile_out) {
   const int32_t* p = leaves + (int64_t)blockIdx.x * 4;
-  const int b = p[0], u0 = p[1], w0 = p[2], s = p[3];
-  const int u1 = min(u0 + s, Hp), w1 = min(w0 + s, Wp);
+  const int img = p[0], s = p[3];
+  const int b = img / T;
+  const DevTile t = ch.tiles[ch.tb + img - b * T];
+  const int cy = t.core_y0 - t.pad_y0, cx = t.core_x0 - t.pad_x0;   // core rect in rectangle coordinates
+  const int u0 = max(p[1], cy), w0 = max(p[2], cx);
+  const int u1 = min(p[1] + s, cy + t.core_h), w1 = min(p[2] + s, cx + t.core_w);
+  if (u1 <= u0 || w1 <= w0) return;
   const int nw = w1 - w0, npatch = (u1 - u0) * nw, n8 = Nh / 8;
   const uint4* src = reinterpret_cast<const uint4*>(g + (int64_t)blockIdx.x * Nh);
+  const int64_t base = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0);
   for (int e = threadIdx.x; e < npatch * n8; e += blockDim.x) {
     const int q = e / n8, c = e - q * n8;
     const int u = u0 + q / nw, w = w0 + q % nw;
-    reinterpret_cast<uint4*>(tile_out + ((int64_t)b * Hp * Wp + (int64_t)u * Wp + w) * Nh)[c] = __ldg(src + c);
+    reinterpret_cast<uint4*>(tile_out + (base + (int64_t)(u - cy) * t.core_w + (w - cx)) * Nh)[c] = __ldg(src + c);
   }
 }
 
@@ -443,7 +464,7 @@ void launch_canny(const float* img, float* tmp, float* tmp2, float* mag, uint8_t
 
 void launch_quadtree(const uint8_t* lab, int32_t* flag, int32_t* bsum, int32_t* total, int32_t* patches,
                      int32_t* offsets, int B, int H, int W, int mn, int mx, double thr, cudaStream_t st, int hr,
-                     int wr) {
+                     int wr, const int32_t* ext) {
   if (hr <= 0) hr = H / mn;
   if (wr <= 0) wr = W / mn;
   int levels = 1;
@@ -453,7 +474,7 @@ void launch_quadtree(const uint8_t* lab, int32_t* flag, int32_t* bsum, int32_t* 
   for (int l = 0; l < levels; ++l) words += (R >> l) * (R >> l);
   const dim3 grid(W / mx, H / mx, B);
   quadtree_kernel<<<grid, std::min(R * R, 1024), words * sizeof(int), st>>>(lab, H, W, mn, levels, thr, hr, wr,
-                                                                            flag);
+                                                                            ext, flag);
   const int64_t n = (int64_t)B * (H / mn) * (W / mn);
   const int64_t nb = (n + SCAN_B - 1) / SCAN_B;
   scan_blocks_kernel<<<(unsigned)nb, SCAN_B, 0, st>>>(flag, n, bsum);
@@ -491,19 +512,20 @@ void launch_detokenize(const float* tok, const int32_t* patches, int n, int B, i
   smooth_kernel<<<dim3((W + 127) / 128, H, B * C), 128, 0, st>>>(work, ws, bs, out, C, H, W);
 }
 
-void launch_cfield(const float* z0, int B, int Hp, int Wp, int D, int Hq, int Wq, float* f, cudaStream_t st) {
-  const int64_t warps = (int64_t)B * Hq * Wq;
-  cfield_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(z0, B, Hp, Wp, D, Hq, Wq, f);
+void launch_cfield(const float* z0, const ChunkDev& ch, int T, int B, int D, int Hq, int Wq, float* f,
+                   cudaStream_t st) {
+  const int64_t warps = (int64_t)B * T * Hq * Wq;
+  cfield_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(z0, ch, T, B, D, Hq, Wq, f);
 }
 
-void launch_ctokens(const float* z0, const int32_t* leaves, int n, int Hp, int Wp, int D, const float* es, float* tok,
-                    cudaStream_t st) {
-  if (n > 0) ctoken_kernel<<<n, std::min(D, 256), 0, st>>>(z0, leaves, Hp, Wp, D, es, tok);
+void launch_ctokens(const float* z0, const ChunkDev& ch, int T, const int32_t* leaves, int n, int D, const float* es,
+                    float* tok, cudaStream_t st) {
+  if (n > 0) ctoken_kernel<<<n, std::min(D, 256), 0, st>>>(z0, ch, T, leaves, D, es, tok);
 }
 
-void launch_decompress(const __nv_bfloat16* g, const int32_t* leaves, int n, int Hp, int Wp, int Nh,
+void launch_decompress(const __nv_bfloat16* g, const ChunkDev& ch, int T, const int32_t* leaves, int n, int Nh,
                        __nv_bfloat16* tile_out, cudaStream_t st) {
-  if (n > 0) decompress_kernel<<<n, 128, 0, st>>>(g, leaves, Hp, Wp, Nh, tile_out);
+  if (n > 0) decompress_kernel<<<n, 128, 0, st>>>(g, ch, T, leaves, Nh, tile_out);
 }
 
 }  // namespace orbit2

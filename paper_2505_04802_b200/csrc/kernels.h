@@ -184,7 +184,7 @@ void launch_edges(const uint8_t* lab, uint8_t* e, int64_t n, cudaStream_t st);
 // offsets[b] = first leaf of image b, *total = n (= offsets[B])
 void launch_quadtree(const uint8_t* lab, int32_t* flag, int32_t* bsum, int32_t* total, int32_t* patches,
                      int32_t* offsets, int B, int H, int W, int mn, int mx, double thr, cudaStream_t st, int hr = 0,
-                     int wr = 0);
+                     int wr = 0, const int32_t* ext = nullptr /* per image [2]: real extents in min cells */);
 void launch_tokenize(const float* feat, const int32_t* patches, int n, int C, int H, int W, int m, int D,
                      int levels, const float* wt, const float* bt, const float* es, float* rows, float* wext,
                      float* tok, cudaStream_t st);
@@ -192,13 +192,15 @@ void launch_detokenize(const float* tok, const int32_t* patches, int n, int B, i
                        const float* wd, const float* bd, const float* ws, const float* bs, float* proj, float* work,
                        float* out, cudaStream_t st);
 
-// R41 (compression inside the forward): channel-mean field of z0 on the padded patch grid,
-// leaf tokens (mean of z0 over the leaf's grid patches + scale embedding), decompression of
-// the per-token head output to every patch of its leaf
-void launch_cfield(const float* z0, int B, int Hp, int Wp, int D, int Hq, int Wq, float* f, cudaStream_t st);
-void launch_ctokens(const float* z0, const int32_t* leaves, int n, int Hp, int Wp, int D, const float* es, float* tok,
-                    cudaStream_t st);
-void launch_decompress(const __nv_bfloat16* g, const int32_t* leaves, int n, int Hp, int Wp, int Nh,
+// R41 / R42 (compression inside the forward, per (sample, tile) image i = b T + t):
+// channel-mean field of the tile's z0 edge-padded to Hq x Wq, leaf tokens (mean of z0 over
+// the leaf's rectangle patches + scale embedding), decompression of the per-token head output
+// to the leaf's CORE patches in tile_out
+void launch_cfield(const float* z0, const ChunkDev& ch, int T, int B, int D, int Hq, int Wq, float* f,
+                   cudaStream_t st);
+void launch_ctokens(const float* z0, const ChunkDev& ch, int T, const int32_t* leaves, int n, int D, const float* es,
+                    float* tok, cudaStream_t st);
+void launch_decompress(const __nv_bfloat16* g, const ChunkDev& ch, int T, const int32_t* leaves, int n, int Nh,
                        __nv_bfloat16* tile_out, cudaStream_t st);
 
 // TMA descriptor encode via the driver entry point (no libcuda link dependency)

@@ -1452,9 +1452,9 @@ orbit2_status orbit2_compress_detokenize(const orbit2_compress_config* cfg, void
  * The Reslim forward on compressed tokens (R41; oracle/compress.py K5)
  * ---------------------------------------------------------------------------- */
 struct CfwdLay {
-  int64_t field, cws_part, leaves, offsets, tok, g, tiles, qblk, qpair, qpc, qg3, qg3c, core_row, total;
+  int64_t field, cws_part, leaves, offsets, ext, tok, g, tiles, qblk, qpair, qpc, qg3, qg3c, core_row, total;
   int64_t part_bytes, cap, tabcap;
-  int Hq, Wq;
+  int Hq, Wq, T, imgs;
 };
 
 static orbit2_status cfwd_layout(const Ctx* c, const orbit2_compression* cp, CfwdLay* L,
@@ -1462,30 +1462,34 @@ static orbit2_status cfwd_layout(const Ctx* c, const orbit2_compression* cp, Cfw
   const Plan& p = c->plan;
   const orbit2_config& cf = p.cfg;
   if (!cp) return set_err(ORBIT2_E_INVALID, "compression: null");
-  if (cf.precision != ORBIT2_BF16 || p.info.n_tiles != 1 || cf.halo != 0 || cf.world_size != 1 || cf.var_agg ||
-      cf.dec_hidden || cf.res_hidden)
-    return set_err(ORBIT2_E_UNSUPPORTED, "compressed forward: a BF16 context with one tile, halo 0, one rank, "
-                                         "no var_agg / dec_hidden / res_hidden (R41)");
+  if (cf.precision != ORBIT2_BF16 || cf.var_agg || cf.dec_hidden || cf.res_hidden)
+    return set_err(ORBIT2_E_UNSUPPORTED, "compressed forward: a BF16 context without var_agg / dec_hidden / "
+                                         "res_hidden (R41, R42)");
+  if (p.info.chunk_tiles < p.info.n_local_tiles)
+    return set_err(ORBIT2_E_UNSUPPORTED, "compressed forward: one call over every rank-local tile (chunk_tiles = 0)");
   const int mx = cp->max_side;
-  L->Hq = (int)round_up(p.Hp, mx);
-  L->Wq = (int)round_up(p.Wp, mx);
-  *cc = orbit2_compress_config{cf.batch, L->Hq, L->Wq, 1, 1, mx, p.D, cp->threshold, cp->sigma, cp->low_frac,
+  L->T = p.info.n_local_tiles;
+  L->imgs = cf.batch * L->T;
+  L->Hq = (int)round_up(p.max_pad_h, mx);   // R42: every tile's field padded to one shape
+  L->Wq = (int)round_up(p.max_pad_w, mx);
+  *cc = orbit2_compress_config{L->imgs, L->Hq, L->Wq, 1, 1, mx, p.D, cp->threshold, cp->sigma, cp->low_frac,
                                cp->high_frac};
   int64_t ws = 0, maxp = 0;
   ORBIT2_TRY(orbit2_compress_plan(cc, &ws, &maxp));
-  const int64_t B = cf.batch;
+  const int64_t I = L->imgs;
   L->cap = maxp;                                         // leaves (upper bound)
-  L->tabcap = L->cap / 128 + 2 * B + 2;                  // 128-token blocks of all images
+  L->tabcap = L->cap / 128 + 2 * I + 2;                  // 128-token blocks of all images
   int64_t off = 0;
   auto take = [&](int64_t b) { int64_t o = off; off = round_up(off + b, 256); return o; };
-  L->field = take(B * L->Hq * L->Wq * 4);
+  L->field = take(I * L->Hq * L->Wq * 4);
   L->part_bytes = ws;
   L->cws_part = take(ws);
   L->leaves = take(L->cap * 16);
-  L->offsets = take((B + 1) * 4);
+  L->offsets = take((I + 1) * 4);
+  L->ext = take(I * 8);
   L->tok = take(L->cap * p.D * 4);
   L->g = take(L->cap * round_up(p.Nh, 8) * 2);
-  L->tiles = take((B + 1) * (int64_t)sizeof(DevTile));
+  L->tiles = take((I + 1) * (int64_t)sizeof(DevTile));
   L->qblk = take(L->tabcap * 4);
   L->qpair = take(L->tabcap * 4);
   L->qpc = take(L->tabcap * 4);
@@ -1533,10 +1537,10 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
   const uint8_t* W8 = reinterpret_cast<const uint8_t*>(packed_w);
   auto wf = [&](int64_t off) { return reinterpret_cast<const float*>(W8 + off); };
   uint8_t* cw = reinterpret_cast<uint8_t*>(cws);
-  const int B = cf.batch, Hp = p.Hp, Wp = p.Wp;
+  const int B = cf.batch, T = L.T, I = L.imgs;
   const int64_t D = p.D, F = 4LL * p.D, mrow = ly.mrow;
-  // 1-2: gather + patch embedding (O2, O3) of every patch: z0 = the ctx's z
-  const Chunk ch = make_chunk(p, 0, 1);
+  // 1-2: gather + patch embedding (O2, O3) of every padded-rectangle patch: z0 = the ctx's z
+  const Chunk ch = make_chunk(p, 0, T);
   const ChunkDev cd = chunk_dev(c, ch);
   const int64_t M0 = (int64_t)B * ch.chunk_tokens;
   int2* rowinfo = c->at<int2>(ly.rowinfo);
@@ -1555,15 +1559,24 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     GemmOperand a{patches, mrow, ly.din_pad, 0}, b{W8 + w.w_e, D, ly.din_pad};
     ORBIT2_TRY(run(c, "embed_gemm", st, [&] { return launch_gemm_tc(EPI_EMBED, 0, a, b, M0, D, ly.din_pad, emb, st); }));
   }
-  // 3: the compression field and its partition (Canny + quad-tree over the patch grid)
+  // 3: every (sample, tile) rectangle's field and its partition (Canny + quad-tree, patch grid)
   float* field = reinterpret_cast<float*>(cw + L.field);
   ORBIT2_TRY(run(c, "compress_field", st, [&] {
-    launch_cfield(z, B, Hp, Wp, (int)D, L.Hq, L.Wq, field, st);
+    launch_cfield(z, cd, T, B, (int)D, L.Hq, L.Wq, field, st);
     return true;
   }));
   int32_t* leaves = reinterpret_cast<int32_t*>(cw + L.leaves);
   int32_t* offsets = reinterpret_cast<int32_t*>(cw + L.offsets);
+  int32_t* ext = reinterpret_cast<int32_t*>(cw + L.ext);
   {
+    std::vector<int32_t> ex(2 * (size_t)I);
+    for (int i = 0; i < I; ++i) {
+      ex[2 * i] = p.dev[i % T].pad_h;
+      ex[2 * i + 1] = p.dev[i % T].pad_w;
+    }
+    cudaError_t e0 = cudaMemcpyAsync(ext, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice, st);
+    if (e0 == cudaSuccess) e0 = cudaStreamSynchronize(st);   // ex is a host temporary
+    if (e0 != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e0));
     CompressLay cl;
     ORBIT2_TRY(compress_check(&cc, &cl));
     uint8_t* pw = cw + L.cws_part;
@@ -1571,18 +1584,19 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     ORBIT2_TRY(run(c, "compress_partition", st, [&] {
       launch_canny(field, reinterpret_cast<float*>(pw + cl.tmp), reinterpret_cast<float*>(pw + cl.tmp2),
                    reinterpret_cast<float*>(pw + cl.mag), pw + cl.dir, pw + cl.lab,
-                   reinterpret_cast<unsigned*>(pw + cl.gmax), reinterpret_cast<int*>(pw + cl.changed), B, L.Hq, L.Wq,
+                   reinterpret_cast<unsigned*>(pw + cl.gmax), reinterpret_cast<int*>(pw + cl.changed), I, L.Hq, L.Wq,
                    cc.sigma, cc.low_frac, cc.high_frac, st, &passes);
       launch_quadtree(pw + cl.lab, reinterpret_cast<int32_t*>(pw + cl.flag), reinterpret_cast<int32_t*>(pw + cl.bsum),
-                      offsets + B, leaves, offsets, B, L.Hq, L.Wq, 1, cp->max_side, (double)cc.threshold, st, Hp, Wp);
+                      offsets + I, leaves, offsets, I, L.Hq, L.Wq, 1, cp->max_side, (double)cc.threshold, st, 0, 0,
+                      ext);
       return true;
     }));
   }
-  std::vector<int32_t> off(B + 1);
-  cudaError_t e = cudaMemcpyAsync(off.data(), offsets, (B + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+  std::vector<int32_t> off(I + 1);
+  cudaError_t e = cudaMemcpyAsync(off.data(), offsets, (I + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e));
-  const int32_t n = off[B];
+  const int32_t n = off[I];
   if (n_tokens_host) *n_tokens_host = n;
   if (leaves_dev) {
     e = cudaMemcpyAsync(leaves_dev, leaves, (size_t)n * 16, cudaMemcpyDeviceToDevice, st);
@@ -1591,26 +1605,26 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
   // 4: tokens (then into the ctx's z: the blocks below use its buffers)
   float* tok = reinterpret_cast<float*>(cw + L.tok);
   ORBIT2_TRY(run(c, "compress_tokens", st, [&] {
-    launch_ctokens(z, leaves, n, Hp, Wp, (int)D, e_scale_dev, tok, st);
+    launch_ctokens(z, cd, T, leaves, n, (int)D, e_scale_dev, tok, st);
     return true;
   }));
   e = cudaMemcpyAsync(z, tok, (size_t)n * D * 4, cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward: ") + cudaGetErrorString(e));
-  // the images as the "tiles" of one call: per image its compressed tokens
-  std::vector<DevTile> dt(B + 1);
+  // the (sample, tile) images as the "tiles" of one call: per image its compressed tokens
+  std::vector<DevTile> dt(I + 1);
   std::vector<int32_t> qblk, qpair, qg3;
   int32_t qb = 0, qp = 0;
-  for (int b = 0; b <= B; ++b) {
+  for (int b = 0; b <= I; ++b) {
     DevTile t{};
-    const int32_t nb = b < B ? off[b + 1] - off[b] : 0;
+    const int32_t nb = b < I ? off[b + 1] - off[b] : 0;
     t.n_tokens = t.n_core = nb;
-    t.tok_off = t.core_off = off[std::min(b, B)];
+    t.tok_off = t.core_off = off[std::min(b, I)];
     t.qb_off = qb;
     t.qp_off = qp;
     t.pad_h = t.core_h = t.out_h = 1;
     t.pad_w = t.core_w = t.out_w = nb;
     dt[b] = t;
-    if (b == B) break;
+    if (b == I) break;
     const int32_t nqb = (nb + 127) / 128;
     for (int32_t i = 0; i < nqb; ++i) qblk.push_back(b);
     for (int32_t i = 0; i < (nqb + 1) / 2; ++i) qpair.push_back(b);
@@ -1618,7 +1632,7 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     qb += nqb;
     qp += (nqb + 1) / 2;
   }
-  if ((int64_t)qblk.size() > L.tabcap || B >= 32768)
+  if ((int64_t)qblk.size() > L.tabcap || I >= 32768)
     return set_err(ORBIT2_E_CAPACITY, "compressed forward: work-list capacity");
   e = cudaMemcpy(cw + L.tiles, dt.data(), dt.size() * sizeof(DevTile), cudaMemcpyHostToDevice);
   if (e == cudaSuccess && !qblk.empty()) e = cudaMemcpy(cw + L.qblk, qblk.data(), qblk.size() * 4, cudaMemcpyHostToDevice);
@@ -1628,7 +1642,7 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
   if (e != cudaSuccess) return set_err(ORBIT2_E_CUDA, std::string("compressed forward tables: ") + cudaGetErrorString(e));
   ChunkDev cc2{};
   cc2.tiles = reinterpret_cast<const DevTile*>(cw + L.tiles);
-  cc2.tb = 0; cc2.tc = B; cc2.tok0 = 0; cc2.core0 = 0; cc2.chunk_tokens = n; cc2.chunk_core = n;
+  cc2.tb = 0; cc2.tc = I; cc2.tok0 = 0; cc2.core0 = 0; cc2.chunk_tokens = n; cc2.chunk_core = n;
   cc2.qb0 = 0; cc2.nqb = qb; cc2.qp0 = 0; cc2.nqp = qp;
   cc2.qblk_tile = reinterpret_cast<const int32_t*>(cw + L.qblk);
   cc2.qpair_tile = reinterpret_cast<const int32_t*>(cw + L.qpair);
@@ -1690,8 +1704,9 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     ep = EpiParams{}; ep.bias = wf(Lw.b_2); ep.C = z; ep.ldc = D;
     ORBIT2_TRY(gemm("mlp_down_gemm", EPI_RESID, 0, hid, F, Lw.w_2, D, F, ep));
   }
-  // 6: LN_f + head per compressed token, decompression to every patch (tile_out: one tile)
-  bf16* hin = c->at<bf16>(ly.hin);
+  // 6: LN_f + head per compressed token (the LN output in xn: with halos the tokens can
+  // outnumber the core rows hin holds), decompression to the core patches
+  bf16* hin = xn;
   bf16* g = reinterpret_cast<bf16*>(cw + L.g);
   if (M > 0) {
     ORBIT2_TRY(run(c, "layernorm", st, [&] {
@@ -1700,11 +1715,11 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     }));
     EpiParams ep{};
     ep.bias = wf(w.b_h); ep.C = g; ep.ldc = p.Nh; ep.M = (int32_t)M; ep.N = p.Nh;
-    GemmOperand a{hin, ly.mcore, D, 0}, b{W8 + w.w_h, p.Nh, D};
+    GemmOperand a{hin, mrow, D, 0}, b{W8 + w.w_h, p.Nh, D};
     ORBIT2_TRY(run(c, "head_gemm", st, [&] { return launch_gemm_tc(EPI_BIAS, 1, a, b, M, p.Nh, D, ep, st); }));
   }
   return run(c, "decompress", st, [&] {
-    launch_decompress(g, leaves, n, Hp, Wp, p.Nh, reinterpret_cast<bf16*>(tile_out_dev), st);
+    launch_decompress(g, cd, T, leaves, n, p.Nh, reinterpret_cast<bf16*>(tile_out_dev), st);
     return true;
   });
 }

@@ -555,7 +555,8 @@ class Context:
     # -- the forward on compressed tokens (R41; include/orbit2.h) -------------------
     def compressed_forward(self, packed, x_dev, e_scale, max_side=8, threshold=0.1, sigma=1.0, low_frac=0.1,
                            high_frac=0.2, out=None, stream=None):
-        """-> (out [B, K, sH, sW], leaves [n, 4] (image, u0, w0, side in patches), n)."""
+        """-> (out [B, K, sH, sW], leaves [n, 4] (image b T + t, u0, w0, side; patches of the tile's
+        padded rectangle), n).  Every rank-local tile compressed on its own (R41, R42)."""
         import torch
         _req(x_dev, torch.float32, "x_dev")
         _req(e_scale, torch.float32, "e_scale")
@@ -568,7 +569,7 @@ class Context:
         if getattr(self, "_cws", None) is None or self._cws.numel() < ws.value:
             self._cws = torch.empty(max(ws.value, 16), dtype=torch.uint8, device=self.device)
         cfg = self.cfg
-        cap = cfg.batch * self.info.core_tokens_per_sample
+        cap = cfg.batch * self.info.local_tokens
         leaves = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=self.device)
         tile_out = self.tile_out_buffer()
         if out is None:
@@ -578,7 +579,7 @@ class Context:
             _check(lib.orbit2_compressed_forward(self.handle, _ptr(packed), _ptr(x_dev), C.byref(cp), _ptr(e_scale),
                                                  _ptr(self._cws), self._cws.numel(), _ptr(tile_out), _ptr(leaves),
                                                  C.byref(n), _stream(stream)), "orbit2_compressed_forward")
-        self.orbit2_stitch(tile_out, x_dev, 0, 1, out, stream)
+        self.orbit2_stitch(tile_out, x_dev, 0, self.info.n_local_tiles, out, stream)
         return out, leaves[:n.value], n.value
 
     # -- instrumentation ------------------------------------------------------

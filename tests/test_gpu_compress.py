@@ -156,3 +156,39 @@ def test_compressed_forward_full_refinement_equals_uncompressed():
     torch.cuda.synchronize()
     assert n == w.batch * (w.H // w.patch) * (w.W // w.patch)
     assert rel_err(out_c.cpu().numpy(), out_u.cpu().numpy()) <= 1e-2
+
+
+def test_compressed_forward_inside_tiles_matches_oracle():
+    """R42: compressed tokens inside TILES tiles (2 x 3 tiles, halo 2, ragged 12 x 13-patch
+    rectangles) against oracle K6 given the GPU's leaves per (sample, tile); and full
+    refinement == the uncompressed TILES forward (GPU, bf16 rounding order only)."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from oracle import reslim_tiles as O
+    from tests.gpu_helpers import rel_err
+    from workloads import make_weights
+    B = 2
+    w = get_config("C2", batch=B, H=48, W=80, tiles_y=2, tiles_x=3, halo=2, depth=2)
+    pr = O.Problem.from_config(w)
+    x = make_input(w, batch=B, seed=12)
+    blob = make_weights(w, seed=12)
+    ctx = o2.Context(o2.config_from(w, precision=o2.BF16))
+    packed = ctx.prepare_weights(torch.from_numpy(blob).cuda())
+    E = (0.1 * np.random.default_rng(2).standard_normal((3, w.embed))).astype(np.float32)
+    xd, Ed = torch.from_numpy(x).cuda(), torch.from_numpy(E).cuda()
+    out, leaves, n = ctx.compressed_forward(packed, xd, Ed, max_side=4, threshold=0.15)
+    torch.cuda.synchronize()
+    out, lv = out.cpu().numpy(), leaves.cpu().numpy()
+    T = w.tiles_y * w.tiles_x
+    assert n < B * ctx.info.local_tokens
+    Wt = pr.weights(blob)
+    for b in range(B):
+        by_tile = [[tuple(int(v) for v in r[1:]) for r in lv if r[0] == b * T + t] for t in range(T)]
+        ref, _ = K.tiles_compressed_forward(x[b].astype(np.float64), pr, Wt, E.astype(np.float64), by_tile)
+        assert rel_err(out[b], ref) <= 2e-2, rel_err(out[b], ref)
+    E0 = torch.zeros_like(Ed)
+    out_c, _, n = ctx.compressed_forward(packed, xd, E0, max_side=4, threshold=-1.0)
+    out_u = ctx.forward(packed, xd)
+    torch.cuda.synchronize()
+    assert n == B * ctx.info.local_tokens
+    assert rel_err(out_c.cpu().numpy(), out_u.cpu().numpy()) <= 1e-2
