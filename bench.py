@@ -42,13 +42,15 @@ def parse():
     ap.add_argument("--batch", type=int, default=0, help="override the config's bench batch")
     ap.add_argument("--chunk", type=int, default=-1, help="tiles per forward call (default: auto-fit HBM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="sp", choices=["dp", "sp", "train", "compress"],
+    ap.add_argument("--mode", default="sp", choices=["dp", "sp", "train", "compress", "sweep"],
                     help="N > 1 only.  sp (default): the tiles of one batch spread over the ranks, halo "
                          "exchange + output gather through NVLink peer memory (strong scaling); dp: every "
                          "rank its own batch (weak scaling).  train (any N): the training step (SURVEY "
                          "§8(f) row 3): forward, Bayesian loss, backward, one gradient all-reduce per batch.  "
                          "compress (N = 1): adaptive spatial compression (§8(f) row 4) of the batch's coarse "
-                         "fields: Canny + quad-tree partition, variable-size tokens, decompression")
+                         "fields: Canny + quad-tree partition, variable-size tokens, decompression.  sweep "
+                         "(N = 1): the tile-count sweep T in {1, 4, 16, 36} of the config (SURVEY §8(d), the "
+                         "shape of Tab. P:379-381), CUDA-graph replay of the forward beside it")
     ap.add_argument("--lam", type=float, default=1e-3, help="train: TV prior weight lambda (R34)")
     ap.add_argument("--delta", type=float, default=1e-3, help="train: Huber width delta (R34)")
     ap.add_argument("--sp-groups", type=int, default=0,
@@ -890,6 +892,62 @@ def _compressed_vs_uncompressed(o2, wf, Bf, D, thr, sigma, stream):
     return fwd
 
 
+# ---------------------------------------------------------------------------
+# tile-count sweep (Tab. P:379-381) + CUDA-graph replay
+# ---------------------------------------------------------------------------
+def run_sweep(args, w, world, rank, local):
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from workloads import make_input, make_weights
+    B = args.batch or 16
+    stream = torch.cuda.current_stream()
+    rows = []
+    for ty, tx in ((1, 1), (2, 2), (4, 4), (6, 6)):
+        wt = w.replace(batch=B, tiles_y=ty, tiles_x=tx, halo=0 if ty * tx == 1 else w.halo)
+        ctx = o2.Context(o2.config_from(wt, precision=o2.BF16))
+        packed = ctx.prepare_weights(torch.from_numpy(make_weights(wt)).cuda())
+        x = torch.from_numpy(make_input(wt, batch=B)).cuda()
+        out = torch.empty((B, wt.K, wt.scale * wt.H, wt.scale * wt.W), dtype=torch.float32, device="cuda")
+        tile_out = ctx.tile_out_buffer()
+        for _ in range(max(3, args.warmup)):
+            ctx.forward(packed, x, out=out, tile_out=tile_out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.forward(packed, x, out=out, tile_out=tile_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        g = ctx.capture_forward(packed, x, out, tile_out=tile_out)
+        g.replay()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.steps):
+            g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_g = e0.elapsed_time(e1) / args.steps
+        info = ctx.info
+        rows.append({"tiles": ty * tx, "halo": wt.halo, "ms_per_step": ms, "ms_per_step_graph": ms_g,
+                     "tokens_per_sample": info.tokens_per_sample,
+                     "attn_flops_per_sample": 4.0 * wt.embed * wt.depth * info.sum_n2_per_sample,
+                     "path_tflops": B * info.flops_per_sample / (ms * 1e-3) / 1e12})
+        del ctx, packed, x, out, tile_out, g
+        torch.cuda.empty_cache()
+    for r in rows:
+        r["speedup_vs_T1"] = rows[0]["ms_per_step"] / r["ms_per_step"]
+    px = B * w.scale * w.H * w.scale * w.W
+    res = {"metric": "tile-count sweep: high-res px/s of the forward at T = 1 / 4 / 16 / 36 tiles",
+           "value": px / (min(r["ms_per_step"] for r in rows) * 1e-3), "unit": UNIT, "n_gpus": 1,
+           "steps": args.steps, "warmup": max(3, args.warmup), "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields, random-init weights)",
+           "config": {"workload": w.name, "batch": B, "mode": "sweep",
+                      "note": "T = 1 without halo; the others with the config's halo (P:379-381 shape)"},
+           "sweep": rows}
+    print(json.dumps(res), flush=True)
+
+
 def relaunch_if_needed(args):
     """`python bench.py --gpus N` without torchrun: re-exec under
     torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
@@ -925,6 +983,8 @@ def main():
             run_train(args, w, world, rank, local)
         elif args.mode == "compress":
             run_compress(args, w, world, rank, local)
+        elif args.mode == "sweep":
+            run_sweep(args, w, world, rank, local)
         elif world > 1 and args.mode == "sp":
             run_sp(args, w, world, rank, local)
         else:

@@ -582,6 +582,26 @@ class Context:
         self.orbit2_stitch(tile_out, x_dev, 0, self.info.n_local_tiles, out, stream)
         return out, leaves[:n.value], n.value
 
+    # -- CUDA-graph capture of the forward ----------------------
+    def capture_forward(self, packed, x_dev, out, tile_out=None, stream=None):
+        """Capture forward(packed, x_dev, out) -- every launch of the pass, on one stream, no
+        host synchronisation inside -- into a CUDA graph; returns the graph (call .replay()).
+        The buffers are baked in: refill x_dev in place between replays."""
+        import torch
+        if tile_out is None:
+            tile_out = self.tile_out_buffer()
+        self._graph_bufs = (packed, x_dev, out, tile_out)
+        s = torch.cuda.Stream(self.device) if stream is None else stream
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self.forward(packed, x_dev, out=out, tile_out=tile_out, stream=s)   # warm-up: attributes, tmaps
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.forward(packed, x_dev, out=out, tile_out=tile_out, stream=s)
+        return g
+
     # -- instrumentation ------------------------------------------------------
     def launch_count(self) -> int:
         return int(lib.orbit2_launch_count(self.handle))

@@ -428,3 +428,25 @@ def test_variable_aggregation_parity(name, over, precision, tol):
     e = rel_err(got, ref)
     print(f"var_agg {name} {over} prec={precision}: rel_err={e:.3e}")
     assert np.isfinite(got).all() and e <= tol
+
+
+@pytest.mark.gpu
+def test_cuda_graph_replay_is_bit_exact():
+    """The forward captured into a CUDA graph (Context.capture_forward) replays to the same
+    bits as the eager forward, including after the input is refilled in place."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    from workloads import get_config, make_input, make_weights
+    w = get_config("C2", batch=2, H=48, W=96, tiles_y=2, tiles_x=3, depth=2)
+    ctx = o2.Context(o2.config_from(w, precision=o2.BF16))
+    packed = ctx.prepare_weights(torch.from_numpy(make_weights(w)).cuda())
+    x = torch.from_numpy(make_input(w, batch=2, seed=1)).cuda()
+    out_g = torch.empty((2, w.K, w.scale * w.H, w.scale * w.W), dtype=torch.float32, device="cuda")
+    g = ctx.capture_forward(packed, x, out_g)
+    for seed in (2, 3):
+        x.copy_(torch.from_numpy(make_input(w, batch=2, seed=seed)))
+        g.replay()
+        torch.cuda.synchronize()
+        ref = ctx.forward(packed, x)
+        torch.cuda.synchronize()
+        assert torch.equal(out_g, ref)
