@@ -235,3 +235,50 @@ def test_backward_scope_and_linearity_in_batch():
     _, g0 = T.train_step_grads(x[:1], y[:1], blob, pr, 0.05, 0.02)
     _, g1 = T.train_step_grads(x[1:], y[1:], blob, pr, 0.05, 0.02)
     np.testing.assert_allclose(g, 0.5 * (g0 + g1), rtol=1e-12, atol=1e-15)
+
+
+def _avg_worker(rank, world, port, q):
+    """One rank: the oracle gradient of ITS half of the batch, then the once-per-batch
+    gradient averaging as bench.py --mode train runs it (all_reduce AVG over gloo)."""
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        pr = problem(depth=1)
+        x, y, blob = data_for(pr, batch=2 * world)
+        sl = slice(2 * rank, 2 * rank + 2)
+        _, g = T.train_step_grads(x[sl], y[sl], blob, pr, 0.05, 0.02)
+        gt = torch.from_numpy(g)
+        dist.all_reduce(gt, op=dist.ReduceOp.AVG)
+        if rank == 0:
+            _, full = T.train_step_grads(x, y, blob, pr, 0.05, 0.02)
+            q.put(("ok", float(np.abs(gt.numpy() - full).max() / np.abs(full).max())))
+        else:
+            q.put(("ok", 0.0))
+    except Exception as e:  # pragma: no cover
+        q.put(("err", repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gradient_averaging_gloo_world2_equals_full_batch():
+    """T4 / R36 ("gradients from all GPUs are averaged"): two ranks with two samples
+    each, one all-reduce (average) of their gradients == the gradient of the 4-sample batch."""
+    import multiprocessing as mp
+    import socket
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = [ctx.Process(target=_avg_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for r in res:
+        assert r[0] == "ok", r
+        assert r[1] <= 1e-12, r
