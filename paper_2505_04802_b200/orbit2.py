@@ -423,13 +423,17 @@ class Context:
         return out
 
     # -- host buffers in, host buffers out (pipelined) ------------------------
-    def forward_host(self, packed, x_host, out_host, stream=None):
+    def forward_host(self, packed, x_host, out_host, stream=None, sync_out=True):
         """The whole pass for N = k * cfg.batch samples held in PINNED host memory:
         x_host [N,V,H,W] fp32 -> out_host [N,K,sH,sW] fp32.  Samples go through the
         device in groups of cfg.batch; the host->device copy of group g+1 and the
         device->host copy of group g-1 run on their own streams (copy engines, both
-        PCIe directions) while group g computes on `stream`.  Returns when the work
-        is queued; completion is ordered before later work on `stream`."""
+        PCIe directions) while group g computes on `stream`.  The two device buffer pairs
+        alternate ACROSS calls too, so back-to-back calls overlap the next call's first
+        input copy and the previous call's last output copy with compute.  Returns when
+        the work is queued.  sync_out=True: completion (output copies included) is ordered
+        before later work on `stream`; False: returns the events of the last output
+        copies instead (wait on them before reading out_host)."""
         import torch
         G = self.cfg.batch
         n = x_host.shape[0]
@@ -445,37 +449,39 @@ class Context:
                         for _ in range(2))
             self._host_bufs = (xs, os_, self.tile_out_buffer(),
                                torch.cuda.Stream(self.device), torch.cuda.Stream(self.device))
+            # per buffer: the last compute that read xs[b] / wrote os_[b], the last copy out of os_[b]
+            self._host_state = {"comp_done": [None, None], "out_done": [None, None], "next": 0}
         xs, os_, tile_out, s_in, s_out = self._host_bufs
-        start = torch.cuda.Event()
-        start.record(comp)
-        s_in.wait_event(start)
-        s_out.wait_event(start)
-        in_done = [torch.cuda.Event(), torch.cuda.Event()]
-        comp_done = [None, None]
-        out_done = [None, None]
+        stt = self._host_state
         for g in range(n // G):
-            b = g & 1
+            b = stt["next"]
+            stt["next"] ^= 1
             sl = slice(g * G, (g + 1) * G)
+            in_done = torch.cuda.Event()
             with torch.cuda.stream(s_in):
-                if comp_done[b] is not None:          # the compute that read xs[b] is done
-                    s_in.wait_event(comp_done[b])
+                if stt["comp_done"][b] is not None:   # the compute that read xs[b] is done
+                    s_in.wait_event(stt["comp_done"][b])
                 xs[b].copy_(x_host[sl], non_blocking=True)
-                in_done[b].record(s_in)
-            comp.wait_event(in_done[b])
-            if out_done[b] is not None:               # os_[b] has been copied out
-                comp.wait_event(out_done[b])
+                in_done.record(s_in)
+            comp.wait_event(in_done)
+            if stt["out_done"][b] is not None:        # os_[b] has been copied out
+                comp.wait_event(stt["out_done"][b])
             self.forward(packed, xs[b], out=os_[b], tile_out=tile_out, stream=comp)
-            comp_done[b] = torch.cuda.Event()
-            comp_done[b].record(comp)
+            cd = torch.cuda.Event()
+            cd.record(comp)
+            stt["comp_done"][b] = cd
             with torch.cuda.stream(s_out):
-                s_out.wait_event(comp_done[b])
+                s_out.wait_event(cd)
                 out_host[sl].copy_(os_[b], non_blocking=True)
-                out_done[b] = torch.cuda.Event()
-                out_done[b].record(s_out)
-        for e in out_done:
-            if e is not None:
+                od = torch.cuda.Event()
+                od.record(s_out)
+            stt["out_done"][b] = od
+        last = [e for e in stt["out_done"] if e is not None]
+        if sync_out:
+            for e in last:
                 comp.wait_event(e)
-        return out_host
+            return out_host
+        return last
 
     # -- training step (include/orbit2.h "Training step") ----
     def train_info(self) -> orbit2_train_info:

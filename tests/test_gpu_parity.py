@@ -316,9 +316,17 @@ def test_forward_host_pipelined_matches_device_forward():
     grp = o2.Context(o2.config_from(w, batch=2, precision=BF16))
     x_pin = torch.from_numpy(x).pin_memory()
     out_pin = torch.full(tuple(ref.shape), float("nan"), dtype=torch.float32).pin_memory()
-    grp.forward_host(grp.prepare_weights(wd), x_pin, out_pin)
+    packed = grp.prepare_weights(wd)
+    grp.forward_host(packed, x_pin, out_pin)
     torch.cuda.synchronize()
     assert torch.equal(out_pin, ref.cpu())
+    # back-to-back calls overlapping across calls (sync_out=False, then a synchronising call)
+    outs = [torch.full(tuple(ref.shape), float("nan"), dtype=torch.float32).pin_memory() for _ in range(3)]
+    for i, o in enumerate(outs):
+        grp.forward_host(packed, x_pin, o, sync_out=i == len(outs) - 1)
+    torch.cuda.synchronize()
+    for o in outs:
+        assert torch.equal(o, ref.cpu())
 
 
 @pytest.mark.gpu
