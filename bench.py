@@ -708,10 +708,19 @@ def run_train(args, w, world, rank, local):
     loss_pin = torch.empty(B, dtype=torch.float64).pin_memory()
     stream = torch.cuda.current_stream()
 
+    # the weight update (R43: AdamW) and the re-packing of the updated weights are part of the step
+    mom = torch.zeros_like(blob)
+    vel = torch.zeros_like(blob)
+    t_step = [0]
+
     def step():
         loss, g, _ = ctx.train_step(packed, x_dev, y_dev, args.lam, args.delta, True, bufs, stream)
         if world > 1:
             dist.all_reduce(g, op=dist.ReduceOp.AVG)   # once per batch
+        t_step[0] += 1
+        o2.adamw_step(blob, g, mom, vel, t_step[0], 1e-4, 0.9, 0.95, 1e-8, 0.01, stream)
+        ctx.prepare_weights(blob, stream, out=packed)
+        ctx.train_prepare(blob, stream)
         return loss
 
     for _ in range(max(3, args.warmup)):
@@ -759,7 +768,7 @@ def run_train(args, w, world, rank, local):
     flops = world * B * ti.flops_per_sample
     pk = peaks()
     res = {
-        "metric": "training high-res px/s (forward + Bayesian loss + backward + gradient all-reduce)",
+        "metric": "training high-res px/s (forward + Bayesian loss + backward + gradient all-reduce + AdamW update)",
         "value": px / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields and truth, random-init weights)",

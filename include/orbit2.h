@@ -387,6 +387,13 @@ orbit2_status orbit2_loss(void *ctx, const float *out_dev, const float *truth_de
  * overwritten with the gradient of the rank-local tiles' contribution. */
 orbit2_status orbit2_train_backward(void *ctx, const void *packed_w, const float *dout_dev, float *grad_dev,
                                     void *stream);
+/* The weight update (the paper names no optimizer; reading R43: AdamW, decoupled weight decay,
+ * bias-corrected moments), elementwise over n fp32 values in place: m, v (caller-owned, zero
+ * before step 1) and w (the canonical blob).  step = t >= 1.  Re-run orbit2_prepare_weights and
+ * orbit2_train_prepare on the updated blob before the next step. */
+orbit2_status orbit2_adamw_step(float *w_dev, const float *grad_dev, float *m_dev, float *v_dev, int64_t n,
+                                int32_t step, float lr, float beta1, float beta2, float eps, float weight_decay,
+                                void *stream);
 
 /* ==========================================================================
  * Adaptive spatial compression (readings R37-R40).

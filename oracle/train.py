@@ -281,3 +281,19 @@ def train_step_grads(x: np.ndarray, y: np.ndarray, blob: np.ndarray, pr: O.Probl
             tile_backward(x[b], t, pr, Wt, dg, grads)
     return loss, pack_grads(grads, pr)
 
+
+
+# ---------------------------------------------------------------------------
+# T5 the weight update (R43)
+# ---------------------------------------------------------------------------
+def adamw(w: np.ndarray, g: np.ndarray, m: np.ndarray, v: np.ndarray, step: int, lr: float, beta1: float = 0.9,
+          beta2: float = 0.999, eps: float = 1e-8, weight_decay: float = 0.0):
+    """AdamW (decoupled weight decay, bias-corrected moments), one step t = step >= 1:
+    m <- b1 m + (1 - b1) g;  v <- b2 v + (1 - b2) g^2;
+    w <- w - lr (wd w + (m / (1 - b1^t)) / (sqrt(v / (1 - b2^t)) + eps)).  Returns (w, m, v)."""
+    w, g, m, v = (np.asarray(a, np.float64) for a in (w, g, m, v))
+    m = beta1 * m + (1.0 - beta1) * g
+    v = beta2 * v + (1.0 - beta2) * g * g
+    mh = m / (1.0 - beta1 ** step)
+    vh = v / (1.0 - beta2 ** step)
+    return w - lr * (weight_decay * w + mh / (np.sqrt(vh) + eps)), m, v

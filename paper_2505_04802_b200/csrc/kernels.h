@@ -171,6 +171,8 @@ void launch_delta(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* delta,
                   int64_t ld_stat, cudaStream_t st);
 void launch_dq_convert(const float* dq, __nv_bfloat16* dqkv, int64_t M, int D, cudaStream_t st);
 void launch_transpose_bf16(const float* W, int n, int k, __nv_bfloat16* Wt, int64_t ld, cudaStream_t st);
+void launch_adamw(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+                  float wd, float c1, float c2, cudaStream_t st);
 
 // ---- adaptive spatial compression (compress.cu) ----
 bool compress_taps(float sigma, float* w, int* r);

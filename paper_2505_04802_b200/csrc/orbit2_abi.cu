@@ -1724,4 +1724,19 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
   });
 }
 
+
+orbit2_status orbit2_adamw_step(float* w_dev, const float* grad_dev, float* m_dev, float* v_dev, int64_t n,
+                                int32_t step, float lr, float beta1, float beta2, float eps, float weight_decay,
+                                void* stream) {
+  if (n < 0 || step < 1 || !(lr >= 0.f) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) ||
+      !(eps > 0.f))
+    return set_err(ORBIT2_E_INVALID, "adamw: n >= 0, step >= 1, lr >= 0, 0 <= beta < 1, eps > 0");
+  if (n > 0 && (!w_dev || !grad_dev || !m_dev || !v_dev)) return set_err(ORBIT2_E_INVALID, "adamw: null pointer");
+  const double c1 = 1.0 / (1.0 - std::pow((double)beta1, step)), c2 = 1.0 / (1.0 - std::pow((double)beta2, step));
+  launch_adamw(w_dev, grad_dev, m_dev, v_dev, n, lr, beta1, beta2, eps, weight_decay, (float)c1, (float)c2,
+               reinterpret_cast<cudaStream_t>(stream));
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? ORBIT2_OK : set_err(ORBIT2_E_CUDA, std::string("adamw: ") + cudaGetErrorString(e));
+}
+
 }  // extern "C"

@@ -286,7 +286,30 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ W, int n, int k,
   }
 }
 
+// AdamW (R43): m = b1 m + (1 - b1) g; v = b2 v + (1 - b2) g^2;
+// w -= lr (wd w + (m c1) / (sqrt(v c2) + eps)), c1 = 1 / (1 - b1^t), c2 = 1 / (1 - b2^t)
+__global__ void adamw_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m,
+                             float* __restrict__ v, int64_t n, float lr, float b1, float b2, float eps, float wd,
+                             float c1, float c2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float mi = fmaf(b1, m[i], (1.f - b1) * gi);
+    const float vi = fmaf(b2, v[i], (1.f - b2) * gi * gi);
+    m[i] = mi;
+    v[i] = vi;
+    const float wi = w[i];
+    w[i] = wi - lr * fmaf(wd, wi, (mi * c1) / (sqrtf(vi * c2) + eps));
+  }
+}
+
 }  // namespace
+
+void launch_adamw(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+                  float wd, float c1, float c2, cudaStream_t st) {
+  if (n <= 0) return;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 16LL * num_sms());
+  adamw_kernel<<<blocks, 256, 0, st>>>(w, g, m, v, n, lr, b1, b2, eps, wd, c1, c2);
+}
 
 void launch_lat_weights(float* w, int sH, cudaStream_t st) { lat_weights_kernel<<<1, 256, 0, st>>>(w, sH); }
 

@@ -102,6 +102,8 @@ def _load():
         "orbit2_train_forward": (i32, [vp, vp, vp, vp, vp]),
         "orbit2_loss": (i32, [vp, vp, vp, C.c_float, C.c_float, i32, vp, vp, vp]),
         "orbit2_train_backward": (i32, [vp, vp, vp, vp, vp]),
+        "orbit2_adamw_step": (i32, [vp, vp, vp, vp, i64, i32, C.c_float, C.c_float, C.c_float, C.c_float, C.c_float,
+                                    vp]),
         "orbit2_compress_plan": (i32, [C.POINTER(orbit2_compress_config), C.POINTER(i64), C.POINTER(i64)]),
         "orbit2_compress_partition": (i32, [C.POINTER(orbit2_compress_config), vp, vp, C.c_size_t, vp, vp, vp,
                                             C.POINTER(i32), vp]),
@@ -131,7 +133,7 @@ EXPORTED = ("orbit2_tiles_plan", "orbit2_create", "orbit2_prepare_weights", "orb
             "orbit2_ipc_export", "orbit2_comm_init", "orbit2_comm_target", "orbit2_halo_exchange",
             "orbit2_comm_barrier", "orbit2_comm_status",
             "orbit2_train_plan", "orbit2_train_bind", "orbit2_train_prepare", "orbit2_train_forward",
-            "orbit2_loss", "orbit2_train_backward",
+            "orbit2_loss", "orbit2_train_backward", "orbit2_adamw_step",
             "orbit2_compress_plan", "orbit2_compress_partition", "orbit2_compress_tokenize",
             "orbit2_compress_detokenize", "orbit2_compressed_plan", "orbit2_compressed_forward",
             "orbit2_launch_count", "orbit2_set_profiling", "orbit2_kernel_times", "orbit2_last_error",
@@ -273,11 +275,13 @@ class Context:
             self.handle = None
 
     # -- lifecycle ---------------------------------------------------------
-    def prepare_weights(self, canonical_dev, stream=None):
+    def prepare_weights(self, canonical_dev, stream=None, out=None):
+        """Pack the canonical fp32 blob (into `out` when given: re-packing after a weight update)."""
         import torch
         assert canonical_dev.dtype == torch.float32 and canonical_dev.is_cuda
         assert canonical_dev.numel() == self.info.canonical_weight_count, "canonical blob size"
-        packed = torch.empty(self.info.packed_weight_bytes, dtype=torch.uint8, device=self.device)
+        packed = torch.empty(self.info.packed_weight_bytes, dtype=torch.uint8, device=self.device) if out is None \
+            else out
         with _on_device(self.device):
             _check(lib.orbit2_prepare_weights(self.handle, _ptr(canonical_dev), _ptr(packed), _stream(stream)),
                    "orbit2_prepare_weights")
@@ -622,6 +626,18 @@ class Context:
         ms = (C.c_double * n)()
         lib.orbit2_kernel_times(self.handle, names, launches, ms, n)
         return {names[i].decode(): (int(launches[i]), float(ms[i])) for i in range(n)}
+
+
+def adamw_step(w, grad, m, v, step, lr, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, stream=None):
+    """orbit2_adamw_step on fp32 CUDA tensors of one size (in place: w, m, v)."""
+    import torch
+    for t, name in ((w, "w"), (grad, "grad"), (m, "m"), (v, "v")):
+        _req(t, torch.float32, name)
+    n = w.numel()
+    if not (grad.numel() == m.numel() == v.numel() == n):
+        raise ValueError("adamw_step: sizes differ")
+    _check(lib.orbit2_adamw_step(_ptr(w), _ptr(grad), _ptr(m), _ptr(v), n, step, lr, beta1, beta2, eps, weight_decay,
+                                 _stream(stream)), "orbit2_adamw_step")
 
 
 class Compressor:

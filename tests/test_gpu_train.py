@@ -175,3 +175,23 @@ def test_train_step_wide_model_matches_oracle():
                                             pr, lam, delta)
     assert abs(loss.mean() - ref_loss) <= LOSS_TOL * abs(ref_loss)
     _check_grads(pr, grad, ref_grad)
+
+
+def test_adamw_step_matches_oracle():
+    """orbit2_adamw_step (R43) over three steps == oracle T5 (fp32 kernel vs fp64)."""
+    import torch
+    from paper_2505_04802_b200 import orbit2 as o2
+    rng = np.random.default_rng(5)
+    n = 10007
+    w0 = rng.standard_normal(n)
+    gs = [rng.standard_normal(n) for _ in range(3)]
+    w = torch.from_numpy(w0.astype(np.float32)).cuda()
+    m, v = torch.zeros_like(w), torch.zeros_like(w)
+    wr, mr, vr = w0.astype(np.float32).astype(np.float64), np.zeros(n), np.zeros(n)
+    for t, g in enumerate(gs, start=1):
+        gd = torch.from_numpy(g.astype(np.float32)).cuda()
+        o2.adamw_step(w, gd, m, v, t, 1e-2, 0.9, 0.95, 1e-8, 0.1)
+        wr, mr, vr = T.adamw(wr, g.astype(np.float32), mr, vr, t, 1e-2, 0.9, 0.95, 1e-8, 0.1)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(w.cpu().numpy(), wr, rtol=0, atol=1e-5)
+    np.testing.assert_allclose(m.cpu().numpy(), mr, rtol=0, atol=1e-5)

@@ -282,3 +282,18 @@ def test_gradient_averaging_gloo_world2_equals_full_batch():
     for r in res:
         assert r[0] == "ok", r
         assert r[1] <= 1e-12, r
+
+
+def test_adamw_matches_torch_optimizer():
+    """T5 / R43: three AdamW steps == torch.optim.AdamW (library, fp64) on the same gradients."""
+    rng = np.random.default_rng(4)
+    w0 = rng.standard_normal(37)
+    gs = [rng.standard_normal(37) for _ in range(3)]
+    p = torch.nn.Parameter(torch.from_numpy(w0.copy()))
+    opt = torch.optim.AdamW([p], lr=1e-2, betas=(0.9, 0.95), eps=1e-8, weight_decay=0.1)
+    w, m, v = w0.copy(), np.zeros(37), np.zeros(37)
+    for t, g in enumerate(gs, start=1):
+        p.grad = torch.from_numpy(g.copy())
+        opt.step()
+        w, m, v = T.adamw(w, g, m, v, t, 1e-2, 0.9, 0.95, 1e-8, 0.1)
+    np.testing.assert_allclose(w, p.detach().numpy(), rtol=1e-13, atol=1e-14)
