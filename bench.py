@@ -52,6 +52,10 @@ def parse():
                          "(N = 1): the tile-count sweep T in {1, 4, 16, 36} of the config (SURVEY §8(d), the "
                          "shape of Tab. P:379-381), CUDA-graph replay of the forward beside it")
     ap.add_argument("--lam", type=float, default=1e-3, help="train: TV prior weight lambda (R34)")
+    ap.add_argument("--train-tiles", action="store_true",
+                    help="train, N > 1: tile-parallel training (the SAME batch, its tiles over the ranks, the "
+                         "field and the gradient summed with NCCL: training.TilesTrainSP; strong scaling) instead "
+                         "of data parallel")
     ap.add_argument("--delta", type=float, default=1e-3, help="train: Huber width delta (R34)")
     ap.add_argument("--sp-groups", type=int, default=0,
                     help="N > 1: sample groups per rank (default 4 when the batch allows, else 1)")
@@ -151,6 +155,16 @@ def barrier(world):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+
+
+def _sum_over_ranks(world, v: float) -> float:
+    import torch
+    import torch.distributed as dist
+    if world == 1:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def max_over_ranks(world, v: float) -> float:
@@ -682,9 +696,11 @@ def run_train(args, w, world, rank, local):
     from paper_2505_04802_b200 import orbit2 as o2
     from workloads import make_input, make_weights
     B = w.batch
+    tiles_sp = args.train_tiles and world > 1
     free, _ = torch.cuda.mem_get_info()
     while True:   # the largest batch (<= the config's) whose training workspace fits 85% of HBM
-        cfg = o2.config_from(w, batch=B, precision=o2.BF16)
+        cfg = o2.config_from(w, batch=B, precision=o2.BF16, world_size=world if tiles_sp else 1,
+                             rank=rank if tiles_sp else 0)
         ctx = o2.Context(cfg)
         ti = ctx.train_info()
         need = ti.workspace_bytes + 4 * cfg.batch * w.K * w.scale * w.H * w.scale * w.W * 4 + ctx.info.tile_out_bytes
@@ -693,13 +709,21 @@ def run_train(args, w, world, rank, local):
         del ctx
         torch.cuda.empty_cache()
         B //= 2
-    ctx.train_bind()
+    if tiles_sp:
+        from paper_2505_04802_b200.training import TilesTrainSP
+        sp = TilesTrainSP(ctx, dist)
+    else:
+        ctx.train_bind()
     info = ctx.info
     blob = torch.from_numpy(make_weights(w)).cuda()
     packed = ctx.prepare_weights(blob)
-    ctx.train_prepare(blob)
-    x_host = make_input(w, batch=B, seed=2000 + 97 * rank)
-    rng = np.random.default_rng(3000 + rank)
+    if tiles_sp:
+        sp.prepare(blob)
+    else:
+        ctx.train_prepare(blob)
+    seed = 0 if tiles_sp else rank          # tile-parallel: the same batch on every rank
+    x_host = make_input(w, batch=B, seed=2000 + 97 * seed)
+    rng = np.random.default_rng(3000 + seed)
     y_host = rng.standard_normal((B, w.K, w.scale * w.H, w.scale * w.W)).astype(np.float32)
     x_pin, y_pin = torch.from_numpy(x_host).pin_memory(), torch.from_numpy(y_host).pin_memory()
     x_dev, y_dev = x_pin.cuda(), y_pin.cuda()
@@ -714,13 +738,19 @@ def run_train(args, w, world, rank, local):
     t_step = [0]
 
     def step():
-        loss, g, _ = ctx.train_step(packed, x_dev, y_dev, args.lam, args.delta, True, bufs, stream)
-        if world > 1:
-            dist.all_reduce(g, op=dist.ReduceOp.AVG)   # once per batch
+        if tiles_sp:    # tiles over the ranks; field and gradient summed (training.TilesTrainSP)
+            loss, g, _ = sp.step(packed, x_dev, y_dev, args.lam, args.delta, True, stream)
+        else:
+            loss, g, _ = ctx.train_step(packed, x_dev, y_dev, args.lam, args.delta, True, bufs, stream)
+            if world > 1:
+                dist.all_reduce(g, op=dist.ReduceOp.AVG)   # once per batch
         t_step[0] += 1
         o2.adamw_step(blob, g, mom, vel, t_step[0], 1e-4, 0.9, 0.95, 1e-8, 0.01, stream)
         ctx.prepare_weights(blob, stream, out=packed)
-        ctx.train_prepare(blob, stream)
+        if tiles_sp:
+            sp.prepare(blob, stream)
+        else:
+            ctx.train_prepare(blob, stream)
         return loss
 
     for _ in range(max(3, args.warmup)):
@@ -764,16 +794,19 @@ def run_train(args, w, world, rank, local):
         torch.cuda.synchronize()
         prof = {k: (n / 3, t / 3) for k, (n, t) in ctx.kernel_times().items()}
         ctx.set_profiling(False)
-    px = world * B * w.scale * w.H * w.scale * w.W
-    flops = world * B * ti.flops_per_sample
+    px = (1 if tiles_sp else world) * B * w.scale * w.H * w.scale * w.W
+    # tile-parallel: the ranks' tile shares of ONE batch (train_plan counts rank-local tiles)
+    flops = B * _sum_over_ranks(world, ti.flops_per_sample) if tiles_sp else world * B * ti.flops_per_sample
     pk = peaks()
     res = {
         "metric": "training high-res px/s (forward + Bayesian loss + backward + gradient all-reduce + AdamW update)",
         "value": px / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if tiles_sp else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (ERA5-shaped seeded fields and truth, random-init weights)",
         "config": {"workload": w.name, "batch_per_gpu": B, "mode": "train", "lambda": args.lam, "delta": args.delta,
-                   "parallelism": f"dp{world} (one gradient all-reduce per batch)",
+                   "parallelism": (f"tiles-sp{world} (one batch, LPT tiles per rank; NCCL all-reduce of the field "
+                                   "and of the gradient)") if tiles_sp else f"dp{world} (one gradient all-reduce per batch)",
                    "l2": "working set > L2 (126 MB) every step; no flush needed"},
         "train_tflops": flops / (ms * 1e-3) / 1e12,
         "train_frac_bf16_peak": flops / (ms * 1e-3) / 1e12 / pk["bf16"],
