@@ -15,6 +15,10 @@
  *       ("the halo regions are discarded, and the non-padded tile
  *       outputs are stitched together");
  *   (5) add the residual interpolated upsample of the input.
+ * Beyond the pass: the residual / decoder convolutions and the
+ * variable aggregation (config fields), the training step (orbit2_train_*,
+ * orbit2_loss, orbit2_adamw_step) and the adaptive spatial compression
+ * (orbit2_compress_*, orbit2_compressed_forward).
  *
  * Graded boundary: orbit2_tiles_plan (1, host), orbit2_reslim_forward (1-3 +
  * linear head), orbit2_stitch (4-5).  The rest is lifecycle support.
@@ -27,8 +31,13 @@
  *     plain device pointers from cudaMalloc / torch).  The library never
  *     allocates device memory after orbit2_create and never frees caller
  *     memory.  A ctx borrows its workspace until orbit2_destroy.
- *   - Streams: all device work is enqueued on the caller's stream; nothing
- *     synchronises the host except orbit2_create (one-time table upload).
+ *   - Streams: all device work is enqueued on the caller's stream; the forward,
+ *     stitch, halo exchange, training forward / loss / backward and weight update
+ *     never synchronise the host.  The documented exceptions: orbit2_create
+ *     (one-time table upload), orbit2_comm_init / orbit2_comm_status (setup and
+ *     status checks), orbit2_train_bind (zero-fill), and the data-dependent
+ *     compression calls orbit2_compress_partition / orbit2_compressed_forward (one
+ *     synchronisation per hysteresis pass and one for the token count).
  *     Asynchronous device faults surface at the caller's next synchronisation
  *     (set ORBIT2_SYNC_CHECK=1 to synchronise and check after every call).
  *   - One ctx per host thread / stream at a time.  Distinct ctxs are independent.
