@@ -35,8 +35,7 @@
  *     stitch, halo exchange, training forward / loss / backward and weight update
  *     never synchronise the host.  The documented exceptions: orbit2_create
  *     (one-time table upload), orbit2_comm_init / orbit2_comm_status (setup and
- *     status checks), orbit2_train_bind (zero-fill), and the data-dependent
- *     compression calls orbit2_compress_partition / orbit2_compressed_forward (one
+ *     status checks), and the data-dependent compression calls orbit2_compress_partition / orbit2_compressed_forward (one
  *     synchronisation per hysteresis pass and one for the token count).
  *     Asynchronous device faults surface at the caller's next synchronisation
  *     (set ORBIT2_SYNC_CHECK=1 to synchronise and check after every call).
