@@ -596,29 +596,67 @@ def run_sp(args, w, world, rank, local):
     clocks = clk.summary()
     ctx.comm_status()
 
-    # ---- end to end: pinned host input -> every rank (H2D of the field), SP step,
-    # root -> pinned host output (D2H); an extra device barrier keeps the next step's
-    # stitches out of the root's field until its D2H has read it ----
+    # ---- end to end: pinned host input -> every rank (H2D of the field), SP step, root ->
+    # pinned host output (D2H).  Two independent SP instances (their own contexts, fields and
+    # barrier flags) alternate, so step k+1's input copy and step k's output copy run on side
+    # streams while the other instance computes.  The root enters an instance's next step
+    # (whose first act is the halo barrier every rank waits on) only after the output copy of
+    # that instance's previous step: no rank stitches into a field still being copied out ----
     out_pin = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() if rank == 0 else None
+    ctx2 = o2.Context(cfg)
+    wctx2 = o2.Context(o2.config_from(w, batch=B // groups, precision=o2.BF16, world_size=world, rank=rank,
+                                      chunk_tiles=chunk)) if groups > 1 else None
+    x2 = x.clone()
+    out2 = torch.empty_like(out) if rank == 0 else None
+    packed2 = ctx2.prepare_weights(torch.from_numpy(blob).cuda())
+    sp2 = PeerSP(ctx2, x2, out2, dist, gather_root=0, work_ctx=wctx2)
+    inst = [(sp, x, out, packed, ctx), (sp2, x2, out2, packed2, ctx2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    comp_done, out_done = [None, None], [None, None]
+    kstep = [0]
 
-    def e2e_step():
-        x.copy_(x_pin, non_blocking=True)
-        sp.step(packed, stream)
+    def e2e_step(last=False):
+        b = kstep[0] & 1
+        kstep[0] += 1
+        spb, xb, outb, pb, _ = inst[b]
+        ev_in = torch.cuda.Event()
+        with torch.cuda.stream(s_in):
+            if comp_done[b] is not None:
+                s_in.wait_event(comp_done[b])
+            xb.copy_(x_pin, non_blocking=True)
+            ev_in.record(s_in)
+        stream.wait_event(ev_in)
+        if rank == 0 and out_done[b] is not None:
+            stream.wait_event(out_done[b])
+        spb.step(pb, stream)
+        cd = torch.cuda.Event()
+        cd.record(stream)
+        comp_done[b] = cd
         if rank == 0:
-            out_pin.copy_(out, non_blocking=True)
-        ctx.comm_barrier(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(cd)
+                out_pin.copy_(outb, non_blocking=True)
+                od = torch.cuda.Event()
+                od.record(s_out)
+            out_done[b] = od
+        if last and rank == 0:
+            for e in out_done:
+                if e is not None:
+                    stream.wait_event(e)
 
-    e2e_step()
+    for _ in range(2):
+        e2e_step(last=True)
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e_steps = max(2, args.steps // 2)
     e0.record(stream)
-    for _ in range(e_steps):
-        e2e_step()
+    for i in range(e_steps):
+        e2e_step(last=i + 1 == e_steps)
     e1.record(stream)
     barrier(world)
     e2e_ms = max_over_ranks(world, e0.elapsed_time(e1) / e_steps)
     ctx.comm_status()
+    ctx2.comm_status()
 
     # ---- per-kernel-class times of this rank (profiled pass, events per launch) ----
     prof = {}
@@ -657,8 +695,9 @@ def run_sp(args, w, world, rank, local):
             "e2e": {"value": px / (e2e_ms * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": world * x_pin.numel() * 4, "d2h_bytes_per_step": out.numel() * 4,
                     "ms_per_step": e2e_ms,
-                    "api": "PeerSP.step with the input field copied from pinned host on every rank and the "
-                           "gathered field copied to pinned host on rank 0"},
+                    "api": "PeerSP.step (two instances alternating, copies on side streams) with the input "
+                           "field copied from pinned host on every rank and the gathered field copied to "
+                           "pinned host on rank 0"},
             "per_rank_kernels": [{k: {"launches": round(n, 2), "ms": round(t, 4)} for k, (n, t) in (pr or {}).items()}
                                  for pr in allprof],
             "note": "strong scaling: one batch over N GPUs; CUDA-event time of K back-to-back steps, max over ranks",
