@@ -158,7 +158,8 @@ typedef struct {
  * Errors (E_INVALID): p does not divide H or W; tiles_* outside [1, extent/p];
  * halo < 0; embed % heads; embed % 4; mlp_hidden != 4*embed; scale < 1;
  * K < 1; K > V without map; map entry outside [0,V); batch < 1; bad rank.
- * E_UNSUPPORTED: head_dim not in {32,64,128}; BF16 with embed % 64 != 0.
+ * E_UNSUPPORTED: head_dim not in {32,64,128}; BF16 with embed % 64 != 0;
+ * BF16 with K*(scale*patch)^2 % 8 != 0 (head-output rows must be 16-byte aligned).
  */
 orbit2_status orbit2_tiles_plan(const orbit2_config *cfg, orbit2_tile *tiles,
                                 int32_t capacity, orbit2_plan_info *info);

@@ -417,13 +417,23 @@ __global__ void decompress_kernel(const __nv_bfloat16* __restrict__ g, ChunkDev 
   const int u0 = max(p[1], cy), w0 = max(p[2], cx);
   const int u1 = min(p[1] + s, cy + t.core_h), w1 = min(p[2] + s, cx + t.core_w);
   if (u1 <= u0 || w1 <= w0) return;
-  const int nw = w1 - w0, npatch = (u1 - u0) * nw, n8 = Nh / 8;
-  const uint4* src = reinterpret_cast<const uint4*>(g + (int64_t)blockIdx.x * Nh);
+  const int nw = w1 - w0, npatch = (u1 - u0) * nw;
   const int64_t base = (int64_t)b * ch.chunk_core + (t.core_off - ch.core0);
-  for (int e = threadIdx.x; e < npatch * n8; e += blockDim.x) {
-    const int q = e / n8, c = e - q * n8;
-    const int u = u0 + q / nw, w = w0 + q % nw;
-    reinterpret_cast<uint4*>(tile_out + (base + (int64_t)(u - cy) * t.core_w + (w - cx)) * Nh)[c] = __ldg(src + c);
+  if (Nh % 8 == 0) {                                 // 16-byte rows: vector copies
+    const int n8 = Nh / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(g + (int64_t)blockIdx.x * Nh);
+    for (int e = threadIdx.x; e < npatch * n8; e += blockDim.x) {
+      const int q = e / n8, c = e - q * n8;
+      const int u = u0 + q / nw, w = w0 + q % nw;
+      reinterpret_cast<uint4*>(tile_out + (base + (int64_t)(u - cy) * t.core_w + (w - cx)) * Nh)[c] = __ldg(src + c);
+    }
+  } else {
+    const __nv_bfloat16* src = g + (int64_t)blockIdx.x * Nh;
+    for (int e = threadIdx.x; e < npatch * Nh; e += blockDim.x) {
+      const int q = e / Nh, c = e - q * Nh;
+      const int u = u0 + q / nw, w = w0 + q % nw;
+      tile_out[(base + (int64_t)(u - cy) * t.core_w + (w - cx)) * Nh + c] = src[c];
+    }
   }
 }
 

@@ -75,6 +75,8 @@ bool validate(const orbit2_config* c, std::string* msg, orbit2_status* st) {
   if (d != 32 && d != 64 && d != 128) return fail(msg, "heads: head_dim = embed/heads must be 32, 64 or 128");
   if (c->precision == ORBIT2_BF16 && c->embed % 64)
     return fail(msg, "embed: BF16 path needs embed % 64 == 0");
+  if (c->precision == ORBIT2_BF16 && (int64_t)c->K * c->scale * c->patch * c->scale * c->patch % 8)
+    return fail(msg, "K: BF16 path needs K * (scale * patch)^2 % 8 == 0 (16-byte head-output rows for the TMA store)");
   *st = ORBIT2_OK;
   return true;
 }

@@ -116,6 +116,17 @@ def test_unsupported_head_dim(o2):
     assert e.value.status == o2.E_UNSUPPORTED
 
 
+def test_bf16_head_rows_must_be_16_byte_aligned(o2):
+    """K (s p)^2 = 9 bf16 head outputs per token: BF16 rejects it (E_UNSUPPORTED, naming K),
+    FP32 plans it."""
+    w = get_config("C1", K=1, scale=3, patch=1)
+    with pytest.raises(o2.Orbit2Error) as e:
+        o2.orbit2_tiles_plan(o2.config_from(w, precision=o2.BF16))
+    assert e.value.status == o2.E_UNSUPPORTED and "K" in str(e.value)
+    _, info = o2.orbit2_tiles_plan(o2.config_from(w, precision=o2.FP32))
+    assert info.n_tiles == 4
+
+
 def test_capacity_two_call_sizing(o2):
     cfg = o2.config_from(get_config("C2"))
     info = o2.orbit2_plan_info()

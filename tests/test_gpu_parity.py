@@ -47,6 +47,15 @@ def test_parity_small(name, over, precision, tol):
     assert ev <= tol
 
 
+def test_parity_fp32_odd_head_width():
+    """FP32 path with K (s p)^2 = 1 * 3^2 = 9 head outputs per token (rows not 16-byte
+    aligned; the BF16 path rejects this at plan time), patch 1, ragged 3 x 5 tiles."""
+    w, x, blob = _case("C1", K=1, scale=3, patch=1, tiles_y=3, tiles_x=5, halo=2, depth=1)
+    ref, ref_vit, up = oracle_full(w, x, blob)
+    got = run_cuda(w, x, blob, FP32)
+    assert rel_err(got, ref) <= FP32_TOL and rel_err(got - up, ref_vit) <= FP32_TOL
+
+
 @pytest.mark.parametrize("precision,tol", [(FP32, FP32_TOL), (BF16, BF16_TOL)])
 def test_parity_C2_full_sample(precision, tol):
     """C2 (ERA5 1.0->0.25 deg, 9.5M-class) on one full sample: 16 tiles of
