@@ -560,7 +560,10 @@ bool launch_block_tail(const void* ao, int64_t rows_alloc, const void* wo, const
   const int sms = num_sms();
   const int64_t tiles = row_blocks != nullptr ? (int64_t)n_row_blocks : (M + BM - 1) / BM;
   if (tiles == 0) return true;
-  const int grid = (int)std::min<int64_t>(tiles, sms);
+#ifndef ORBIT2_BLOCK_GRID_DIV   // A/B experiments only: fewer persistent CTAs than SMs
+#define ORBIT2_BLOCK_GRID_DIV 1
+#endif
+  const int grid = (int)std::min<int64_t>(tiles, sms / ORBIT2_BLOCK_GRID_DIV);
   block_tc_kernel<<<grid, THREADS, SMEM, st>>>(ta, two, t1, t2, tz, txn, bo, ln2_g, ln2_b, b1, b2, ln1n_g, ln1n_b,
                                                M, row_blocks, n_row_blocks, g_mlp_timeline);
   return true;
