@@ -588,7 +588,10 @@ __global__ void __launch_bounds__(384, 1)
                 }
               } else {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = tc::gelu_erf_fast(v[j]);
+                for (int j = 0; j < 32; j += 2) {   // packed f32x2: half the FMA-pipe issues
+                  const float2 g2 = tc::gelu2_erf_fast(make_float2(v[j], v[j + 1]));
+                  v[j] = g2.x; v[j + 1] = g2.y;
+                }
               }
             }
             uint8_t* sb = my_stg + (nst & 1) * 2048;
