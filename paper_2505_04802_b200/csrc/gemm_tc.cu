@@ -229,8 +229,11 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 #ifndef ORBIT2_GEMM_WS
 #define ORBIT2_GEMM_WS 1
 #endif
+#ifndef ORBIT2_GEMM_PAIR   // 0: single-CTA tiles only (A/B builds)
+#define ORBIT2_GEMM_PAIR 1
+#endif
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS, bool WS = false>
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS, bool WS = false, bool PAIR = false>
 __global__ void __launch_bounds__(384, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmD, int64_t M,
@@ -248,7 +251,13 @@ __global__ void __launch_bounds__(384, 1)
   // number of column tiles, so a CTA keeps one column tile) streams only its
   // activation block through the ring: 3x less L2 -> SM traffic for the QKV GEMM.
   constexpr int A_BYTES = BM * BK * 2;
-  constexpr int B_BYTES = BN * BK * 2;
+  // PAIR (cta_group::2 on a 2-CTA cluster): a tile is 2 BM kernel rows x BN; CTA r loads A rows
+  // [m0 + BM r, + BM) and B rows [n0 + BN/2 r, + BN/2), the leader issues M = 2 BM MMAs, and
+  // each CTA's TMEM / epilogue holds its own BM rows: 2/3 of the L2 -> SM operand bytes per FLOP.
+  constexpr int BNL = PAIR ? BN / 2 : BN;   // B rows this CTA loads
+  constexpr int PM = PAIR ? 2 * BM : BM;    // kernel rows per tile
+  constexpr int B_BYTES = BNL * BK * 2;
+  static_assert(!PAIR || (!WS && EPI != EPI_RESID_LN && EPI != EPI_EMBED_LN), "pair: plain epilogues only");
   constexpr int WS_K = 256;
   constexpr int B_RING = WS ? (WS_K / BK) : STAGES;   // B atoms resident (WS) or ring slots
   constexpr uint32_t TMEM_COLS = 2 * BN;
@@ -272,12 +281,15 @@ __global__ void __launch_bounds__(384, 1)
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) && OUT_BF16 && !TRANS;
   const int nk = K / BK;
   const int64_t num_n = (Ncols + BN - 1) / BN;
-  const int64_t num_m = (M + BM - 1) / BM;
+  const int64_t num_m = (M + PM - 1) / PM;
   const int64_t num_tiles = num_m * num_n;
   auto tile_mn = [&](int64_t tile, int64_t& m0, int64_t& n0) {
-    if (TRANS) { m0 = (tile % num_m) * BM; n0 = (tile / num_m) * BN; }
-    else       { m0 = (tile / num_n) * BM; n0 = (tile % num_n) * BN; }
+    if (TRANS) { m0 = (tile % num_m) * PM; n0 = (tile / num_m) * BN; }
+    else       { m0 = (tile / num_n) * PM; n0 = (tile % num_n) * BN; }
   };
+  const uint32_t rank = PAIR ? tc::cluster_ctarank() : 0u;
+  const int64_t t_first = PAIR ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;   // pair index
+  const int64_t t_step = PAIR ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
   uint8_t* stg = sB + B_RING * B_BYTES;   // TMA-store staging: 8 warps x 2 x (32 x 32 bf16);
                                           // *_LN: 2 warpgroups x 2 x (128 x 32 fp32)
 
@@ -292,15 +304,20 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(&tfull[s], 1);
-      tc::mbar_init(&tempty[s], LN ? 128 : 256);   // *_LN: one warpgroup drains a buffer
+      // *_LN: one warpgroup drains a buffer; PAIR: one arrive per epilogue warp of both CTAs
+      tc::mbar_init(&tempty[s], PAIR ? 16 : LN ? 128 : 256);
     }
     for (int s = 0; s < 4; ++s) tc::mbar_init(&zfull[s], 1);
     tc::mbar_init(wfull, 1);
     tc::fence_barrier_init();
   }
-  if (warp == 2) tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) {
+    if constexpr (PAIR) tc::tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else tc::tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();   // both CTAs' barriers initialised before any remote signal
+  else __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -314,12 +331,19 @@ __global__ void __launch_bounds__(384, 1)
         tc::mbar_arrive_expect_tx(wfull, B_RING * B_BYTES);
         for (int kb = 0; kb < B_RING; ++kb) tc::tma_load_2d(&tmB, sB + kb * B_BYTES, wfull, kb * BK, (int32_t)n0);
       }
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int64_t tile = t_first; tile < num_tiles; tile += t_step) {
         int64_t m0, n0;
         tile_mn(tile, m0, n0);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t s = it % STAGES, ph = (it / STAGES) & 1;
           tc::mbar_wait(&empty[s], ph ^ 1);
+          if constexpr (PAIR) {   // both halves complete on the leader's full barrier
+            if (rank == 0) tc::mbar_arrive_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+            const uint32_t fb = tc::map_rank(tc::smem_u32(&full[s]), 0);
+            tc::tma_load_2d_pair(&tmA, sA + s * A_BYTES, fb, kb * BK, (int32_t)(m0 + rank * BM));
+            tc::tma_load_2d_pair(&tmB, sB + s * B_BYTES, fb, kb * BK, (int32_t)(n0 + rank * BNL));
+            continue;
+          }
           tc::mbar_arrive_expect_tx(&full[s], WS ? A_BYTES : A_BYTES + B_BYTES);
           tc::tma_load_2d(&tmA, sA + s * A_BYTES, &full[s], kb * BK, (int32_t)m0);
           if (!WS) tc::tma_load_2d(&tmB, sB + s * B_BYTES, &full[s], kb * BK, (int32_t)n0);
@@ -327,12 +351,12 @@ __global__ void __launch_bounds__(384, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, 0, 0);
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (PAIR: the leader CTA only) ----------------
+      constexpr uint32_t idesc = tc::idesc_bf16(PM, BN, 0, 0);
       uint32_t it = 0, lt = 0;
       if (WS) tc::mbar_wait(wfull, 0);
-      for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+      for (int64_t tile = t_first; tile < num_tiles; tile += t_step, ++lt) {
         const uint32_t buf = lt & 1;
         tc::mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
         tc::tc_fence_after();
@@ -346,11 +370,14 @@ __global__ void __launch_bounds__(384, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             const uint64_t ad = tc::sdesc(a0 + kk * 32, 16, 1024, tc::SW_128B);
             const uint64_t bd = tc::sdesc(b0 + kk * 32, 16, 1024, tc::SW_128B);
-            tc::mma_bf16_ss(acc, ad, bd, idesc, (kb | kk) != 0);
+            if constexpr (PAIR) tc::mma_bf16_ss_pair(acc, ad, bd, idesc, (kb | kk) != 0);
+            else tc::mma_bf16_ss(acc, ad, bd, idesc, (kb | kk) != 0);
           }
-          tc::mma_commit(&empty[s]);
+          if constexpr (PAIR) tc::mma_commit_pair(&empty[s]);   // frees the stage in both CTAs
+          else tc::mma_commit(&empty[s]);
         }
-        tc::mma_commit(&tfull[buf]);
+        if constexpr (PAIR) tc::mma_commit_pair(&tfull[buf]);
+        else tc::mma_commit(&tfull[buf]);
       }
     }
   } else if (LN && warp >= 4) {
@@ -370,7 +397,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* zf = zfull + wg * 2;
     uint32_t zuse[2] = {0, 0};                          // loads completed per buffer (parity)
     uint32_t lt = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t tile = t_first; tile < num_tiles; tile += t_step, ++lt) {
       if ((int)(lt & 1) != wg) continue;
       const uint32_t buf = lt & 1;
       int64_t m0, n0;
@@ -497,10 +524,11 @@ __global__ void __launch_bounds__(384, 1)
     const int half = (warp - 4) >> 2;        // column half
     uint8_t* my_stg = stg + (warp - 4) * 2 * 2048;
     uint32_t lt = 0, nst = 0;
-    for (int64_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++lt) {
+    for (int64_t tile = t_first; tile < num_tiles; tile += t_step, ++lt) {
       const uint32_t buf = lt & 1;
       int64_t m0, n0;
       tile_mn(tile, m0, n0);
+      m0 += rank * BM;                       // PAIR: this CTA's rows of the tile
       tc::mbar_wait(&tfull[buf], (lt >> 1) & 1);
       tc::tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
@@ -512,7 +540,12 @@ __global__ void __launch_bounds__(384, 1)
         tc::tmem_ld_wait();
         if (c0 + 32 >= (half + 1) * (BN / 2)) {   // my half read: hand the buffer back
           tc::tc_fence_before();
-          tc::mbar_arrive(&tempty[buf]);
+          if constexpr (PAIR) {                   // to the leader's barrier, one arrive per warp
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(tc::map_rank(tc::smem_u32(&tempty[buf]), 0));
+          } else {
+            tc::mbar_arrive(&tempty[buf]);
+          }
         }
         if constexpr (TRANS) {
           // rows = output features, columns = tokens: z[t][f] += acc + bias[f]
@@ -632,14 +665,16 @@ __global__ void __launch_bounds__(384, 1)
     if (TMA_OUT && lane == 0) tc::bulk_wait_all();
   }
   tc::tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) tc::cluster_sync();   // neither CTA leaves while the pair's MMAs / arrives target it
+  else __syncthreads();
   if (warp == 2) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, TMEM_COLS);
+    if constexpr (PAIR) tc::tmem_dealloc_pair(tmem, TMEM_COLS);
+    else tc::tmem_dealloc(tmem, TMEM_COLS);
   }
 }
 
-template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false, bool WS = false>
+template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS = false, bool WS = false, bool PAIR = false>
 bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t N, int64_t K, const EpiParams& ep,
                  cudaStream_t st) {
   // normal: kernel rows = activations A (M), cols = weights Bw (N)
@@ -652,7 +687,8 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
   // round_up(Din, 64)); the TMA zero-fills the rest of the K range
   if (!make_tmap_bf16(&ta, ka.ptr, ka.rows, ka.cols ? ka.cols : K, ka.ld, BM, BK, CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
-  if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, kb.cols ? kb.cols : K, kb.ld, BN, BK, CU_TENSOR_MAP_SWIZZLE_128B))
+  constexpr int BNL = PAIR ? BN / 2 : BN;
+  if (!make_tmap_bf16(&tb, kb.ptr, kb.rows, kb.cols ? kb.cols : K, kb.ld, BNL, BK, CU_TENSOR_MAP_SWIZZLE_128B))
     return false;
   constexpr bool TMA_OUT = (EPI == EPI_BIAS || EPI == EPI_GELU || EPI == EPI_DGELU) && OUT_BF16 && !TRANS;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
@@ -669,13 +705,29 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
     if (!make_tmap_bf16(&tdm, ep.xn, M, N, N, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
   }
   constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
-  constexpr int smem = STAGES * BM * BK * 2 + (WS ? 256 / BK : STAGES) * BN * BK * 2 + STG + 1024 + 256;
+  constexpr int smem = STAGES * BM * BK * 2 + (WS ? 256 / BK : STAGES) * BNL * BK * 2 + STG + 1024 + 256;
   static_assert(smem <= 227 * 1024, "shared memory");
   if (WS && K != 256) return false;
-  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS, WS>;
+  auto kern = gemm_tc_kernel<BN, STAGES, EPI, OUT_BF16, TRANS, WS, PAIR>;
   static std::atomic<uint64_t> attr_done{0};   // per instantiation, per device
   if (!smem_attr_once(reinterpret_cast<const void*>(kern), smem, &attr_done)) return false;
   const int64_t num_n = (Nk + BN - 1) / BN;
+  if (PAIR) {   // 2-CTA clusters, one pair per tile in flight: grid = 2 x min(tiles, SMs / 2)
+    const int64_t tiles = ((Mk + 2 * BM - 1) / (2 * BM)) * num_n;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(tiles, num_sms() / 2)));
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, tdm, Mk, Nk, (int)K, ep) == cudaSuccess;
+  }
   const int64_t tiles = ((Mk + BM - 1) / BM) * num_n;
   int grid = (int)std::min<int64_t>(tiles, num_sms());
   if (WS) grid = (int)std::max<int64_t>(num_n, grid / num_n * num_n);   // a CTA keeps one column tile
@@ -693,12 +745,32 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
     return epi == EPI_RESID_LN ? launch_impl<256, 3, EPI_RESID_LN, false>(A, Bw, M, N, K, ep, st)
                                : launch_impl<256, 3, EPI_EMBED_LN, false>(A, Bw, M, N, K, ep, st);
   }
+  // CTA pairs (cta_group::2) for BN = 256 GEMMs with at least one 256 x 256 tile per pair:
+  // the large GEMMs at D >= 1024 are bound by the L2 -> SM operand stream (~15.4 TB/s,
+  // profiles/r02az), which a pair cuts to 2/3 per FLOP
+  auto pair_ok = [&](int64_t Mk, int64_t Nk) {
+    return ORBIT2_GEMM_PAIR && ((Mk + 255) / 256) * ((Nk + 255) / 256) >= num_sms() / 2;
+  };
   // Residual update: transposed tiles (features on TMEM lanes) for coalesced z.
-  if (epi == EPI_RESID && N % BM == 0) return launch_impl<256, 3, EPI_RESID, false, true>(A, Bw, M, N, K, ep, st);
+  if (epi == EPI_RESID && N % BM == 0) {
+    if (pair_ok(N, M)) return launch_impl<256, 4, EPI_RESID, false, true, false, true>(A, Bw, M, N, K, ep, st);
+    return launch_impl<256, 3, EPI_RESID, false, true>(A, Bw, M, N, K, ep, st);
+  }
   // BN = 256 halves the shared-memory operand traffic per FLOP; 128 when N is
   // not a multiple of 256 (e.g. the decoder head, K*P*P = 192).
   if (N % 256 == 0) {
     constexpr int BN = 256, ST = 3;
+    if (pair_ok(M, N) && !(epi == EPI_BIAS && out_bf16 && K == 256 && ORBIT2_GEMM_WS)) {
+      switch (epi) {
+        case EPI_BIAS:
+          return out_bf16 ? launch_impl<BN, 4, EPI_BIAS, true, false, false, true>(A, Bw, M, N, K, ep, st)
+                          : launch_impl<BN, 4, EPI_BIAS, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_GELU: return launch_impl<BN, 4, EPI_GELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_RESID: return launch_impl<BN, 4, EPI_RESID, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_EMBED: return launch_impl<BN, 4, EPI_EMBED, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_DGELU: return launch_impl<BN, 4, EPI_DGELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
+      }
+    }
     switch (epi) {
       case EPI_BIAS:
         if (out_bf16 && K == 256 && ORBIT2_GEMM_WS)   // QKV at D = 256: weight-stationary
