@@ -232,6 +232,12 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 #ifndef ORBIT2_GEMM_PAIR   // 0: single-CTA tiles only (A/B builds)
 #define ORBIT2_GEMM_PAIR 1
 #endif
+#ifndef ORBIT2_PAIR_STAGES   // ring depth of the pair tiles (the residual GEMMs take one more)
+#define ORBIT2_PAIR_STAGES 4
+#endif
+#ifndef ORBIT2_GEMM_GELU_TANH   // tanh-form GELU (reading R28) in the inference MLP-up epilogue
+#define ORBIT2_GEMM_GELU_TANH 1
+#endif
 
 template <int BN, int STAGES, int EPI, bool OUT_BF16, bool TRANS, bool WS = false, bool PAIR = false>
 __global__ void __launch_bounds__(384, 1)
@@ -622,7 +628,8 @@ __global__ void __launch_bounds__(384, 1)
               } else {
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {   // packed f32x2: half the FMA-pipe issues
-                  const float2 g2 = tc::gelu2_erf_fast(make_float2(v[j], v[j + 1]));
+                  const float2 g2 = ORBIT2_GEMM_GELU_TANH ? tc::gelu2_tanh_fast(make_float2(v[j], v[j + 1]))
+                                                          : tc::gelu2_erf_fast(make_float2(v[j], v[j + 1]));
                   v[j] = g2.x; v[j + 1] = g2.y;
                 }
               }
@@ -748,12 +755,14 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
   // CTA pairs (cta_group::2) for BN = 256 GEMMs with at least one 256 x 256 tile per pair:
   // the large GEMMs at D >= 1024 are bound by the L2 -> SM operand stream (~15.4 TB/s,
   // profiles/r02az), which a pair cuts to 2/3 per FLOP
+  // (K >= 512: with 4 K-steps per tile the pair's longer tiles lose more than the operand
+  // savings win -- the D = 256 training GEMMs with K = 256 measured 6-10 % slower, r02bc)
   auto pair_ok = [&](int64_t Mk, int64_t Nk) {
-    return ORBIT2_GEMM_PAIR && ((Mk + 255) / 256) * ((Nk + 255) / 256) >= num_sms() / 2;
+    return ORBIT2_GEMM_PAIR && K >= 512 && ((Mk + 255) / 256) * ((Nk + 255) / 256) >= num_sms() / 2;
   };
   // Residual update: transposed tiles (features on TMEM lanes) for coalesced z.
   if (epi == EPI_RESID && N % BM == 0) {
-    if (pair_ok(N, M)) return launch_impl<256, 4, EPI_RESID, false, true, false, true>(A, Bw, M, N, K, ep, st);
+    if (pair_ok(N, M)) return launch_impl<256, ORBIT2_PAIR_STAGES + 1, EPI_RESID, false, true, false, true>(A, Bw, M, N, K, ep, st);
     return launch_impl<256, 3, EPI_RESID, false, true>(A, Bw, M, N, K, ep, st);
   }
   // BN = 256 halves the shared-memory operand traffic per FLOP; 128 when N is
@@ -763,12 +772,12 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
     if (pair_ok(M, N) && !(epi == EPI_BIAS && out_bf16 && K == 256 && ORBIT2_GEMM_WS)) {
       switch (epi) {
         case EPI_BIAS:
-          return out_bf16 ? launch_impl<BN, 4, EPI_BIAS, true, false, false, true>(A, Bw, M, N, K, ep, st)
-                          : launch_impl<BN, 4, EPI_BIAS, false, false, false, true>(A, Bw, M, N, K, ep, st);
-        case EPI_GELU: return launch_impl<BN, 4, EPI_GELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
-        case EPI_RESID: return launch_impl<BN, 4, EPI_RESID, false, false, false, true>(A, Bw, M, N, K, ep, st);
-        case EPI_EMBED: return launch_impl<BN, 4, EPI_EMBED, false, false, false, true>(A, Bw, M, N, K, ep, st);
-        case EPI_DGELU: return launch_impl<BN, 4, EPI_DGELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
+          return out_bf16 ? launch_impl<BN, ORBIT2_PAIR_STAGES, EPI_BIAS, true, false, false, true>(A, Bw, M, N, K, ep, st)
+                          : launch_impl<BN, ORBIT2_PAIR_STAGES, EPI_BIAS, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_GELU: return launch_impl<BN, ORBIT2_PAIR_STAGES, EPI_GELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_RESID: return launch_impl<BN, ORBIT2_PAIR_STAGES + 1, EPI_RESID, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_EMBED: return launch_impl<BN, ORBIT2_PAIR_STAGES, EPI_EMBED, false, false, false, true>(A, Bw, M, N, K, ep, st);
+        case EPI_DGELU: return launch_impl<BN, ORBIT2_PAIR_STAGES, EPI_DGELU, true, false, false, true>(A, Bw, M, N, K, ep, st);
       }
     }
     switch (epi) {
