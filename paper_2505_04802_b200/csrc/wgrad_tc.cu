@@ -116,26 +116,47 @@ __global__ void __launch_bounds__(256, 1)
     // ---------------- epilogue (thread = output row n0 + r) ----------------
     const int q = warp & 3;
     const int r = q * 32 + lane;
-    float bsum = 0.f;
-    if (bias) {   // column r of every dY stage (tokens past M are TMA zero-fill)
-      const uint8_t* col = sA + (r >> 6) * ATOM + (r & 7) * 2;
-      const int ch = (r & 63) >> 3;
+    // bias: thread (a, ch, g) = (r >> 6, (r >> 3) & 7, r & 7) sums the 8 columns
+    // 64 a + 8 ch + [0, 8) of dY over the tokens t = 8 i + g of every stage (16-byte loads;
+    // the 8 g-lanes of a chunk hit 8 different bank groups), then a 3-step shuffle over g
+    float bsum[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int ga = r >> 6, gch = (r >> 3) & 7, gg = r & 7;
+    if (bias) {   // tokens past M are TMA zero-fill
+      const uint8_t* abase = sA + ga * ATOM + gg * 128 + ((gch ^ gg) << 4);   // token g, swizzled chunk
       for (int c = 0; c < nck; ++c) {
         const uint32_t s = c % STAGES, ph = (c / STAGES) & 1;
         tc::mbar_wait(&full[s], ph);
-        const uint8_t* base = col + s * C::A_BYTES;
-        float acc = 0.f;
-#pragma unroll 8
-        for (int t = 0; t < TK; ++t)
-          acc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(base + t * 128 + ((ch ^ (t & 7)) << 4)));
-        bsum += acc;
+        const uint8_t* base = abase + s * C::A_BYTES;
+#pragma unroll
+        for (int i = 0; i < TK / 8; ++i) {   // token 8 i + g: same swizzle phase (t & 7 == g)
+          const uint4 w = *reinterpret_cast<const uint4*>(base + i * 8 * 128);
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(h[e]);
+            bsum[2 * e] += f.x;
+            bsum[2 * e + 1] += f.y;
+          }
+        }
         tc::mbar_arrive(&empty[s]);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        bsum[j] += __shfl_xor_sync(0xffffffffu, bsum[j], 1);
+        bsum[j] += __shfl_xor_sync(0xffffffffu, bsum[j], 2);
+        bsum[j] += __shfl_xor_sync(0xffffffffu, bsum[j], 4);
       }
     }
     tc::mbar_wait(done, 0);
     tc::tc_fence_after();
+    if (bias && gg == 0 && nck > 0) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int nb = n0 + ga * 64 + gch * 8 + j;
+        if (nb < N) atomicAdd(dbias + nb, bsum[j]);
+      }
+    }
     const int n = n0 + r;
-    if (bias && n < N && nck > 0) atomicAdd(dbias + n, bsum);
     const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16);
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -178,12 +199,32 @@ bool launch_bn(const GemmOperand& A, const GemmOperand& X, int64_t M, int N, int
   const int64_t chunks = (M + TK - 1) / TK;
   // split the token range (each split >= 16 chunks = 1024 tokens) so the grid fills whole
   // waves of SMs as well as possible: tiles x splits / (SMs x waves), the fewest splits among
-  // the best (fewer fp32 atomics); at most max(8 splits, 4 waves)
+  // the best (fewer fp32 atomics); at most max(32 splits, 16 waves): many short CTAs also
+  // spread the slower bias-summing tiles (C3 QKV weight gradient 28.8 -> 20.9 ms, r02bf)
   const int sms = num_sms();
-  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(std::max<int64_t>(8, 4LL * sms / tiles), chunks / 16));
-  int64_t splits = 1;
+#ifndef ORBIT2_WGRAD_SPLITS_BASE   // many short CTAs balance the bias-summing tiles (r02bf)
+#define ORBIT2_WGRAD_SPLITS_BASE 32
+#endif
+#ifndef ORBIT2_WGRAD_WAVES
+#define ORBIT2_WGRAD_WAVES 16
+#endif
+#ifndef ORBIT2_WGRAD_SPLITS_MAX   // A/B experiments: cap on the token splits
+#define ORBIT2_WGRAD_SPLITS_MAX 1 << 30
+#endif
+  const int64_t smax = std::max<int64_t>(
+      1, std::min<int64_t>({std::max<int64_t>(ORBIT2_WGRAD_SPLITS_BASE, (int64_t)ORBIT2_WGRAD_WAVES * sms / tiles),
+                            chunks / 16, (int64_t)(ORBIT2_WGRAD_SPLITS_MAX)}));
+#ifndef ORBIT2_WGRAD_CHUNK_TARGET   // > 0: at most this many 64-token chunks per CTA (A/B experiments)
+#define ORBIT2_WGRAD_CHUNK_TARGET 0
+#endif
+  int64_t splits = 1, sp_lo = 1, sp_hi = smax;
+  if (ORBIT2_WGRAD_CHUNK_TARGET > 0) {   // short token ranges: the CTAs sharing a range stay within L2 reach
+    sp_lo = std::max<int64_t>(1, (chunks + ORBIT2_WGRAD_CHUNK_TARGET - 1) / ORBIT2_WGRAD_CHUNK_TARGET);
+    sp_hi = 2 * sp_lo;
+    splits = sp_lo;
+  }
   double best = 0.0;
-  for (int64_t sp = 1; sp <= smax; ++sp) {
+  for (int64_t sp = sp_lo; sp <= sp_hi; ++sp) {
     const int64_t ctas = tiles * sp, waves = (ctas + sms - 1) / sms;
     const double eff = (double)ctas / (double)(waves * sms);
     if (eff > best + 0.02) {
