@@ -758,7 +758,7 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
   // (K >= 512: with 4 K-steps per tile the pair's longer tiles lose more than the operand
   // savings win -- the D = 256 training GEMMs with K = 256 measured 6-10 % slower, r02bc)
   auto pair_ok = [&](int64_t Mk, int64_t Nk) {
-    return ORBIT2_GEMM_PAIR && K >= 512 && ((Mk + 255) / 256) * ((Nk + 255) / 256) >= num_sms() / 2;
+    return ORBIT2_GEMM_PAIR && !ep.single_cta && K >= 512 && ((Mk + 255) / 256) * ((Nk + 255) / 256) >= num_sms() / 2;
   };
   // Residual update: transposed tiles (features on TMEM lanes) for coalesced z.
   if (epi == EPI_RESID && N % BM == 0) {

@@ -43,6 +43,7 @@ struct EpiParams {
   // reads the residual input from here (fp32, same ldc) instead of C (C = aux + acc + bias);
   // EPI_DGELU: the GELU' factor it multiplies by
   const void* aux = nullptr;
+  int32_t single_cta = 0;  // host-side: 1 = no CTA-pair tiles (ORBIT2_SINGLE_CTA_GEMM=1, tests / A/B)
 };
 
 struct GemmOperand {

@@ -59,6 +59,7 @@ struct Ctx {
   bool trace = false;         // ORBIT2_TRACE=1: kernel names to stderr before each launch (hang hunting)
   bool unfused_mlp = false;   // ORBIT2_UNFUSED_MLP=1: two GEMMs instead of mlp_fused (D = 256)
   bool unfused_ln = false;    // ORBIT2_UNFUSED_LN=1: separate LayerNorm kernels after embed / O-proj
+  int single_cta_gemm = 0;    // ORBIT2_SINGLE_CTA_GEMM=1: no CTA-pair GEMM tiles (bit-exactness tests)
   bool unfused_block = false; // ORBIT2_UNFUSED_BLOCK=1: O-proj(+LN2) GEMM and fused MLP as two kernels (D = 256)
   bool all_queries_last = false;  // ORBIT2_ALL_QUERIES_LAST=1: last block's attention over every query pair
   bool simt_gather = false;       // ORBIT2_SIMT_GATHER=1: smem-staged SIMT gather instead of the TMA one
@@ -242,6 +243,8 @@ orbit2_status orbit2_create(const orbit2_config* cfg, void* workspace_dev, size_
   c->unfused_mlp = um && um[0] == '1';
   const char* ul = std::getenv("ORBIT2_UNFUSED_LN");
   c->unfused_ln = ul && ul[0] == '1';
+  const char* sct = std::getenv("ORBIT2_SINGLE_CTA_GEMM");
+  c->single_cta_gemm = sct && sct[0] == '1';
   const char* ub = std::getenv("ORBIT2_UNFUSED_BLOCK");
   c->unfused_block = ub && ub[0] == '1';
   const char* aq = std::getenv("ORBIT2_ALL_QUERIES_LAST");
@@ -444,7 +447,10 @@ orbit2_status orbit2_reslim_forward(void* ctx, const void* packed_w, const float
       GemmOperand a{A, arows, lda, acols}, b{W8 + wo, n, k};
       ep.M = (int32_t)rows;
       ep.N = (int32_t)n;
-      return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+      return run(c, name, st, [&] {
+        ep.single_cta = c->single_cta_gemm;
+        return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st);
+      });
     };
     // step (1): TMA-staged gather (CLAMP halos) into patch rows of ld_patch columns;
     // the smem-staged SIMT gather with zero-padded rows otherwise (REPLICATE halos
@@ -1105,7 +1111,10 @@ orbit2_status orbit2_train_forward(void* ctx, const void* packed_w, const float*
     GemmOperand a{A, R, lda, acols}, b{W8 + wo, n, k};
     ep.M = (int32_t)rows;
     ep.N = (int32_t)n;
-    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+    return run(c, name, st, [&] {
+      ep.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st);
+    });
   };
   int64_t lda_patch = ly.din_pad, cols_patch = 0;
   if (cf.halo_mode == ORBIT2_HALO_CLAMP && !c->simt_gather) {
@@ -1137,7 +1146,10 @@ orbit2_status orbit2_train_forward(void* ctx, const void* packed_w, const float*
     GemmOperand a{patches, ly.mrow, lda_patch, cols_patch}, b{W8 + w.w_e, D, ly.din_pad};
     emb.M = (int32_t)M;
     emb.N = (int32_t)D;
-    ORBIT2_TRY(run(c, "embed_gemm", st, [&] { return launch_gemm_tc(EPI_EMBED, 0, a, b, M, D, ly.din_pad, emb, st); }));
+    ORBIT2_TRY(run(c, "embed_gemm", st, [&] {
+      emb.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(EPI_EMBED, 0, a, b, M, D, ly.din_pad, emb, st);
+    }));
   }
   for (int l = 0; l < cf.depth; ++l) {
     const LayerW& L = w.layers[l];
@@ -1178,7 +1190,10 @@ orbit2_status orbit2_train_forward(void* ctx, const void* packed_w, const float*
   e.bias = wf(w.b_h); e.C = tile_out_dev; e.ldc = p.Nh; e.M = (int32_t)Mc; e.N = p.Nh;
   {
     GemmOperand a{hin, t.rows_core, D, 0}, b{W8 + w.w_h, p.Nh, D};
-    ORBIT2_TRY(run(c, "head_gemm", st, [&] { return launch_gemm_tc(EPI_BIAS, 1, a, b, Mc, p.Nh, D, e, st); }));
+    ORBIT2_TRY(run(c, "head_gemm", st, [&] {
+      e.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(EPI_BIAS, 1, a, b, Mc, p.Nh, D, e, st);
+    }));
   }
   return ORBIT2_OK;
 }
@@ -1236,7 +1251,10 @@ orbit2_status orbit2_train_backward(void* ctx, const void* packed_w, const float
     GemmOperand a{A, arows, lda, acols}, b{Bt, n, k};
     EpiParams ep{};
     ep.M = (int32_t)rows; ep.N = (int32_t)n; ep.bias = zero; ep.C = C; ep.ldc = ldc; ep.aux = aux;
-    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st); });
+    return run(c, name, st, [&] {
+      ep.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(epi, out_bf, a, b, rows, n, k, ep, st);
+    });
   };
   auto wg = [&](const char* name, const void* dY, int64_t ldy, const void* X, int64_t ldx, int64_t rows, int n,
                 int kc, int64_t gw, int64_t gb) {
@@ -1557,7 +1575,10 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     emb.rowinfo = rowinfo; emb.pos_u = c->at<float>(ly.pos_u); emb.pos_w = c->at<float>(ly.pos_w);
     emb.pos_off = cf.halo; emb.half = (int32_t)(D / 2);
     GemmOperand a{patches, mrow, ly.din_pad, 0}, b{W8 + w.w_e, D, ly.din_pad};
-    ORBIT2_TRY(run(c, "embed_gemm", st, [&] { return launch_gemm_tc(EPI_EMBED, 0, a, b, M0, D, ly.din_pad, emb, st); }));
+    ORBIT2_TRY(run(c, "embed_gemm", st, [&] {
+      emb.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(EPI_EMBED, 0, a, b, M0, D, ly.din_pad, emb, st);
+    }));
   }
   // 3: every (sample, tile) rectangle's field and its partition (Canny + quad-tree, patch grid)
   float* field = reinterpret_cast<float*>(cw + L.field);
@@ -1667,7 +1688,10 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     GemmOperand a{A, mrow, lda, 0}, b{W8 + wo, nn, k};
     ep.M = (int32_t)M;
     ep.N = (int32_t)nn;
-    return run(c, name, st, [&] { return launch_gemm_tc(epi, out_bf, a, b, M, nn, k, ep, st); });
+    return run(c, name, st, [&] {
+      ep.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(epi, out_bf, a, b, M, nn, k, ep, st);
+    });
   };
   const bool tail_fused = D == 256;
   for (int l = 0; l < cf.depth && M > 0; ++l) {
@@ -1716,7 +1740,10 @@ orbit2_status orbit2_compressed_forward(void* ctx, const void* packed_w, const f
     EpiParams ep{};
     ep.bias = wf(w.b_h); ep.C = g; ep.ldc = p.Nh; ep.M = (int32_t)M; ep.N = p.Nh;
     GemmOperand a{hin, mrow, D, 0}, b{W8 + w.w_h, p.Nh, D};
-    ORBIT2_TRY(run(c, "head_gemm", st, [&] { return launch_gemm_tc(EPI_BIAS, 1, a, b, M, p.Nh, D, ep, st); }));
+    ORBIT2_TRY(run(c, "head_gemm", st, [&] {
+      ep.single_cta = c->single_cta_gemm;
+      return launch_gemm_tc(EPI_BIAS, 1, a, b, M, p.Nh, D, ep, st);
+    }));
   }
   return run(c, "decompress", st, [&] {
     launch_decompress(g, cd, T, leaves, n, p.Nh, reinterpret_cast<bf16*>(tile_out_dev), st);

@@ -312,6 +312,21 @@ def test_unfused_paths_match_oracle(env, monkeypatch):
 
 
 @pytest.mark.gpu
+def test_cta_pair_gemms_bit_identical_and_match_oracle(monkeypatch):
+    """D = 512, B = 2 (~11k token rows): the QKV, MLP-up, MLP-down and O-projection GEMMs
+    are large enough (K >= 512, >= 74 256 x 256 tiles) to run as CTA pairs
+    (cta_group::2).  Same output bits as the single-CTA tiles (ORBIT2_SINGLE_CTA_GEMM=1),
+    and within the bf16 tolerance of the oracle."""
+    w, x, blob = _case("C2", batch=2, H=96, W=192, embed=512, heads=8, depth=1)
+    pair = run_cuda(w, x, blob, BF16)
+    monkeypatch.setenv("ORBIT2_SINGLE_CTA_GEMM", "1")
+    single = run_cuda(w, x, blob, BF16)
+    assert np.array_equal(pair, single)
+    ref = oracle_full(w, x, blob)[0]
+    assert rel_err(pair, ref) <= BF16_TOL
+
+
+@pytest.mark.gpu
 def test_forward_host_pipelined_matches_device_forward():
     """Context.forward_host (pinned host in/out, groups of the context batch with
     the PCIe copies overlapped on side streams) is bit-identical to the
