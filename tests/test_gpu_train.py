@@ -177,6 +177,24 @@ def test_train_step_wide_model_matches_oracle():
     _check_grads(pr, grad, ref_grad)
 
 
+def test_train_step_cta_pair_gemms_match_oracle(monkeypatch):
+    """D = 512 (8 heads of 64) on a 48 x 96 grid, B = 2 (~3.6k token rows): the forward QKV
+    and MLP-up GEMMs and the MLP-down input gradient (K >= 512, >= 74 256 x 256 tiles) run as
+    CTA pairs (cta_group::2).  Loss and every gradient within tolerance of the oracle, with
+    the pairs and with single-CTA tiles (ORBIT2_SINGLE_CTA_GEMM=1)."""
+    w, pr, blob, x, y = _problem_and_data(H=48, W=96, embed=512, heads=8, depth=1, batch=2, seed=13)
+    lam, delta = 0.05, 0.02
+    ref_loss, ref_grad = T.train_step_grads(x.astype(np.float64), y.astype(np.float64), blob.astype(np.float64),
+                                            pr, lam, delta)
+    _, loss, grad, _ = _gpu_step(w, x, y, blob, lam, delta)
+    assert abs(loss.mean() - ref_loss) <= LOSS_TOL * abs(ref_loss)
+    _check_grads(pr, grad, ref_grad)
+    monkeypatch.setenv("ORBIT2_SINGLE_CTA_GEMM", "1")
+    _, loss1, grad1, _ = _gpu_step(w, x, y, blob, lam, delta)
+    assert abs(loss1.mean() - ref_loss) <= LOSS_TOL * abs(ref_loss)
+    _check_grads(pr, grad1, ref_grad)
+
+
 def test_adamw_step_matches_oracle():
     """orbit2_adamw_step (R43) over three steps == oracle T5 (fp32 kernel vs fp64)."""
     import torch
