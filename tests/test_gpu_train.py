@@ -178,11 +178,13 @@ def test_train_step_wide_model_matches_oracle():
 
 
 def test_train_step_cta_pair_gemms_match_oracle(monkeypatch):
-    """D = 512 (8 heads of 64) on a 48 x 96 grid, B = 2 (~3.6k token rows): the forward QKV
-    and MLP-up GEMMs and the MLP-down input gradient (K >= 512, >= 74 256 x 256 tiles) run as
-    CTA pairs (cta_group::2).  Loss and every gradient within tolerance of the oracle, with
-    the pairs and with single-CTA tiles (ORBIT2_SINGLE_CTA_GEMM=1)."""
-    w, pr, blob, x, y = _problem_and_data(H=48, W=96, embed=512, heads=8, depth=1, batch=2, seed=13)
+    """D = 512 (8 heads of 64) on a 48 x 96 grid, B = 6 (~10.7k token rows): every GEMM of
+    the step with K >= 512 and >= 74 256 x 256 tiles runs as a CTA pair (cta_group::2) --
+    the forward QKV / MLP-up (bf16 out), the residual GEMMs (transposed fp32 epilogue), the
+    MLP-down input gradient (EPI_DGELU) and the fp32 input gradients.  Loss and every
+    gradient within tolerance of the oracle, with the pairs and with single-CTA tiles
+    (ORBIT2_SINGLE_CTA_GEMM=1)."""
+    w, pr, blob, x, y = _problem_and_data(H=48, W=96, embed=512, heads=8, depth=1, batch=6, seed=13)
     lam, delta = 0.05, 0.02
     ref_loss, ref_grad = T.train_step_grads(x.astype(np.float64), y.astype(np.float64), blob.astype(np.float64),
                                             pr, lam, delta)
