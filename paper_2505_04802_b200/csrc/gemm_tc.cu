@@ -232,6 +232,15 @@ __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row,
 #ifndef ORBIT2_GEMM_PAIR   // 0: single-CTA tiles only (A/B builds)
 #define ORBIT2_GEMM_PAIR 1
 #endif
+// Epilogue global loads one chunk ahead (A/B, profiles/r02bl): the GELU' chunk of the DGELU
+// epilogue gains (C2 training dx_mlp_down 10.38 -> 10.04 ms); the residual z chunk of the
+// transposed residual GEMMs loses (C3 O-projection 6.90 -> 7.25 ms), so it is off.
+#ifndef ORBIT2_EPI_PREFETCH_A
+#define ORBIT2_EPI_PREFETCH_A 1
+#endif
+#ifndef ORBIT2_EPI_PREFETCH_Z
+#define ORBIT2_EPI_PREFETCH_Z 0
+#endif
 #ifndef ORBIT2_PAIR_STAGES   // ring depth of the pair tiles (the residual GEMMs take one more)
 #define ORBIT2_PAIR_STAGES 4
 #endif
@@ -539,8 +548,49 @@ __global__ void __launch_bounds__(384, 1)
       tc::tc_fence_after();
       const int64_t row = m0 + q * 32 + lane;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN;
+      // Loads the epilogue needs from global memory (TRANS: the residual z chunk; DGELU: the
+      // GELU' chunk) are issued one chunk ahead, so their latency overlaps the current chunk.
+      constexpr bool PF_Z = ORBIT2_EPI_PREFETCH_Z && TRANS && EPI == EPI_RESID;
+      constexpr bool PF_A = ORBIT2_EPI_PREFETCH_A && TMA_OUT && EPI == EPI_DGELU;
+      float zpf[PF_Z ? 32 : 1];
+      uint4 apf[PF_A ? 4 : 1];
+      auto z_full = [&](int c) { return row < M && n0 + c + 32 <= ep.M; };
+      auto z_src = [&](int c) {
+        return ep.aux ? reinterpret_cast<const float*>(ep.aux) + (n0 + c) * ep.ldc + row
+                      : reinterpret_cast<const float*>(ep.C) + (n0 + c) * ep.ldc + row;
+      };
+      auto a_full = [&](int c) { return row < M && n0 + c + 32 <= ep.N; };
+      auto prefetch = [&](int c) {
+        if constexpr (PF_Z) {
+          if (z_full(c)) {
+            const float* zs = z_src(c);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) zpf[j] = zs[(int64_t)j * ep.ldc];
+          }
+        }
+        if constexpr (PF_A) {
+          if (a_full(c)) {
+            const uint4* a4 = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(ep.aux) +
+                                                             row * ep.ldc + n0 + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) apf[u] = __ldg(a4 + u);
+          }
+        }
+      };
+      prefetch(half * (BN / 2));
 #pragma unroll 1
       for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+        float zcur[PF_Z ? 32 : 1];
+        uint4 acur[PF_A ? 4 : 1];
+        if constexpr (PF_Z) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) zcur[j] = zpf[j];
+        }
+        if constexpr (PF_A) {
+#pragma unroll
+          for (int u = 0; u < 4; ++u) acur[u] = apf[u];
+        }
+        if (c0 + 32 < (half + 1) * (BN / 2)) prefetch(c0 + 32);
         uint32_t r[32];
         tc::tmem_ld32(taddr + c0, r);
         tc::tmem_ld_wait();
@@ -564,7 +614,7 @@ __global__ void __launch_bounds__(384, 1)
             if (t0 + 32 <= ep.M) {
               float zv[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) zv[j] = zs[(int64_t)j * ep.ldc];
+              for (int j = 0; j < 32; ++j) zv[j] = PF_Z ? zcur[PF_Z ? j : 0] : zs[(int64_t)j * ep.ldc];
 #pragma unroll
               for (int j = 0; j < 32; ++j) zc[(int64_t)j * ep.ldc] = zv[j] + (__uint_as_float(r[j]) + bf);
             } else {
@@ -582,7 +632,7 @@ __global__ void __launch_bounds__(384, 1)
                                                                  row * ep.ldc + n0 + c0);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                  const uint4 w = __ldg(a4 + u);
+                  const uint4 w = PF_A ? acur[PF_A ? u : 0] : __ldg(a4 + u);
                   const __nv_bfloat162* hp = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
                   for (int e = 0; e < 4; ++e) {
