@@ -130,6 +130,14 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 constexpr int LN_CHUNK_BYTES = BM * 32 * 4;   // *_LN staging: 128 rows x 32 fp32 columns (16 KB)
+// *_LN staging buffers per warpgroup: the embedding epilogue (K = Din: a short main loop, the
+// epilogue is the kernel) keeps 4 so a chunk's store rarely waits for the one before last to
+// have read its buffer; the residual form keeps 2 (its z loads are tied to 2 barriers)
+#ifndef ORBIT2_EMBED_LN_BUFS
+#define ORBIT2_EMBED_LN_BUFS 4
+#endif
+template <int EPI>
+__host__ __device__ constexpr int ln_bufs() { return EPI == EPI_EMBED_LN ? ORBIT2_EMBED_LN_BUFS : 2; }
 
 template <int EPI, bool OUT_BF16>
 __device__ __forceinline__ void epilogue_chunk(const EpiParams& ep, int64_t row, int n0, const uint32_t (&r)[32]) {
@@ -278,7 +286,8 @@ __global__ void __launch_bounds__(384, 1)
   constexpr uint32_t TMEM_COLS = 2 * BN;
   constexpr bool LN = EPI == EPI_RESID_LN || EPI == EPI_EMBED_LN;
   // GELU: a second staging set for the training forward's GELU' store (aux)
-  constexpr int STG_BYTES = LN ? 2 * 2 * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
+  constexpr int LNB = ln_bufs<EPI>();
+  constexpr int STG_BYTES = LN ? 2 * LNB * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // align inside the __shared__ array (keeps the shared address space: STS, not generic ST)
   uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -408,7 +417,7 @@ __global__ void __launch_bounds__(384, 1)
     const int rr = q * 32 + lane;                       // row within the tile
     const bool issuer = q == 0 && lane == 0;
     const uint32_t nb = 1 + wg;                         // named barrier of this warpgroup
-    uint8_t* zb = stg + wg * 2 * LN_CHUNK_BYTES;
+    uint8_t* zb = stg + wg * LNB * LN_CHUNK_BYTES;
     uint64_t* zf = zfull + wg * 2;
     uint32_t zuse[2] = {0, 0};                          // loads completed per buffer (parity)
     uint32_t lt = 0;
@@ -435,12 +444,12 @@ __global__ void __launch_bounds__(384, 1)
       float sum = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 8; ++c) {
-        uint8_t* sb = zb + (c & 1) * LN_CHUNK_BYTES + rr * 128;   // this row's 128 bytes (SW128)
+        uint8_t* sb = zb + (c % LNB) * LN_CHUNK_BYTES + rr * 128;   // this row's 128 bytes (SW128)
         if (EPI == EPI_RESID_LN) {
           tc::mbar_wait(&zf[c & 1], zuse[c & 1] & 1);
           ++zuse[c & 1];
         } else {                                         // staging reuse: the buffer's last store has read it
-          if (issuer) tc::bulk_wait_read<1>();
+          if (issuer) tc::bulk_wait_read<LNB - 1>();
           asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
         }
         uint32_t r[32];
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(384, 1)
         tc::fence_proxy_async_smem();
         asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
         if (issuer) {
-          tc::tma_store_2d(&tmC, zb + (c & 1) * LN_CHUNK_BYTES, c * 32, (int32_t)m0);
+          tc::tma_store_2d(&tmC, zb + (c % LNB) * LN_CHUNK_BYTES, c * 32, (int32_t)m0);
           tc::bulk_commit();
           if (EPI == EPI_RESID_LN && c + 2 < 8) load_z(c + 2);
         }
@@ -503,8 +512,8 @@ __global__ void __launch_bounds__(384, 1)
           tc::tc_fence_before();
           tc::mbar_arrive(&tempty[buf]);
         }
-        uint8_t* sb = zb + (c & 1) * LN_CHUNK_BYTES;    // bf16 box [128 rows][64 B], SWIZZLE_64B
-        if (issuer) tc::bulk_wait_read<1>();
+        uint8_t* sb = zb + (c % LNB) * LN_CHUNK_BYTES;    // bf16 box [128 rows][64 B], SWIZZLE_64B
+        if (issuer) tc::bulk_wait_read<LNB - 1>();
         asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
         const float4* g4 = reinterpret_cast<const float4*>(ep.ln_g + c * 32);
         const float4* e4 = reinterpret_cast<const float4*>(ep.ln_b + c * 32);
@@ -761,7 +770,7 @@ bool launch_impl(const GemmOperand& A, const GemmOperand& Bw, int64_t M, int64_t
     if (!make_tmap_f32(&tcm, ep.C, M, N, ep.ldc, BM, 32, CU_TENSOR_MAP_SWIZZLE_128B)) return false;
     if (!make_tmap_bf16(&tdm, ep.xn, M, N, N, BM, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return false;
   }
-  constexpr int STG = LN ? 2 * 2 * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
+  constexpr int STG = LN ? 2 * ln_bufs<EPI>() * LN_CHUNK_BYTES : (EPI == EPI_GELU ? 2 : 1) * 8 * 2 * 2048;
   constexpr int smem = STAGES * BM * BK * 2 + (WS ? 256 / BK : STAGES) * BNL * BK * 2 + STG + 1024 + 256;
   static_assert(smem <= 227 * 1024, "shared memory");
   if (WS && K != 256) return false;
@@ -800,7 +809,7 @@ bool launch_gemm_tc(int epi, int out_bf16, const GemmOperand& A, const GemmOpera
   if (epi == EPI_RESID_LN || epi == EPI_EMBED_LN) {   // whole rows in one 256-column tile
     if (N != 256 || ep.ldc != 256) return false;
     return epi == EPI_RESID_LN ? launch_impl<256, 3, EPI_RESID_LN, false>(A, Bw, M, N, K, ep, st)
-                               : launch_impl<256, 3, EPI_EMBED_LN, false>(A, Bw, M, N, K, ep, st);
+                               : launch_impl<256, (ORBIT2_EMBED_LN_BUFS > 2 ? 2 : 3), EPI_EMBED_LN, false>(A, Bw, M, N, K, ep, st);
   }
   // CTA pairs (cta_group::2) for BN = 256 GEMMs with at least one 256 x 256 tile per pair:
   // the large GEMMs at D >= 1024 are bound by the L2 -> SM operand stream (~15.4 TB/s,
