@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (tlr) TL3(qt, cs, 4);
         // p = 2^(s log2(e)/sqrt(d) - m_ref) -> bf16 P in TMEM (A operand of PV), fp32 row sums
         uint32_t pk[KB / 2];
-        float2 rs = make_float2(0.f, 0.f);
+        float2 rs[ORBIT2_ATTN3_RS_SPLIT];   // independent partial sums (no 32-long add chain)
+#pragma unroll
+        for (int u = 0; u < ORBIT2_ATTN3_RS_SPLIT; ++u) rs[u] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int e = 0; e < KB; e += 2) {
           float x0 = sv[e], x1 = sv[e + 1];
@@ -417,15 +419,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           float2 pr;
           if ((e & 15) < kPolyPer16) pr = ex2_poly2(x0, x1);
           else pr = make_float2(ex2(x0), ex2(x1));
-          rs = tc::add2(rs, pr);
+          rs[(e / 2) % ORBIT2_ATTN3_RS_SPLIT] = tc::add2(rs[(e / 2) % ORBIT2_ATTN3_RS_SPLIT], pr);
           pk[e / 2] = tc::pack_bf16(pr.x, pr.y);
         }
+#pragma unroll
+        for (int u = 1; u < ORBIT2_ATTN3_RS_SPLIT; ++u) rs[0] = tc::add2(rs[0], rs[u]);
         tc::tmem_st32(p_tm, pk);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         tc::mbar_arrive(&p_full[qt]);
         if (tlr) TL3(qt, cs, 5);
-        l_run += rs.x + rs.y;
+        l_run += rs[0].x + rs[0].y;
       }
       // epilogue: O / l  (wait for the item's last PV)
       tc::mbar_wait(&p_free[qt], (cs - 1) & 1);

@@ -646,7 +646,11 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
             for (int c0 = h * KP; c0 < (h + 1) * KP; c0 += 64) {
               if (kTailSkip && SPW == 1 && c0 >= kv_blk) break;   // half past the tile end
               uint32_t pk[32];
-              float2 rs = make_float2(0.f, 0.f);
+              // ORBIT2_ATTN_RS_SPLIT independent packed partial sums: the row sum is not one
+              // 32-long chain of dependent adds behind the exponentials
+              float2 rs[ORBIT2_ATTN_RS_SPLIT];
+#pragma unroll
+              for (int u = 0; u < ORBIT2_ATTN_RS_SPLIT; ++u) rs[u] = make_float2(0.f, 0.f);
 #pragma unroll
               for (int e = 0; e < 64; e += 2) {
                 float x0 = sv[c0 + e], x1 = sv[c0 + e + 1];
@@ -654,11 +658,13 @@ __global__ void __launch_bounds__(AttnCfg<DH, NQ>::THREADS, 1)
                 float2 pr;
                 if ((e & 15) < kPolyPer16) pr = ex2_poly2(x0, x1);
                 else pr = make_float2(ex2(x0), ex2(x1));
-                rs = tc::add2(rs, pr);                     // packed row-sum accumulation
+                rs[(e / 2) % ORBIT2_ATTN_RS_SPLIT] = tc::add2(rs[(e / 2) % ORBIT2_ATTN_RS_SPLIT], pr);
                 pk[e / 2] = tc::pack_bf16(pr.x, pr.y);     // column = keys (2c, 2c+1), lower key in low half
               }
-              rs0 += rs.x;
-              rs1 += rs.y;
+#pragma unroll
+              for (int u = 1; u < ORBIT2_ATTN_RS_SPLIT; ++u) rs[0] = tc::add2(rs[0], rs[u]);
+              rs0 += rs[0].x;
+              rs1 += rs[0].y;
               tc::tmem_st32(p_tm + c0 / 2, pk);
               if (desync && qt == 0 && c0 == c_arr) asm volatile("bar.arrive %0, 64;" ::"r"(dbar) : "memory");
             }

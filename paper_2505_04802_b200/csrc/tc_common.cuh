@@ -10,6 +10,16 @@
 
 #include <cstdint>
 
+// attention kernels: independent packed partial row sums per 64-key chunk (1 = one chain);
+// profiles/r02bp: 4 sums take the two-Q-tile kernel 19.21 -> 18.91 ms at C2 (8: 19.96), while
+// the three-Q-tile kernel is faster with one (C3 13.44 vs 13.74 ms)
+#ifndef ORBIT2_ATTN_RS_SPLIT
+#define ORBIT2_ATTN_RS_SPLIT 4
+#endif
+#ifndef ORBIT2_ATTN3_RS_SPLIT
+#define ORBIT2_ATTN3_RS_SPLIT 1
+#endif
+
 namespace orbit2 {
 namespace tc {
 
