@@ -374,7 +374,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (zi == 0 && hb == 0 && u == 0) shift = y0;
             const float d0 = y0 - shift, d1 = y1 - shift, d2 = y2 - shift, d3 = y3 - shift;
             sum += (d0 + d1) + (d2 + d3);
-            sq = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, sq))));
+            // (d0^2 + d1^2) + (d2^2 + d3^2): one dependent add per 4 values, not 4 FMAs
+            sq += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
             a[4 * u] = __float_as_uint(y0);
             a[4 * u + 1] = __float_as_uint(y1);
             a[4 * u + 2] = __float_as_uint(y2);
@@ -474,7 +475,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (k == 0 && u == 0) shift2 = y.x;
           const float d0 = y.x - shift2, d1 = y.y - shift2, d2 = y.z - shift2, d3 = y.w - shift2;
           sum2 += (d0 + d1) + (d2 + d3);
-          sq2 = fmaf(d0, d0, fmaf(d1, d1, fmaf(d2, d2, fmaf(d3, d3, sq2))));
+          sq2 += fmaf(d0, d0, d1 * d1) + fmaf(d2, d2, d3 * d3);
           *reinterpret_cast<float4*>(srow + ((u ^ sw) << 4)) = y;
         }
         tc::fence_proxy_async_smem();

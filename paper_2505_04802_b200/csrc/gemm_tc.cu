@@ -474,11 +474,13 @@ __global__ void __launch_bounds__(384, 1)
           *reinterpret_cast<float4*>(sb + ((u ^ (rr & 7)) << 4)) =
               make_float4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
         }
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};    // 4 partial sums: no 256-long chain of dependent adds
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          sum += v[j];
+          s4[j & 3] += v[j];
           r[j] = __float_as_uint(v[j]);
         }
+        sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
         tc::tmem_st32(taddr + c * 32, r);
         tc::fence_proxy_async_smem();
         asm volatile("bar.sync %0, 128;" ::"r"(nb) : "memory");
@@ -496,11 +498,13 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t r[32];
         tc::tmem_ld32(taddr + c * 32, r);
         tc::tmem_ld_wait();
+        float v4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float d = __uint_as_float(r[j]) - mean;
-          var += d * d;
+          v4[j & 3] = fmaf(d, d, v4[j & 3]);
         }
+        var += (v4[0] + v4[1]) + (v4[2] + v4[3]);
       }
       const float rstd = rsqrtf(var * (1.0f / 256.0f) + 1e-5f);
 #pragma unroll 1
