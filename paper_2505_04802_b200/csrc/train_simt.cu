@@ -236,25 +236,31 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ d
 // Delta[h][row] = sum_{d < dh} dO[row][h dh + d] O[row][h dh + d]  (fp32), one thread per (row, head)
 __global__ void delta_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
                              float* __restrict__ delta, int64_t M, int D, int heads, int64_t ld_stat) {
-  const int dh = D / heads;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < M * heads;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = e / heads;
-    const int h = (int)(e - row * heads);
-    const uint4* a = reinterpret_cast<const uint4*>(dO + row * D + h * dh);
-    const uint4* o = reinterpret_cast<const uint4*>(O + row * D + h * dh);
+  // thread = one 16-byte chunk (8 values) of a row; the dh / 8 consecutive lanes of a head
+  // (4, 8 or 16: a power of two dividing 32) reduce by shuffles, so a warp reads 512
+  // contiguous bytes of dO and of O per step
+  const int dh = D / heads, cph = dh / 8, cpr = D / 8;
+  const int64_t n = M * cpr, n_pad = (n + 31) / 32 * 32;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n_pad; e += (int64_t)gridDim.x * blockDim.x) {
     float s = 0.f;
-    for (int c = 0; c < dh / 8; ++c) {
-      const uint4 x = __ldg(a + c), y = __ldg(o + c);
+    const bool valid = e < n;
+    const int64_t row = valid ? e / cpr : 0;
+    const int c = valid ? (int)(e - row * cpr) : 0;
+    if (valid) {
+      const uint4 x = __ldg(reinterpret_cast<const uint4*>(dO + row * D) + c);
+      const uint4 y = __ldg(reinterpret_cast<const uint4*>(O + row * D) + c);
       const __nv_bfloat162* xp = reinterpret_cast<const __nv_bfloat162*>(&x);
       const __nv_bfloat162* yp = reinterpret_cast<const __nv_bfloat162*>(&y);
+      float s2[2] = {0.f, 0.f};
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float2 xf = __bfloat1622float2(xp[u]), yf = __bfloat1622float2(yp[u]);
-        s += xf.x * yf.x + xf.y * yf.y;
+        s2[u & 1] = fmaf(xf.x, yf.x, fmaf(xf.y, yf.y, s2[u & 1]));
       }
+      s = s2[0] + s2[1];
     }
-    delta[(int64_t)h * ld_stat + row] = s;
+    for (int o = cph / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (valid && c % cph == 0) delta[(int64_t)(c / cph) * ld_stat + row] = s;
   }
 }
 
@@ -351,7 +357,7 @@ bool launch_ln_bwd(const float* dy, int64_t ldy, const float* z, const float* g,
 
 void launch_delta(const __nv_bfloat16* dO, const __nv_bfloat16* O, float* delta, int64_t M, int D, int heads,
                   int64_t ld_stat, cudaStream_t st) {
-  const int64_t n = M * heads;
+  const int64_t n = M * (D / 8);
   if (n <= 0) return;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 16LL * num_sms());
   delta_kernel<<<blocks, 256, 0, st>>>(dO, O, delta, M, D, heads, ld_stat);
