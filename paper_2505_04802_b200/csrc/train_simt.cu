@@ -129,6 +129,49 @@ __global__ void stitch_bwd_kernel(const float* __restrict__ dout, __nv_bfloat16*
   for (int e = Nh + threadIdx.x; e < ldg; e += blockDim.x) row[e] = __float2bfloat16_rn(0.f);
 }
 
+// The same gather with 16-byte reads (P % 4 == 0, sW % 4 == 0): thread = (token, k, al, 4 be);
+// SB_TPB tokens per block, each thread finds its token's tile by binary search over the
+// (ascending) core offsets; writes of 4 bf16 (8 bytes) are contiguous along the dG row.
+#ifndef ORBIT2_STITCH_BWD_VEC   // 0: the one-block-per-token kernel (A/B)
+#define ORBIT2_STITCH_BWD_VEC 1
+#endif
+constexpr int SB_TPB = 16;
+__global__ void stitch_bwd_vec_kernel(const float* __restrict__ dout, __nv_bfloat16* __restrict__ dg, int64_t ldg,
+                                      ChunkDev ch, int K, int P, int sH, int sW) {
+  const int b = blockIdx.y;
+  const int q4 = P / 4, segs = K * P * q4;          // float4 segments per token
+  const int64_t t0 = (int64_t)blockIdx.x * SB_TPB;
+  const int Nh = K * P * P;
+  for (int e = threadIdx.x; e < SB_TPB * segs; e += blockDim.x) {
+    const int64_t t = t0 + e / segs;
+    if (t >= ch.chunk_core) break;                   // e grows: every later e is past the end too
+    const int sidx = e - (int)(e / segs) * segs;
+    int lo = 0, hi = ch.tc - 1;                      // last tile with core_off - core0 <= t
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (ch.tiles[ch.tb + mid].core_off - ch.core0 <= t) lo = mid;
+      else hi = mid - 1;
+    }
+    const DevTile& tl = ch.tiles[ch.tb + lo];
+    const int64_t loc = t - (tl.core_off - ch.core0);
+    const int u = tl.out_y0 + (int)(loc / tl.out_w), w = tl.out_x0 + (int)(loc % tl.out_w);
+    const int k = sidx / (P * q4), rem = sidx - k * P * q4, al = rem / q4, q = rem - al * q4;
+    const float4 v = __ldg(reinterpret_cast<const float4*>(
+                               dout + (((int64_t)b * K + k) * sH + (int64_t)P * u + al) * sW + (int64_t)P * w) +
+                           q);
+    __nv_bfloat162 h2[2] = {__floats2bfloat162_rn(v.x, v.y), __floats2bfloat162_rn(v.z, v.w)};
+    *reinterpret_cast<uint2*>(dg + ((int64_t)b * ch.chunk_core + t) * ldg + (k * P + al) * P + 4 * q) = *reinterpret_cast<const uint2*>(h2);
+  }
+  // zero the padding columns [Nh, ldg) of the block's tokens
+  const int pad = (int)(ldg - Nh);
+  for (int e = threadIdx.x; e < SB_TPB * pad; e += blockDim.x) {
+    const int64_t t = t0 + e / pad;
+    if (t >= ch.chunk_core) break;
+    dg[((int64_t)b * ch.chunk_core + t) * ldg + Nh + (e - (int)(e / pad) * pad)] = __float2bfloat16_rn(0.f);
+  }
+}
+
+
 // LayerNorm backward, one warp per row; lane l owns the float4 columns 4 l + 128 k
 // (k < D / 128: coalesced 16-byte accesses):
 //   xh = (z - mu) rstd;  dxh = dy g;  dz = rstd (dxh - mean(dxh) - xh mean(dxh xh))
@@ -328,6 +371,11 @@ void launch_loss(const float* out, const float* truth, int B, int K, int sH, int
 void launch_stitch_bwd(const float* dout, __nv_bfloat16* dg, int64_t ldg, const ChunkDev& ch, int B, int K, int P,
                        int sH, int sW, cudaStream_t st) {
   if (ch.chunk_core <= 0) return;
+  if (P % 4 == 0 && sW % 4 == 0 && ldg % 4 == 0 && ORBIT2_STITCH_BWD_VEC) {
+    const unsigned blocks = (unsigned)((ch.chunk_core + SB_TPB - 1) / SB_TPB);
+    stitch_bwd_vec_kernel<<<dim3(blocks, (unsigned)B), 256, 0, st>>>(dout, dg, ldg, ch, K, P, sH, sW);
+    return;
+  }
   stitch_bwd_kernel<<<dim3((unsigned)ch.chunk_core, (unsigned)B), 192, 0, st>>>(dout, dg, ldg, ch, K, P, sH, sW);
 }
 

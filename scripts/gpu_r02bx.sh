@@ -1,0 +1,10 @@
+#!/bin/bash
+# 16-byte stitch backward (16 tokens per block, binary-searched tiles) vs one block per token:
+# training parity, C2 / C3 training A/B
+OUT=gpurun_out/r02bx
+mkdir -p $OUT
+P=$PWD/paper_2505_04802_b200
+timeout 900 python -m pytest tests/test_gpu_train.py tests/test_gpu_train_sp.py -m gpu -q -x > $OUT/pytest_train.log 2>&1
+echo "pytest exit $?" >> $OUT/pytest_train.log
+timeout 900 python scripts/train_ab.py C2 64 $P/liborbit2_sbv0.so $P/liborbit2.so > $OUT/train_ab_C2.log 2>&1
+timeout 900 python scripts/train_ab.py C3 16 $P/liborbit2_sbv0.so $P/liborbit2.so > $OUT/train_ab_C3.log 2>&1
